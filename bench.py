@@ -1,0 +1,436 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 downscaler (arxiv 1103.4881 hot path).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config hd420|hd444|4k420|4k444|cif420] [--frames F]
+
+One step = one ds_run over the whole per-rank batch of frames (every row of
+SURVEY 8(a): H task -> u8 intermediate -> V task, all planes, all frames)
+with the input already resident in HBM.  N = 1 runs BASELINE configs[2]
+(300-frame HD 4:2:0 stream on one B200); N > 1 runs configs[3] (3000-frame
+HD stream frame-sharded over N GPUs, launched with torchrun).  Rank 0 prints
+ONE JSON line.  See DESIGN.md "Measurement" for every field.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import platform
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = ("frames/s and achieved HBM GB/s (% of B200 peak) at 1/2/4/8 GPUs vs CPU oracle")
+
+CONFIGS = {
+    "hd420": dict(w=1920, h=1080, channels=3, chroma=1, label="HD 1920x1080 YUV 4:2:0"),
+    "hd444": dict(w=1920, h=1080, channels=3, chroma=0, label="HD 1920x1080 YUV 4:4:4"),
+    "4k420": dict(w=3840, h=2160, channels=3, chroma=1, label="4K 3840x2160 YUV 4:2:0"),
+    "4k444": dict(w=3840, h=2160, channels=3, chroma=0, label="4K 3840x2160 YUV 4:4:4"),
+    "cif420": dict(w=352, h=288, channels=3, chroma=1, label="CIF 352x288 YUV 4:2:0"),
+}
+FALLBACK_HBM_GBS = 6650.0   # B200_PROFILING.md fallback, only if MEASURED_PEAKS.json is absent
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=300)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="hd420")
+    ap.add_argument("--frames", type=int, default=0,
+                    help="total frames (default: 300 at N=1, 3000 at N>1; 4K: 1000)")
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--stages", type=int, default=0)
+    ap.add_argument("--ctas", type=int, default=0)
+    ap.add_argument("--kernel", choices=["auto", "fused", "generic"], default="auto")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0,
+                    help="CPU-oracle sample budget (seconds of 1-core work)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--gather", action="store_true", help="N>1: time the NCCL gather to rank 0")
+    return ap.parse_args()
+
+
+def workload(args, world):
+    cfg = dict(CONFIGS[args.config])
+    if args.frames:
+        total = args.frames
+    elif args.config.startswith("4k"):
+        total = 1000
+    else:
+        total = 300 if world == 1 else 3000
+    cfg["total"] = total
+    if args.config.startswith("hd") and world == 1 and total == 300:
+        cfg["name"] = f"configs[2]: 300-frame {cfg['label']} stream on 1 B200"
+    elif args.config.startswith("hd") and total == 3000:
+        cfg["name"] = f"configs[3]: 3000-frame {cfg['label']} stream frame-sharded over {world} B200"
+    elif args.config.startswith("4k") and total == 1000:
+        cfg["name"] = f"configs[4]: 1000-frame {cfg['label']} stream over {world} B200"
+    else:
+        cfg["name"] = f"{total}-frame {cfg['label']} stream over {world} B200"
+    return cfg
+
+
+def geometry(cfg):
+    import synth
+
+    dims = synth.plane_dims(cfg["w"], cfg["h"], cfg["channels"], cfg["chroma"])
+    fin = sum(w * h for w, h in dims)
+    fout = sum((3 * w // 8) * (4 * h // 9) for w, h in dims)    # SURVEY a7 closed form
+    fin_live = fin * 8 // 9                                     # dead row 4 of 9
+    return fin, fout, fin_live
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            j = json.load(f)
+        return float(j["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, torch copy_)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """NVML sampling of SM clock and throttle reasons DURING the timed region."""
+
+    REASONS = {
+        0x0000000000000001: "gpu_idle", 0x0000000000000002: "applications_clocks_setting",
+        0x0000000000000004: "sw_power_cap", 0x0000000000000008: "hw_slowdown",
+        0x0000000000000010: "sync_boost", 0x0000000000000020: "sw_thermal_slowdown",
+        0x0000000000000040: "hw_thermal_slowdown", 0x0000000000000080: "hw_power_brake_slowdown",
+        0x0000000000000100: "display_clock_setting",
+    }
+
+    def __init__(self, device_index: int, period_s: float = 0.005):
+        self.samples, self.reasons = [], set()
+        self.period = period_s
+        self._stop = threading.Event()
+        self.ok = False
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.hdl = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.hdl, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover
+            self.err = str(e)
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.hdl, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.hdl)
+                for bit, name in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.ok:
+            self.t.join()
+
+    def result(self):
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "error": self.err}
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons - {"gpu_idle"}),
+                "samples": len(self.samples)}
+
+
+def ncu_traffic(config_key):
+    """Per-launch DRAM bytes from the committed ncu --set full summary, if one
+    exists for this config (profiles/ncu_summary.json)."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(p) as f:
+            j = json.load(f)
+        e = j[config_key]
+        return e["dram_bytes_per_launch"], e.get("source")
+    except Exception:
+        return None, None
+
+
+def cpu_oracle_sample(cfg, seed, budget_s, gpu_out_fn=None):
+    """Time the CPU oracle (O1 tiler executor, plain C, 1 thread) on the first
+    frames of the same stream until ~budget_s of work; optionally compare the
+    GPU's output for those frames.  Test infrastructure: only this leg of
+    bench.py touches oracle/."""
+    import numpy as np
+
+    import oracle
+    import synth
+
+    try:
+        os.sched_setaffinity(0, {sorted(os.sched_getaffinity(0))[0]})
+        core = sorted(os.sched_getaffinity(0))[0]
+    except Exception:
+        core = None
+    W, H, ch, chroma = cfg["w"], cfg["h"], cfg["channels"], cfg["chroma"]
+    times, k, same = [], 0, 0
+    t_all = time.perf_counter()
+    while k < max(1, cfg["total"]) and (k < 2 or sum(times) < budget_s):
+        fr = synth.random_frames(seed, k, 1, W, H, ch, chroma)
+        t0 = time.perf_counter()
+        out = oracle.execute_frames(fr, W, H, ch, chroma)
+        times.append(time.perf_counter() - t0)
+        if gpu_out_fn is not None:
+            same += int(np.array_equal(out[0], gpu_out_fn(k)))
+        k += 1
+    wall = time.perf_counter() - t_all
+    per = statistics.median(times)
+    return {
+        "value": 1.0 / per, "unit": "frames/s", "cores": 1, "kind": "oracle",
+        "sample": f"frames 0..{k - 1} of the same seeded stream ({k} frames), O1 tiler executor "
+                  f"(oracle/ds_oracle.c, gcc -O2, 1 thread pinned to core {core}); "
+                  f"median per-frame time {per * 1e3:.1f} ms; {wall:.1f} s of CPU work",
+        "frames": k, "host_cpu": platform.processor() or platform.machine(),
+        "parity_checked_frames": k if gpu_out_fn is not None else 0,
+        "parity_bit_exact_frames": same if gpu_out_fn is not None else None,
+    }
+
+
+def lscpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return platform.processor()
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle as it stands, timed on the host cores;
+    rank 0 only.  Each step = one frame of the workload through O1."""
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    if rank != 0:
+        return 0
+    import oracle
+    import synth
+
+    cfg = workload(args, world)
+    W, H, ch, chroma = cfg["w"], cfg["h"], cfg["channels"], cfg["chroma"]
+    try:
+        os.sched_setaffinity(0, {sorted(os.sched_getaffinity(0))[0]})
+    except Exception:
+        pass
+    frames = [synth.random_frames(args.seed, k % cfg["total"], 1, W, H, ch, chroma)
+              for k in range(min(args.steps + args.warmup, 8))]
+    for k in range(args.warmup):
+        oracle.execute_frames(frames[k % len(frames)], W, H, ch, chroma)
+    t0 = time.perf_counter()
+    for k in range(args.steps):
+        oracle.execute_frames(frames[k % len(frames)], W, H, ch, chroma)
+    dt = time.perf_counter() - t0
+    fps = args.steps / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": fps, "unit": "frames/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
+        "scaling": "weak" if world == 1 else "strong", "vs_baseline": None, "dtype": "u8",
+        "data": "synthetic (splitmix64 counter-hash frames, seed %d)" % args.seed,
+        "config": {"workload": cfg["name"], "frames": cfg["total"], "w": W, "h": H,
+                   "channels": ch, "chroma": "4:2:0" if chroma else "4:4:4",
+                   "step": "one frame of the workload through the CPU oracle"},
+        "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": 1, "kind": "oracle",
+                         "sample": f"{args.steps} frames (one per step) of the workload, O1 tiler "
+                                   f"executor, plain C -O2, 1 thread, host {lscpu_model()}"},
+        "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1103_4881_b200 as ds
+    from paper_1103_4881_b200.dist import shard_range
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.cuda.current_device()
+
+    cfg = workload(args, world)
+    fin, fout, fin_live = geometry(cfg)
+    lo, hi = shard_range(cfg["total"], world, rank)
+    n = hi - lo
+
+    d = ds.Downscaler(cfg["w"], cfg["h"], cfg["channels"], chroma=cfg["chroma"])
+    assert d.in_frame_bytes == fin and d.out_frame_bytes == fout
+    if args.kernel != "auto":
+        d.set_kernel({"fused": ds.DS_KERNEL_FUSED, "generic": ds.DS_KERNEL_GENERIC}[args.kernel])
+    if args.stages or args.ctas:
+        d.set_tuning(args.stages or 4, args.ctas)
+    stream = torch.cuda.current_stream()
+    x = ds.generate_frames(n, fin, seed=args.seed, first_frame=lo)   # resident in HBM
+    y = d.alloc_out(n)
+    torch.cuda.synchronize()
+
+    # ---- warm-up (untimed) -------------------------------------------------
+    for _ in range(max(args.warmup, 3)):
+        d(x, y)
+    torch.cuda.synchronize()
+    kernel_used = d.last_kernel()
+
+    # ---- timed region: K steps, CUDA events on the launching stream ---------
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(2 * args.steps)]
+    with ClockSampler(dev) as clk:
+        for k in range(args.steps):
+            evs[2 * k].record(stream)
+            d(x, y)
+            evs[2 * k + 1].record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    per = [evs[2 * k].elapsed_time(evs[2 * k + 1]) for k in range(args.steps)]
+    total_ms = evs[0].elapsed_time(evs[-1])
+    t = torch.tensor([total_ms, statistics.mean(per)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms, kern_ms = float(t[0]), float(t[1])
+
+    frames_all = cfg["total"] * args.steps
+    fps = frames_all / (total_ms / 1e3)
+    peak, peak_src = peaks()
+    alg_bytes = n * (fin_live + fout)            # required bytes per launch (per rank)
+    achieved = alg_bytes / (kern_ms / 1e3) / 1e9
+    eff_full = n * (fin + fout) / (kern_ms / 1e3) / 1e9
+    traffic, traffic_src = ncu_traffic(args.config)
+
+    # ---- optional NCCL gather (C-1), timed separately -----------------------
+    gather_ms = None
+    if world > 1 and args.gather:
+        from paper_1103_4881_b200.dist import gather_frames
+
+        dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        gather_frames(y, cfg["total"])
+        torch.cuda.synchronize()
+        gt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
+        dist.all_reduce(gt, op=dist.ReduceOp.MAX)
+        gather_ms = float(gt[0]) * 1e3
+
+    # ---- e2e: host pinned frames -> ds_run_host -> host, copies timed -------
+    e2e = None
+    if not args.no_e2e:
+        hin = torch.empty((n, fin), dtype=torch.uint8, pin_memory=True)
+        hin.copy_(x)
+        hout = torch.empty((n, fout), dtype=torch.uint8, pin_memory=True)
+        d.run_host(hin, hout)
+        torch.cuda.synchronize()
+        ks = max(1, args.e2e_steps)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(ks):
+            d.run_host(hin, hout)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        et = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        e2e = {"value": cfg["total"] * ks / (float(et[0]) / 1e3), "unit": "frames/s",
+               "h2d_bytes_per_step": n * fin, "d2h_bytes_per_step": n * fout,
+               "steps": ks, "api": "Downscaler.run_host -> ds_run_host (pinned host buffers)"}
+        ok = torch.equal(hout, y.cpu())
+        e2e["matches_device_path"] = bool(ok)
+        del hin, hout
+
+    # ---- CPU oracle baseline (rank 0, N = 1 only) ---------------------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_oracle_sample(cfg, args.seed, args.cpu_seconds,
+                                gpu_out_fn=lambda k: y[k].cpu().numpy())
+        cpu["host_cpu"] = lscpu_model()
+
+    if rank == 0:
+        g, b, s = d.launch_shape(n) if d.plan.fused_eligible else (None, None, None)
+        line = {
+            "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": world,
+            "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": total_ms / args.steps,
+            "higher_is_better": True, "scaling": "weak" if world == 1 else "strong",
+            "vs_baseline": None, "dtype": "u8",
+            "data": f"synthetic (splitmix64 counter-hash frames by global byte index, seed {args.seed})",
+            "config": {
+                "workload": cfg["name"], "frames": cfg["total"], "frames_per_rank": n,
+                "w": cfg["w"], "h": cfg["h"], "channels": cfg["channels"],
+                "chroma": "4:2:0" if cfg["chroma"] else "4:4:4",
+                "in_frame_bytes": fin, "out_frame_bytes": fout,
+                "parallelism": f"frame-sharded x{world}" if world > 1 else "single GPU",
+                "l2": f"inputs larger than L2: {n * (fin + fout) / 1e9:.3f} GB touched per step "
+                      f"per GPU vs 126 MB L2 (no flush needed)",
+                "kernel": ds.KERNEL_NAMES.get(kernel_used), "grid": g, "block": b,
+                "smem_bytes": s,
+            },
+            "roofline": {
+                "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": traffic,
+                "kernel": "ds_fused_band_kernel" if kernel_used == ds.DS_KERNEL_FUSED
+                          else "ds_generic_kernel",
+                "algorithmic_bytes_per_launch": alg_bytes,
+                "bytes_rule": "per frame (8/9)*in + out: input rows 9g+4 carry zero V weight "
+                              "(S:540) and are not required; see DESIGN.md",
+                "avg_launch_ms": kern_ms,
+                "peak_source": peak_src,
+                "traffic_source": traffic_src,
+                "effective_gbs_full_in_out": eff_full,
+                "pct_of_8tbps_nominal_full_in_out": eff_full / 8000.0,
+            },
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": args.steps,
+            "clocks": clk.result(),
+            "gather_ms": gather_ms,
+            "impl": "ours",
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,211 @@
+/*
+ * ds.h -- C ABI of libds.so, the B200 (sm_100a) downscaler of
+ * arxiv 1103.4881 ("Programming Massively Parallel Architectures using
+ * MARTE: a Case Study").
+ *
+ * Citation key: P:n = PAPER.md line n; S:n = SPEC.md line n; SURVEY sec. n.
+ *
+ * The operation (PAPER sec. 3, P:64-90 and sec. 3.1): a stream of N
+ * frames, each made of u8 colour planes, goes in; every plane goes through
+ * an Array-OL horizontal repetitive task (pattern 8 -> 3, "interpolating
+ * packets of 8 pixels"; taps S:530) and then a vertical one
+ * (pattern 9 -> 4, 288 -> 128 lines; taps S:540), each applied via
+ * tilers (origin, paving, fitting).  N frames of
+ * (3W/8) x (4H/9) planes come out (352x288 -> 132x128).  Pixel
+ * arithmetic is integer; the intermediate array is u8;
+ * results are bit-exact and independent of kernel, grid and GPU count.
+ *
+ * Frame layout: plane 0 (Y), plane 1, plane 2 back to back, each
+ * row-major u8, no headers, frames contiguous.  4:2:0 chroma planes are
+ * (W/2, H/2); 4:4:4 is three equal planes ("24-bit RGB").
+ *
+ * Threading: every function is thread-safe.  A handle holds immutable
+ * tables plus (after the first ds_run_host) staging buffers guarded by a
+ * mutex; ds_run itself has no mutable state, so one handle may run
+ * concurrently on several streams.
+ *
+ * Plain C: no C++ or torch types cross this boundary.
+ */
+#ifndef DS_H
+#define DS_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define DS_API __attribute__((visibility("default")))
+#else
+#define DS_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct ds_handle ds_handle;        /* opaque; owned by the library   */
+typedef struct CUstream_st* ds_stream_t;   /* == cudaStream_t; NULL = legacy
+                                              default stream                 */
+
+/* Error codes (negative).  S:551 "non-divisible shape -> error"
+ * "missing input array; shape mismatch" -> error. */
+enum {
+    DS_OK = 0,
+    DS_EINVAL = -1,        /* bad argument: NULL, negative n, overlap, wrong device */
+    DS_ESHAPE = -2,        /* plane not divisible by the paving steps       */
+    DS_EUNSUPPORTED = -3,  /* channels not 1/3, spec over its limits               */
+    DS_ECUDA = -4,         /* CUDA runtime / launch failure                         */
+    DS_ENOMEM = -5         /* allocation failure                                    */
+};
+
+/* Colour layouts. */
+enum { DS_CHROMA_444 = 0, DS_CHROMA_420 = 1 };
+
+enum { DS_MAX_PATTERN = 16, DS_MAX_OUTPUTS = 8, DS_MAX_PLANES = 3 };
+
+/* Kernel selection (ds_set_kernel / ds_last_kernel). */
+enum {
+    DS_KERNEL_AUTO = 0,     /* fused band kernel when eligible, else generic     */
+    DS_KERNEL_FUSED = 1,    /* K-N1: TMA-staged fused H+V band kernel            */
+    DS_KERNEL_GENERIC = 2   /* K-N2: one thread per output pixel, any spec       */
+};
+
+/*
+ * One separable Array-OL stage, i.e. one repetitive task with its tilers
+ * along one axis, plus its elementary function:
+ *   input tiler : origin `origin` (along the axis), paving step `paving`,
+ *                 fitting 1, pattern [pattern]   (toroidal modulo)
+ *   output tiler: origin 0, paving step `outputs`, fitting 1, pattern
+ *                 [outputs]  -- exact coverage by construction
+ *   body        : out[k] = clamp_0^255( trunc( (sum_i weight[k][i]*in[i]
+ *                 + bias) / divisor ) )
+ * pattern > paving gives a halo of pattern - paving elements.
+ * Limits: 1 <= pattern <= 16, 1 <= paving <= 4096, 1 <= outputs <= 8,
+ * 1 <= divisor <= 2^24, |weight| <= 65535, |bias| <= 2^24,
+ * |origin| <= 2^20; otherwise DS_EUNSUPPORTED.
+ */
+typedef struct {
+    int32_t pattern;
+    int32_t paving;
+    int32_t origin;
+    int32_t outputs;
+    int32_t weight[DS_MAX_OUTPUTS][DS_MAX_PATTERN];
+    int32_t divisor;
+    int32_t bias;
+} ds_stage_spec;
+
+/* h applies along rows ("horizontal filter"), v along columns of the
+ * intermediate.  chroma is used when channels == 3. */
+typedef struct {
+    ds_stage_spec h;
+    ds_stage_spec v;
+    int32_t chroma;
+} ds_filter_spec;
+
+/* Geometry of a frame under a spec (host-only, no GPU needed). */
+typedef struct {
+    int64_t in_frame_bytes;              /* e.g. 3,110,400 for HD 4:2:0          */
+    int64_t out_frame_bytes;             /* e.g.   518,400                       */
+    int32_t n_planes;
+    int32_t in_w[DS_MAX_PLANES], in_h[DS_MAX_PLANES];
+    int32_t out_w[DS_MAX_PLANES], out_h[DS_MAX_PLANES];
+    int64_t in_offset[DS_MAX_PLANES];    /* byte offset of each plane in a frame */
+    int64_t out_offset[DS_MAX_PLANES];
+    int32_t fused_eligible;              /* 1 if K-N1 can run this geometry+spec */
+    int32_t band_groups[DS_MAX_PLANES];  /* K-N1: 9-row groups per work unit     */
+    int64_t units_per_frame;             /* K-N1 work units per frame            */
+    int64_t unit_in_bytes_max;           /* K-N1 bytes staged per unit (max)     */
+    int64_t unit_out_bytes_max;
+} ds_plan_info;
+
+/* Fill *out with SPEC's downscaler (hfilter_8to3 S:527-535, vfilter_9to4
+ * S:537-545); chroma = DS_CHROMA_420.  Returns DS_OK. */
+DS_API int ds_default_spec(ds_filter_spec* out);
+
+/* Validate (frame_w, frame_h, channels, spec) and describe the geometry.
+ * spec NULL = ds_default_spec.  Returns DS_OK or DS_EINVAL / DS_ESHAPE /
+ * DS_EUNSUPPORTED (same rules as ds_create).  Host-only. */
+DS_API int ds_plan(int32_t frame_w, int32_t frame_h, int32_t channels,
+                   const ds_filter_spec* spec, ds_plan_info* out);
+
+/* Create a downscaler bound to the CUDA device current at the call.
+ * channels in {1, 3}.  spec NULL = SPEC's downscaler, 4:2:0 when
+ * channels == 3.  Every plane must satisfy W_p % h.paving == 0 and
+ * H_p % v.paving == 0 (4:2:0 with the default spec: W % 16 == 0 and
+ * H % 18 == 0), else NULL with ds_last_error() == DS_ESHAPE.
+ * The spec is copied.  Returns NULL on error (see ds_last_error). */
+DS_API ds_handle* ds_create(int32_t frame_w, int32_t frame_h, int32_t channels,
+                            const ds_filter_spec* filter_spec);
+
+/* Downscale n_frames device-resident frames.
+ *   in_frames : device pointer, n_frames * ds_in_frame_bytes(h) bytes, read
+ *               only ("const", the read-only flowPort of P:132-135)
+ *   out_frames: device pointer, n_frames * ds_out_frame_bytes(h) bytes
+ * Both on the handle's device, caller-owned, not retained, must not
+ * overlap and must stay alive until work on `stream` completes.
+ * Asynchronous on `stream`; faults surface at the caller's sync.
+ * n_frames == 0 is a successful no-op.  Any alignment is accepted
+ * (misalignment selects K-N2, never an error).
+ * Returns DS_OK, DS_EINVAL (NULL handle/pointer with n > 0, n < 0,
+ * overlapping ranges, pointer not on the handle's device) or DS_ECUDA. */
+DS_API int ds_run(ds_handle* h, const uint8_t* in_frames, int64_t n_frames,
+                  uint8_t* out_frames, ds_stream_t stream);
+
+/* Same result from HOST buffers (the paper's host-resident setting, P:146,
+ * P:148): the library streams chunks of frames host -> device, runs the
+ * downscaler and copies results device -> host, overlapping the three on
+ * internal streams and staging buffers it owns (allocated on first use,
+ * freed by ds_destroy).  host_in / host_out should be page-locked
+ * (cudaHostAlloc / cudaHostRegister) for the copies to be asynchronous;
+ * pageable memory works but serialises.  Asynchronous on `stream`:
+ * host_out is valid after `stream` synchronises; both buffers must stay
+ * alive until then.  Calls on one handle are serialised internally.
+ * Returns as ds_run, plus DS_ENOMEM. */
+DS_API int ds_run_host(ds_handle* h, const uint8_t* host_in, int64_t n_frames,
+                       uint8_t* host_out, ds_stream_t stream);
+
+/* Frames per chunk for ds_run_host (0 = automatic, ~32 MiB per chunk). */
+DS_API int ds_set_host_chunk(ds_handle* h, int64_t frames_per_chunk);
+
+/* Release the handle and its staging buffers (synchronises them).
+ * NULL-safe. */
+DS_API void ds_destroy(ds_handle* h);
+
+/* Thread-local code of the last failed ds_create (DS_OK if none). */
+DS_API int ds_last_error(void);
+
+/* Static description of an error code; never NULL. */
+DS_API const char* ds_strerror(int code);
+
+/* Geometry queries; -1 / DS_EINVAL on a NULL handle. */
+DS_API int64_t ds_in_frame_bytes(const ds_handle* h);
+DS_API int64_t ds_out_frame_bytes(const ds_handle* h);
+DS_API int ds_plane_dims(const ds_handle* h, int plane, int32_t* in_w, int32_t* in_h,
+                         int32_t* out_w, int32_t* out_h);
+
+/* Force a kernel (DS_KERNEL_*).  DS_KERNEL_FUSED on an ineligible
+ * geometry returns DS_EUNSUPPORTED and leaves the setting unchanged. */
+DS_API int ds_set_kernel(ds_handle* h, int32_t kernel);
+
+/* Kernel used by the most recent ds_run on this handle (any thread), or
+ * DS_KERNEL_AUTO if none yet. */
+DS_API int ds_last_kernel(const ds_handle* h);
+
+/* K-N1 tuning: ring stages per CTA (2..8) and CTAs per SM (0 = maximum
+ * occupancy).  Returns DS_EINVAL when out of range. */
+DS_API int ds_set_tuning(ds_handle* h, int32_t stages, int32_t ctas_per_sm);
+
+/* K-N1 launch shape that ds_run would use for n_frames:
+ * grid CTAs, threads per CTA, dynamic shared memory bytes. */
+DS_API int ds_launch_shape(const ds_handle* h, int64_t n_frames, int32_t* grid,
+                           int32_t* block, int32_t* smem_bytes);
+
+/* Synthetic input (bench / test infrastructure, not part of the method):
+ * fills dev[0 .. n_bytes) on the current device with
+ *   byte(i) = splitmix64(seed * 0x9E3779B97F4A7C15 + start_index + i) >> 56
+ * (the counter hash of synth/__init__.py).  Asynchronous on `stream`. */
+DS_API int ds_generate(uint8_t* dev, int64_t n_bytes, uint64_t seed, int64_t start_index,
+                       ds_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DS_H */

@@ -1,0 +1,343 @@
+"""Python binding of libds.so (include/ds.h): the B200 downscaler of
+arxiv 1103.4881.
+
+Argument marshalling only -- every step of the hot path runs in the CUDA
+kernels of ``csrc/``.  Functions keep the C names (``ds_create``,
+``ds_run``, ...); ``Downscaler`` wraps them for ``torch.uint8`` CUDA
+tensors, using PyTorch only for device memory and streams.  There is no CPU
+fallback: if libds.so is missing or cannot be built this module raises.
+
+Citation key: P:n = PAPER.md line n, S:n = SPEC.md line n.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+from . import _build
+
+DS_OK, DS_EINVAL, DS_ESHAPE, DS_EUNSUPPORTED, DS_ECUDA, DS_ENOMEM = 0, -1, -2, -3, -4, -5
+DS_CHROMA_444, DS_CHROMA_420 = 0, 1
+DS_KERNEL_AUTO, DS_KERNEL_FUSED, DS_KERNEL_GENERIC = 0, 1, 2
+DS_MAX_PATTERN, DS_MAX_OUTPUTS, DS_MAX_PLANES = 16, 8, 3
+KERNEL_NAMES = {DS_KERNEL_AUTO: "none", DS_KERNEL_FUSED: "K-N1 fused band (TMA ring)",
+                DS_KERNEL_GENERIC: "K-N2 generic"}
+
+
+class ds_stage_spec(C.Structure):
+    _fields_ = [
+        ("pattern", C.c_int32),
+        ("paving", C.c_int32),
+        ("origin", C.c_int32),
+        ("outputs", C.c_int32),
+        ("weight", (C.c_int32 * DS_MAX_PATTERN) * DS_MAX_OUTPUTS),
+        ("divisor", C.c_int32),
+        ("bias", C.c_int32),
+    ]
+
+
+class ds_filter_spec(C.Structure):
+    _fields_ = [("h", ds_stage_spec), ("v", ds_stage_spec), ("chroma", C.c_int32)]
+
+
+class ds_plan_info(C.Structure):
+    _fields_ = [
+        ("in_frame_bytes", C.c_int64),
+        ("out_frame_bytes", C.c_int64),
+        ("n_planes", C.c_int32),
+        ("in_w", C.c_int32 * DS_MAX_PLANES),
+        ("in_h", C.c_int32 * DS_MAX_PLANES),
+        ("out_w", C.c_int32 * DS_MAX_PLANES),
+        ("out_h", C.c_int32 * DS_MAX_PLANES),
+        ("in_offset", C.c_int64 * DS_MAX_PLANES),
+        ("out_offset", C.c_int64 * DS_MAX_PLANES),
+        ("fused_eligible", C.c_int32),
+        ("band_groups", C.c_int32 * DS_MAX_PLANES),
+        ("units_per_frame", C.c_int64),
+        ("unit_in_bytes_max", C.c_int64),
+        ("unit_out_bytes_max", C.c_int64),
+    ]
+
+
+class DSError(RuntimeError):
+    def __init__(self, code: int, what: str):
+        super().__init__(f"{what}: {ds_strerror(code)} ({code})")
+        self.code = code
+
+
+_lib = None
+_lock = threading.Lock()
+
+# (name, restype, argtypes) of every entry point declared in include/ds.h
+_P8 = C.POINTER(C.c_uint8)
+_PI32 = C.POINTER(C.c_int32)
+SIGNATURES = [
+    ("ds_default_spec", C.c_int, [C.POINTER(ds_filter_spec)]),
+    ("ds_plan", C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.POINTER(ds_filter_spec),
+                          C.POINTER(ds_plan_info)]),
+    ("ds_create", C.c_void_p, [C.c_int32, C.c_int32, C.c_int32, C.POINTER(ds_filter_spec)]),
+    ("ds_run", C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),
+    ("ds_run_host", C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),
+    ("ds_set_host_chunk", C.c_int, [C.c_void_p, C.c_int64]),
+    ("ds_destroy", None, [C.c_void_p]),
+    ("ds_last_error", C.c_int, []),
+    ("ds_strerror", C.c_char_p, [C.c_int]),
+    ("ds_in_frame_bytes", C.c_int64, [C.c_void_p]),
+    ("ds_out_frame_bytes", C.c_int64, [C.c_void_p]),
+    ("ds_plane_dims", C.c_int, [C.c_void_p, C.c_int, _PI32, _PI32, _PI32, _PI32]),
+    ("ds_set_kernel", C.c_int, [C.c_void_p, C.c_int32]),
+    ("ds_last_kernel", C.c_int, [C.c_void_p]),
+    ("ds_set_tuning", C.c_int, [C.c_void_p, C.c_int32, C.c_int32]),
+    ("ds_launch_shape", C.c_int, [C.c_void_p, C.c_int64, _PI32, _PI32, _PI32]),
+    ("ds_generate", C.c_int, [C.c_void_p, C.c_int64, C.c_uint64, C.c_int64, C.c_void_p]),
+]
+
+
+def lib():
+    """Load (building in-tree first if stale) libds.so.  Raises if it cannot."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            path = _build.LIB
+            if _build.stale():
+                try:
+                    _build.build()
+                except Exception as e:  # no silent fallback: the CUDA path is the product
+                    if not os.path.exists(path):
+                        raise ImportError(f"libds.so is missing and could not be built: {e}")
+            L = C.CDLL(path)
+            for name, res, args in SIGNATURES:
+                fn = getattr(L, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = L
+    return _lib
+
+
+def lib_path() -> str:
+    return _build.LIB
+
+
+# ----------------------------------------------------------- thin C names --
+def ds_strerror(code: int) -> str:
+    return lib().ds_strerror(code).decode()
+
+
+def ds_last_error() -> int:
+    return lib().ds_last_error()
+
+
+def _stage_from(d) -> ds_stage_spec:
+    if isinstance(d, ds_stage_spec):
+        return d
+    s = ds_stage_spec()
+    s.pattern, s.paving, s.origin = d["pattern"], d["paving"], d.get("origin", 0)
+    s.outputs = len(d["weights"])
+    for k, row in enumerate(d["weights"]):
+        for i, w in enumerate(row):
+            s.weight[k][i] = int(w)
+    s.divisor, s.bias = d["divisor"], d["bias"]
+    return s
+
+
+def make_spec(h=None, v=None, chroma: int = DS_CHROMA_420) -> ds_filter_spec:
+    """Build a ds_filter_spec from dicts {pattern, paving, origin, weights
+    (Q rows of <= P ints), divisor, bias}; None = SPEC's stage."""
+    spec = ds_default_spec()
+    if h is not None:
+        spec.h = _stage_from(h)
+    if v is not None:
+        spec.v = _stage_from(v)
+    spec.chroma = chroma
+    return spec
+
+
+def stage_to_dict(s: ds_stage_spec) -> dict:
+    return dict(pattern=s.pattern, paving=s.paving, origin=s.origin,
+                weights=[[s.weight[k][i] for i in range(s.pattern)] for k in range(s.outputs)],
+                divisor=s.divisor, bias=s.bias)
+
+
+def ds_default_spec() -> ds_filter_spec:
+    s = ds_filter_spec()
+    rc = lib().ds_default_spec(C.byref(s))
+    if rc:
+        raise DSError(rc, "ds_default_spec")
+    return s
+
+
+def ds_plan(frame_w: int, frame_h: int, channels: int = 3, spec: ds_filter_spec | None = None):
+    info = ds_plan_info()
+    rc = lib().ds_plan(frame_w, frame_h, channels, C.byref(spec) if spec is not None else None,
+                       C.byref(info))
+    if rc:
+        raise DSError(rc, "ds_plan")
+    return info
+
+
+def ds_create(frame_w: int, frame_h: int, channels: int = 3, spec: ds_filter_spec | None = None):
+    h = lib().ds_create(frame_w, frame_h, channels,
+                        C.byref(spec) if spec is not None else None)
+    if not h:
+        raise DSError(lib().ds_last_error(), "ds_create")
+    return h
+
+
+def ds_run(h, in_ptr: int, n_frames: int, out_ptr: int, stream: int = 0) -> None:
+    rc = lib().ds_run(h, in_ptr, n_frames, out_ptr, stream or None)
+    if rc:
+        raise DSError(rc, "ds_run")
+
+
+def ds_run_host(h, in_ptr: int, n_frames: int, out_ptr: int, stream: int = 0) -> None:
+    rc = lib().ds_run_host(h, in_ptr, n_frames, out_ptr, stream or None)
+    if rc:
+        raise DSError(rc, "ds_run_host")
+
+
+def ds_destroy(h) -> None:
+    lib().ds_destroy(h)
+
+
+def ds_generate(dev_ptr: int, n_bytes: int, seed: int, start_index: int, stream: int = 0) -> None:
+    rc = lib().ds_generate(dev_ptr, n_bytes, seed, start_index, stream or None)
+    if rc:
+        raise DSError(rc, "ds_generate")
+
+
+# ------------------------------------------------------------ torch facade --
+class Downscaler:
+    """``Downscaler(w, h, channels=3, chroma="420", spec=None)(frames)``.
+
+    frames: ``torch.uint8`` CUDA tensor holding n whole frames (shape
+    ``(n, in_frame_bytes)`` or anything with n*in_frame_bytes elements,
+    contiguous).  Returns (or fills ``out``) ``(n, out_frame_bytes)``.
+    Runs on ``torch.cuda.current_stream()``.
+    """
+
+    def __init__(self, w: int, h: int, channels: int = 3, chroma: str | int = "420",
+                 spec: ds_filter_spec | None = None, kernel: int = DS_KERNEL_AUTO):
+        import torch
+
+        if not torch.cuda.is_available():
+            raise RuntimeError("Downscaler needs a CUDA device (no CPU fallback)")
+        c = chroma if isinstance(chroma, int) else {"420": DS_CHROMA_420, "444": DS_CHROMA_444}[
+            str(chroma)]
+        if spec is None:
+            spec = ds_default_spec()
+        spec.chroma = c
+        self.spec = spec
+        self.w, self.h, self.channels = w, h, channels
+        self.device = torch.cuda.current_device()
+        self._h = ds_create(w, h, channels, spec)
+        self.in_frame_bytes = lib().ds_in_frame_bytes(self._h)
+        self.out_frame_bytes = lib().ds_out_frame_bytes(self._h)
+        self.plan = ds_plan(w, h, channels, spec)
+        if kernel != DS_KERNEL_AUTO:
+            self.set_kernel(kernel)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            try:
+                ds_destroy(h)
+            except Exception:
+                pass
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    def plane_dims(self):
+        out = []
+        for p in range(self.channels):
+            a, b, c, d = C.c_int32(), C.c_int32(), C.c_int32(), C.c_int32()
+            rc = lib().ds_plane_dims(self._h, p, C.byref(a), C.byref(b), C.byref(c), C.byref(d))
+            if rc:
+                raise DSError(rc, "ds_plane_dims")
+            out.append(((a.value, b.value), (c.value, d.value)))
+        return out
+
+    def set_kernel(self, kernel: int) -> None:
+        rc = lib().ds_set_kernel(self._h, kernel)
+        if rc:
+            raise DSError(rc, "ds_set_kernel")
+
+    def last_kernel(self) -> int:
+        return lib().ds_last_kernel(self._h)
+
+    def set_tuning(self, stages: int, ctas_per_sm: int = 0) -> None:
+        rc = lib().ds_set_tuning(self._h, stages, ctas_per_sm)
+        if rc:
+            raise DSError(rc, "ds_set_tuning")
+
+    def set_host_chunk(self, frames: int) -> None:
+        rc = lib().ds_set_host_chunk(self._h, frames)
+        if rc:
+            raise DSError(rc, "ds_set_host_chunk")
+
+    def launch_shape(self, n_frames: int):
+        g, b, s = C.c_int32(), C.c_int32(), C.c_int32()
+        rc = lib().ds_launch_shape(self._h, n_frames, C.byref(g), C.byref(b), C.byref(s))
+        if rc:
+            raise DSError(rc, "ds_launch_shape")
+        return g.value, b.value, s.value
+
+    def alloc_out(self, n: int):
+        import torch
+
+        return torch.empty((n, self.out_frame_bytes), dtype=torch.uint8,
+                           device=f"cuda:{self.device}")
+
+    def __call__(self, frames, out=None, stream=None):
+        import torch
+
+        if frames.dtype != torch.uint8 or not frames.is_cuda or not frames.is_contiguous():
+            raise ValueError("frames must be a contiguous torch.uint8 CUDA tensor")
+        if frames.numel() % self.in_frame_bytes:
+            raise ValueError("frames does not hold a whole number of frames")
+        n = frames.numel() // self.in_frame_bytes
+        if out is None:
+            out = self.alloc_out(n)
+        elif (out.dtype != torch.uint8 or not out.is_cuda or not out.is_contiguous()
+              or out.numel() != n * self.out_frame_bytes):
+            raise ValueError("out has the wrong dtype, device, layout or size")
+        s = stream if stream is not None else torch.cuda.current_stream()
+        ds_run(self._h, frames.data_ptr(), n, out.data_ptr(), s.cuda_stream)
+        return out
+
+    def run_host(self, host_frames, host_out=None, stream=None):
+        """Host-resident path (ds_run_host): pinned CPU uint8 tensors in/out.
+        Asynchronous on the stream; synchronise before reading host_out."""
+        import torch
+
+        if host_frames.dtype != torch.uint8 or host_frames.is_cuda or not host_frames.is_contiguous():
+            raise ValueError("host_frames must be a contiguous CPU torch.uint8 tensor")
+        n = host_frames.numel() // self.in_frame_bytes
+        if host_out is None:
+            host_out = torch.empty((n, self.out_frame_bytes), dtype=torch.uint8,
+                                   pin_memory=host_frames.is_pinned())
+        s = stream if stream is not None else torch.cuda.current_stream()
+        ds_run_host(self._h, host_frames.data_ptr(), n, host_out.data_ptr(), s.cuda_stream)
+        return host_out
+
+
+def generate_frames(n: int, in_frame_bytes: int, seed: int = 1, first_frame: int = 0,
+                    device=None, out=None):
+    """Synthetic frames on the device by global frame index (ds_generate),
+    byte-identical to synth.random_frames(seed, first_frame, n, ...)."""
+    import torch
+
+    if out is None:
+        out = torch.empty((n, in_frame_bytes), dtype=torch.uint8,
+                          device=device if device is not None else "cuda")
+    ds_generate(out.data_ptr(), n * in_frame_bytes, seed, first_frame * in_frame_bytes,
+                torch.cuda.current_stream(out.device).cuda_stream)
+    return out
+
+
+__all__ = [n for n, _, _ in SIGNATURES] + [
+    "Downscaler", "DSError", "make_spec", "generate_frames", "lib", "lib_path", "stage_to_dict",
+]

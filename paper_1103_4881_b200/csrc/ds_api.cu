@@ -1,0 +1,587 @@
+// ds_api.cu -- the C ABI of include/ds.h: validation, planning, launches,
+// and the host-resident streaming path.  Citations: P:n = PAPER.md line n,
+// S:n = SPEC.md line n, SURVEY sec. n.
+#include <algorithm>
+#include <atomic>
+#include <climits>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+
+#include "ds.h"
+#include "ds_kernels.cuh"
+
+namespace {
+
+thread_local int g_last_error = DS_OK;
+
+constexpr int kHostSlots = 3;                       // ds_run_host pipeline depth
+constexpr int64_t kUnitTargetBytes = 24 * 1024;     // K-N1 band size target
+constexpr int kSmemLimit = 227 * 1024;              // per-CTA opt-in maximum
+constexpr int64_t kHostChunkBytes = 32LL << 20;     // ds_run_host chunk target
+
+struct HostSlot {
+    uint8_t* d_in = nullptr;
+    uint8_t* d_out = nullptr;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t done = nullptr;
+};
+
+int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+}  // namespace
+
+struct ds_handle {
+    int device = 0;
+    int sm_count = 0;
+    int32_t W = 0, H = 0, channels = 0;
+    ds_filter_spec spec{};
+    ds_plan_info plan{};
+    // K-N1 launch configuration
+    int ncw = 4;                 // consumer warps per CTA
+    int stages = 4;              // ring depth
+    int ctas_per_sm = 0;         // 0 = occupancy maximum
+    int32_t stage_stride = 0, out_stride = 0;
+    int kernel_pref = DS_KERNEL_AUTO;
+    std::atomic<int> last_kernel{DS_KERNEL_AUTO};
+    // ds_run_host state (lazily allocated, guarded by host_mu)
+    std::mutex host_mu;
+    int64_t host_chunk = 0;      // frames per chunk, 0 = auto
+    int64_t host_alloc_frames = 0;
+    HostSlot slots[kHostSlots];
+    cudaEvent_t fork_ev = nullptr;
+    bool host_init = false;
+};
+
+namespace {
+
+void default_spec(ds_filter_spec* s) {
+    std::memset(s, 0, sizeof *s);
+    // hfilter_8to3
+    s->h.pattern = 8; s->h.paving = 8; s->h.origin = 0; s->h.outputs = 3;
+    s->h.weight[0][0] = 1; s->h.weight[0][1] = 5;
+    s->h.weight[1][3] = 3; s->h.weight[1][4] = 3;
+    s->h.weight[2][6] = 5; s->h.weight[2][7] = 1;
+    s->h.divisor = 6; s->h.bias = 3;
+    // vfilter_9to4
+    s->v.pattern = 9; s->v.paving = 9; s->v.origin = 0; s->v.outputs = 4;
+    s->v.weight[0][0] = 3; s->v.weight[0][1] = 5;
+    s->v.weight[1][2] = 1; s->v.weight[1][3] = 7;
+    s->v.weight[2][5] = 7; s->v.weight[2][6] = 1;
+    s->v.weight[3][7] = 5; s->v.weight[3][8] = 3;
+    s->v.divisor = 8; s->v.bias = 4;
+    s->chroma = DS_CHROMA_420;
+}
+
+bool stage_equal(const ds_stage_spec& a, const ds_stage_spec& b) {
+    return std::memcmp(&a, &b, sizeof a) == 0;
+}
+
+int check_stage(const ds_stage_spec& s) {
+    if (s.pattern < 1 || s.pattern > DS_MAX_PATTERN) return DS_EUNSUPPORTED;
+    if (s.paving < 1 || s.paving > 4096) return DS_EUNSUPPORTED;
+    if (s.outputs < 1 || s.outputs > DS_MAX_OUTPUTS) return DS_EUNSUPPORTED;
+    if (s.divisor < 1 || s.divisor > (1 << 24)) return DS_EUNSUPPORTED;
+    if (s.bias < -(1 << 24) || s.bias > (1 << 24)) return DS_EUNSUPPORTED;
+    if (s.origin < -(1 << 20) || s.origin > (1 << 20)) return DS_EUNSUPPORTED;
+    for (int k = 0; k < DS_MAX_OUTPUTS; ++k)
+        for (int i = 0; i < DS_MAX_PATTERN; ++i) {
+            const int32_t w = s.weight[k][i];
+            if (w < -65535 || w > 65535) return DS_EUNSUPPORTED;
+            if ((k >= s.outputs || i >= s.pattern) && w != 0) return DS_EUNSUPPORTED;
+        }
+    return DS_OK;
+}
+
+// K-N1 band choice: luma takes the largest
+// divisor k of its 9-row group count with 8 k W <= target; the other planes
+// take the divisor whose staged bytes are closest to luma's, so units are
+// (near-)equal in bytes and a static round-robin balances the SMs.
+int largest_divisor_below(int G, int64_t per_group, int64_t target) {
+    int best = 1;
+    for (int d = 1; d <= G; ++d)
+        if (G % d == 0 && per_group * d <= target) best = d;
+    return best;
+}
+int closest_divisor(int G, int64_t per_group, int64_t target) {
+    int best = 1;
+    int64_t bestd = INT64_MAX;
+    for (int d = 1; d <= G; ++d) {
+        if (G % d) continue;
+        const int64_t diff = std::llabs(per_group * d - target);
+        if (diff < bestd) { bestd = diff; best = d; }
+    }
+    return best;
+}
+
+int64_t fused_smem_bytes(int stages, int32_t stage_stride, int32_t out_stride) {
+    return (int64_t)stages * stage_stride + (int64_t)ds::kOutSlots * out_stride +
+           (int64_t)2 * stages * 8;
+}
+
+int make_plan(int32_t W, int32_t H, int32_t channels, const ds_filter_spec* spec_in,
+              ds_filter_spec* spec_out, ds_plan_info* info) {
+    ds_filter_spec spec;
+    if (spec_in) spec = *spec_in; else default_spec(&spec);
+    if (W < 1 || H < 1) return DS_ESHAPE;
+    if (channels != 1 && channels != 3) return DS_EUNSUPPORTED;
+    if (channels == 3 && spec.chroma != DS_CHROMA_444 && spec.chroma != DS_CHROMA_420)
+        return DS_EUNSUPPORTED;
+    int rc = check_stage(spec.h);
+    if (rc) return rc;
+    rc = check_stage(spec.v);
+    if (rc) return rc;
+
+    ds_plan_info pi;
+    std::memset(&pi, 0, sizeof pi);
+    pi.n_planes = channels;
+    int64_t inb = 0, outb = 0;
+    for (int p = 0; p < channels; ++p) {
+        int32_t pw = W, ph = H;
+        if (channels == 3 && spec.chroma == DS_CHROMA_420 && p > 0) {
+            if (W % 2 || H % 2) return DS_ESHAPE;
+            pw = W / 2; ph = H / 2;
+        }
+        if (pw % spec.h.paving || ph % spec.v.paving) return DS_ESHAPE;
+        pi.in_w[p] = pw; pi.in_h[p] = ph;
+        pi.out_w[p] = spec.h.outputs * (pw / spec.h.paving);    // 3W/8
+        pi.out_h[p] = spec.v.outputs * (ph / spec.v.paving);    // 4H/9
+        pi.in_offset[p] = inb; pi.out_offset[p] = outb;
+        inb += (int64_t)pw * ph;
+        outb += (int64_t)pi.out_w[p] * pi.out_h[p];
+    }
+    pi.in_frame_bytes = inb;
+    pi.out_frame_bytes = outb;
+
+    ds_filter_spec def;
+    default_spec(&def);
+    // K-N1 eligibility: SPEC's taps (the kernel hard-codes them and skips the
+    // dead row 4 of every 9-row group) and every plane width a multiple of
+    // 16 (two packets per 16-byte vector; 16-byte-aligned bulk copies).
+    bool fused = stage_equal(spec.h, def.h) && stage_equal(spec.v, def.v);
+    for (int p = 0; p < channels && fused; ++p) fused = (pi.in_w[p] % 16 == 0);
+    if (fused) {
+        const int G0 = pi.in_h[0] / 9;
+        const int k0 = largest_divisor_below(G0, 8LL * pi.in_w[0], kUnitTargetBytes);
+        const int64_t target = 8LL * k0 * pi.in_w[0];
+        int64_t units = 0, umax = 0, omax = 0;
+        for (int p = 0; p < channels; ++p) {
+            const int G = pi.in_h[p] / 9;
+            const int k = p == 0 ? k0 : closest_divisor(G, 8LL * pi.in_w[p], target);
+            pi.band_groups[p] = k;
+            units += G / k;
+            umax = std::max<int64_t>(umax, 8LL * k * pi.in_w[p]);
+            omax = std::max<int64_t>(omax, 4LL * k * pi.out_w[p]);
+        }
+        pi.units_per_frame = units;
+        pi.unit_in_bytes_max = umax;
+        pi.unit_out_bytes_max = omax;
+        // at least a 2-deep ring must fit in one CTA's shared memory
+        fused = fused_smem_bytes(2, (int32_t)round_up(umax, 128), (int32_t)round_up(omax, 128)) <=
+                kSmemLimit;
+    }
+    pi.fused_eligible = fused ? 1 : 0;
+    if (!fused) {
+        for (int p = 0; p < DS_MAX_PLANES; ++p) pi.band_groups[p] = 0;
+        pi.units_per_frame = pi.unit_in_bytes_max = pi.unit_out_bytes_max = 0;
+    }
+    *info = pi;
+    if (spec_out) *spec_out = spec;
+    return DS_OK;
+}
+
+// ----------------------------------------------------------- K-N1 launch --
+using FusedFn = void (*)(const ds::FusedParams);
+
+FusedFn fused_fn(int ncw) {
+    switch (ncw) {
+        case 1: return ds::ds_fused_band_kernel<1>;
+        case 2: return ds::ds_fused_band_kernel<2>;
+        case 4: return ds::ds_fused_band_kernel<4>;
+        default: return ds::ds_fused_band_kernel<8>;
+    }
+}
+
+int max_tasks(const ds_plan_info& pi) {
+    int t = 0;
+    for (int p = 0; p < pi.n_planes; ++p) t = std::max(t, pi.in_w[p] / 16 * pi.band_groups[p]);
+    return t;
+}
+
+// Ring depth that fits, capped by the request.
+int fit_stages(const ds_handle* h, int want) {
+    int s = std::max(2, std::min(8, want));
+    while (s > 2 && fused_smem_bytes(s, h->stage_stride, h->out_stride) > kSmemLimit) --s;
+    return s;
+}
+
+int fused_grid(const ds_handle* h, int64_t n_units, int* grid, int* block, int* smem) {
+    const int stages = fit_stages(h, h->stages);
+    const int sm = (int)fused_smem_bytes(stages, h->stage_stride, h->out_stride);
+    const int threads = (h->ncw + 1) * 32;
+    FusedFn fn = fused_fn(h->ncw);
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, sm) != cudaSuccess)
+        return DS_ECUDA;
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, sm) != cudaSuccess ||
+        occ < 1)
+        return DS_ECUDA;
+    if (h->ctas_per_sm > 0) occ = std::min(occ, h->ctas_per_sm);
+    const int64_t g = std::min<int64_t>(n_units, (int64_t)occ * h->sm_count);
+    *grid = (int)std::max<int64_t>(g, 1);
+    *block = threads;
+    *smem = sm;
+    return DS_OK;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+int launch_fused(ds_handle* h, const uint8_t* in, int64_t n, uint8_t* out, cudaStream_t st) {
+    const ds_plan_info& pi = h->plan;
+    ds::FusedParams p;
+    std::memset(&p, 0, sizeof p);
+    p.in = in; p.out = out;
+    p.in_frame = pi.in_frame_bytes; p.out_frame = pi.out_frame_bytes;
+    p.upf = (int32_t)pi.units_per_frame;
+    p.n_units = n * pi.units_per_frame;
+    p.n_planes = pi.n_planes;
+    p.stage_stride = h->stage_stride;
+    p.out_stride = h->out_stride;
+    const bool out_al = aligned16(out) && pi.out_frame_bytes % 16 == 0;
+    int32_t start = 0;
+    for (int q = 0; q < pi.n_planes; ++q) {
+        ds::FusedPlane& P = p.pl[q];
+        P.in_off = pi.in_offset[q];
+        P.out_off = pi.out_offset[q];
+        P.W = pi.in_w[q];
+        P.Wout = pi.out_w[q];
+        P.k = pi.band_groups[q];
+        P.chunks = P.W / 16;
+        P.tasks = P.chunks * P.k;
+        P.unit_start = start;
+        P.unit_in = 8 * P.k * P.W;
+        P.unit_out = 4 * P.k * P.Wout;
+        P.bulk_store = (out_al && P.out_off % 16 == 0 && P.unit_out % 16 == 0) ? 1 : 0;
+        start += pi.in_h[q] / (9 * P.k);
+    }
+    int grid, block, smem;
+    int rc = fused_grid(h, p.n_units, &grid, &block, &smem);
+    if (rc) return rc;
+    p.stages = fit_stages(h, h->stages);
+    fused_fn(h->ncw)<<<grid, block, smem, st>>>(p);
+    return cudaGetLastError() == cudaSuccess ? DS_OK : DS_ECUDA;
+}
+
+int launch_generic(ds_handle* h, const uint8_t* in, int64_t n, uint8_t* out, cudaStream_t st) {
+    const ds_plan_info& pi = h->plan;
+    ds::GenericParams p;
+    std::memset(&p, 0, sizeof p);
+    p.in = in; p.out = out;
+    p.in_frame = pi.in_frame_bytes; p.out_frame = pi.out_frame_bytes;
+    p.total_out = n * pi.out_frame_bytes;
+    p.n_planes = pi.n_planes;
+    for (int q = 0; q < pi.n_planes; ++q) {
+        p.in_off[q] = pi.in_offset[q];
+        p.out_off[q] = pi.out_offset[q];
+        p.W[q] = pi.in_w[q];
+        p.H[q] = pi.in_h[q];
+        p.Wout[q] = pi.out_w[q];
+    }
+    p.h = h->spec.h;
+    p.v = h->spec.v;
+    const int threads = 256;
+    const int64_t blocks = std::min<int64_t>((p.total_out + threads - 1) / threads,
+                                             (int64_t)h->sm_count * 8);
+    ds::ds_generic_kernel<<<(int)std::max<int64_t>(blocks, 1), threads, 0, st>>>(p);
+    return cudaGetLastError() == cudaSuccess ? DS_OK : DS_ECUDA;
+}
+
+int choose_kernel(const ds_handle* h, const uint8_t* in) {
+    if (h->kernel_pref == DS_KERNEL_GENERIC) return DS_KERNEL_GENERIC;
+    if (!h->plan.fused_eligible || !aligned16(in)) return DS_KERNEL_GENERIC;
+    return DS_KERNEL_FUSED;
+}
+
+// Device binding: run with the handle's device current, restore after.
+struct DeviceGuard {
+    int prev = -1;
+    bool ok = true;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) != cudaSuccess) { ok = false; return; }
+        if (prev != dev && cudaSetDevice(dev) != cudaSuccess) ok = false;
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+bool device_ptr_on(const void* p, int dev) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    if (a.type != cudaMemoryTypeDevice && a.type != cudaMemoryTypeManaged) return false;
+    return a.device == dev;
+}
+
+bool ranges_overlap(const void* a, int64_t na, const void* b, int64_t nb) {
+    const uintptr_t x = reinterpret_cast<uintptr_t>(a), y = reinterpret_cast<uintptr_t>(b);
+    return x < y + (uintptr_t)nb && y < x + (uintptr_t)na;
+}
+
+int run_device(ds_handle* h, const uint8_t* in, int64_t n, uint8_t* out, cudaStream_t st) {
+    const int k = choose_kernel(h, in);
+    const int rc = (k == DS_KERNEL_FUSED) ? launch_fused(h, in, n, out, st)
+                                          : launch_generic(h, in, n, out, st);
+    if (rc == DS_OK) h->last_kernel.store(k);
+    return rc;
+}
+
+void free_host_state(ds_handle* h) {
+    for (auto& s : h->slots) {
+        if (s.stream) cudaStreamSynchronize(s.stream);
+        if (s.d_in) cudaFree(s.d_in);
+        if (s.d_out) cudaFree(s.d_out);
+        if (s.done) cudaEventDestroy(s.done);
+        if (s.stream) cudaStreamDestroy(s.stream);
+        s = HostSlot{};
+    }
+    if (h->fork_ev) cudaEventDestroy(h->fork_ev);
+    h->fork_ev = nullptr;
+    h->host_alloc_frames = 0;
+    h->host_init = false;
+}
+
+}  // namespace
+
+// ================================================================ C ABI ==
+extern "C" {
+
+DS_API int ds_default_spec(ds_filter_spec* out) {
+    if (!out) return DS_EINVAL;
+    default_spec(out);
+    return DS_OK;
+}
+
+DS_API int ds_plan(int32_t frame_w, int32_t frame_h, int32_t channels,
+                   const ds_filter_spec* spec, ds_plan_info* out) {
+    if (!out) return DS_EINVAL;
+    return make_plan(frame_w, frame_h, channels, spec, nullptr, out);
+}
+
+DS_API ds_handle* ds_create(int32_t frame_w, int32_t frame_h, int32_t channels,
+                            const ds_filter_spec* filter_spec) {
+    ds_filter_spec spec;
+    ds_plan_info pi;
+    int rc = make_plan(frame_w, frame_h, channels, filter_spec, &spec, &pi);
+    if (rc) { g_last_error = rc; return nullptr; }
+    int dev = 0, sms = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+        cudaGetLastError();
+        g_last_error = DS_ECUDA;
+        return nullptr;
+    }
+    ds_handle* h = new (std::nothrow) ds_handle();
+    if (!h) { g_last_error = DS_ENOMEM; return nullptr; }
+    h->device = dev;
+    h->sm_count = sms;
+    h->W = frame_w; h->H = frame_h; h->channels = channels;
+    h->spec = spec;
+    h->plan = pi;
+    if (pi.fused_eligible) {
+        const int t = max_tasks(pi);
+        const int w = (t + 31) / 32;
+        h->ncw = w <= 1 ? 1 : w <= 2 ? 2 : w <= 4 ? 4 : 8;
+        h->stage_stride = (int32_t)round_up(pi.unit_in_bytes_max, 128);
+        h->out_stride = (int32_t)round_up(pi.unit_out_bytes_max, 128);
+        h->stages = 4;
+    }
+    g_last_error = DS_OK;
+    return h;
+}
+
+DS_API int ds_run(ds_handle* h, const uint8_t* in, int64_t n, uint8_t* out, ds_stream_t stream) {
+    if (!h || n < 0) return DS_EINVAL;
+    if (n == 0) return DS_OK;
+    if (!in || !out) return DS_EINVAL;
+    const int64_t nin = n * h->plan.in_frame_bytes, nout = n * h->plan.out_frame_bytes;
+    if (ranges_overlap(in, nin, out, nout)) return DS_EINVAL;
+    DeviceGuard g(h->device);
+    if (!g.ok) { cudaGetLastError(); return DS_ECUDA; }
+    if (!device_ptr_on(in, h->device) || !device_ptr_on(out, h->device)) return DS_EINVAL;
+    return run_device(h, in, n, out, reinterpret_cast<cudaStream_t>(stream));
+}
+
+DS_API int ds_set_host_chunk(ds_handle* h, int64_t frames) {
+    if (!h || frames < 0) return DS_EINVAL;
+    std::lock_guard<std::mutex> lk(h->host_mu);
+    h->host_chunk = frames;
+    return DS_OK;
+}
+
+DS_API int ds_run_host(ds_handle* h, const uint8_t* host_in, int64_t n, uint8_t* host_out,
+                       ds_stream_t stream) {
+    if (!h || n < 0) return DS_EINVAL;
+    if (n == 0) return DS_OK;
+    if (!host_in || !host_out) return DS_EINVAL;
+    const int64_t fin = h->plan.in_frame_bytes, fout = h->plan.out_frame_bytes;
+    if (ranges_overlap(host_in, n * fin, host_out, n * fout)) return DS_EINVAL;
+    std::lock_guard<std::mutex> lk(h->host_mu);
+    DeviceGuard g(h->device);
+    if (!g.ok) { cudaGetLastError(); return DS_ECUDA; }
+    cudaStream_t caller = reinterpret_cast<cudaStream_t>(stream);
+    int64_t chunk = h->host_chunk > 0 ? h->host_chunk
+                                      : std::max<int64_t>(1, kHostChunkBytes / std::max<int64_t>(fin, 1));
+    chunk = std::min(chunk, n);
+    if (!h->host_init) {
+        for (auto& s : h->slots) {
+            if (cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking) != cudaSuccess ||
+                cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming) != cudaSuccess) {
+                cudaGetLastError();
+                free_host_state(h);
+                return DS_ECUDA;
+            }
+        }
+        if (cudaEventCreateWithFlags(&h->fork_ev, cudaEventDisableTiming) != cudaSuccess) {
+            cudaGetLastError();
+            free_host_state(h);
+            return DS_ECUDA;
+        }
+        h->host_init = true;
+    }
+    if (h->host_alloc_frames < chunk) {
+        for (auto& s : h->slots) {
+            cudaStreamSynchronize(s.stream);
+            if (s.d_in) cudaFree(s.d_in);
+            if (s.d_out) cudaFree(s.d_out);
+            s.d_in = s.d_out = nullptr;
+        }
+        h->host_alloc_frames = 0;
+        for (auto& s : h->slots) {
+            // +16: keep device buffers 16-byte aligned for K-N1 bulk copies
+            if (cudaMalloc(&s.d_in, chunk * fin) != cudaSuccess ||
+                cudaMalloc(&s.d_out, chunk * fout) != cudaSuccess) {
+                cudaGetLastError();
+                free_host_state(h);
+                return DS_ENOMEM;
+            }
+        }
+        h->host_alloc_frames = chunk;
+    }
+    // fork: internal streams start after the work already queued on `stream`
+    if (cudaEventRecord(h->fork_ev, caller) != cudaSuccess) { cudaGetLastError(); return DS_ECUDA; }
+    for (auto& s : h->slots)
+        if (cudaStreamWaitEvent(s.stream, h->fork_ev, 0) != cudaSuccess) { cudaGetLastError(); return DS_ECUDA; }
+    // chunk c on slot c % 3: H2D -> kernel -> D2H in stream order; slots
+    // overlap each other's copies (two copy engines) and compute.
+    int64_t c = 0;
+    for (int64_t f0 = 0; f0 < n; f0 += chunk, ++c) {
+        const int64_t m = std::min(chunk, n - f0);
+        HostSlot& s = h->slots[c % kHostSlots];
+        if (cudaMemcpyAsync(s.d_in, host_in + f0 * fin, m * fin, cudaMemcpyHostToDevice, s.stream) !=
+            cudaSuccess) { cudaGetLastError(); return DS_ECUDA; }
+        int rc = run_device(h, s.d_in, m, s.d_out, s.stream);
+        if (rc) return rc;
+        if (cudaMemcpyAsync(host_out + f0 * fout, s.d_out, m * fout, cudaMemcpyDeviceToHost,
+                            s.stream) != cudaSuccess) { cudaGetLastError(); return DS_ECUDA; }
+    }
+    // join: `stream` waits for every slot
+    for (auto& s : h->slots) {
+        if (cudaEventRecord(s.done, s.stream) != cudaSuccess ||
+            cudaStreamWaitEvent(caller, s.done, 0) != cudaSuccess) { cudaGetLastError(); return DS_ECUDA; }
+    }
+    return DS_OK;
+}
+
+DS_API void ds_destroy(ds_handle* h) {
+    if (!h) return;
+    {
+        std::lock_guard<std::mutex> lk(h->host_mu);
+        DeviceGuard g(h->device);
+        free_host_state(h);
+    }
+    delete h;
+}
+
+DS_API int ds_last_error(void) { return g_last_error; }
+
+DS_API const char* ds_strerror(int code) {
+    switch (code) {
+        case DS_OK: return "ok";
+        case DS_EINVAL: return "invalid argument";
+        case DS_ESHAPE: return "plane shape not divisible by the tiler paving (S:551)";
+        case DS_EUNSUPPORTED: return "unsupported channels or filter spec";
+        case DS_ECUDA: return "CUDA runtime error";
+        case DS_ENOMEM: return "out of memory";
+        default: return "unknown error";
+    }
+}
+
+DS_API int64_t ds_in_frame_bytes(const ds_handle* h) { return h ? h->plan.in_frame_bytes : -1; }
+DS_API int64_t ds_out_frame_bytes(const ds_handle* h) { return h ? h->plan.out_frame_bytes : -1; }
+
+DS_API int ds_plane_dims(const ds_handle* h, int plane, int32_t* in_w, int32_t* in_h,
+                         int32_t* out_w, int32_t* out_h) {
+    if (!h || plane < 0 || plane >= h->plan.n_planes) return DS_EINVAL;
+    if (in_w) *in_w = h->plan.in_w[plane];
+    if (in_h) *in_h = h->plan.in_h[plane];
+    if (out_w) *out_w = h->plan.out_w[plane];
+    if (out_h) *out_h = h->plan.out_h[plane];
+    return DS_OK;
+}
+
+DS_API int ds_set_kernel(ds_handle* h, int32_t kernel) {
+    if (!h) return DS_EINVAL;
+    if (kernel != DS_KERNEL_AUTO && kernel != DS_KERNEL_FUSED && kernel != DS_KERNEL_GENERIC)
+        return DS_EINVAL;
+    if (kernel == DS_KERNEL_FUSED && !h->plan.fused_eligible) return DS_EUNSUPPORTED;
+    h->kernel_pref = kernel;
+    return DS_OK;
+}
+
+DS_API int ds_last_kernel(const ds_handle* h) { return h ? h->last_kernel.load() : DS_EINVAL; }
+
+DS_API int ds_set_tuning(ds_handle* h, int32_t stages, int32_t ctas_per_sm) {
+    if (!h || stages < 2 || stages > 8 || ctas_per_sm < 0 || ctas_per_sm > 32) return DS_EINVAL;
+    h->stages = stages;
+    h->ctas_per_sm = ctas_per_sm;
+    return DS_OK;
+}
+
+DS_API int ds_launch_shape(const ds_handle* h, int64_t n, int32_t* grid, int32_t* block,
+                           int32_t* smem) {
+    if (!h || n < 0 || !h->plan.fused_eligible) return DS_EINVAL;
+    DeviceGuard g(h->device);
+    int gr, bl, sm;
+    const int rc = fused_grid(h, std::max<int64_t>(1, n * h->plan.units_per_frame), &gr, &bl, &sm);
+    if (rc) return rc;
+    if (grid) *grid = gr;
+    if (block) *block = bl;
+    if (smem) *smem = sm;
+    return DS_OK;
+}
+
+DS_API int ds_generate(uint8_t* dev, int64_t n_bytes, uint64_t seed, int64_t start,
+                       ds_stream_t stream) {
+    if (n_bytes < 0 || start < 0 || (n_bytes > 0 && !dev)) return DS_EINVAL;
+    if (n_bytes == 0) return DS_OK;
+    int d = 0, sms = 0;
+    if (cudaGetDevice(&d) != cudaSuccess ||
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d) != cudaSuccess) {
+        cudaGetLastError();
+        return DS_ECUDA;
+    }
+    const int threads = 256;
+    const int64_t blocks =
+        std::min<int64_t>((n_bytes / 16 + threads) / threads, (int64_t)sms * 16);
+    ds::ds_generate_kernel<<<(int)std::max<int64_t>(blocks, 1), threads, 0,
+                             reinterpret_cast<cudaStream_t>(stream)>>>(
+        dev, n_bytes, seed * 0x9E3779B97F4A7C15ull, start, aligned16(dev) ? 1 : 0);
+    return cudaGetLastError() == cudaSuccess ? DS_OK : DS_ECUDA;
+}
+
+}  // extern "C"

@@ -1,0 +1,378 @@
+// ds_kernels.cuh -- sm_100a kernels of the arxiv 1103.4881 downscaler.
+//
+// Citation key: P:n = PAPER.md line n, S:n = SPEC.md line n, SURVEY sec. n.
+//
+//   K-N1 ds_fused_band_kernel   persistent, warp-specialised: one producer
+//        lane streams whole-width row bands (the input patterns of a group
+//        of vertical repetitions, minus the dead row) HBM -> shared memory
+//        with 1-D TMA bulk copies (cp.async.bulk + mbarrier ring); consumer
+//        warps run the horizontal task (taps S:530) and the vertical
+//        task (taps S:540) on-chip with the u8 intermediate in
+//        registers, stage the output band in shared memory and
+//        write it back with one TMA bulk store.  No tensor cores: this is a
+//        memory-bound stencil.
+//   K-N2 ds_generic_kernel      one thread per output pixel, any stage spec
+//        (halos P > S, origin != 0, any taps), any alignment; follows the
+//        tiler definition e = (o + S r + f) mod n directly.
+//   K-N4 ds_generate_kernel     counter-hash synthetic frames (test/bench).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "ds.h"
+
+namespace ds {
+
+// ------------------------------------------------------------- parameters --
+struct FusedPlane {
+    int64_t in_off, out_off;   // plane offsets inside one frame (bytes)
+    int32_t W, Wout;           // input / output row bytes
+    int32_t k;                 // 9-row groups per unit (band)
+    int32_t chunks;            // 16-byte column chunks per row = W / 16
+    int32_t tasks;             // chunks * k  (one task = 16 B x 8 rows)
+    int32_t unit_start;        // first per-frame unit index of this plane
+    int32_t unit_in;           // bytes staged per unit = 8 * k * W
+    int32_t unit_out;          // bytes produced per unit = 4 * k * Wout
+    int32_t bulk_store;        // 1: TMA bulk store legal (16 B aligned)
+    int32_t pad_;
+};
+
+struct FusedParams {
+    const uint8_t* in;
+    uint8_t* out;
+    int64_t in_frame, out_frame;
+    int64_t n_units;           // n_frames * units_per_frame
+    int32_t upf;               // units per frame
+    int32_t n_planes;
+    int32_t stages;            // ring depth
+    int32_t stage_stride;      // bytes per ring slot (>= max unit_in, 128-aligned)
+    int32_t out_stride;        // bytes per output slot (>= max unit_out, 128-aligned)
+    int32_t pad_;
+    FusedPlane pl[DS_MAX_PLANES];
+};
+
+struct GenericParams {
+    const uint8_t* in;
+    uint8_t* out;
+    int64_t in_frame, out_frame, total_out;
+    int64_t in_off[DS_MAX_PLANES], out_off[DS_MAX_PLANES];
+    int32_t W[DS_MAX_PLANES], H[DS_MAX_PLANES], Wout[DS_MAX_PLANES];
+    int32_t n_planes;
+    ds_stage_spec h, v;
+};
+
+constexpr int kOutSlots = 3;   // output staging ring (one barrier per unit)
+
+// ------------------------------------------------------ PTX helper wrappers --
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+                 : "memory");
+}
+__device__ __forceinline__ void fence_barrier_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "DS_WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra DS_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+// 1-D TMA bulk copy global -> shared, completion counted on `bar` (bytes).
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
+// 1-D TMA bulk copy shared -> global (bulk-group completion).
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+                 "r"(smem_u32(src)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() {
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+__device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+__device__ __forceinline__ uint4 lds128(const uint8_t* p) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "r"(smem_u32(p)));
+    return v;
+}
+__device__ __forceinline__ void sts16(uint8_t* p, uint32_t v) {
+    asm volatile("st.shared.u16 [%0], %1;" ::"r"(smem_u32(p)), "h"((unsigned short)v)
+                 : "memory");
+}
+
+// ------------------------------------------------------- filter arithmetic --
+// floor(x / 6) for 0 <= x < 2^31: umulhi(x, ceil(2^32 / 6)).
+__device__ __forceinline__ uint32_t div6(uint32_t x) { return __umulhi(x, 0x2AAAAAABu); }
+
+// Horizontal task on one 16-byte row chunk = two 8-pixel packets
+// (S:527-531): out0 = (p0 + 5 p1 + 3)/6, out1 = (3 p3 + 3 p4 + 3)/6 =
+// (p3 + p4 + 1) >> 1, out2 = (5 p6 + p7 + 3)/6; p2 and p5 have zero weight.
+// The six u8 mid values are returned packed in 16-bit lanes:
+//   q0 = A0 | A1 << 16,  q1 = A2 | B0 << 16,  q2 = B1 | B2 << 16.
+__device__ __forceinline__ void h_chunk(uint4 v, uint32_t& q0, uint32_t& q1, uint32_t& q2) {
+    const uint32_t tA = __byte_perm(v.x, v.y, 0x7643);   // [p3 p4 p6 p7] of packet A
+    const uint32_t tB = __byte_perm(v.z, v.w, 0x7643);
+    const uint32_t a0 = div6(__dp4a(v.x, 0x0501u, 3u));
+    const uint32_t a1 = __dp4a(tA, 0x0101u, 1u) >> 1;
+    const uint32_t a2 = div6(__dp4a(tA, 0x01050000u, 3u));
+    const uint32_t b0 = div6(__dp4a(v.z, 0x0501u, 3u));
+    const uint32_t b1 = __dp4a(tB, 0x0101u, 1u) >> 1;
+    const uint32_t b2 = div6(__dp4a(tB, 0x01050000u, 3u));
+    q0 = __byte_perm(a0, a1, 0x5410);
+    q1 = __byte_perm(a2, b0, 0x5410);
+    q2 = __byte_perm(b1, b2, 0x5410);
+}
+
+// Vertical task output row: (wa*m_a + wb*m_b + 4) >> 3 on two
+// 16-bit lanes at once.  Scaling by 32 puts the quotient in byte 1 of each
+// lane: 32*(wa*m_a + wb*m_b + 4) <= 32*2044 < 2^16, so lanes never carry.
+template <uint32_t WA, uint32_t WB>
+__device__ __forceinline__ uint32_t v_pair(uint32_t qa, uint32_t qb) {
+    return qa * (32u * WA) + qb * (32u * WB) + 0x00800080u;
+}
+
+// ------------------------------------------------------------------- K-N1 --
+// Work unit = (frame, plane, band of k 9-row groups), full plane width.
+// Ring slot layout: for group g, rows 8g..8g+3 hold input rows 9g+0..3 and
+// rows 8g+4..8g+7 hold input rows 9g+5..8 (row 9g+4 has zero V weight,
+// S:540, and is never read from HBM).
+template <int NCW>
+__global__ void __launch_bounds__((NCW + 1) * 32)
+    ds_fused_band_kernel(const __grid_constant__ FusedParams p) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    constexpr int NC = NCW * 32;
+    const int S = p.stages;
+    uint8_t* ring = smem;
+    uint8_t* outs = smem + (size_t)S * p.stage_stride;
+    uint64_t* full = reinterpret_cast<uint64_t*>(outs + (size_t)kOutSlots * p.out_stride);
+    uint64_t* empty = full + S;
+
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], NCW);
+        }
+        fence_barrier_init();
+    }
+    __syncthreads();
+
+    const int warp = tid >> 5, lane = tid & 31;
+    if (warp == NCW) {
+        // ---------------- producer: one lane streams bands into the ring --
+        if (lane == 0) {
+            const uint64_t pol = policy_evict_first();
+            int64_t i = 0;
+            for (int64_t u = blockIdx.x; u < p.n_units; u += gridDim.x, ++i) {
+                const int s = (int)(i % S);
+                const uint32_t use = (uint32_t)(i / S);
+                if (use > 0) mbar_wait(&empty[s], (use - 1) & 1);
+                const int64_t f = u / p.upf;
+                const int local = (int)(u - f * p.upf);
+                const int pi = (p.n_planes > 2 && local >= p.pl[2].unit_start)   ? 2
+                               : (p.n_planes > 1 && local >= p.pl[1].unit_start) ? 1
+                                                                                 : 0;
+                const FusedPlane& P = p.pl[pi];
+                const int band = local - P.unit_start;
+                const uint8_t* src =
+                    p.in + f * p.in_frame + P.in_off + (int64_t)band * 9 * P.k * P.W;
+                uint8_t* dst = ring + (size_t)s * p.stage_stride;
+                mbar_arrive_expect_tx(&full[s], (uint32_t)P.unit_in);
+                const uint32_t half = 4u * (uint32_t)P.W;
+                for (int g = 0; g < P.k; ++g) {
+                    const uint8_t* sg = src + (int64_t)9 * g * P.W;
+                    uint8_t* dg = dst + (size_t)8 * g * P.W;
+                    bulk_g2s(dg, sg, half, &full[s], pol);                       // rows 0..3
+                    bulk_g2s(dg + half, sg + (int64_t)5 * P.W, half, &full[s], pol);  // rows 5..8
+                }
+            }
+        }
+        return;
+    }
+
+    // ---------------- consumers ---------------------------------------------
+    int64_t i = 0;
+    for (int64_t u = blockIdx.x; u < p.n_units; u += gridDim.x, ++i) {
+        const int s = (int)(i % S);
+        const int64_t f = u / p.upf;
+        const int local = (int)(u - f * p.upf);
+        const int pi = (p.n_planes > 2 && local >= p.pl[2].unit_start)   ? 2
+                       : (p.n_planes > 1 && local >= p.pl[1].unit_start) ? 1
+                                                                         : 0;
+        const FusedPlane& P = p.pl[pi];
+        const int band = local - P.unit_start;
+        const uint8_t* st = ring + (size_t)s * p.stage_stride;
+        uint8_t* ob = outs + (size_t)(i % kOutSlots) * p.out_stride;
+        const int W = P.W, Wout = P.Wout;
+
+        mbar_wait(&full[s], (uint32_t)(i / S) & 1);
+
+        for (int t = tid; t < P.tasks; t += NC) {
+            const int g = t / P.chunks;
+            const int c = t - g * P.chunks;
+            const uint8_t* base = st + (size_t)8 * g * W + 16 * c;
+            uint4 r[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) r[j] = lds128(base + (size_t)j * W);
+            uint32_t q[8][3];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) h_chunk(r[j], q[j][0], q[j][1], q[j][2]);
+            // V taps: out0 rows (0,1) w (3,5); out1 rows (2,3) w (1,7);
+            // out2 rows (5,6) w (7,1); out3 rows (7,8) w (5,3); slots skip row 4.
+            uint32_t o[4][3];
+#pragma unroll
+            for (int e = 0; e < 3; ++e) {
+                o[0][e] = v_pair<3, 5>(q[0][e], q[1][e]);
+                o[1][e] = v_pair<1, 7>(q[2][e], q[3][e]);
+                o[2][e] = v_pair<7, 1>(q[4][e], q[5][e]);
+                o[3][e] = v_pair<5, 3>(q[6][e], q[7][e]);
+            }
+            uint8_t* orow = ob + (size_t)4 * g * Wout + 6 * c;
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+                const uint32_t lo = __byte_perm(o[kk][0], o[kk][1], 0x7531);
+                const uint32_t hi = __byte_perm(o[kk][2], 0u, 0x4431);
+                uint8_t* d = orow + (size_t)kk * Wout;
+                sts16(d, lo);
+                sts16(d + 2, lo >> 16);
+                sts16(d + 4, hi);
+            }
+        }
+        // every lane of this warp has consumed its reads of slot s
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+
+        uint8_t* dst = p.out + f * p.out_frame + P.out_off + (int64_t)band * P.unit_out;
+        if (P.bulk_store) {
+            fence_proxy_async_smem();      // generic-proxy smem writes -> async proxy
+            named_bar_sync(1, NC);
+            if (tid == 0) {
+                bulk_s2g(dst, ob, (uint32_t)P.unit_out);
+                bulk_commit();
+                bulk_wait_read<1>();       // slot (i-1)%3 free before next barrier
+            }
+        } else {
+            named_bar_sync(1, NC);
+            for (int x = tid; x < P.unit_out; x += NC) dst[x] = ob[x];
+        }
+    }
+    if (tid == 0) bulk_wait_all();
+}
+
+// ------------------------------------------------------------------- K-N2 --
+__device__ __forceinline__ int32_t nn_mod(int32_t a, int32_t m) {
+    int32_t r = a % m;
+    return r < 0 ? r + m : r;
+}
+__device__ __forceinline__ int32_t clamp255(int32_t v) { return v < 0 ? 0 : (v > 255 ? 255 : v); }
+
+// Output (R, C) of a plane: V repetition r0 = R / Qv at slot kv = R % Qv,
+// H repetition r1 = C / Qh at slot jh = C % Qh.  Its V pattern element i is
+// the mid value at row (ov + Sv r0 + i) mod H, column C; each mid value is
+// the H stage over columns (oh + Sh r1 + i') mod W of that row (S:248-252,
+// S:517-520), rounded to u8 before the V stage.
+__global__ void __launch_bounds__(256) ds_generic_kernel(const __grid_constant__ GenericParams p) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < p.total_out;
+         idx += stride) {
+        const int64_t f = idx / p.out_frame;
+        int64_t o = idx - f * p.out_frame;
+        const int pi = (p.n_planes > 2 && o >= p.out_off[2])   ? 2
+                       : (p.n_planes > 1 && o >= p.out_off[1]) ? 1
+                                                               : 0;
+        o -= p.out_off[pi];
+        const int32_t W = p.W[pi], H = p.H[pi], Wout = p.Wout[pi];
+        const int32_t R = (int32_t)(o / Wout), C = (int32_t)(o - (int64_t)R * Wout);
+        const int32_t r0 = R / p.v.outputs, kv = R - r0 * p.v.outputs;
+        const int32_t r1 = C / p.h.outputs, jh = C - r1 * p.h.outputs;
+        const uint8_t* plane = p.in + f * p.in_frame + p.in_off[pi];
+        int32_t accv = p.v.bias;
+        for (int i = 0; i < p.v.pattern; ++i) {
+            const int32_t wv = p.v.weight[kv][i];
+            if (wv == 0) continue;
+            const int32_t row = nn_mod(p.v.origin + p.v.paving * r0 + i, H);
+            const uint8_t* rp = plane + (int64_t)row * W;
+            int32_t acch = p.h.bias;
+            for (int i2 = 0; i2 < p.h.pattern; ++i2) {
+                const int32_t wh = p.h.weight[jh][i2];
+                if (wh == 0) continue;
+                acch += wh * (int32_t)__ldg(rp + nn_mod(p.h.origin + p.h.paving * r1 + i2, W));
+            }
+            accv += wv * clamp255(acch / p.h.divisor);
+        }
+        p.out[f * p.out_frame + p.out_off[pi] + o] = (uint8_t)clamp255(accv / p.v.divisor);
+    }
+}
+
+// ------------------------------------------------------------------- K-N4 --
+__device__ __forceinline__ uint64_t splitmix64(uint64_t z) {
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+__global__ void __launch_bounds__(256)
+    ds_generate_kernel(uint8_t* dst, int64_t n, uint64_t base, int64_t start, int aligned) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x * 16;
+    for (int64_t i0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 16; i0 < n;
+         i0 += stride) {
+        uint32_t w[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            uint32_t x = 0;
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                const uint64_t h = splitmix64(base + (uint64_t)(start + i0 + 4 * q + b));
+                x |= (uint32_t)(h >> 56) << (8 * b);
+            }
+            w[q] = x;
+        }
+        if (aligned && i0 + 16 <= n) {
+            *reinterpret_cast<uint4*>(dst + i0) = make_uint4(w[0], w[1], w[2], w[3]);
+        } else {
+            for (int b = 0; b < 16 && i0 + b < n; ++b) dst[i0 + b] = (uint8_t)(w[b >> 2] >> (8 * (b & 3)));
+        }
+    }
+}
+
+}  // namespace ds

@@ -1,0 +1,73 @@
+"""Frame-parallel sharding across the GPUs of one box.
+
+Frames carry no state between them ("no inter-frame
+state"), so rank r of P owns the contiguous block
+[floor(r N / P), floor((r+1) N / P)) and filters it with no communication.
+The only collective is the final gather of output shards to rank 0, in rank
+(= frame) order, over NCCL (NVLink/NVSwitch) -- never inside the filter.
+
+Host-side logic only; the per-rank compute is ds_run (Downscaler).  The
+gather works with any torch.distributed backend (NCCL on GPUs, gloo in the
+CPU tests).
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+
+def shard_range(total: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous frame block of `rank` (balanced to within one frame)."""
+    if total < 0 or world < 1 or not 0 <= rank < world:
+        raise ValueError("bad shard arguments")
+    return (total * rank) // world, (total * (rank + 1)) // world
+
+
+def gather_frames(local: torch.Tensor, total: int, group=None, dst: int = 0):
+    """Gather every rank's (n_r, frame_bytes) shard to `dst` in frame order.
+
+    Uses point-to-point batches (shards may differ in size by one frame).
+    Returns the (total, frame_bytes) tensor on dst, None elsewhere."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    fb = local.shape[1] if local.dim() == 2 else local.numel()
+    if rank != dst:
+        if local.numel():
+            dist.send(local.contiguous(), dst, group=group)
+        return None
+    out = torch.empty((total, fb), dtype=local.dtype, device=local.device)
+    ops = []
+    for r in range(world):
+        lo, hi = shard_range(total, world, r)
+        if hi == lo:
+            continue
+        if r == dst:
+            out[lo:hi].copy_(local.view(hi - lo, fb))
+        else:
+            ops.append(dist.P2POp(dist.irecv, out[lo:hi], r, group=group))
+    if ops:
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+    return out
+
+
+def run_sharded(total_frames: int, w: int, h: int, channels: int = 3, chroma: str = "420",
+                seed: int = 1, gather: bool = True, spec=None):
+    """Each rank generates its frames by GLOBAL frame index on its own GPU,
+    downscales them with one ds_run, then (optionally) rank 0 gathers.
+
+    Returns (rank-0 gathered output or None, local output, (lo, hi))."""
+    from . import Downscaler, generate_frames
+
+    world = dist.get_world_size() if dist.is_initialized() else 1
+    rank = dist.get_rank() if dist.is_initialized() else 0
+    lo, hi = shard_range(total_frames, world, rank)
+    d = Downscaler(w, h, channels, chroma=chroma, spec=spec)
+    x = generate_frames(hi - lo, d.in_frame_bytes, seed=seed, first_frame=lo)
+    y = d(x)
+    full = None
+    if gather and world > 1:
+        full = gather_frames(y, total_frames)
+    elif gather:
+        full = y
+    return full, y, (lo, hi)

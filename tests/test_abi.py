@@ -1,0 +1,145 @@
+"""Boundary tests that need no GPU: libds.so loads, exports every symbol
+include/ds.h declares, and its host-only logic (validation, geometry,
+K-N1 band planning) is right.  Compute calls are in test_parity_gpu.py."""
+import os
+import re
+import subprocess
+
+import pytest
+
+import paper_1103_4881_b200 as ds
+from conftest import ROOT
+
+HEADER = os.path.join(ROOT, "include", "ds.h")
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    return sorted(set(re.findall(r"DS_API\s+[\w\s\*]+?\b(ds_\w+)\s*\(", src)))
+
+
+def test_header_declares_the_north_star_calls():
+    names = declared_functions()
+    for must in ("ds_create", "ds_run", "ds_destroy"):
+        assert must in names
+
+
+def test_library_exports_every_declared_symbol():
+    L = ds.lib()
+    for name in declared_functions():
+        assert hasattr(L, name), name
+    out = subprocess.check_output(["nm", "-D", "--defined-only", ds.lib_path()], text=True)
+    exported = set(re.findall(r"\bT (ds_\w+)", out))
+    assert set(declared_functions()) <= exported
+    # the binding wraps exactly the header's calls
+    assert sorted(n for n, _, _ in ds.SIGNATURES) == declared_functions()
+
+
+def test_library_is_sm100a():
+    out = subprocess.check_output(["cuobjdump", "--list-elf", ds.lib_path()], text=True)
+    assert "sm_100a" in out
+
+
+def test_strerror_and_no_error_yet():
+    for code in (0, -1, -2, -3, -4, -5, 7):
+        assert isinstance(ds.ds_strerror(code), str) and ds.ds_strerror(code)
+
+
+def test_default_spec_is_spec_taps():
+    s = ds.ds_default_spec()
+    h, v = ds.stage_to_dict(s.h), ds.stage_to_dict(s.v)
+    # compared with the literal values printed in SPEC
+    assert h == dict(pattern=8, paving=8, origin=0, divisor=6, bias=3,
+                     weights=[[1, 5, 0, 0, 0, 0, 0, 0], [0, 0, 0, 3, 3, 0, 0, 0],
+                              [0, 0, 0, 0, 0, 0, 5, 1]])
+    assert v == dict(pattern=9, paving=9, origin=0, divisor=8, bias=4,
+                     weights=[[3, 5, 0, 0, 0, 0, 0, 0, 0], [0, 0, 1, 7, 0, 0, 0, 0, 0],
+                              [0, 0, 0, 0, 0, 7, 1, 0, 0], [0, 0, 0, 0, 0, 0, 0, 5, 3]])
+    assert s.chroma == ds.DS_CHROMA_420
+
+
+@pytest.mark.parametrize("W,H,ch,chroma,fin,fout", [
+    (1920, 1080, 3, 1, 3110400, 518400),
+    (1920, 1080, 3, 0, 6220800, 1036800),
+    (3840, 2160, 3, 1, 12441600, 2073600),
+    (352, 288, 3, 1, 152064, 25344),
+    (48, 27, 1, 1, 1296, 216),
+])
+def test_plan_geometry(W, H, ch, chroma, fin, fout):
+    spec = ds.ds_default_spec()
+    spec.chroma = chroma
+    p = ds.ds_plan(W, H, ch, spec)
+    assert (p.in_frame_bytes, p.out_frame_bytes) == (fin, fout)
+    for q in range(ch):
+        assert p.out_w[q] == 3 * p.in_w[q] // 8 and p.out_h[q] == 4 * p.in_h[q] // 9
+
+
+def test_plan_cif_matches_paper():
+    p = ds.ds_plan(352, 288, 3)
+    assert (p.out_w[0], p.out_h[0]) == (132, 128)
+    assert (p.out_w[1], p.out_h[1]) == (66, 64)
+    assert p.fused_eligible == 1
+
+
+def test_plan_hd_bands_equal_bytes():
+    p = ds.ds_plan(1920, 1080, 3)
+    assert p.fused_eligible == 1
+    assert list(p.band_groups) == [1, 2, 2]                # 15,360 B each
+    assert p.units_per_frame == 120 + 30 + 30
+    assert p.unit_in_bytes_max == 8 * 1920
+    assert p.unit_out_bytes_max == 4 * 720
+
+
+def test_plan_tiny_is_fused_eligible_but_unaligned_out():
+    p = ds.ds_plan(48, 27, 1)
+    assert p.fused_eligible == 1 and p.out_frame_bytes == 216
+
+
+@pytest.mark.parametrize("W,H,ch", [(50, 27, 1), (48, 28, 1), (352, 289, 3), (1920, 1081, 3),
+                                    (0, 27, 1), (48, -9, 1), (360, 288, 3)])
+def test_plan_rejects_non_divisible(W, H, ch):
+    # S:551 non-divisible shape -> error; 4:2:0 needs W % 16 == 0, H % 18 == 0
+    with pytest.raises(ds.DSError) as e:
+        ds.ds_plan(W, H, ch)
+    assert e.value.code == ds.DS_ESHAPE
+
+
+def test_plan_rejects_bad_channels_and_specs():
+    with pytest.raises(ds.DSError) as e:
+        ds.ds_plan(48, 27, 2)
+    assert e.value.code == ds.DS_EUNSUPPORTED
+    for bad in (dict(pattern=17), dict(divisor=0), dict(outputs=9)):
+        s = ds.ds_default_spec()
+        for k, v in bad.items():
+            setattr(s.h, k, v)
+        with pytest.raises(ds.DSError) as e:
+            ds.ds_plan(48, 27, 1, s)
+        assert e.value.code == ds.DS_EUNSUPPORTED
+    s = ds.ds_default_spec()
+    s.h.weight[0][12] = 1          # tap beyond the pattern
+    with pytest.raises(ds.DSError):
+        ds.ds_plan(48, 27, 1, s)
+
+
+def test_plan_generic_spec_not_fused():
+    h = dict(pattern=13, paving=8, origin=2, weights=[[1, 2, 3], [0, 0, 0, 4, 4], [1] * 13],
+             divisor=8, bias=4)
+    p = ds.ds_plan(48, 27, 1, ds.make_spec(h=h))
+    assert p.fused_eligible == 0 and p.out_w[0] == 18
+
+
+def test_create_validates_before_touching_cuda():
+    with pytest.raises(ds.DSError) as e:
+        ds.ds_create(50, 27, 1)
+    assert e.value.code == ds.DS_ESHAPE
+    assert ds.ds_last_error() == ds.DS_ESHAPE
+
+
+def test_null_handle_calls():
+    L = ds.lib()
+    assert L.ds_run(None, None, 0, None, None) == ds.DS_EINVAL
+    assert L.ds_in_frame_bytes(None) == -1
+    assert L.ds_set_kernel(None, 0) == ds.DS_EINVAL
+    L.ds_destroy(None)                                    # NULL-safe
+    assert L.ds_generate(None, 0, 1, 0, None) == ds.DS_OK   # n = 0 no-op
+    assert L.ds_generate(None, 16, 1, 0, None) == ds.DS_EINVAL

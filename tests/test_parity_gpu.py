@@ -1,0 +1,349 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle,
+byte for byte.  SPEC fixes integer pixel arithmetic,
+so the tolerance is zero.  P:n = PAPER.md line n, S:n = SPEC.md line n."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+torch = pytest.importorskip("torch")
+ds = pytest.importorskip("paper_1103_4881_b200")
+
+pytestmark = pytest.mark.gpu
+
+FUSED, GENERIC = ds.DS_KERNEL_FUSED, ds.DS_KERNEL_GENERIC
+
+
+def _run(d, frames_np, kernel=None):
+    if kernel is not None:
+        d.set_kernel(kernel)
+    x = torch.from_numpy(np.ascontiguousarray(frames_np)).cuda()
+    y = d(x)
+    torch.cuda.synchronize()
+    return y.cpu().numpy()
+
+
+def _assert_same(got, want, what=""):
+    if not np.array_equal(got, want):
+        idx = np.argwhere(got != want)
+        raise AssertionError(f"{what}: {len(idx)} bytes differ; first at {idx[:5].tolist()} "
+                             f"got {got[tuple(idx[0])]} want {want[tuple(idx[0])]}")
+
+
+def _spec_chroma(chroma):
+    s = ds.ds_default_spec()
+    s.chroma = chroma
+    return s
+
+
+# ------------------------------------------------------------- config 0 --
+@pytest.mark.parametrize("kernel", [FUSED, GENERIC])
+def test_tiny_48x27(kernel):
+    """BASELINE configs[0]: a tiny 48x27 1-channel frame (output frame of
+    216 B is not 16-byte aligned: K-N1 takes its cooperative-store path)."""
+    d = ds.Downscaler(48, 27, 1)
+    for seed in range(5):
+        fr = synth.random_frames(seed, 0, 3, 48, 27, 1)
+        got = _run(d, fr, kernel)
+        assert d.last_kernel() == kernel
+        _assert_same(got, oracle.execute_frames(fr, 48, 27, 1, 1), f"tiny seed {seed}")
+    # the golden of tests/golden/linear_48x27.json through the GPU
+    fr = synth.linear_frames(1, 48, 27, 1)
+    _assert_same(_run(d, fr, kernel), oracle.execute_frames(fr, 48, 27, 1, 1), "tiny linear")
+
+
+# ---------------------------------------------------------- paper testbed --
+@pytest.mark.parametrize("kernel", [FUSED, GENERIC])
+def test_cif_420_100_seeded_frames(kernel):
+    """100 random seeded CIF 4:2:0 frames bit-identical to the oracle."""
+    d = ds.Downscaler(352, 288, 3)
+    fr = synth.random_frames(0, 0, 100, 352, 288)
+    got = _run(d, fr, kernel)
+    assert d.last_kernel() == kernel
+    _assert_same(got, oracle.execute_frames(fr, 352, 288), "cif")
+    assert got.shape == (100, 132 * 128 + 2 * 66 * 64)
+
+
+@pytest.mark.parametrize("chroma", [ds.DS_CHROMA_420, ds.DS_CHROMA_444])
+def test_structured_frames_cif(chroma):
+    d = ds.Downscaler(352, 288, 3, chroma=chroma)
+    frames = [synth.constant_frames(c, 1, 352, 288, 3, chroma) for c in (0, 1, 100, 254, 255)]
+    frames += [synth.checkerboard_frames(2, 352, 288, 3, chroma),
+               synth.ramp_frames(4, 352, 288, 3, chroma),
+               synth.linear_frames(2, 352, 288, 3, chroma)]
+    fr = np.concatenate(frames)
+    _assert_same(_run(d, fr), oracle.execute_frames(fr, 352, 288, 3, chroma), "structured")
+    for c in (0, 1, 100, 254, 255):   # constants preserved
+        one = synth.constant_frames(c, 1, 352, 288, 3, chroma)
+        assert (_run(d, one) == c).all()
+
+
+def test_impulses_every_tile_position():
+    """An impulse at each of the 72 (row, col) positions of a 9x8 tile,
+    tiled across a frame with varying amplitudes (dead taps included)."""
+    W, H = 352, 288
+    d = ds.Downscaler(W, H, 1)
+    frames = []
+    for r in range(9):
+        for c in range(8):
+            y, x = np.mgrid[0:H, 0:W]
+            amp = ((x // 8 + 3 * (y // 9)) * 37) % 256
+            fr = np.where((y % 9 == r) & (x % 8 == c), amp, 0).astype(np.uint8)
+            frames.append(fr.reshape(1, -1))
+    fr = np.concatenate(frames)
+    _assert_same(_run(d, fr), oracle.execute_frames(fr, W, H, 1, 1), "impulses")
+
+
+# ------------------------------------------------------- exhaustive pairs --
+def test_exhaustive_h_pairs():
+    """All 65,536 (a, b) pairs in every horizontal tap pair (p0,p1), (p3,p4),
+    (p6,p7): row y carries a = y mod 256, packet p carries b = p."""
+    W, H = 8 * 256, 9 * 256
+    y, x = np.mgrid[0:H, 0:W]
+    pos = x % 8
+    a = y % 256
+    b = x // 8
+    plane = np.where(np.isin(pos, (0, 3, 6)), a, np.where(np.isin(pos, (1, 4, 7)), b, 77))
+    fr = plane.astype(np.uint8).reshape(1, -1)
+    d = ds.Downscaler(W, H, 1)
+    _assert_same(_run(d, fr), oracle.execute_frames(fr, W, H, 1, 1), "h pairs")
+
+
+def test_exhaustive_v_pairs():
+    """All 65,536 (m_a, m_b) pairs in every vertical tap pair: constant
+    packets make mid = the constant; rows 0,2,5,7 of group g hold g, rows
+    1,3,6,8 hold the packet index, row 4 (dead) holds noise."""
+    W, H = 8 * 256, 9 * 256
+    y, x = np.mgrid[0:H, 0:W]
+    g, r, p = y // 9, y % 9, x // 8
+    noise = synth.random_frames(3, 0, 1, W, H, 1)[0].reshape(H, W)
+    plane = np.where(np.isin(r, (0, 2, 5, 7)), g, np.where(np.isin(r, (1, 3, 6, 8)), p, noise))
+    fr = plane.astype(np.uint8).reshape(1, -1)
+    d = ds.Downscaler(W, H, 1)
+    _assert_same(_run(d, fr), oracle.execute_frames(fr, W, H, 1, 1), "v pairs")
+
+
+# -------------------------------------------------------------- HD / 4K --
+@pytest.mark.parametrize("chroma", [ds.DS_CHROMA_420, ds.DS_CHROMA_444])
+@pytest.mark.parametrize("kernel", [FUSED, GENERIC])
+def test_one_hd_frame(chroma, kernel):
+    """BASELINE configs[1]: one HD 1920x1080 frame."""
+    d = ds.Downscaler(1920, 1080, 3, chroma=chroma)
+    fr = np.concatenate([synth.random_frames(1, 0, 1, 1920, 1080, 3, chroma),
+                         synth.ramp_frames(1, 1920, 1080, 3, chroma)])
+    got = _run(d, fr, kernel)
+    assert d.last_kernel() == kernel
+    _assert_same(got, oracle.execute_frames(fr, 1920, 1080, 3, chroma), "hd")
+
+
+@pytest.mark.parametrize("chroma", [ds.DS_CHROMA_420, ds.DS_CHROMA_444])
+def test_4k_frames(chroma):
+    d = ds.Downscaler(3840, 2160, 3, chroma=chroma)
+    fr = synth.random_frames(5, 7, 2, 3840, 2160, 3, chroma)
+    _assert_same(_run(d, fr), oracle.execute_frames(fr, 3840, 2160, 3, chroma), "4k")
+
+
+# --------------------------------------------------------- ragged shapes --
+@pytest.mark.parametrize("W,H,ch", [(16, 9, 1), (32, 18, 3), (400, 9, 1), (48, 99, 1),
+                                    (40, 45, 1), (208, 90, 3), (1504, 54, 3), (2000, 27, 1),
+                                    (176, 144, 3), (8, 9, 1), (720, 576, 3)])
+def test_ragged_geometries(W, H, ch):
+    """Widths that are / are not multiples of 16 (K-N1 vs K-N2 auto choice),
+    band counts that leave a ragged tail over the persistent grid."""
+    d = ds.Downscaler(W, H, ch)
+    fr = synth.random_frames(W + H, 0, 7, W, H, ch, 1)
+    got = _run(d, fr)
+    want_kernel = FUSED if d.plan.fused_eligible else GENERIC
+    assert d.last_kernel() == want_kernel
+    _assert_same(got, oracle.execute_frames(fr, W, H, ch, 1), f"{W}x{H}x{ch}")
+
+
+def test_zero_frames_noop():
+    d = ds.Downscaler(352, 288, 3)
+    x = torch.empty((0, d.in_frame_bytes), dtype=torch.uint8, device="cuda")
+    y = d(x)
+    assert y.shape == (0, d.out_frame_bytes)
+
+
+# ----------------------------------------------------- general specs (K-N2) --
+def _halo_spec():
+    h = dict(pattern=13, paving=8, origin=3,
+             weights=[[1, 2, 3, 0, 0, 0, 0, 0, 0, 0, 0, 1, 1], [0, 0, 0, 2, 2, 2, 0, 0, 0, 0, 0, 0, 2],
+                      [0, 0, 0, 0, 0, 0, 4, 4, 1, 1, 0, 0, 0]], divisor=8, bias=4)
+    v = dict(pattern=14, paving=9, origin=-5,
+             weights=[[2, 2, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 4], [0, 0, 4, 4],
+                      [0, 0, 0, 0, 0, 3, 3, 0, 0, 0, 0, 2], [0, 0, 0, 0, 0, 0, 0, 5, 3]],
+             divisor=8, bias=4)
+    return h, v
+
+
+def _oracle_stage(d):
+    return oracle.make_stage(d["pattern"], d["paving"], d["origin"], d["weights"], d["divisor"],
+                             d["bias"])
+
+
+@pytest.mark.parametrize("W,H,ch", [(48, 27, 1), (352, 288, 3), (64, 36, 3)])
+def test_halo_and_origin_spec(W, H, ch):
+    """P > S halos with toroidal wrap and origin != 0."""
+    hd, vd = _halo_spec()
+    spec = ds.make_spec(h=hd, v=vd, chroma=ds.DS_CHROMA_420)
+    d = ds.Downscaler(W, H, ch, spec=spec)
+    fr = synth.random_frames(9, 0, 3, W, H, ch, 1)
+    got = _run(d, fr)
+    assert d.last_kernel() == GENERIC
+    want = oracle.execute_frames(fr, W, H, ch, 1, _oracle_stage(hd), _oracle_stage(vd))
+    _assert_same(got, want, "halo")
+
+
+def test_negative_weights_and_other_ratio():
+    """Negative lobes (truncation toward zero, clamp) and a 4->2 / 3->1 ratio."""
+    hd = dict(pattern=6, paving=4, origin=-1, weights=[[-1, 3, 3, -1], [0, 0, -1, 3, 3, -1]],
+              divisor=4, bias=2)
+    vd = dict(pattern=3, paving=3, origin=0, weights=[[1, 2, 1]], divisor=4, bias=-2)
+    spec = ds.make_spec(h=hd, v=vd)
+    d = ds.Downscaler(64, 30, 1, spec=spec)
+    fr = synth.random_frames(4, 0, 4, 64, 30, 1)
+    want = oracle.execute_frames(fr, 64, 30, 1, 1, _oracle_stage(hd), _oracle_stage(vd))
+    _assert_same(_run(d, fr), want, "negative")
+
+
+# ------------------------------------------------------- alignment / API --
+def test_misaligned_pointers():
+    """Misaligned input selects K-N2; misaligned output makes K-N1 fall back
+    to cooperative stores -- results identical, never an error."""
+    W, H = 352, 288
+    d = ds.Downscaler(W, H, 3)
+    fr = synth.random_frames(2, 0, 3, W, H)
+    want = oracle.execute_frames(fr, W, H)
+    buf = torch.zeros(fr.size + 64, dtype=torch.uint8, device="cuda")
+    x = buf[1: 1 + fr.size]
+    x.copy_(torch.from_numpy(fr.ravel()).cuda())
+    obuf = torch.zeros(want.size + 64, dtype=torch.uint8, device="cuda")
+    y = obuf[3: 3 + want.size]
+    ds.ds_run(d.handle, x.data_ptr(), 3, y.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert d.last_kernel() == GENERIC
+    _assert_same(y.cpu().numpy().reshape(want.shape), want, "misaligned in")
+    x2 = torch.from_numpy(fr).cuda()
+    ds.ds_run(d.handle, x2.data_ptr(), 3, y.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert d.last_kernel() == FUSED
+    _assert_same(y.cpu().numpy().reshape(want.shape), want, "misaligned out")
+
+
+def test_run_errors():
+    d = ds.Downscaler(352, 288, 3)
+    x = torch.zeros((2, d.in_frame_bytes), dtype=torch.uint8, device="cuda")
+    L = ds.lib()
+    s = torch.cuda.current_stream().cuda_stream
+    assert L.ds_run(d.handle, x.data_ptr(), -1, x.data_ptr(), s) == ds.DS_EINVAL
+    # overlapping in/out
+    assert L.ds_run(d.handle, x.data_ptr(), 1, x.data_ptr() + 100, s) == ds.DS_EINVAL
+    # host pointer is not a device pointer
+    hx = torch.zeros((2, d.in_frame_bytes), dtype=torch.uint8)
+    y = d.alloc_out(2)
+    assert L.ds_run(d.handle, hx.data_ptr(), 2, y.data_ptr(), s) == ds.DS_EINVAL
+    assert L.ds_run(d.handle, 0, 2, y.data_ptr(), s) == ds.DS_EINVAL
+    assert L.ds_run(d.handle, x.data_ptr(), 0, y.data_ptr(), s) == ds.DS_OK
+
+
+def test_tuning_does_not_change_results():
+    W, H = 1920, 1080
+    d = ds.Downscaler(W, H, 3)
+    fr = synth.random_frames(11, 0, 6, W, H)
+    x = torch.from_numpy(fr).cuda()
+    ref = d(x).cpu().numpy()
+    _assert_same(ref, oracle.execute_frames(fr, W, H), "tuning ref")
+    for stages in (2, 3, 5, 8):
+        for ctas in (0, 1, 2):
+            d.set_tuning(stages, ctas)
+            y = d(x)
+            torch.cuda.synchronize()
+            _assert_same(y.cpu().numpy(), ref, f"stages={stages} ctas={ctas}")
+
+
+def test_two_streams_one_handle():
+    W, H = 352, 288
+    d = ds.Downscaler(W, H, 3)
+    fr = synth.random_frames(6, 0, 40, W, H)
+    x = torch.from_numpy(fr).cuda()
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    y1, y2 = d.alloc_out(40), d.alloc_out(40)
+    torch.cuda.synchronize()
+    with torch.cuda.stream(s1):
+        d(x, y1)
+    with torch.cuda.stream(s2):
+        d(x, y2)
+    torch.cuda.synchronize()
+    want = oracle.execute_frames(fr, W, H)
+    _assert_same(y1.cpu().numpy(), want, "s1")
+    _assert_same(y2.cpu().numpy(), want, "s2")
+
+
+def test_device_generator_matches_host_generator():
+    fb = synth.in_frame_bytes(1920, 1080)
+    g = ds.generate_frames(3, fb, seed=1, first_frame=5)
+    torch.cuda.synchronize()
+    _assert_same(g.cpu().numpy(), synth.random_frames(1, 5, 3, 1920, 1080), "generator")
+    # unaligned / ragged tail
+    buf = torch.zeros(1000, dtype=torch.uint8, device="cuda")
+    ds.ds_generate(buf.data_ptr() + 3, 997, 9, 12345, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    _assert_same(buf.cpu().numpy()[3:], synth.random_bytes(9, 12345, 997), "gen tail")
+
+
+# ------------------------------------------------------------- host path --
+def test_run_host_pinned_and_pageable():
+    W, H = 352, 288
+    d = ds.Downscaler(W, H, 3)
+    n = 50
+    fr = synth.random_frames(8, 0, n, W, H)
+    want = oracle.execute_frames(fr, W, H)
+    for pinned in (True, False):
+        hin = torch.from_numpy(fr)
+        if pinned:
+            hin = hin.pin_memory()
+        d.set_host_chunk(7)                      # several chunks, ragged last one
+        hout = d.run_host(hin)
+        torch.cuda.current_stream().synchronize()
+        _assert_same(hout.numpy(), want, f"host pinned={pinned}")
+
+
+def test_run_host_hd_auto_chunk():
+    W, H = 1920, 1080
+    d = ds.Downscaler(W, H, 3)
+    n = 24
+    fr = synth.random_frames(12, 0, n, W, H)
+    hin = torch.from_numpy(fr).pin_memory()
+    hout = d.run_host(hin)
+    torch.cuda.current_stream().synchronize()
+    idx = [0, 9, 10, 23]
+    _assert_same(hout.numpy()[idx], oracle.execute_frames(fr[idx], W, H), "host hd")
+
+
+# ------------------------------------------------- full-size, bench config --
+def test_hd_300_frame_stream_bench_config():
+    """BASELINE configs[2] at full size, in bench.py's launch configuration
+    (device-generated frames, default tuning): whole-frame oracle checks on
+    sampled frames, O3 per-pixel checks on many more, and frame-independence
+    (no cross-frame contamination) via the last frame."""
+    W, H, N = 1920, 1080, 300
+    d = ds.Downscaler(W, H, 3)
+    x = ds.generate_frames(N, d.in_frame_bytes, seed=1)
+    y = d(x)
+    torch.cuda.synchronize()
+    assert d.last_kernel() == FUSED
+    for f in (0, 1, 149, 298, 299):
+        fr = synth.random_frames(1, f, 1, W, H)
+        _assert_same(y[f].cpu().numpy()[None], oracle.execute_frames(fr, W, H), f"frame {f}")
+    rng = np.random.default_rng(0)
+    for f in rng.choice(N, 20, replace=False):
+        fr = synth.random_frames(1, int(f), 1, W, H)[0]
+        out = y[int(f)].cpu().numpy()
+        ins = oracle.split_planes(fr, W, H)
+        outs = oracle.split_planes(out, W, H, out=True)
+        for pin, pout in zip(ins, outs):
+            ho, wo = pout.shape
+            for R, Cc in zip(rng.integers(0, ho, 200), rng.integers(0, wo, 200)):
+                assert pout[R, Cc] == oracle.pixel(pin, int(R), int(Cc))
