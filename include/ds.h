@@ -175,6 +175,9 @@ DS_API int ds_last_error(void);
 /* Static description of an error code; never NULL. */
 DS_API const char* ds_strerror(int code);
 
+/* The handle's current plan (band sizes follow ds_set_band_bytes). */
+DS_API int ds_get_plan(const ds_handle* h, ds_plan_info* out);
+
 /* Geometry queries; -1 / DS_EINVAL on a NULL handle. */
 DS_API int64_t ds_in_frame_bytes(const ds_handle* h);
 DS_API int64_t ds_out_frame_bytes(const ds_handle* h);
@@ -190,8 +193,17 @@ DS_API int ds_set_kernel(ds_handle* h, int32_t kernel);
 DS_API int ds_last_kernel(const ds_handle* h);
 
 /* K-N1 tuning: ring stages per CTA (2..8) and CTAs per SM (0 = maximum
- * occupancy).  Returns DS_EINVAL when out of range. */
+ * occupancy).  Defaults: one CTA per SM and a ring of ~120 KB (the TMA
+ * read optimum measured by tools/bw_probe).  Returns DS_EINVAL when out of
+ * range.  Not synchronised with ds_run calls in flight on other threads. */
 DS_API int ds_set_tuning(ds_handle* h, int32_t stages, int32_t ctas_per_sm);
+
+/* K-N1 work-unit (band) size: the largest number of 9-row groups whose
+ * staged bytes stay <= target_bytes for plane 0, other planes matched to
+ * it (0 = default, 32 KiB).  Resets ds_set_tuning to the defaults for the
+ * new unit size.  Output is unaffected.  Not synchronised with ds_run calls
+ * in flight on other threads. */
+DS_API int ds_set_band_bytes(ds_handle* h, int64_t target_bytes);
 
 /* K-N1 launch shape that ds_run would use for n_frames:
  * grid CTAs, threads per CTA, dynamic shared memory bytes. */

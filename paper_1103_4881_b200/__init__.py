@@ -85,10 +85,12 @@ SIGNATURES = [
     ("ds_strerror", C.c_char_p, [C.c_int]),
     ("ds_in_frame_bytes", C.c_int64, [C.c_void_p]),
     ("ds_out_frame_bytes", C.c_int64, [C.c_void_p]),
+    ("ds_get_plan", C.c_int, [C.c_void_p, C.POINTER(ds_plan_info)]),
     ("ds_plane_dims", C.c_int, [C.c_void_p, C.c_int, _PI32, _PI32, _PI32, _PI32]),
     ("ds_set_kernel", C.c_int, [C.c_void_p, C.c_int32]),
     ("ds_last_kernel", C.c_int, [C.c_void_p]),
     ("ds_set_tuning", C.c_int, [C.c_void_p, C.c_int32, C.c_int32]),
+    ("ds_set_band_bytes", C.c_int, [C.c_void_p, C.c_int64]),
     ("ds_launch_shape", C.c_int, [C.c_void_p, C.c_int64, _PI32, _PI32, _PI32]),
     ("ds_generate", C.c_int, [C.c_void_p, C.c_int64, C.c_uint64, C.c_int64, C.c_void_p]),
 ]
@@ -233,7 +235,7 @@ class Downscaler:
         self._h = ds_create(w, h, channels, spec)
         self.in_frame_bytes = lib().ds_in_frame_bytes(self._h)
         self.out_frame_bytes = lib().ds_out_frame_bytes(self._h)
-        self.plan = ds_plan(w, h, channels, spec)
+        self.plan = self.get_plan()
         if kernel != DS_KERNEL_AUTO:
             self.set_kernel(kernel)
 
@@ -272,6 +274,19 @@ class Downscaler:
         rc = lib().ds_set_tuning(self._h, stages, ctas_per_sm)
         if rc:
             raise DSError(rc, "ds_set_tuning")
+
+    def set_band_bytes(self, target: int) -> None:
+        rc = lib().ds_set_band_bytes(self._h, target)
+        if rc:
+            raise DSError(rc, "ds_set_band_bytes")
+        self.plan = self.get_plan()
+
+    def get_plan(self):
+        info = ds_plan_info()
+        rc = lib().ds_get_plan(self._h, C.byref(info))
+        if rc:
+            raise DSError(rc, "ds_get_plan")
+        return info
 
     def set_host_chunk(self, frames: int) -> None:
         rc = lib().ds_set_host_chunk(self._h, frames)

@@ -17,7 +17,9 @@ namespace {
 thread_local int g_last_error = DS_OK;
 
 constexpr int kHostSlots = 3;                       // ds_run_host pipeline depth
-constexpr int64_t kUnitTargetBytes = 24 * 1024;     // K-N1 band size target
+constexpr int64_t kUnitTargetBytes = 32 * 1024;     // K-N1 band size target (bytes staged)
+constexpr int64_t kInFlightTarget = 120 * 1024;     // K-N1 bytes in flight per SM (measured
+                                                    // optimum of tools/bw_probe tma_read)
 constexpr int kSmemLimit = 227 * 1024;              // per-CTA opt-in maximum
 constexpr int64_t kHostChunkBytes = 32LL << 20;     // ds_run_host chunk target
 
@@ -41,7 +43,8 @@ struct ds_handle {
     // K-N1 launch configuration
     int ncw = 4;                 // consumer warps per CTA
     int stages = 4;              // ring depth
-    int ctas_per_sm = 0;         // 0 = occupancy maximum
+    int ctas_per_sm = 1;         // 0 = occupancy maximum
+    int64_t band_target = kUnitTargetBytes;
     int32_t stage_stride = 0, out_stride = 0;
     int kernel_pref = DS_KERNEL_AUTO;
     std::atomic<int> last_kernel{DS_KERNEL_AUTO};
@@ -121,7 +124,8 @@ int64_t fused_smem_bytes(int stages, int32_t stage_stride, int32_t out_stride) {
 }
 
 int make_plan(int32_t W, int32_t H, int32_t channels, const ds_filter_spec* spec_in,
-              ds_filter_spec* spec_out, ds_plan_info* info) {
+              ds_filter_spec* spec_out, ds_plan_info* info,
+              int64_t unit_target = kUnitTargetBytes) {
     ds_filter_spec spec;
     if (spec_in) spec = *spec_in; else default_spec(&spec);
     if (W < 1 || H < 1) return DS_ESHAPE;
@@ -163,7 +167,7 @@ int make_plan(int32_t W, int32_t H, int32_t channels, const ds_filter_spec* spec
     for (int p = 0; p < channels && fused; ++p) fused = (pi.in_w[p] % 16 == 0);
     if (fused) {
         const int G0 = pi.in_h[0] / 9;
-        const int k0 = largest_divisor_below(G0, 8LL * pi.in_w[0], kUnitTargetBytes);
+        const int k0 = largest_divisor_below(G0, 8LL * pi.in_w[0], unit_target);
         const int64_t target = 8LL * k0 * pi.in_w[0];
         int64_t units = 0, umax = 0, omax = 0;
         for (int p = 0; p < channels; ++p) {
@@ -192,6 +196,24 @@ int make_plan(int32_t W, int32_t H, int32_t channels, const ds_filter_spec* spec
 }
 
 // ----------------------------------------------------------- K-N1 launch --
+// Launch shape from the plan: enough consumer warps for one task each (cap
+// 8), and a ring deep enough for ~kInFlightTarget bytes in flight per SM at
+// one CTA per SM (tools/bw_probe: 120 KB/SM is the TMA read optimum; more
+// in flight lowers DRAM efficiency).
+int max_tasks(const ds_plan_info& pi);
+void configure_fused(ds_handle* h) {
+    const ds_plan_info& pi = h->plan;
+    if (!pi.fused_eligible) return;
+    const int t = max_tasks(pi);
+    const int w = (t + 31) / 32;
+    h->ncw = w <= 1 ? 1 : w <= 2 ? 2 : w <= 4 ? 4 : 8;
+    h->stage_stride = (int32_t)round_up(pi.unit_in_bytes_max, 128);
+    h->out_stride = (int32_t)round_up(pi.unit_out_bytes_max, 128);
+    h->stages = (int)std::max<int64_t>(2, std::min<int64_t>(8, (kInFlightTarget + h->stage_stride / 2) /
+                                                                   h->stage_stride));
+    h->ctas_per_sm = 1;
+}
+
 using FusedFn = void (*)(const ds::FusedParams);
 
 FusedFn fused_fn(int ncw) {
@@ -205,7 +227,8 @@ FusedFn fused_fn(int ncw) {
 
 int max_tasks(const ds_plan_info& pi) {
     int t = 0;
-    for (int p = 0; p < pi.n_planes; ++p) t = std::max(t, pi.in_w[p] / 16 * pi.band_groups[p]);
+    for (int p = 0; p < pi.n_planes; ++p)
+        t = std::max(t, 2 * pi.band_groups[p] * (pi.in_w[p] / 16));
     return t;
 }
 
@@ -258,7 +281,8 @@ int launch_fused(ds_handle* h, const uint8_t* in, int64_t n, uint8_t* out, cudaS
         P.Wout = pi.out_w[q];
         P.k = pi.band_groups[q];
         P.chunks = P.W / 16;
-        P.tasks = P.chunks * P.k;
+        P.tasks = 2 * P.k * P.chunks;
+        P.chunks_rcp = P.chunks > 1 ? (uint32_t)((0x100000000ULL + P.chunks - 1) / P.chunks) : 0u;
         P.unit_start = start;
         P.unit_in = 8 * P.k * P.W;
         P.unit_out = 4 * P.k * P.Wout;
@@ -392,14 +416,7 @@ DS_API ds_handle* ds_create(int32_t frame_w, int32_t frame_h, int32_t channels,
     h->W = frame_w; h->H = frame_h; h->channels = channels;
     h->spec = spec;
     h->plan = pi;
-    if (pi.fused_eligible) {
-        const int t = max_tasks(pi);
-        const int w = (t + 31) / 32;
-        h->ncw = w <= 1 ? 1 : w <= 2 ? 2 : w <= 4 ? 4 : 8;
-        h->stage_stride = (int32_t)round_up(pi.unit_in_bytes_max, 128);
-        h->out_stride = (int32_t)round_up(pi.unit_out_bytes_max, 128);
-        h->stages = 4;
-    }
+    configure_fused(h);
     g_last_error = DS_OK;
     return h;
 }
@@ -521,6 +538,12 @@ DS_API const char* ds_strerror(int code) {
     }
 }
 
+DS_API int ds_get_plan(const ds_handle* h, ds_plan_info* out) {
+    if (!h || !out) return DS_EINVAL;
+    *out = h->plan;
+    return DS_OK;
+}
+
 DS_API int64_t ds_in_frame_bytes(const ds_handle* h) { return h ? h->plan.in_frame_bytes : -1; }
 DS_API int64_t ds_out_frame_bytes(const ds_handle* h) { return h ? h->plan.out_frame_bytes : -1; }
 
@@ -549,6 +572,18 @@ DS_API int ds_set_tuning(ds_handle* h, int32_t stages, int32_t ctas_per_sm) {
     if (!h || stages < 2 || stages > 8 || ctas_per_sm < 0 || ctas_per_sm > 32) return DS_EINVAL;
     h->stages = stages;
     h->ctas_per_sm = ctas_per_sm;
+    return DS_OK;
+}
+
+DS_API int ds_set_band_bytes(ds_handle* h, int64_t target) {
+    if (!h || target < 0) return DS_EINVAL;
+    if (target == 0) target = kUnitTargetBytes;
+    ds_plan_info pi;
+    const int rc = make_plan(h->W, h->H, h->channels, &h->spec, nullptr, &pi, target);
+    if (rc) return rc;
+    h->plan = pi;
+    h->band_target = target;
+    configure_fused(h);
     return DS_OK;
 }
 

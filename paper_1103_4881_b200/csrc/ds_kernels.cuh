@@ -29,12 +29,12 @@ struct FusedPlane {
     int32_t W, Wout;           // input / output row bytes
     int32_t k;                 // 9-row groups per unit (band)
     int32_t chunks;            // 16-byte column chunks per row = W / 16
-    int32_t tasks;             // chunks * k  (one task = 16 B x 8 rows)
+    int32_t tasks;             // 2 * k * chunks  (one task = 16 B x 4 slot rows)
     int32_t unit_start;        // first per-frame unit index of this plane
     int32_t unit_in;           // bytes staged per unit = 8 * k * W
     int32_t unit_out;          // bytes produced per unit = 4 * k * Wout
     int32_t bulk_store;        // 1: TMA bulk store legal (16 B aligned)
-    int32_t pad_;
+    uint32_t chunks_rcp;       // ceil(2^32 / chunks) (chunks > 1): t / chunks = umulhi(t, rcp)
 };
 
 struct FusedParams {
@@ -175,6 +175,40 @@ __device__ __forceinline__ uint32_t v_pair(uint32_t qa, uint32_t qb) {
 // Ring slot layout: for group g, rows 8g..8g+3 hold input rows 9g+0..3 and
 // rows 8g+4..8g+7 hold input rows 9g+5..8 (row 9g+4 has zero V weight,
 // S:540, and is never read from HBM).
+//
+// Consumer task = (half-group hg, 16-byte column chunk c): the 4 slot rows
+// 8(hg>>1) + 4(hg&1) .. +3, i.e. the two V outputs 4g+2(hg&1) and +1 of the
+// six columns 6c..6c+5.  Consecutive lanes take consecutive chunks (conflict
+// -free LDS.128).  No runtime integer division anywhere in the unit loop:
+// unit -> (frame, plane, band) and ring/phase counters advance
+// incrementally, task -> (hg, c) uses a precomputed reciprocal.
+
+// Per-CTA walk over its units u = blockIdx.x + i * gridDim.x.
+struct UnitCursor {
+    int64_t u, f;
+    int32_t local;
+    int32_t gdiv, gmod, upf;
+    __device__ __forceinline__ void init(const FusedParams& p) {
+        u = blockIdx.x;
+        upf = p.upf;
+        f = (int64_t)(blockIdx.x / (uint32_t)upf);
+        local = (int32_t)(blockIdx.x - (uint32_t)f * (uint32_t)upf);
+        gdiv = (int32_t)(gridDim.x / (uint32_t)upf);
+        gmod = (int32_t)(gridDim.x - (uint32_t)gdiv * (uint32_t)upf);
+    }
+    __device__ __forceinline__ void next() {
+        u += gridDim.x;
+        f += gdiv;
+        local += gmod;
+        if (local >= upf) { local -= upf; ++f; }
+    }
+    __device__ __forceinline__ int plane(const FusedParams& p) const {
+        return (p.n_planes > 2 && local >= p.pl[2].unit_start)   ? 2
+               : (p.n_planes > 1 && local >= p.pl[1].unit_start) ? 1
+                                                                 : 0;
+    }
+};
+
 template <int NCW>
 __global__ void __launch_bounds__((NCW + 1) * 32)
     ds_fused_band_kernel(const __grid_constant__ FusedParams p) {
@@ -197,78 +231,72 @@ __global__ void __launch_bounds__((NCW + 1) * 32)
     __syncthreads();
 
     const int warp = tid >> 5, lane = tid & 31;
+    UnitCursor cur;
+    cur.init(p);
+    int s = 0;
+    uint32_t phase = 0;
     if (warp == NCW) {
         // ---------------- producer: one lane streams bands into the ring --
         if (lane == 0) {
             const uint64_t pol = policy_evict_first();
-            int64_t i = 0;
-            for (int64_t u = blockIdx.x; u < p.n_units; u += gridDim.x, ++i) {
-                const int s = (int)(i % S);
-                const uint32_t use = (uint32_t)(i / S);
-                if (use > 0) mbar_wait(&empty[s], (use - 1) & 1);
-                const int64_t f = u / p.upf;
-                const int local = (int)(u - f * p.upf);
-                const int pi = (p.n_planes > 2 && local >= p.pl[2].unit_start)   ? 2
-                               : (p.n_planes > 1 && local >= p.pl[1].unit_start) ? 1
-                                                                                 : 0;
-                const FusedPlane& P = p.pl[pi];
-                const int band = local - P.unit_start;
+            bool first_round = true;
+            for (; cur.u < p.n_units; cur.next()) {
+                if (!first_round) mbar_wait(&empty[s], phase ^ 1);
+                const FusedPlane& P = p.pl[cur.plane(p)];
+                const int band = cur.local - P.unit_start;
                 const uint8_t* src =
-                    p.in + f * p.in_frame + P.in_off + (int64_t)band * 9 * P.k * P.W;
+                    p.in + cur.f * p.in_frame + P.in_off + (int64_t)band * 9 * P.k * P.W;
                 uint8_t* dst = ring + (size_t)s * p.stage_stride;
                 mbar_arrive_expect_tx(&full[s], (uint32_t)P.unit_in);
                 const uint32_t half = 4u * (uint32_t)P.W;
                 for (int g = 0; g < P.k; ++g) {
                     const uint8_t* sg = src + (int64_t)9 * g * P.W;
                     uint8_t* dg = dst + (size_t)8 * g * P.W;
-                    bulk_g2s(dg, sg, half, &full[s], pol);                       // rows 0..3
+                    bulk_g2s(dg, sg, half, &full[s], pol);                            // rows 0..3
                     bulk_g2s(dg + half, sg + (int64_t)5 * P.W, half, &full[s], pol);  // rows 5..8
                 }
+                if (++s == S) { s = 0; phase ^= 1; first_round = false; }
             }
         }
         return;
     }
 
     // ---------------- consumers ---------------------------------------------
-    int64_t i = 0;
-    for (int64_t u = blockIdx.x; u < p.n_units; u += gridDim.x, ++i) {
-        const int s = (int)(i % S);
-        const int64_t f = u / p.upf;
-        const int local = (int)(u - f * p.upf);
-        const int pi = (p.n_planes > 2 && local >= p.pl[2].unit_start)   ? 2
-                       : (p.n_planes > 1 && local >= p.pl[1].unit_start) ? 1
-                                                                         : 0;
-        const FusedPlane& P = p.pl[pi];
-        const int band = local - P.unit_start;
+    int oslot = 0;
+    for (; cur.u < p.n_units; cur.next()) {
+        const FusedPlane& P = p.pl[cur.plane(p)];
+        const int band = cur.local - P.unit_start;
         const uint8_t* st = ring + (size_t)s * p.stage_stride;
-        uint8_t* ob = outs + (size_t)(i % kOutSlots) * p.out_stride;
-        const int W = P.W, Wout = P.Wout;
+        uint8_t* ob = outs + (size_t)oslot * p.out_stride;
+        const int W = P.W, Wout = P.Wout, chunks = P.chunks, tasks = P.tasks;
+        const uint32_t rcp = P.chunks_rcp;
 
-        mbar_wait(&full[s], (uint32_t)(i / S) & 1);
+        mbar_wait(&full[s], phase);
 
-        for (int t = tid; t < P.tasks; t += NC) {
-            const int g = t / P.chunks;
-            const int c = t - g * P.chunks;
-            const uint8_t* base = st + (size_t)8 * g * W + 16 * c;
-            uint4 r[8];
+        for (int t = tid; t < tasks; t += NC) {
+            const int hg = chunks == 1 ? t : (int)__umulhi((uint32_t)t, rcp);   // t / chunks
+            const int c = t - hg * chunks;
+            const int half = hg & 1;
+            const uint8_t* base = st + (size_t)4 * hg * W + 16 * c;
+            uint4 r[4];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) r[j] = lds128(base + (size_t)j * W);
-            uint32_t q[8][3];
+            for (int j = 0; j < 4; ++j) r[j] = lds128(base + (size_t)j * W);
+            uint32_t q[4][3];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) h_chunk(r[j], q[j][0], q[j][1], q[j][2]);
-            // V taps: out0 rows (0,1) w (3,5); out1 rows (2,3) w (1,7);
-            // out2 rows (5,6) w (7,1); out3 rows (7,8) w (5,3); slots skip row 4.
-            uint32_t o[4][3];
+            for (int j = 0; j < 4; ++j) h_chunk(r[j], q[j][0], q[j][1], q[j][2]);
+            // V taps: half 0 -> out0 rows (0,1) w (3,5), out1 rows (2,3)
+            // w (1,7); half 1 -> out2 rows (5,6) w (7,1), out3 rows (7,8) w (5,3).
+            const uint32_t wa0 = half ? 32u * 7 : 32u * 3, wb0 = half ? 32u * 1 : 32u * 5;
+            const uint32_t wa1 = half ? 32u * 5 : 32u * 1, wb1 = half ? 32u * 3 : 32u * 7;
+            uint32_t o[2][3];
 #pragma unroll
             for (int e = 0; e < 3; ++e) {
-                o[0][e] = v_pair<3, 5>(q[0][e], q[1][e]);
-                o[1][e] = v_pair<1, 7>(q[2][e], q[3][e]);
-                o[2][e] = v_pair<7, 1>(q[4][e], q[5][e]);
-                o[3][e] = v_pair<5, 3>(q[6][e], q[7][e]);
+                o[0][e] = q[0][e] * wa0 + q[1][e] * wb0 + 0x00800080u;
+                o[1][e] = q[2][e] * wa1 + q[3][e] * wb1 + 0x00800080u;
             }
-            uint8_t* orow = ob + (size_t)4 * g * Wout + 6 * c;
+            uint8_t* orow = ob + (size_t)2 * hg * Wout + 6 * c;
 #pragma unroll
-            for (int kk = 0; kk < 4; ++kk) {
+            for (int kk = 0; kk < 2; ++kk) {
                 const uint32_t lo = __byte_perm(o[kk][0], o[kk][1], 0x7531);
                 const uint32_t hi = __byte_perm(o[kk][2], 0u, 0x4431);
                 uint8_t* d = orow + (size_t)kk * Wout;
@@ -281,19 +309,21 @@ __global__ void __launch_bounds__((NCW + 1) * 32)
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
 
-        uint8_t* dst = p.out + f * p.out_frame + P.out_off + (int64_t)band * P.unit_out;
+        uint8_t* dst = p.out + cur.f * p.out_frame + P.out_off + (int64_t)band * P.unit_out;
         if (P.bulk_store) {
             fence_proxy_async_smem();      // generic-proxy smem writes -> async proxy
             named_bar_sync(1, NC);
             if (tid == 0) {
                 bulk_s2g(dst, ob, (uint32_t)P.unit_out);
                 bulk_commit();
-                bulk_wait_read<1>();       // slot (i-1)%3 free before next barrier
+                bulk_wait_read<1>();       // slot (oslot-1)%3 free before next barrier
             }
         } else {
             named_bar_sync(1, NC);
             for (int x = tid; x < P.unit_out; x += NC) dst[x] = ob[x];
         }
+        if (++s == S) { s = 0; phase ^= 1; }
+        if (++oslot == kOutSlots) oslot = 0;
     }
     if (tid == 0) bulk_wait_all();
 }

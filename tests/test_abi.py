@@ -84,10 +84,11 @@ def test_plan_cif_matches_paper():
 def test_plan_hd_bands_equal_bytes():
     p = ds.ds_plan(1920, 1080, 3)
     assert p.fused_eligible == 1
-    assert list(p.band_groups) == [1, 2, 2]                # 15,360 B each
-    assert p.units_per_frame == 120 + 30 + 30
-    assert p.unit_in_bytes_max == 8 * 1920
-    assert p.unit_out_bytes_max == 4 * 720
+    # 32 KiB band target: luma 2 groups, chroma 4 groups -> 30,720 B staged each
+    assert list(p.band_groups) == [2, 4, 4]
+    assert p.units_per_frame == 60 + 15 + 15
+    assert p.unit_in_bytes_max == 8 * 2 * 1920
+    assert p.unit_out_bytes_max == 4 * 2 * 720
 
 
 def test_plan_tiny_is_fused_eligible_but_unaligned_out():

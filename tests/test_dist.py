@@ -1,0 +1,82 @@
+"""Multi-process path on the CPU (gloo, world_size 2 and 3): frame-block
+sharding and the gather to rank 0.  Frames are independent
+(S:576), so sharded output must equal the unsharded output.  The
+per-rank compute here is the CPU oracle (test infrastructure) standing in
+for ds_run; the sharding and gather code is the product's
+(paper_1103_4881_b200/dist.py)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_1103_4881_b200.dist import gather_frames, shard_range
+
+
+def test_shard_ranges_partition_the_stream():
+    for total in (0, 1, 7, 300, 3000, 1000):
+        for world in (1, 2, 3, 4, 8):
+            blocks = [shard_range(total, world, r) for r in range(world)]
+            assert blocks[0][0] == 0 and blocks[-1][1] == total
+            for (a, b), (c, d) in zip(blocks, blocks[1:]):
+                assert b == c and a <= b
+            sizes = [b - a for a, b in blocks]
+            assert max(sizes) - min(sizes) <= 1
+    # 3000 frames over 8 GPUs -> 375 each; 1000 -> 125
+    assert shard_range(3000, 8, 3) == (1125, 1500)
+    assert shard_range(1000, 8, 7) == (875, 1000)
+    with pytest.raises(ValueError):
+        shard_range(10, 0, 0)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, total, W, H, q):
+    import oracle
+    import synth
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        lo, hi = shard_range(total, world, rank)
+        frames = synth.random_frames(5, lo, hi - lo, W, H)          # by GLOBAL frame index
+        fin, fout = oracle.frame_bytes(W, H)
+        local = oracle.execute_frames(frames, W, H) if hi > lo else np.zeros((0, fout), np.uint8)
+        full = gather_frames(torch.from_numpy(local.copy()), total)
+        if rank == 0:
+            q.put(full.numpy())
+        else:
+            assert full is None
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,total", [(2, 7), (3, 5), (2, 1)])
+def test_gloo_sharded_equals_unsharded(world, total):
+    import oracle
+    import synth
+
+    W, H = 48, 36
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, total, W, H, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    got = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    want = oracle.execute_frames(synth.random_frames(5, 0, total, W, H), W, H)
+    assert got.shape == want.shape
+    assert np.array_equal(got, want)

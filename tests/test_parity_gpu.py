@@ -255,12 +255,15 @@ def test_tuning_does_not_change_results():
     x = torch.from_numpy(fr).cuda()
     ref = d(x).cpu().numpy()
     _assert_same(ref, oracle.execute_frames(fr, W, H), "tuning ref")
-    for stages in (2, 3, 5, 8):
-        for ctas in (0, 1, 2):
-            d.set_tuning(stages, ctas)
-            y = d(x)
-            torch.cuda.synchronize()
-            _assert_same(y.cpu().numpy(), ref, f"stages={stages} ctas={ctas}")
+    for band in (0, 8 * 1920, 64 * 1024, 1):
+        d.set_band_bytes(band)
+        for stages in (2, 3, 5, 8):
+            for ctas in (0, 1, 2):
+                d.set_tuning(stages, ctas)
+                y = d(x)
+                torch.cuda.synchronize()
+                assert d.last_kernel() == FUSED
+                _assert_same(y.cpu().numpy(), ref, f"band={band} stages={stages} ctas={ctas}")
 
 
 def test_two_streams_one_handle():
