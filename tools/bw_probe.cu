@@ -93,6 +93,47 @@ __global__ void k_tma_read(const uint8_t* in, size_t n_chunks, uint32_t chunk, i
     }
 }
 
+// TMA ring that also writes: after each chunk lands, bulk-store `wbytes`
+// of it to `out` (the downscaler's 5.33:1 read:write mix with wbytes = chunk*3/16)
+__global__ void k_tma_rw(const uint8_t* in, uint8_t* out, size_t n_chunks, uint32_t chunk,
+                         uint32_t wbytes, int stages) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)stages * chunk);
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < stages; ++s)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&full[s])));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    size_t my = 0;
+    for (size_t c = blockIdx.x; c < n_chunks; c += gridDim.x) ++my;
+    size_t issued = 0, c_issue = blockIdx.x, c_done = blockIdx.x;
+    for (; issued < my && issued < (size_t)stages; ++issued, c_issue += gridDim.x) {
+        int s = issued % stages;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&full[s])), "r"(chunk) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                     ::"r"(su32(smem + (size_t)s * chunk)), "l"(in + c_issue * chunk), "r"(chunk), "r"(su32(&full[s])) : "memory");
+    }
+    for (size_t i = 0; i < my; ++i, c_done += gridDim.x) {
+        int s = i % stages;
+        uint32_t ph = (i / stages) & 1;
+        asm volatile("{\n .reg .pred p;\nW_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra W_%=;\n}"
+                     ::"r"(su32(&full[s])), "r"(ph) : "memory");
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(out + c_done * wbytes),
+                     "r"(su32(smem + (size_t)s * chunk)), "r"(wbytes) : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        if (issued < my) {
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&full[s])), "r"(chunk) : "memory");
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                         ::"r"(su32(smem + (size_t)s * chunk)), "l"(in + c_issue * chunk), "r"(chunk), "r"(su32(&full[s])) : "memory");
+            ++issued; c_issue += gridDim.x;
+        }
+    }
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 template <class F>
 float best_ms(F f, int reps = 10) {
     cudaEvent_t a, b; CK(cudaEventCreate(&a)); CK(cudaEventCreate(&b));
@@ -132,6 +173,16 @@ int main() {
         float t = best_ms([&] { k_tma_read<<<grid, 32, smem>>>(in, nch, chunk, stages); });
         printf("tma_read chunk=%5u stages=%d ctas/sm=%d : %7.1f GB/s (%.0f KB in flight/SM)\n", chunk, stages, cps,
                nch * (double)chunk / t / 1e6, stages * cps * chunk / 1024.0);
+    }
+    for (uint32_t chunk : {15360u, 30720u}) for (int stages : {3, 4, 5}) {
+        size_t smem = (size_t)stages * chunk + 64;
+        CK(cudaFuncSetAttribute(k_tma_rw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        size_t nch = bytes / chunk;
+        uint32_t wb = chunk * 3 / 16;          // 30720 -> 5760 (the HD unit's output band)
+        int grid = sms;
+        float t = best_ms([&] { k_tma_rw<<<grid, 32, smem>>>(in, out, nch, chunk, wb, stages); });
+        printf("tma_rw   chunk=%5u out=%5u stages=%d ctas/sm=1 : %7.1f GB/s (read+write)\n", chunk, wb, stages,
+               nch * (double)(chunk + wb) / t / 1e6);
     }
     return 0;
 }
