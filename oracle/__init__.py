@@ -85,6 +85,7 @@ def lib():
         L.orc_default_stages.argtypes = [PS, PS]
         L.orc_default_stages.restype = None
         L.orc_execute_plane.argtypes = [P8, C.c_int32, C.c_int32, PS, PS, P8, C.c_int32]
+        L.orc_execute_plane_mid.argtypes = [P8, C.c_int32, C.c_int32, PS, PS, P8, P8, C.c_int32]
         L.orc_plane_dims.argtypes = [C.c_int32] * 5 + [C.POINTER(C.c_int32)] * 2
         L.orc_execute_frames.argtypes = [P8, C.c_int64, C.c_int32, C.c_int32, C.c_int32,
                                          C.c_int32, PS, PS, P8]
@@ -256,6 +257,46 @@ def execute_plane(plane: np.ndarray, h: Stage | None = None, v: Stage | None = N
     _check(lib().orc_execute_plane(_p8(a), W, Hh, C.byref(h), C.byref(v), _p8(out), order),
            "execute_plane")
     return out
+
+
+def execute_plane_mid(plane: np.ndarray, h: Stage | None = None, v: Stage | None = None):
+    """O1 on one plane, returning (Mid, Out): Mid is the H task's u8 output
+    array, the array the paper's unfused kernels keep in global memory."""
+    if h is None:
+        h, v = default_stages()
+    Hh, W = plane.shape
+    a = np.ascontiguousarray(plane, dtype=np.uint8)
+    if W % h.paving or Hh % v.paving:
+        raise OracleError(-2, "execute_plane_mid")
+    mid = np.zeros((Hh, h.outputs * (W // h.paving)), np.uint8)
+    out = np.zeros((v.outputs * (Hh // v.paving), h.outputs * (W // h.paving)), np.uint8)
+    _check(lib().orc_execute_plane_mid(_p8(a), W, Hh, C.byref(h), C.byref(v), _p8(mid), _p8(out),
+                                       0), "execute_plane_mid")
+    return mid, out
+
+
+def execute_frames_mid(frames: np.ndarray, W, H, channels=3, chroma=1,
+                       h: Stage | None = None, v: Stage | None = None):
+    """O1 over a stream returning (mids, outs); mids is (n, mid_frame_bytes)
+    with the planes' Mid arrays back to back (same layout rule as S:583)."""
+    if h is None:
+        h, v = default_stages()
+    fin, fout = frame_bytes(W, H, channels, chroma, h, v)
+    a = np.ascontiguousarray(frames, dtype=np.uint8).reshape(-1, fin)
+    dims = plane_dims(W, H, channels, chroma)
+    fmid = sum(ph * h.outputs * (pw // h.paving) for pw, ph in dims)
+    mids = np.zeros((a.shape[0], fmid), np.uint8)
+    outs = np.zeros((a.shape[0], fout), np.uint8)
+    for f in range(a.shape[0]):
+        ip = split_planes(a[f], W, H, channels, chroma)
+        mo = oo = 0
+        for (pw, ph), pl in zip(dims, ip):
+            m, o = execute_plane_mid(pl, h, v)
+            mids[f, mo: mo + m.size] = m.ravel()
+            outs[f, oo: oo + o.size] = o.ravel()
+            mo += m.size
+            oo += o.size
+    return mids, outs
 
 
 def execute_frames(frames: np.ndarray, W, H, channels=3, chroma=1,

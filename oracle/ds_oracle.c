@@ -257,6 +257,14 @@ static void run_task(const uint8_t* in, const orc_tiler* tin,
 int orc_execute_plane(const uint8_t* in, int32_t W, int32_t H,
                       const orc_stage* h, const orc_stage* v,
                       uint8_t* out, int32_t order) {
+    return orc_execute_plane_mid(in, W, H, h, v, NULL, out, order);
+}
+
+/* Same as orc_execute_plane; if mid_out is not NULL the intermediate array
+ * Mid (H x Qh*W/Sh, the H task's output array) is copied there. */
+int orc_execute_plane_mid(const uint8_t* in, int32_t W, int32_t H,
+                          const orc_stage* h, const orc_stage* v,
+                          uint8_t* mid_out, uint8_t* out, int32_t order) {
     if (!in || !out || !stage_ok(h) || !stage_ok(v) || W < 1 || H < 1) return ORC_EINVAL;
     if (W % h->paving != 0 || H % v->paving != 0) return ORC_ESHAPE;   /* S:551 */
     int64_t Wm = (int64_t)h->outputs * (W / h->paving);
@@ -290,6 +298,7 @@ int orc_execute_plane(const uint8_t* in, int32_t W, int32_t H,
     int64_t vrep[2] = { H / v->paving, Wm };
     run_task(in, &hin, mid, &hout, hrep, h, order);    /* toposort: H before V */
     run_task(mid, &vin, out, &vout, vrep, v, order);
+    if (mid_out) memcpy(mid_out, mid, (size_t)(H * Wm));
     free(mid);
     return ORC_OK;
 }

@@ -494,3 +494,15 @@ def test_negative_weights_truncate_and_clamp():
     assert list(oracle.stage_apply(s, [0, 255])) == [127, 0]
     s2 = oracle.make_stage(1, 1, 0, [[4]], 1, 0)
     assert list(oracle.stage_apply(s2, [200])) == [255]
+
+
+def test_mid_array_is_the_h_task_output():
+    """The exposed intermediate equals SPEC's literal hfilter_8to3 on
+    every consecutive 8-pixel packet of every row (O2's first loop)."""
+    rng = np.random.default_rng(21)
+    plane = rng.integers(0, 256, (18, 64)).astype(np.uint8)
+    mid, out = oracle.execute_plane_mid(plane)
+    want = np.array([[v for p in range(8) for v in oracle.hfilter_8to3(row[8 * p: 8 * p + 8])]
+                     for row in plane], np.uint8)
+    assert (mid == want).all()
+    assert (out == oracle.execute_plane(plane)).all()
