@@ -210,6 +210,67 @@ DS_API int ds_set_band_bytes(ds_handle* h, int64_t target_bytes);
 DS_API int ds_launch_shape(const ds_handle* h, int64_t n_frames, int32_t* grid,
                            int32_t* block, int32_t* smem_bytes);
 
+/* ---- the paper's unfused structure and its transfer schedules
+ *
+ * Bytes of one frame's intermediate arrays Mid (the H task's u8 output,
+ * S:365): planes' (H_p x Qh*W_p/Sh) arrays back to back, the same layout
+ * rule as frames.  -1 on a NULL handle. */
+DS_API int64_t ds_mid_frame_bytes(const ds_handle* h);
+
+/* K-N3: one repetitive task per launch, as the paper's generated code does
+ * ("the six repetitive tasks ... allocated onto the GPU in order to
+ * generate kernels"), with Mid in HBM.  ds_run_htask: in -> mid (H task);
+ * ds_run_vtask: mid -> out (V task); over planes [plane_first,
+ * plane_first + plane_count) of n frames.  Pointers are frame-base device
+ * pointers (n * in/mid/out frame bytes), caller-owned, non-overlapping.
+ * SPEC taps with aligned geometry take vectorised kernels, anything else a
+ * literal tiler kernel.  Asynchronous on `stream`.  Returns as ds_run. */
+DS_API int ds_run_htask(ds_handle* h, const uint8_t* in_frames, int64_t n_frames, uint8_t* mid,
+                        int32_t plane_first, int32_t plane_count, ds_stream_t stream);
+DS_API int ds_run_vtask(ds_handle* h, const uint8_t* mid, int64_t n_frames, uint8_t* out_frames,
+                        int32_t plane_first, int32_t plane_count, ds_stream_t stream);
+
+/* Host <-> device transfer schedules of a host-resident stream. */
+enum {
+    DS_SCHED_NAIVE = 0,      /* H2D every task input, D2H every task
+                                output -> 12 transfers/frame ("not optimized") */
+    DS_SCHED_OPTIMIZED = 1,  /* residency-aware -> 3 H2D + 3 D2H per frame
+                                ("performance tuning")                   */
+    DS_SCHED_FUSED = 2,      /* per frame: 1 H2D, one fused K-N1 launch, 1 D2H      */
+    DS_SCHED_STREAMED = 3    /* ds_run_host: chunked, overlapped on 3 streams       */
+};
+
+typedef struct {
+    int64_t frames;
+    int64_t h2d_count, d2h_count;         /* transfers                                */
+    int64_t h2d_bytes, d2h_bytes;
+    int64_t launches;
+    double h2d_ms, d2h_ms, kernel_ms;     /* device time per phase: CUDA events around
+                                             every step, steps serialised on one stream
+                                             (STREAMED: 0, steps overlap)              */
+    double kernel_ms_plane[DS_MAX_PLANES];/* per colour component ("y-component") */
+    double total_ms;                      /* first to last event                       */
+} ds_schedule_stats;
+
+/* Per-frame transfer counts / bytes / launches of a schedule for a frame
+ * geometry (host-only, like ds_plan; the deterministic quantities behind
+ * P:148's "about 30% and 70% faster transfer times"; for STREAMED one
+ * transfer each way per chunk).  Returns DS_OK, DS_EINVAL or ds_plan's
+ * errors. */
+DS_API int ds_schedule_plan(int32_t frame_w, int32_t frame_h, int32_t channels,
+                            const ds_filter_spec* spec, int32_t schedule,
+                            ds_schedule_stats* per_frame);
+
+/* Run n host-resident frames (host_in -> host_out, pinned memory advised)
+ * frame by frame under `schedule`, on `stream`, and fill *stats (totals
+ * over the call).  SYNCHRONOUS: returns after host_out is written.  Uses
+ * one frame of library-owned device scratch (and a pinned host copy of Mid
+ * for NAIVE), freed by ds_destroy; calls on one handle are serialised.
+ * Returns as ds_run_host. */
+DS_API int ds_run_schedule(ds_handle* h, const uint8_t* host_in, int64_t n_frames,
+                           uint8_t* host_out, int32_t schedule, ds_schedule_stats* stats,
+                           ds_stream_t stream);
+
 /* Synthetic input (bench / test infrastructure, not part of the method):
  * fills dev[0 .. n_bytes) on the current device with
  *   byte(i) = splitmix64(seed * 0x9E3779B97F4A7C15 + start_index + i) >> 56

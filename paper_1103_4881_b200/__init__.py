@@ -60,6 +60,32 @@ class ds_plan_info(C.Structure):
     ]
 
 
+class ds_schedule_stats(C.Structure):
+    _fields_ = [
+        ("frames", C.c_int64),
+        ("h2d_count", C.c_int64),
+        ("d2h_count", C.c_int64),
+        ("h2d_bytes", C.c_int64),
+        ("d2h_bytes", C.c_int64),
+        ("launches", C.c_int64),
+        ("h2d_ms", C.c_double),
+        ("d2h_ms", C.c_double),
+        ("kernel_ms", C.c_double),
+        ("kernel_ms_plane", C.c_double * DS_MAX_PLANES),
+        ("total_ms", C.c_double),
+    ]
+
+    def as_dict(self):
+        d = {k: getattr(self, k) for k, _ in self._fields_ if k != "kernel_ms_plane"}
+        d["kernel_ms_plane"] = list(self.kernel_ms_plane)
+        return d
+
+
+DS_SCHED_NAIVE, DS_SCHED_OPTIMIZED, DS_SCHED_FUSED, DS_SCHED_STREAMED = 0, 1, 2, 3
+SCHED_NAMES = {DS_SCHED_NAIVE: "naive", DS_SCHED_OPTIMIZED: "optimized", DS_SCHED_FUSED: "fused",
+               DS_SCHED_STREAMED: "streamed"}
+
+
 class DSError(RuntimeError):
     def __init__(self, code: int, what: str):
         super().__init__(f"{what}: {ds_strerror(code)} ({code})")
@@ -92,6 +118,15 @@ SIGNATURES = [
     ("ds_set_tuning", C.c_int, [C.c_void_p, C.c_int32, C.c_int32]),
     ("ds_set_band_bytes", C.c_int, [C.c_void_p, C.c_int64]),
     ("ds_launch_shape", C.c_int, [C.c_void_p, C.c_int64, _PI32, _PI32, _PI32]),
+    ("ds_mid_frame_bytes", C.c_int64, [C.c_void_p]),
+    ("ds_run_htask", C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int32, C.c_int32,
+                               C.c_void_p]),
+    ("ds_run_vtask", C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int32, C.c_int32,
+                               C.c_void_p]),
+    ("ds_schedule_plan", C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.POINTER(ds_filter_spec),
+                                   C.c_int32, C.POINTER(ds_schedule_stats)]),
+    ("ds_run_schedule", C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int32,
+                                  C.POINTER(ds_schedule_stats), C.c_void_p]),
     ("ds_generate", C.c_int, [C.c_void_p, C.c_int64, C.c_uint64, C.c_int64, C.c_void_p]),
 ]
 
@@ -176,6 +211,16 @@ def ds_plan(frame_w: int, frame_h: int, channels: int = 3, spec: ds_filter_spec 
     if rc:
         raise DSError(rc, "ds_plan")
     return info
+
+
+def ds_schedule_plan(frame_w: int, frame_h: int, channels: int, schedule: int,
+                     spec: ds_filter_spec | None = None) -> dict:
+    st = ds_schedule_stats()
+    rc = lib().ds_schedule_plan(frame_w, frame_h, channels,
+                                C.byref(spec) if spec is not None else None, schedule, C.byref(st))
+    if rc:
+        raise DSError(rc, "ds_schedule_plan")
+    return st.as_dict()
 
 
 def ds_create(frame_w: int, frame_h: int, channels: int = 3, spec: ds_filter_spec | None = None):
@@ -299,6 +344,59 @@ class Downscaler:
         if rc:
             raise DSError(rc, "ds_launch_shape")
         return g.value, b.value, s.value
+
+    # ---- the paper's unfused structure / schedules --------
+    @property
+    def mid_frame_bytes(self) -> int:
+        return lib().ds_mid_frame_bytes(self._h)
+
+    def htask(self, frames, mid=None, planes=None, stream=None):
+        """H task alone (K-N3): frames -> Mid (n, mid_frame_bytes) in HBM."""
+        import torch
+
+        n = frames.numel() // self.in_frame_bytes
+        if mid is None:
+            mid = torch.empty((n, self.mid_frame_bytes), dtype=torch.uint8, device=frames.device)
+        p0, pc = planes if planes is not None else (0, self.channels)
+        s = stream if stream is not None else torch.cuda.current_stream()
+        rc = lib().ds_run_htask(self._h, frames.data_ptr(), n, mid.data_ptr(), p0, pc, s.cuda_stream)
+        if rc:
+            raise DSError(rc, "ds_run_htask")
+        return mid
+
+    def vtask(self, mid, out=None, planes=None, stream=None):
+        """V task alone (K-N3): Mid -> frames out."""
+        import torch
+
+        n = mid.numel() // self.mid_frame_bytes
+        if out is None:
+            out = self.alloc_out(n)
+        p0, pc = planes if planes is not None else (0, self.channels)
+        s = stream if stream is not None else torch.cuda.current_stream()
+        rc = lib().ds_run_vtask(self._h, mid.data_ptr(), n, out.data_ptr(), p0, pc, s.cuda_stream)
+        if rc:
+            raise DSError(rc, "ds_run_vtask")
+        return out
+
+    def schedule_plan(self, schedule: int) -> dict:
+        return ds_schedule_plan(self.w, self.h, self.channels, schedule, self.spec)
+
+    def run_schedule(self, host_frames, schedule: int, host_out=None, stream=None):
+        """Synchronous host-resident run under a transfer schedule; returns
+        (host_out, stats dict)."""
+        import torch
+
+        n = host_frames.numel() // self.in_frame_bytes
+        if host_out is None:
+            host_out = torch.empty((n, self.out_frame_bytes), dtype=torch.uint8,
+                                   pin_memory=host_frames.is_pinned())
+        st = ds_schedule_stats()
+        s = stream if stream is not None else torch.cuda.current_stream()
+        rc = lib().ds_run_schedule(self._h, host_frames.data_ptr(), n, host_out.data_ptr(), schedule,
+                                   C.byref(st), s.cuda_stream)
+        if rc:
+            raise DSError(rc, "ds_run_schedule")
+        return host_out, st.as_dict()
 
     def alloc_out(self, n: int):
         import torch

@@ -10,54 +10,16 @@
 #include <mutex>
 
 #include "ds.h"
+#include "ds_internal.h"
 #include "ds_kernels.cuh"
 
 namespace {
-
 thread_local int g_last_error = DS_OK;
-
-constexpr int kHostSlots = 3;                       // ds_run_host pipeline depth
-constexpr int64_t kUnitTargetBytes = 32 * 1024;     // K-N1 band size target (bytes staged)
-constexpr int64_t kInFlightTarget = 120 * 1024;     // K-N1 bytes in flight per SM (measured
-                                                    // optimum of tools/bw_probe tma_read)
-constexpr int kSmemLimit = 227 * 1024;              // per-CTA opt-in maximum
-constexpr int64_t kHostChunkBytes = 32LL << 20;     // ds_run_host chunk target
-
-struct HostSlot {
-    uint8_t* d_in = nullptr;
-    uint8_t* d_out = nullptr;
-    cudaStream_t stream = nullptr;
-    cudaEvent_t done = nullptr;
-};
-
-int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
-
 }  // namespace
 
-struct ds_handle {
-    int device = 0;
-    int sm_count = 0;
-    int32_t W = 0, H = 0, channels = 0;
-    ds_filter_spec spec{};
-    ds_plan_info plan{};
-    // K-N1 launch configuration
-    int ncw = 4;                 // consumer warps per CTA
-    int stages = 4;              // ring depth
-    int ctas_per_sm = 1;         // 0 = occupancy maximum
-    int64_t band_target = kUnitTargetBytes;
-    int32_t stage_stride = 0, out_stride = 0;
-    int kernel_pref = DS_KERNEL_AUTO;
-    std::atomic<int> last_kernel{DS_KERNEL_AUTO};
-    // ds_run_host state (lazily allocated, guarded by host_mu)
-    std::mutex host_mu;
-    int64_t host_chunk = 0;      // frames per chunk, 0 = auto
-    int64_t host_alloc_frames = 0;
-    HostSlot slots[kHostSlots];
-    cudaEvent_t fork_ev = nullptr;
-    bool host_init = false;
-};
+using namespace dsi;
 
-namespace {
+namespace dsi {
 
 void default_spec(ds_filter_spec* s) {
     std::memset(s, 0, sizeof *s);
@@ -124,8 +86,7 @@ int64_t fused_smem_bytes(int stages, int32_t stage_stride, int32_t out_stride) {
 }
 
 int make_plan(int32_t W, int32_t H, int32_t channels, const ds_filter_spec* spec_in,
-              ds_filter_spec* spec_out, ds_plan_info* info,
-              int64_t unit_target = kUnitTargetBytes) {
+              ds_filter_spec* spec_out, ds_plan_info* info, int64_t unit_target) {
     ds_filter_spec spec;
     if (spec_in) spec = *spec_in; else default_spec(&spec);
     if (W < 1 || H < 1) return DS_ESHAPE;
@@ -327,19 +288,6 @@ int choose_kernel(const ds_handle* h, const uint8_t* in) {
     return DS_KERNEL_FUSED;
 }
 
-// Device binding: run with the handle's device current, restore after.
-struct DeviceGuard {
-    int prev = -1;
-    bool ok = true;
-    explicit DeviceGuard(int dev) {
-        if (cudaGetDevice(&prev) != cudaSuccess) { ok = false; return; }
-        if (prev != dev && cudaSetDevice(dev) != cudaSuccess) ok = false;
-    }
-    ~DeviceGuard() {
-        int cur = -1;
-        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
-    }
-};
 
 bool device_ptr_on(const void* p, int dev) {
     cudaPointerAttributes a;
@@ -379,7 +327,8 @@ void free_host_state(ds_handle* h) {
     h->host_init = false;
 }
 
-}  // namespace
+}  // namespace dsi
+
 
 // ================================================================ C ABI ==
 extern "C" {
@@ -520,6 +469,7 @@ DS_API void ds_destroy(ds_handle* h) {
         std::lock_guard<std::mutex> lk(h->host_mu);
         DeviceGuard g(h->device);
         free_host_state(h);
+        free_sched_state(h);
     }
     delete h;
 }

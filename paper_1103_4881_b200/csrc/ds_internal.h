@@ -1,0 +1,93 @@
+// ds_internal.h -- shared internals of libds.so (not part of the C ABI).
+#pragma once
+#include <atomic>
+#include <cstdint>
+#include <mutex>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "ds.h"
+
+namespace dsi {
+
+constexpr int kHostSlots = 3;                       // ds_run_host pipeline depth
+constexpr int64_t kUnitTargetBytes = 32 * 1024;     // K-N1 band size target (bytes staged)
+constexpr int64_t kInFlightTarget = 120 * 1024;     // K-N1 bytes in flight per SM (measured
+                                                    // optimum of tools/bw_probe tma_read)
+constexpr int kSmemLimit = 227 * 1024;              // per-CTA opt-in maximum
+constexpr int64_t kHostChunkBytes = 32LL << 20;     // ds_run_host chunk target
+
+struct HostSlot {
+    uint8_t* d_in = nullptr;
+    uint8_t* d_out = nullptr;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t done = nullptr;
+};
+
+// ds_run_schedule scratch: one frame of device arrays + a pinned host copy of
+// the intermediate (the naive schedule moves it to the host and back).
+struct SchedState {
+    uint8_t* d_in = nullptr;
+    uint8_t* d_mid = nullptr;
+    uint8_t* d_out = nullptr;
+    uint8_t* h_mid = nullptr;
+    std::vector<cudaEvent_t> events;
+    bool ready = false;
+};
+
+inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+}  // namespace dsi
+
+struct ds_handle {
+    int device = 0;
+    int sm_count = 0;
+    int32_t W = 0, H = 0, channels = 0;
+    ds_filter_spec spec{};
+    ds_plan_info plan{};
+    // K-N1 launch configuration
+    int ncw = 4;                 // consumer warps per CTA
+    int stages = 4;              // ring depth
+    int ctas_per_sm = 1;         // 0 = occupancy maximum
+    int64_t band_target = dsi::kUnitTargetBytes;
+    int32_t stage_stride = 0, out_stride = 0;
+    int kernel_pref = DS_KERNEL_AUTO;
+    std::atomic<int> last_kernel{DS_KERNEL_AUTO};
+    // ds_run_host / ds_run_schedule state (lazily allocated, guarded by host_mu)
+    std::mutex host_mu;
+    int64_t host_chunk = 0;      // frames per chunk, 0 = auto
+    int64_t host_alloc_frames = 0;
+    dsi::HostSlot slots[dsi::kHostSlots];
+    cudaEvent_t fork_ev = nullptr;
+    bool host_init = false;
+    dsi::SchedState sched;
+};
+
+namespace dsi {
+
+void default_spec(ds_filter_spec* s);
+bool stage_equal(const ds_stage_spec& a, const ds_stage_spec& b);
+bool aligned16(const void* p);
+bool device_ptr_on(const void* p, int dev);
+bool ranges_overlap(const void* a, int64_t na, const void* b, int64_t nb);
+int run_device(ds_handle* h, const uint8_t* in, int64_t n, uint8_t* out, cudaStream_t st);
+void free_sched_state(ds_handle* h);
+int make_plan(int32_t W, int32_t H, int32_t channels, const ds_filter_spec* spec_in,
+              ds_filter_spec* spec_out, ds_plan_info* info, int64_t unit_target = kUnitTargetBytes);
+
+// Device binding: run with the handle's device current, restore after.
+struct DeviceGuard {
+    int prev = -1;
+    bool ok = true;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) != cudaSuccess) { ok = false; return; }
+        if (prev != dev && cudaSetDevice(dev) != cudaSuccess) ok = false;
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+}  // namespace dsi

@@ -1,0 +1,193 @@
+// ds_tasks.cuh -- K-N3: the paper's unfused structure on sm_100a.
+//
+// PAPER sec. 3.1: "the six repetitive tasks in horizontal and vertical
+// filters are allocated onto the GPU in order to generate kernels" -- one
+// kernel per task, the intermediate array (the H task's output) held
+// in global memory between them.  Here that structure is kept as an A/B
+// baseline for the fused kernel and as the device side of the transfer
+// schedules of S:369-387 (ds_run_schedule):
+//
+//   ds_htask_kernel   H task, SPEC taps: the input stream is a flat array of
+//                     8-byte packets (W % 8 == 0), packet p -> Mid bytes
+//                     3p..3p+2 (the H output tiler is exact), so
+//                     any contiguous byte range of frames/planes maps to the
+//                     Mid range at 3/8 of its offset.  16-byte loads, warp
+//                     repack through shared memory into 16-byte stores.
+//   ds_vtask_kernel   V task, SPEC taps: thread = (frame, plane, 9-row group,
+//                     4 Mid columns); 8 LDG.32 (row 4 has zero weight),
+//                     4 STG.32.
+//   ds_htask_generic / ds_vtask_generic: any ds_stage_spec, one thread per
+//                     output element, literal tiler indexing.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "ds.h"
+
+namespace ds {
+
+struct TaskPlanes {
+    int64_t in_frame, mid_frame, out_frame;
+    int64_t in_off[DS_MAX_PLANES], mid_off[DS_MAX_PLANES], out_off[DS_MAX_PLANES];
+    int32_t W[DS_MAX_PLANES], H[DS_MAX_PLANES], Wm[DS_MAX_PLANES], Hout[DS_MAX_PLANES];
+    int32_t plane_first, plane_count;
+    int64_t n_frames;
+};
+
+// ------------------------------------------------------------ H task, SPEC --
+__device__ __forceinline__ uint32_t t_div6(uint32_t x) { return __umulhi(x, 0x2AAAAAABu); }
+
+// 16 input bytes (two packets) -> 6 mid bytes, returned as lo (4 bytes) + hi (2 bytes)
+__device__ __forceinline__ void t_hchunk(uint4 v, uint32_t& lo, uint32_t& hi) {
+    const uint32_t tA = __byte_perm(v.x, v.y, 0x7643);
+    const uint32_t tB = __byte_perm(v.z, v.w, 0x7643);
+    const uint32_t a0 = t_div6(__dp4a(v.x, 0x0501u, 3u));
+    const uint32_t a1 = __dp4a(tA, 0x0101u, 1u) >> 1;
+    const uint32_t a2 = t_div6(__dp4a(tA, 0x01050000u, 3u));
+    const uint32_t b0 = t_div6(__dp4a(v.z, 0x0501u, 3u));
+    const uint32_t b1 = __dp4a(tB, 0x0101u, 1u) >> 1;
+    const uint32_t b2 = t_div6(__dp4a(tB, 0x01050000u, 3u));
+    lo = a0 | (a1 << 8) | (a2 << 16) | (b0 << 24);
+    hi = b1 | (b2 << 8);
+}
+
+// n_chunks 16-byte input chunks at `in` (16-byte aligned) -> 6 * n_chunks
+// bytes at `mid` (2-byte aligned; kVec: 16-byte aligned).
+template <bool kVec>
+__global__ void __launch_bounds__(256)
+    ds_htask_kernel(const uint8_t* __restrict__ in, uint8_t* __restrict__ mid, int64_t n_chunks) {
+    __shared__ __align__(16) uint8_t stage[8][192];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x + w * 32; base < n_chunks;
+         base += stride) {
+        const int64_t c = base + lane;
+        const int64_t valid = n_chunks - base < 32 ? n_chunks - base : 32;
+        uint32_t lo = 0, hi = 0;
+        if (c < n_chunks) {
+            const uint4 v = __ldcs(reinterpret_cast<const uint4*>(in) + c);
+            t_hchunk(v, lo, hi);
+        }
+        if (kVec && valid == 32) {
+            uint8_t* s = stage[w] + 6 * lane;
+            *reinterpret_cast<uint16_t*>(s) = (uint16_t)lo;
+            *reinterpret_cast<uint16_t*>(s + 2) = (uint16_t)(lo >> 16);
+            *reinterpret_cast<uint16_t*>(s + 4) = (uint16_t)hi;
+            __syncwarp();
+            if (lane < 12)
+                __stcs(reinterpret_cast<uint4*>(mid + 6 * base) + lane,
+                       *reinterpret_cast<const uint4*>(stage[w] + 16 * lane));
+            __syncwarp();
+        } else if (c < n_chunks) {
+            uint16_t* d = reinterpret_cast<uint16_t*>(mid + 6 * c);
+            d[0] = (uint16_t)lo;
+            d[1] = (uint16_t)(lo >> 16);
+            d[2] = (uint16_t)hi;
+        }
+    }
+}
+
+// ------------------------------------------------------------ V task, SPEC --
+// Four mid columns per thread; rows 9g + {0,1,2,3,5,6,7,8}.
+__device__ __forceinline__ uint32_t t_vquad(uint32_t a, uint32_t b, uint32_t wa, uint32_t wb) {
+    // bytes -> two 16-bit-lane pairs, V on both, quotients are byte 1 of each lane
+    const uint32_t a_lo = __byte_perm(a, 0, 0x4140), a_hi = __byte_perm(a, 0, 0x4342);
+    const uint32_t b_lo = __byte_perm(b, 0, 0x4140), b_hi = __byte_perm(b, 0, 0x4342);
+    const uint32_t s_lo = a_lo * wa + b_lo * wb + 0x00800080u;
+    const uint32_t s_hi = a_hi * wa + b_hi * wb + 0x00800080u;
+    return __byte_perm(s_lo, s_hi, 0x7531);
+}
+
+__global__ void __launch_bounds__(256)
+    ds_vtask_kernel(const uint8_t* __restrict__ mid, uint8_t* __restrict__ out,
+                    const __grid_constant__ TaskPlanes tp) {
+    const int p = tp.plane_first + blockIdx.y;
+    const int quads = tp.Wm[p] >> 2;
+    const int groups = tp.H[p] / 9;
+    const int64_t items = (int64_t)quads * groups;
+    for (int64_t f = blockIdx.z; f < tp.n_frames; f += gridDim.z) {
+        const uint8_t* mp = mid + f * tp.mid_frame + tp.mid_off[p];
+        uint8_t* op = out + f * tp.out_frame + tp.out_off[p];
+        for (int64_t it = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; it < items;
+             it += (int64_t)gridDim.x * blockDim.x) {
+            const int g = (int)(it / quads), q = (int)(it - (int64_t)g * quads);
+            const uint32_t* col = reinterpret_cast<const uint32_t*>(mp + (int64_t)9 * g * tp.Wm[p]) + q;
+            const int wq = tp.Wm[p] >> 2;
+            const uint32_t m0 = __ldcs(col), m1 = __ldcs(col + wq), m2 = __ldcs(col + 2 * wq),
+                           m3 = __ldcs(col + 3 * wq), m5 = __ldcs(col + 5 * wq),
+                           m6 = __ldcs(col + 6 * wq), m7 = __ldcs(col + 7 * wq),
+                           m8 = __ldcs(col + 8 * wq);
+            uint32_t* o = reinterpret_cast<uint32_t*>(op + (int64_t)4 * g * tp.Wm[p]) + q;
+            __stcs(o, t_vquad(m0, m1, 96u, 160u));
+            __stcs(o + wq, t_vquad(m2, m3, 32u, 224u));
+            __stcs(o + 2 * wq, t_vquad(m5, m6, 224u, 32u));
+            __stcs(o + 3 * wq, t_vquad(m7, m8, 160u, 96u));
+        }
+    }
+}
+
+// --------------------------------------------------------- generic task kernels --
+__device__ __forceinline__ int32_t t_mod(int32_t a, int32_t m) {
+    int32_t r = a % m;
+    return r < 0 ? r + m : r;
+}
+__device__ __forceinline__ int32_t t_clamp(int32_t v) { return v < 0 ? 0 : (v > 255 ? 255 : v); }
+
+struct GenericTask {
+    TaskPlanes tp;
+    ds_stage_spec s;
+};
+
+// H task, any spec: Mid[row][Qh r1 + j] = stage_h(In[row][(oh + Sh r1 + i) mod W]).
+__global__ void __launch_bounds__(256) ds_htask_generic(const uint8_t* __restrict__ in,
+                                                        uint8_t* __restrict__ mid,
+                                                        const __grid_constant__ GenericTask gt) {
+    const TaskPlanes& tp = gt.tp;
+    const ds_stage_spec& s = gt.s;
+    const int p = tp.plane_first + blockIdx.y;
+    const int64_t items = (int64_t)tp.H[p] * tp.Wm[p];
+    for (int64_t f = blockIdx.z; f < tp.n_frames; f += gridDim.z) {
+        const uint8_t* ip = in + f * tp.in_frame + tp.in_off[p];
+        uint8_t* mp = mid + f * tp.mid_frame + tp.mid_off[p];
+        for (int64_t it = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; it < items;
+             it += (int64_t)gridDim.x * blockDim.x) {
+            const int row = (int)(it / tp.Wm[p]), col = (int)(it - (int64_t)row * tp.Wm[p]);
+            const int r1 = col / s.outputs, j = col - r1 * s.outputs;
+            int32_t acc = s.bias;
+            for (int i = 0; i < s.pattern; ++i) {
+                const int32_t w = s.weight[j][i];
+                if (w) acc += w * (int32_t)__ldg(ip + (int64_t)row * tp.W[p] +
+                                                  t_mod(s.origin + s.paving * r1 + i, tp.W[p]));
+            }
+            mp[it] = (uint8_t)t_clamp(acc / s.divisor);
+        }
+    }
+}
+
+// V task, any spec: Out[Qv r0 + k][c] = stage_v(Mid[(ov + Sv r0 + i) mod H][c]).
+__global__ void __launch_bounds__(256) ds_vtask_generic(const uint8_t* __restrict__ mid,
+                                                        uint8_t* __restrict__ out,
+                                                        const __grid_constant__ GenericTask gt) {
+    const TaskPlanes& tp = gt.tp;
+    const ds_stage_spec& s = gt.s;
+    const int p = tp.plane_first + blockIdx.y;
+    const int64_t items = (int64_t)tp.Hout[p] * tp.Wm[p];
+    for (int64_t f = blockIdx.z; f < tp.n_frames; f += gridDim.z) {
+        const uint8_t* mp = mid + f * tp.mid_frame + tp.mid_off[p];
+        uint8_t* op = out + f * tp.out_frame + tp.out_off[p];
+        for (int64_t it = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; it < items;
+             it += (int64_t)gridDim.x * blockDim.x) {
+            const int R = (int)(it / tp.Wm[p]), col = (int)(it - (int64_t)R * tp.Wm[p]);
+            const int r0 = R / s.outputs, k = R - r0 * s.outputs;
+            int32_t acc = s.bias;
+            for (int i = 0; i < s.pattern; ++i) {
+                const int32_t w = s.weight[k][i];
+                if (w) acc += w * (int32_t)__ldg(mp + (int64_t)t_mod(s.origin + s.paving * r0 + i,
+                                                                      tp.H[p]) * tp.Wm[p] + col);
+            }
+            op[it] = (uint8_t)t_clamp(acc / s.divisor);
+        }
+    }
+}
+
+}  // namespace ds

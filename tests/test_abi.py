@@ -144,3 +144,28 @@ def test_null_handle_calls():
     L.ds_destroy(None)                                    # NULL-safe
     assert L.ds_generate(None, 0, 1, 0, None) == ds.DS_OK   # n = 0 no-op
     assert L.ds_generate(None, 16, 1, 0, None) == ds.DS_EINVAL
+
+
+def test_schedule_byte_model_matches_spec_and_paper():
+    """S:375 / S:385: naive 12 transfers per frame, optimised 6; S:365 byte
+    sizes.  The byte reductions 27.3% (H2D) and 69.2% (D2H) are the
+    deterministic counterpart of P:148's "about 30% and 70% faster transfer
+    times in host to device and device to host"."""
+    naive = ds.ds_schedule_plan(352, 288, 3, ds.DS_SCHED_NAIVE)
+    opt = ds.ds_schedule_plan(352, 288, 3, ds.DS_SCHED_OPTIMIZED)
+    assert naive["h2d_count"] + naive["d2h_count"] == 12 and naive["launches"] == 6
+    assert opt["h2d_count"] == 3 and opt["d2h_count"] == 3 and opt["launches"] == 6
+    # Y input array 352x288 = 101,376 B; Mid = 288x132 + 2 * 144x66
+    assert (naive["h2d_bytes"], naive["d2h_bytes"]) == (152064 + 57024, 57024 + 25344)
+    assert (opt["h2d_bytes"], opt["d2h_bytes"]) == (152064, 25344)
+    h2d_cut = 1 - opt["h2d_bytes"] / naive["h2d_bytes"]
+    d2h_cut = 1 - opt["d2h_bytes"] / naive["d2h_bytes"]
+    assert abs(h2d_cut - 0.273) < 0.001 and abs(d2h_cut - 0.692) < 0.001
+    assert abs(h2d_cut - 0.30) < 0.05 and abs(d2h_cut - 0.70) < 0.05     # P:148 "about"
+    fused = ds.ds_schedule_plan(352, 288, 3, ds.DS_SCHED_FUSED)
+    assert fused["h2d_count"] == fused["d2h_count"] == fused["launches"] == 1
+    # the reductions depend only on the 8->3 / 9->4 geometry, not on the taps
+    hd = ds.ds_schedule_plan(1920, 1080, 3, ds.DS_SCHED_NAIVE)
+    assert 1 - 3110400 / hd["h2d_bytes"] == pytest.approx(h2d_cut, abs=1e-3)
+    with pytest.raises(ds.DSError):
+        ds.ds_schedule_plan(352, 288, 3, 9)
