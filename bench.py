@@ -50,6 +50,10 @@ def parse():
     ap.add_argument("--stages", type=int, default=0)
     ap.add_argument("--ctas", type=int, default=0)
     ap.add_argument("--kernel", choices=["auto", "fused", "generic"], default="auto")
+    ap.add_argument("--band-bytes", type=int, default=0, help="K-N1 band size (0 = default)")
+    ap.add_argument("--graph", action="store_true",
+                    help="capture the K timed ds_run calls in one CUDA graph and replay it "
+                         "(removes host launch overhead; for the launch-bound 1-frame config)")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
                     help="CPU-oracle sample budget (seconds of 1-core work)")
@@ -68,7 +72,9 @@ def workload(args, world):
     else:
         total = 300 if world == 1 else 3000
     cfg["total"] = total
-    if args.config.startswith("hd") and world == 1 and total == 300:
+    if args.config.startswith("hd") and world == 1 and total == 1:
+        cfg["name"] = f"configs[1]: one {cfg['label']} frame on 1 B200 (latency; L2-resident)"
+    elif args.config.startswith("hd") and world == 1 and total == 300:
         cfg["name"] = f"configs[2]: 300-frame {cfg['label']} stream on 1 B200"
     elif args.config.startswith("hd") and total == 3000:
         cfg["name"] = f"configs[3]: 3000-frame {cfg['label']} stream frame-sharded over {world} B200"
@@ -158,15 +164,21 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
-def ncu_traffic(config_key):
-    """Per-launch DRAM bytes from the committed ncu --set full summary, if one
-    exists for this config (profiles/ncu_summary.json)."""
+def ncu_traffic(config_key, frames_per_launch):
+    """Per-launch DRAM bytes from the committed ncu --set full summary of this
+    config (profiles/ncu_summary.json), scaled per frame if the captured
+    launch processed a different number of frames (streaming: linear)."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         with open(p) as f:
             j = json.load(f)
         e = j[config_key]
-        return e["dram_bytes_per_launch"], e.get("source")
+        n0 = e.get("frames_per_launch", frames_per_launch)
+        t = e["dram_bytes_per_launch"] * frames_per_launch / n0
+        src = e.get("source", "")
+        if n0 != frames_per_launch:
+            src += f" (scaled from {n0} to {frames_per_launch} frames per launch)"
+        return t, src
     except Exception:
         return None, None
 
@@ -278,9 +290,17 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # NCCL over NVLink for the real multi-GPU run; DS_DIST_BACKEND=gloo lets the
+    # N>1 plumbing run with several ranks on one GPU (tests only: the ranks'
+    # kernels never wait on one another, collectives go through the host).
+    backend = os.environ.get("DS_DIST_BACKEND", "nccl")
+    coll_dev = "cuda" if backend == "nccl" else "cpu"
     if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        torch.cuda.set_device(local % torch.cuda.device_count())
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     else:
         torch.cuda.set_device(0)
     dev = torch.cuda.current_device()
@@ -294,6 +314,8 @@ def main():
     assert d.in_frame_bytes == fin and d.out_frame_bytes == fout
     if args.kernel != "auto":
         d.set_kernel({"fused": ds.DS_KERNEL_FUSED, "generic": ds.DS_KERNEL_GENERIC}[args.kernel])
+    if args.band_bytes:
+        d.set_band_bytes(args.band_bytes)
     if args.stages or args.ctas:
         d.set_tuning(args.stages or 4, args.ctas)
     stream = torch.cuda.current_stream()
@@ -311,19 +333,48 @@ def main():
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    evs = [torch.cuda.Event(enable_timing=True) for _ in range(2 * args.steps)]
-    with ClockSampler(dev) as clk:
-        for k in range(args.steps):
-            evs[2 * k].record(stream)
-            d(x, y)
-            evs[2 * k + 1].record(stream)
+    host_call_us = None
+    if args.graph:
+        g = torch.cuda.CUDAGraph()
+        cs = torch.cuda.Stream()
+        cs.wait_stream(stream)
+        with torch.cuda.stream(cs):
+            d(x, y)                                   # warm the capture stream
         torch.cuda.synchronize()
+        with torch.cuda.graph(g, stream=cs):
+            for _ in range(args.steps):
+                d(x, y)
+        g.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with ClockSampler(dev) as clk:
+            e0.record(stream)
+            g.replay()
+            e1.record(stream)
+            torch.cuda.synchronize()
+        total_ms = e0.elapsed_time(e1)
+        per = [total_ms / args.steps]
+        # host cost of one un-captured call (ctypes + argument checks + launch)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(200):
+            d(x, y)
+        host_call_us = (time.perf_counter() - t0) / 200 * 1e6
+        torch.cuda.synchronize()
+    else:
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(2 * args.steps)]
+        with ClockSampler(dev) as clk:
+            for k in range(args.steps):
+                evs[2 * k].record(stream)
+                d(x, y)
+                evs[2 * k + 1].record(stream)
+            torch.cuda.synchronize()
+        per = [evs[2 * k].elapsed_time(evs[2 * k + 1]) for k in range(args.steps)]
+        total_ms = evs[0].elapsed_time(evs[-1])
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    per = [evs[2 * k].elapsed_time(evs[2 * k + 1]) for k in range(args.steps)]
-    total_ms = evs[0].elapsed_time(evs[-1])
-    t = torch.tensor([total_ms, statistics.mean(per)], dtype=torch.float64, device="cuda")
+    t = torch.tensor([total_ms, statistics.mean(per)], dtype=torch.float64, device=coll_dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms, kern_ms = float(t[0]), float(t[1])
@@ -334,7 +385,7 @@ def main():
     alg_bytes = n * (fin_live + fout)            # required bytes per launch (per rank)
     achieved = alg_bytes / (kern_ms / 1e3) / 1e9
     eff_full = n * (fin + fout) / (kern_ms / 1e3) / 1e9
-    traffic, traffic_src = ncu_traffic(args.config)
+    traffic, traffic_src = ncu_traffic(args.config, n)
 
     # ---- optional NCCL gather (C-1), timed separately -----------------------
     gather_ms = None
@@ -344,9 +395,9 @@ def main():
         dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        gather_frames(y, cfg["total"])
+        gather_frames(y if backend == "nccl" else y.cpu(), cfg["total"])
         torch.cuda.synchronize()
-        gt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
+        gt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=coll_dev)
         dist.all_reduce(gt, op=dist.ReduceOp.MAX)
         gather_ms = float(gt[0]) * 1e3
 
@@ -368,7 +419,7 @@ def main():
             d.run_host(hin, hout)
         e1.record(stream)
         torch.cuda.synchronize()
-        et = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
+        et = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=coll_dev)
         if world > 1:
             dist.all_reduce(et, op=dist.ReduceOp.MAX)
         e2e = {"value": cfg["total"] * ks / (float(et[0]) / 1e3), "unit": "frames/s",
@@ -423,6 +474,9 @@ def main():
             "gpu_launches": args.steps,
             "clocks": clk.result(),
             "gather_ms": gather_ms,
+            "timing": ("one CUDA graph of the K ds_run calls, replayed between two events"
+                       if args.graph else "CUDA events around each ds_run on the launching stream"),
+            "host_call_us": host_call_us,
             "impl": "ours",
         }
         print(json.dumps(line), flush=True)

@@ -157,22 +157,46 @@ int make_plan(int32_t W, int32_t H, int32_t channels, const ds_filter_spec* spec
 }
 
 // ----------------------------------------------------------- K-N1 launch --
-// Launch shape from the plan: enough consumer warps for one task each (cap
-// 8), and a ring deep enough for ~kInFlightTarget bytes in flight per SM at
-// one CTA per SM (tools/bw_probe: 120 KB/SM is the TMA read optimum; more
+// Launch shape from a band plan: enough consumer warps for one task each
+// (cap 8), and a ring deep enough for ~kInFlightTarget bytes in flight per
+// SM at one CTA per SM (tools/bw_probe: ~120 KB/SM is the TMA optimum; more
 // in flight lowers DRAM efficiency).
-int max_tasks(const ds_plan_info& pi);
-void configure_fused(ds_handle* h) {
-    const ds_plan_info& pi = h->plan;
-    if (!pi.fused_eligible) return;
-    const int t = max_tasks(pi);
-    const int w = (t + 31) / 32;
-    h->ncw = w <= 1 ? 1 : w <= 2 ? 2 : w <= 4 ? 4 : 8;
-    h->stage_stride = (int32_t)round_up(pi.unit_in_bytes_max, 128);
-    h->out_stride = (int32_t)round_up(pi.unit_out_bytes_max, 128);
-    h->stages = (int)std::max<int64_t>(2, std::min<int64_t>(8, (kInFlightTarget + h->stage_stride / 2) /
-                                                                   h->stage_stride));
-    h->ctas_per_sm = 1;
+int max_tasks(const ds_plan_info& pi) {
+    int t = 0;
+    for (int p = 0; p < pi.n_planes; ++p)
+        t = std::max(t, 2 * pi.band_groups[p] * (pi.in_w[p] / 16));
+    return t;
+}
+
+FusedCfg make_cfg(const ds_plan_info& pi) {
+    FusedCfg c;
+    c.plan = pi;
+    if (!pi.fused_eligible) return c;
+    const int w = (max_tasks(pi) + 31) / 32;
+    c.ncw = w <= 1 ? 1 : w <= 2 ? 2 : w <= 4 ? 4 : 8;
+    c.stage_stride = (int32_t)round_up(pi.unit_in_bytes_max, 128);
+    c.out_stride = (int32_t)round_up(pi.unit_out_bytes_max, 128);
+    c.stages = (int)std::max<int64_t>(2, std::min<int64_t>(8, (kInFlightTarget + c.stage_stride / 2) /
+                                                                  c.stage_stride));
+    c.ctas_per_sm = 1;
+    c.valid = true;
+    return c;
+}
+
+int prepare_cfg(FusedCfg& c);
+int configure_fused(ds_handle* h) {
+    h->fused = make_cfg(h->plan);
+    h->fine = FusedCfg{};
+    if (!h->plan.fused_eligible) return DS_OK;
+    ds_plan_info fp;
+    if (make_plan(h->W, h->H, h->channels, &h->spec, nullptr, &fp,
+                  std::min<int64_t>(kFineUnitTarget, h->band_target)) == DS_OK &&
+        fp.fused_eligible && fp.units_per_frame > h->plan.units_per_frame)
+        h->fine = make_cfg(fp);
+    DeviceGuard g(h->device);
+    int rc = prepare_cfg(h->fused);
+    if (!rc) rc = prepare_cfg(h->fine);
+    return rc;
 }
 
 using FusedFn = void (*)(const ds::FusedParams);
@@ -186,43 +210,63 @@ FusedFn fused_fn(int ncw) {
     }
 }
 
-int max_tasks(const ds_plan_info& pi) {
-    int t = 0;
-    for (int p = 0; p < pi.n_planes; ++p)
-        t = std::max(t, 2 * pi.band_groups[p] * (pi.in_w[p] / 16));
-    return t;
-}
-
 // Ring depth that fits, capped by the request.
-int fit_stages(const ds_handle* h, int want) {
+int fit_stages(const FusedCfg& c, int want) {
     int s = std::max(2, std::min(8, want));
-    while (s > 2 && fused_smem_bytes(s, h->stage_stride, h->out_stride) > kSmemLimit) --s;
+    while (s > 2 && fused_smem_bytes(s, c.stage_stride, c.out_stride) > kSmemLimit) --s;
     return s;
 }
 
-int fused_grid(const ds_handle* h, int64_t n_units, int* grid, int* block, int* smem) {
-    const int stages = fit_stages(h, h->stages);
-    const int sm = (int)fused_smem_bytes(stages, h->stage_stride, h->out_stride);
-    const int threads = (h->ncw + 1) * 32;
-    FusedFn fn = fused_fn(h->ncw);
-    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, sm) != cudaSuccess)
+// Which configuration a call of n frames uses.
+const FusedCfg& pick_cfg(const ds_handle* h, int64_t n) {
+    if (h->fine.valid && n * h->fused.plan.units_per_frame < 2LL * h->sm_count) return h->fine;
+    return h->fused;
+}
+
+// Resolve and cache the launch shape of a configuration on the current
+// device (sets the kernel's dynamic shared-memory attribute once).
+int prepare_cfg(FusedCfg& c) {
+    if (!c.valid) return DS_OK;
+    const int stages = fit_stages(c, c.stages);
+    const int sm = (int)fused_smem_bytes(stages, c.stage_stride, c.out_stride);
+    const int threads = (c.ncw + 1) * 32;
+    FusedFn fn = fused_fn(c.ncw);
+    // the attribute belongs to the kernel function (shared by every handle and
+    // configuration using this instantiation): always the opt-in maximum
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit) !=
+        cudaSuccess) {
+        cudaGetLastError();
         return DS_ECUDA;
+    }
     int occ = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, sm) != cudaSuccess ||
-        occ < 1)
+        occ < 1) {
+        cudaGetLastError();
         return DS_ECUDA;
-    if (h->ctas_per_sm > 0) occ = std::min(occ, h->ctas_per_sm);
-    const int64_t g = std::min<int64_t>(n_units, (int64_t)occ * h->sm_count);
+    }
+    if (c.ctas_per_sm > 0) occ = std::min(occ, c.ctas_per_sm);
+    c.grid_per_sm = occ;
+    c.threads = threads;
+    c.smem = sm;
+    c.run_stages = stages;
+    return DS_OK;
+}
+
+int fused_grid(const ds_handle* h, const FusedCfg& c, int64_t n_units, int* grid, int* block,
+               int* smem) {
+    if (c.grid_per_sm < 1) return DS_ECUDA;
+    const int64_t g = std::min<int64_t>(n_units, (int64_t)c.grid_per_sm * h->sm_count);
     *grid = (int)std::max<int64_t>(g, 1);
-    *block = threads;
-    *smem = sm;
+    *block = c.threads;
+    *smem = c.smem;
     return DS_OK;
 }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 int launch_fused(ds_handle* h, const uint8_t* in, int64_t n, uint8_t* out, cudaStream_t st) {
-    const ds_plan_info& pi = h->plan;
+    const FusedCfg& c = pick_cfg(h, n);
+    const ds_plan_info& pi = c.plan;
     ds::FusedParams p;
     std::memset(&p, 0, sizeof p);
     p.in = in; p.out = out;
@@ -230,8 +274,8 @@ int launch_fused(ds_handle* h, const uint8_t* in, int64_t n, uint8_t* out, cudaS
     p.upf = (int32_t)pi.units_per_frame;
     p.n_units = n * pi.units_per_frame;
     p.n_planes = pi.n_planes;
-    p.stage_stride = h->stage_stride;
-    p.out_stride = h->out_stride;
+    p.stage_stride = c.stage_stride;
+    p.out_stride = c.out_stride;
     const bool out_al = aligned16(out) && pi.out_frame_bytes % 16 == 0;
     int32_t start = 0;
     for (int q = 0; q < pi.n_planes; ++q) {
@@ -251,10 +295,10 @@ int launch_fused(ds_handle* h, const uint8_t* in, int64_t n, uint8_t* out, cudaS
         start += pi.in_h[q] / (9 * P.k);
     }
     int grid, block, smem;
-    int rc = fused_grid(h, p.n_units, &grid, &block, &smem);
+    int rc = fused_grid(h, c, p.n_units, &grid, &block, &smem);
     if (rc) return rc;
-    p.stages = fit_stages(h, h->stages);
-    fused_fn(h->ncw)<<<grid, block, smem, st>>>(p);
+    p.stages = c.run_stages;
+    fused_fn(c.ncw)<<<grid, block, smem, st>>>(p);
     return cudaGetLastError() == cudaSuccess ? DS_OK : DS_ECUDA;
 }
 
@@ -365,7 +409,12 @@ DS_API ds_handle* ds_create(int32_t frame_w, int32_t frame_h, int32_t channels,
     h->W = frame_w; h->H = frame_h; h->channels = channels;
     h->spec = spec;
     h->plan = pi;
-    configure_fused(h);
+    const int crc = configure_fused(h);
+    if (crc) {
+        delete h;
+        g_last_error = crc;
+        return nullptr;
+    }
     g_last_error = DS_OK;
     return h;
 }
@@ -520,9 +569,11 @@ DS_API int ds_last_kernel(const ds_handle* h) { return h ? h->last_kernel.load()
 
 DS_API int ds_set_tuning(ds_handle* h, int32_t stages, int32_t ctas_per_sm) {
     if (!h || stages < 2 || stages > 8 || ctas_per_sm < 0 || ctas_per_sm > 32) return DS_EINVAL;
-    h->stages = stages;
-    h->ctas_per_sm = ctas_per_sm;
-    return DS_OK;
+    h->fused.stages = stages;
+    h->fused.ctas_per_sm = ctas_per_sm;
+    h->fine = FusedCfg{};          // an explicit tuning applies to every call size
+    DeviceGuard g(h->device);
+    return prepare_cfg(h->fused);
 }
 
 DS_API int ds_set_band_bytes(ds_handle* h, int64_t target) {
@@ -533,8 +584,7 @@ DS_API int ds_set_band_bytes(ds_handle* h, int64_t target) {
     if (rc) return rc;
     h->plan = pi;
     h->band_target = target;
-    configure_fused(h);
-    return DS_OK;
+    return configure_fused(h);
 }
 
 DS_API int ds_launch_shape(const ds_handle* h, int64_t n, int32_t* grid, int32_t* block,
@@ -542,7 +592,8 @@ DS_API int ds_launch_shape(const ds_handle* h, int64_t n, int32_t* grid, int32_t
     if (!h || n < 0 || !h->plan.fused_eligible) return DS_EINVAL;
     DeviceGuard g(h->device);
     int gr, bl, sm;
-    const int rc = fused_grid(h, std::max<int64_t>(1, n * h->plan.units_per_frame), &gr, &bl, &sm);
+    const FusedCfg& c = pick_cfg(h, n);
+    const int rc = fused_grid(h, c, std::max<int64_t>(1, n * c.plan.units_per_frame), &gr, &bl, &sm);
     if (rc) return rc;
     if (grid) *grid = gr;
     if (block) *block = bl;

@@ -38,6 +38,21 @@ struct SchedState {
 
 inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
+// One K-N1 launch configuration: a band plan plus its launch shape.
+struct FusedCfg {
+    ds_plan_info plan{};
+    int ncw = 4;                 // consumer warps per CTA
+    int stages = 4;              // ring depth
+    int ctas_per_sm = 1;         // 0 = occupancy maximum
+    int32_t stage_stride = 0, out_stride = 0;
+    bool valid = false;
+    // cached launch shape (computed when the configuration is set, so ds_run
+    // makes no occupancy / attribute calls)
+    int grid_per_sm = 0, threads = 0, smem = 0, run_stages = 0;
+};
+
+constexpr int64_t kFineUnitTarget = 16 * 1024;      // small batches: more, smaller units
+
 }  // namespace dsi
 
 struct ds_handle {
@@ -46,12 +61,11 @@ struct ds_handle {
     int32_t W = 0, H = 0, channels = 0;
     ds_filter_spec spec{};
     ds_plan_info plan{};
-    // K-N1 launch configuration
-    int ncw = 4;                 // consumer warps per CTA
-    int stages = 4;              // ring depth
-    int ctas_per_sm = 1;         // 0 = occupancy maximum
+    // K-N1 launch configurations: `fused` (bands of ~band_target bytes, used
+    // for streams) and `fine` (~16 KiB bands, used when a call has fewer
+    // coarse units than 2 per SM, e.g. one HD frame)
     int64_t band_target = dsi::kUnitTargetBytes;
-    int32_t stage_stride = 0, out_stride = 0;
+    dsi::FusedCfg fused, fine;
     int kernel_pref = DS_KERNEL_AUTO;
     std::atomic<int> last_kernel{DS_KERNEL_AUTO};
     // ds_run_host / ds_run_schedule state (lazily allocated, guarded by host_mu)

@@ -350,3 +350,27 @@ def test_hd_300_frame_stream_bench_config():
             ho, wo = pout.shape
             for R, Cc in zip(rng.integers(0, ho, 200), rng.integers(0, wo, 200)):
                 assert pout[R, Cc] == oracle.pixel(pin, int(R), int(Cc))
+
+
+def test_cuda_graph_capture():
+    """ds_run is capturable in a CUDA graph (the launch-bound 1-frame config
+    replays a graph); replayed output equals the oracle."""
+    W, H = 1920, 1080
+    d = ds.Downscaler(W, H, 3)
+    fr = synth.random_frames(21, 0, 1, W, H)
+    x = torch.from_numpy(fr).cuda()
+    y = d.alloc_out(1)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        d(x, y)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    y.zero_()
+    with torch.cuda.graph(g, stream=s):
+        d(x, y)
+    y.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    _assert_same(y.cpu().numpy(), oracle.execute_frames(fr, W, H), "graph replay")
+    assert d.launch_shape(1) != d.launch_shape(300)     # small batches use the fine band plan

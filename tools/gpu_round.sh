@@ -1,0 +1,10 @@
+# parity tests, the default bench line, one-frame latency (coarse vs fine units), and the
+# N>1 bench path run as 2 ranks on one GPU with the gloo backend (plumbing check only)
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest=$?" > gpurun_out/status.txt
+timeout 300 python bench.py > gpurun_out/bench.log 2>&1; echo "bench=$?" >> gpurun_out/status.txt
+: > gpurun_out/latency.jsonl
+for extra in "" "--graph"; do timeout 120 python bench.py --frames 1 --steps 2000 --no-cpu-baseline --no-e2e $extra >> gpurun_out/latency.jsonl 2>&1; done
+DS_DIST_BACKEND=gloo timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 2 --steps 20 --warmup 3 --frames 600 --gather > gpurun_out/bench_2rank_gloo.log 2>&1; echo "bench2=$?" >> gpurun_out/status.txt
+DS_DIST_BACKEND=gloo timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29534 bench.py --impl reference --gpus 2 --steps 3 --warmup 1 > gpurun_out/bench_2rank_ref.log 2>&1; echo "bench2ref=$?" >> gpurun_out/status.txt
+echo done

@@ -93,6 +93,8 @@ def main():
     ap.add_argument("--launches", default=os.path.join(ROOT, "gpurun_out", "launches.csv"))
     ap.add_argument("--rep", action="append", default=[])
     ap.add_argument("--note", default="")
+    ap.add_argument("--frames", type=int, action="append", default=[],
+                    help="frames per profiled launch, one per --rep (default: bench defaults)")
     a = ap.parse_args()
     outdir = os.path.join(ROOT, "profiles", a.round)
     os.makedirs(outdir, exist_ok=True)
@@ -114,8 +116,9 @@ def main():
 
     summ_path = os.path.join(ROOT, "profiles", "ncu_summary.json")
     summ = json.load(open(summ_path)) if os.path.exists(summ_path) else {}
-    for spec in a.rep:
+    for ri, spec in enumerate(a.rep):
         cfg, rep = spec.split("=", 1)
+        frames = a.frames[ri] if ri < len(a.frames) else (1000 if cfg.startswith("4k") else 300)
         ms = raw_metrics(rep)
         txt = [f"# ncu --set full: {os.path.basename(rep)} ({a.round}, config {cfg})"]
         for i, d in enumerate(ms):
@@ -137,7 +140,7 @@ def main():
         wr = scale(*d["dram__bytes_write.sum"])
         dur = scale(*d["gpu__time_duration.sum"])
         summ[cfg] = {"dram_bytes_per_launch": rd + wr, "dram_read_bytes": rd, "dram_write_bytes": wr,
-                     "duration_us_under_ncu": dur,
+                     "duration_us_under_ncu": dur, "frames_per_launch": frames,
                      "source": f"profiles/{a.round}/ncu_full_{cfg}.txt (ncu --set full --clock-control none)"}
     if a.rep:
         json.dump(summ, open(summ_path, "w"), indent=1)
