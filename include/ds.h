@@ -65,7 +65,9 @@ enum { DS_MAX_PATTERN = 16, DS_MAX_OUTPUTS = 8, DS_MAX_PLANES = 3 };
 enum {
     DS_KERNEL_AUTO = 0,     /* fused band kernel when eligible, else generic     */
     DS_KERNEL_FUSED = 1,    /* K-N1: TMA-staged fused H+V band kernel            */
-    DS_KERNEL_GENERIC = 2   /* K-N2: one thread per output pixel, any spec       */
+    DS_KERNEL_GENERIC = 2,  /* K-N2: one thread per output pixel, any spec       */
+    DS_KERNEL_FUSED_GENERAL = 3  /* K-N1g: TMA-staged fused band kernel for any spec:
+                                    halo rows staged in smem, smem intermediate     */
 };
 
 /*
@@ -114,6 +116,10 @@ typedef struct {
     int64_t units_per_frame;             /* K-N1 work units per frame            */
     int64_t unit_in_bytes_max;           /* K-N1 bytes staged per unit (max)     */
     int64_t unit_out_bytes_max;
+    int32_t fused_general_eligible;      /* 1 if K-N1g can run this geometry+spec  */
+    int32_t general_band_reps[DS_MAX_PLANES];  /* K-N1g: V repetitions per unit */
+    int64_t general_units_per_frame;
+    int64_t general_stage_bytes_max;     /* K-N1g: staged rows (band + halo) bytes */
 } ds_plan_info;
 
 /* Fill *out with SPEC's downscaler (hfilter_8to3 S:527-535, vfilter_9to4
@@ -184,8 +190,11 @@ DS_API int64_t ds_out_frame_bytes(const ds_handle* h);
 DS_API int ds_plane_dims(const ds_handle* h, int plane, int32_t* in_w, int32_t* in_h,
                          int32_t* out_w, int32_t* out_h);
 
-/* Force a kernel (DS_KERNEL_*).  DS_KERNEL_FUSED on an ineligible
- * geometry returns DS_EUNSUPPORTED and leaves the setting unchanged. */
+/* Force a kernel (DS_KERNEL_*).  DS_KERNEL_FUSED / DS_KERNEL_FUSED_GENERAL
+ * on an ineligible geometry/spec returns DS_EUNSUPPORTED and leaves the
+ * setting unchanged.  A forced fused kernel still yields to K-N2 when the
+ * input pointer is not 16-byte aligned.  AUTO picks K-N1 (SPEC taps), then
+ * K-N1g, then K-N2. */
 DS_API int ds_set_kernel(ds_handle* h, int32_t kernel);
 
 /* Kernel used by the most recent ds_run on this handle (any thread), or

@@ -19,10 +19,11 @@ from . import _build
 
 DS_OK, DS_EINVAL, DS_ESHAPE, DS_EUNSUPPORTED, DS_ECUDA, DS_ENOMEM = 0, -1, -2, -3, -4, -5
 DS_CHROMA_444, DS_CHROMA_420 = 0, 1
-DS_KERNEL_AUTO, DS_KERNEL_FUSED, DS_KERNEL_GENERIC = 0, 1, 2
+DS_KERNEL_AUTO, DS_KERNEL_FUSED, DS_KERNEL_GENERIC, DS_KERNEL_FUSED_GENERAL = 0, 1, 2, 3
 DS_MAX_PATTERN, DS_MAX_OUTPUTS, DS_MAX_PLANES = 16, 8, 3
 KERNEL_NAMES = {DS_KERNEL_AUTO: "none", DS_KERNEL_FUSED: "K-N1 fused band (TMA ring)",
-                DS_KERNEL_GENERIC: "K-N2 generic"}
+                DS_KERNEL_GENERIC: "K-N2 generic",
+                DS_KERNEL_FUSED_GENERAL: "K-N1g fused band, any spec (TMA ring, smem halo + mid)"}
 
 
 class ds_stage_spec(C.Structure):
@@ -57,6 +58,10 @@ class ds_plan_info(C.Structure):
         ("units_per_frame", C.c_int64),
         ("unit_in_bytes_max", C.c_int64),
         ("unit_out_bytes_max", C.c_int64),
+        ("fused_general_eligible", C.c_int32),
+        ("general_band_reps", C.c_int32 * DS_MAX_PLANES),
+        ("general_units_per_frame", C.c_int64),
+        ("general_stage_bytes_max", C.c_int64),
     ]
 
 
@@ -263,17 +268,20 @@ class Downscaler:
     Runs on ``torch.cuda.current_stream()``.
     """
 
-    def __init__(self, w: int, h: int, channels: int = 3, chroma: str | int = "420",
+    def __init__(self, w: int, h: int, channels: int = 3, chroma: str | int | None = None,
                  spec: ds_filter_spec | None = None, kernel: int = DS_KERNEL_AUTO):
+        """chroma: "420" / "444" / DS_CHROMA_*; None = the spec's own (4:2:0 by default)."""
         import torch
 
         if not torch.cuda.is_available():
             raise RuntimeError("Downscaler needs a CUDA device (no CPU fallback)")
-        c = chroma if isinstance(chroma, int) else {"420": DS_CHROMA_420, "444": DS_CHROMA_444}[
-            str(chroma)]
         if spec is None:
             spec = ds_default_spec()
-        spec.chroma = c
+        else:
+            spec = ds_filter_spec.from_buffer_copy(spec)
+        if chroma is not None:
+            spec.chroma = chroma if isinstance(chroma, int) else {
+                "420": DS_CHROMA_420, "444": DS_CHROMA_444}[str(chroma)]
         self.spec = spec
         self.w, self.h, self.channels = w, h, channels
         self.device = torch.cuda.current_device()

@@ -12,6 +12,7 @@
 #include "ds.h"
 #include "ds_internal.h"
 #include "ds_kernels.cuh"
+#include "ds_general.cuh"
 
 namespace {
 thread_local int g_last_error = DS_OK;
@@ -145,6 +146,43 @@ int make_plan(int32_t W, int32_t H, int32_t channels, const ds_filter_spec* spec
         // at least a 2-deep ring must fit in one CTA's shared memory
         fused = fused_smem_bytes(2, (int32_t)round_up(umax, 128), (int32_t)round_up(omax, 128)) <=
                 kSmemLimit;
+    }
+    // K-N1g (any spec): whole-width staged rows need 16-byte rows; bands of
+    // k V repetitions stage R = Sv (k-1) + Pv rows (band + halo).
+    bool general = true;
+    for (int p = 0; p < channels && general; ++p) general = (pi.in_w[p] % 16 == 0);
+    if (general) {
+        int64_t units = 0, smax = 0, mmax = 0, omax = 0;
+        for (int p = 0; p < channels; ++p) {
+            const int G = pi.in_h[p] / spec.v.paving;
+            int best = 1;
+            for (int d = 1; d <= G; ++d) {
+                if (G % d) continue;
+                const int64_t R = (int64_t)spec.v.paving * (d - 1) + spec.v.pattern;
+                if (R * pi.in_w[p] <= kGeneralStageTarget) best = d;
+            }
+            const int64_t R = (int64_t)spec.v.paving * (best - 1) + spec.v.pattern;
+            pi.general_band_reps[p] = best;
+            units += G / best;
+            smax = std::max<int64_t>(smax, R * pi.in_w[p]);
+            mmax = std::max<int64_t>(mmax, (R + 3) * pi.out_w[p]);   // +3: dp4a row blocks
+            omax = std::max<int64_t>(omax, (int64_t)spec.v.outputs * best * pi.out_w[p]);
+            // exact reciprocal index division: items * divisor < 2^32
+            const int64_t np = pi.in_w[p] / spec.h.paving;
+            if (R * np * np >= (1LL << 32) ||
+                (int64_t)spec.v.outputs * best * pi.out_w[p] * pi.out_w[p] >= (1LL << 32))
+                general = false;
+        }
+        const int64_t need = 2 * round_up(smax, 128) + round_up(mmax, 128) + 2 * round_up(omax, 128) +
+                             2 * DS_MAX_OUTPUTS * DS_MAX_PATTERN * 4 + 64;
+        if (need > kSmemLimit) general = false;
+        pi.general_units_per_frame = units;
+        pi.general_stage_bytes_max = smax;
+    }
+    pi.fused_general_eligible = general ? 1 : 0;
+    if (!general) {
+        for (int p = 0; p < DS_MAX_PLANES; ++p) pi.general_band_reps[p] = 0;
+        pi.general_units_per_frame = pi.general_stage_bytes_max = 0;
     }
     pi.fused_eligible = fused ? 1 : 0;
     if (!fused) {
@@ -302,6 +340,125 @@ int launch_fused(ds_handle* h, const uint8_t* in, int64_t n, uint8_t* out, cudaS
     return cudaGetLastError() == cudaSuccess ? DS_OK : DS_ECUDA;
 }
 
+// ------------------------------------------------------------ K-N1g launch --
+using GeneralFn = void (*)(const ds::GeneralParams);
+
+int64_t general_smem(const GeneralCfg& c, int stages) {
+    return (int64_t)stages * c.stage_stride + c.mid_stride + 2LL * c.out_stride + 2LL * stages * 8;
+}
+
+int configure_general(ds_handle* h) {
+    GeneralCfg c;
+    const ds_plan_info& pi = h->plan;
+    if (!pi.fused_general_eligible) { h->general = c; return DS_OK; }
+    const ds_filter_spec& sp = h->spec;
+    int64_t smax = 0, mmax = 0, omax = 0;
+    int32_t upf = 0;
+    for (int p = 0; p < pi.n_planes; ++p) {
+        c.k[p] = pi.general_band_reps[p];
+        c.R[p] = sp.v.paving * (c.k[p] - 1) + sp.v.pattern;
+        smax = std::max<int64_t>(smax, (int64_t)c.R[p] * pi.in_w[p]);
+        mmax = std::max<int64_t>(mmax, (int64_t)(c.R[p] + 3) * pi.out_w[p]);   // V reads 4-row blocks
+        omax = std::max<int64_t>(omax, (int64_t)sp.v.outputs * c.k[p] * pi.out_w[p]);
+        upf += (pi.in_h[p] / sp.v.paving) / c.k[p];
+    }
+    c.upf = upf;
+    c.stage_stride = (int32_t)round_up(smax, 128);
+    c.mid_stride = (int32_t)round_up(mmax, 128);
+    c.out_stride = (int32_t)round_up(omax, 128);
+    // K-N1g is issue-bound (tools/general_perf.py sweep, profiles/r01/general.md):
+    // 2 CTAs x 8 consumer warps per SM with a 2-deep ring beat deeper rings
+    // and 16-warp CTAs
+    c.stages = 2;
+    c.ncw = 8;
+    const int want_ctas = 2;
+    c.threads = (c.ncw + 1) * 32;
+    c.smem = (int)general_smem(c, c.stages);
+    GeneralFn fn = c.ncw == 16 ? ds::ds_fused_general_kernel<16> : ds::ds_fused_general_kernel<8>;
+    DeviceGuard g(h->device);
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             kSmemLimit - 2 * DS_MAX_OUTPUTS * DS_MAX_PATTERN * 4) != cudaSuccess) {
+        cudaGetLastError();
+        return DS_ECUDA;
+    }
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, c.threads, c.smem) != cudaSuccess || occ < 1) {
+        cudaGetLastError();
+        return DS_ECUDA;
+    }
+    c.grid_per_sm = std::min(occ, want_ctas);
+
+    c.valid = true;
+    h->general = c;
+    return DS_OK;
+}
+
+ds::GenStage gen_stage(const ds_stage_spec& s) {
+    ds::GenStage g;
+    std::memset(&g, 0, sizeof g);
+    g.P = s.pattern; g.S = s.paving; g.Q = s.outputs; g.bias = s.bias;
+    g.D = (uint32_t)s.divisor;
+    g.D_rcp = s.divisor == 1 ? 0xffffffffu : (uint32_t)((1ULL << 32) / (uint64_t)s.divisor);
+    std::memcpy(g.w, s.weight, sizeof g.w);
+    g.s8 = 1;
+    for (int k = 0; k < DS_MAX_OUTPUTS; ++k)
+        for (int i = 0; i < DS_MAX_PATTERN; ++i) {
+            const int32_t w = s.weight[k][i];
+            if (w < -128 || w > 127) g.s8 = 0;
+            g.wp[k][i / 4] |= (uint32_t)(uint8_t)(int8_t)(w < -128 ? 0 : w > 127 ? 0 : w) << (8 * (i % 4));
+        }
+    return g;
+}
+
+uint32_t rcp32(int32_t d) { return d > 1 ? (uint32_t)((0x100000000ULL + d - 1) / (uint64_t)d) : 0u; }
+
+int launch_general(ds_handle* h, const uint8_t* in, int64_t n, uint8_t* out, cudaStream_t st) {
+    const GeneralCfg& c = h->general;
+    const ds_plan_info& pi = h->plan;
+    const ds_filter_spec& sp = h->spec;
+    ds::GeneralParams p;
+    std::memset(&p, 0, sizeof p);
+    p.in = in; p.out = out;
+    p.in_frame = pi.in_frame_bytes; p.out_frame = pi.out_frame_bytes;
+    p.upf = c.upf;
+    p.n_units = n * c.upf;
+    p.n_planes = pi.n_planes;
+    p.stages = c.stages;
+    p.stage_stride = c.stage_stride;
+    p.mid_stride = c.mid_stride;
+    p.out_stride = c.out_stride;
+    p.h = gen_stage(sp.h);
+    p.v = gen_stage(sp.v);
+    const bool out_al = aligned16(out) && pi.out_frame_bytes % 16 == 0;
+    int32_t start = 0;
+    for (int q = 0; q < pi.n_planes; ++q) {
+        ds::GenPlane& P = p.pl[q];
+        P.in_off = pi.in_offset[q];
+        P.out_off = pi.out_offset[q];
+        P.W = pi.in_w[q];
+        P.H = pi.in_h[q];
+        P.Wm = pi.out_w[q];
+        P.k = c.k[q];
+        P.R = c.R[q];
+        P.np = P.W / sp.h.paving;
+        P.np_rcp = rcp32(P.np);
+        P.wm_rcp = rcp32(P.Wm);
+        P.quads_rcp = rcp32(P.Wm / 4);
+        P.oh = (int32_t)(((int64_t)sp.h.origin % P.W + P.W) % P.W);
+        P.ov = (int32_t)(((int64_t)sp.v.origin % P.H + P.H) % P.H);
+        P.unit_start = start;
+        P.unit_out = sp.v.outputs * P.k * P.Wm;
+        P.bulk_store = (out_al && P.out_off % 16 == 0 && P.unit_out % 16 == 0) ? 1 : 0;
+        start += (P.H / sp.v.paving) / P.k;
+    }
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(p.n_units, (int64_t)c.grid_per_sm * h->sm_count));
+    if (c.ncw == 16)
+        ds::ds_fused_general_kernel<16><<<(unsigned)grid, c.threads, c.smem, st>>>(p);
+    else
+        ds::ds_fused_general_kernel<8><<<(unsigned)grid, c.threads, c.smem, st>>>(p);
+    return cudaGetLastError() == cudaSuccess ? DS_OK : DS_ECUDA;
+}
+
 int launch_generic(ds_handle* h, const uint8_t* in, int64_t n, uint8_t* out, cudaStream_t st) {
     const ds_plan_info& pi = h->plan;
     ds::GenericParams p;
@@ -327,9 +484,12 @@ int launch_generic(ds_handle* h, const uint8_t* in, int64_t n, uint8_t* out, cud
 }
 
 int choose_kernel(const ds_handle* h, const uint8_t* in) {
-    if (h->kernel_pref == DS_KERNEL_GENERIC) return DS_KERNEL_GENERIC;
-    if (!h->plan.fused_eligible || !aligned16(in)) return DS_KERNEL_GENERIC;
-    return DS_KERNEL_FUSED;
+    if (h->kernel_pref == DS_KERNEL_GENERIC || !aligned16(in)) return DS_KERNEL_GENERIC;
+    const bool k1 = h->plan.fused_eligible && h->fused.valid;
+    const bool k1g = h->plan.fused_general_eligible && h->general.valid;
+    if (h->kernel_pref == DS_KERNEL_FUSED) return k1 ? DS_KERNEL_FUSED : DS_KERNEL_GENERIC;
+    if (h->kernel_pref == DS_KERNEL_FUSED_GENERAL) return k1g ? DS_KERNEL_FUSED_GENERAL : DS_KERNEL_GENERIC;
+    return k1 ? DS_KERNEL_FUSED : k1g ? DS_KERNEL_FUSED_GENERAL : DS_KERNEL_GENERIC;
 }
 
 
@@ -350,8 +510,9 @@ bool ranges_overlap(const void* a, int64_t na, const void* b, int64_t nb) {
 
 int run_device(ds_handle* h, const uint8_t* in, int64_t n, uint8_t* out, cudaStream_t st) {
     const int k = choose_kernel(h, in);
-    const int rc = (k == DS_KERNEL_FUSED) ? launch_fused(h, in, n, out, st)
-                                          : launch_generic(h, in, n, out, st);
+    const int rc = (k == DS_KERNEL_FUSED)           ? launch_fused(h, in, n, out, st)
+                   : (k == DS_KERNEL_FUSED_GENERAL) ? launch_general(h, in, n, out, st)
+                                                    : launch_generic(h, in, n, out, st);
     if (rc == DS_OK) h->last_kernel.store(k);
     return rc;
 }
@@ -409,7 +570,8 @@ DS_API ds_handle* ds_create(int32_t frame_w, int32_t frame_h, int32_t channels,
     h->W = frame_w; h->H = frame_h; h->channels = channels;
     h->spec = spec;
     h->plan = pi;
-    const int crc = configure_fused(h);
+    int crc = configure_fused(h);
+    if (!crc) crc = configure_general(h);
     if (crc) {
         delete h;
         g_last_error = crc;
@@ -558,9 +720,11 @@ DS_API int ds_plane_dims(const ds_handle* h, int plane, int32_t* in_w, int32_t* 
 
 DS_API int ds_set_kernel(ds_handle* h, int32_t kernel) {
     if (!h) return DS_EINVAL;
-    if (kernel != DS_KERNEL_AUTO && kernel != DS_KERNEL_FUSED && kernel != DS_KERNEL_GENERIC)
+    if (kernel != DS_KERNEL_AUTO && kernel != DS_KERNEL_FUSED && kernel != DS_KERNEL_GENERIC &&
+        kernel != DS_KERNEL_FUSED_GENERAL)
         return DS_EINVAL;
     if (kernel == DS_KERNEL_FUSED && !h->plan.fused_eligible) return DS_EUNSUPPORTED;
+    if (kernel == DS_KERNEL_FUSED_GENERAL && !h->plan.fused_general_eligible) return DS_EUNSUPPORTED;
     h->kernel_pref = kernel;
     return DS_OK;
 }
@@ -584,7 +748,8 @@ DS_API int ds_set_band_bytes(ds_handle* h, int64_t target) {
     if (rc) return rc;
     h->plan = pi;
     h->band_target = target;
-    return configure_fused(h);
+    const int crc = configure_fused(h);
+    return crc ? crc : configure_general(h);
 }
 
 DS_API int ds_launch_shape(const ds_handle* h, int64_t n, int32_t* grid, int32_t* block,

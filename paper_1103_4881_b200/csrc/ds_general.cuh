@@ -1,0 +1,312 @@
+// ds_general.cuh -- K-N1g: the fused band kernel for ANY separable stage spec
+// (SURVEY f3): halos (pattern P > paving S) with toroidal wrap,
+// origin != 0, other ratios, negative lobes, any divisor.
+//
+// Same persistent, warp-specialised TMA pipeline as K-N1.  A work unit is
+// (frame, plane, band of k V repetitions).  Those repetitions read input rows
+// (o_v + S_v g + i) mod H for g in the band, i < P_v: R = S_v (k-1) + P_v
+// consecutive rows modulo H, i.e. the band plus its halo.  The producer
+// stages them whole-width with one bulk copy per non-wrapping segment (the
+// bottom halo wraps to the plane's first rows).  Consumers run the H task on
+// every staged row into a u8 intermediate in shared memory, then the
+// V task from it, stage the output band in shared memory and bulk-store it.
+// Divisions by runtime values use a reciprocal plus one correction step, so
+// results are exact (truncation toward zero, then clamp).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "ds.h"
+#include "ds_kernels.cuh"
+
+namespace ds {
+
+struct GenPlane {
+    int64_t in_off, out_off;
+    int32_t W, H, Wm;          // input row bytes, rows, mid/output row bytes
+    int32_t k;                 // V repetitions per unit
+    int32_t R;                 // staged rows per unit = Sv (k-1) + Pv
+    int32_t np;                // H repetitions per row = W / Sh
+    uint32_t np_rcp;           // ceil(2^32 / np) (np > 1)
+    uint32_t wm_rcp;           // ceil(2^32 / Wm) (Wm > 1)
+    uint32_t quads_rcp;        // ceil(2^32 / (Wm / 4)) (Wm / 4 > 1)
+    int32_t oh;                // H origin reduced mod W (>= 0)
+    int32_t ov;                // V origin reduced mod H (>= 0)
+    int32_t unit_start;
+    int32_t unit_out;          // Qv * k * Wm
+    int32_t bulk_store;
+};
+
+struct GenStage {
+    int32_t P, S, Q, bias;
+    uint32_t D, D_rcp;         // divisor and floor(2^32 / D) (D = 1: 0xffffffff)
+    int32_t s8;                // 1: every weight fits in s8 -> dp4a fast path
+    int32_t pad_;
+    int32_t w[DS_MAX_OUTPUTS][DS_MAX_PATTERN];
+    uint32_t wp[DS_MAX_OUTPUTS][DS_MAX_PATTERN / 4];   // s8-packed weights, 4 taps per word
+};
+
+struct GeneralParams {
+    const uint8_t* in;
+    uint8_t* out;
+    int64_t in_frame, out_frame, n_units;
+    int32_t upf, n_planes, stages, stage_stride, mid_stride, out_stride;
+    GenPlane pl[DS_MAX_PLANES];
+    GenStage h, v;
+};
+
+// floor(a / D) for 0 <= a < 2^32: q0 = umulhi(a, floor(2^32/D)) is q or q-1.
+__device__ __forceinline__ uint32_t g_udiv(uint32_t a, uint32_t D, uint32_t rcp) {
+    uint32_t q = __umulhi(a, rcp);
+    if (a - q * D >= D) ++q;
+    return q;
+}
+// clamp_0^255(trunc(acc / D))
+__device__ __forceinline__ uint32_t g_stage_out(int32_t acc, uint32_t D, uint32_t rcp) {
+    if (acc <= 0) {
+        // trunc toward zero of a non-positive quotient is <= 0 -> clamps to 0
+        return 0u;
+    }
+    const uint32_t q = g_udiv((uint32_t)acc, D, rcp);
+    return q > 255u ? 255u : q;
+}
+// d = c + sum_i a.u8[i] * b.s8[i]
+__device__ __forceinline__ int32_t dp4a_us(uint32_t a, uint32_t b, int32_t c) {
+    int32_t d;
+    asm("dp4a.u32.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+__device__ __forceinline__ uint32_t lds32(const uint8_t* p) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)));
+    return v;
+}
+__device__ __forceinline__ int32_t g_div_small(int32_t t, int32_t d, uint32_t rcp) {
+    return d == 1 ? t : (int32_t)__umulhi((uint32_t)t, rcp);
+}
+
+struct GenCursor {
+    int64_t u, f;
+    int32_t local, gdiv, gmod, upf;
+    __device__ __forceinline__ void init(const GeneralParams& p) {
+        u = blockIdx.x;
+        upf = p.upf;
+        f = (int64_t)(blockIdx.x / (uint32_t)upf);
+        local = (int32_t)(blockIdx.x - (uint32_t)f * (uint32_t)upf);
+        gdiv = (int32_t)(gridDim.x / (uint32_t)upf);
+        gmod = (int32_t)(gridDim.x - (uint32_t)gdiv * (uint32_t)upf);
+    }
+    __device__ __forceinline__ void next() {
+        u += gridDim.x;
+        f += gdiv;
+        local += gmod;
+        if (local >= upf) { local -= upf; ++f; }
+    }
+    __device__ __forceinline__ int plane(const GeneralParams& p) const {
+        return (p.n_planes > 2 && local >= p.pl[2].unit_start)   ? 2
+               : (p.n_planes > 1 && local >= p.pl[1].unit_start) ? 1
+                                                                 : 0;
+    }
+};
+
+// <8>: register cap (<= 75) so two CTAs fit per SM -- the register file is
+// split across 4 SMSPs, so 18 warps need <= 102 registers each; <16>: one CTA.
+template <int NCW>
+__global__ void __launch_bounds__((NCW + 1) * 32, NCW == 8 ? 3 : 1)
+    ds_fused_general_kernel(const __grid_constant__ GeneralParams p) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    constexpr int NC = NCW * 32;
+    const int S = p.stages;
+    uint8_t* ring = smem;
+    uint8_t* mid = smem + (size_t)S * p.stage_stride;
+    uint8_t* outs = mid + p.mid_stride;
+    uint64_t* full = reinterpret_cast<uint64_t*>(outs + (size_t)2 * p.out_stride);
+    uint64_t* empty = full + S;
+    __shared__ int32_t wh[DS_MAX_OUTPUTS][DS_MAX_PATTERN], wv[DS_MAX_OUTPUTS][DS_MAX_PATTERN];
+
+    const int tid = threadIdx.x;
+    for (int i = tid; i < DS_MAX_OUTPUTS * DS_MAX_PATTERN; i += blockDim.x) {
+        wh[i / DS_MAX_PATTERN][i % DS_MAX_PATTERN] = p.h.w[i / DS_MAX_PATTERN][i % DS_MAX_PATTERN];
+        wv[i / DS_MAX_PATTERN][i % DS_MAX_PATTERN] = p.v.w[i / DS_MAX_PATTERN][i % DS_MAX_PATTERN];
+    }
+    if (tid == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], NCW);
+        }
+        fence_barrier_init();
+    }
+    __syncthreads();
+
+    const int warp = tid >> 5, lane = tid & 31;
+    GenCursor cur;
+    cur.init(p);
+    int s = 0;
+    uint32_t phase = 0;
+    if (warp == NCW) {
+        if (lane == 0) {
+            const uint64_t pol = policy_evict_first();
+            bool first_round = true;
+            for (; cur.u < p.n_units; cur.next()) {
+                if (!first_round) mbar_wait(&empty[s], phase ^ 1);
+                const GenPlane& P = p.pl[cur.plane(p)];
+                const int band = cur.local - P.unit_start;
+                const uint8_t* plane = p.in + cur.f * p.in_frame + P.in_off;
+                uint8_t* dst = ring + (size_t)s * p.stage_stride;
+                mbar_arrive_expect_tx(&full[s], (uint32_t)P.R * (uint32_t)P.W);
+                // rows ov + Sv*k*band .. + R-1, modulo H, in non-wrapping segments
+                int row = (int)(((int64_t)P.ov + (int64_t)p.v.S * P.k * band) % P.H);
+                int left = P.R;
+                while (left > 0) {
+                    const int seg = min(left, P.H - row);
+                    bulk_g2s(dst, plane + (int64_t)row * P.W, (uint32_t)seg * (uint32_t)P.W, &full[s], pol);
+                    dst += (size_t)seg * P.W;
+                    left -= seg;
+                    row = 0;
+                }
+                if (++s == S) { s = 0; phase ^= 1; first_round = false; }
+            }
+        }
+        return;
+    }
+
+    int oslot = 0;
+    for (; cur.u < p.n_units; cur.next()) {
+        const GenPlane& P = p.pl[cur.plane(p)];
+        const int band = cur.local - P.unit_start;
+        const uint8_t* st = ring + (size_t)s * p.stage_stride;
+        uint8_t* ob = outs + (size_t)oslot * p.out_stride;
+        const int W = P.W, Wm = P.Wm, np = P.np;
+        mbar_wait(&full[s], phase);
+
+        // ---- H task on every staged row -> mid (u8); item = (row, H rep)
+        const int QH = p.h.Q, PH = p.h.P, SH = p.h.S;
+        const int h_items = P.R * np;
+        for (int it = tid; it < h_items; it += NC) {
+            {
+                const int r = g_div_small(it, np, P.np_rcp);
+                const int r1 = it - r * np;
+                const uint8_t* rowp = st + (size_t)r * W;
+                uint8_t* mrow = mid + (size_t)r * Wm;
+                int c0 = P.oh + SH * r1;
+                if (c0 >= W) c0 -= W;                 // oh < W and Sh*r1 < W
+                uint8_t* mo = mrow + QH * r1;
+                if (p.h.s8 && c0 + PH <= W) {
+                    // window of nw+1 aligned words (bytes past the row meet zero taps)
+                    const uint8_t* wb = rowp + (c0 & ~3);
+                    const uint32_t sel = 0x3210u + 0x1111u * (uint32_t)(c0 & 3);
+                    const uint32_t w0 = lds32(wb), w1 = lds32(wb + 4), w2 = lds32(wb + 8),
+                                   w3 = lds32(wb + 12), w4 = lds32(wb + 16);
+                    const uint32_t x0 = __byte_perm(w0, w1, sel), x1 = __byte_perm(w1, w2, sel),
+                                   x2 = __byte_perm(w2, w3, sel), x3 = __byte_perm(w3, w4, sel);
+#pragma unroll
+                    for (int j = 0; j < DS_MAX_OUTPUTS; ++j) {
+                        if (j < QH) {
+                            int32_t acc = dp4a_us(x0, p.h.wp[j][0], p.h.bias);
+                            acc = dp4a_us(x1, p.h.wp[j][1], acc);
+                            acc = dp4a_us(x2, p.h.wp[j][2], acc);
+                            acc = dp4a_us(x3, p.h.wp[j][3], acc);
+                            mo[j] = (uint8_t)g_stage_out(acc, p.h.D, p.h.D_rcp);
+                        }
+                    }
+                } else {
+                    for (int j = 0; j < QH; ++j) {
+                        int32_t acc = p.h.bias;
+                        int c = c0;
+                        for (int i = 0; i < PH; ++i) {
+                            const int32_t w = wh[j][i];
+                            if (w) acc += w * (int32_t)rowp[c];
+                            if (++c == W) c = 0;
+                        }
+                        mo[j] = (uint8_t)g_stage_out(acc, p.h.D, p.h.D_rcp);
+                    }
+                }
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);     // ring slot no longer read
+        named_bar_sync(1, NC);                      // mid complete
+
+        // ---- V task from mid -> output band
+        if (p.v.s8 && (Wm & 3) == 0) {
+            // item = (V repetition g, 4 mid columns): 4x4 byte transposes turn
+            // 4 rows x 4 columns into 4 column words, one dp4a per 4 taps
+            const int quads = Wm >> 2;
+            const int QV = p.v.Q, nb = (p.v.P + 3) >> 2;
+            const int v_items = P.k * quads;
+            for (int it = tid; it < v_items; it += NC) {
+                {
+                    const int g = g_div_small(it, quads, P.quads_rcp);
+                    const int q = it - g * quads;
+                    const uint8_t* mb = mid + (size_t)(p.v.S * g) * Wm + 4 * q;
+                    int32_t acc[DS_MAX_OUTPUTS][4];
+#pragma unroll
+                    for (int kk = 0; kk < DS_MAX_OUTPUTS; ++kk)
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) acc[kk][e] = p.v.bias;
+                    for (int b4 = 0; b4 < nb; ++b4) {
+                        const uint8_t* rb = mb + (size_t)(4 * b4) * Wm;
+                        const uint32_t r0 = lds32(rb), r1 = lds32(rb + Wm), r2 = lds32(rb + 2 * Wm),
+                                       r3 = lds32(rb + 3 * Wm);
+                        const uint32_t ta = __byte_perm(r0, r1, 0x5140), tb = __byte_perm(r2, r3, 0x5140);
+                        const uint32_t tc = __byte_perm(r0, r1, 0x7362), td = __byte_perm(r2, r3, 0x7362);
+                        const uint32_t col0 = __byte_perm(ta, tb, 0x5410), col1 = __byte_perm(ta, tb, 0x7632),
+                                       col2 = __byte_perm(tc, td, 0x5410), col3 = __byte_perm(tc, td, 0x7632);
+#pragma unroll
+                        for (int kk = 0; kk < DS_MAX_OUTPUTS; ++kk) {
+                            if (kk < QV) {
+                                const uint32_t wq = p.v.wp[kk][b4];
+                                acc[kk][0] = dp4a_us(col0, wq, acc[kk][0]);
+                                acc[kk][1] = dp4a_us(col1, wq, acc[kk][1]);
+                                acc[kk][2] = dp4a_us(col2, wq, acc[kk][2]);
+                                acc[kk][3] = dp4a_us(col3, wq, acc[kk][3]);
+                            }
+                        }
+                    }
+#pragma unroll
+                    for (int kk = 0; kk < DS_MAX_OUTPUTS; ++kk) {
+                        if (kk < QV) {
+                            const uint32_t o = g_stage_out(acc[kk][0], p.v.D, p.v.D_rcp) |
+                                               (g_stage_out(acc[kk][1], p.v.D, p.v.D_rcp) << 8) |
+                                               (g_stage_out(acc[kk][2], p.v.D, p.v.D_rcp) << 16) |
+                                               (g_stage_out(acc[kk][3], p.v.D, p.v.D_rcp) << 24);
+                            *reinterpret_cast<uint32_t*>(ob + (size_t)(QV * g + kk) * Wm + 4 * q) = o;
+                        }
+                    }
+                }
+            }
+        } else {
+            const int v_items = P.unit_out;
+            for (int it = tid; it < v_items; it += NC) {
+                const int orow = g_div_small(it, Wm, P.wm_rcp);
+                const int c = it - orow * Wm;
+                const int g = orow / p.v.Q, kk = orow - g * p.v.Q;
+                const uint8_t* mcol = mid + (size_t)(p.v.S * g) * Wm + c;
+                int32_t acc = p.v.bias;
+                for (int i = 0; i < p.v.P; ++i) {
+                    const int32_t w = wv[kk][i];
+                    if (w) acc += w * (int32_t)mcol[(size_t)i * Wm];
+                }
+                ob[it] = (uint8_t)g_stage_out(acc, p.v.D, p.v.D_rcp);
+            }
+        }
+        uint8_t* dst = p.out + cur.f * p.out_frame + P.out_off + (int64_t)band * P.unit_out;
+        if (P.bulk_store) {
+            fence_proxy_async_smem();
+            named_bar_sync(1, NC);                  // output band complete; mid free
+            if (tid == 0) {
+                bulk_s2g(dst, ob, (uint32_t)P.unit_out);
+                bulk_commit();
+                bulk_wait_read<1>();                // the other out slot is free
+            }
+        } else {
+            named_bar_sync(1, NC);
+            for (int x = tid; x < P.unit_out; x += NC) dst[x] = ob[x];
+        }
+        if (++s == S) { s = 0; phase ^= 1; }
+        oslot ^= 1;
+    }
+    if (tid == 0) bulk_wait_all();
+}
+
+}  // namespace ds

@@ -52,6 +52,18 @@ struct FusedCfg {
 };
 
 constexpr int64_t kFineUnitTarget = 16 * 1024;      // small batches: more, smaller units
+constexpr int64_t kGeneralStageTarget = 40 * 1024;  // K-N1g staged rows per unit
+
+// K-N1g launch configuration (any stage spec).
+struct GeneralCfg {
+    bool valid = false;
+    int32_t k[DS_MAX_PLANES] = {0, 0, 0};     // V repetitions per unit
+    int32_t R[DS_MAX_PLANES] = {0, 0, 0};     // staged rows per unit
+    int32_t upf = 0;
+    int32_t stage_stride = 0, mid_stride = 0, out_stride = 0;
+    int stages = 2, ncw = 8;
+    int grid_per_sm = 0, threads = 0, smem = 0;
+};
 
 }  // namespace dsi
 
@@ -66,6 +78,7 @@ struct ds_handle {
     // coarse units than 2 per SM, e.g. one HD frame)
     int64_t band_target = dsi::kUnitTargetBytes;
     dsi::FusedCfg fused, fine;
+    dsi::GeneralCfg general;
     int kernel_pref = DS_KERNEL_AUTO;
     std::atomic<int> last_kernel{DS_KERNEL_AUTO};
     // ds_run_host / ds_run_schedule state (lazily allocated, guarded by host_mu)

@@ -85,6 +85,7 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// Consumer wait: spin on try_wait (a hinted sleep wakes late on a full slot).
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred p;\n"
@@ -92,6 +93,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
         "@!p bra DS_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
         "r"(parity)
+        : "memory");
+}
+// Producer wait: hinted, so the single producer lane sleeps in hardware
+// instead of spinning and taking issue slots from the consumer warps.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "DS_WAITS_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+        "@!p bra DS_WAITS_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity), "r"(0x989680u)
         : "memory");
 }
 __device__ __forceinline__ uint64_t policy_evict_first() {
@@ -340,7 +352,7 @@ __device__ __forceinline__ int32_t clamp255(int32_t v) { return v < 0 ? 0 : (v >
 // the mid value at row (ov + Sv r0 + i) mod H, column C; each mid value is
 // the H stage over columns (oh + Sh r1 + i') mod W of that row (S:248-252,
 // S:517-520), rounded to u8 before the V stage.
-__global__ void __launch_bounds__(256) ds_generic_kernel(const __grid_constant__ GenericParams p) {
+__global__ void __launch_bounds__(256, 1) ds_generic_kernel(const __grid_constant__ GenericParams p) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < p.total_out;
          idx += stride) {

@@ -127,6 +127,16 @@ def test_plan_generic_spec_not_fused():
              divisor=8, bias=4)
     p = ds.ds_plan(48, 27, 1, ds.make_spec(h=h))
     assert p.fused_eligible == 0 and p.out_w[0] == 18
+    # K-N1g takes it: bands of k V repetitions stage Sv (k-1) + Pv rows
+    assert p.fused_general_eligible == 1
+    k = p.general_band_reps[0]
+    assert 3 % k == 0 and p.general_units_per_frame == 3 // k
+    assert p.general_stage_bytes_max == (9 * (k - 1) + 9) * 48
+
+
+def test_plan_general_needs_16_byte_rows():
+    p = ds.ds_plan(40, 45, 1)                      # W % 16 != 0
+    assert p.fused_eligible == 0 and p.fused_general_eligible == 0
 
 
 def test_create_validates_before_touching_cuda():

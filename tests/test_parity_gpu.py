@@ -183,15 +183,18 @@ def _oracle_stage(d):
                              d["bias"])
 
 
-@pytest.mark.parametrize("W,H,ch", [(48, 27, 1), (352, 288, 3), (64, 36, 3)])
-def test_halo_and_origin_spec(W, H, ch):
-    """P > S halos with toroidal wrap and origin != 0."""
+@pytest.mark.parametrize("W,H,ch", [(48, 27, 1), (352, 288, 3), (64, 36, 3), (1920, 1080, 3)])
+@pytest.mark.parametrize("kernel", [ds.DS_KERNEL_FUSED_GENERAL, GENERIC])
+def test_halo_and_origin_spec(W, H, ch, kernel):
+    """P > S halos with toroidal wrap and origin != 0:
+    K-N1g (halo rows staged in smem, smem intermediate) and K-N2."""
     hd, vd = _halo_spec()
     spec = ds.make_spec(h=hd, v=vd, chroma=ds.DS_CHROMA_420)
     d = ds.Downscaler(W, H, ch, spec=spec)
+    assert d.plan.fused_general_eligible == 1 and d.plan.fused_eligible == 0
     fr = synth.random_frames(9, 0, 3, W, H, ch, 1)
-    got = _run(d, fr)
-    assert d.last_kernel() == GENERIC
+    got = _run(d, fr, kernel)
+    assert d.last_kernel() == kernel
     want = oracle.execute_frames(fr, W, H, ch, 1, _oracle_stage(hd), _oracle_stage(vd))
     _assert_same(got, want, "halo")
 
@@ -206,6 +209,58 @@ def test_negative_weights_and_other_ratio():
     fr = synth.random_frames(4, 0, 4, 64, 30, 1)
     want = oracle.execute_frames(fr, 64, 30, 1, 1, _oracle_stage(hd), _oracle_stage(vd))
     _assert_same(_run(d, fr), want, "negative")
+    assert d.last_kernel() == ds.DS_KERNEL_FUSED_GENERAL
+    _assert_same(_run(d, fr, GENERIC), want, "negative K-N2")
+
+
+@pytest.mark.parametrize("W,H,ch,chroma", [(352, 288, 3, 1), (1920, 1080, 3, 1), (1920, 1080, 3, 0),
+                                           (48, 27, 1, 1)])
+def test_general_kernel_on_spec_taps(W, H, ch, chroma):
+    """K-N1g forced on SPEC's own downscaler equals the oracle (and K-N1)."""
+    d = ds.Downscaler(W, H, ch, chroma=chroma)
+    fr = synth.random_frames(17, 0, 3, W, H, ch, chroma)
+    got = _run(d, fr, ds.DS_KERNEL_FUSED_GENERAL)
+    assert d.last_kernel() == ds.DS_KERNEL_FUSED_GENERAL
+    _assert_same(got, oracle.execute_frames(fr, W, H, ch, chroma), "K-N1g spec taps")
+
+
+def _random_spec(rng):
+    def stage(max_p):
+        P = int(rng.integers(1, max_p + 1))
+        S = int(rng.integers(1, P + 3))
+        Q = int(rng.integers(1, 5))
+        D = int(rng.choice([1, 2, 3, 5, 6, 7, 8, 16, 100, 1 << 20]))
+        w = [[int(x) if rng.random() < 0.7 else 0 for x in rng.integers(-40, 120, P)] for _ in range(Q)]
+        total = max(1, sum(max(0, x) for row in w for x in row))
+        return dict(pattern=P, paving=S, origin=int(rng.integers(-50, 50)), weights=w,
+                    divisor=max(D, total // 255 if D == 1 else D), bias=int(rng.integers(-200, 400)))
+    return stage(16), stage(16)
+
+
+def test_general_kernel_fuzz_random_specs():
+    """Random separable specs (halos, gaps P < S, origins, negative taps,
+    divisors incl. 1 and 2^20) on random geometries, K-N1g vs the oracle."""
+    rng = np.random.default_rng(2024)
+    checked = 0
+    for trial in range(40):
+        hd, vd = _random_spec(rng)
+        ch = int(rng.choice([1, 3]))
+        chroma = int(rng.integers(0, 2))
+        mult_w = hd["paving"] * 16 * (2 if ch == 3 and chroma == 1 else 1)
+        mult_h = vd["paving"] * (2 if ch == 3 and chroma == 1 else 1)
+        W = mult_w * int(rng.integers(1, max(2, 200 // mult_w + 1)))
+        H = mult_h * int(rng.integers(1, max(2, 60 // mult_h + 1)))
+        spec = ds.make_spec(h=hd, v=vd, chroma=chroma)
+        d = ds.Downscaler(W, H, ch, spec=spec)
+        if not d.plan.fused_general_eligible:
+            continue
+        fr = synth.random_frames(trial, 0, 2, W, H, ch, chroma)
+        want = oracle.execute_frames(fr, W, H, ch, chroma, _oracle_stage(hd), _oracle_stage(vd))
+        got = _run(d, fr, ds.DS_KERNEL_FUSED_GENERAL)
+        assert d.last_kernel() == ds.DS_KERNEL_FUSED_GENERAL
+        _assert_same(got, want, f"fuzz {trial}: {W}x{H}x{ch} h={hd} v={vd}")
+        checked += 1
+    assert checked >= 25
 
 
 # ------------------------------------------------------- alignment / API --

@@ -1,0 +1,82 @@
+#!/usr/bin/env python
+"""SURVEY f3 measurement: K-N1g (fused band kernel, any spec) on the HD
+stream, against K-N2 (per-pixel literal kernel) on the same spec, and against
+K-N1 on SPEC's own taps.
+
+    python tools/general_perf.py [--out gpurun_out/general_perf.json]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch
+
+import paper_1103_4881_b200 as ds
+
+# a longer Array-OL downscaler reading: 13-tap H / 14-tap V windows
+HALO_H = dict(pattern=13, paving=8, origin=-2,
+              weights=[[1, 3, 5, 3, 1, 0, 0, 0, 0, 0, 0, 0, 0], [0, 0, 0, 1, 3, 5, 3, 1],
+                       [0, 0, 0, 0, 0, 0, 1, 3, 5, 3, 1]], divisor=13, bias=6)
+HALO_V = dict(pattern=14, paving=9, origin=-2,
+              weights=[[1, 2, 4, 2, 1], [0, 0, 1, 2, 4, 2, 1], [0, 0, 0, 0, 0, 1, 2, 4, 2, 1],
+                       [0, 0, 0, 0, 0, 0, 0, 0, 1, 2, 4, 2, 1]], divisor=10, bias=5)
+
+
+def timed(fn, steps):
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(steps):
+        fn()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / steps
+
+
+def run(W, H, n, spec, kernels, steps=20):
+    d = ds.Downscaler(W, H, 3, spec=spec)
+    x = ds.generate_frames(n, d.in_frame_bytes, seed=1)
+    outs, res = {}, {}
+    for k in kernels:
+        d.set_kernel(k)
+        y = d.alloc_out(n)
+        ms = timed(lambda: d(x, y), steps if k != ds.DS_KERNEL_GENERIC else 3)
+        assert d.last_kernel() == k
+        outs[k] = y
+        fb = n * (d.in_frame_bytes + d.out_frame_bytes)
+        res[ds.KERNEL_NAMES[k]] = {"ms": ms, "fps": n / ms * 1e3, "in_plus_out_gbs": fb / ms / 1e6}
+    ref = outs[kernels[0]]
+    res["all_kernels_bit_identical"] = all(torch.equal(ref, o) for o in outs.values())
+    p = d.plan
+    res["k1g_bands"] = list(p.general_band_reps)
+    res["k1g_staged_bytes_max"] = p.general_stage_bytes_max
+    return res
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--out", default="gpurun_out/general_perf.json")
+    a = ap.parse_args()
+    torch.cuda.set_device(0)
+    halo = ds.make_spec(h=HALO_H, v=HALO_V)
+    out = {
+        "halo_spec": {"h": HALO_H, "v": HALO_V},
+        "hd420_300_halo_spec": run(1920, 1080, 300, halo,
+                                   [ds.DS_KERNEL_FUSED_GENERAL, ds.DS_KERNEL_GENERIC]),
+        "hd420_300_spec_taps": run(1920, 1080, 300, None,
+                                   [ds.DS_KERNEL_FUSED, ds.DS_KERNEL_FUSED_GENERAL]),
+    }
+    os.makedirs(os.path.dirname(a.out) or ".", exist_ok=True)
+    json.dump(out, open(a.out, "w"), indent=1)
+    print(json.dumps(out, indent=1))
+
+
+if __name__ == "__main__":
+    main()
