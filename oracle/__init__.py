@@ -86,6 +86,7 @@ def lib():
         L.orc_default_stages.restype = None
         L.orc_execute_plane.argtypes = [P8, C.c_int32, C.c_int32, PS, PS, P8, C.c_int32]
         L.orc_execute_plane_mid.argtypes = [P8, C.c_int32, C.c_int32, PS, PS, P8, P8, C.c_int32]
+        L.orc_run_task.argtypes = [P8, PT, P8, PT, C.c_int32, P64, PS, C.c_int32]
         L.orc_plane_dims.argtypes = [C.c_int32] * 5 + [C.POINTER(C.c_int32)] * 2
         L.orc_execute_frames.argtypes = [P8, C.c_int64, C.c_int32, C.c_int32, C.c_int32,
                                          C.c_int32, PS, PS, P8]
@@ -167,6 +168,18 @@ def check_coverage(t: Tiler, rep_shape, max_wit: int = 10):
                                   C.byref(nw))
     _check(rc, "check_coverage")
     return ("exact", "overlaps", "gaps")[rc], [wit[i] for i in range(nw.value)]
+
+
+def run_task(arr_in: np.ndarray, tin: Tiler, out_shape, tout: Tiler, rep_shape, body,
+             order: int = 0, out_init: np.ndarray | None = None) -> np.ndarray:
+    """A general repetitive task executed as S:517-520; body is a
+    Stage whose pattern = input pattern elements, outputs = output pattern
+    elements.  Elements of out not covered by tout keep out_init (zeros)."""
+    a = np.ascontiguousarray(arr_in, dtype=np.uint8)
+    out = np.zeros(out_shape, np.uint8) if out_init is None else np.ascontiguousarray(out_init).copy()
+    _check(lib().orc_run_task(_p8(a), C.byref(tin), _p8(out), C.byref(tout), len(rep_shape),
+                              _p64(rep_shape), C.byref(body), order), "run_task")
+    return out
 
 
 # ---------------------------------------------------------------- stages --

@@ -303,6 +303,36 @@ int orc_execute_plane_mid(const uint8_t* in, int32_t W, int32_t H,
     return ORC_OK;
 }
 
+/* A general repetitive task (executed as S:517-520): for every
+ * repetition index r of rep_shape (row-major, or reverse when order = 1),
+ * pattern = extract(in, tin, r); out pattern = body(pattern); write(out,
+ * tout, r).  The body is the linear integer stage over the row-major
+ * flattened input pattern (body->pattern elements), producing
+ * body->outputs elements in the output pattern's row-major order. */
+int orc_run_task(const uint8_t* in, const orc_tiler* tin, uint8_t* out,
+                 const orc_tiler* tout, int32_t nrep, const int64_t* rep_shape,
+                 const orc_stage* body, int32_t order) {
+    if (!in || !out || !tiler_ok(tin) || !tiler_ok(tout) || !rep_shape || !body) return ORC_EINVAL;
+    if (nrep != tin->nrep || nrep != tout->nrep) return ORC_EINVAL;
+    if (pattern_size(tin) != body->pattern || pattern_size(tout) != body->outputs) return ORC_EINVAL;
+    if (body->pattern > ORC_MAXPAT || body->outputs > ORC_MAXOUT || body->divisor < 1) return ORC_EINVAL;
+    int64_t nr = 1;
+    for (int j = 0; j < nrep; ++j) {
+        if (rep_shape[j] < 1) return ORC_EINVAL;
+        nr *= rep_shape[j];
+    }
+    uint8_t pat[ORC_MAXPAT], res[ORC_MAXOUT];
+    for (int64_t q = 0; q < nr; ++q) {
+        int64_t lin = order ? (nr - 1 - q) : q;
+        int64_t r[ORC_MAXDIM] = {0};
+        for (int j = nrep - 1; j >= 0; --j) { r[j] = lin % rep_shape[j]; lin /= rep_shape[j]; }
+        orc_extract_pattern(in, tin, r, pat);
+        orc_stage_apply(body, pat, res);
+        orc_write_pattern(out, tout, r, res);
+    }
+    return ORC_OK;
+}
+
 /* Plane layout of a frame: Y then plane 1 then plane 2, row-major u8, no
  * headers; 4:2:0 chroma is (W/2, H/2) (SPEC default), 4:4:4
  * is three equal planes (the paper's "24-bit RGB"). */

@@ -94,6 +94,11 @@ int orc_execute_plane_mid(const uint8_t* in, int32_t W, int32_t H,
                           const orc_stage* h, const orc_stage* v,
                           uint8_t* mid_out, uint8_t* out, int32_t order);
 
+/* ---- a general repetitive task with arbitrary tilers */
+int orc_run_task(const uint8_t* in, const orc_tiler* tin, uint8_t* out,
+                 const orc_tiler* tout, int32_t nrep, const int64_t* rep_shape,
+                 const orc_stage* body, int32_t order);
+
 /* ---- whole frames: planes Y, plane 1, plane 2 contiguous --------
  * chroma: 0 = 4:4:4 (three equal planes), 1 = 4:2:0 (W/2 x H/2 chroma).  */
 int orc_plane_dims(int32_t W, int32_t H, int32_t channels, int32_t chroma,

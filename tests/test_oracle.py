@@ -506,3 +506,46 @@ def test_mid_array_is_the_h_task_output():
                      for row in plane], np.uint8)
     assert (mid == want).all()
     assert (out == oracle.execute_plane(plane)).all()
+
+
+# ------------------------------------------------- general tasks (row f4) --
+def _identity_body(n):
+    return oracle.make_stage(n, n, 0, [[1 if i == k else 0 for i in range(n)] for k in range(n)], 1, 0)
+
+
+def test_run_task_identity_model():
+    # S:525 "identity model (pass-through body, identity tilers) -> output equals input"
+    rng = np.random.default_rng(4)
+    a = rng.integers(0, 256, (6, 10)).astype(np.uint8)
+    t = oracle.make_tiler((6, 10), (0, 0), [[1, 0], [0, 1]], [[], []], [])
+    out = oracle.run_task(a, t, (6, 10), t, (6, 10), _identity_body(1))
+    assert (out == a).all()
+
+
+def test_run_task_transpose_and_blocks_match_numpy():
+    """Tilers that realise np.transpose and a 2x3-block regrouping (library
+    routines), with a 2x3 pattern and a pass-through body."""
+    rng = np.random.default_rng(5)
+    a = rng.integers(0, 256, (4, 6)).astype(np.uint8)
+    # transpose: out[c][r] = in[r][c]; rep (r, c); in paving identity, out paving swapped
+    tin = oracle.make_tiler((4, 6), (0, 0), [[1, 0], [0, 1]], [[], []], [])
+    tout = oracle.make_tiler((6, 4), (0, 0), [[0, 1], [1, 0]], [[], []], [])
+    assert (oracle.run_task(a, tin, (6, 4), tout, (4, 6), _identity_body(1)) == a.T).all()
+    # blocks: rep (bi, bj) over (2, 2); pattern 2x3 from in; written as row bi*2+bj of a (4, 6) array
+    tin = oracle.make_tiler((4, 6), (0, 0), [[2, 0], [0, 3]], [[1, 0], [0, 1]], [2, 3])
+    tout = oracle.make_tiler((4, 6), (0, 0), [[2, 1], [0, 0]], [[0], [1]], [6])
+    got = oracle.run_task(a, tin, (4, 6), tout, (2, 2), _identity_body(6))
+    want = a.reshape(2, 2, 2, 3).transpose(0, 2, 1, 3).reshape(4, 6)
+    assert (got == want).all()
+
+
+def test_run_task_reproduces_the_downscaler_h_task():
+    """The downscaler's yhfk task through the general executor equals
+    the Mid array of O1 and SPEC's literal hfilter_8to3."""
+    plane = synth.random_frames(2, 0, 1, 352, 288, 1)[0].reshape(288, 352)
+    h, v = oracle.default_stages()
+    tin = oracle.make_tiler((288, 352), (0, 0), [[1, 0], [0, 8]], [[0], [1]], [8])
+    tout = oracle.make_tiler((288, 132), (0, 0), [[1, 0], [0, 3]], [[0], [1]], [3])
+    mid = oracle.run_task(plane, tin, (288, 132), tout, (288, 44), h)
+    assert (mid == oracle.execute_plane_mid(plane)[0]).all()
+    assert (mid[5, 6:9] == oracle.hfilter_8to3(plane[5, 16:24])).all()
