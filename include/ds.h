@@ -280,6 +280,82 @@ DS_API int ds_run_schedule(ds_handle* h, const uint8_t* host_in, int64_t n_frame
                            uint8_t* host_out, int32_t schedule, ds_schedule_stats* stats,
                            ds_stream_t stream);
 
+/* ---- general Array-OL repetitive tasks --------------------------
+ *
+ * A tiler: element_index(r, f) = (origin + paving.r + fitting.f)
+ * mod shape, component-wise, non-negative modulo.  paving is
+ * array dims x repetition dims, fitting array dims x pattern dims (row-major
+ * [array dim][k]).  Limits: 1..4 array dims, 1..4 repetition dims, 0..4
+ * pattern dims; every extent >= 1; product(shape) <= 2^32; repetition
+ * extents < 2^31; origin/paving/fitting entries |x| <= 2^40. */
+typedef struct {
+    int32_t ndim;
+    int64_t shape[4];
+    int64_t origin[4];
+    int32_t nrep;
+    int64_t paving[4][4];
+    int32_t npat;
+    int64_t fitting[4][4];
+    int64_t pattern[4];
+} ds_tiler;
+
+/* Elementary function of a task: a linear integer body over the
+ * row-major flattened input pattern (n_in <= 16 elements) producing n_out
+ * <= 8 elements in the output pattern's row-major order:
+ * out[k] = clamp_0^255(trunc((sum_i weight[k][i] * in[i] + bias) / divisor))
+ * (the form of S:530/S:540; limits as ds_stage_spec). */
+typedef struct {
+    int32_t n_in, n_out;
+    int32_t weight[DS_MAX_OUTPUTS][DS_MAX_PATTERN];
+    int32_t divisor, bias;
+} ds_task_body;
+
+/* Launch topology (rule S:349-357; the paper's lost Fig. 3,
+ * P:122-130): collapse dimensions beyond max_dims by multiplying trailing
+ * extents; below min_items one work-group sized to the multiplicity;
+ * otherwise a power-of-two local box, product <= min(max_wg, wg_threshold),
+ * grown one dimension at a time round-robin from the largest dimension while
+ * the padded global size stays < 2 x the multiplicity; global[d] = smallest
+ * multiple of local[d] >= multiplicity[d]; guarded iff padded. */
+typedef struct {
+    int32_t ndim;                 /* collapsed dims, 1..3            */
+    int64_t multiplicity[3];      /* collapsed repetition extents    */
+    int32_t local[3];
+    int64_t global[3];
+    int32_t guarded;
+} ds_topology;
+
+enum { DS_TOPO_FLAT = 0, DS_TOPO_SPEC = 1 };
+
+/* Host-only.  max_wg = device max work-group size (0 -> DS_EINVAL);
+ * max_dims 1..3; min_items default 64 and wg_threshold default 256. */
+DS_API int ds_compute_topology(int32_t nrep, const int64_t* multiplicity, int32_t max_wg,
+                               int32_t max_dims, int32_t min_items, int32_t wg_threshold,
+                               ds_topology* out);
+
+/* Run one repetitive task on the current device (S:72-77 executed as
+ * S:517-520): for every repetition index r of rep_shape, pattern =
+ * extract(in, t_in, r); write(out, t_out, r, body(pattern)).  in / out are
+ * device arrays of product(t_in.shape) / product(t_out.shape) bytes,
+ * caller-owned, non-overlapping; elements not covered by t_out are left
+ * untouched.  Repetitions run in parallel: if t_out is not an exact
+ * cover (ds_tiler_coverage) multiply-written elements are unspecified.
+ * policy DS_TOPO_FLAT: grid-stride over repetitions; DS_TOPO_SPEC: the
+ * ds_compute_topology launch (B200 limits), guarded.  Asynchronous on
+ * `stream`.  Returns DS_OK, DS_EINVAL (bad tiler/body/pointers),
+ * DS_EUNSUPPORTED (over the limits) or DS_ECUDA. */
+DS_API int ds_run_task(const uint8_t* in, const ds_tiler* t_in, uint8_t* out, const ds_tiler* t_out,
+                       int32_t nrep, const int64_t* rep_shape, const ds_task_body* body,
+                       int32_t policy, ds_stream_t stream);
+
+/* check_coverage on the device: count, for every element of
+ * t's array, the (r, f) pairs that hit it; *overlaps = elements hit more
+ * than once, *gaps = elements never hit (exact iff both are 0).
+ * SYNCHRONOUS on `stream`; allocates a temporary 4-byte counter per
+ * element.  Returns as ds_run_task, plus DS_ENOMEM. */
+DS_API int ds_tiler_coverage(const ds_tiler* t, int32_t nrep, const int64_t* rep_shape,
+                             int64_t* overlaps, int64_t* gaps, ds_stream_t stream);
+
 /* Synthetic input (bench / test infrastructure, not part of the method):
  * fills dev[0 .. n_bytes) on the current device with
  *   byte(i) = splitmix64(seed * 0x9E3779B97F4A7C15 + start_index + i) >> 56

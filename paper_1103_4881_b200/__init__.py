@@ -86,6 +86,46 @@ class ds_schedule_stats(C.Structure):
         return d
 
 
+class ds_tiler(C.Structure):
+    _fields_ = [
+        ("ndim", C.c_int32),
+        ("shape", C.c_int64 * 4),
+        ("origin", C.c_int64 * 4),
+        ("nrep", C.c_int32),
+        ("paving", (C.c_int64 * 4) * 4),
+        ("npat", C.c_int32),
+        ("fitting", (C.c_int64 * 4) * 4),
+        ("pattern", C.c_int64 * 4),
+    ]
+
+
+class ds_task_body(C.Structure):
+    _fields_ = [
+        ("n_in", C.c_int32),
+        ("n_out", C.c_int32),
+        ("weight", (C.c_int32 * DS_MAX_PATTERN) * DS_MAX_OUTPUTS),
+        ("divisor", C.c_int32),
+        ("bias", C.c_int32),
+    ]
+
+
+class ds_topology(C.Structure):
+    _fields_ = [
+        ("ndim", C.c_int32),
+        ("multiplicity", C.c_int64 * 3),
+        ("local", C.c_int32 * 3),
+        ("global_", C.c_int64 * 3),
+        ("guarded", C.c_int32),
+    ]
+
+    def as_dict(self):
+        n = self.ndim
+        return dict(multiplicity=list(self.multiplicity[:n]), local=list(self.local[:n]),
+                    global_=list(self.global_[:n]), guarded=bool(self.guarded))
+
+
+DS_TOPO_FLAT, DS_TOPO_SPEC = 0, 1
+
 DS_SCHED_NAIVE, DS_SCHED_OPTIMIZED, DS_SCHED_FUSED, DS_SCHED_STREAMED = 0, 1, 2, 3
 SCHED_NAMES = {DS_SCHED_NAIVE: "naive", DS_SCHED_OPTIMIZED: "optimized", DS_SCHED_FUSED: "fused",
                DS_SCHED_STREAMED: "streamed"}
@@ -132,6 +172,12 @@ SIGNATURES = [
                                    C.c_int32, C.POINTER(ds_schedule_stats)]),
     ("ds_run_schedule", C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int32,
                                   C.POINTER(ds_schedule_stats), C.c_void_p]),
+    ("ds_compute_topology", C.c_int, [C.c_int32, C.POINTER(C.c_int64), C.c_int32, C.c_int32, C.c_int32,
+                                      C.c_int32, C.POINTER(ds_topology)]),
+    ("ds_run_task", C.c_int, [C.c_void_p, C.POINTER(ds_tiler), C.c_void_p, C.POINTER(ds_tiler), C.c_int32,
+                              C.POINTER(C.c_int64), C.POINTER(ds_task_body), C.c_int32, C.c_void_p]),
+    ("ds_tiler_coverage", C.c_int, [C.POINTER(ds_tiler), C.c_int32, C.POINTER(C.c_int64),
+                                    C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.c_void_p]),
     ("ds_generate", C.c_int, [C.c_void_p, C.c_int64, C.c_uint64, C.c_int64, C.c_void_p]),
 ]
 
@@ -256,6 +302,78 @@ def ds_generate(dev_ptr: int, n_bytes: int, seed: int, start_index: int, stream:
     rc = lib().ds_generate(dev_ptr, n_bytes, seed, start_index, stream or None)
     if rc:
         raise DSError(rc, "ds_generate")
+
+
+# ------------------------------------------------- general tasks --
+def make_tiler(shape, origin, paving, fitting, pattern) -> ds_tiler:
+    """Array-OL tiler: paving is array dims x repetition dims,
+    fitting array dims x pattern dims, pattern the pattern shape."""
+    t = ds_tiler()
+    t.ndim = len(shape)
+    for d, x in enumerate(shape):
+        t.shape[d] = x
+        t.origin[d] = origin[d]
+    t.nrep = len(paving[0]) if len(paving) else 0
+    t.npat = len(pattern)
+    for d in range(len(shape)):
+        for j in range(t.nrep):
+            t.paving[d][j] = paving[d][j]
+        for k in range(t.npat):
+            t.fitting[d][k] = fitting[d][k]
+    for k, x in enumerate(pattern):
+        t.pattern[k] = x
+    return t
+
+
+def make_body(weights, divisor=1, bias=0, n_in=None) -> ds_task_body:
+    b = ds_task_body()
+    b.n_out = len(weights)
+    b.n_in = n_in if n_in is not None else max(len(r) for r in weights)
+    for k, row in enumerate(weights):
+        for i, w in enumerate(row):
+            b.weight[k][i] = int(w)
+    b.divisor, b.bias = divisor, bias
+    return b
+
+
+def _i64(seq):
+    return (C.c_int64 * max(1, len(seq)))(*[int(x) for x in seq])
+
+
+def ds_compute_topology(multiplicity, max_wg=1024, max_dims=3, min_items=64, wg_threshold=256) -> dict:
+    t = ds_topology()
+    rc = lib().ds_compute_topology(len(multiplicity), _i64(multiplicity), max_wg, max_dims, min_items,
+                                   wg_threshold, C.byref(t))
+    if rc:
+        raise DSError(rc, "ds_compute_topology")
+    return t.as_dict()
+
+
+def run_task(x, t_in: ds_tiler, out, t_out: ds_tiler, rep_shape, body: ds_task_body,
+             policy: int = DS_TOPO_FLAT, stream=None):
+    """One repetitive task on torch uint8 CUDA tensors x -> out (in place)."""
+    import torch
+
+    s = stream if stream is not None else torch.cuda.current_stream()
+    rc = lib().ds_run_task(x.data_ptr(), C.byref(t_in), out.data_ptr(), C.byref(t_out), len(rep_shape),
+                           _i64(rep_shape), C.byref(body), policy, s.cuda_stream)
+    if rc:
+        raise DSError(rc, "ds_run_task")
+    return out
+
+
+def tiler_coverage(t: ds_tiler, rep_shape, stream=None):
+    """("exact"|"overlaps"|"gaps", n_overlapping_elements, n_gap_elements), on the device."""
+    import torch
+
+    s = stream if stream is not None else torch.cuda.current_stream()
+    ov, gp = C.c_int64(), C.c_int64()
+    rc = lib().ds_tiler_coverage(C.byref(t), len(rep_shape), _i64(rep_shape), C.byref(ov), C.byref(gp),
+                                 s.cuda_stream)
+    if rc:
+        raise DSError(rc, "ds_tiler_coverage")
+    kind = "overlaps" if ov.value else ("gaps" if gp.value else "exact")
+    return kind, ov.value, gp.value
 
 
 # ------------------------------------------------------------ torch facade --

@@ -1,0 +1,391 @@
+// ds_tiler.cu -- SURVEY f4: a general Array-OL repetitive task on sm_100a
+// (arbitrary <= 4-D origin / paving / fitting tilers), SPEC's launch
+// topology rule as an optional launch policy, and check_coverage
+// on the device.  Citations: P:n = PAPER.md line n, S:n = SPEC.md
+// line n.
+//
+// Element indices follow S:248-252 exactly: (origin + paving.r + fitting.f)
+// mod shape with the non-negative modulo.  The host reduces origin, paving
+// columns and the per-pattern-element fitting offsets modulo the shape once;
+// a thread then needs, per array dim, one product-sum and one modulo per
+// repetition plus one conditional subtraction per pattern element.
+#include <algorithm>
+#include <climits>
+#include <cstring>
+
+#include "ds.h"
+#include "ds_internal.h"
+
+namespace {
+
+struct TTiler {
+    int32_t ndim, npe;                 // array dims, pattern elements
+    int64_t shape[4];
+    int64_t stride[4];                 // row-major element strides
+    int64_t origin[4];                 // reduced mod shape
+    int64_t pav[4][4];                 // [array dim][rep dim], reduced mod shape
+    int64_t foff[DS_MAX_PATTERN][4];   // fitting . f for each pattern element, reduced mod shape
+};
+
+struct TaskParams {
+    const uint8_t* in;
+    uint8_t* out;
+    int64_t n_reps;
+    int32_t nrep;
+    int32_t policy;
+    int64_t rep[4];
+    TTiler tin, tout;
+    int32_t n_in, n_out, divisor, bias;
+    int32_t w[DS_MAX_OUTPUTS][DS_MAX_PATTERN];
+    // DS_TOPO_SPEC: collapsed multiplicity (row-major, last fastest -> CUDA x)
+    int32_t tdim;
+    int64_t tmult[3];
+};
+
+__device__ __forceinline__ int64_t t_mod(int64_t a, int64_t m) {
+    const int64_t r = a % m;
+    return r < 0 ? r + m : r;
+}
+
+// Base index (origin + paving.r) mod shape for every array dim.
+__device__ __forceinline__ void t_base(const TTiler& t, int nrep, const int64_t* r, int64_t* base) {
+    for (int d = 0; d < t.ndim; ++d) {
+        int64_t v = t.origin[d];
+        for (int j = 0; j < nrep; ++j) v += (t.pav[d][j] * r[j]) % t.shape[d];
+        base[d] = t_mod(v, t.shape[d]);
+    }
+}
+
+__device__ __forceinline__ int64_t t_lin(const TTiler& t, const int64_t* base, int f) {
+    int64_t off = 0;
+    for (int d = 0; d < t.ndim; ++d) {
+        int64_t i = base[d] + t.foff[f][d];
+        if (i >= t.shape[d]) i -= t.shape[d];
+        off += i * t.stride[d];
+    }
+    return off;
+}
+
+__device__ __forceinline__ void t_unravel(int64_t q, int nrep, const int64_t* rep, int64_t* r) {
+    for (int j = nrep - 1; j >= 0; --j) {
+        r[j] = q % rep[j];
+        q /= rep[j];
+    }
+}
+
+__device__ __forceinline__ void task_one(const TaskParams& p, int64_t q) {
+    int64_t r[4] = {0, 0, 0, 0}, base[4];
+    t_unravel(q, p.nrep, p.rep, r);
+    uint8_t pat[DS_MAX_PATTERN];
+    t_base(p.tin, p.nrep, r, base);
+    for (int f = 0; f < p.n_in; ++f) pat[f] = __ldg(p.in + t_lin(p.tin, base, f));
+    t_base(p.tout, p.nrep, r, base);
+    for (int k = 0; k < p.n_out; ++k) {
+        int32_t acc = p.bias;
+        for (int f = 0; f < p.n_in; ++f) acc += p.w[k][f] * (int32_t)pat[f];
+        int32_t v = acc / p.divisor;                      // truncation toward zero
+        v = v < 0 ? 0 : (v > 255 ? 255 : v);
+        p.out[t_lin(p.tout, base, k)] = (uint8_t)v;
+    }
+}
+
+__global__ void __launch_bounds__(256) ds_task_kernel(const __grid_constant__ TaskParams p) {
+    if (p.policy == DS_TOPO_SPEC) {
+        // NDRange work-item = one elementary task; guarded padding
+        const int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+        const int64_t y = (int64_t)blockIdx.y * blockDim.y + threadIdx.y;
+        const int64_t z = (int64_t)blockIdx.z * blockDim.z + threadIdx.z;
+        int64_t c[3] = {0, 0, 0};
+        if (p.tdim == 1) { c[0] = x; }
+        else if (p.tdim == 2) { c[0] = y; c[1] = x; }
+        else { c[0] = z; c[1] = y; c[2] = x; }
+        int64_t q = 0;
+        for (int d = 0; d < p.tdim; ++d) {
+            if (c[d] >= p.tmult[d]) return;               // guard
+            q = q * p.tmult[d] + c[d];
+        }
+        task_one(p, q);
+        return;
+    }
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < p.n_reps; q += stride)
+        task_one(p, q);
+}
+
+__global__ void __launch_bounds__(256) ds_cover_count_kernel(const __grid_constant__ TaskParams p,
+                                                             uint32_t* count) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < p.n_reps; q += stride) {
+        int64_t r[4] = {0, 0, 0, 0}, base[4];
+        t_unravel(q, p.nrep, p.rep, r);
+        t_base(p.tout, p.nrep, r, base);
+        for (int k = 0; k < p.tout.npe; ++k) atomicAdd(count + t_lin(p.tout, base, k), 1u);
+    }
+}
+
+__global__ void __launch_bounds__(256) ds_cover_reduce_kernel(const uint32_t* count, int64_t n,
+                                                              unsigned long long* res) {
+    unsigned long long over = 0, gap = 0;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const uint32_t c = count[i];
+        over += c > 1;
+        gap += c == 0;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        over += __shfl_xor_sync(0xffffffffu, over, o);
+        gap += __shfl_xor_sync(0xffffffffu, gap, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (over) atomicAdd(res, over);
+        if (gap) atomicAdd(res + 1, gap);
+    }
+}
+
+int64_t h_mod(int64_t a, int64_t m) {
+    const int64_t r = a % m;
+    return r < 0 ? r + m : r;
+}
+
+int64_t pattern_elems(const ds_tiler& t) {
+    int64_t n = 1;
+    for (int k = 0; k < t.npat; ++k) n *= t.pattern[k];
+    return n;
+}
+
+// Validate a tiler against the limits of include/ds.h and reduce it.
+int prep_tiler(const ds_tiler& t, int32_t nrep, TTiler* o, int64_t* elems) {
+    if (t.ndim < 1 || t.ndim > 4 || t.nrep != nrep || t.npat < 0 || t.npat > 4) return DS_EINVAL;
+    const int64_t lim = 1LL << 40;
+    int64_t n = 1;
+    for (int d = 0; d < t.ndim; ++d) {
+        if (t.shape[d] < 1) return DS_EINVAL;
+        if (t.shape[d] > (1LL << 32) || n > (1LL << 32) / t.shape[d]) return DS_EUNSUPPORTED;
+        n *= t.shape[d];
+        if (t.origin[d] < -lim || t.origin[d] > lim) return DS_EUNSUPPORTED;
+        for (int j = 0; j < nrep; ++j)
+            if (t.paving[d][j] < -lim || t.paving[d][j] > lim) return DS_EUNSUPPORTED;
+        for (int k = 0; k < t.npat; ++k)
+            if (t.fitting[d][k] < -lim || t.fitting[d][k] > lim) return DS_EUNSUPPORTED;
+    }
+    for (int k = 0; k < t.npat; ++k)
+        if (t.pattern[k] < 1) return DS_EINVAL;
+    const int64_t npe = pattern_elems(t);
+    if (npe > DS_MAX_PATTERN) return DS_EUNSUPPORTED;
+    std::memset(o, 0, sizeof *o);
+    o->ndim = t.ndim;
+    o->npe = (int32_t)npe;
+    int64_t st = 1;
+    for (int d = t.ndim - 1; d >= 0; --d) {
+        o->shape[d] = t.shape[d];
+        o->stride[d] = st;
+        st *= t.shape[d];
+        o->origin[d] = h_mod(t.origin[d], t.shape[d]);
+        for (int j = 0; j < nrep; ++j) o->pav[d][j] = h_mod(t.paving[d][j], t.shape[d]);
+    }
+    for (int64_t e = 0; e < npe; ++e) {
+        int64_t f[4] = {0, 0, 0, 0}, rem = e;
+        for (int k = t.npat - 1; k >= 0; --k) { f[k] = rem % t.pattern[k]; rem /= t.pattern[k]; }
+        for (int d = 0; d < t.ndim; ++d) {
+            int64_t v = 0;
+            for (int k = 0; k < t.npat; ++k) v += h_mod(t.fitting[d][k], t.shape[d]) * f[k];
+            o->foff[e][d] = h_mod(v, t.shape[d]);
+        }
+    }
+    *elems = n;
+    return DS_OK;
+}
+
+int prep_reps(int32_t nrep, const int64_t* rep, TaskParams* p) {
+    if (nrep < 1 || nrep > 4 || !rep) return DS_EINVAL;
+    int64_t n = 1;
+    for (int j = 0; j < nrep; ++j) {
+        if (rep[j] < 1) return DS_EINVAL;
+        if (rep[j] >= (1LL << 31) || n > LLONG_MAX / rep[j]) return DS_EUNSUPPORTED;
+        n *= rep[j];
+        p->rep[j] = rep[j];
+    }
+    p->nrep = nrep;
+    p->n_reps = n;
+    return DS_OK;
+}
+
+int64_t next_pow2(int64_t x) {
+    int64_t p = 1;
+    while (p < x) p <<= 1;
+    return p;
+}
+
+}  // namespace
+
+extern "C" {
+
+DS_API int ds_compute_topology(int32_t nrep, const int64_t* mult, int32_t max_wg, int32_t max_dims,
+                               int32_t min_items, int32_t wg_threshold, ds_topology* out) {
+    if (!out || !mult || nrep < 1 || nrep > 4 || max_wg < 1 || max_dims < 1 || max_dims > 3 ||
+        min_items < 0 || wg_threshold < 1)
+        return DS_EINVAL;
+    for (int j = 0; j < nrep; ++j)
+        if (mult[j] < 1) return DS_EINVAL;
+    ds_topology t;
+    std::memset(&t, 0, sizeof t);
+    // (1) collapse dimensions beyond max_dims by multiplying trailing extents
+    t.ndim = std::min(nrep, max_dims);
+    for (int d = 0; d < t.ndim; ++d) t.multiplicity[d] = mult[d];
+    for (int j = t.ndim; j < nrep; ++j) t.multiplicity[t.ndim - 1] *= mult[j];
+    int64_t total = 1;
+    for (int d = 0; d < t.ndim; ++d) total *= t.multiplicity[d];
+    const int64_t cap_raw = std::min<int64_t>(max_wg, wg_threshold);
+    int64_t cap = 1;
+    while (cap * 2 <= cap_raw) cap *= 2;
+    if (total < min_items && total <= cap_raw) {
+        // (2) small multiplicity: one work-group sized to it
+        for (int d = 0; d < t.ndim; ++d) {
+            t.local[d] = (int32_t)t.multiplicity[d];
+            t.global[d] = t.multiplicity[d];
+        }
+        t.guarded = 0;
+        *out = t;
+        return DS_OK;
+    }
+    // (3) power-of-two box, round-robin from the largest dimension, keeping
+    // the padded size < 2 x multiplicity (the padding bound of S:651)
+    int order[3] = {0, 1, 2};
+    std::stable_sort(order, order + t.ndim,
+                     [&](int a, int b) { return t.multiplicity[a] > t.multiplicity[b]; });
+    int64_t loc[3] = {1, 1, 1};
+    bool frozen[3] = {false, false, false};
+    int64_t prod = 1;
+    bool progress = true;
+    while (progress && prod * 2 <= cap) {
+        progress = false;
+        for (int oi = 0; oi < t.ndim && prod * 2 <= cap; ++oi) {
+            const int d = order[oi];
+            if (frozen[d]) continue;
+            const int64_t cand = loc[d] * 2;
+            if (cand > next_pow2(t.multiplicity[d])) { frozen[d] = true; continue; }
+            int64_t padded = 1;
+            for (int e = 0; e < t.ndim; ++e) {
+                const int64_t l = e == d ? cand : loc[e];
+                padded *= (t.multiplicity[e] + l - 1) / l * l;
+            }
+            if (padded >= 2 * total) { frozen[d] = true; continue; }
+            loc[d] = cand;
+            prod *= 2;
+            progress = true;
+        }
+    }
+    // (4) global = smallest multiple of local >= multiplicity
+    t.guarded = 0;
+    for (int d = 0; d < t.ndim; ++d) {
+        t.local[d] = (int32_t)loc[d];
+        t.global[d] = (t.multiplicity[d] + loc[d] - 1) / loc[d] * loc[d];
+        if (t.global[d] != t.multiplicity[d]) t.guarded = 1;
+    }
+    *out = t;
+    return DS_OK;
+}
+
+DS_API int ds_run_task(const uint8_t* in, const ds_tiler* t_in, uint8_t* out, const ds_tiler* t_out,
+                       int32_t nrep, const int64_t* rep_shape, const ds_task_body* body,
+                       int32_t policy, ds_stream_t stream) {
+    if (!in || !out || !t_in || !t_out || !body) return DS_EINVAL;
+    if (policy != DS_TOPO_FLAT && policy != DS_TOPO_SPEC) return DS_EINVAL;
+    TaskParams p;
+    std::memset(&p, 0, sizeof p);
+    int rc = prep_reps(nrep, rep_shape, &p);
+    if (rc) return rc;
+    int64_t nin = 0, nout = 0;
+    if ((rc = prep_tiler(*t_in, nrep, &p.tin, &nin))) return rc;
+    if ((rc = prep_tiler(*t_out, nrep, &p.tout, &nout))) return rc;
+    if (body->n_in != p.tin.npe || body->n_out != p.tout.npe || body->n_out > DS_MAX_OUTPUTS ||
+        body->divisor < 1)
+        return DS_EINVAL;
+    if (body->divisor > (1 << 24) || body->bias < -(1 << 24) || body->bias > (1 << 24))
+        return DS_EUNSUPPORTED;
+    for (int k = 0; k < DS_MAX_OUTPUTS; ++k)
+        for (int i = 0; i < DS_MAX_PATTERN; ++i)
+            if (body->weight[k][i] < -65535 || body->weight[k][i] > 65535) return DS_EUNSUPPORTED;
+    if (dsi::ranges_overlap(in, nin, out, nout)) return DS_EINVAL;
+    int dev = 0, sms = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+        cudaGetLastError();
+        return DS_ECUDA;
+    }
+    if (!dsi::device_ptr_on(in, dev) || !dsi::device_ptr_on(out, dev)) return DS_EINVAL;
+    p.in = in;
+    p.out = out;
+    p.policy = policy;
+    p.n_in = body->n_in;
+    p.n_out = body->n_out;
+    p.divisor = body->divisor;
+    p.bias = body->bias;
+    std::memcpy(p.w, body->weight, sizeof p.w);
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if (policy == DS_TOPO_SPEC) {
+        ds_topology topo;
+        if ((rc = ds_compute_topology(nrep, rep_shape, 1024, 3, 64, 256, &topo))) return rc;
+        p.tdim = topo.ndim;
+        dim3 block(1, 1, 1), grid(1, 1, 1);
+        const int64_t lim[3] = {2147483647LL, 65535LL, 65535LL};
+        for (int d = 0; d < topo.ndim; ++d) {
+            p.tmult[d] = topo.multiplicity[d];
+            const int ax = topo.ndim - 1 - d;      // last collapsed dim -> x
+            const int64_t g = topo.global[d] / topo.local[d];
+            if (g > lim[ax]) return DS_EUNSUPPORTED;
+            (ax == 0 ? block.x : ax == 1 ? block.y : block.z) = (unsigned)topo.local[d];
+            (ax == 0 ? grid.x : ax == 1 ? grid.y : grid.z) = (unsigned)g;
+        }
+        ds_task_kernel<<<grid, block, 0, st>>>(p);
+    } else {
+        const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((p.n_reps + 255) / 256, (int64_t)sms * 16));
+        ds_task_kernel<<<(unsigned)blocks, 256, 0, st>>>(p);
+    }
+    return cudaGetLastError() == cudaSuccess ? DS_OK : DS_ECUDA;
+}
+
+DS_API int ds_tiler_coverage(const ds_tiler* t, int32_t nrep, const int64_t* rep_shape, int64_t* overlaps,
+                             int64_t* gaps, ds_stream_t stream) {
+    if (!t || !overlaps || !gaps) return DS_EINVAL;
+    TaskParams p;
+    std::memset(&p, 0, sizeof p);
+    int rc = prep_reps(nrep, rep_shape, &p);
+    if (rc) return rc;
+    int64_t n = 0;
+    if ((rc = prep_tiler(*t, nrep, &p.tout, &n))) return rc;
+    int dev = 0, sms = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+        cudaGetLastError();
+        return DS_ECUDA;
+    }
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    uint32_t* count = nullptr;
+    unsigned long long* res = nullptr;
+    if (cudaMallocAsync(&count, (size_t)n * 4, st) != cudaSuccess ||
+        cudaMallocAsync(&res, 16, st) != cudaSuccess) {
+        cudaGetLastError();
+        if (count) cudaFreeAsync(count, st);
+        return DS_ENOMEM;
+    }
+    cudaMemsetAsync(count, 0, (size_t)n * 4, st);
+    cudaMemsetAsync(res, 0, 16, st);
+    const int64_t b1 = std::max<int64_t>(1, std::min<int64_t>((p.n_reps + 255) / 256, (int64_t)sms * 16));
+    ds_cover_count_kernel<<<(unsigned)b1, 256, 0, st>>>(p, count);
+    const int64_t b2 = std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)sms * 16));
+    ds_cover_reduce_kernel<<<(unsigned)b2, 256, 0, st>>>(count, n, res);
+    unsigned long long h[2] = {0, 0};
+    cudaMemcpyAsync(h, res, 16, cudaMemcpyDeviceToHost, st);
+    cudaFreeAsync(count, st);
+    cudaFreeAsync(res, st);
+    if (cudaStreamSynchronize(st) != cudaSuccess) {
+        cudaGetLastError();
+        return DS_ECUDA;
+    }
+    *overlaps = (int64_t)h[0];
+    *gaps = (int64_t)h[1];
+    return DS_OK;
+}
+
+}  // extern "C"

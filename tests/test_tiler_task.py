@@ -1,0 +1,163 @@
+"""the general Array-OL repetitive task (arbitrary tilers, S:65-70,
+S:248-252, executed as S:517-520) and SPEC's launch topology rule
+(S:349-357).  Topology tests are host-only; task/coverage parity runs on the
+GPU against the oracle's general task executor."""
+import numpy as np
+import pytest
+
+import oracle
+import paper_1103_4881_b200 as ds
+import synth
+
+
+# ---------------------------------------------------------------- topology --
+def test_topology_spec_examples():
+    # S:355 multiplicity [288,44], max_wg 256 -> local [16,16], global [288,48], guarded
+    t = ds.ds_compute_topology([288, 44], max_wg=256)
+    assert t == dict(multiplicity=[288, 44], local=[16, 16], global_=[288, 48], guarded=True)
+    # S:356 multiplicity [8], min_items 64 -> local [8], global [8], not guarded
+    t = ds.ds_compute_topology([8], max_wg=256)
+    assert t == dict(multiplicity=[8], local=[8], global_=[8], guarded=False)
+    # S:357 [2,3,4,5] on a 3-dim device -> collapsed to [2,3,20]
+    assert ds.ds_compute_topology([2, 3, 4, 5], max_dims=3)["multiplicity"] == [2, 3, 20]
+
+
+def test_topology_invariants_random():
+    """product(local) <= max_wg, global multiple of local, product(global)
+    >= product(multiplicity), padding < 2x when product >= min_items."""
+    rng = np.random.default_rng(651)
+    for _ in range(1000):
+        nd = int(rng.integers(1, 5))
+        mult = [int(rng.integers(1, 400)) for _ in range(nd)]
+        max_wg = int(rng.choice([32, 64, 100, 256, 1024]))
+        max_dims = int(rng.integers(1, 4))
+        t = ds.ds_compute_topology(mult, max_wg=max_wg, max_dims=max_dims)
+        m, loc, glob = t["multiplicity"], t["local"], t["global_"]
+        assert len(m) == min(nd, max_dims)
+        assert int(np.prod(m)) == int(np.prod(mult))
+        assert int(np.prod(loc)) <= max_wg
+        assert all(g % l == 0 and g >= mm for g, l, mm in zip(glob, loc, m))
+        assert t["guarded"] == (glob != m)
+        if int(np.prod(m)) >= 64:
+            assert int(np.prod(glob)) < 2 * int(np.prod(m))
+
+
+def test_topology_errors():
+    with pytest.raises(ds.DSError):
+        ds.ds_compute_topology([4, 4], max_wg=0)          # S:354 zero max work-group -> error
+    with pytest.raises(ds.DSError):
+        ds.ds_compute_topology([0])
+
+
+# ------------------------------------------------------------ GPU parity --
+torch = pytest.importorskip("torch")
+
+
+def _exact_out_tiler(rng, nrep_shape, npat_shape):
+    """An exact-cover output tiler of a 2-D array for the given repetition and
+    pattern shapes (1-D each): blocked, transposed or interleaved, random origin."""
+    r, p = nrep_shape[0], npat_shape[0]
+    kind = int(rng.integers(0, 3))
+    if kind == 0:      # rows of blocks: out[r][f]
+        shape, pav, fit = (r, p), [[1], [0]], [[0], [1]]
+    elif kind == 1:    # transposed: out[f][r]
+        shape, pav, fit = (p, r), [[0], [1]], [[1], [0]]
+    else:              # interleaved 1-D: out[r + R f]
+        shape, pav, fit = (r * p,), [[1]], [[r]]
+    origin = [int(rng.integers(-50, 50)) for _ in shape]
+    return shape, oracle.make_tiler(shape, origin, pav, fit, [p]), ds.make_tiler(shape, origin, pav, fit, [p])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("policy", [ds.DS_TOPO_FLAT, ds.DS_TOPO_SPEC])
+def test_run_task_random_tilers(policy):
+    rng = np.random.default_rng(77 + policy)
+    for trial in range(60):
+        nd = int(rng.integers(1, 4))
+        in_shape = [int(rng.integers(1, 30)) for _ in range(nd)]
+        R = int(rng.integers(1, 200))
+        P = int(rng.integers(1, 17))
+        Q = int(rng.integers(1, 9))
+        origin = [int(rng.integers(-100, 100)) for _ in range(nd)]
+        pav = [[int(rng.integers(-7, 8))] for _ in range(nd)]
+        fit = [[int(rng.integers(-5, 6))] for _ in range(nd)]
+        tin_o = oracle.make_tiler(in_shape, origin, pav, fit, [P])
+        tin_d = ds.make_tiler(in_shape, origin, pav, fit, [P])
+        out_shape, tout_o, tout_d = _exact_out_tiler(rng, [R], [Q])
+        w = [[int(x) for x in rng.integers(-20, 60, P)] for _ in range(Q)]
+        D, B = int(rng.integers(1, 50)), int(rng.integers(-100, 100))
+        body_o = oracle.make_stage(P, P, 0, w, D, B)
+        body_d = ds.make_body(w, D, B, n_in=P)
+        a = rng.integers(0, 256, in_shape).astype(np.uint8)
+        want = oracle.run_task(a, tin_o, out_shape, tout_o, [R], body_o)
+        x = torch.from_numpy(a).cuda()
+        y = torch.zeros(out_shape, dtype=torch.uint8, device="cuda")
+        ds.run_task(x, tin_d, y, tout_d, [R], body_d, policy=policy)
+        torch.cuda.synchronize()
+        assert np.array_equal(y.cpu().numpy(), want), (trial, in_shape, R, P, Q)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("policy", [ds.DS_TOPO_FLAT, ds.DS_TOPO_SPEC])
+def test_run_task_downscaler_tasks(policy):
+    """The paper's yhfk task (multiplicity [288,44]) and its V task
+    through the general executor equal the dedicated kernels and the oracle."""
+    W, H = 352, 288
+    plane = synth.random_frames(3, 0, 1, W, H, 1)[0].reshape(H, W)
+    mid_o, out_o = oracle.execute_plane_mid(plane)
+    spec = ds.ds_default_spec()
+    hw = [[spec.h.weight[k][i] for i in range(8)] for k in range(3)]
+    vw = [[spec.v.weight[k][i] for i in range(9)] for k in range(4)]
+    x = torch.from_numpy(plane).cuda()
+    mid = torch.zeros((H, 132), dtype=torch.uint8, device="cuda")
+    out = torch.zeros((128, 132), dtype=torch.uint8, device="cuda")
+    ds.run_task(x, ds.make_tiler((H, W), (0, 0), [[1, 0], [0, 8]], [[0], [1]], [8]), mid,
+                ds.make_tiler((H, 132), (0, 0), [[1, 0], [0, 3]], [[0], [1]], [3]), [288, 44],
+                ds.make_body(hw, 6, 3, n_in=8), policy=policy)
+    ds.run_task(mid, ds.make_tiler((H, 132), (0, 0), [[9, 0], [0, 1]], [[1], [0]], [9]), out,
+                ds.make_tiler((128, 132), (0, 0), [[4, 0], [0, 1]], [[1], [0]], [4]), [32, 132],
+                ds.make_body(vw, 8, 4, n_in=9), policy=policy)
+    torch.cuda.synchronize()
+    assert np.array_equal(mid.cpu().numpy(), mid_o)
+    assert np.array_equal(out.cpu().numpy(), out_o)
+
+
+@pytest.mark.gpu
+def test_tiler_coverage_matches_oracle():
+    # S:284-286 examples plus random tilers; classification and counts
+    cases = [((288, 132), (0, 0), [[1, 0], [0, 3]], [[0], [1]], [3], (288, 44), "exact"),
+             ((352,), (0,), [[4]], [[1]], [8], (88,), "overlaps"),
+             ((12,), (0,), [[4]], [[1]], [3], (3,), "gaps")]
+    for shape, origin, pav, fit, pat, rep, kind in cases:
+        got = ds.tiler_coverage(ds.make_tiler(shape, origin, pav, fit, pat), rep)
+        assert got[0] == kind
+        assert oracle.check_coverage(oracle.make_tiler(shape, origin, pav, fit, pat), rep)[0] == kind
+    assert ds.tiler_coverage(ds.make_tiler((12,), (0,), [[4]], [[1]], [3]), (3,))[2] == 3
+    rng = np.random.default_rng(9)
+    for _ in range(100):
+        nd = int(rng.integers(1, 3))
+        shape = [int(rng.integers(1, 20)) for _ in range(nd)]
+        rep = [int(rng.integers(1, 6))]
+        pat = [int(rng.integers(1, 5))]
+        origin = [int(rng.integers(-9, 9)) for _ in range(nd)]
+        pav = [[int(rng.integers(-4, 5))] for _ in range(nd)]
+        fit = [[int(rng.integers(-3, 4))] for _ in range(nd)]
+        counts = np.zeros(shape, np.int64)
+        for r in range(rep[0]):
+            for f in range(pat[0]):
+                idx = tuple((o + p[0] * r + q[0] * f) % s for o, p, q, s in zip(origin, pav, fit, shape))
+                counts[idx] += 1
+        kind, over, gaps = ds.tiler_coverage(ds.make_tiler(shape, origin, pav, fit, pat), rep)
+        assert over == int((counts > 1).sum()) and gaps == int((counts == 0).sum())
+        assert kind == oracle.check_coverage(oracle.make_tiler(shape, origin, pav, fit, pat), rep)[0]
+
+
+@pytest.mark.gpu
+def test_run_task_errors():
+    x = torch.zeros(16, dtype=torch.uint8, device="cuda")
+    y = torch.zeros(16, dtype=torch.uint8, device="cuda")
+    t = ds.make_tiler((16,), (0,), [[1]], [[0]], [])
+    with pytest.raises(ds.DSError):          # body arity mismatch
+        ds.run_task(x, t, y, t, [16], ds.make_body([[1, 1]], n_in=2))
+    with pytest.raises(ds.DSError):          # in and out overlap
+        ds.run_task(x, t, x, t, [16], ds.make_body([[1]], n_in=1))
