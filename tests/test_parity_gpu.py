@@ -429,3 +429,26 @@ def test_cuda_graph_capture():
     torch.cuda.synchronize()
     _assert_same(y.cpu().numpy(), oracle.execute_frames(fr, W, H), "graph replay")
     assert d.launch_shape(1) != d.launch_shape(300)     # small batches use the fine band plan
+
+
+@pytest.mark.parametrize("kernel", [FUSED, ds.DS_KERNEL_FUSED_GENERAL, GENERIC])
+@pytest.mark.parametrize("W,H,ch,n", [(1920, 1080, 3, 3), (352, 288, 3, 5), (48, 27, 1, 4)])
+def test_every_output_byte_written(kernel, W, H, ch, n):
+    """compute-sanitizer is closed on this pool; instead, outputs pre-filled
+    with two different sentinels must both come back equal to the oracle, so
+    every output byte is written by the kernel (and nothing else is)."""
+    d = ds.Downscaler(W, H, ch)
+    d.set_kernel(kernel)
+    fr = synth.random_frames(31, 0, n, W, H, ch, 1)
+    want = oracle.execute_frames(fr, W, H, ch, 1)
+    x = torch.from_numpy(fr).cuda()
+    guard = 4096
+    for sentinel in (0x00, 0xA5):
+        buf = torch.full((n * d.out_frame_bytes + 2 * guard,), sentinel, dtype=torch.uint8, device="cuda")
+        y = buf[guard: guard + n * d.out_frame_bytes].view(n, -1)
+        d(x, y)
+        torch.cuda.synchronize()
+        assert d.last_kernel() == kernel
+        _assert_same(y.cpu().numpy(), want, f"sentinel {sentinel:#x}")
+        b = buf.cpu().numpy()
+        assert (b[:guard] == sentinel).all() and (b[-guard:] == sentinel).all(), "write outside output"

@@ -60,6 +60,32 @@ def run(W, H, n, spec, kernels, steps=20):
     return res
 
 
+def generic_task(n=300, W=1920, H=1080):
+    """The paper's yhfk H task over n HD luma planes as ONE 3-D Array-OL task
+    (frames are a repetition dimension), through ds_run_task (both launch
+    policies) vs the dedicated unfused H-task kernel (K-N3)."""
+    x = ds.generate_frames(n, W * H, seed=1)
+    mid = torch.empty((n, H, W // 8 * 3), dtype=torch.uint8, device="cuda")
+    mid2 = torch.empty_like(mid)
+    spec = ds.ds_default_spec()
+    hw = [[spec.h.weight[k][i] for i in range(8)] for k in range(3)]
+    tin = ds.make_tiler((n, H, W), (0, 0, 0), [[1, 0, 0], [0, 1, 0], [0, 0, 8]], [[0], [0], [1]], [8])
+    tout = ds.make_tiler((n, H, W // 8 * 3), (0, 0, 0), [[1, 0, 0], [0, 1, 0], [0, 0, 3]],
+                         [[0], [0], [1]], [3])
+    body = ds.make_body(hw, 6, 3, n_in=8)
+    res = {}
+    for pol, name in ((ds.DS_TOPO_FLAT, "flat"), (ds.DS_TOPO_SPEC, "spec_topology")):
+        ms = timed(lambda: ds.run_task(x, tin, mid, tout, [n, H, W // 8], body, policy=pol), 5)
+        res[f"ds_run_task_{name}_ms"] = ms
+    d = ds.Downscaler(W, H, 1)
+    res["htask_kernel_ms"] = timed(lambda: d.htask(x, mid2), 20)
+    res["bit_identical"] = bool(torch.equal(mid, mid2))
+    res["bytes"] = n * W * H * (1 + 3 / 8)
+    res["ds_run_task_flat_gbs"] = res["bytes"] / res["ds_run_task_flat_ms"] / 1e6
+    res["htask_kernel_gbs"] = res["bytes"] / res["htask_kernel_ms"] / 1e6
+    return res
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default="gpurun_out/general_perf.json")
@@ -67,11 +93,13 @@ def main():
     torch.cuda.set_device(0)
     halo = ds.make_spec(h=HALO_H, v=HALO_V)
     out = {
+        "gpu": torch.cuda.get_device_name(0),
         "halo_spec": {"h": HALO_H, "v": HALO_V},
         "hd420_300_halo_spec": run(1920, 1080, 300, halo,
                                    [ds.DS_KERNEL_FUSED_GENERAL, ds.DS_KERNEL_GENERIC]),
         "hd420_300_spec_taps": run(1920, 1080, 300, None,
                                    [ds.DS_KERNEL_FUSED, ds.DS_KERNEL_FUSED_GENERAL]),
+        "generic_task_yhfk_300_hd_luma": generic_task(),
     }
     os.makedirs(os.path.dirname(a.out) or ".", exist_ok=True)
     json.dump(out, open(a.out, "w"), indent=1)
