@@ -27,10 +27,20 @@ struct TTiler {
     int64_t foff[DS_MAX_PATTERN][4];   // fitting . f for each pattern element, reduced mod shape
 };
 
+// n / d and n % d for 0 <= n < 2^31 by multiply-high (d > 1), after the
+// classic round-up reciprocal: p = 31 + ceil(log2 d), m = ceil(2^p / d).
+struct FastDiv {
+    uint32_t d, m, s;
+};
+
 struct TaskParams {
     const uint8_t* in;
     uint8_t* out;
     int64_t n_reps;
+    int32_t fast32;                    // every index quantity < 2^31 (host-checked)
+    int32_t pad_;
+    FastDiv rdiv[4];                   // repetition extents
+    FastDiv sdiv_in[4], sdiv_out[4];   // array extents
     int32_t nrep;
     int32_t policy;
     int64_t rep[4];
@@ -73,7 +83,69 @@ __device__ __forceinline__ void t_unravel(int64_t q, int nrep, const int64_t* re
     }
 }
 
+__device__ __forceinline__ uint32_t fdiv(const FastDiv& f, uint32_t n) {
+    return f.d == 1 ? n : (__umulhi(n, f.m) >> f.s);
+}
+__device__ __forceinline__ uint32_t fmod32(const FastDiv& f, uint32_t n) { return n - fdiv(f, n) * f.d; }
+
+// 32-bit path: origin + paving.r stays < 2^31 (host bound), one modulo per
+// dim.  Loops are fully unrolled over the maximum extents with predicates so
+// the pattern and index arrays stay in registers.
+__device__ __forceinline__ uint32_t t_lin32(const TTiler& t, const FastDiv* sd, const uint32_t* base,
+                                            int f) {
+    uint32_t off = 0;
+#pragma unroll
+    for (int d = 0; d < 4; ++d)
+        if (d < t.ndim) off += fmod32(sd[d], base[d] + (uint32_t)t.foff[f][d]) * (uint32_t)t.stride[d];
+    return off;
+}
+
+__device__ __forceinline__ void t_base32(const TTiler& t, int nrep, const uint32_t* r, uint32_t* base) {
+#pragma unroll
+    for (int d = 0; d < 4; ++d) {
+        uint32_t v = (uint32_t)t.origin[d];
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if (j < nrep) v += (uint32_t)t.pav[d][j] * r[j];
+        base[d] = v;
+    }
+}
+
+__device__ __forceinline__ void task_one32(const TaskParams& p, uint32_t q) {
+    uint32_t r[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int j = 3; j >= 0; --j) {
+        if (j < p.nrep) {
+            const uint32_t qq = fdiv(p.rdiv[j], q);
+            r[j] = q - qq * p.rdiv[j].d;
+            q = qq;
+        }
+    }
+    uint32_t base[4];
+    t_base32(p.tin, p.nrep, r, base);
+    uint32_t pat[DS_MAX_PATTERN];
+#pragma unroll
+    for (int f = 0; f < DS_MAX_PATTERN; ++f)
+        pat[f] = f < p.n_in ? (uint32_t)__ldg(p.in + t_lin32(p.tin, p.sdiv_in, base, f)) : 0u;
+    t_base32(p.tout, p.nrep, r, base);
+#pragma unroll
+    for (int k = 0; k < DS_MAX_OUTPUTS; ++k) {
+        if (k < p.n_out) {
+            int32_t acc = p.bias;
+#pragma unroll
+            for (int f = 0; f < DS_MAX_PATTERN; ++f) acc += p.w[k][f] * (int32_t)pat[f];
+            int32_t v = acc / p.divisor;                  // truncation toward zero
+            v = v < 0 ? 0 : (v > 255 ? 255 : v);
+            p.out[t_lin32(p.tout, p.sdiv_out, base, k)] = (uint8_t)v;
+        }
+    }
+}
+
 __device__ __forceinline__ void task_one(const TaskParams& p, int64_t q) {
+    if (p.fast32) {
+        task_one32(p, (uint32_t)q);
+        return;
+    }
     int64_t r[4] = {0, 0, 0, 0}, base[4];
     t_unravel(q, p.nrep, p.rep, r);
     uint8_t pat[DS_MAX_PATTERN];
@@ -89,7 +161,7 @@ __device__ __forceinline__ void task_one(const TaskParams& p, int64_t q) {
     }
 }
 
-__global__ void __launch_bounds__(256) ds_task_kernel(const __grid_constant__ TaskParams p) {
+__global__ void __launch_bounds__(256, 1) ds_task_kernel(const __grid_constant__ TaskParams p) {
     if (p.policy == DS_TOPO_SPEC) {
         // NDRange work-item = one elementary task; guarded padding
         const int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -210,6 +282,35 @@ int prep_reps(int32_t nrep, const int64_t* rep, TaskParams* p) {
     return DS_OK;
 }
 
+FastDiv make_fdiv(int64_t d) {
+    FastDiv f{(uint32_t)d, 0u, 0u};
+    if (d > 1) {
+        uint32_t l = 0;
+        while ((1ULL << l) < (uint64_t)d) ++l;            // ceil(log2 d)
+        const uint64_t pw = 31 + l;
+        f.m = (uint32_t)(((1ULL << pw) + (uint64_t)d - 1) / (uint64_t)d);
+        f.s = (uint32_t)(pw - 32);
+    }
+    return f;
+}
+
+// The 32-bit path applies when every quantity it forms stays below 2^31:
+// reps, array extents, and origin + foff + sum_j pav[d][j] * (rep_j - 1).
+bool fits32(const TaskParams& p, const TTiler& t) {
+    const int64_t lim = (1LL << 31);
+    for (int d = 0; d < t.ndim; ++d) {
+        if (t.shape[d] >= lim) return false;
+        int64_t foff_max = 0;
+        for (int e = 0; e < t.npe; ++e) foff_max = std::max(foff_max, t.foff[e][d]);
+        int64_t b = t.origin[d] + foff_max;
+        for (int j = 0; j < p.nrep; ++j) b += t.pav[d][j] * (p.rep[j] - 1);
+        if (b >= lim) return false;
+    }
+    int64_t n = 1;
+    for (int d = 0; d < t.ndim; ++d) n *= t.shape[d];
+    return n < lim;
+}
+
 int64_t next_pow2(int64_t x) {
     int64_t p = 1;
     while (p < x) p <<= 1;
@@ -317,6 +418,10 @@ DS_API int ds_run_task(const uint8_t* in, const ds_tiler* t_in, uint8_t* out, co
     p.in = in;
     p.out = out;
     p.policy = policy;
+    p.fast32 = (p.n_reps < (1LL << 31) && fits32(p, p.tin) && fits32(p, p.tout)) ? 1 : 0;
+    for (int j = 0; j < nrep; ++j) p.rdiv[j] = make_fdiv(p.rep[j]);
+    for (int d = 0; d < p.tin.ndim; ++d) p.sdiv_in[d] = make_fdiv(p.tin.shape[d]);
+    for (int d = 0; d < p.tout.ndim; ++d) p.sdiv_out[d] = make_fdiv(p.tout.shape[d]);
     p.n_in = body->n_in;
     p.n_out = body->n_out;
     p.divisor = body->divisor;

@@ -161,3 +161,24 @@ def test_run_task_errors():
         ds.run_task(x, t, y, t, [16], ds.make_body([[1, 1]], n_in=2))
     with pytest.raises(ds.DSError):          # in and out overlap
         ds.run_task(x, t, x, t, [16], ds.make_body([[1]], n_in=1))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("policy", [ds.DS_TOPO_FLAT, ds.DS_TOPO_SPEC])
+def test_run_task_large_extents(policy):
+    """Large, odd extents exercise the 32-bit multiply-high divisions (and a
+    3-D repetition space with frames as its outer dimension)."""
+    rng = np.random.default_rng(12)
+    n, H, W = 3, 999, 1000003 // 1000 * 8      # W = 8000
+    a = rng.integers(0, 256, (n, H, W)).astype(np.uint8)
+    tin_args = ((n, H, W), (1, -3, 5), [[1, 0, 0], [0, 1, 0], [0, 0, 8]], [[0], [0], [1]], [8])
+    tout_args = ((n, H, W // 8 * 3), (0, 7, 0), [[1, 0, 0], [0, 1, 0], [0, 0, 3]], [[0], [0], [1]], [3])
+    w = [[1, 5, 0, 0, 0, 0, 0, 0], [0, 0, 0, 3, 3, 0, 0, 0], [0, 0, 0, 0, 0, 0, 5, 1]]
+    want = oracle.run_task(a, oracle.make_tiler(*tin_args), tout_args[0], oracle.make_tiler(*tout_args),
+                           [n, H, W // 8], oracle.make_stage(8, 8, 0, w, 6, 3))
+    x = torch.from_numpy(a).cuda()
+    y = torch.zeros(tout_args[0], dtype=torch.uint8, device="cuda")
+    ds.run_task(x, ds.make_tiler(*tin_args), y, ds.make_tiler(*tout_args), [n, H, W // 8],
+                ds.make_body(w, 6, 3, n_in=8), policy=policy)
+    torch.cuda.synchronize()
+    assert np.array_equal(y.cpu().numpy(), want)
