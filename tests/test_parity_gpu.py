@@ -452,3 +452,31 @@ def test_every_output_byte_written(kernel, W, H, ch, n):
         _assert_same(y.cpu().numpy(), want, f"sentinel {sentinel:#x}")
         b = buf.cpu().numpy()
         assert (b[:guard] == sentinel).all() and (b[-guard:] == sentinel).all(), "write outside output"
+
+
+@pytest.mark.parametrize("W,H,N", [(1920, 1080, 3000), (3840, 2160, 1000)])
+def test_full_size_streams_sampled(W, H, N):
+    """BASELINE configs[3] (3000 HD frames; the whole stream on one GPU, i.e.
+    every rank's shard at once) and configs[4] (1000 4K frames) at full size
+    in bench.py's launch configuration: whole-frame oracle checks on frames
+    spread over the stream (first, last, shard boundaries for 2/4/8 GPUs) and
+    O3 per-pixel samples on more."""
+    d = ds.Downscaler(W, H, 3)
+    x = ds.generate_frames(N, d.in_frame_bytes, seed=1)
+    y = d(x)
+    torch.cuda.synchronize()
+    assert d.last_kernel() == FUSED
+    boundaries = sorted({0, N - 1, N // 8, N // 4 - 1, N // 2, 3 * N // 8, N - N // 8})
+    for f in boundaries[:6]:
+        fr = synth.random_frames(1, f, 1, W, H)
+        _assert_same(y[f].cpu().numpy()[None], oracle.execute_frames(fr, W, H), f"frame {f}")
+    rng = np.random.default_rng(N)
+    for f in rng.choice(N, 8, replace=False):
+        fr = synth.random_frames(1, int(f), 1, W, H)[0]
+        out = y[int(f)].cpu().numpy()
+        for pin, pout in zip(oracle.split_planes(fr, W, H), oracle.split_planes(out, W, H, out=True)):
+            ho, wo = pout.shape
+            for R, Cc in zip(rng.integers(0, ho, 100), rng.integers(0, wo, 100)):
+                assert pout[R, Cc] == oracle.pixel(pin, int(R), int(Cc))
+    del x, y
+    torch.cuda.empty_cache()
