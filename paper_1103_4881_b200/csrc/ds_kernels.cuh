@@ -260,13 +260,17 @@ __global__ void __launch_bounds__((NCW + 1) * 32)
                     p.in + cur.f * p.in_frame + P.in_off + (int64_t)band * 9 * P.k * P.W;
                 uint8_t* dst = ring + (size_t)s * p.stage_stride;
                 mbar_arrive_expect_tx(&full[s], (uint32_t)P.unit_in);
+                // live rows of the band: 0..3 | 5..12 | 14..21 | ... | 9k-4..9k-1.
+                // Rows 5..8 of group g and 0..3 of group g+1 are contiguous both in
+                // HBM and in the slot, so a band of k groups takes k + 1 copies
+                // (measured +1.5% on HD 4:2:0 over two copies per group).
                 const uint32_t half = 4u * (uint32_t)P.W;
-                for (int g = 0; g < P.k; ++g) {
-                    const uint8_t* sg = src + (int64_t)9 * g * P.W;
-                    uint8_t* dg = dst + (size_t)8 * g * P.W;
-                    bulk_g2s(dg, sg, half, &full[s], pol);                            // rows 0..3
-                    bulk_g2s(dg + half, sg + (int64_t)5 * P.W, half, &full[s], pol);  // rows 5..8
-                }
+                bulk_g2s(dst, src, half, &full[s], pol);                                  // g0 rows 0..3
+                for (int g = 0; g + 1 < P.k; ++g)
+                    bulk_g2s(dst + (size_t)(8 * g + 4) * P.W, src + (int64_t)(9 * g + 5) * P.W,
+                             2u * half, &full[s], pol);                                   // rows 5..8 | 0..3
+                bulk_g2s(dst + (size_t)(8 * P.k - 4) * P.W, src + (int64_t)(9 * P.k - 4) * P.W, half,
+                         &full[s], pol);                                                  // last rows 5..8
                 if (++s == S) { s = 0; phase ^= 1; first_round = false; }
             }
         }
