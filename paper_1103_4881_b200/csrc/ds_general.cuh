@@ -85,6 +85,54 @@ __device__ __forceinline__ int32_t g_div_small(int32_t t, int32_t d, uint32_t rc
     return d == 1 ? t : (int32_t)__umulhi((uint32_t)t, rcp);
 }
 
+// H outputs of one window (compile-time Q: straight-line code, no per-output branch)
+template <int Q>
+__device__ __forceinline__ void g_h_out(const GenStage& g, uint32_t x0, uint32_t x1, uint32_t x2,
+                                        uint32_t x3, uint8_t* mo) {
+#pragma unroll
+    for (int j = 0; j < Q; ++j) {
+        int32_t acc = dp4a_us(x0, g.wp[j][0], g.bias);
+        acc = dp4a_us(x1, g.wp[j][1], acc);
+        acc = dp4a_us(x2, g.wp[j][2], acc);
+        acc = dp4a_us(x3, g.wp[j][3], acc);
+        mo[j] = (uint8_t)g_stage_out(acc, g.D, g.D_rcp);
+    }
+}
+
+// V outputs of one 4-column group (compile-time Q)
+template <int Q>
+__device__ __forceinline__ void g_v_quad(const GenStage& g, const uint8_t* mb, int Wm, uint8_t* ob0) {
+    int32_t acc[Q][4];
+#pragma unroll
+    for (int kk = 0; kk < Q; ++kk)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[kk][e] = g.bias;
+    const int nb = (g.P + 3) >> 2;
+    for (int b4 = 0; b4 < nb; ++b4) {
+        const uint8_t* rb = mb + (size_t)(4 * b4) * Wm;
+        const uint32_t r0 = lds32(rb), r1 = lds32(rb + Wm), r2 = lds32(rb + 2 * Wm), r3 = lds32(rb + 3 * Wm);
+        const uint32_t ta = __byte_perm(r0, r1, 0x5140), tb = __byte_perm(r2, r3, 0x5140);
+        const uint32_t tc = __byte_perm(r0, r1, 0x7362), td = __byte_perm(r2, r3, 0x7362);
+        const uint32_t c0 = __byte_perm(ta, tb, 0x5410), c1 = __byte_perm(ta, tb, 0x7632),
+                       c2 = __byte_perm(tc, td, 0x5410), c3 = __byte_perm(tc, td, 0x7632);
+#pragma unroll
+        for (int kk = 0; kk < Q; ++kk) {
+            const uint32_t wq = g.wp[kk][b4];
+            acc[kk][0] = dp4a_us(c0, wq, acc[kk][0]);
+            acc[kk][1] = dp4a_us(c1, wq, acc[kk][1]);
+            acc[kk][2] = dp4a_us(c2, wq, acc[kk][2]);
+            acc[kk][3] = dp4a_us(c3, wq, acc[kk][3]);
+        }
+    }
+#pragma unroll
+    for (int kk = 0; kk < Q; ++kk) {
+        const uint32_t o = g_stage_out(acc[kk][0], g.D, g.D_rcp) | (g_stage_out(acc[kk][1], g.D, g.D_rcp) << 8) |
+                           (g_stage_out(acc[kk][2], g.D, g.D_rcp) << 16) |
+                           (g_stage_out(acc[kk][3], g.D, g.D_rcp) << 24);
+        *reinterpret_cast<uint32_t*>(ob0 + (size_t)kk * Wm) = o;
+    }
+}
+
 struct GenCursor {
     int64_t u, f;
     int32_t local, gdiv, gmod, upf;
@@ -199,15 +247,15 @@ __global__ void __launch_bounds__((NCW + 1) * 32, NCW == 8 ? 3 : 1)
                                    w3 = lds32(wb + 12), w4 = lds32(wb + 16);
                     const uint32_t x0 = __byte_perm(w0, w1, sel), x1 = __byte_perm(w1, w2, sel),
                                    x2 = __byte_perm(w2, w3, sel), x3 = __byte_perm(w3, w4, sel);
-#pragma unroll
-                    for (int j = 0; j < DS_MAX_OUTPUTS; ++j) {
-                        if (j < QH) {
-                            int32_t acc = dp4a_us(x0, p.h.wp[j][0], p.h.bias);
-                            acc = dp4a_us(x1, p.h.wp[j][1], acc);
-                            acc = dp4a_us(x2, p.h.wp[j][2], acc);
-                            acc = dp4a_us(x3, p.h.wp[j][3], acc);
-                            mo[j] = (uint8_t)g_stage_out(acc, p.h.D, p.h.D_rcp);
-                        }
+                    switch (QH) {
+                        case 1: g_h_out<1>(p.h, x0, x1, x2, x3, mo); break;
+                        case 2: g_h_out<2>(p.h, x0, x1, x2, x3, mo); break;
+                        case 3: g_h_out<3>(p.h, x0, x1, x2, x3, mo); break;
+                        case 4: g_h_out<4>(p.h, x0, x1, x2, x3, mo); break;
+                        case 5: g_h_out<5>(p.h, x0, x1, x2, x3, mo); break;
+                        case 6: g_h_out<6>(p.h, x0, x1, x2, x3, mo); break;
+                        case 7: g_h_out<7>(p.h, x0, x1, x2, x3, mo); break;
+                        default: g_h_out<8>(p.h, x0, x1, x2, x3, mo); break;
                     }
                 } else {
                     for (int j = 0; j < QH; ++j) {
@@ -232,46 +280,23 @@ __global__ void __launch_bounds__((NCW + 1) * 32, NCW == 8 ? 3 : 1)
             // item = (V repetition g, 4 mid columns): 4x4 byte transposes turn
             // 4 rows x 4 columns into 4 column words, one dp4a per 4 taps
             const int quads = Wm >> 2;
-            const int QV = p.v.Q, nb = (p.v.P + 3) >> 2;
+            const int QV = p.v.Q;
             const int v_items = P.k * quads;
             for (int it = tid; it < v_items; it += NC) {
                 {
                     const int g = g_div_small(it, quads, P.quads_rcp);
                     const int q = it - g * quads;
                     const uint8_t* mb = mid + (size_t)(p.v.S * g) * Wm + 4 * q;
-                    int32_t acc[DS_MAX_OUTPUTS][4];
-#pragma unroll
-                    for (int kk = 0; kk < DS_MAX_OUTPUTS; ++kk)
-#pragma unroll
-                        for (int e = 0; e < 4; ++e) acc[kk][e] = p.v.bias;
-                    for (int b4 = 0; b4 < nb; ++b4) {
-                        const uint8_t* rb = mb + (size_t)(4 * b4) * Wm;
-                        const uint32_t r0 = lds32(rb), r1 = lds32(rb + Wm), r2 = lds32(rb + 2 * Wm),
-                                       r3 = lds32(rb + 3 * Wm);
-                        const uint32_t ta = __byte_perm(r0, r1, 0x5140), tb = __byte_perm(r2, r3, 0x5140);
-                        const uint32_t tc = __byte_perm(r0, r1, 0x7362), td = __byte_perm(r2, r3, 0x7362);
-                        const uint32_t col0 = __byte_perm(ta, tb, 0x5410), col1 = __byte_perm(ta, tb, 0x7632),
-                                       col2 = __byte_perm(tc, td, 0x5410), col3 = __byte_perm(tc, td, 0x7632);
-#pragma unroll
-                        for (int kk = 0; kk < DS_MAX_OUTPUTS; ++kk) {
-                            if (kk < QV) {
-                                const uint32_t wq = p.v.wp[kk][b4];
-                                acc[kk][0] = dp4a_us(col0, wq, acc[kk][0]);
-                                acc[kk][1] = dp4a_us(col1, wq, acc[kk][1]);
-                                acc[kk][2] = dp4a_us(col2, wq, acc[kk][2]);
-                                acc[kk][3] = dp4a_us(col3, wq, acc[kk][3]);
-                            }
-                        }
-                    }
-#pragma unroll
-                    for (int kk = 0; kk < DS_MAX_OUTPUTS; ++kk) {
-                        if (kk < QV) {
-                            const uint32_t o = g_stage_out(acc[kk][0], p.v.D, p.v.D_rcp) |
-                                               (g_stage_out(acc[kk][1], p.v.D, p.v.D_rcp) << 8) |
-                                               (g_stage_out(acc[kk][2], p.v.D, p.v.D_rcp) << 16) |
-                                               (g_stage_out(acc[kk][3], p.v.D, p.v.D_rcp) << 24);
-                            *reinterpret_cast<uint32_t*>(ob + (size_t)(QV * g + kk) * Wm + 4 * q) = o;
-                        }
+                    uint8_t* ob0 = ob + (size_t)(QV * g) * Wm + 4 * q;
+                    switch (QV) {
+                        case 1: g_v_quad<1>(p.v, mb, Wm, ob0); break;
+                        case 2: g_v_quad<2>(p.v, mb, Wm, ob0); break;
+                        case 3: g_v_quad<3>(p.v, mb, Wm, ob0); break;
+                        case 4: g_v_quad<4>(p.v, mb, Wm, ob0); break;
+                        case 5: g_v_quad<5>(p.v, mb, Wm, ob0); break;
+                        case 6: g_v_quad<6>(p.v, mb, Wm, ob0); break;
+                        case 7: g_v_quad<7>(p.v, mb, Wm, ob0); break;
+                        default: g_v_quad<8>(p.v, mb, Wm, ob0); break;
                     }
                 }
             }
