@@ -422,8 +422,9 @@ def main():
         et = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=coll_dev)
         if world > 1:
             dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        h2d_pf = d.schedule_plan(ds.DS_SCHED_STREAMED)["h2d_bytes"]   # dead rows not sent
         e2e = {"value": cfg["total"] * ks / (float(et[0]) / 1e3), "unit": "frames/s",
-               "h2d_bytes_per_step": n * fin, "d2h_bytes_per_step": n * fout,
+               "h2d_bytes_per_step": n * h2d_pf, "d2h_bytes_per_step": n * fout,
                "steps": ks, "api": "Downscaler.run_host -> ds_run_host (pinned host buffers)"}
         ok = torch.equal(hout, y.cpu())
         e2e["matches_device_path"] = bool(ok)

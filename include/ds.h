@@ -159,7 +159,10 @@ DS_API int ds_run(ds_handle* h, const uint8_t* in_frames, int64_t n_frames,
  * P:148): the library streams chunks of frames host -> device, runs the
  * downscaler and copies results device -> host, overlapping the three on
  * internal streams and staging buffers it owns (allocated on first use,
- * freed by ds_destroy).  host_in / host_out should be page-locked
+ * freed by ds_destroy).  In the spirit of the paper's transfer tuning
+ * ("avoid extra data transfers"), with SPEC's taps the input rows
+ * 9g+4 -- zero V weight, read by no kernel -- are not transferred
+ * (8/9 of the input bytes cross PCIe).  host_in / host_out should be page-locked
  * (cudaHostAlloc / cudaHostRegister) for the copies to be asynchronous;
  * pageable memory works but serialises.  Asynchronous on `stream`:
  * host_out is valid after `stream` synchronises; both buffers must stay

@@ -517,6 +517,48 @@ int run_device(ds_handle* h, const uint8_t* in, int64_t n, uint8_t* out, cudaStr
     return rc;
 }
 
+// Host -> device copy of m frames for the fused path.  With SPEC's taps row
+// 9g+4 of every plane has zero V weight and no kernel reads it, so
+// only rows 0..3 and 5..8 of each 9-row group cross PCIe: per plane one
+// strided 3-D copy per half when the frame stride is a whole number of
+// 9-row pitches, else one 2-D copy per frame and half.  Returns bytes copied
+// (< 0 on error).  The skipped rows of the device buffer stay stale.
+int64_t live_rows_h2d(const ds_handle* h, uint8_t* dst, const uint8_t* src, int64_t m,
+                      cudaStream_t st) {
+    const ds_plan_info& pi = h->plan;
+    ds_filter_spec def;
+    default_spec(&def);
+    const int64_t fin = pi.in_frame_bytes;
+    if (!(stage_equal(h->spec.v, def.v) && stage_equal(h->spec.h, def.h) && pi.fused_eligible)) {
+        if (cudaMemcpyAsync(dst, src, m * fin, cudaMemcpyHostToDevice, st) != cudaSuccess) return -1;
+        return m * fin;
+    }
+    int64_t bytes = 0;
+    for (int p = 0; p < pi.n_planes; ++p) {
+        const int64_t W = pi.in_w[p], G = pi.in_h[p] / 9, pitch = 9 * W;
+        for (int half = 0; half < 2; ++half) {
+            const int64_t off = pi.in_offset[p] + (half ? 5 : 0) * W;
+            if (fin % pitch == 0) {
+                cudaMemcpy3DParms c;
+                std::memset(&c, 0, sizeof c);
+                c.srcPtr = make_cudaPitchedPtr(const_cast<uint8_t*>(src) + off, (size_t)pitch, (size_t)(4 * W),
+                                               (size_t)(fin / pitch));
+                c.dstPtr = make_cudaPitchedPtr(dst + off, (size_t)pitch, (size_t)(4 * W), (size_t)(fin / pitch));
+                c.extent = make_cudaExtent((size_t)(4 * W), (size_t)G, (size_t)m);
+                c.kind = cudaMemcpyHostToDevice;
+                if (cudaMemcpy3DAsync(&c, st) != cudaSuccess) return -1;
+            } else {
+                for (int64_t f = 0; f < m; ++f)
+                    if (cudaMemcpy2DAsync(dst + f * fin + off, (size_t)pitch, src + f * fin + off, (size_t)pitch,
+                                          (size_t)(4 * W), (size_t)G, cudaMemcpyHostToDevice, st) != cudaSuccess)
+                        return -1;
+            }
+            bytes += m * G * 4 * W;
+        }
+    }
+    return bytes;
+}
+
 void free_host_state(ds_handle* h) {
     for (auto& s : h->slots) {
         if (s.stream) cudaStreamSynchronize(s.stream);
@@ -659,8 +701,10 @@ DS_API int ds_run_host(ds_handle* h, const uint8_t* host_in, int64_t n, uint8_t*
     for (int64_t f0 = 0; f0 < n; f0 += chunk, ++c) {
         const int64_t m = std::min(chunk, n - f0);
         HostSlot& s = h->slots[c % kHostSlots];
-        if (cudaMemcpyAsync(s.d_in, host_in + f0 * fin, m * fin, cudaMemcpyHostToDevice, s.stream) !=
-            cudaSuccess) { cudaGetLastError(); return DS_ECUDA; }
+        if (live_rows_h2d(h, s.d_in, host_in + f0 * fin, m, s.stream) < 0) {
+            cudaGetLastError();
+            return DS_ECUDA;
+        }
         int rc = run_device(h, s.d_in, m, s.d_out, s.stream);
         if (rc) return rc;
         if (cudaMemcpyAsync(host_out + f0 * fout, s.d_out, m * fout, cudaMemcpyDeviceToHost,

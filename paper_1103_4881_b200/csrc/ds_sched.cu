@@ -262,8 +262,13 @@ DS_API int ds_schedule_plan(int32_t frame_w, int32_t frame_h, int32_t channels,
     std::memset(s, 0, sizeof *s);
     s->frames = 1;
     if (schedule == DS_SCHED_STREAMED) {
-        // per frame, amortised: one H2D and one D2H per chunk of frames
-        s->h2d_bytes = h->plan.in_frame_bytes;
+        // per frame, amortised: one H2D and one D2H per chunk of frames; with
+        // SPEC's taps the dead row 9g+4 of every plane is not transferred
+        ds_filter_spec def;
+        default_spec(&def);
+        const bool skip = stage_equal(h->spec.h, def.h) && stage_equal(h->spec.v, def.v) &&
+                          h->plan.fused_eligible;
+        s->h2d_bytes = skip ? h->plan.in_frame_bytes / 9 * 8 : h->plan.in_frame_bytes;
         s->d2h_bytes = h->plan.out_frame_bytes;
         s->h2d_count = s->d2h_count = s->launches = 1;
         return DS_OK;
@@ -313,7 +318,9 @@ DS_API int ds_run_schedule(ds_handle* h, const uint8_t* host_in, int64_t n, uint
         const int64_t chunks = n ? (n + chunk - 1) / chunk : 0;
         stats->frames = n;
         stats->h2d_count = stats->d2h_count = stats->launches = chunks;
-        stats->h2d_bytes = n * fin;
+        ds_schedule_stats pf;
+        ds_schedule_plan(h->W, h->H, h->channels, &h->spec, DS_SCHED_STREAMED, &pf);
+        stats->h2d_bytes = n * pf.h2d_bytes;
         stats->d2h_bytes = n * fout;
         stats->total_ms = ms;
         return DS_OK;

@@ -95,7 +95,8 @@ def test_schedules_produce_the_oracle_output(sched, pinned):
         assert st["h2d_ms"] > 0 and st["d2h_ms"] > 0 and st["kernel_ms"] > 0
         assert st["total_ms"] >= 0.9 * (st["h2d_ms"] + st["d2h_ms"] + st["kernel_ms"])
     else:
-        assert st["h2d_bytes"] == n * d.in_frame_bytes and st["h2d_count"] == 2
+        # the dead input row 9g+4 (zero V weight) is not transferred
+        assert st["h2d_bytes"] == n * d.in_frame_bytes // 9 * 8 and st["h2d_count"] == 2
 
 
 def test_schedule_zero_frames_and_errors():
