@@ -7,8 +7,9 @@
 One step = one ds_run over the whole per-rank batch of frames (every row of
 SURVEY 8(a): H task -> u8 intermediate -> V task, all planes, all frames)
 with the input already resident in HBM.  N = 1 runs BASELINE configs[2]
-(300-frame HD 4:2:0 stream on one B200); N > 1 runs configs[3] (3000-frame
-HD stream frame-sharded over N GPUs, launched with torchrun).  Rank 0 prints
+(300-frame HD 4:2:0 stream on one B200); N > 1 (torchrun) weak-scales it,
+300 frames per GPU frame-sharded by global index (--frames 3000 runs
+configs[3]'s fixed 3000-frame stream instead).  Rank 0 prints
 ONE JSON line.  See DESIGN.md "Measurement" for every field.
 """
 from __future__ import annotations
@@ -45,7 +46,8 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="hd420")
     ap.add_argument("--frames", type=int, default=0,
-                    help="total frames (default: 300 at N=1, 3000 at N>1; 4K: 1000)")
+                    help="TOTAL frames (strong scaling); default: 300 HD / 1000 4K frames "
+                         "per GPU (weak scaling)")
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--stages", type=int, default=0)
     ap.add_argument("--ctas", type=int, default=0)
@@ -64,20 +66,30 @@ def parse():
 
 
 def workload(args, world):
+    """Frames per run.  Default: weak scaling, 300 HD frames per GPU (N = 1 is
+    configs[2] exactly; frames are independent, so ranks share no data
+    path).  --frames F fixes the TOTAL instead (strong scaling; --frames 3000
+    is configs[3] literally)."""
     cfg = dict(CONFIGS[args.config])
+    per_gpu = 1000 if args.config.startswith("4k") else 300
     if args.frames:
-        total = args.frames
-    elif args.config.startswith("4k"):
-        total = 1000
+        total, scaling = args.frames, ("weak" if world == 1 else "strong")
     else:
-        total = 300 if world == 1 else 3000
+        total, scaling = per_gpu * world, "weak"
     cfg["total"] = total
+    cfg["scaling"] = scaling
     if args.config.startswith("hd") and world == 1 and total == 1:
         cfg["name"] = f"configs[1]: one {cfg['label']} frame on 1 B200 (latency; L2-resident)"
     elif args.config.startswith("hd") and world == 1 and total == 300:
         cfg["name"] = f"configs[2]: 300-frame {cfg['label']} stream on 1 B200"
+    elif args.config.startswith("hd") and not args.frames:
+        cfg["name"] = (f"configs[2] per GPU, weak-scaled: {total}-frame {cfg['label']} stream "
+                       f"frame-sharded over {world} B200 (300 frames per GPU; configs[3] scale)")
     elif args.config.startswith("hd") and total == 3000:
         cfg["name"] = f"configs[3]: 3000-frame {cfg['label']} stream frame-sharded over {world} B200"
+    elif args.config.startswith("4k") and total == 1000 * max(1, world) and not args.frames:
+        cfg["name"] = (f"configs[4] per GPU, weak-scaled: {total}-frame {cfg['label']} stream over "
+                       f"{world} B200")
     elif args.config.startswith("4k") and total == 1000:
         cfg["name"] = f"configs[4]: 1000-frame {cfg['label']} stream over {world} B200"
     else:
@@ -261,7 +273,7 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": fps, "unit": "frames/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
-        "scaling": "weak" if world == 1 else "strong", "vs_baseline": None, "dtype": "u8",
+        "scaling": cfg["scaling"], "vs_baseline": None, "dtype": "u8",
         "data": "synthetic (splitmix64 counter-hash frames, seed %d)" % args.seed,
         "config": {"workload": cfg["name"], "frames": cfg["total"], "w": W, "h": H,
                    "channels": ch, "chroma": "4:2:0" if chroma else "4:4:4",
@@ -442,7 +454,7 @@ def main():
         line = {
             "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": world,
             "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": total_ms / args.steps,
-            "higher_is_better": True, "scaling": "weak" if world == 1 else "strong",
+            "higher_is_better": True, "scaling": cfg["scaling"],
             "vs_baseline": None, "dtype": "u8",
             "data": f"synthetic (splitmix64 counter-hash frames by global byte index, seed {args.seed})",
             "config": {
