@@ -128,24 +128,30 @@ int make_plan(int32_t W, int32_t H, int32_t channels, const ds_filter_spec* spec
     bool fused = stage_equal(spec.h, def.h) && stage_equal(spec.v, def.v);
     for (int p = 0; p < channels && fused; ++p) fused = (pi.in_w[p] % 16 == 0);
     if (fused) {
+        // shrink the band target until a 2-deep ring fits one CTA's shared
+        // memory (a caller's large ds_set_band_bytes never loses K-N1)
         const int G0 = pi.in_h[0] / 9;
-        const int k0 = largest_divisor_below(G0, 8LL * pi.in_w[0], unit_target);
-        const int64_t target = 8LL * k0 * pi.in_w[0];
-        int64_t units = 0, umax = 0, omax = 0;
-        for (int p = 0; p < channels; ++p) {
-            const int G = pi.in_h[p] / 9;
-            const int k = p == 0 ? k0 : closest_divisor(G, 8LL * pi.in_w[p], target);
-            pi.band_groups[p] = k;
-            units += G / k;
-            umax = std::max<int64_t>(umax, 8LL * k * pi.in_w[p]);
-            omax = std::max<int64_t>(omax, 4LL * k * pi.out_w[p]);
+        int64_t want = unit_target;
+        for (;;) {
+            const int k0 = largest_divisor_below(G0, 8LL * pi.in_w[0], want);
+            const int64_t target = 8LL * k0 * pi.in_w[0];
+            int64_t units = 0, umax = 0, omax = 0;
+            for (int p = 0; p < channels; ++p) {
+                const int G = pi.in_h[p] / 9;
+                const int k = p == 0 ? k0 : closest_divisor(G, 8LL * pi.in_w[p], target);
+                pi.band_groups[p] = k;
+                units += G / k;
+                umax = std::max<int64_t>(umax, 8LL * k * pi.in_w[p]);
+                omax = std::max<int64_t>(omax, 4LL * k * pi.out_w[p]);
+            }
+            pi.units_per_frame = units;
+            pi.unit_in_bytes_max = umax;
+            pi.unit_out_bytes_max = omax;
+            fused = fused_smem_bytes(2, (int32_t)round_up(umax, 128), (int32_t)round_up(omax, 128)) <=
+                    kSmemLimit;
+            if (fused || k0 == 1) break;
+            want = 8LL * k0 * pi.in_w[0] - 1;      // next smaller luma band
         }
-        pi.units_per_frame = units;
-        pi.unit_in_bytes_max = umax;
-        pi.unit_out_bytes_max = omax;
-        // at least a 2-deep ring must fit in one CTA's shared memory
-        fused = fused_smem_bytes(2, (int32_t)round_up(umax, 128), (int32_t)round_up(omax, 128)) <=
-                kSmemLimit;
     }
     // K-N1g (any spec): whole-width staged rows need 16-byte rows; bands of
     // k V repetitions stage R = Sv (k-1) + Pv rows (band + halo).

@@ -179,3 +179,13 @@ def test_schedule_byte_model_matches_spec_and_paper():
     assert 1 - 3110400 / hd["h2d_bytes"] == pytest.approx(h2d_cut, abs=1e-3)
     with pytest.raises(ds.DSError):
         ds.ds_schedule_plan(352, 288, 3, 9)
+
+
+def test_plan_wide_planes_and_smem_limit():
+    # 7680-wide (8K) luma: one group stages 61,440 B; a 2-deep ring + 3 output
+    # slots fits 227 KB -> K-N1 with 1 group per band
+    p = ds.ds_plan(7680, 4320, 1)
+    assert p.fused_eligible == 1 and p.band_groups[0] == 1
+    # 11520-wide: 92,160 B per group -> 2 x 92,160 + 3 x 17,280 > 227 KB -> not K-N1
+    p = ds.ds_plan(11520, 2160, 1)
+    assert p.fused_eligible == 0 and p.fused_general_eligible == 0

@@ -480,3 +480,36 @@ def test_full_size_streams_sampled(W, H, N):
                 assert pout[R, Cc] == oracle.pixel(pin, int(R), int(Cc))
     del x, y
     torch.cuda.empty_cache()
+
+
+def test_fused_kernel_fuzz():
+    """Random geometries (W % 16 == 0, H % 9 or 18 == 0), channel/chroma
+    modes, frame counts, band sizes, ring depths and output-pointer
+    alignments: K-N1 byte-for-byte against the oracle."""
+    rng = np.random.default_rng(4242)
+    for trial in range(40):
+        ch = int(rng.choice([1, 3]))
+        chroma = int(rng.integers(0, 2))
+        wmul = 32 if (ch == 3 and chroma == 1) else 16
+        hmul = 18 if (ch == 3 and chroma == 1) else 9
+        W = wmul * int(rng.integers(1, 40))
+        H = hmul * int(rng.integers(1, 30))
+        n = int(rng.integers(1, 9))
+        d = ds.Downscaler(W, H, ch, chroma=chroma)
+        if not d.plan.fused_eligible:
+            continue
+        band = int(rng.choice([0, 1, 4096, 20000, 100000]))
+        d.set_band_bytes(band)
+        if rng.random() < 0.5:
+            d.set_tuning(int(rng.integers(2, 9)), int(rng.integers(0, 3)))
+        fr = synth.random_frames(trial, int(rng.integers(0, 1000)), n, W, H, ch, chroma)
+        want = oracle.execute_frames(fr, W, H, ch, chroma)
+        x = torch.from_numpy(fr).cuda()
+        off = int(rng.choice([0, 0, 16, 1, 3]))
+        buf = torch.full((n * d.out_frame_bytes + 64,), 0x5A, dtype=torch.uint8, device="cuda")
+        y = buf[off: off + n * d.out_frame_bytes].view(n, -1)
+        ds.ds_run(d.handle, x.data_ptr(), n, y.data_ptr(), torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        assert d.last_kernel() == FUSED
+        _assert_same(y.cpu().numpy(), want, f"trial {trial}: {W}x{H}x{ch} chroma={chroma} n={n} "
+                                              f"band={band} off={off}")
