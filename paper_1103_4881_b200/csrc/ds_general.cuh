@@ -61,14 +61,14 @@ __device__ __forceinline__ uint32_t g_udiv(uint32_t a, uint32_t D, uint32_t rcp)
     if (a - q * D >= D) ++q;
     return q;
 }
-// clamp_0^255(trunc(acc / D))
+// clamp_0^255(trunc(acc / D)), branch-free: a non-positive accumulator
+// truncates to a non-positive quotient, which clamps to 0 -- so divide
+// max(acc, 0) instead of branching on the sign.
 __device__ __forceinline__ uint32_t g_stage_out(int32_t acc, uint32_t D, uint32_t rcp) {
-    if (acc <= 0) {
-        // trunc toward zero of a non-positive quotient is <= 0 -> clamps to 0
-        return 0u;
-    }
-    const uint32_t q = g_udiv((uint32_t)acc, D, rcp);
-    return q > 255u ? 255u : q;
+    const uint32_t a = (uint32_t)max(acc, 0);
+    uint32_t q = __umulhi(a, rcp);
+    q += (a - q * D >= D) ? 1u : 0u;
+    return min(q, 255u);
 }
 // d = c + sum_i a.u8[i] * b.s8[i]
 __device__ __forceinline__ int32_t dp4a_us(uint32_t a, uint32_t b, int32_t c) {
