@@ -41,7 +41,7 @@ struct GenStage {
     int32_t P, S, Q, bias;
     uint32_t D, D_rcp;         // divisor and floor(2^32 / D) (D = 1: 0xffffffff)
     int32_t s8;                // 1: every weight fits in s8 -> dp4a fast path
-    int32_t pad_;
+    int32_t reserved_;         // keeps wp 8-byte aligned in the parameter block
     int32_t w[DS_MAX_OUTPUTS][DS_MAX_PATTERN];
     uint32_t wp[DS_MAX_OUTPUTS][DS_MAX_PATTERN / 4];   // s8-packed weights, 4 taps per word
 };
@@ -55,15 +55,11 @@ struct GeneralParams {
     GenStage h, v;
 };
 
-// floor(a / D) for 0 <= a < 2^32: q0 = umulhi(a, floor(2^32/D)) is q or q-1.
-__device__ __forceinline__ uint32_t g_udiv(uint32_t a, uint32_t D, uint32_t rcp) {
-    uint32_t q = __umulhi(a, rcp);
-    if (a - q * D >= D) ++q;
-    return q;
-}
 // clamp_0^255(trunc(acc / D)), branch-free: a non-positive accumulator
 // truncates to a non-positive quotient, which clamps to 0 -- so divide
-// max(acc, 0) instead of branching on the sign.
+// max(acc, 0) instead of branching on the sign.  floor(a / D) for
+// 0 <= a < 2^32: q0 = umulhi(a, floor(2^32 / D)) is q or q - 1, one
+// correction step makes it exact.
 __device__ __forceinline__ uint32_t g_stage_out(int32_t acc, uint32_t D, uint32_t rcp) {
     const uint32_t a = (uint32_t)max(acc, 0);
     uint32_t q = __umulhi(a, rcp);

@@ -47,7 +47,7 @@ struct FusedParams {
     int32_t stages;            // ring depth
     int32_t stage_stride;      // bytes per ring slot (>= max unit_in, 128-aligned)
     int32_t out_stride;        // bytes per output slot (>= max unit_out, 128-aligned)
-    int32_t pad_;
+    int32_t reserved_;         // keeps pl[] 8-byte aligned
     FusedPlane pl[DS_MAX_PLANES];
 };
 

@@ -38,7 +38,7 @@ struct TaskParams {
     uint8_t* out;
     int64_t n_reps;
     int32_t fast32;                    // every index quantity < 2^31 (host-checked)
-    int32_t pad_;
+    int32_t reserved_;
     FastDiv rdiv[4];                   // repetition extents
     FastDiv sdiv_in[4], sdiv_out[4];   // array extents
     int32_t nrep;
