@@ -27,9 +27,12 @@ def gather_frames(local: torch.Tensor, total: int, group=None, dst: int = 0):
     """Gather every rank's (n_r, frame_bytes) shard to `dst` in frame order.
 
     Uses point-to-point batches (shards may differ in size by one frame).
-    Returns the (total, frame_bytes) tensor on dst, None elsewhere."""
+    Returns the (total, frame_bytes) tensor on dst, None elsewhere (on the
+    host when the group's backend is gloo)."""
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
+    if local.is_cuda and dist.get_backend(group) == "gloo":
+        local = local.cpu()              # gloo moves host tensors (tests on one GPU)
     fb = local.shape[1] if local.dim() == 2 else local.numel()
     if rank != dst:
         if local.numel():
