@@ -223,12 +223,21 @@ def cpu_oracle_sample(cfg, seed, budget_s, gpu_out_fn=None):
         k += 1
     wall = time.perf_counter() - t_all
     per = statistics.median(times)
+    # O2, the direct nested-loop oracle, on a few of the same frames
+    o2_times = []
+    for k2 in range(min(k, 5)):
+        fr = synth.random_frames(seed, k2, 1, W, H, ch, chroma)
+        t0 = time.perf_counter()
+        oracle.direct_frames(fr, W, H, ch, chroma)
+        o2_times.append(time.perf_counter() - t0)
     return {
         "value": 1.0 / per, "unit": "frames/s", "cores": 1, "kind": "oracle",
         "sample": f"frames 0..{k - 1} of the same seeded stream ({k} frames), O1 tiler executor "
                   f"(oracle/ds_oracle.c, gcc -O2, 1 thread pinned to core {core}); "
                   f"median per-frame time {per * 1e3:.1f} ms; {wall:.1f} s of CPU work",
         "frames": k, "host_cpu": platform.processor() or platform.machine(),
+        "o2_direct_value": 1.0 / statistics.median(o2_times), "oracle_core_id": core,
+        "host_cores": os.cpu_count(),
         "parity_checked_frames": k if gpu_out_fn is not None else 0,
         "parity_bit_exact_frames": same if gpu_out_fn is not None else None,
     }
@@ -466,7 +475,8 @@ def main():
                 "l2": f"inputs larger than L2: {n * (fin + fout) / 1e9:.3f} GB touched per step "
                       f"per GPU vs 126 MB L2 (no flush needed)",
                 "kernel": ds.KERNEL_NAMES.get(kernel_used), "grid": g, "block": b,
-                "smem_bytes": s,
+                "smem_bytes": s, "band_groups": list(d.plan.band_groups)[: cfg["channels"]],
+                "units_per_frame": d.plan.units_per_frame,
             },
             "roofline": {
                 "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
