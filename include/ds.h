@@ -359,6 +359,18 @@ DS_API int ds_run_task(const uint8_t* in, const ds_tiler* t_in, uint8_t* out, co
 DS_API int ds_tiler_coverage(const ds_tiler* t, int32_t nrep, const int64_t* rep_shape,
                              int64_t* overlaps, int64_t* gaps, ds_stream_t stream);
 
+/* ---- debug: work-unit accounting (stand-in for compute-sanitizer, which is
+ * closed on this GPU pool).  When counts != NULL, every K-N1 / K-N1g work
+ * unit u processed by a later ds_run / ds_run_host adds 1 to counts[u]
+ * (device array of ds_units(h, n, kernel) u32, caller-zeroed); a correct
+ * persistent schedule leaves every entry exactly 1.  NULL switches it off
+ * (the default; costs one predicate per unit). */
+DS_API int ds_set_debug_counter(ds_handle* h, uint32_t* counts);
+
+/* Work units of a ds_run over n frames with K-N1 (DS_KERNEL_FUSED) or K-N1g
+ * (DS_KERNEL_FUSED_GENERAL); -1 if that kernel cannot run the handle. */
+DS_API int64_t ds_units(const ds_handle* h, int64_t n_frames, int32_t kernel);
+
 /* Synthetic input (bench / test infrastructure, not part of the method):
  * fills dev[0 .. n_bytes) on the current device with
  *   byte(i) = splitmix64(seed * 0x9E3779B97F4A7C15 + start_index + i) >> 56

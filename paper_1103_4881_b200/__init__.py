@@ -178,6 +178,8 @@ SIGNATURES = [
                               C.POINTER(C.c_int64), C.POINTER(ds_task_body), C.c_int32, C.c_void_p]),
     ("ds_tiler_coverage", C.c_int, [C.POINTER(ds_tiler), C.c_int32, C.POINTER(C.c_int64),
                                     C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.c_void_p]),
+    ("ds_set_debug_counter", C.c_int, [C.c_void_p, C.c_void_p]),
+    ("ds_units", C.c_int64, [C.c_void_p, C.c_int64, C.c_int32]),
     ("ds_generate", C.c_int, [C.c_void_p, C.c_int64, C.c_uint64, C.c_int64, C.c_void_p]),
 ]
 

@@ -314,6 +314,7 @@ int launch_fused(ds_handle* h, const uint8_t* in, int64_t n, uint8_t* out, cudaS
     ds::FusedParams p;
     std::memset(&p, 0, sizeof p);
     p.in = in; p.out = out;
+    p.unit_count = h->debug_unit_count;
     p.in_frame = pi.in_frame_bytes; p.out_frame = pi.out_frame_bytes;
     p.upf = (int32_t)pi.units_per_frame;
     p.n_units = n * pi.units_per_frame;
@@ -425,6 +426,7 @@ int launch_general(ds_handle* h, const uint8_t* in, int64_t n, uint8_t* out, cud
     ds::GeneralParams p;
     std::memset(&p, 0, sizeof p);
     p.in = in; p.out = out;
+    p.unit_count = h->debug_unit_count;
     p.in_frame = pi.in_frame_bytes; p.out_frame = pi.out_frame_bytes;
     p.upf = c.upf;
     p.n_units = n * c.upf;
@@ -800,6 +802,19 @@ DS_API int ds_set_band_bytes(ds_handle* h, int64_t target) {
     h->band_target = target;
     const int crc = configure_fused(h);
     return crc ? crc : configure_general(h);
+}
+
+DS_API int ds_set_debug_counter(ds_handle* h, uint32_t* counts) {
+    if (!h) return DS_EINVAL;
+    h->debug_unit_count = counts;
+    return DS_OK;
+}
+
+DS_API int64_t ds_units(const ds_handle* h, int64_t n, int32_t kernel) {
+    if (!h || n < 0) return -1;
+    if (kernel == DS_KERNEL_FUSED) return h->plan.fused_eligible ? n * pick_cfg(h, n).plan.units_per_frame : -1;
+    if (kernel == DS_KERNEL_FUSED_GENERAL) return h->general.valid ? n * h->general.upf : -1;
+    return -1;
 }
 
 DS_API int ds_launch_shape(const ds_handle* h, int64_t n, int32_t* grid, int32_t* block,

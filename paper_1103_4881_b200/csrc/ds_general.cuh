@@ -49,6 +49,7 @@ struct GenStage {
 struct GeneralParams {
     const uint8_t* in;
     uint8_t* out;
+    uint32_t* unit_count;      // debug: +1 per unit processed, else null
     int64_t in_frame, out_frame, n_units;
     int32_t upf, n_planes, stages, stage_stride, mid_stride, out_stride;
     GenPlane pl[DS_MAX_PLANES];
@@ -312,6 +313,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, NCW == 8 ? 3 : 1)
             }
         }
         uint8_t* dst = p.out + cur.f * p.out_frame + P.out_off + (int64_t)band * P.unit_out;
+        if (p.unit_count != nullptr && tid == 0) atomicAdd(p.unit_count + cur.u, 1u);
         if (P.bulk_store) {
             fence_proxy_async_smem();
             named_bar_sync(1, NC);                  // output band complete; mid free

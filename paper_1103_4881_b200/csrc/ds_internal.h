@@ -80,6 +80,7 @@ struct ds_handle {
     dsi::FusedCfg fused, fine;
     dsi::GeneralCfg general;
     int kernel_pref = DS_KERNEL_AUTO;
+    uint32_t* debug_unit_count = nullptr;   // ds_set_debug_counter
     std::atomic<int> last_kernel{DS_KERNEL_AUTO};
     // ds_run_host / ds_run_schedule state (lazily allocated, guarded by host_mu)
     std::mutex host_mu;

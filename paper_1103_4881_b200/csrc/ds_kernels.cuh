@@ -40,6 +40,7 @@ struct FusedPlane {
 struct FusedParams {
     const uint8_t* in;
     uint8_t* out;
+    uint32_t* unit_count;      // debug (ds_set_debug_counter): +1 per unit processed, else null
     int64_t in_frame, out_frame;
     int64_t n_units;           // n_frames * units_per_frame
     int32_t upf;               // units per frame
@@ -326,6 +327,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32)
         if (lane == 0) mbar_arrive(&empty[s]);
 
         uint8_t* dst = p.out + cur.f * p.out_frame + P.out_off + (int64_t)band * P.unit_out;
+        if (p.unit_count != nullptr && tid == 0) atomicAdd(p.unit_count + cur.u, 1u);
         if (P.bulk_store) {
             fence_proxy_async_smem();      // generic-proxy smem writes -> async proxy
             named_bar_sync(1, NC);

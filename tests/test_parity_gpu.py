@@ -513,3 +513,34 @@ def test_fused_kernel_fuzz():
         assert d.last_kernel() == FUSED
         _assert_same(y.cpu().numpy(), want, f"trial {trial}: {W}x{H}x{ch} chroma={chroma} n={n} "
                                               f"band={band} off={off}")
+
+
+@pytest.mark.parametrize("kernel", [FUSED, ds.DS_KERNEL_FUSED_GENERAL])
+def test_every_unit_processed_exactly_once(kernel):
+    """Debug unit accounting (ds_set_debug_counter): over many frame counts,
+    band sizes and ring/CTA tunings, the persistent schedule processes every
+    work unit exactly once."""
+    W, H = 1920, 1080
+    d = ds.Downscaler(W, H, 3)
+    d.set_kernel(kernel)
+    L = ds.lib()
+    x = ds.generate_frames(40, d.in_frame_bytes, seed=2)
+    rng = np.random.default_rng(1)
+    for trial in range(12):
+        n = int(rng.integers(1, 41))
+        if kernel == FUSED and trial % 3 == 1:
+            d.set_band_bytes(int(rng.choice([0, 8000, 16000, 64000])))
+        if kernel == FUSED and trial % 3 == 2:
+            d.set_tuning(int(rng.integers(2, 7)), int(rng.integers(0, 3)))
+        units = L.ds_units(d.handle, n, kernel)
+        assert units > 0
+        counts = torch.zeros(units, dtype=torch.int32, device="cuda")
+        assert L.ds_set_debug_counter(d.handle, counts.data_ptr()) == 0
+        y = d(x[:n])
+        torch.cuda.synchronize()
+        assert L.ds_set_debug_counter(d.handle, None) == 0
+        assert d.last_kernel() == kernel
+        c = counts.cpu().numpy()
+        assert (c == 1).all(), (trial, n, int((c == 0).sum()), int((c > 1).sum()))
+    _assert_same(y.cpu().numpy(), oracle.execute_frames(synth.random_frames(2, 0, n, W, H), W, H),
+                 "after accounting")
