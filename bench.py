@@ -34,6 +34,9 @@ CONFIGS = {
     "4k420": dict(w=3840, h=2160, channels=3, chroma=1, label="4K 3840x2160 YUV 4:2:0"),
     "4k444": dict(w=3840, h=2160, channels=3, chroma=0, label="4K 3840x2160 YUV 4:4:4"),
     "cif420": dict(w=352, h=288, channels=3, chroma=1, label="CIF 352x288 YUV 4:2:0"),
+    # rows that are not 16-byte multiples (chroma 360 / 88 B): K-N1g with staged rows
+    "sd420": dict(w=720, h=576, channels=3, chroma=1, label="PAL SD 720x576 YUV 4:2:0"),
+    "qcif420": dict(w=176, h=144, channels=3, chroma=1, label="QCIF 176x144 YUV 4:2:0"),
 }
 FALLBACK_HBM_GBS = 6650.0   # B200_PROFILING.md fallback, only if MEASURED_PEAKS.json is absent
 
@@ -481,8 +484,9 @@ def main():
             "roofline": {
                 "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic,
-                "kernel": "ds_fused_band_kernel" if kernel_used == ds.DS_KERNEL_FUSED
-                          else "ds_generic_kernel",
+                "kernel": {ds.DS_KERNEL_FUSED: "ds_fused_band_kernel",
+                           ds.DS_KERNEL_FUSED_GENERAL: "ds_fused_general_kernel"}.get(
+                               kernel_used, "ds_generic_kernel"),
                 "algorithmic_bytes_per_launch": alg_bytes,
                 "bytes_rule": "per frame (8/9)*in + out: input rows 9g+4 carry zero V weight "
                               "(S:540) and are not required; see DESIGN.md",

@@ -153,10 +153,10 @@ int make_plan(int32_t W, int32_t H, int32_t channels, const ds_filter_spec* spec
             want = 8LL * k0 * pi.in_w[0] - 1;      // next smaller luma band
         }
     }
-    // K-N1g (any spec): whole-width staged rows need 16-byte rows; bands of
-    // k V repetitions stage R = Sv (k-1) + Pv rows (band + halo).
-    bool general = true;
-    for (int p = 0; p < channels && general; ++p) general = (pi.in_w[p] % 16 == 0);
+    // K-N1g (any spec, any width): bands of k V repetitions stage
+    // R = Sv (k-1) + Pv rows (band + halo) -- by TMA when rows are 16-byte
+    // multiples, else by the producer warp with plain loads.
+    bool general = true;         // any width: unaligned rows are staged with plain loads
     if (general) {
         int64_t units = 0, smax = 0, mmax = 0, omax = 0;
         for (int p = 0; p < channels; ++p) {
@@ -438,6 +438,7 @@ int launch_general(ds_handle* h, const uint8_t* in, int64_t n, uint8_t* out, cud
     p.h = gen_stage(sp.h);
     p.v = gen_stage(sp.v);
     const bool out_al = aligned16(out) && pi.out_frame_bytes % 16 == 0;
+    const bool in_al = aligned16(in);
     int32_t start = 0;
     for (int q = 0; q < pi.n_planes; ++q) {
         ds::GenPlane& P = p.pl[q];
@@ -457,6 +458,8 @@ int launch_general(ds_handle* h, const uint8_t* in, int64_t n, uint8_t* out, cud
         P.unit_start = start;
         P.unit_out = sp.v.outputs * P.k * P.Wm;
         P.bulk_store = (out_al && P.out_off % 16 == 0 && P.unit_out % 16 == 0) ? 1 : 0;
+        P.coop = (in_al && P.W % 16 == 0 && P.in_off % 16 == 0 && pi.in_frame_bytes % 16 == 0) ? 0 : 1;
+        P.row4 = (P.W % 4 == 0) ? 1 : 0;
         start += (P.H / sp.v.paving) / P.k;
     }
     const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(p.n_units, (int64_t)c.grid_per_sm * h->sm_count));
@@ -491,9 +494,11 @@ int launch_generic(ds_handle* h, const uint8_t* in, int64_t n, uint8_t* out, cud
     return cudaGetLastError() == cudaSuccess ? DS_OK : DS_ECUDA;
 }
 
+// K-N1 needs 16-byte rows and a 16-byte-aligned input (TMA); K-N1g stages
+// unaligned rows itself; K-N2 takes whatever neither can (no smem fit).
 int choose_kernel(const ds_handle* h, const uint8_t* in) {
-    if (h->kernel_pref == DS_KERNEL_GENERIC || !aligned16(in)) return DS_KERNEL_GENERIC;
-    const bool k1 = h->plan.fused_eligible && h->fused.valid;
+    if (h->kernel_pref == DS_KERNEL_GENERIC) return DS_KERNEL_GENERIC;
+    const bool k1 = h->plan.fused_eligible && h->fused.valid && aligned16(in);
     const bool k1g = h->plan.fused_general_eligible && h->general.valid;
     if (h->kernel_pref == DS_KERNEL_FUSED) return k1 ? DS_KERNEL_FUSED : DS_KERNEL_GENERIC;
     if (h->kernel_pref == DS_KERNEL_FUSED_GENERAL) return k1g ? DS_KERNEL_FUSED_GENERAL : DS_KERNEL_GENERIC;

@@ -35,6 +35,8 @@ struct GenPlane {
     int32_t unit_start;
     int32_t unit_out;          // Qv * k * Wm
     int32_t bulk_store;
+    int32_t coop;              // 1: rows staged by the producer warp with plain loads
+    int32_t row4;              // 1: W % 4 == 0 (smem rows word-aligned: dp4a window path)
 };
 
 struct GenStage {
@@ -130,6 +132,38 @@ __device__ __forceinline__ void g_v_quad(const GenStage& g, const uint8_t* mb, i
     }
 }
 
+// Producer-warp staging of `left` rows starting at `row` (mod H) for planes
+// the TMA cannot copy; out of line so its registers do not count against the
+// consumer path.
+__device__ __forceinline__ void g_coop_stage(uint8_t* dst, const uint8_t* plane, int row, int left, int H,
+                                          int W, int lane) {
+    while (left > 0) {
+        const int seg = min(left, H - row);
+        const uint8_t* src = plane + (int64_t)row * W;
+        const int64_t nb = (int64_t)seg * W;
+        if ((((uintptr_t)src | (uintptr_t)dst | (uintptr_t)nb) & 3) == 0) {
+            const uint32_t* s4 = reinterpret_cast<const uint32_t*>(src);
+            uint32_t* d4 = reinterpret_cast<uint32_t*>(dst);
+            const int64_t n4 = nb >> 2;
+            int64_t x = lane;
+            for (; x + 96 < n4; x += 128) {             // 4 loads in flight per lane
+                const uint32_t a = __ldg(s4 + x), b = __ldg(s4 + x + 32), c = __ldg(s4 + x + 64),
+                               d = __ldg(s4 + x + 96);
+                d4[x] = a;
+                d4[x + 32] = b;
+                d4[x + 64] = c;
+                d4[x + 96] = d;
+            }
+            for (; x < n4; x += 32) d4[x] = __ldg(s4 + x);
+        } else {
+            for (int64_t x = lane; x < nb; x += 32) dst[x] = __ldg(src + x);
+        }
+        dst += nb;
+        left -= seg;
+        row = 0;
+    }
+}
+
 struct GenCursor {
     int64_t u, f;
     int32_t local, gdiv, gmod, upf;
@@ -157,7 +191,7 @@ struct GenCursor {
 // <8>: register cap (<= 75) so two CTAs fit per SM -- the register file is
 // split across 4 SMSPs, so 18 warps need <= 102 registers each; <16>: one CTA.
 template <int NCW>
-__global__ void __launch_bounds__((NCW + 1) * 32, NCW == 8 ? 3 : 1)
+__global__ void __launch_bounds__((NCW + 1) * 32, NCW == 8 ? 2 : 1)
     ds_fused_general_kernel(const __grid_constant__ GeneralParams p) {
     extern __shared__ __align__(1024) uint8_t smem[];
     constexpr int NC = NCW * 32;
@@ -189,28 +223,39 @@ __global__ void __launch_bounds__((NCW + 1) * 32, NCW == 8 ? 3 : 1)
     int s = 0;
     uint32_t phase = 0;
     if (warp == NCW) {
-        if (lane == 0) {
-            const uint64_t pol = policy_evict_first();
-            bool first_round = true;
-            for (; cur.u < p.n_units; cur.next()) {
-                if (!first_round) mbar_wait(&empty[s], phase ^ 1);
-                const GenPlane& P = p.pl[cur.plane(p)];
-                const int band = cur.local - P.unit_start;
-                const uint8_t* plane = p.in + cur.f * p.in_frame + P.in_off;
-                uint8_t* dst = ring + (size_t)s * p.stage_stride;
-                mbar_arrive_expect_tx(&full[s], (uint32_t)P.R * (uint32_t)P.W);
-                // rows ov + Sv*k*band .. + R-1, modulo H, in non-wrapping segments
-                int row = (int)(((int64_t)P.ov + (int64_t)p.v.S * P.k * band) % P.H);
-                int left = P.R;
-                while (left > 0) {
-                    const int seg = min(left, P.H - row);
-                    bulk_g2s(dst, plane + (int64_t)row * P.W, (uint32_t)seg * (uint32_t)P.W, &full[s], pol);
-                    dst += (size_t)seg * P.W;
-                    left -= seg;
-                    row = 0;
+        // ---------------- producer warp: band + halo rows into the ring.
+        // Bulk-copy planes: lane 0 issues one TMA copy per non-wrapping
+        // segment.  Planes whose rows are not 16-byte aligned (or a
+        // misaligned input pointer): all 32 lanes copy with plain loads and
+        // lane 0 arrives on full[s] without a transaction count.
+        const uint64_t pol = policy_evict_first();
+        bool first_round = true;
+        for (; cur.u < p.n_units; cur.next()) {
+            if (!first_round) mbar_wait(&empty[s], phase ^ 1);
+            const GenPlane& P = p.pl[cur.plane(p)];
+            const int band = cur.local - P.unit_start;
+            const uint8_t* plane = p.in + cur.f * p.in_frame + P.in_off;
+            uint8_t* dst = ring + (size_t)s * p.stage_stride;
+            // rows ov + Sv*k*band .. + R-1, modulo H, in non-wrapping segments
+            int row = (int)(((int64_t)P.ov + (int64_t)p.v.S * P.k * band) % P.H);
+            int left = P.R;
+            if (!P.coop) {
+                if (lane == 0) {
+                    mbar_arrive_expect_tx(&full[s], (uint32_t)P.R * (uint32_t)P.W);
+                    while (left > 0) {
+                        const int seg = min(left, P.H - row);
+                        bulk_g2s(dst, plane + (int64_t)row * P.W, (uint32_t)seg * (uint32_t)P.W, &full[s], pol);
+                        dst += (size_t)seg * P.W;
+                        left -= seg;
+                        row = 0;
+                    }
                 }
-                if (++s == S) { s = 0; phase ^= 1; first_round = false; }
+            } else {
+                g_coop_stage(dst, plane, row, left, P.H, P.W, lane);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&full[s]);      // release: generic smem writes
             }
+            if (++s == S) { s = 0; phase ^= 1; first_round = false; }
         }
         return;
     }
@@ -236,7 +281,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, NCW == 8 ? 3 : 1)
                 int c0 = P.oh + SH * r1;
                 if (c0 >= W) c0 -= W;                 // oh < W and Sh*r1 < W
                 uint8_t* mo = mrow + QH * r1;
-                if (p.h.s8 && c0 + PH <= W) {
+                if (p.h.s8 && P.row4 && c0 + PH <= W) {
                     // window of nw+1 aligned words (bytes past the row meet zero taps)
                     const uint8_t* wb = rowp + (c0 & ~3);
                     const uint32_t sel = 0x3210u + 0x1111u * (uint32_t)(c0 & 3);

@@ -134,9 +134,12 @@ def test_plan_generic_spec_not_fused():
     assert p.general_stage_bytes_max == (9 * (k - 1) + 9) * 48
 
 
-def test_plan_general_needs_16_byte_rows():
-    p = ds.ds_plan(40, 45, 1)                      # W % 16 != 0
-    assert p.fused_eligible == 0 and p.fused_general_eligible == 0
+def test_plan_unaligned_rows_go_to_the_general_fused_kernel():
+    # W % 16 != 0: K-N1 (TMA rows) cannot run it; K-N1g stages the rows itself
+    p = ds.ds_plan(40, 45, 1)
+    assert p.fused_eligible == 0 and p.fused_general_eligible == 1
+    p = ds.ds_plan(720, 576, 3)                    # PAL SD 4:2:0: chroma rows are 360 B
+    assert p.fused_eligible == 0 and p.fused_general_eligible == 1
 
 
 def test_create_validates_before_touching_cuda():

@@ -147,14 +147,16 @@ def test_4k_frames(chroma):
 # --------------------------------------------------------- ragged shapes --
 @pytest.mark.parametrize("W,H,ch", [(16, 9, 1), (32, 18, 3), (400, 9, 1), (48, 99, 1),
                                     (40, 45, 1), (208, 90, 3), (1504, 54, 3), (2000, 27, 1),
-                                    (176, 144, 3), (8, 9, 1), (720, 576, 3)])
+                                    (176, 144, 3), (8, 9, 1), (720, 576, 3), (24, 9, 1),
+                                    (1440, 1080, 3), (720, 486, 3)])
 def test_ragged_geometries(W, H, ch):
     """Widths that are / are not multiples of 16 (K-N1 vs K-N2 auto choice),
     band counts that leave a ragged tail over the persistent grid."""
     d = ds.Downscaler(W, H, ch)
     fr = synth.random_frames(W + H, 0, 7, W, H, ch, 1)
     got = _run(d, fr)
-    want_kernel = FUSED if d.plan.fused_eligible else GENERIC
+    want_kernel = (FUSED if d.plan.fused_eligible else
+                   ds.DS_KERNEL_FUSED_GENERAL if d.plan.fused_general_eligible else GENERIC)
     assert d.last_kernel() == want_kernel
     _assert_same(got, oracle.execute_frames(fr, W, H, ch, 1), f"{W}x{H}x{ch}")
 
@@ -265,8 +267,9 @@ def test_general_kernel_fuzz_random_specs():
 
 # ------------------------------------------------------- alignment / API --
 def test_misaligned_pointers():
-    """Misaligned input selects K-N2; misaligned output makes K-N1 fall back
-    to cooperative stores -- results identical, never an error."""
+    """Misaligned input moves off K-N1 (TMA needs 16-byte sources) to K-N1g,
+    which stages the rows with plain loads; misaligned output makes K-N1 fall
+    back to cooperative stores -- results identical, never an error."""
     W, H = 352, 288
     d = ds.Downscaler(W, H, 3)
     fr = synth.random_frames(2, 0, 3, W, H)
@@ -278,8 +281,15 @@ def test_misaligned_pointers():
     y = obuf[3: 3 + want.size]
     ds.ds_run(d.handle, x.data_ptr(), 3, y.data_ptr(), torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
-    assert d.last_kernel() == GENERIC
+    assert d.last_kernel() == ds.DS_KERNEL_FUSED_GENERAL
     _assert_same(y.cpu().numpy().reshape(want.shape), want, "misaligned in")
+    d.set_kernel(GENERIC)
+    y.zero_()
+    ds.ds_run(d.handle, x.data_ptr(), 3, y.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert d.last_kernel() == GENERIC
+    _assert_same(y.cpu().numpy().reshape(want.shape), want, "misaligned in, K-N2")
+    d.set_kernel(ds.DS_KERNEL_AUTO)
     x2 = torch.from_numpy(fr).cuda()
     ds.ds_run(d.handle, x2.data_ptr(), 3, y.data_ptr(), torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
@@ -432,12 +442,15 @@ def test_cuda_graph_capture():
 
 
 @pytest.mark.parametrize("kernel", [FUSED, ds.DS_KERNEL_FUSED_GENERAL, GENERIC])
-@pytest.mark.parametrize("W,H,ch,n", [(1920, 1080, 3, 3), (352, 288, 3, 5), (48, 27, 1, 4)])
+@pytest.mark.parametrize("W,H,ch,n", [(1920, 1080, 3, 3), (352, 288, 3, 5), (48, 27, 1, 4),
+                                      (720, 576, 3, 2), (176, 144, 3, 3)])
 def test_every_output_byte_written(kernel, W, H, ch, n):
     """compute-sanitizer is closed on this pool; instead, outputs pre-filled
     with two different sentinels must both come back equal to the oracle, so
     every output byte is written by the kernel (and nothing else is)."""
     d = ds.Downscaler(W, H, ch)
+    if kernel == FUSED and not d.plan.fused_eligible:
+        pytest.skip("K-N1 needs 16-byte rows in every plane")
     d.set_kernel(kernel)
     fr = synth.random_frames(31, 0, n, W, H, ch, 1)
     want = oracle.execute_frames(fr, W, H, ch, 1)
