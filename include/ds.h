@@ -171,7 +171,7 @@ DS_API int ds_run(ds_handle* h, const uint8_t* in_frames, int64_t n_frames,
 DS_API int ds_run_host(ds_handle* h, const uint8_t* host_in, int64_t n_frames,
                        uint8_t* host_out, ds_stream_t stream);
 
-/* Frames per chunk for ds_run_host (0 = automatic, ~32 MiB per chunk). */
+/* Frames per chunk for ds_run_host (0 = automatic, ~96 MiB per chunk). */
 DS_API int ds_set_host_chunk(ds_handle* h, int64_t frames_per_chunk);
 
 /* Release the handle and its staging buffers (synchronises them).

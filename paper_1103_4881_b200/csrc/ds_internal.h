@@ -16,7 +16,7 @@ constexpr int64_t kUnitTargetBytes = 32 * 1024;     // K-N1 band size target (by
 constexpr int64_t kInFlightTarget = 120 * 1024;     // K-N1 bytes in flight per SM (measured
                                                     // optimum of tools/bw_probe tma_read)
 constexpr int kSmemLimit = 227 * 1024;              // per-CTA opt-in maximum
-constexpr int64_t kHostChunkBytes = 32LL << 20;     // ds_run_host chunk target
+constexpr int64_t kHostChunkBytes = 96LL << 20;     // ds_run_host chunk target (tools/e2e_sweep.py)
 
 struct HostSlot {
     uint8_t* d_in = nullptr;
