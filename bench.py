@@ -179,6 +179,17 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
+def ncu_dram_rate(config_key):
+    """DRAM GB/s of the committed ncu capture (read + write bytes / ncu duration)."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(p) as f:
+            e = json.load(f)[config_key]
+        return e["dram_bytes_per_launch"] / (e["duration_us_under_ncu"] * 1e-6) / 1e9
+    except Exception:
+        return None
+
+
 def ncu_traffic(config_key, frames_per_launch):
     """Per-launch DRAM bytes from the committed ncu --set full summary of this
     config (profiles/ncu_summary.json), scaled per frame if the captured
@@ -495,6 +506,9 @@ def main():
                 "traffic_source": traffic_src,
                 "effective_gbs_full_in_out": eff_full,
                 "pct_of_8tbps_nominal_full_in_out": eff_full / 8000.0,
+                "ncu_dram_gbs": ncu_dram_rate(args.config),
+                "ncu_dram_pct_of_8tbps": (ncu_dram_rate(args.config) or 0) / 8000.0 or None,
+                "ncu_dram_pct_of_measured_copy": (ncu_dram_rate(args.config) or 0) / peak or None,
             },
             "cpu_baseline": cpu,
             "e2e": e2e,
