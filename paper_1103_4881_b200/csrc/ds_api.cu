@@ -126,22 +126,28 @@ int make_plan(int32_t W, int32_t H, int32_t channels, const ds_filter_spec* spec
     // dead row 4 of every 9-row group) and every plane width a multiple of
     // 16 (two packets per 16-byte vector; 16-byte-aligned bulk copies).
     bool fused = stage_equal(spec.h, def.h) && stage_equal(spec.v, def.v);
-    for (int p = 0; p < channels && fused; ++p) fused = (pi.in_w[p] % 16 == 0);
+    // planes with W % 16 == 8 ("narrow") are staged as whole bands from a
+    // 16-aligned superset, which needs 16-aligned frames
+    bool any_narrow = false;
+    for (int p = 0; p < channels; ++p) any_narrow |= (pi.in_w[p] % 16 != 0);
+    if (any_narrow && pi.in_frame_bytes % 16 != 0) fused = false;
     if (fused) {
+        // staged bytes per 9-row group: 8 live rows, or all 9 for narrow planes
+        auto per_group = [&](int p) { return (pi.in_w[p] % 16 == 0 ? 8LL : 9LL) * pi.in_w[p]; };
         // shrink the band target until a 2-deep ring fits one CTA's shared
         // memory (a caller's large ds_set_band_bytes never loses K-N1)
         const int G0 = pi.in_h[0] / 9;
         int64_t want = unit_target;
         for (;;) {
-            const int k0 = largest_divisor_below(G0, 8LL * pi.in_w[0], want);
-            const int64_t target = 8LL * k0 * pi.in_w[0];
+            const int k0 = largest_divisor_below(G0, per_group(0), want);
+            const int64_t target = per_group(0) * k0;
             int64_t units = 0, umax = 0, omax = 0;
             for (int p = 0; p < channels; ++p) {
                 const int G = pi.in_h[p] / 9;
-                const int k = p == 0 ? k0 : closest_divisor(G, 8LL * pi.in_w[p], target);
+                const int k = p == 0 ? k0 : closest_divisor(G, per_group(p), target);
                 pi.band_groups[p] = k;
                 units += G / k;
-                umax = std::max<int64_t>(umax, 8LL * k * pi.in_w[p]);
+                umax = std::max<int64_t>(umax, per_group(p) * k + (pi.in_w[p] % 16 ? 16 : 0));
                 omax = std::max<int64_t>(omax, 4LL * k * pi.out_w[p]);
             }
             pi.units_per_frame = units;
@@ -150,8 +156,13 @@ int make_plan(int32_t W, int32_t H, int32_t channels, const ds_filter_spec* spec
             fused = fused_smem_bytes(2, (int32_t)round_up(umax, 128), (int32_t)round_up(omax, 128)) <=
                     kSmemLimit;
             if (fused || k0 == 1) break;
-            want = 8LL * k0 * pi.in_w[0] - 1;      // next smaller luma band
+            want = per_group(0) * k0 - 1;      // next smaller luma band
         }
+    }
+    pi.fused_eligible = fused ? 1 : 0;
+    if (!fused) {
+        for (int p = 0; p < DS_MAX_PLANES; ++p) pi.band_groups[p] = 0;
+        pi.units_per_frame = pi.unit_in_bytes_max = pi.unit_out_bytes_max = 0;
     }
     // K-N1g (any spec, any width): bands of k V repetitions stage
     // R = Sv (k-1) + Pv rows (band + halo) -- by TMA when rows are 16-byte
@@ -190,11 +201,6 @@ int make_plan(int32_t W, int32_t H, int32_t channels, const ds_filter_spec* spec
         for (int p = 0; p < DS_MAX_PLANES; ++p) pi.general_band_reps[p] = 0;
         pi.general_units_per_frame = pi.general_stage_bytes_max = 0;
     }
-    pi.fused_eligible = fused ? 1 : 0;
-    if (!fused) {
-        for (int p = 0; p < DS_MAX_PLANES; ++p) pi.band_groups[p] = 0;
-        pi.units_per_frame = pi.unit_in_bytes_max = pi.unit_out_bytes_max = 0;
-    }
     *info = pi;
     if (spec_out) *spec_out = spec;
     return DS_OK;
@@ -208,7 +214,7 @@ int make_plan(int32_t W, int32_t H, int32_t channels, const ds_filter_spec* spec
 int max_tasks(const ds_plan_info& pi) {
     int t = 0;
     for (int p = 0; p < pi.n_planes; ++p)
-        t = std::max(t, 2 * pi.band_groups[p] * (pi.in_w[p] / 16));
+        t = std::max(t, 2 * pi.band_groups[p] * ((pi.in_w[p] + 15) / 16));
     return t;
 }
 
@@ -330,11 +336,12 @@ int launch_fused(ds_handle* h, const uint8_t* in, int64_t n, uint8_t* out, cudaS
         P.W = pi.in_w[q];
         P.Wout = pi.out_w[q];
         P.k = pi.band_groups[q];
-        P.chunks = P.W / 16;
+        P.narrow = (P.W % 16 != 0) ? 1 : 0;
+        P.chunks = (P.W + 15) / 16;
         P.tasks = 2 * P.k * P.chunks;
         P.chunks_rcp = P.chunks > 1 ? (uint32_t)((0x100000000ULL + P.chunks - 1) / P.chunks) : 0u;
         P.unit_start = start;
-        P.unit_in = 8 * P.k * P.W;
+        P.unit_in = (P.narrow ? 9 : 8) * P.k * P.W;
         P.unit_out = 4 * P.k * P.Wout;
         P.bulk_store = (out_al && P.out_off % 16 == 0 && P.unit_out % 16 == 0) ? 1 : 0;
         start += pi.in_h[q] / (9 * P.k);

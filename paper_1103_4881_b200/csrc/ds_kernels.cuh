@@ -35,6 +35,10 @@ struct FusedPlane {
     int32_t unit_out;          // bytes produced per unit = 4 * k * Wout
     int32_t bulk_store;        // 1: TMA bulk store legal (16 B aligned)
     uint32_t chunks_rcp;       // ceil(2^32 / chunks) (chunks > 1): t / chunks = umulhi(t, rcp)
+    int32_t narrow;            // 1: W % 16 == 8 -- the whole band (dead rows included) is
+                               // bulk-copied from a 16-aligned superset; rows are 8-aligned
+                               // in smem, the last chunk of a row holds one packet
+    int32_t reserved_;
 };
 
 struct FusedParams {
@@ -147,6 +151,15 @@ __device__ __forceinline__ uint4 lds128(const uint8_t* p) {
                  : "r"(smem_u32(p)));
     return v;
 }
+__device__ __forceinline__ uint2 lds64(const uint8_t* p) {
+    uint2 v;
+    asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(smem_u32(p)));
+    return v;
+}
+__device__ __forceinline__ void sts8(uint8_t* p, uint32_t v) {
+    asm volatile("st.shared.u8 [%0], %1;" ::"r"(smem_u32(p)), "h"((unsigned short)(v & 0xff))
+                 : "memory");
+}
 __device__ __forceinline__ void sts16(uint8_t* p, uint32_t v) {
     asm volatile("st.shared.u16 [%0], %1;" ::"r"(smem_u32(p)), "h"((unsigned short)v)
                  : "memory");
@@ -181,6 +194,30 @@ __device__ __forceinline__ void h_chunk(uint4 v, uint32_t& q0, uint32_t& q1, uin
 template <uint32_t WA, uint32_t WB>
 __device__ __forceinline__ uint32_t v_pair(uint32_t qa, uint32_t qb) {
     return qa * (32u * WA) + qb * (32u * WB) + 0x00800080u;
+}
+
+// One consumer task: 4 slot rows x 16 bytes -> H task -> two V output rows of
+// 6 bytes (lo = bytes 0..3, hi = bytes 4..5).  V taps: half 0 ->
+// out0 rows (0,1) w (3,5), out1 rows (2,3) w (1,7); half 1 -> out2 rows
+// (5,6) w (7,1), out3 rows (7,8) w (5,3).
+__device__ __forceinline__ void k1_task(const uint4 (&r)[4], int half, uint32_t (&lo)[2],
+                                        uint32_t (&hi)[2]) {
+    uint32_t q[4][3];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) h_chunk(r[j], q[j][0], q[j][1], q[j][2]);
+    const uint32_t wa0 = half ? 32u * 7 : 32u * 3, wb0 = half ? 32u * 1 : 32u * 5;
+    const uint32_t wa1 = half ? 32u * 5 : 32u * 1, wb1 = half ? 32u * 3 : 32u * 7;
+    uint32_t o[2][3];
+#pragma unroll
+    for (int e = 0; e < 3; ++e) {
+        o[0][e] = q[0][e] * wa0 + q[1][e] * wb0 + 0x00800080u;
+        o[1][e] = q[2][e] * wa1 + q[3][e] * wb1 + 0x00800080u;
+    }
+#pragma unroll
+    for (int kk = 0; kk < 2; ++kk) {
+        lo[kk] = __byte_perm(o[kk][0], o[kk][1], 0x7531);
+        hi[kk] = __byte_perm(o[kk][2], 0u, 0x4431);
+    }
 }
 
 // ------------------------------------------------------------------- K-N1 --
@@ -260,6 +297,17 @@ __global__ void __launch_bounds__((NCW + 1) * 32)
                 const uint8_t* src =
                     p.in + cur.f * p.in_frame + P.in_off + (int64_t)band * 9 * P.k * P.W;
                 uint8_t* dst = ring + (size_t)s * p.stage_stride;
+                if (P.narrow) {
+                    // one copy of the whole band from its 16-aligned superset: the
+                    // start is at most 8 bytes into the previous band (never before
+                    // the buffer: frames are 16-aligned), the end at most 15 bytes
+                    // past the band (never past the buffer, whose end is aligned)
+                    const uintptr_t a = reinterpret_cast<uintptr_t>(src);
+                    const uintptr_t a0 = a & ~uintptr_t(15);
+                    const uintptr_t a1 = (a + (uintptr_t)9 * P.k * P.W + 15) & ~uintptr_t(15);
+                    mbar_arrive_expect_tx(&full[s], (uint32_t)(a1 - a0));
+                    bulk_g2s(dst, reinterpret_cast<const uint8_t*>(a0), (uint32_t)(a1 - a0), &full[s], pol);
+                } else {
                 mbar_arrive_expect_tx(&full[s], (uint32_t)P.unit_in);
                 // live rows of the band: 0..3 | 5..12 | 14..21 | ... | 9k-4..9k-1.
                 // Rows 5..8 of group g and 0..3 of group g+1 are contiguous both in
@@ -272,6 +320,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32)
                              2u * half, &full[s], pol);                                   // rows 5..8 | 0..3
                 bulk_g2s(dst + (size_t)(8 * P.k - 4) * P.W, src + (int64_t)(9 * P.k - 4) * P.W, half,
                          &full[s], pol);                                                  // last rows 5..8
+                }
                 if (++s == S) { s = 0; phase ^= 1; first_round = false; }
             }
         }
@@ -290,36 +339,57 @@ __global__ void __launch_bounds__((NCW + 1) * 32)
 
         mbar_wait(&full[s], phase);
 
-        for (int t = tid; t < tasks; t += NC) {
-            const int hg = chunks == 1 ? t : (int)__umulhi((uint32_t)t, rcp);   // t / chunks
-            const int c = t - hg * chunks;
-            const int half = hg & 1;
-            const uint8_t* base = st + (size_t)4 * hg * W + 16 * c;
-            uint4 r[4];
+        if (!P.narrow) {
+            for (int t = tid; t < tasks; t += NC) {
+                const int hg = chunks == 1 ? t : (int)__umulhi((uint32_t)t, rcp);   // t / chunks
+                const int c = t - hg * chunks;
+                const uint8_t* base = st + (size_t)4 * hg * W + 16 * c;
+                uint4 r[4];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) r[j] = lds128(base + (size_t)j * W);
-            uint32_t q[4][3];
+                for (int j = 0; j < 4; ++j) r[j] = lds128(base + (size_t)j * W);
+                uint32_t lo[2], hi[2];
+                k1_task(r, hg & 1, lo, hi);
+                uint8_t* orow = ob + (size_t)2 * hg * Wout + 6 * c;
 #pragma unroll
-            for (int j = 0; j < 4; ++j) h_chunk(r[j], q[j][0], q[j][1], q[j][2]);
-            // V taps: half 0 -> out0 rows (0,1) w (3,5), out1 rows (2,3)
-            // w (1,7); half 1 -> out2 rows (5,6) w (7,1), out3 rows (7,8) w (5,3).
-            const uint32_t wa0 = half ? 32u * 7 : 32u * 3, wb0 = half ? 32u * 1 : 32u * 5;
-            const uint32_t wa1 = half ? 32u * 5 : 32u * 1, wb1 = half ? 32u * 3 : 32u * 7;
-            uint32_t o[2][3];
-#pragma unroll
-            for (int e = 0; e < 3; ++e) {
-                o[0][e] = q[0][e] * wa0 + q[1][e] * wb0 + 0x00800080u;
-                o[1][e] = q[2][e] * wa1 + q[3][e] * wb1 + 0x00800080u;
+                for (int kk = 0; kk < 2; ++kk) {
+                    uint8_t* d = orow + (size_t)kk * Wout;
+                    sts16(d, lo[kk]);
+                    sts16(d + 2, lo[kk] >> 16);
+                    sts16(d + 4, hi[kk]);
+                }
             }
-            uint8_t* orow = ob + (size_t)2 * hg * Wout + 6 * c;
+        } else {
+            // narrow plane (W % 16 == 8): slot byte 0 is the band's 16-aligned
+            // superset start; rows are 8-byte aligned; the last chunk of a row
+            // holds one packet; output rows are odd -> byte stores
+            const int nphase = (int)((p.in_frame * cur.f + P.in_off + (int64_t)band * 9 * P.k * W) & 15);
+            for (int t = tid; t < tasks; t += NC) {
+                const int hg = chunks == 1 ? t : (int)__umulhi((uint32_t)t, rcp);   // t / chunks
+                const int c = t - hg * chunks;
+                const int half = hg & 1;
+                const uint8_t* base = st + nphase + (size_t)(9 * (hg >> 1) + 5 * half) * W + 16 * c;
+                uint4 r[4];
 #pragma unroll
-            for (int kk = 0; kk < 2; ++kk) {
-                const uint32_t lo = __byte_perm(o[kk][0], o[kk][1], 0x7531);
-                const uint32_t hi = __byte_perm(o[kk][2], 0u, 0x4431);
-                uint8_t* d = orow + (size_t)kk * Wout;
-                sts16(d, lo);
-                sts16(d + 2, lo >> 16);
-                sts16(d + 4, hi);
+                for (int j = 0; j < 4; ++j) {
+                    const uint2 a = lds64(base + (size_t)j * W), b = lds64(base + (size_t)j * W + 8);
+                    r[j] = make_uint4(a.x, a.y, b.x, b.y);
+                }
+                uint32_t lo[2], hi[2];
+                k1_task(r, half, lo, hi);
+                uint8_t* orow = ob + (size_t)2 * hg * Wout + 6 * c;
+                const bool two = c + 1 < chunks;
+#pragma unroll
+                for (int kk = 0; kk < 2; ++kk) {
+                    uint8_t* d = orow + (size_t)kk * Wout;
+                    sts8(d, lo[kk]);
+                    sts8(d + 1, lo[kk] >> 8);
+                    sts8(d + 2, lo[kk] >> 16);
+                    if (two) {
+                        sts8(d + 3, lo[kk] >> 24);
+                        sts8(d + 4, hi[kk]);
+                        sts8(d + 5, hi[kk] >> 8);
+                    }
+                }
             }
         }
         // every lane of this warp has consumed its reads of slot s

@@ -134,11 +134,15 @@ def test_plan_generic_spec_not_fused():
     assert p.general_stage_bytes_max == (9 * (k - 1) + 9) * 48
 
 
-def test_plan_unaligned_rows_go_to_the_general_fused_kernel():
-    # W % 16 != 0: K-N1 (TMA rows) cannot run it; K-N1g stages the rows itself
-    p = ds.ds_plan(40, 45, 1)
-    assert p.fused_eligible == 0 and p.fused_general_eligible == 1
-    p = ds.ds_plan(720, 576, 3)                    # PAL SD 4:2:0: chroma rows are 360 B
+def test_plan_narrow_rows():
+    # W % 16 == 8 planes (PAL SD / QCIF 4:2:0 chroma: 360 / 88 B rows) stay on K-N1:
+    # whole bands are bulk-copied from a 16-aligned superset (needs 16-aligned frames)
+    p = ds.ds_plan(720, 576, 3)
+    assert p.fused_eligible == 1 and list(p.band_groups) == [4, 8, 8]
+    assert p.unit_in_bytes_max == 9 * 8 * 360 + 16          # 9 rows per group + alignment slack
+    assert ds.ds_plan(176, 144, 3).fused_eligible == 1        # QCIF
+    # frames that are not 16-byte multiples: K-N1g stages the rows itself
+    p = ds.ds_plan(40, 45, 1)                                 # 1,800-byte frames
     assert p.fused_eligible == 0 and p.fused_general_eligible == 1
 
 
