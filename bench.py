@@ -54,7 +54,7 @@ def parse():
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--stages", type=int, default=0)
     ap.add_argument("--ctas", type=int, default=0)
-    ap.add_argument("--kernel", choices=["auto", "fused", "generic"], default="auto")
+    ap.add_argument("--kernel", choices=["auto", "fused", "fused_general", "generic"], default="auto")
     ap.add_argument("--band-bytes", type=int, default=0, help="K-N1 band size (0 = default)")
     ap.add_argument("--graph", action="store_true",
                     help="capture the K timed ds_run calls in one CUDA graph and replay it "
@@ -348,7 +348,8 @@ def main():
     d = ds.Downscaler(cfg["w"], cfg["h"], cfg["channels"], chroma=cfg["chroma"])
     assert d.in_frame_bytes == fin and d.out_frame_bytes == fout
     if args.kernel != "auto":
-        d.set_kernel({"fused": ds.DS_KERNEL_FUSED, "generic": ds.DS_KERNEL_GENERIC}[args.kernel])
+        d.set_kernel({"fused": ds.DS_KERNEL_FUSED, "fused_general": ds.DS_KERNEL_FUSED_GENERAL,
+                      "generic": ds.DS_KERNEL_GENERIC}[args.kernel])
     if args.band_bytes:
         d.set_band_bytes(args.band_bytes)
     if args.stages or args.ctas:

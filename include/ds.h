@@ -111,7 +111,10 @@ typedef struct {
     int32_t out_w[DS_MAX_PLANES], out_h[DS_MAX_PLANES];
     int64_t in_offset[DS_MAX_PLANES];    /* byte offset of each plane in a frame */
     int64_t out_offset[DS_MAX_PLANES];
-    int32_t fused_eligible;              /* 1 if K-N1 can run this geometry+spec */
+    int32_t fused_eligible;              /* 1 if K-N1 can run this geometry+spec:
+                                            SPEC's taps, every plane W % 16 in {0, 8}
+                                            (8 also needs in_frame_bytes % 16 == 0),
+                                            one 9-row group staged within smem      */
     int32_t band_groups[DS_MAX_PLANES];  /* K-N1: 9-row groups per work unit     */
     int64_t units_per_frame;             /* K-N1 work units per frame            */
     int64_t unit_in_bytes_max;           /* K-N1 bytes staged per unit (max)     */

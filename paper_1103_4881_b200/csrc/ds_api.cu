@@ -123,8 +123,9 @@ int make_plan(int32_t W, int32_t H, int32_t channels, const ds_filter_spec* spec
     ds_filter_spec def;
     default_spec(&def);
     // K-N1 eligibility: SPEC's taps (the kernel hard-codes them and skips the
-    // dead row 4 of every 9-row group) and every plane width a multiple of
-    // 16 (two packets per 16-byte vector; 16-byte-aligned bulk copies).
+    // dead row 4 of every 9-row group).  SPEC's H paving makes every width a
+    // multiple of 8: W % 16 == 0 planes stage their 8 live rows per group by
+    // 16-byte-aligned bulk copies, W % 16 == 8 planes as below.
     bool fused = stage_equal(spec.h, def.h) && stage_equal(spec.v, def.v);
     // planes with W % 16 == 8 ("narrow") are staged as whole bands from a
     // 16-aligned superset, which needs 16-aligned frames
