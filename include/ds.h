@@ -122,7 +122,8 @@ typedef struct {
     int32_t fused_general_eligible;      /* 1 if K-N1g can run this geometry+spec  */
     int32_t general_band_reps[DS_MAX_PLANES];  /* K-N1g: V repetitions per unit */
     int64_t general_units_per_frame;
-    int64_t general_stage_bytes_max;     /* K-N1g: staged rows (band + halo) bytes */
+    int64_t general_stage_bytes_max;     /* K-N1g: staged bytes per unit: R rows (band + halo)
+                                            at a pitch of round_up(W, 16) + 32 (wrap pad) */
 } ds_plan_info;
 
 /* Fill *out with SPEC's downscaler (hfilter_8to3 S:527-535, vfilter_9to4

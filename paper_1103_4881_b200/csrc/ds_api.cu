@@ -166,23 +166,25 @@ int make_plan(int32_t W, int32_t H, int32_t channels, const ds_filter_spec* spec
         pi.units_per_frame = pi.unit_in_bytes_max = pi.unit_out_bytes_max = 0;
     }
     // K-N1g (any spec, any width): bands of k V repetitions stage
-    // R = Sv (k-1) + Pv rows (band + halo) -- by TMA when rows are 16-byte
+    // R = Sv (k-1) + Pv rows (band + halo), each at a pitch of
+    // round_up(W, 16) + 32 (row + wrap pad) -- by TMA when rows are 16-byte
     // multiples, else by the producer warp with plain loads.
     bool general = true;         // any width: unaligned rows are staged with plain loads
     if (general) {
         int64_t units = 0, smax = 0, mmax = 0, omax = 0;
         for (int p = 0; p < channels; ++p) {
             const int G = pi.in_h[p] / spec.v.paving;
+            const int64_t pitch = general_pitch(pi.in_w[p]);
             int best = 1;
             for (int d = 1; d <= G; ++d) {
                 if (G % d) continue;
                 const int64_t R = (int64_t)spec.v.paving * (d - 1) + spec.v.pattern;
-                if (R * pi.in_w[p] <= kGeneralStageTarget) best = d;
+                if (R * pitch <= kGeneralStageTarget) best = d;
             }
             const int64_t R = (int64_t)spec.v.paving * (best - 1) + spec.v.pattern;
             pi.general_band_reps[p] = best;
             units += G / best;
-            smax = std::max<int64_t>(smax, R * pi.in_w[p]);
+            smax = std::max<int64_t>(smax, R * pitch);
             mmax = std::max<int64_t>(mmax, (R + 3) * pi.out_w[p]);   // +3: dp4a row blocks
             omax = std::max<int64_t>(omax, (int64_t)spec.v.outputs * best * pi.out_w[p]);
             // exact reciprocal index division: items * divisor < 2^32
@@ -362,6 +364,44 @@ int64_t general_smem(const GeneralCfg& c, int stages) {
     return (int64_t)stages * c.stage_stride + c.mid_stride + 2LL * c.out_stride + 2LL * stages * 8;
 }
 
+// Stage constants for K-N1g.  FASTDIV (M != 0): floor(a / D) = umulhi(a, M)
+// with M = ceil(2^32 / D) is exact for 0 <= a <= amax when amax * e < 2^32,
+// e = M D - 2^32 (the error a e / (D 2^32) stays below 1 / D).  amax is the
+// largest accumulator any window can reach: bias + 255 * (sum of positive taps).
+// D = 1 uses M = 2^32 - 1 with the accumulator biased by +1 (umulhi(a + 1,
+// 2^32 - 1) = a) and a clamp floor of 1 instead of 0.
+ds::GenStage gen_stage(const ds_stage_spec& s) {
+    ds::GenStage g;
+    std::memset(&g, 0, sizeof g);
+    g.P = s.pattern; g.S = s.paving; g.Q = s.outputs; g.bias = s.bias;
+    g.D = (uint32_t)s.divisor;
+    g.D_rcp = s.divisor == 1 ? 0xffffffffu : (uint32_t)((1ULL << 32) / (uint64_t)s.divisor);
+    std::memcpy(g.w, s.weight, sizeof g.w);
+    g.s8 = 1;
+    int64_t amax = 0;
+    for (int k = 0; k < DS_MAX_OUTPUTS; ++k) {
+        int64_t pos = 0;
+        for (int i = 0; i < DS_MAX_PATTERN; ++i) {
+            const int32_t w = s.weight[k][i];
+            if (w < -128 || w > 127) g.s8 = 0;
+            g.wp[k][i / 4] |= (uint32_t)(uint8_t)(int8_t)(w < -128 ? 0 : w > 127 ? 0 : w) << (8 * (i % 4));
+            if (k < s.outputs && i < s.pattern && w > 0) pos += w;
+        }
+        if (k < s.outputs) amax = std::max<int64_t>(amax, (int64_t)s.bias + 255 * pos);
+    }
+    if (s.divisor == 1) {
+        if (amax < (int64_t)0x7fffffff) { g.M = 0xffffffffu; g.lo = 1; g.fbias = s.bias + 1; }
+    } else {
+        const uint64_t D = (uint64_t)s.divisor;
+        const uint64_t M = ((1ULL << 32) + D - 1) / D;
+        const uint64_t e = M * D - (1ULL << 32);
+        if (amax < (int64_t)0x7fffffff && (unsigned __int128)(uint64_t)amax * e < ((unsigned __int128)1 << 32)) {
+            g.M = (uint32_t)M; g.lo = 0; g.fbias = s.bias;
+        }
+    }
+    return g;
+}
+
 int configure_general(ds_handle* h) {
     GeneralCfg c;
     const ds_plan_info& pi = h->plan;
@@ -372,7 +412,7 @@ int configure_general(ds_handle* h) {
     for (int p = 0; p < pi.n_planes; ++p) {
         c.k[p] = pi.general_band_reps[p];
         c.R[p] = sp.v.paving * (c.k[p] - 1) + sp.v.pattern;
-        smax = std::max<int64_t>(smax, (int64_t)c.R[p] * pi.in_w[p]);
+        smax = std::max<int64_t>(smax, (int64_t)c.R[p] * general_pitch(pi.in_w[p]));
         mmax = std::max<int64_t>(mmax, (int64_t)(c.R[p] + 3) * pi.out_w[p]);   // V reads 4-row blocks
         omax = std::max<int64_t>(omax, (int64_t)sp.v.outputs * c.k[p] * pi.out_w[p]);
         upf += (pi.in_h[p] / sp.v.paving) / c.k[p];
@@ -389,7 +429,8 @@ int configure_general(ds_handle* h) {
     const int want_ctas = 2;
     c.threads = (c.ncw + 1) * 32;
     c.smem = (int)general_smem(c, c.stages);
-    GeneralFn fn = c.ncw == 16 ? ds::ds_fused_general_kernel<16> : ds::ds_fused_general_kernel<8>;
+    c.fast = gen_stage(sp.h).M != 0 && gen_stage(sp.v).M != 0;
+    GeneralFn fn = c.fast ? ds::ds_fused_general_kernel<true> : ds::ds_fused_general_kernel<false>;
     DeviceGuard g(h->device);
     if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              kSmemLimit - 2 * DS_MAX_OUTPUTS * DS_MAX_PATTERN * 4) != cudaSuccess) {
@@ -406,23 +447,6 @@ int configure_general(ds_handle* h) {
     c.valid = true;
     h->general = c;
     return DS_OK;
-}
-
-ds::GenStage gen_stage(const ds_stage_spec& s) {
-    ds::GenStage g;
-    std::memset(&g, 0, sizeof g);
-    g.P = s.pattern; g.S = s.paving; g.Q = s.outputs; g.bias = s.bias;
-    g.D = (uint32_t)s.divisor;
-    g.D_rcp = s.divisor == 1 ? 0xffffffffu : (uint32_t)((1ULL << 32) / (uint64_t)s.divisor);
-    std::memcpy(g.w, s.weight, sizeof g.w);
-    g.s8 = 1;
-    for (int k = 0; k < DS_MAX_OUTPUTS; ++k)
-        for (int i = 0; i < DS_MAX_PATTERN; ++i) {
-            const int32_t w = s.weight[k][i];
-            if (w < -128 || w > 127) g.s8 = 0;
-            g.wp[k][i / 4] |= (uint32_t)(uint8_t)(int8_t)(w < -128 ? 0 : w > 127 ? 0 : w) << (8 * (i % 4));
-        }
-    return g;
 }
 
 uint32_t rcp32(int32_t d) { return d > 1 ? (uint32_t)((0x100000000ULL + d - 1) / (uint64_t)d) : 0u; }
@@ -466,15 +490,16 @@ int launch_general(ds_handle* h, const uint8_t* in, int64_t n, uint8_t* out, cud
         P.unit_start = start;
         P.unit_out = sp.v.outputs * P.k * P.Wm;
         P.bulk_store = (out_al && P.out_off % 16 == 0 && P.unit_out % 16 == 0) ? 1 : 0;
-        P.coop = (in_al && P.W % 16 == 0 && P.in_off % 16 == 0 && pi.in_frame_bytes % 16 == 0) ? 0 : 1;
-        P.row4 = (P.W % 4 == 0) ? 1 : 0;
+        P.coop = (in_al && P.W % 16 == 0 && P.W >= 32 && P.in_off % 16 == 0 && pi.in_frame_bytes % 16 == 0)
+                     ? 0 : 1;
+        P.pitch = (int32_t)general_pitch(P.W);
         start += (P.H / sp.v.paving) / P.k;
     }
     const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(p.n_units, (int64_t)c.grid_per_sm * h->sm_count));
-    if (c.ncw == 16)
-        ds::ds_fused_general_kernel<16><<<(unsigned)grid, c.threads, c.smem, st>>>(p);
+    if (c.fast)
+        ds::ds_fused_general_kernel<true><<<(unsigned)grid, c.threads, c.smem, st>>>(p);
     else
-        ds::ds_fused_general_kernel<8><<<(unsigned)grid, c.threads, c.smem, st>>>(p);
+        ds::ds_fused_general_kernel<false><<<(unsigned)grid, c.threads, c.smem, st>>>(p);
     return cudaGetLastError() == cudaSuccess ? DS_OK : DS_ECUDA;
 }
 

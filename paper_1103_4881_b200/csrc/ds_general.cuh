@@ -5,13 +5,17 @@
 // Same persistent, warp-specialised TMA pipeline as K-N1.  A work unit is
 // (frame, plane, band of k V repetitions).  Those repetitions read input rows
 // (o_v + S_v g + i) mod H for g in the band, i < P_v: R = S_v (k-1) + P_v
-// consecutive rows modulo H, i.e. the band plus its halo.  The producer
-// stages them whole-width with one bulk copy per non-wrapping segment (the
-// bottom halo wraps to the plane's first rows).  Consumers run the H task on
-// every staged row into a u8 intermediate in shared memory, then the
-// V task from it, stage the output band in shared memory and bulk-store it.
-// Divisions by runtime values use a reciprocal plus one correction step, so
-// results are exact (truncation toward zero, then clamp).
+// consecutive rows modulo H, i.e. the band plus its halo (the bottom halo
+// wraps to the plane's first rows).  The producer stages each row at a pitch
+// of round_up(W, 16) + 32 bytes: the row, then a 32-byte pad holding its first
+// bytes again (row[j mod W]), so an H window that wraps past the row end
+// reads straight on into the pad -- no wrap test, no divergent slow
+// path.  Consumers run the H task on every staged row into a u8 intermediate
+// in shared memory, then the V task from it, stage the output band in
+// shared memory and bulk-store it.  Divisions by runtime values are exact
+// (truncation toward zero, then clamp): one multiply-high when the host
+// proves the accumulator range allows it (FASTDIV), else a reciprocal plus one
+// correction step.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -24,6 +28,7 @@ namespace ds {
 struct GenPlane {
     int64_t in_off, out_off;
     int32_t W, H, Wm;          // input row bytes, rows, mid/output row bytes
+    int32_t pitch;             // staged row stride: round_up(W, 16) + 32 (row, then wrap pad)
     int32_t k;                 // V repetitions per unit
     int32_t R;                 // staged rows per unit = Sv (k-1) + Pv
     int32_t np;                // H repetitions per row = W / Sh
@@ -36,14 +41,17 @@ struct GenPlane {
     int32_t unit_out;          // Qv * k * Wm
     int32_t bulk_store;
     int32_t coop;              // 1: rows staged by the producer warp with plain loads
-    int32_t row4;              // 1: W % 4 == 0 (smem rows word-aligned: dp4a window path)
 };
 
 struct GenStage {
     int32_t P, S, Q, bias;
     uint32_t D, D_rcp;         // divisor and floor(2^32 / D) (D = 1: 0xffffffff)
     int32_t s8;                // 1: every weight fits in s8 -> dp4a fast path
-    int32_t reserved_;         // keeps wp 8-byte aligned in the parameter block
+    // FASTDIV: clamp(trunc(acc / D)) = min(umulhi(max(acc + fbias - bias, lo), M), 255)
+    // with M = ceil(2^32 / D), exact while max_acc * (M D - 2^32) < 2^32 (host-checked);
+    // D = 1: M = 2^32 - 1, accumulator biased by +1 and lo = 1
+    int32_t fbias;             // accumulator start on the FASTDIV path (bias, or bias + 1 for D = 1)
+    uint32_t M, lo;
     int32_t w[DS_MAX_OUTPUTS][DS_MAX_PATTERN];
     uint32_t wp[DS_MAX_OUTPUTS][DS_MAX_PATTERN / 4];   // s8-packed weights, 4 taps per word
 };
@@ -69,6 +77,15 @@ __device__ __forceinline__ uint32_t g_stage_out(int32_t acc, uint32_t D, uint32_
     q += (a - q * D >= D) ? 1u : 0u;
     return min(q, 255u);
 }
+template <bool FAST>
+__device__ __forceinline__ uint32_t g_out(const GenStage& g, int32_t acc) {
+    if (FAST) return min(__umulhi((uint32_t)max(acc, (int32_t)g.lo), g.M), 255u);
+    return g_stage_out(acc, g.D, g.D_rcp);
+}
+template <bool FAST>
+__device__ __forceinline__ int32_t g_bias(const GenStage& g) {
+    return FAST ? g.fbias : g.bias;
+}
 // d = c + sum_i a.u8[i] * b.s8[i]
 __device__ __forceinline__ int32_t dp4a_us(uint32_t a, uint32_t b, int32_t c) {
     int32_t d;
@@ -85,27 +102,27 @@ __device__ __forceinline__ int32_t g_div_small(int32_t t, int32_t d, uint32_t rc
 }
 
 // H outputs of one window (compile-time Q: straight-line code, no per-output branch)
-template <int Q>
+template <int Q, bool FAST>
 __device__ __forceinline__ void g_h_out(const GenStage& g, uint32_t x0, uint32_t x1, uint32_t x2,
                                         uint32_t x3, uint8_t* mo) {
 #pragma unroll
     for (int j = 0; j < Q; ++j) {
-        int32_t acc = dp4a_us(x0, g.wp[j][0], g.bias);
+        int32_t acc = dp4a_us(x0, g.wp[j][0], g_bias<FAST>(g));
         acc = dp4a_us(x1, g.wp[j][1], acc);
         acc = dp4a_us(x2, g.wp[j][2], acc);
         acc = dp4a_us(x3, g.wp[j][3], acc);
-        mo[j] = (uint8_t)g_stage_out(acc, g.D, g.D_rcp);
+        mo[j] = (uint8_t)g_out<FAST>(g, acc);
     }
 }
 
 // V outputs of one 4-column group (compile-time Q)
-template <int Q>
+template <int Q, bool FAST>
 __device__ __forceinline__ void g_v_quad(const GenStage& g, const uint8_t* mb, int Wm, uint8_t* ob0) {
     int32_t acc[Q][4];
 #pragma unroll
     for (int kk = 0; kk < Q; ++kk)
 #pragma unroll
-        for (int e = 0; e < 4; ++e) acc[kk][e] = g.bias;
+        for (int e = 0; e < 4; ++e) acc[kk][e] = g_bias<FAST>(g);
     const int nb = (g.P + 3) >> 2;
     for (int b4 = 0; b4 < nb; ++b4) {
         const uint8_t* rb = mb + (size_t)(4 * b4) * Wm;
@@ -125,43 +142,33 @@ __device__ __forceinline__ void g_v_quad(const GenStage& g, const uint8_t* mb, i
     }
 #pragma unroll
     for (int kk = 0; kk < Q; ++kk) {
-        const uint32_t o = g_stage_out(acc[kk][0], g.D, g.D_rcp) | (g_stage_out(acc[kk][1], g.D, g.D_rcp) << 8) |
-                           (g_stage_out(acc[kk][2], g.D, g.D_rcp) << 16) |
-                           (g_stage_out(acc[kk][3], g.D, g.D_rcp) << 24);
+        const uint32_t o = g_out<FAST>(g, acc[kk][0]) | (g_out<FAST>(g, acc[kk][1]) << 8) |
+                           (g_out<FAST>(g, acc[kk][2]) << 16) | (g_out<FAST>(g, acc[kk][3]) << 24);
         *reinterpret_cast<uint32_t*>(ob0 + (size_t)kk * Wm) = o;
     }
 }
 
-// Producer-warp staging of `left` rows starting at `row` (mod H) for planes
-// the TMA cannot copy; out of line so its registers do not count against the
-// consumer path.
-__device__ __forceinline__ void g_coop_stage(uint8_t* dst, const uint8_t* plane, int row, int left, int H,
-                                          int W, int lane) {
-    while (left > 0) {
-        const int seg = min(left, H - row);
-        const uint8_t* src = plane + (int64_t)row * W;
-        const int64_t nb = (int64_t)seg * W;
-        if ((((uintptr_t)src | (uintptr_t)dst | (uintptr_t)nb) & 3) == 0) {
-            const uint32_t* s4 = reinterpret_cast<const uint32_t*>(src);
-            uint32_t* d4 = reinterpret_cast<uint32_t*>(dst);
-            const int64_t n4 = nb >> 2;
-            int64_t x = lane;
-            for (; x + 96 < n4; x += 128) {             // 4 loads in flight per lane
-                const uint32_t a = __ldg(s4 + x), b = __ldg(s4 + x + 32), c = __ldg(s4 + x + 64),
-                               d = __ldg(s4 + x + 96);
-                d4[x] = a;
-                d4[x + 32] = b;
-                d4[x + 64] = c;
-                d4[x + 96] = d;
-            }
-            for (; x < n4; x += 32) d4[x] = __ldg(s4 + x);
-        } else {
-            for (int64_t x = lane; x < nb; x += 32) dst[x] = __ldg(src + x);
+// Producer-warp staging of one row for planes the TMA cannot copy: the W
+// row bytes, then the 32-byte wrap pad row[j mod W].
+__device__ __forceinline__ void g_coop_row(uint8_t* dst, const uint8_t* src, int W, int lane) {
+    if ((((uintptr_t)src | (uintptr_t)W) & 3) == 0) {
+        const uint32_t* s4 = reinterpret_cast<const uint32_t*>(src);
+        uint32_t* d4 = reinterpret_cast<uint32_t*>(dst);
+        const int n4 = W >> 2;
+        int x = lane;
+        for (; x + 96 < n4; x += 128) {             // 4 loads in flight per lane
+            const uint32_t a = __ldg(s4 + x), b = __ldg(s4 + x + 32), c = __ldg(s4 + x + 64),
+                           d = __ldg(s4 + x + 96);
+            d4[x] = a;
+            d4[x + 32] = b;
+            d4[x + 64] = c;
+            d4[x + 96] = d;
         }
-        dst += nb;
-        left -= seg;
-        row = 0;
+        for (; x < n4; x += 32) d4[x] = __ldg(s4 + x);
+    } else {
+        for (int x = lane; x < W; x += 32) dst[x] = __ldg(src + x);
     }
+    dst[W + lane] = __ldg(src + (lane < W ? lane : lane % W));
 }
 
 struct GenCursor {
@@ -188,11 +195,11 @@ struct GenCursor {
     }
 };
 
-// <8>: register cap (<= 75) so two CTAs fit per SM -- the register file is
-// split across 4 SMSPs, so 18 warps need <= 102 registers each; <16>: one CTA.
-template <int NCW>
-__global__ void __launch_bounds__((NCW + 1) * 32, NCW == 8 ? 2 : 1)
-    ds_fused_general_kernel(const __grid_constant__ GeneralParams p) {
+// 2 CTAs x (8 consumer + 1 producer) warps per SM: the register file is
+// split across 4 SMSPs, so 18 warps need <= 102 registers each.
+template <bool FAST>
+__global__ void __launch_bounds__(9 * 32, 2) ds_fused_general_kernel(const __grid_constant__ GeneralParams p) {
+    constexpr int NCW = 8;
     extern __shared__ __align__(1024) uint8_t smem[];
     constexpr int NC = NCW * 32;
     const int S = p.stages;
@@ -223,35 +230,33 @@ __global__ void __launch_bounds__((NCW + 1) * 32, NCW == 8 ? 2 : 1)
     int s = 0;
     uint32_t phase = 0;
     if (warp == NCW) {
-        // ---------------- producer warp: band + halo rows into the ring.
-        // Bulk-copy planes: lane 0 issues one TMA copy per non-wrapping
-        // segment.  Planes whose rows are not 16-byte aligned (or a
-        // misaligned input pointer): all 32 lanes copy with plain loads and
-        // lane 0 arrives on full[s] without a transaction count.
+        // ---------------- producer warp: band + halo rows into the ring, one
+        // staged row (pitch P.pitch) per input row (o_v + S_v k band + i) mod H.
+        // Bulk-copy planes: lane 0 posts the byte count, then every lane issues
+        // the TMA copies of its rows (row, then its first 32 bytes as the pad).
+        // Other planes: all 32 lanes copy with plain loads and lane 0 arrives
+        // on full[s] without a transaction count.
         const uint64_t pol = policy_evict_first();
         bool first_round = true;
         for (; cur.u < p.n_units; cur.next()) {
-            if (!first_round) mbar_wait(&empty[s], phase ^ 1);
+            if (!first_round) mbar_wait_sleep(&empty[s], phase ^ 1);
             const GenPlane& P = p.pl[cur.plane(p)];
             const int band = cur.local - P.unit_start;
             const uint8_t* plane = p.in + cur.f * p.in_frame + P.in_off;
             uint8_t* dst = ring + (size_t)s * p.stage_stride;
-            // rows ov + Sv*k*band .. + R-1, modulo H, in non-wrapping segments
-            int row = (int)(((int64_t)P.ov + (int64_t)p.v.S * P.k * band) % P.H);
-            int left = P.R;
+            const int row0 = (int)(((int64_t)P.ov + (int64_t)p.v.S * P.k * band) % P.H);
             if (!P.coop) {
-                if (lane == 0) {
-                    mbar_arrive_expect_tx(&full[s], (uint32_t)P.R * (uint32_t)P.W);
-                    while (left > 0) {
-                        const int seg = min(left, P.H - row);
-                        bulk_g2s(dst, plane + (int64_t)row * P.W, (uint32_t)seg * (uint32_t)P.W, &full[s], pol);
-                        dst += (size_t)seg * P.W;
-                        left -= seg;
-                        row = 0;
-                    }
+                if (lane == 0) mbar_arrive_expect_tx(&full[s], (uint32_t)P.R * (uint32_t)(P.W + 32));
+                __syncwarp();
+                for (int i = lane; i < P.R; i += 32) {
+                    const uint8_t* src = plane + (int64_t)((row0 + i) % P.H) * P.W;
+                    uint8_t* d = dst + (size_t)i * P.pitch;
+                    bulk_g2s(d, src, (uint32_t)P.W, &full[s], pol);
+                    bulk_g2s(d + P.W, src, 32u, &full[s], pol);
                 }
             } else {
-                g_coop_stage(dst, plane, row, left, P.H, P.W, lane);
+                for (int i = 0; i < P.R; ++i)
+                    g_coop_row(dst + (size_t)i * P.pitch, plane + (int64_t)((row0 + i) % P.H) * P.W, P.W, lane);
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&full[s]);      // release: generic smem writes
             }
@@ -269,47 +274,41 @@ __global__ void __launch_bounds__((NCW + 1) * 32, NCW == 8 ? 2 : 1)
         const int W = P.W, Wm = P.Wm, np = P.np;
         mbar_wait(&full[s], phase);
 
-        // ---- H task on every staged row -> mid (u8); item = (row, H rep)
+        // ---- H task on every staged row -> mid (u8); item = (row, H rep).
+        // The window starts at c0 < W and runs at most 19 bytes on, inside
+        // row + pad.
         const int QH = p.h.Q, PH = p.h.P, SH = p.h.S;
         const int h_items = P.R * np;
         for (int it = tid; it < h_items; it += NC) {
-            {
-                const int r = g_div_small(it, np, P.np_rcp);
-                const int r1 = it - r * np;
-                const uint8_t* rowp = st + (size_t)r * W;
-                uint8_t* mrow = mid + (size_t)r * Wm;
-                int c0 = P.oh + SH * r1;
-                if (c0 >= W) c0 -= W;                 // oh < W and Sh*r1 < W
-                uint8_t* mo = mrow + QH * r1;
-                if (p.h.s8 && P.row4 && c0 + PH <= W) {
-                    // window of nw+1 aligned words (bytes past the row meet zero taps)
-                    const uint8_t* wb = rowp + (c0 & ~3);
-                    const uint32_t sel = 0x3210u + 0x1111u * (uint32_t)(c0 & 3);
-                    const uint32_t w0 = lds32(wb), w1 = lds32(wb + 4), w2 = lds32(wb + 8),
-                                   w3 = lds32(wb + 12), w4 = lds32(wb + 16);
-                    const uint32_t x0 = __byte_perm(w0, w1, sel), x1 = __byte_perm(w1, w2, sel),
-                                   x2 = __byte_perm(w2, w3, sel), x3 = __byte_perm(w3, w4, sel);
-                    switch (QH) {
-                        case 1: g_h_out<1>(p.h, x0, x1, x2, x3, mo); break;
-                        case 2: g_h_out<2>(p.h, x0, x1, x2, x3, mo); break;
-                        case 3: g_h_out<3>(p.h, x0, x1, x2, x3, mo); break;
-                        case 4: g_h_out<4>(p.h, x0, x1, x2, x3, mo); break;
-                        case 5: g_h_out<5>(p.h, x0, x1, x2, x3, mo); break;
-                        case 6: g_h_out<6>(p.h, x0, x1, x2, x3, mo); break;
-                        case 7: g_h_out<7>(p.h, x0, x1, x2, x3, mo); break;
-                        default: g_h_out<8>(p.h, x0, x1, x2, x3, mo); break;
-                    }
-                } else {
-                    for (int j = 0; j < QH; ++j) {
-                        int32_t acc = p.h.bias;
-                        int c = c0;
-                        for (int i = 0; i < PH; ++i) {
-                            const int32_t w = wh[j][i];
-                            if (w) acc += w * (int32_t)rowp[c];
-                            if (++c == W) c = 0;
-                        }
-                        mo[j] = (uint8_t)g_stage_out(acc, p.h.D, p.h.D_rcp);
-                    }
+            const int r = g_div_small(it, np, P.np_rcp);
+            const int r1 = it - r * np;
+            const uint8_t* rowp = st + (size_t)r * P.pitch;
+            int c0 = P.oh + SH * r1;
+            if (c0 >= W) c0 -= W;                 // oh < W and Sh*r1 < W
+            uint8_t* mo = mid + (size_t)r * Wm + QH * r1;
+            if (p.h.s8) {
+                // 5 aligned words, byte-shifted into a 16-byte window (taps past P are 0)
+                const uint8_t* wb = rowp + (c0 & ~3);
+                const uint32_t sel = 0x3210u + 0x1111u * (uint32_t)(c0 & 3);
+                const uint32_t w0 = lds32(wb), w1 = lds32(wb + 4), w2 = lds32(wb + 8),
+                               w3 = lds32(wb + 12), w4 = lds32(wb + 16);
+                const uint32_t x0 = __byte_perm(w0, w1, sel), x1 = __byte_perm(w1, w2, sel),
+                               x2 = __byte_perm(w2, w3, sel), x3 = __byte_perm(w3, w4, sel);
+                switch (QH) {
+                    case 1: g_h_out<1, FAST>(p.h, x0, x1, x2, x3, mo); break;
+                    case 2: g_h_out<2, FAST>(p.h, x0, x1, x2, x3, mo); break;
+                    case 3: g_h_out<3, FAST>(p.h, x0, x1, x2, x3, mo); break;
+                    case 4: g_h_out<4, FAST>(p.h, x0, x1, x2, x3, mo); break;
+                    case 5: g_h_out<5, FAST>(p.h, x0, x1, x2, x3, mo); break;
+                    case 6: g_h_out<6, FAST>(p.h, x0, x1, x2, x3, mo); break;
+                    case 7: g_h_out<7, FAST>(p.h, x0, x1, x2, x3, mo); break;
+                    default: g_h_out<8, FAST>(p.h, x0, x1, x2, x3, mo); break;
+                }
+            } else {
+                for (int j = 0; j < QH; ++j) {
+                    int32_t acc = g_bias<FAST>(p.h);
+                    for (int i = 0; i < PH; ++i) acc += wh[j][i] * (int32_t)rowp[c0 + i];
+                    mo[j] = (uint8_t)g_out<FAST>(p.h, acc);
                 }
             }
         }
@@ -331,14 +330,14 @@ __global__ void __launch_bounds__((NCW + 1) * 32, NCW == 8 ? 2 : 1)
                     const uint8_t* mb = mid + (size_t)(p.v.S * g) * Wm + 4 * q;
                     uint8_t* ob0 = ob + (size_t)(QV * g) * Wm + 4 * q;
                     switch (QV) {
-                        case 1: g_v_quad<1>(p.v, mb, Wm, ob0); break;
-                        case 2: g_v_quad<2>(p.v, mb, Wm, ob0); break;
-                        case 3: g_v_quad<3>(p.v, mb, Wm, ob0); break;
-                        case 4: g_v_quad<4>(p.v, mb, Wm, ob0); break;
-                        case 5: g_v_quad<5>(p.v, mb, Wm, ob0); break;
-                        case 6: g_v_quad<6>(p.v, mb, Wm, ob0); break;
-                        case 7: g_v_quad<7>(p.v, mb, Wm, ob0); break;
-                        default: g_v_quad<8>(p.v, mb, Wm, ob0); break;
+                        case 1: g_v_quad<1, FAST>(p.v, mb, Wm, ob0); break;
+                        case 2: g_v_quad<2, FAST>(p.v, mb, Wm, ob0); break;
+                        case 3: g_v_quad<3, FAST>(p.v, mb, Wm, ob0); break;
+                        case 4: g_v_quad<4, FAST>(p.v, mb, Wm, ob0); break;
+                        case 5: g_v_quad<5, FAST>(p.v, mb, Wm, ob0); break;
+                        case 6: g_v_quad<6, FAST>(p.v, mb, Wm, ob0); break;
+                        case 7: g_v_quad<7, FAST>(p.v, mb, Wm, ob0); break;
+                        default: g_v_quad<8, FAST>(p.v, mb, Wm, ob0); break;
                     }
                 }
             }
@@ -349,12 +348,9 @@ __global__ void __launch_bounds__((NCW + 1) * 32, NCW == 8 ? 2 : 1)
                 const int c = it - orow * Wm;
                 const int g = orow / p.v.Q, kk = orow - g * p.v.Q;
                 const uint8_t* mcol = mid + (size_t)(p.v.S * g) * Wm + c;
-                int32_t acc = p.v.bias;
-                for (int i = 0; i < p.v.P; ++i) {
-                    const int32_t w = wv[kk][i];
-                    if (w) acc += w * (int32_t)mcol[(size_t)i * Wm];
-                }
-                ob[it] = (uint8_t)g_stage_out(acc, p.v.D, p.v.D_rcp);
+                int32_t acc = g_bias<FAST>(p.v);
+                for (int i = 0; i < p.v.P; ++i) acc += wv[kk][i] * (int32_t)mcol[(size_t)i * Wm];
+                ob[it] = (uint8_t)g_out<FAST>(p.v, acc);
             }
         }
         uint8_t* dst = p.out + cur.f * p.out_frame + P.out_off + (int64_t)band * P.unit_out;

@@ -62,8 +62,12 @@ struct GeneralCfg {
     int32_t upf = 0;
     int32_t stage_stride = 0, mid_stride = 0, out_stride = 0;
     int stages = 2, ncw = 8;
+    bool fast = false;                        // FASTDIV instantiation (both stages qualify)
     int grid_per_sm = 0, threads = 0, smem = 0;
 };
+
+// K-N1g staged row stride: the row, rounded to 16 bytes, then the 32-byte wrap pad
+inline int64_t general_pitch(int64_t W) { return (W + 15) / 16 * 16 + 32; }
 
 }  // namespace dsi
 

@@ -131,7 +131,7 @@ def test_plan_generic_spec_not_fused():
     assert p.fused_general_eligible == 1
     k = p.general_band_reps[0]
     assert 3 % k == 0 and p.general_units_per_frame == 3 // k
-    assert p.general_stage_bytes_max == (9 * (k - 1) + 9) * 48
+    assert p.general_stage_bytes_max == (9 * (k - 1) + 9) * (48 + 32)   # row pitch: 48 + 32-byte wrap pad
 
 
 def test_plan_narrow_rows():
