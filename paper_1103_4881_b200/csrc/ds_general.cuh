@@ -92,32 +92,83 @@ __device__ __forceinline__ int32_t dp4a_us(uint32_t a, uint32_t b, int32_t c) {
     asm("dp4a.u32.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
     return d;
 }
-__device__ __forceinline__ uint32_t lds32(const uint8_t* p) {
+// shared-window accesses on 32-bit shared addresses (no generic->shared
+// conversion per access)
+__device__ __forceinline__ uint32_t lds32s(uint32_t a) {
     uint32_t v;
-    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)));
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
     return v;
+}
+__device__ __forceinline__ uint32_t lds8s(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sts8s(uint32_t a, uint32_t v) {
+    asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void sts32s(uint32_t a, uint32_t v) {
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
 __device__ __forceinline__ int32_t g_div_small(int32_t t, int32_t d, uint32_t rcp) {
     return d == 1 ? t : (int32_t)__umulhi((uint32_t)t, rcp);
 }
 
-// H outputs of one window (compile-time Q: straight-line code, no per-output branch)
-template <int Q, bool FAST>
-__device__ __forceinline__ void g_h_out(const GenStage& g, uint32_t x0, uint32_t x1, uint32_t x2,
-                                        uint32_t x3, uint8_t* mo) {
+// ---- H pass over one staged unit: item = (staged row r, H repetition r1),
+// Q outputs into mid row r at 3 r1 ...  The window starts at
+// c0 = (o_h + S_h r1) mod W < W and runs at most 19 bytes on, inside the row
+// and its wrap pad: 5 aligned words byte-shifted into a 16-byte window (taps
+// past P are zero in the packed weights), one dp4a per 4 taps.
+template <int Q, bool FAST, int NC>
+__device__ __forceinline__ void g_h_pass(const GenStage& g, const GenPlane& P, uint32_t st, uint32_t mid,
+                                         int tid) {
+    const int np = P.np, W = P.W, items = P.R * np;
+    for (int it = tid; it < items; it += NC) {
+        const int r = g_div_small(it, np, P.np_rcp);
+        const int r1 = it - r * np;
+        int c0 = P.oh + g.S * r1;
+        if (c0 >= W) c0 -= W;                 // oh < W and Sh*r1 < W
+        const uint32_t wb = st + r * P.pitch + (c0 & ~3);
+        const uint32_t sel = 0x3210u + 0x1111u * (uint32_t)(c0 & 3);
+        const uint32_t w0 = lds32s(wb), w1 = lds32s(wb + 4), w2 = lds32s(wb + 8), w3 = lds32s(wb + 12),
+                       w4 = lds32s(wb + 16);
+        const uint32_t x0 = __byte_perm(w0, w1, sel), x1 = __byte_perm(w1, w2, sel),
+                       x2 = __byte_perm(w2, w3, sel), x3 = __byte_perm(w3, w4, sel);
+        const uint32_t mo = mid + r * P.Wm + Q * r1;
 #pragma unroll
-    for (int j = 0; j < Q; ++j) {
-        int32_t acc = dp4a_us(x0, g.wp[j][0], g_bias<FAST>(g));
-        acc = dp4a_us(x1, g.wp[j][1], acc);
-        acc = dp4a_us(x2, g.wp[j][2], acc);
-        acc = dp4a_us(x3, g.wp[j][3], acc);
-        mo[j] = (uint8_t)g_out<FAST>(g, acc);
+        for (int j = 0; j < Q; ++j) {
+            int32_t acc = dp4a_us(x0, g.wp[j][0], g_bias<FAST>(g));
+            acc = dp4a_us(x1, g.wp[j][1], acc);
+            acc = dp4a_us(x2, g.wp[j][2], acc);
+            acc = dp4a_us(x3, g.wp[j][3], acc);
+            sts8s(mo + j, g_out<FAST>(g, acc));
+        }
+    }
+}
+// Taps outside s8: byte loop (same item space, same window bounds)
+template <bool FAST, int NC>
+__device__ __forceinline__ void g_h_pass_bytes(const GenStage& g, const int32_t (*w)[DS_MAX_PATTERN],
+                                               const GenPlane& P, uint32_t st, uint32_t mid, int tid) {
+    const int np = P.np, W = P.W, items = P.R * np;
+    for (int it = tid; it < items; it += NC) {
+        const int r = g_div_small(it, np, P.np_rcp);
+        const int r1 = it - r * np;
+        int c0 = P.oh + g.S * r1;
+        if (c0 >= W) c0 -= W;
+        const uint32_t rowp = st + r * P.pitch + c0;
+        const uint32_t mo = mid + r * P.Wm + g.Q * r1;
+        for (int j = 0; j < g.Q; ++j) {
+            int32_t acc = g_bias<FAST>(g);
+            for (int i = 0; i < g.P; ++i) acc += w[j][i] * (int32_t)lds8s(rowp + i);
+            sts8s(mo + j, g_out<FAST>(g, acc));
+        }
     }
 }
 
-// V outputs of one 4-column group (compile-time Q)
+// V outputs k0 .. k0+Q-1 of one 4-column group: 4x4 byte transposes turn 4
+// mid rows x 4 columns into 4 column words, one dp4a per 4 taps.
 template <int Q, bool FAST>
-__device__ __forceinline__ void g_v_quad(const GenStage& g, const uint8_t* mb, int Wm, uint8_t* ob0) {
+__device__ __forceinline__ void g_v_quad(const GenStage& g, int k0, uint32_t mb, int Wm, uint32_t ob0) {
     int32_t acc[Q][4];
 #pragma unroll
     for (int kk = 0; kk < Q; ++kk)
@@ -125,15 +176,15 @@ __device__ __forceinline__ void g_v_quad(const GenStage& g, const uint8_t* mb, i
         for (int e = 0; e < 4; ++e) acc[kk][e] = g_bias<FAST>(g);
     const int nb = (g.P + 3) >> 2;
     for (int b4 = 0; b4 < nb; ++b4) {
-        const uint8_t* rb = mb + (size_t)(4 * b4) * Wm;
-        const uint32_t r0 = lds32(rb), r1 = lds32(rb + Wm), r2 = lds32(rb + 2 * Wm), r3 = lds32(rb + 3 * Wm);
+        const uint32_t rb = mb + 4 * b4 * Wm;
+        const uint32_t r0 = lds32s(rb), r1 = lds32s(rb + Wm), r2 = lds32s(rb + 2 * Wm), r3 = lds32s(rb + 3 * Wm);
         const uint32_t ta = __byte_perm(r0, r1, 0x5140), tb = __byte_perm(r2, r3, 0x5140);
         const uint32_t tc = __byte_perm(r0, r1, 0x7362), td = __byte_perm(r2, r3, 0x7362);
         const uint32_t c0 = __byte_perm(ta, tb, 0x5410), c1 = __byte_perm(ta, tb, 0x7632),
                        c2 = __byte_perm(tc, td, 0x5410), c3 = __byte_perm(tc, td, 0x7632);
 #pragma unroll
         for (int kk = 0; kk < Q; ++kk) {
-            const uint32_t wq = g.wp[kk][b4];
+            const uint32_t wq = g.wp[k0 + kk][b4];
             acc[kk][0] = dp4a_us(c0, wq, acc[kk][0]);
             acc[kk][1] = dp4a_us(c1, wq, acc[kk][1]);
             acc[kk][2] = dp4a_us(c2, wq, acc[kk][2]);
@@ -144,7 +195,37 @@ __device__ __forceinline__ void g_v_quad(const GenStage& g, const uint8_t* mb, i
     for (int kk = 0; kk < Q; ++kk) {
         const uint32_t o = g_out<FAST>(g, acc[kk][0]) | (g_out<FAST>(g, acc[kk][1]) << 8) |
                            (g_out<FAST>(g, acc[kk][2]) << 16) | (g_out<FAST>(g, acc[kk][3]) << 24);
-        *reinterpret_cast<uint32_t*>(ob0 + (size_t)kk * Wm) = o;
+        sts32s(ob0 + (k0 + kk) * Wm, o);
+    }
+}
+// ---- V pass (Wm % 4 == 0, s8 taps): item = (V repetition gi, 4 mid columns);
+// outputs in groups of at most 4 (QA, then QB) to bound live accumulators.
+template <int QA, int QB, bool FAST, int NC>
+__device__ __forceinline__ void g_v_pass(const GenStage& g, const GenPlane& P, uint32_t mid, uint32_t ob,
+                                         int tid) {
+    const int Wm = P.Wm, quads = Wm >> 2, items = P.k * quads;
+    for (int it = tid; it < items; it += NC) {
+        const int gi = g_div_small(it, quads, P.quads_rcp);
+        const int q = it - gi * quads;
+        const uint32_t mb = mid + g.S * gi * Wm + 4 * q;
+        const uint32_t ob0 = ob + (QA + QB) * gi * Wm + 4 * q;
+        g_v_quad<QA, FAST>(g, 0, mb, Wm, ob0);
+        if (QB > 0) g_v_quad<(QB > 0 ? QB : 1), FAST>(g, QA, mb, Wm, ob0);
+    }
+}
+// V pass, general: item = output byte of the band
+template <bool FAST, int NC>
+__device__ __forceinline__ void g_v_pass_bytes(const GenStage& g, const int32_t (*w)[DS_MAX_PATTERN],
+                                               const GenPlane& P, uint32_t mid, uint32_t ob, int tid) {
+    const int Wm = P.Wm;
+    for (int it = tid; it < P.unit_out; it += NC) {
+        const int orow = g_div_small(it, Wm, P.wm_rcp);
+        const int c = it - orow * Wm;
+        const int gi = orow / g.Q, kk = orow - gi * g.Q;
+        const uint32_t mcol = mid + g.S * gi * Wm + c;
+        int32_t acc = g_bias<FAST>(g);
+        for (int i = 0; i < g.P; ++i) acc += w[kk][i] * (int32_t)lds8s(mcol + i * Wm);
+        sts8s(ob + it, g_out<FAST>(g, acc));
     }
 }
 
@@ -269,89 +350,44 @@ __global__ void __launch_bounds__(9 * 32, 2) ds_fused_general_kernel(const __gri
     for (; cur.u < p.n_units; cur.next()) {
         const GenPlane& P = p.pl[cur.plane(p)];
         const int band = cur.local - P.unit_start;
-        const uint8_t* st = ring + (size_t)s * p.stage_stride;
+        const uint32_t st = smem_u32(ring) + s * p.stage_stride;
         uint8_t* ob = outs + (size_t)oslot * p.out_stride;
-        const int W = P.W, Wm = P.Wm, np = P.np;
+        const uint32_t ob_s = smem_u32(ob), mid_s = smem_u32(mid);
         mbar_wait(&full[s], phase);
 
-        // ---- H task on every staged row -> mid (u8); item = (row, H rep).
-        // The window starts at c0 < W and runs at most 19 bytes on, inside
-        // row + pad.
-        const int QH = p.h.Q, PH = p.h.P, SH = p.h.S;
-        const int h_items = P.R * np;
-        for (int it = tid; it < h_items; it += NC) {
-            const int r = g_div_small(it, np, P.np_rcp);
-            const int r1 = it - r * np;
-            const uint8_t* rowp = st + (size_t)r * P.pitch;
-            int c0 = P.oh + SH * r1;
-            if (c0 >= W) c0 -= W;                 // oh < W and Sh*r1 < W
-            uint8_t* mo = mid + (size_t)r * Wm + QH * r1;
-            if (p.h.s8) {
-                // 5 aligned words, byte-shifted into a 16-byte window (taps past P are 0)
-                const uint8_t* wb = rowp + (c0 & ~3);
-                const uint32_t sel = 0x3210u + 0x1111u * (uint32_t)(c0 & 3);
-                const uint32_t w0 = lds32(wb), w1 = lds32(wb + 4), w2 = lds32(wb + 8),
-                               w3 = lds32(wb + 12), w4 = lds32(wb + 16);
-                const uint32_t x0 = __byte_perm(w0, w1, sel), x1 = __byte_perm(w1, w2, sel),
-                               x2 = __byte_perm(w2, w3, sel), x3 = __byte_perm(w3, w4, sel);
-                switch (QH) {
-                    case 1: g_h_out<1, FAST>(p.h, x0, x1, x2, x3, mo); break;
-                    case 2: g_h_out<2, FAST>(p.h, x0, x1, x2, x3, mo); break;
-                    case 3: g_h_out<3, FAST>(p.h, x0, x1, x2, x3, mo); break;
-                    case 4: g_h_out<4, FAST>(p.h, x0, x1, x2, x3, mo); break;
-                    case 5: g_h_out<5, FAST>(p.h, x0, x1, x2, x3, mo); break;
-                    case 6: g_h_out<6, FAST>(p.h, x0, x1, x2, x3, mo); break;
-                    case 7: g_h_out<7, FAST>(p.h, x0, x1, x2, x3, mo); break;
-                    default: g_h_out<8, FAST>(p.h, x0, x1, x2, x3, mo); break;
-                }
-            } else {
-                for (int j = 0; j < QH; ++j) {
-                    int32_t acc = g_bias<FAST>(p.h);
-                    for (int i = 0; i < PH; ++i) acc += wh[j][i] * (int32_t)rowp[c0 + i];
-                    mo[j] = (uint8_t)g_out<FAST>(p.h, acc);
-                }
+        // ---- H task on every staged row -> mid (u8)
+        if (p.h.s8) {
+            switch (p.h.Q) {
+                case 1: g_h_pass<1, FAST, NC>(p.h, P, st, mid_s, tid); break;
+                case 2: g_h_pass<2, FAST, NC>(p.h, P, st, mid_s, tid); break;
+                case 3: g_h_pass<3, FAST, NC>(p.h, P, st, mid_s, tid); break;
+                case 4: g_h_pass<4, FAST, NC>(p.h, P, st, mid_s, tid); break;
+                case 5: g_h_pass<5, FAST, NC>(p.h, P, st, mid_s, tid); break;
+                case 6: g_h_pass<6, FAST, NC>(p.h, P, st, mid_s, tid); break;
+                case 7: g_h_pass<7, FAST, NC>(p.h, P, st, mid_s, tid); break;
+                default: g_h_pass<8, FAST, NC>(p.h, P, st, mid_s, tid); break;
             }
+        } else {
+            g_h_pass_bytes<FAST, NC>(p.h, wh, P, st, mid_s, tid);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);     // ring slot no longer read
         named_bar_sync(1, NC);                      // mid complete
 
         // ---- V task from mid -> output band
-        if (p.v.s8 && (Wm & 3) == 0) {
-            // item = (V repetition g, 4 mid columns): 4x4 byte transposes turn
-            // 4 rows x 4 columns into 4 column words, one dp4a per 4 taps
-            const int quads = Wm >> 2;
-            const int QV = p.v.Q;
-            const int v_items = P.k * quads;
-            for (int it = tid; it < v_items; it += NC) {
-                {
-                    const int g = g_div_small(it, quads, P.quads_rcp);
-                    const int q = it - g * quads;
-                    const uint8_t* mb = mid + (size_t)(p.v.S * g) * Wm + 4 * q;
-                    uint8_t* ob0 = ob + (size_t)(QV * g) * Wm + 4 * q;
-                    switch (QV) {
-                        case 1: g_v_quad<1, FAST>(p.v, mb, Wm, ob0); break;
-                        case 2: g_v_quad<2, FAST>(p.v, mb, Wm, ob0); break;
-                        case 3: g_v_quad<3, FAST>(p.v, mb, Wm, ob0); break;
-                        case 4: g_v_quad<4, FAST>(p.v, mb, Wm, ob0); break;
-                        case 5: g_v_quad<5, FAST>(p.v, mb, Wm, ob0); break;
-                        case 6: g_v_quad<6, FAST>(p.v, mb, Wm, ob0); break;
-                        case 7: g_v_quad<7, FAST>(p.v, mb, Wm, ob0); break;
-                        default: g_v_quad<8, FAST>(p.v, mb, Wm, ob0); break;
-                    }
-                }
+        if (p.v.s8 && (P.Wm & 3) == 0) {
+            switch (p.v.Q) {
+                case 1: g_v_pass<1, 0, FAST, NC>(p.v, P, mid_s, ob_s, tid); break;
+                case 2: g_v_pass<2, 0, FAST, NC>(p.v, P, mid_s, ob_s, tid); break;
+                case 3: g_v_pass<3, 0, FAST, NC>(p.v, P, mid_s, ob_s, tid); break;
+                case 4: g_v_pass<4, 0, FAST, NC>(p.v, P, mid_s, ob_s, tid); break;
+                case 5: g_v_pass<4, 1, FAST, NC>(p.v, P, mid_s, ob_s, tid); break;
+                case 6: g_v_pass<4, 2, FAST, NC>(p.v, P, mid_s, ob_s, tid); break;
+                case 7: g_v_pass<4, 3, FAST, NC>(p.v, P, mid_s, ob_s, tid); break;
+                default: g_v_pass<4, 4, FAST, NC>(p.v, P, mid_s, ob_s, tid); break;
             }
         } else {
-            const int v_items = P.unit_out;
-            for (int it = tid; it < v_items; it += NC) {
-                const int orow = g_div_small(it, Wm, P.wm_rcp);
-                const int c = it - orow * Wm;
-                const int g = orow / p.v.Q, kk = orow - g * p.v.Q;
-                const uint8_t* mcol = mid + (size_t)(p.v.S * g) * Wm + c;
-                int32_t acc = g_bias<FAST>(p.v);
-                for (int i = 0; i < p.v.P; ++i) acc += wv[kk][i] * (int32_t)mcol[(size_t)i * Wm];
-                ob[it] = (uint8_t)g_out<FAST>(p.v, acc);
-            }
+            g_v_pass_bytes<FAST, NC>(p.v, wv, P, mid_s, ob_s, tid);
         }
         uint8_t* dst = p.out + cur.f * p.out_frame + P.out_off + (int64_t)band * P.unit_out;
         if (p.unit_count != nullptr && tid == 0) atomicAdd(p.unit_count + cur.u, 1u);
