@@ -426,7 +426,10 @@ int configure_general(ds_handle* h) {
     // and 16-warp CTAs
     c.stages = 2;
     c.ncw = 8;
-    const int want_ctas = 2;
+#ifndef DS_GEN_CTAS
+#define DS_GEN_CTAS 2
+#endif
+    const int want_ctas = DS_GEN_CTAS;
     c.threads = (c.ncw + 1) * 32;
     c.smem = (int)general_smem(c, c.stages);
     c.fast = gen_stage(sp.h).M != 0 && gen_stage(sp.v).M != 0;

@@ -119,30 +119,59 @@ __device__ __forceinline__ int32_t g_div_small(int32_t t, int32_t d, uint32_t rc
 // c0 = (o_h + S_h r1) mod W < W and runs at most 19 bytes on, inside the row
 // and its wrap pad: 5 aligned words byte-shifted into a 16-byte window (taps
 // past P are zero in the packed weights), one dp4a per 4 taps.
+template <int Q, bool FAST>
+__device__ __forceinline__ void g_h_load(const GenStage& g, const GenPlane& P, uint32_t st, uint32_t mid, int it,
+                                         uint32_t (&x)[4], uint32_t& mo) {
+    const int r = g_div_small(it, P.np, P.np_rcp);
+    const int r1 = it - r * P.np;
+    int c0 = P.oh + g.S * r1;
+    if (c0 >= P.W) c0 -= P.W;                 // oh < W and Sh*r1 < W
+    const uint32_t wb = st + r * P.pitch + (c0 & ~3);
+    const uint32_t sel = 0x3210u + 0x1111u * (uint32_t)(c0 & 3);
+    const uint32_t w0 = lds32s(wb), w1 = lds32s(wb + 4), w2 = lds32s(wb + 8), w3 = lds32s(wb + 12),
+                   w4 = lds32s(wb + 16);
+    x[0] = __byte_perm(w0, w1, sel);
+    x[1] = __byte_perm(w1, w2, sel);
+    x[2] = __byte_perm(w2, w3, sel);
+    x[3] = __byte_perm(w3, w4, sel);
+    mo = mid + r * P.Wm + Q * r1;
+}
+template <int Q, bool FAST>
+__device__ __forceinline__ void g_h_dot(const GenStage& g, const uint32_t (&x)[4], uint32_t (&o)[Q]) {
+#pragma unroll
+    for (int j = 0; j < Q; ++j) {
+        int32_t acc = dp4a_us(x[0], g.wp[j][0], g_bias<FAST>(g));
+        acc = dp4a_us(x[1], g.wp[j][1], acc);
+        acc = dp4a_us(x[2], g.wp[j][2], acc);
+        acc = dp4a_us(x[3], g.wp[j][3], acc);
+        o[j] = g_out<FAST>(g, acc);
+    }
+}
+// Two items per thread per step (it, it + NC), loads of both issued before
+// either's arithmetic: two independent chains to hide LDS / dp4a latency.
 template <int Q, bool FAST, int NC>
 __device__ __forceinline__ void g_h_pass(const GenStage& g, const GenPlane& P, uint32_t st, uint32_t mid,
                                          int tid) {
-    const int np = P.np, W = P.W, items = P.R * np;
-    for (int it = tid; it < items; it += NC) {
-        const int r = g_div_small(it, np, P.np_rcp);
-        const int r1 = it - r * np;
-        int c0 = P.oh + g.S * r1;
-        if (c0 >= W) c0 -= W;                 // oh < W and Sh*r1 < W
-        const uint32_t wb = st + r * P.pitch + (c0 & ~3);
-        const uint32_t sel = 0x3210u + 0x1111u * (uint32_t)(c0 & 3);
-        const uint32_t w0 = lds32s(wb), w1 = lds32s(wb + 4), w2 = lds32s(wb + 8), w3 = lds32s(wb + 12),
-                       w4 = lds32s(wb + 16);
-        const uint32_t x0 = __byte_perm(w0, w1, sel), x1 = __byte_perm(w1, w2, sel),
-                       x2 = __byte_perm(w2, w3, sel), x3 = __byte_perm(w3, w4, sel);
-        const uint32_t mo = mid + r * P.Wm + Q * r1;
+    const int items = P.R * P.np;
+    int it = tid;
+    for (; it + NC < items; it += 2 * NC) {
+        uint32_t xa[4], xb[4], ma, mb, oa[Q], ob[Q];
+        g_h_load<Q, FAST>(g, P, st, mid, it, xa, ma);
+        g_h_load<Q, FAST>(g, P, st, mid, it + NC, xb, mb);
+        g_h_dot<Q, FAST>(g, xa, oa);
+        g_h_dot<Q, FAST>(g, xb, ob);
 #pragma unroll
         for (int j = 0; j < Q; ++j) {
-            int32_t acc = dp4a_us(x0, g.wp[j][0], g_bias<FAST>(g));
-            acc = dp4a_us(x1, g.wp[j][1], acc);
-            acc = dp4a_us(x2, g.wp[j][2], acc);
-            acc = dp4a_us(x3, g.wp[j][3], acc);
-            sts8s(mo + j, g_out<FAST>(g, acc));
+            sts8s(ma + j, oa[j]);
+            sts8s(mb + j, ob[j]);
         }
+    }
+    if (it < items) {
+        uint32_t xa[4], ma, oa[Q];
+        g_h_load<Q, FAST>(g, P, st, mid, it, xa, ma);
+        g_h_dot<Q, FAST>(g, xa, oa);
+#pragma unroll
+        for (int j = 0; j < Q; ++j) sts8s(ma + j, oa[j]);
     }
 }
 // Taps outside s8: byte loop (same item space, same window bounds)
@@ -278,8 +307,11 @@ struct GenCursor {
 
 // 2 CTAs x (8 consumer + 1 producer) warps per SM: the register file is
 // split across 4 SMSPs, so 18 warps need <= 102 registers each.
+#ifndef DS_GEN_MINB
+#define DS_GEN_MINB 2
+#endif
 template <bool FAST>
-__global__ void __launch_bounds__(9 * 32, 2) ds_fused_general_kernel(const __grid_constant__ GeneralParams p) {
+__global__ void __launch_bounds__(9 * 32, DS_GEN_MINB) ds_fused_general_kernel(const __grid_constant__ GeneralParams p) {
     constexpr int NCW = 8;
     extern __shared__ __align__(1024) uint8_t smem[];
     constexpr int NC = NCW * 32;

@@ -52,7 +52,10 @@ struct FusedCfg {
 };
 
 constexpr int64_t kFineUnitTarget = 16 * 1024;      // small batches: more, smaller units
-constexpr int64_t kGeneralStageTarget = 40 * 1024;  // K-N1g staged rows per unit
+#ifndef DS_GEN_STAGE_TARGET
+#define DS_GEN_STAGE_TARGET (40 * 1024)
+#endif
+constexpr int64_t kGeneralStageTarget = DS_GEN_STAGE_TARGET;  // K-N1g staged rows per unit
 
 // K-N1g launch configuration (any stage spec).
 struct GeneralCfg {

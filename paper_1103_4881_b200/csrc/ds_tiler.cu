@@ -50,6 +50,17 @@ struct TaskParams {
     // DS_TOPO_SPEC: collapsed multiplicity (row-major, last fastest -> CUDA x)
     int32_t tdim;
     int64_t tmult[3];
+    // Affine path (host-proved: no tiler index wraps anywhere in the box, so the
+    // element offset is A + sum_j a[j] r_j + b[e], all in [0, n) < 2^31)
+    int32_t affine;                    // 0: modulo path; 1: byte loads; 2: word loads + dp4a
+    uint32_t in_A, out_A;
+    uint32_t in_a[4], out_a[4];
+    int32_t in_b[DS_MAX_PATTERN], out_b[DS_MAX_OUTPUTS];
+    uint32_t wp[DS_MAX_OUTPUTS][DS_MAX_PATTERN / 4];   // s8-packed weights (affine == 2)
+    // exact division: clamp(trunc(acc / D)) = min(umulhi(max(acc + fb - bias, lo), M), 255)
+    // when fastdiv (host-checked range), else the integer division
+    int32_t fastdiv, fbias;
+    uint32_t M, lo;
 };
 
 __device__ __forceinline__ int64_t t_mod(int64_t a, int64_t m) {
@@ -158,6 +169,102 @@ __device__ __forceinline__ void task_one(const TaskParams& p, int64_t q) {
         int32_t v = acc / p.divisor;                      // truncation toward zero
         v = v < 0 ? 0 : (v > 255 ? 255 : v);
         p.out[t_lin(p.tout, base, k)] = (uint8_t)v;
+    }
+}
+
+// d = c + sum_i a.u8[i] * b.s8[i]
+__device__ __forceinline__ int32_t t_dp4a(uint32_t a, uint32_t b, int32_t c) {
+    int32_t d;
+    asm("dp4a.u32.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+__device__ __forceinline__ uint8_t t_out(const TaskParams& p, int32_t acc) {
+    if (p.fastdiv) return (uint8_t)min(__umulhi((uint32_t)max(acc, (int32_t)p.lo), p.M), 255u);
+    int32_t v = acc / p.divisor;                          // truncation toward zero
+    return (uint8_t)(v < 0 ? 0 : (v > 255 ? 255 : v));
+}
+
+// One elementary task on the affine path (same result as task_one: the
+// offsets are the S:248-252 element indices, proved wrap-free on the host).
+// NI = n_in rounded up to 4 (weights past n_in are zero); WORDS: the pattern is
+// NI contiguous, 4-byte aligned input bytes and the taps fit s8.
+template <int NI, bool WORDS>
+__device__ __forceinline__ void task_affine(const TaskParams& p, uint32_t q) {
+    uint32_t bi = p.in_A, bo = p.out_A;
+#pragma unroll
+    for (int j = 3; j >= 0; --j) {
+        if (j < p.nrep) {
+            const uint32_t qq = fdiv(p.rdiv[j], q);
+            const uint32_t r = q - qq * p.rdiv[j].d;
+            bi += p.in_a[j] * r;
+            bo += p.out_a[j] * r;
+            q = qq;
+        }
+    }
+    int32_t acc[DS_MAX_OUTPUTS];
+    if (WORDS) {
+        uint32_t x[NI / 4];
+        const uint32_t* src = reinterpret_cast<const uint32_t*>(p.in + bi);
+#pragma unroll
+        for (int i = 0; i < NI / 4; ++i) x[i] = __ldg(src + i);
+#pragma unroll
+        for (int k = 0; k < DS_MAX_OUTPUTS; ++k) {
+            if (k < p.n_out) {
+                int32_t a = p.bias;
+#pragma unroll
+                for (int i = 0; i < NI / 4; ++i) a = t_dp4a(x[i], p.wp[k][i], a);
+                acc[k] = a;
+            }
+        }
+    } else {
+        int32_t pat[NI];
+#pragma unroll
+        for (int e = 0; e < NI; ++e) pat[e] = e < p.n_in ? (int32_t)__ldg(p.in + bi + p.in_b[e]) : 0;
+#pragma unroll
+        for (int k = 0; k < DS_MAX_OUTPUTS; ++k) {
+            if (k < p.n_out) {
+                int32_t a = p.bias;
+#pragma unroll
+                for (int e = 0; e < NI; ++e) a += p.w[k][e] * pat[e];
+                acc[k] = a;
+            }
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < DS_MAX_OUTPUTS; ++k)
+        if (k < p.n_out) p.out[bo + p.out_b[k]] = t_out(p, acc[k] + (p.fastdiv ? p.fbias - p.bias : 0));
+}
+
+template <int NI, bool WORDS>
+__global__ void __launch_bounds__(256) ds_task_affine_kernel(const __grid_constant__ TaskParams p) {
+    if (p.policy == DS_TOPO_SPEC) {
+        const uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
+        const uint32_t y = blockIdx.y * blockDim.y + threadIdx.y;
+        const uint32_t z = blockIdx.z * blockDim.z + threadIdx.z;
+        uint32_t c[3] = {0, 0, 0};
+        if (p.tdim == 1) { c[0] = x; }
+        else if (p.tdim == 2) { c[0] = y; c[1] = x; }
+        else { c[0] = z; c[1] = y; c[2] = x; }
+        uint32_t q = 0;
+        for (int d = 0; d < p.tdim; ++d) {
+            if (c[d] >= (uint32_t)p.tmult[d]) return;     // guard
+            q = q * (uint32_t)p.tmult[d] + c[d];
+        }
+        task_affine<NI, WORDS>(p, q);
+        return;
+    }
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < (uint32_t)p.n_reps; q += stride)
+        task_affine<NI, WORDS>(p, q);
+}
+
+using TaskFn = void (*)(const TaskParams);
+TaskFn affine_fn(int ni, bool words) {
+    switch ((ni + 3) / 4) {
+        case 1: return words ? ds_task_affine_kernel<4, true> : ds_task_affine_kernel<4, false>;
+        case 2: return words ? ds_task_affine_kernel<8, true> : ds_task_affine_kernel<8, false>;
+        case 3: return words ? ds_task_affine_kernel<12, true> : ds_task_affine_kernel<12, false>;
+        default: return words ? ds_task_affine_kernel<16, true> : ds_task_affine_kernel<16, false>;
     }
 }
 
@@ -311,6 +418,64 @@ bool fits32(const TaskParams& p, const TTiler& t) {
     return n < lim;
 }
 
+// Affine analysis of a tiler over the repetition box (host).  Every origin /
+// paving / fitting coefficient c may be replaced by any value congruent to it
+// mod the extent s; for each array dim, search the two
+// representatives c mod s and c mod s - s of every coefficient with a nonzero
+// range for a choice under which origin + paving.r + fitting.f stays inside
+// [0, s) over the whole box.  If every dim has one, no modulo ever applies and
+// the row-major element offset is A + sum_j a[j] r_j + b[e].
+bool affine_tiler(const ds_tiler& t, int32_t nrep, const int64_t* rep, uint32_t* A, uint32_t* a,
+                  int32_t* b, int nb_max) {
+    int64_t stride[4], st = 1;
+    for (int d = t.ndim - 1; d >= 0; --d) { stride[d] = st; st *= t.shape[d]; }
+    if (st >= (1LL << 31)) return false;
+    const int64_t npe = pattern_elems(t);
+    if (npe > nb_max) return false;
+    int64_t A64 = 0, a64[4] = {0, 0, 0, 0};
+    int64_t fit[4][4] = {};
+    for (int d = 0; d < t.ndim; ++d) {
+        const int64_t s = t.shape[d];
+        const int64_t o = h_mod(t.origin[d], s);
+        // coefficients (reps then pattern dims) and their index ranges
+        int64_t c[8], n[8];
+        int nc = 0;
+        for (int j = 0; j < nrep; ++j) { c[nc] = h_mod(t.paving[d][j], s); n[nc++] = rep[j] - 1; }
+        for (int k = 0; k < t.npat; ++k) { c[nc] = h_mod(t.fitting[d][k], s); n[nc++] = t.pattern[k] - 1; }
+        bool found = false;
+        int64_t best[8];
+        for (uint32_t m = 0; m < (1u << nc) && !found; ++m) {
+            int64_t lo = o, hi = o, v[8];
+            bool skip = false;
+            for (int i = 0; i < nc; ++i) {
+                const bool neg = (m >> i) & 1u;
+                if (neg && (c[i] == 0 || n[i] == 0)) { skip = true; break; }   // one choice suffices
+                v[i] = neg ? c[i] - s : c[i];
+                const int64_t ext = v[i] * n[i];
+                (ext < 0 ? lo : hi) += ext;
+            }
+            if (skip || lo < 0 || hi >= s) continue;
+            found = true;
+            for (int i = 0; i < nc; ++i) best[i] = v[i];
+        }
+        if (!found) return false;
+        A64 += o * stride[d];
+        for (int j = 0; j < nrep; ++j) a64[j] += best[j] * stride[d];
+        for (int k = 0; k < t.npat; ++k) fit[d][k] = best[nrep + k];
+    }
+    for (int64_t e = 0; e < npe; ++e) {
+        int64_t f[4] = {0, 0, 0, 0}, rem = e;
+        for (int k = t.npat - 1; k >= 0; --k) { f[k] = rem % t.pattern[k]; rem /= t.pattern[k]; }
+        int64_t off = 0;
+        for (int d = 0; d < t.ndim; ++d)
+            for (int k = 0; k < t.npat; ++k) off += fit[d][k] * f[k] * stride[d];
+        b[e] = (int32_t)off;
+    }
+    *A = (uint32_t)A64;
+    for (int j = 0; j < 4; ++j) a[j] = (uint32_t)(j < nrep ? a64[j] : 0);
+    return true;
+}
+
 int64_t next_pow2(int64_t x) {
     int64_t p = 1;
     while (p < x) p <<= 1;
@@ -427,6 +592,37 @@ DS_API int ds_run_task(const uint8_t* in, const ds_tiler* t_in, uint8_t* out, co
     p.divisor = body->divisor;
     p.bias = body->bias;
     std::memcpy(p.w, body->weight, sizeof p.w);
+    // affine path: both tilers wrap-free, 32-bit offsets and repetition index
+    if (p.n_reps < (1LL << 31) && affine_tiler(*t_in, nrep, rep_shape, &p.in_A, p.in_a, p.in_b, DS_MAX_PATTERN) &&
+        affine_tiler(*t_out, nrep, rep_shape, &p.out_A, p.out_a, p.out_b, DS_MAX_OUTPUTS)) {
+        p.affine = 1;
+        bool words = p.n_in % 4 == 0 && (reinterpret_cast<uintptr_t>(in) & 3) == 0 && p.in_A % 4 == 0;
+        for (int j = 0; j < nrep; ++j) words = words && p.in_a[j] % 4 == 0;
+        for (int e = 0; e < p.n_in; ++e) words = words && p.in_b[e] == e;
+        int64_t amax = 0;
+        for (int k = 0; k < p.n_out; ++k) {
+            int64_t pos = body->bias;
+            for (int e = 0; e < p.n_in; ++e) {
+                const int32_t w = body->weight[k][e];
+                if (w < -128 || w > 127) words = false;
+                if (w > 0) pos += 255LL * w;
+                p.wp[k][e / 4] |= (uint32_t)(uint8_t)(int8_t)(w < -128 || w > 127 ? 0 : w) << (8 * (e % 4));
+            }
+            amax = std::max(amax, pos);
+        }
+        if (words) p.affine = 2;
+        // exact multiply-high division (same derivation as K-N1g's FASTDIV)
+        const uint64_t D = (uint64_t)body->divisor;
+        if (D == 1) {
+            if (amax < 0x7fffffffLL) { p.fastdiv = 1; p.M = 0xffffffffu; p.lo = 1; p.fbias = body->bias + 1; }
+        } else {
+            const uint64_t M = ((1ULL << 32) + D - 1) / D, e = M * D - (1ULL << 32);
+            if ((unsigned __int128)(uint64_t)amax * e < ((unsigned __int128)1 << 32)) {
+                p.fastdiv = 1; p.M = (uint32_t)M; p.lo = 0; p.fbias = body->bias;
+            }
+        }
+    }
+    const TaskFn fn = p.affine ? affine_fn(p.n_in, p.affine == 2) : ds_task_kernel;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     if (policy == DS_TOPO_SPEC) {
         ds_topology topo;
@@ -442,10 +638,10 @@ DS_API int ds_run_task(const uint8_t* in, const ds_tiler* t_in, uint8_t* out, co
             (ax == 0 ? block.x : ax == 1 ? block.y : block.z) = (unsigned)topo.local[d];
             (ax == 0 ? grid.x : ax == 1 ? grid.y : grid.z) = (unsigned)g;
         }
-        ds_task_kernel<<<grid, block, 0, st>>>(p);
+        fn<<<grid, block, 0, st>>>(p);
     } else {
         const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((p.n_reps + 255) / 256, (int64_t)sms * 16));
-        ds_task_kernel<<<(unsigned)blocks, 256, 0, st>>>(p);
+        fn<<<(unsigned)blocks, 256, 0, st>>>(p);
     }
     return cudaGetLastError() == cudaSuccess ? DS_OK : DS_ECUDA;
 }

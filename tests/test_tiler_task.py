@@ -182,3 +182,84 @@ def test_run_task_large_extents(policy):
                 ds.make_body(w, 6, 3, n_in=8), policy=policy)
     torch.cuda.synchronize()
     assert np.array_equal(y.cpu().numpy(), want)
+
+
+def _affine_in_tiler(rng, in_shape, R, P):
+    """A wrap-free 1-rep / 1-pattern input tiler on `in_shape` (possibly with
+    negative paving or fitting and a shifted origin): the affine task path."""
+    nd = len(in_shape)
+    pav, fit, origin = [], [], []
+    for d in range(nd):
+        s = in_shape[d]
+        p = int(rng.integers(-(s // max(R, 1)), s // max(R, 1) + 1)) if R > 1 else int(rng.integers(-3, 4))
+        f = int(rng.integers(-(s // max(P, 1)), s // max(P, 1) + 1)) if P > 1 else int(rng.integers(-3, 4))
+        lo = min(0, p * (R - 1)) + min(0, f * (P - 1))
+        hi = max(0, p * (R - 1)) + max(0, f * (P - 1))
+        if hi - lo >= s:
+            p, f, lo, hi = 0, 0, 0, 0
+        o = int(rng.integers(-lo, s - hi))
+        # add multiples of the extent: same tiler mod shape (S:251), still affine
+        pav.append([p + s * int(rng.integers(-2, 3))])
+        fit.append([f + s * int(rng.integers(-2, 3))])
+        origin.append(o + s * int(rng.integers(-2, 3)))
+    return origin, pav, fit
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("policy", [ds.DS_TOPO_FLAT, ds.DS_TOPO_SPEC])
+def test_run_task_affine_random(policy):
+    """Wrap-free tilers take the affine path (offsets A + a.r + b[e], no
+    modulo); results must equal the oracle's modulo tiler semantics."""
+    rng = np.random.default_rng(4881 + policy)
+    for trial in range(60):
+        nd = int(rng.integers(1, 4))
+        R = int(rng.integers(1, 300))
+        P = int(rng.integers(1, 17))
+        Q = int(rng.integers(1, 9))
+        in_shape = [int(rng.integers(1, 40)) for _ in range(nd)]
+        in_shape[-1] = max(in_shape[-1], int(rng.integers(P, 4 * P + 2)))
+        origin, pav, fit = _affine_in_tiler(rng, in_shape, R, P)
+        tin_o = oracle.make_tiler(in_shape, origin, pav, fit, [P])
+        tin_d = ds.make_tiler(in_shape, origin, pav, fit, [P])
+        kind = int(rng.integers(0, 2))
+        out_shape = (R, Q) if kind == 0 else (Q, R)
+        opav, ofit = ([[1], [0]], [[0], [1]]) if kind == 0 else ([[0], [1]], [[1], [0]])
+        tout_o = oracle.make_tiler(out_shape, (0, 0), opav, ofit, [Q])
+        tout_d = ds.make_tiler(out_shape, (0, 0), opav, ofit, [Q])
+        wide = trial % 3 == 0
+        w = [[int(x) for x in rng.integers(-300 if wide else -20, 300 if wide else 60, P)] for _ in range(Q)]
+        D = int(rng.choice([1, 2, 3, 6, 7, 8, 255, 1000, 65537, 1 << 20]))
+        B = int(rng.integers(-100, 100))
+        a = rng.integers(0, 256, in_shape).astype(np.uint8)
+        want = oracle.run_task(a, tin_o, out_shape, tout_o, [R], oracle.make_stage(P, P, 0, w, D, B))
+        x = torch.from_numpy(a).cuda()
+        y = torch.zeros(out_shape, dtype=torch.uint8, device="cuda")
+        ds.run_task(x, tin_d, y, tout_d, [R], ds.make_body(w, D, B, n_in=P), policy=policy)
+        torch.cuda.synchronize()
+        assert np.array_equal(y.cpu().numpy(), want), (trial, in_shape, origin, pav, fit, R, P, Q, D)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("P", [4, 8, 12, 16])
+def test_run_task_affine_words(P):
+    """Contiguous, word-aligned patterns with s8 taps take the word-load + dp4a
+    affine path; a 3-D repetition space (frames outermost) as in the paper's
+    yhfk task, plus a 1-byte-shifted origin that forces the byte path."""
+    rng = np.random.default_rng(P)
+    n, H, Wp = 3, 37, 24
+    W = P * Wp
+    a = rng.integers(0, 256, (n, H, W)).astype(np.uint8)
+    Q = 3
+    w = [[int(x) for x in rng.integers(-128, 128, P)] for _ in range(Q)]
+    for origin in ((0, 0, 0), (0, 0, 1)):
+        reps = [n, H, Wp - (1 if origin[2] else 0)]
+        tin = ((n, H, W), origin, [[1, 0, 0], [0, 1, 0], [0, 0, P]], [[0], [0], [1]], [P])
+        tout = ((n, H, reps[2] * Q), (0, 0, 0), [[1, 0, 0], [0, 1, 0], [0, 0, Q]], [[0], [0], [1]], [Q])
+        for D, B in ((1, 0), (6, 3), (1 << 20, 5)):
+            want = oracle.run_task(a, oracle.make_tiler(*tin), tout[0], oracle.make_tiler(*tout), reps,
+                                   oracle.make_stage(P, P, 0, w, D, B))
+            y = torch.zeros(tout[0], dtype=torch.uint8, device="cuda")
+            ds.run_task(torch.from_numpy(a).cuda(), ds.make_tiler(*tin), y, ds.make_tiler(*tout), reps,
+                        ds.make_body(w, D, B, n_in=P))
+            torch.cuda.synchronize()
+            assert np.array_equal(y.cpu().numpy(), want), (origin, D, B)

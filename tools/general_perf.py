@@ -89,9 +89,16 @@ def generic_task(n=300, W=1920, H=1080):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default="gpurun_out/general_perf.json")
+    ap.add_argument("--quick", action="store_true", help="K-N1g only, one line per spec")
     a = ap.parse_args()
     torch.cuda.set_device(0)
     halo = ds.make_spec(h=HALO_H, v=HALO_V)
+    if a.quick:
+        h = run(1920, 1080, 300, halo, [ds.DS_KERNEL_FUSED_GENERAL], steps=50)
+        t = run(1920, 1080, 300, None, [ds.DS_KERNEL_FUSED_GENERAL], steps=50)
+        k = ds.KERNEL_NAMES[ds.DS_KERNEL_FUSED_GENERAL]
+        print(json.dumps({"halo_ms": round(h[k]["ms"], 4), "spec_taps_ms": round(t[k]["ms"], 4)}))
+        return
     out = {
         "gpu": torch.cuda.get_device_name(0),
         "halo_spec": {"h": HALO_H, "v": HALO_V},
