@@ -61,6 +61,7 @@ struct TaskParams {
     // when fastdiv (host-checked range), else the integer division
     int32_t fastdiv, fbias;
     uint32_t M, lo;
+    int32_t dense;                     // affine == 2 and both tilers are dense row-major runs
 };
 
 __device__ __forceinline__ int64_t t_mod(int64_t a, int64_t m) {
@@ -258,7 +259,61 @@ __global__ void __launch_bounds__(256) ds_task_affine_kernel(const __grid_consta
         task_affine<NI, WORDS>(p, q);
 }
 
+// Dense task (host-proved: input element offset in_A + n_in q + e, output
+// offset out_A + n_out q + k, q the row-major repetition index; taps s8,
+// n_in % 4 == 0, input run 16-byte aligned, output run 4-byte aligned): a
+// streaming map.  Each lane takes 4 consecutive repetitions (16-byte loads);
+// the warp stages its 128 Q output bytes in shared memory and writes them as
+// coalesced words.  Repetitions past the last full warp use task_affine.
+template <int NI>
+__global__ void __launch_bounds__(256) ds_task_dense_kernel(const __grid_constant__ TaskParams p) {
+    __shared__ __align__(16) uint8_t buf[8][128 * DS_MAX_OUTPUTS];
+    const int lane = threadIdx.x & 31;
+    uint8_t* b = buf[threadIdx.x >> 5];
+    const uint32_t Q = (uint32_t)p.n_out;
+    const uint32_t full = (uint32_t)(p.n_reps / 128);
+    const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < full; w += nw) {
+        const uint32_t rep0 = w * 128 + 4 * lane;
+        const uint4* src = reinterpret_cast<const uint4*>(p.in + p.in_A + (uint32_t)NI * rep0);
+        uint32_t x[NI];
+#pragma unroll
+        for (int i = 0; i < NI / 4; ++i) {
+            const uint4 v = __ldg(src + i);
+            x[4 * i] = v.x; x[4 * i + 1] = v.y; x[4 * i + 2] = v.z; x[4 * i + 3] = v.w;
+        }
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+#pragma unroll
+            for (int k = 0; k < DS_MAX_OUTPUTS; ++k) {
+                if (k < (int)Q) {
+                    int32_t acc = p.fastdiv ? p.fbias : p.bias;
+#pragma unroll
+                    for (int i = 0; i < NI / 4; ++i) acc = t_dp4a(x[r * (NI / 4) + i], p.wp[k][i], acc);
+                    b[(4 * lane + r) * Q + k] = t_out(p, acc);
+                }
+            }
+        }
+        __syncwarp();
+        uint32_t* dst = reinterpret_cast<uint32_t*>(p.out + p.out_A + Q * 128 * w);
+        const uint32_t* bw = reinterpret_cast<const uint32_t*>(b);
+        for (uint32_t j = lane; j < 32 * Q; j += 32) dst[j] = bw[j];
+        __syncwarp();
+    }
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t q = full * 128 + blockIdx.x * blockDim.x + threadIdx.x; q < (uint32_t)p.n_reps; q += stride)
+        task_affine<NI, true>(p, q);
+}
+
 using TaskFn = void (*)(const TaskParams);
+TaskFn dense_fn(int ni) {
+    switch ((ni + 3) / 4) {
+        case 1: return ds_task_dense_kernel<4>;
+        case 2: return ds_task_dense_kernel<8>;
+        case 3: return ds_task_dense_kernel<12>;
+        default: return ds_task_dense_kernel<16>;
+    }
+}
 TaskFn affine_fn(int ni, bool words) {
     switch ((ni + 3) / 4) {
         case 1: return words ? ds_task_affine_kernel<4, true> : ds_task_affine_kernel<4, false>;
@@ -611,6 +666,17 @@ DS_API int ds_run_task(const uint8_t* in, const ds_tiler* t_in, uint8_t* out, co
             amax = std::max(amax, pos);
         }
         if (words) p.affine = 2;
+        // dense: both tilers are row-major runs over the repetition index
+        bool dense = words && policy == DS_TOPO_FLAT &&
+                     ((reinterpret_cast<uintptr_t>(in) + p.in_A) & 15) == 0 &&
+                     ((reinterpret_cast<uintptr_t>(out) + p.out_A) & 3) == 0;
+        int64_t inner = 1;
+        for (int j = nrep - 1; j >= 0; --j) {
+            dense = dense && p.in_a[j] == (uint64_t)(p.n_in * inner) && p.out_a[j] == (uint64_t)(p.n_out * inner);
+            inner *= rep_shape[j];
+        }
+        for (int k = 0; k < p.n_out; ++k) dense = dense && p.out_b[k] == k;
+        p.dense = dense ? 1 : 0;
         // exact multiply-high division (same derivation as K-N1g's FASTDIV)
         const uint64_t D = (uint64_t)body->divisor;
         if (D == 1) {
@@ -622,7 +688,7 @@ DS_API int ds_run_task(const uint8_t* in, const ds_tiler* t_in, uint8_t* out, co
             }
         }
     }
-    const TaskFn fn = p.affine ? affine_fn(p.n_in, p.affine == 2) : ds_task_kernel;
+    const TaskFn fn = p.dense ? dense_fn(p.n_in) : p.affine ? affine_fn(p.n_in, p.affine == 2) : ds_task_kernel;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     if (policy == DS_TOPO_SPEC) {
         ds_topology topo;

@@ -242,14 +242,15 @@ def test_run_task_affine_random(policy):
 @pytest.mark.gpu
 @pytest.mark.parametrize("P", [4, 8, 12, 16])
 def test_run_task_affine_words(P):
-    """Contiguous, word-aligned patterns with s8 taps take the word-load + dp4a
-    affine path; a 3-D repetition space (frames outermost) as in the paper's
-    yhfk task, plus a 1-byte-shifted origin that forces the byte path."""
+    """Contiguous, word-aligned patterns with s8 taps take the dense streaming
+    path (both tilers row-major runs; 20 full warps of 128 repetitions plus a
+    ragged tail) -- a 3-D repetition space, frames outermost, as in the paper's
+    yhfk task; a 1-byte-shifted origin forces the affine byte path."""
     rng = np.random.default_rng(P)
     n, H, Wp = 3, 37, 24
     W = P * Wp
     a = rng.integers(0, 256, (n, H, W)).astype(np.uint8)
-    Q = 3
+    Q = {4: 1, 8: 3, 12: 5, 16: 8}[P]       # dense path: 128 Q output bytes per warp
     w = [[int(x) for x in rng.integers(-128, 128, P)] for _ in range(Q)]
     for origin in ((0, 0, 0), (0, 0, 1)):
         reps = [n, H, Wp - (1 if origin[2] else 0)]
