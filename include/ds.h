@@ -221,6 +221,17 @@ DS_API int ds_set_tuning(ds_handle* h, int32_t stages, int32_t ctas_per_sm);
  * in flight on other threads. */
 DS_API int ds_set_band_bytes(ds_handle* h, int64_t target_bytes);
 
+/* K-N1g run length: with a V halo (v.pattern > v.paving) a work unit is a
+ * run of consecutive bands of one plane, and each band after the first
+ * reuses the previous band's intermediate rows for the Pv - Sv halo rows
+ * instead of staging and H-filtering them again.  bands > 0 forces that
+ * many bands per run (clamped to the plane); 0 (default) picks runs per
+ * launch, split evenly within each plane, as long as the launch keeps
+ * >= 16 units per CTA slot.  No effect
+ * without a V halo.  Output is unaffected.  Not synchronised with ds_run
+ * calls in flight on other threads. */
+DS_API int ds_set_run_bands(ds_handle* h, int32_t bands);
+
 /* K-N1 launch shape that ds_run would use for n_frames:
  * grid CTAs, threads per CTA, dynamic shared memory bytes. */
 DS_API int ds_launch_shape(const ds_handle* h, int64_t n_frames, int32_t* grid,

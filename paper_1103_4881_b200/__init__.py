@@ -162,6 +162,7 @@ SIGNATURES = [
     ("ds_last_kernel", C.c_int, [C.c_void_p]),
     ("ds_set_tuning", C.c_int, [C.c_void_p, C.c_int32, C.c_int32]),
     ("ds_set_band_bytes", C.c_int, [C.c_void_p, C.c_int64]),
+    ("ds_set_run_bands", C.c_int, [C.c_void_p, C.c_int32]),
     ("ds_launch_shape", C.c_int, [C.c_void_p, C.c_int64, _PI32, _PI32, _PI32]),
     ("ds_mid_frame_bytes", C.c_int64, [C.c_void_p]),
     ("ds_run_htask", C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int32, C.c_int32,
@@ -453,6 +454,12 @@ class Downscaler:
         if rc:
             raise DSError(rc, "ds_set_band_bytes")
         self.plan = self.get_plan()
+
+    def set_run_bands(self, bands: int) -> None:
+        """K-N1g: bands per run when the V stage has a halo (0 = automatic)."""
+        rc = lib().ds_set_run_bands(self._h, bands)
+        if rc:
+            raise DSError(rc, "ds_set_run_bands")
 
     def get_plan(self):
         info = ds_plan_info()

@@ -172,6 +172,9 @@ int make_plan(int32_t W, int32_t H, int32_t channels, const ds_filter_spec* spec
     bool general = true;         // any width: unaligned rows are staged with plain loads
     if (general) {
         int64_t units = 0, smax = 0, mmax = 0, omax = 0;
+        // with a V halo (Pv > Sv) consecutive bands of a run reuse the halo's mid
+        // rows, so small bands cost little and leave smem for a second mid buffer
+        const int64_t stage_target = spec.v.pattern > spec.v.paving ? kGeneralStageTargetReuse : kGeneralStageTarget;
         for (int p = 0; p < channels; ++p) {
             const int G = pi.in_h[p] / spec.v.paving;
             const int64_t pitch = general_pitch(pi.in_w[p]);
@@ -179,7 +182,7 @@ int make_plan(int32_t W, int32_t H, int32_t channels, const ds_filter_spec* spec
             for (int d = 1; d <= G; ++d) {
                 if (G % d) continue;
                 const int64_t R = (int64_t)spec.v.paving * (d - 1) + spec.v.pattern;
-                if (R * pitch <= kGeneralStageTarget) best = d;
+                if (R * pitch <= stage_target) best = d;
             }
             const int64_t R = (int64_t)spec.v.paving * (best - 1) + spec.v.pattern;
             pi.general_band_reps[p] = best;
@@ -193,7 +196,8 @@ int make_plan(int32_t W, int32_t H, int32_t channels, const ds_filter_spec* spec
                 (int64_t)spec.v.outputs * best * pi.out_w[p] * pi.out_w[p] >= (1LL << 32))
                 general = false;
         }
-        const int64_t need = 2 * round_up(smax, 128) + round_up(mmax, 128) + 2 * round_up(omax, 128) +
+        const int64_t mids = spec.v.pattern > spec.v.paving ? 2 : 1;
+        const int64_t need = 2 * round_up(smax, 128) + mids * round_up(mmax, 128) + 2 * round_up(omax, 128) +
                              2 * DS_MAX_OUTPUTS * DS_MAX_PATTERN * 4 + 64;
         if (need > kSmemLimit) general = false;
         pi.general_units_per_frame = units;
@@ -361,7 +365,46 @@ int launch_fused(ds_handle* h, const uint8_t* in, int64_t n, uint8_t* out, cudaS
 using GeneralFn = void (*)(const ds::GeneralParams);
 
 int64_t general_smem(const GeneralCfg& c, int stages) {
-    return (int64_t)stages * c.stage_stride + c.mid_stride + 2LL * c.out_stride + 2LL * stages * 8;
+    return (int64_t)stages * c.stage_stride + c.mid_stride + c.mid_alt + 2LL * c.out_stride + 2LL * stages * 8;
+}
+
+// K-N1g run lengths for a launch over n frames: with a V halo, a unit is a
+// run of L_p consecutive bands of one plane (the halo's mid rows carry over).
+// Runs grow (by work per band, split evenly within a plane) while the
+// launch keeps >= 16 units per CTA slot, so the persistent schedule's tail
+// stays <= ~1/16 (tools/general_perf.py --run-bands sweep: 8 HD luma bands
+// per run beat 1, 2, 4, 16 and whole planes).  Returns units per frame.
+int32_t general_runs(const ds_handle* h, int64_t n, int32_t* L) {
+    const GeneralCfg& c = h->general;
+    const ds_plan_info& pi = h->plan;
+    int64_t bb[DS_MAX_PLANES], bbmax = 1;
+    for (int q = 0; q < pi.n_planes; ++q) {
+        L[q] = 1;
+        bb[q] = (int64_t)c.R[q] * pi.in_w[q];
+        bbmax = std::max(bbmax, bb[q]);
+    }
+    auto upf_of = [&](const int32_t* l) {
+        int32_t u = 0;
+        for (int q = 0; q < pi.n_planes; ++q) u += (c.nb[q] + l[q] - 1) / l[q];
+        return u;
+    };
+    if (c.mid_alt == 0) return upf_of(L);
+    if (h->run_bands > 0) {
+        for (int q = 0; q < pi.n_planes; ++q) L[q] = std::min<int32_t>(h->run_bands, c.nb[q]);
+        return upf_of(L);
+    }
+    const int64_t slots = std::max<int64_t>(1, (int64_t)c.grid_per_sm * h->sm_count);
+    for (int64_t T = 2 * bbmax; T <= 64 * bbmax; T *= 2) {
+        int32_t l[DS_MAX_PLANES];
+        for (int q = 0; q < pi.n_planes; ++q) {
+            const int64_t want = std::max<int64_t>(1, std::min<int64_t>(c.nb[q], T / bb[q]));
+            const int64_t runs = (c.nb[q] + want - 1) / want;
+            l[q] = (int32_t)((c.nb[q] + runs - 1) / runs);      // equal runs within the plane
+        }
+        if (n * upf_of(l) < 16 * slots) break;
+        for (int q = 0; q < pi.n_planes; ++q) L[q] = l[q];
+    }
+    return upf_of(L);
 }
 
 // Stage constants for K-N1g.  FASTDIV (M != 0): floor(a / D) = umulhi(a, M)
@@ -411,6 +454,7 @@ int configure_general(ds_handle* h) {
     int32_t upf = 0;
     for (int p = 0; p < pi.n_planes; ++p) {
         c.k[p] = pi.general_band_reps[p];
+        c.nb[p] = (pi.in_h[p] / sp.v.paving) / c.k[p];
         c.R[p] = sp.v.paving * (c.k[p] - 1) + sp.v.pattern;
         smax = std::max<int64_t>(smax, (int64_t)c.R[p] * general_pitch(pi.in_w[p]));
         mmax = std::max<int64_t>(mmax, (int64_t)(c.R[p] + 3) * pi.out_w[p]);   // V reads 4-row blocks
@@ -420,6 +464,8 @@ int configure_general(ds_handle* h) {
     c.upf = upf;
     c.stage_stride = (int32_t)round_up(smax, 128);
     c.mid_stride = (int32_t)round_up(mmax, 128);
+    c.ovl = std::max(0, sp.v.pattern - sp.v.paving);
+    c.mid_alt = c.ovl > 0 ? c.mid_stride : 0;     // second mid buffer for halo reuse
     c.out_stride = (int32_t)round_up(omax, 128);
     // K-N1g is issue-bound (tools/general_perf.py sweep, profiles/r01/general.md):
     // 2 CTAs x 8 consumer warps per SM with a 2-deep ring beat deeper rings
@@ -463,13 +509,16 @@ int launch_general(ds_handle* h, const uint8_t* in, int64_t n, uint8_t* out, cud
     p.in = in; p.out = out;
     p.unit_count = h->debug_unit_count;
     p.in_frame = pi.in_frame_bytes; p.out_frame = pi.out_frame_bytes;
-    p.upf = c.upf;
-    p.n_units = n * c.upf;
+    int32_t L[DS_MAX_PLANES] = {1, 1, 1};
+    p.upf = general_runs(h, n, L);
+    p.n_units = n * p.upf;
     p.n_planes = pi.n_planes;
     p.stages = c.stages;
     p.stage_stride = c.stage_stride;
     p.mid_stride = c.mid_stride;
     p.out_stride = c.out_stride;
+    p.ovl = c.ovl;
+    p.mid_alt = c.mid_alt;
     p.h = gen_stage(sp.h);
     p.v = gen_stage(sp.v);
     const bool out_al = aligned16(out) && pi.out_frame_bytes % 16 == 0;
@@ -491,12 +540,14 @@ int launch_general(ds_handle* h, const uint8_t* in, int64_t n, uint8_t* out, cud
         P.oh = (int32_t)(((int64_t)sp.h.origin % P.W + P.W) % P.W);
         P.ov = (int32_t)(((int64_t)sp.v.origin % P.H + P.H) % P.H);
         P.unit_start = start;
+        P.nb = c.nb[q];
+        P.L = L[q];
         P.unit_out = sp.v.outputs * P.k * P.Wm;
         P.bulk_store = (out_al && P.out_off % 16 == 0 && P.unit_out % 16 == 0) ? 1 : 0;
         P.coop = (in_al && P.W % 16 == 0 && P.W >= 32 && P.in_off % 16 == 0 && pi.in_frame_bytes % 16 == 0)
                      ? 0 : 1;
         P.pitch = (int32_t)general_pitch(P.W);
-        start += (P.H / sp.v.paving) / P.k;
+        start += (P.nb + P.L - 1) / P.L;
     }
     const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(p.n_units, (int64_t)c.grid_per_sm * h->sm_count));
     if (c.fast)
@@ -845,6 +896,12 @@ DS_API int ds_set_band_bytes(ds_handle* h, int64_t target) {
     return crc ? crc : configure_general(h);
 }
 
+DS_API int ds_set_run_bands(ds_handle* h, int32_t bands) {
+    if (!h || bands < 0) return DS_EINVAL;
+    h->run_bands = bands;
+    return DS_OK;
+}
+
 DS_API int ds_set_debug_counter(ds_handle* h, uint32_t* counts) {
     if (!h) return DS_EINVAL;
     h->debug_unit_count = counts;
@@ -854,7 +911,11 @@ DS_API int ds_set_debug_counter(ds_handle* h, uint32_t* counts) {
 DS_API int64_t ds_units(const ds_handle* h, int64_t n, int32_t kernel) {
     if (!h || n < 0) return -1;
     if (kernel == DS_KERNEL_FUSED) return h->plan.fused_eligible ? n * pick_cfg(h, n).plan.units_per_frame : -1;
-    if (kernel == DS_KERNEL_FUSED_GENERAL) return h->general.valid ? n * h->general.upf : -1;
+    if (kernel == DS_KERNEL_FUSED_GENERAL) {
+        if (!h->general.valid) return -1;
+        int32_t L[DS_MAX_PLANES];
+        return n * general_runs(h, n, L);
+    }
     return -1;
 }
 

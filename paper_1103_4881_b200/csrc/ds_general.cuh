@@ -37,8 +37,10 @@ struct GenPlane {
     uint32_t quads_rcp;        // ceil(2^32 / (Wm / 4)) (Wm / 4 > 1)
     int32_t oh;                // H origin reduced mod W (>= 0)
     int32_t ov;                // V origin reduced mod H (>= 0)
-    int32_t unit_start;
-    int32_t unit_out;          // Qv * k * Wm
+    int32_t unit_start;        // first unit (run) of this plane within a frame
+    int32_t nb;                // bands in the plane: (H / Sv) / k
+    int32_t L;                 // bands per run (unit); consecutive bands reuse the halo's mid rows
+    int32_t unit_out;          // Qv * k * Wm (output bytes of one band)
     int32_t bulk_store;
     int32_t coop;              // 1: rows staged by the producer warp with plain loads
 };
@@ -62,6 +64,8 @@ struct GeneralParams {
     uint32_t* unit_count;      // debug: +1 per unit processed, else null
     int64_t in_frame, out_frame, n_units;
     int32_t upf, n_planes, stages, stage_stride, mid_stride, out_stride;
+    int32_t ovl;               // Pv - Sv > 0: mid rows a band shares with the next
+    int32_t mid_alt;           // byte offset of the second mid buffer (0: one buffer)
     GenPlane pl[DS_MAX_PLANES];
     GenStage h, v;
 };
@@ -151,8 +155,8 @@ __device__ __forceinline__ void g_h_dot(const GenStage& g, const uint32_t (&x)[4
 // either's arithmetic: two independent chains to hide LDS / dp4a latency.
 template <int Q, bool FAST, int NC>
 __device__ __forceinline__ void g_h_pass(const GenStage& g, const GenPlane& P, uint32_t st, uint32_t mid,
-                                         int tid) {
-    const int items = P.R * P.np;
+                                         int rows, int tid) {
+    const int items = rows * P.np;
     int it = tid;
     for (; it + NC < items; it += 2 * NC) {
         uint32_t xa[4], xb[4], ma, mb, oa[Q], ob[Q];
@@ -177,8 +181,9 @@ __device__ __forceinline__ void g_h_pass(const GenStage& g, const GenPlane& P, u
 // Taps outside s8: byte loop (same item space, same window bounds)
 template <bool FAST, int NC>
 __device__ __forceinline__ void g_h_pass_bytes(const GenStage& g, const int32_t (*w)[DS_MAX_PATTERN],
-                                               const GenPlane& P, uint32_t st, uint32_t mid, int tid) {
-    const int np = P.np, W = P.W, items = P.R * np;
+                                               const GenPlane& P, uint32_t st, uint32_t mid, int rows,
+                                               int tid) {
+    const int np = P.np, W = P.W, items = rows * np;
     for (int it = tid; it < items; it += NC) {
         const int r = g_div_small(it, np, P.np_rcp);
         const int r1 = it - r * np;
@@ -318,7 +323,7 @@ __global__ void __launch_bounds__(9 * 32, DS_GEN_MINB) ds_fused_general_kernel(c
     const int S = p.stages;
     uint8_t* ring = smem;
     uint8_t* mid = smem + (size_t)S * p.stage_stride;
-    uint8_t* outs = mid + p.mid_stride;
+    uint8_t* outs = mid + p.mid_stride + p.mid_alt;
     uint64_t* full = reinterpret_cast<uint64_t*>(outs + (size_t)2 * p.out_stride);
     uint64_t* empty = full + S;
     __shared__ int32_t wh[DS_MAX_OUTPUTS][DS_MAX_PATTERN], wv[DS_MAX_OUTPUTS][DS_MAX_PATTERN];
@@ -352,91 +357,116 @@ __global__ void __launch_bounds__(9 * 32, DS_GEN_MINB) ds_fused_general_kernel(c
         const uint64_t pol = policy_evict_first();
         bool first_round = true;
         for (; cur.u < p.n_units; cur.next()) {
-            if (!first_round) mbar_wait_sleep(&empty[s], phase ^ 1);
             const GenPlane& P = p.pl[cur.plane(p)];
-            const int band = cur.local - P.unit_start;
+            const int b0 = (cur.local - P.unit_start) * P.L, b1 = min(b0 + P.L, P.nb);
             const uint8_t* plane = p.in + cur.f * p.in_frame + P.in_off;
-            uint8_t* dst = ring + (size_t)s * p.stage_stride;
-            const int row0 = (int)(((int64_t)P.ov + (int64_t)p.v.S * P.k * band) % P.H);
-            if (!P.coop) {
-                if (lane == 0) mbar_arrive_expect_tx(&full[s], (uint32_t)P.R * (uint32_t)(P.W + 32));
-                __syncwarp();
-                for (int i = lane; i < P.R; i += 32) {
-                    const uint8_t* src = plane + (int64_t)((row0 + i) % P.H) * P.W;
-                    uint8_t* d = dst + (size_t)i * P.pitch;
-                    bulk_g2s(d, src, (uint32_t)P.W, &full[s], pol);
-                    bulk_g2s(d + P.W, src, 32u, &full[s], pol);
+            for (int band = b0; band < b1; ++band) {
+                if (!first_round) mbar_wait_sleep(&empty[s], phase ^ 1);
+                uint8_t* dst = ring + (size_t)s * p.stage_stride;
+                // first band of a run: all R rows; later bands: the Sv k rows
+                // past the ovl rows whose mid the previous band produced
+                const int reuse = band > b0 ? p.ovl : 0;
+                const int rows = P.R - reuse;
+                const int row0 = (int)(((int64_t)P.ov + (int64_t)p.v.S * P.k * band + reuse) % P.H);
+                if (!P.coop) {
+                    if (lane == 0) mbar_arrive_expect_tx(&full[s], (uint32_t)rows * (uint32_t)(P.W + 32));
+                    __syncwarp();
+                    for (int i = lane; i < rows; i += 32) {
+                        const uint8_t* src = plane + (int64_t)((row0 + i) % P.H) * P.W;
+                        uint8_t* d = dst + (size_t)i * P.pitch;
+                        bulk_g2s(d, src, (uint32_t)P.W, &full[s], pol);
+                        bulk_g2s(d + P.W, src, 32u, &full[s], pol);
+                    }
+                } else {
+                    for (int i = 0; i < rows; ++i)
+                        g_coop_row(dst + (size_t)i * P.pitch, plane + (int64_t)((row0 + i) % P.H) * P.W, P.W,
+                                   lane);
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&full[s]);      // release: generic smem writes
                 }
-            } else {
-                for (int i = 0; i < P.R; ++i)
-                    g_coop_row(dst + (size_t)i * P.pitch, plane + (int64_t)((row0 + i) % P.H) * P.W, P.W, lane);
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&full[s]);      // release: generic smem writes
+                if (++s == S) { s = 0; phase ^= 1; first_round = false; }
             }
-            if (++s == S) { s = 0; phase ^= 1; first_round = false; }
         }
         return;
     }
 
     int oslot = 0;
+    uint32_t mpar = 0;                              // which mid buffer the next band writes
     for (; cur.u < p.n_units; cur.next()) {
         const GenPlane& P = p.pl[cur.plane(p)];
-        const int band = cur.local - P.unit_start;
-        const uint32_t st = smem_u32(ring) + s * p.stage_stride;
-        uint8_t* ob = outs + (size_t)oslot * p.out_stride;
-        const uint32_t ob_s = smem_u32(ob), mid_s = smem_u32(mid);
-        mbar_wait(&full[s], phase);
-
-        // ---- H task on every staged row -> mid (u8)
-        if (p.h.s8) {
-            switch (p.h.Q) {
-                case 1: g_h_pass<1, FAST, NC>(p.h, P, st, mid_s, tid); break;
-                case 2: g_h_pass<2, FAST, NC>(p.h, P, st, mid_s, tid); break;
-                case 3: g_h_pass<3, FAST, NC>(p.h, P, st, mid_s, tid); break;
-                case 4: g_h_pass<4, FAST, NC>(p.h, P, st, mid_s, tid); break;
-                case 5: g_h_pass<5, FAST, NC>(p.h, P, st, mid_s, tid); break;
-                case 6: g_h_pass<6, FAST, NC>(p.h, P, st, mid_s, tid); break;
-                case 7: g_h_pass<7, FAST, NC>(p.h, P, st, mid_s, tid); break;
-                default: g_h_pass<8, FAST, NC>(p.h, P, st, mid_s, tid); break;
-            }
-        } else {
-            g_h_pass_bytes<FAST, NC>(p.h, wh, P, st, mid_s, tid);
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[s]);     // ring slot no longer read
-        named_bar_sync(1, NC);                      // mid complete
-
-        // ---- V task from mid -> output band
-        if (p.v.s8 && (P.Wm & 3) == 0) {
-            switch (p.v.Q) {
-                case 1: g_v_pass<1, 0, FAST, NC>(p.v, P, mid_s, ob_s, tid); break;
-                case 2: g_v_pass<2, 0, FAST, NC>(p.v, P, mid_s, ob_s, tid); break;
-                case 3: g_v_pass<3, 0, FAST, NC>(p.v, P, mid_s, ob_s, tid); break;
-                case 4: g_v_pass<4, 0, FAST, NC>(p.v, P, mid_s, ob_s, tid); break;
-                case 5: g_v_pass<4, 1, FAST, NC>(p.v, P, mid_s, ob_s, tid); break;
-                case 6: g_v_pass<4, 2, FAST, NC>(p.v, P, mid_s, ob_s, tid); break;
-                case 7: g_v_pass<4, 3, FAST, NC>(p.v, P, mid_s, ob_s, tid); break;
-                default: g_v_pass<4, 4, FAST, NC>(p.v, P, mid_s, ob_s, tid); break;
-            }
-        } else {
-            g_v_pass_bytes<FAST, NC>(p.v, wv, P, mid_s, ob_s, tid);
-        }
-        uint8_t* dst = p.out + cur.f * p.out_frame + P.out_off + (int64_t)band * P.unit_out;
+        const int b0 = (cur.local - P.unit_start) * P.L, b1 = min(b0 + P.L, P.nb);
         if (p.unit_count != nullptr && tid == 0) atomicAdd(p.unit_count + cur.u, 1u);
-        if (P.bulk_store) {
-            fence_proxy_async_smem();
-            named_bar_sync(1, NC);                  // output band complete; mid free
-            if (tid == 0) {
-                bulk_s2g(dst, ob, (uint32_t)P.unit_out);
-                bulk_commit();
-                bulk_wait_read<1>();                // the other out slot is free
+        for (int band = b0; band < b1; ++band) {
+            const uint32_t st = smem_u32(ring) + s * p.stage_stride;
+            uint8_t* ob = outs + (size_t)oslot * p.out_stride;
+            const uint32_t ob_s = smem_u32(ob);
+            const uint32_t mid_s = smem_u32(mid) + mpar * p.mid_alt;
+            const int reuse = band > b0 ? p.ovl : 0;
+            if (reuse) {
+                // the previous band's mid rows [Sv k, R) are this band's rows
+                // [0, ovl) (its buffer is not written again before two more barriers)
+                const uint32_t src = smem_u32(mid) + (mpar ^ 1) * p.mid_alt + p.v.S * P.k * P.Wm;
+                const int nbytes = reuse * P.Wm;
+                if ((P.Wm & 3) == 0)
+                    for (int x = 4 * tid; x < nbytes; x += 4 * NC) sts32s(mid_s + x, lds32s(src + x));
+                else
+                    for (int x = tid; x < nbytes; x += NC) sts8s(mid_s + x, lds8s(src + x));
             }
-        } else {
-            named_bar_sync(1, NC);
-            for (int x = tid; x < P.unit_out; x += NC) dst[x] = ob[x];
+            const int rows = P.R - reuse;
+            const uint32_t mid_h = mid_s + reuse * P.Wm;
+            mbar_wait(&full[s], phase);
+
+            // ---- H task on every newly staged row -> mid (u8)
+            if (p.h.s8) {
+                switch (p.h.Q) {
+                    case 1: g_h_pass<1, FAST, NC>(p.h, P, st, mid_h, rows, tid); break;
+                    case 2: g_h_pass<2, FAST, NC>(p.h, P, st, mid_h, rows, tid); break;
+                    case 3: g_h_pass<3, FAST, NC>(p.h, P, st, mid_h, rows, tid); break;
+                    case 4: g_h_pass<4, FAST, NC>(p.h, P, st, mid_h, rows, tid); break;
+                    case 5: g_h_pass<5, FAST, NC>(p.h, P, st, mid_h, rows, tid); break;
+                    case 6: g_h_pass<6, FAST, NC>(p.h, P, st, mid_h, rows, tid); break;
+                    case 7: g_h_pass<7, FAST, NC>(p.h, P, st, mid_h, rows, tid); break;
+                    default: g_h_pass<8, FAST, NC>(p.h, P, st, mid_h, rows, tid); break;
+                }
+            } else {
+                g_h_pass_bytes<FAST, NC>(p.h, wh, P, st, mid_h, rows, tid);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);     // ring slot no longer read
+            named_bar_sync(1, NC);                      // mid complete
+
+            // ---- V task from mid -> output band
+            if (p.v.s8 && (P.Wm & 3) == 0) {
+                switch (p.v.Q) {
+                    case 1: g_v_pass<1, 0, FAST, NC>(p.v, P, mid_s, ob_s, tid); break;
+                    case 2: g_v_pass<2, 0, FAST, NC>(p.v, P, mid_s, ob_s, tid); break;
+                    case 3: g_v_pass<3, 0, FAST, NC>(p.v, P, mid_s, ob_s, tid); break;
+                    case 4: g_v_pass<4, 0, FAST, NC>(p.v, P, mid_s, ob_s, tid); break;
+                    case 5: g_v_pass<4, 1, FAST, NC>(p.v, P, mid_s, ob_s, tid); break;
+                    case 6: g_v_pass<4, 2, FAST, NC>(p.v, P, mid_s, ob_s, tid); break;
+                    case 7: g_v_pass<4, 3, FAST, NC>(p.v, P, mid_s, ob_s, tid); break;
+                    default: g_v_pass<4, 4, FAST, NC>(p.v, P, mid_s, ob_s, tid); break;
+                }
+            } else {
+                g_v_pass_bytes<FAST, NC>(p.v, wv, P, mid_s, ob_s, tid);
+            }
+            uint8_t* dst = p.out + cur.f * p.out_frame + P.out_off + (int64_t)band * P.unit_out;
+            if (P.bulk_store) {
+                fence_proxy_async_smem();
+                named_bar_sync(1, NC);                  // output band complete; mid free
+                if (tid == 0) {
+                    bulk_s2g(dst, ob, (uint32_t)P.unit_out);
+                    bulk_commit();
+                    bulk_wait_read<1>();                // the other out slot is free
+                }
+            } else {
+                named_bar_sync(1, NC);
+                for (int x = tid; x < P.unit_out; x += NC) dst[x] = ob[x];
+            }
+            if (++s == S) { s = 0; phase ^= 1; }
+            oslot ^= 1;
+            mpar ^= (p.mid_alt != 0);
         }
-        if (++s == S) { s = 0; phase ^= 1; }
-        oslot ^= 1;
     }
     if (tid == 0) bulk_wait_all();
 }

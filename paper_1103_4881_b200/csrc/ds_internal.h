@@ -55,13 +55,20 @@ constexpr int64_t kFineUnitTarget = 16 * 1024;      // small batches: more, smal
 #ifndef DS_GEN_STAGE_TARGET
 #define DS_GEN_STAGE_TARGET (40 * 1024)
 #endif
-constexpr int64_t kGeneralStageTarget = DS_GEN_STAGE_TARGET;  // K-N1g staged rows per unit
+constexpr int64_t kGeneralStageTarget = DS_GEN_STAGE_TARGET;  // K-N1g staged rows per band
+#ifndef DS_GEN_STAGE_TARGET_REUSE
+#define DS_GEN_STAGE_TARGET_REUSE (28 * 1024)
+#endif
+constexpr int64_t kGeneralStageTargetReuse = DS_GEN_STAGE_TARGET_REUSE;  // ... when bands reuse a V halo
 
 // K-N1g launch configuration (any stage spec).
 struct GeneralCfg {
     bool valid = false;
-    int32_t k[DS_MAX_PLANES] = {0, 0, 0};     // V repetitions per unit
-    int32_t R[DS_MAX_PLANES] = {0, 0, 0};     // staged rows per unit
+    int32_t k[DS_MAX_PLANES] = {0, 0, 0};     // V repetitions per band
+    int32_t nb[DS_MAX_PLANES] = {0, 0, 0};    // bands per plane
+    int32_t R[DS_MAX_PLANES] = {0, 0, 0};     // staged rows per band (first band of a run)
+    int32_t ovl = 0;                          // Pv - Sv > 0: halo rows shared by consecutive bands
+    int32_t mid_alt = 0;                      // second mid buffer offset (0: one buffer)
     int32_t upf = 0;
     int32_t stage_stride = 0, mid_stride = 0, out_stride = 0;
     int stages = 2, ncw = 8;
@@ -87,6 +94,7 @@ struct ds_handle {
     dsi::FusedCfg fused, fine;
     dsi::GeneralCfg general;
     int kernel_pref = DS_KERNEL_AUTO;
+    int32_t run_bands = 0;                  // ds_set_run_bands (0 = automatic)
     uint32_t* debug_unit_count = nullptr;   // ds_set_debug_counter
     std::atomic<int> last_kernel{DS_KERNEL_AUTO};
     // ds_run_host / ds_run_schedule state (lazily allocated, guarded by host_mu)

@@ -189,16 +189,20 @@ def _oracle_stage(d):
 @pytest.mark.parametrize("kernel", [ds.DS_KERNEL_FUSED_GENERAL, GENERIC])
 def test_halo_and_origin_spec(W, H, ch, kernel):
     """P > S halos with toroidal wrap and origin != 0:
-    K-N1g (halo rows staged in smem, smem intermediate) and K-N2."""
+    K-N1g (halo rows staged in smem, smem intermediate; runs of bands that
+    reuse the halo's intermediate rows, forced from 1 band to whole planes)
+    and K-N2."""
     hd, vd = _halo_spec()
     spec = ds.make_spec(h=hd, v=vd, chroma=ds.DS_CHROMA_420)
     d = ds.Downscaler(W, H, ch, spec=spec)
     assert d.plan.fused_general_eligible == 1 and d.plan.fused_eligible == 0
     fr = synth.random_frames(9, 0, 3, W, H, ch, 1)
-    got = _run(d, fr, kernel)
-    assert d.last_kernel() == kernel
     want = oracle.execute_frames(fr, W, H, ch, 1, _oracle_stage(hd), _oracle_stage(vd))
-    _assert_same(got, want, "halo")
+    for bands in ((0, 1, 2, 3, 1 << 20) if kernel == ds.DS_KERNEL_FUSED_GENERAL else (0,)):
+        d.set_run_bands(bands)
+        got = _run(d, fr, kernel)
+        assert d.last_kernel() == kernel
+        _assert_same(got, want, f"halo, run bands {bands}")
 
 
 def test_negative_weights_and_other_ratio():
@@ -258,6 +262,7 @@ def test_general_kernel_fuzz_random_specs():
             continue
         fr = synth.random_frames(trial, 0, 2, W, H, ch, chroma)
         want = oracle.execute_frames(fr, W, H, ch, chroma, _oracle_stage(hd), _oracle_stage(vd))
+        d.set_run_bands(int(rng.choice([0, 1, 2, 3, 7, 1 << 20])))   # halo reuse across bands
         got = _run(d, fr, ds.DS_KERNEL_FUSED_GENERAL)
         assert d.last_kernel() == ds.DS_KERNEL_FUSED_GENERAL
         _assert_same(got, want, f"fuzz {trial}: {W}x{H}x{ch} h={hd} v={vd}")
@@ -531,13 +536,16 @@ def test_fused_kernel_fuzz():
     assert checked >= 30
 
 
-@pytest.mark.parametrize("kernel", [FUSED, ds.DS_KERNEL_FUSED_GENERAL])
-def test_every_unit_processed_exactly_once(kernel):
+@pytest.mark.parametrize("kernel,halo", [(FUSED, False), (ds.DS_KERNEL_FUSED_GENERAL, False),
+                                         (ds.DS_KERNEL_FUSED_GENERAL, True)])
+def test_every_unit_processed_exactly_once(kernel, halo):
     """Debug unit accounting (ds_set_debug_counter): over many frame counts,
-    band sizes and ring/CTA tunings, the persistent schedule processes every
+    band sizes and ring/CTA tunings (K-N1), and automatic or forced run
+    lengths (K-N1g with a V halo), the persistent schedule processes every
     work unit exactly once."""
     W, H = 1920, 1080
-    d = ds.Downscaler(W, H, 3)
+    spec = ds.make_spec(*_halo_spec(), chroma=ds.DS_CHROMA_420) if halo else None
+    d = ds.Downscaler(W, H, 3, spec=spec)
     d.set_kernel(kernel)
     L = ds.lib()
     x = ds.generate_frames(40, d.in_frame_bytes, seed=2)
@@ -548,6 +556,8 @@ def test_every_unit_processed_exactly_once(kernel):
             d.set_band_bytes(int(rng.choice([0, 8000, 16000, 64000])))
         if kernel == FUSED and trial % 3 == 2:
             d.set_tuning(int(rng.integers(2, 7)), int(rng.integers(0, 3)))
+        if halo:
+            d.set_run_bands(int(rng.choice([0, 0, 1, 5, 1 << 20])))
         units = L.ds_units(d.handle, n, kernel)
         assert units > 0
         counts = torch.zeros(units, dtype=torch.int32, device="cuda")
@@ -558,5 +568,7 @@ def test_every_unit_processed_exactly_once(kernel):
         assert d.last_kernel() == kernel
         c = counts.cpu().numpy()
         assert (c == 1).all(), (trial, n, int((c == 0).sum()), int((c > 1).sum()))
-    _assert_same(y.cpu().numpy(), oracle.execute_frames(synth.random_frames(2, 0, n, W, H), W, H),
-                 "after accounting")
+    fr = synth.random_frames(2, 0, n, W, H)
+    want = (oracle.execute_frames(fr, W, H, 3, 1, *[_oracle_stage(x) for x in _halo_spec()]) if halo
+            else oracle.execute_frames(fr, W, H))
+    _assert_same(y.cpu().numpy(), want, "after accounting")

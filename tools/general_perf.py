@@ -40,8 +40,9 @@ def timed(fn, steps):
     return a.elapsed_time(b) / steps
 
 
-def run(W, H, n, spec, kernels, steps=20):
+def run(W, H, n, spec, kernels, steps=20, run_bands=0):
     d = ds.Downscaler(W, H, 3, spec=spec)
+    d.set_run_bands(run_bands)
     x = ds.generate_frames(n, d.in_frame_bytes, seed=1)
     outs, res = {}, {}
     for k in kernels:
@@ -90,11 +91,12 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default="gpurun_out/general_perf.json")
     ap.add_argument("--quick", action="store_true", help="K-N1g only, one line per spec")
+    ap.add_argument("--run-bands", type=int, default=0, help="K-N1g bands per run (0 = automatic)")
     a = ap.parse_args()
     torch.cuda.set_device(0)
     halo = ds.make_spec(h=HALO_H, v=HALO_V)
     if a.quick:
-        h = run(1920, 1080, 300, halo, [ds.DS_KERNEL_FUSED_GENERAL], steps=50)
+        h = run(1920, 1080, 300, halo, [ds.DS_KERNEL_FUSED_GENERAL], steps=50, run_bands=a.run_bands)
         t = run(1920, 1080, 300, None, [ds.DS_KERNEL_FUSED_GENERAL], steps=50)
         k = ds.KERNEL_NAMES[ds.DS_KERNEL_FUSED_GENERAL]
         print(json.dumps({"halo_ms": round(h[k]["ms"], 4), "spec_taps_ms": round(t[k]["ms"], 4)}))
