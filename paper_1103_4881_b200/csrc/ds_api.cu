@@ -407,6 +407,11 @@ int32_t general_runs(const ds_handle* h, int64_t n, int32_t* L) {
     return upf_of(L);
 }
 
+GeneralFn general_fn(int fast) {
+    return fast == 2 ? ds::ds_fused_general_kernel<2>
+                     : fast == 1 ? ds::ds_fused_general_kernel<1> : ds::ds_fused_general_kernel<0>;
+}
+
 // Stage constants for K-N1g.  FASTDIV (M != 0): floor(a / D) = umulhi(a, M)
 // with M = ceil(2^32 / D) is exact for 0 <= a <= amax when amax * e < 2^32,
 // e = M D - 2^32 (the error a e / (D 2^32) stays below 1 / D).  amax is the
@@ -421,16 +426,19 @@ ds::GenStage gen_stage(const ds_stage_spec& s) {
     g.D_rcp = s.divisor == 1 ? 0xffffffffu : (uint32_t)((1ULL << 32) / (uint64_t)s.divisor);
     std::memcpy(g.w, s.weight, sizeof g.w);
     g.s8 = 1;
-    int64_t amax = 0;
+    int64_t amax = 0, amin = INT64_MAX;
     for (int k = 0; k < DS_MAX_OUTPUTS; ++k) {
-        int64_t pos = 0;
+        int64_t pos = 0, neg = 0;
         for (int i = 0; i < DS_MAX_PATTERN; ++i) {
             const int32_t w = s.weight[k][i];
             if (w < -128 || w > 127) g.s8 = 0;
             g.wp[k][i / 4] |= (uint32_t)(uint8_t)(int8_t)(w < -128 ? 0 : w > 127 ? 0 : w) << (8 * (i % 4));
-            if (k < s.outputs && i < s.pattern && w > 0) pos += w;
+            if (k < s.outputs && i < s.pattern) (w > 0 ? pos : neg) += w;
         }
-        if (k < s.outputs) amax = std::max<int64_t>(amax, (int64_t)s.bias + 255 * pos);
+        if (k < s.outputs) {
+            amax = std::max<int64_t>(amax, (int64_t)s.bias + 255 * pos);
+            amin = std::min<int64_t>(amin, (int64_t)s.bias + 255 * neg);
+        }
     }
     if (s.divisor == 1) {
         if (amax < (int64_t)0x7fffffff) { g.M = 0xffffffffu; g.lo = 1; g.fbias = s.bias + 1; }
@@ -442,6 +450,8 @@ ds::GenStage gen_stage(const ds_stage_spec& s) {
             g.M = (uint32_t)M; g.lo = 0; g.fbias = s.bias;
         }
     }
+    // both clamps dead: every accumulator is >= 0 and its quotient <= 255
+    g.exact = (g.M != 0 && amin >= 0 && amax < 256 * (int64_t)s.divisor) ? 1 : 0;
     return g;
 }
 
@@ -478,8 +488,9 @@ int configure_general(ds_handle* h) {
     const int want_ctas = DS_GEN_CTAS;
     c.threads = (c.ncw + 1) * 32;
     c.smem = (int)general_smem(c, c.stages);
-    c.fast = gen_stage(sp.h).M != 0 && gen_stage(sp.v).M != 0;
-    GeneralFn fn = c.fast ? ds::ds_fused_general_kernel<true> : ds::ds_fused_general_kernel<false>;
+    const ds::GenStage gh = gen_stage(sp.h), gv = gen_stage(sp.v);
+    c.fast = (gh.M == 0 || gv.M == 0) ? 0 : (gh.exact && gv.exact) ? 2 : 1;
+    GeneralFn fn = general_fn(c.fast);
     DeviceGuard g(h->device);
     if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              kSmemLimit - 2 * DS_MAX_OUTPUTS * DS_MAX_PATTERN * 4) != cudaSuccess) {
@@ -550,10 +561,7 @@ int launch_general(ds_handle* h, const uint8_t* in, int64_t n, uint8_t* out, cud
         start += (P.nb + P.L - 1) / P.L;
     }
     const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(p.n_units, (int64_t)c.grid_per_sm * h->sm_count));
-    if (c.fast)
-        ds::ds_fused_general_kernel<true><<<(unsigned)grid, c.threads, c.smem, st>>>(p);
-    else
-        ds::ds_fused_general_kernel<false><<<(unsigned)grid, c.threads, c.smem, st>>>(p);
+    general_fn(c.fast)<<<(unsigned)grid, c.threads, c.smem, st>>>(p);
     return cudaGetLastError() == cudaSuccess ? DS_OK : DS_ECUDA;
 }
 

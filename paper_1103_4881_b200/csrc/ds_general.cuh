@@ -54,6 +54,7 @@ struct GenStage {
     // D = 1: M = 2^32 - 1, accumulator biased by +1 and lo = 1
     int32_t fbias;             // accumulator start on the FASTDIV path (bias, or bias + 1 for D = 1)
     uint32_t M, lo;
+    int32_t exact;             // FASTDIV and 0 <= acc < 256 D for every window: no clamps needed
     int32_t w[DS_MAX_OUTPUTS][DS_MAX_PATTERN];
     uint32_t wp[DS_MAX_OUTPUTS][DS_MAX_PATTERN / 4];   // s8-packed weights, 4 taps per word
 };
@@ -81,12 +82,16 @@ __device__ __forceinline__ uint32_t g_stage_out(int32_t acc, uint32_t D, uint32_
     q += (a - q * D >= D) ? 1u : 0u;
     return min(q, 255u);
 }
-template <bool FAST>
+// Division modes (host-chosen, both stages): 0 reciprocal + correction,
+// 1 FASTDIV with clamps, 2 FASTDIV where the host proved lo <= acc and
+// acc / D <= 255 for every window, so both clamps are dead: one IMAD.HI.
+template <int FAST>
 __device__ __forceinline__ uint32_t g_out(const GenStage& g, int32_t acc) {
-    if (FAST) return min(__umulhi((uint32_t)max(acc, (int32_t)g.lo), g.M), 255u);
+    if (FAST == 2) return __umulhi((uint32_t)acc, g.M);
+    if (FAST == 1) return min(__umulhi((uint32_t)max(acc, (int32_t)g.lo), g.M), 255u);
     return g_stage_out(acc, g.D, g.D_rcp);
 }
-template <bool FAST>
+template <int FAST>
 __device__ __forceinline__ int32_t g_bias(const GenStage& g) {
     return FAST ? g.fbias : g.bias;
 }
@@ -123,7 +128,7 @@ __device__ __forceinline__ int32_t g_div_small(int32_t t, int32_t d, uint32_t rc
 // c0 = (o_h + S_h r1) mod W < W and runs at most 19 bytes on, inside the row
 // and its wrap pad: 5 aligned words byte-shifted into a 16-byte window (taps
 // past P are zero in the packed weights), one dp4a per 4 taps.
-template <int Q, bool FAST>
+template <int Q, int FAST>
 __device__ __forceinline__ void g_h_load(const GenStage& g, const GenPlane& P, uint32_t st, uint32_t mid, int it,
                                          uint32_t (&x)[4], uint32_t& mo) {
     const int r = g_div_small(it, P.np, P.np_rcp);
@@ -140,7 +145,7 @@ __device__ __forceinline__ void g_h_load(const GenStage& g, const GenPlane& P, u
     x[3] = __byte_perm(w3, w4, sel);
     mo = mid + r * P.Wm + Q * r1;
 }
-template <int Q, bool FAST>
+template <int Q, int FAST>
 __device__ __forceinline__ void g_h_dot(const GenStage& g, const uint32_t (&x)[4], uint32_t (&o)[Q]) {
 #pragma unroll
     for (int j = 0; j < Q; ++j) {
@@ -153,7 +158,7 @@ __device__ __forceinline__ void g_h_dot(const GenStage& g, const uint32_t (&x)[4
 }
 // Two items per thread per step (it, it + NC), loads of both issued before
 // either's arithmetic: two independent chains to hide LDS / dp4a latency.
-template <int Q, bool FAST, int NC>
+template <int Q, int FAST, int NC>
 __device__ __forceinline__ void g_h_pass(const GenStage& g, const GenPlane& P, uint32_t st, uint32_t mid,
                                          int rows, int tid) {
     const int items = rows * P.np;
@@ -179,7 +184,7 @@ __device__ __forceinline__ void g_h_pass(const GenStage& g, const GenPlane& P, u
     }
 }
 // Taps outside s8: byte loop (same item space, same window bounds)
-template <bool FAST, int NC>
+template <int FAST, int NC>
 __device__ __forceinline__ void g_h_pass_bytes(const GenStage& g, const int32_t (*w)[DS_MAX_PATTERN],
                                                const GenPlane& P, uint32_t st, uint32_t mid, int rows,
                                                int tid) {
@@ -201,7 +206,7 @@ __device__ __forceinline__ void g_h_pass_bytes(const GenStage& g, const int32_t 
 
 // V outputs k0 .. k0+Q-1 of one 4-column group: 4x4 byte transposes turn 4
 // mid rows x 4 columns into 4 column words, one dp4a per 4 taps.
-template <int Q, bool FAST>
+template <int Q, int FAST>
 __device__ __forceinline__ void g_v_quad(const GenStage& g, int k0, uint32_t mb, int Wm, uint32_t ob0) {
     int32_t acc[Q][4];
 #pragma unroll
@@ -234,7 +239,7 @@ __device__ __forceinline__ void g_v_quad(const GenStage& g, int k0, uint32_t mb,
 }
 // ---- V pass (Wm % 4 == 0, s8 taps): item = (V repetition gi, 4 mid columns);
 // outputs in groups of at most 4 (QA, then QB) to bound live accumulators.
-template <int QA, int QB, bool FAST, int NC>
+template <int QA, int QB, int FAST, int NC>
 __device__ __forceinline__ void g_v_pass(const GenStage& g, const GenPlane& P, uint32_t mid, uint32_t ob,
                                          int tid) {
     const int Wm = P.Wm, quads = Wm >> 2, items = P.k * quads;
@@ -248,7 +253,7 @@ __device__ __forceinline__ void g_v_pass(const GenStage& g, const GenPlane& P, u
     }
 }
 // V pass, general: item = output byte of the band
-template <bool FAST, int NC>
+template <int FAST, int NC>
 __device__ __forceinline__ void g_v_pass_bytes(const GenStage& g, const int32_t (*w)[DS_MAX_PATTERN],
                                                const GenPlane& P, uint32_t mid, uint32_t ob, int tid) {
     const int Wm = P.Wm;
@@ -315,7 +320,7 @@ struct GenCursor {
 #ifndef DS_GEN_MINB
 #define DS_GEN_MINB 2
 #endif
-template <bool FAST>
+template <int FAST>
 __global__ void __launch_bounds__(9 * 32, DS_GEN_MINB) ds_fused_general_kernel(const __grid_constant__ GeneralParams p) {
     constexpr int NCW = 8;
     extern __shared__ __align__(1024) uint8_t smem[];

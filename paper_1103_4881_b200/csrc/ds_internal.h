@@ -72,7 +72,7 @@ struct GeneralCfg {
     int32_t upf = 0;
     int32_t stage_stride = 0, mid_stride = 0, out_stride = 0;
     int stages = 2, ncw = 8;
-    bool fast = false;                        // FASTDIV instantiation (both stages qualify)
+    int fast = 0;                             // division mode (ds_general.cuh g_out): 0, 1 or 2
     int grid_per_sm = 0, threads = 0, smem = 0;
 };
 

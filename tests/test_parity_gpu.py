@@ -235,7 +235,9 @@ def _random_spec(rng):
         P = int(rng.integers(1, max_p + 1))
         S = int(rng.integers(1, P + 3))
         Q = int(rng.integers(1, 5))
-        D = int(rng.choice([1, 2, 3, 5, 6, 7, 8, 16, 100, 1 << 20]))
+        # 999983: M D - 2^32 = 959672, so large taps leave the FASTDIV bound
+        # (K-N1g's reciprocal + correction instantiation)
+        D = int(rng.choice([1, 2, 3, 5, 6, 7, 8, 16, 100, 1 << 20, 999983]))
         w = [[int(x) if rng.random() < 0.7 else 0 for x in rng.integers(-40, 120, P)] for _ in range(Q)]
         total = max(1, sum(max(0, x) for row in w for x in row))
         return dict(pattern=P, paving=S, origin=int(rng.integers(-50, 50)), weights=w,
