@@ -553,6 +553,7 @@ int launch_general(ds_handle* h, const uint8_t* in, int64_t n, uint8_t* out, cud
         P.unit_start = start;
         P.nb = c.nb[q];
         P.L = L[q];
+        P.hgroups = P.np <= 8 * 32 ? (8 * 32) / P.np : 1;     // consumer threads / np
         P.unit_out = sp.v.outputs * P.k * P.Wm;
         P.bulk_store = (out_al && P.out_off % 16 == 0 && P.unit_out % 16 == 0) ? 1 : 0;
         P.coop = (in_al && P.W % 16 == 0 && P.W >= 32 && P.in_off % 16 == 0 && pi.in_frame_bytes % 16 == 0)

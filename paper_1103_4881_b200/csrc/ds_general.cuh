@@ -39,6 +39,7 @@ struct GenPlane {
     int32_t ov;                // V origin reduced mod H (>= 0)
     int32_t unit_start;        // first unit (run) of this plane within a frame
     int32_t nb;                // bands in the plane: (H / Sv) / k
+    int32_t hgroups;           // H pass row groups: NC / np when np <= NC, else 1
     int32_t L;                 // bands per run (unit); consecutive bands reuse the halo's mid rows
     int32_t unit_out;          // Qv * k * Wm (output bytes of one band)
     int32_t bulk_store;
@@ -129,23 +130,6 @@ __device__ __forceinline__ int32_t g_div_small(int32_t t, int32_t d, uint32_t rc
 // and its wrap pad: 5 aligned words byte-shifted into a 16-byte window (taps
 // past P are zero in the packed weights), one dp4a per 4 taps.
 template <int Q, int FAST>
-__device__ __forceinline__ void g_h_load(const GenStage& g, const GenPlane& P, uint32_t st, uint32_t mid, int it,
-                                         uint32_t (&x)[4], uint32_t& mo) {
-    const int r = g_div_small(it, P.np, P.np_rcp);
-    const int r1 = it - r * P.np;
-    int c0 = P.oh + g.S * r1;
-    if (c0 >= P.W) c0 -= P.W;                 // oh < W and Sh*r1 < W
-    const uint32_t wb = st + r * P.pitch + (c0 & ~3);
-    const uint32_t sel = 0x3210u + 0x1111u * (uint32_t)(c0 & 3);
-    const uint32_t w0 = lds32s(wb), w1 = lds32s(wb + 4), w2 = lds32s(wb + 8), w3 = lds32s(wb + 12),
-                   w4 = lds32s(wb + 16);
-    x[0] = __byte_perm(w0, w1, sel);
-    x[1] = __byte_perm(w1, w2, sel);
-    x[2] = __byte_perm(w2, w3, sel);
-    x[3] = __byte_perm(w3, w4, sel);
-    mo = mid + r * P.Wm + Q * r1;
-}
-template <int Q, int FAST>
 __device__ __forceinline__ void g_h_dot(const GenStage& g, const uint32_t (&x)[4], uint32_t (&o)[Q]) {
 #pragma unroll
     for (int j = 0; j < Q; ++j) {
@@ -156,31 +140,62 @@ __device__ __forceinline__ void g_h_dot(const GenStage& g, const uint32_t (&x)[4
         o[j] = g_out<FAST>(g, acc);
     }
 }
-// Two items per thread per step (it, it + NC), loads of both issued before
-// either's arithmetic: two independent chains to hide LDS / dp4a latency.
+// One H item at window words wb (byte shift in sel) -> Q bytes at mo.
+template <int Q, int FAST>
+__device__ __forceinline__ void g_h_win(uint32_t wb, uint32_t sel, uint32_t (&x)[4]) {
+    const uint32_t w0 = lds32s(wb), w1 = lds32s(wb + 4), w2 = lds32s(wb + 8), w3 = lds32s(wb + 12),
+                   w4 = lds32s(wb + 16);
+    x[0] = __byte_perm(w0, w1, sel);
+    x[1] = __byte_perm(w1, w2, sel);
+    x[2] = __byte_perm(w2, w3, sel);
+    x[3] = __byte_perm(w3, w4, sel);
+}
+// H pass, column-fixed: a thread keeps one H repetition r1 (its window start
+// c0, byte shift and mid column never change) and walks the staged rows, two
+// rows per step (loads of both first: two independent chains).  With
+// np <= NC the threads form G = NC / np row groups (thread -> (group, r1));
+// with np > NC a thread takes columns tid, tid + NC, ... for every row.
 template <int Q, int FAST, int NC>
 __device__ __forceinline__ void g_h_pass(const GenStage& g, const GenPlane& P, uint32_t st, uint32_t mid,
                                          int rows, int tid) {
-    const int items = rows * P.np;
-    int it = tid;
-    for (; it + NC < items; it += 2 * NC) {
-        uint32_t xa[4], xb[4], ma, mb, oa[Q], ob[Q];
-        g_h_load<Q, FAST>(g, P, st, mid, it, xa, ma);
-        g_h_load<Q, FAST>(g, P, st, mid, it + NC, xb, mb);
-        g_h_dot<Q, FAST>(g, xa, oa);
-        g_h_dot<Q, FAST>(g, xb, ob);
-#pragma unroll
-        for (int j = 0; j < Q; ++j) {
-            sts8s(ma + j, oa[j]);
-            sts8s(mb + j, ob[j]);
-        }
+    const int np = P.np;
+    int r1 = tid, r = 0, G = 1;
+    if (np <= NC) {
+        G = P.hgroups;                                // NC / np
+        r = g_div_small(tid, np, P.np_rcp);           // row group
+        if (r >= G) return;                           // idle: NC % np threads
+        r1 = tid - r * np;
     }
-    if (it < items) {
-        uint32_t xa[4], ma, oa[Q];
-        g_h_load<Q, FAST>(g, P, st, mid, it, xa, ma);
-        g_h_dot<Q, FAST>(g, xa, oa);
+    for (; r1 < np; r1 += NC) {
+        int c0 = P.oh + g.S * r1;
+        if (c0 >= P.W) c0 -= P.W;                     // oh < W and Sh*r1 < W
+        const uint32_t sel = 0x3210u + 0x1111u * (uint32_t)(c0 & 3);
+        const uint32_t wstep = G * P.pitch, mstep = G * P.Wm;
+        uint32_t wb = st + r * P.pitch + (c0 & ~3);
+        uint32_t mo = mid + r * P.Wm + Q * r1;
+        int rr = r;
+        for (; rr + G < rows; rr += 2 * G) {
+            uint32_t xa[4], xb[4], oa[Q], ob[Q];
+            g_h_win<Q, FAST>(wb, sel, xa);
+            g_h_win<Q, FAST>(wb + wstep, sel, xb);
+            g_h_dot<Q, FAST>(g, xa, oa);
+            g_h_dot<Q, FAST>(g, xb, ob);
 #pragma unroll
-        for (int j = 0; j < Q; ++j) sts8s(ma + j, oa[j]);
+            for (int j = 0; j < Q; ++j) {
+                sts8s(mo + j, oa[j]);
+                sts8s(mo + mstep + j, ob[j]);
+            }
+            wb += 2 * wstep;
+            mo += 2 * mstep;
+        }
+        if (rr < rows) {
+            uint32_t xa[4], oa[Q];
+            g_h_win<Q, FAST>(wb, sel, xa);
+            g_h_dot<Q, FAST>(g, xa, oa);
+#pragma unroll
+            for (int j = 0; j < Q; ++j) sts8s(mo + j, oa[j]);
+        }
+        if (np <= NC) break;
     }
 }
 // Taps outside s8: byte loop (same item space, same window bounds)
