@@ -23,6 +23,12 @@
 #include "ds.h"
 #include "ds_kernels.cuh"
 
+// build-time tuning knob (tools/build_variant.sh): CTAs per SM the register
+// budget is sized for
+#ifndef DS_GEN_MINB
+#define DS_GEN_MINB 2
+#endif
+
 namespace ds {
 
 struct GenPlane {
@@ -332,9 +338,7 @@ struct GenCursor {
 
 // 2 CTAs x (8 consumer + 1 producer) warps per SM: the register file is
 // split across 4 SMSPs, so 18 warps need <= 102 registers each.
-#ifndef DS_GEN_MINB
-#define DS_GEN_MINB 2
-#endif
+
 template <int FAST>
 __global__ void __launch_bounds__(9 * 32, DS_GEN_MINB) ds_fused_general_kernel(const __grid_constant__ GeneralParams p) {
     constexpr int NCW = 8;
