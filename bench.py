@@ -513,6 +513,13 @@ def main():
             },
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "per_launch": {
+                "median_ms": statistics.median(per), "min_ms": min(per),
+                "fps_median": n * world / (statistics.median(per) / 1e3),
+                "fps_best": n * world / (min(per) / 1e3),
+                "note": "rank 0's CUDA-event time of each timed ds_run (x world for the fps)"
+                        if world > 1 else "CUDA-event time of each timed ds_run",
+            } if not args.graph else None,
             "gpu_launches": args.steps,
             "clocks": clk.result(),
             "gather_ms": gather_ms,
