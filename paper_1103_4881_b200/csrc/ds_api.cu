@@ -782,17 +782,19 @@ DS_API int ds_run_host(ds_handle* h, const uint8_t* host_in, int64_t n, uint8_t*
         h->host_init = true;
     }
     if (h->host_alloc_frames < chunk) {
+        // grow the staging buffers stream-ordered on each slot's stream: the
+        // old buffers are released after the slot's queued work, and no
+        // device-wide synchronisation (cudaFree) stalls other streams
+        // (allocations are 256-byte aligned, as the K-N1 bulk copies need)
         for (auto& s : h->slots) {
-            cudaStreamSynchronize(s.stream);
-            if (s.d_in) cudaFree(s.d_in);
-            if (s.d_out) cudaFree(s.d_out);
+            if (s.d_in) cudaFreeAsync(s.d_in, s.stream);
+            if (s.d_out) cudaFreeAsync(s.d_out, s.stream);
             s.d_in = s.d_out = nullptr;
         }
         h->host_alloc_frames = 0;
         for (auto& s : h->slots) {
-            // +16: keep device buffers 16-byte aligned for K-N1 bulk copies
-            if (cudaMalloc(&s.d_in, chunk * fin) != cudaSuccess ||
-                cudaMalloc(&s.d_out, chunk * fout) != cudaSuccess) {
+            if (cudaMallocAsync(reinterpret_cast<void**>(&s.d_in), chunk * fin, s.stream) != cudaSuccess ||
+                cudaMallocAsync(reinterpret_cast<void**>(&s.d_out), chunk * fout, s.stream) != cudaSuccess) {
                 cudaGetLastError();
                 free_host_state(h);
                 return DS_ENOMEM;

@@ -65,6 +65,17 @@ bool spec_is_default(const ds_stage_spec& s, bool horizontal) {
 
 bool aligned(const void* p, uintptr_t a) { return (reinterpret_cast<uintptr_t>(p) & (a - 1)) == 0; }
 
+ds::TDiv tdiv(uint32_t d) {
+    ds::TDiv f{d, 0u, 0u};
+    if (d > 1) {
+        uint32_t l = 0;
+        while ((1ULL << l) < d) ++l;                       // ceil(log2 d)
+        f.m = (uint32_t)(((1ULL << (31 + l)) + d - 1) / d);
+        f.s = l - 1;
+    }
+    return f;
+}
+
 dim3 task_grid(const ds_handle* h, int64_t items, int pc, int64_t n) {
     const int64_t target = (int64_t)h->sm_count * 8;
     int64_t x = std::max<int64_t>(1, std::min<int64_t>((items + 255) / 256, target));
@@ -116,9 +127,36 @@ int launch_vtask(ds_handle* h, const uint8_t* mid, int64_t n, uint8_t* out, int 
     for (int p = p0; p < p0 + pc && fast; ++p)
         fast = (tp.Wm[p] % 4 == 0) && (tp.mid_off[p] % 4 == 0) && (tp.out_off[p] % 4 == 0);
     if (fast) {
-        int64_t items = 0;
-        for (int p = p0; p < p0 + pc; ++p) items = std::max<int64_t>(items, (int64_t)(tp.Wm[p] / 4) * (tp.H[p] / 9));
-        ds::ds_vtask_kernel<<<task_grid(h, items, pc, n), 256, 0, st>>>(mid, out, tp);
+        // one flat item space per block of frames (32-bit indices); 8-byte
+        // column groups when every plane's rows and offsets allow it
+        bool v8 = aligned(mid, 8) && aligned(out, 8) && tp.mid_frame % 8 == 0 && tp.out_frame % 8 == 0;
+        for (int p = p0; p < p0 + pc && v8; ++p)
+            v8 = (tp.Wm[p] % 8 == 0) && (tp.mid_off[p] % 8 == 0) && (tp.out_off[p] % 8 == 0);
+        const int vec = v8 ? 8 : 4;
+        ds::VFlat vf;
+        std::memset(&vf, 0, sizeof vf);
+        vf.planes = pc;
+        uint32_t per = 0;
+        for (int i = 0; i < pc; ++i) {
+            const int p = p0 + i;
+            const uint32_t quads = (uint32_t)(tp.Wm[p] / vec);
+            vf.pstart[i] = per;
+            vf.qdiv[i] = tdiv(quads);
+            per += quads * (uint32_t)(tp.H[p] / 9);
+        }
+        vf.per_frame = per;
+        vf.fdiv = tdiv(per);
+        const int64_t fmax = std::max<int64_t>(1, ((1LL << 31) - 1) / std::max<uint32_t>(per, 1));
+        for (int64_t f0 = 0; f0 < n && per > 0; f0 += fmax) {
+            const int64_t nf = std::min<int64_t>(fmax, n - f0);
+            const uint32_t items = (uint32_t)(nf * per);
+            const int64_t blocks = std::max<int64_t>(
+                1, std::min<int64_t>(((int64_t)items + 511) / 512, (int64_t)h->sm_count * 8));
+            if (v8)
+                ds::ds_vtask_kernel<uint2><<<(unsigned)blocks, 256, 0, st>>>(mid, out, tp, vf, f0, items);
+            else
+                ds::ds_vtask_kernel<uint32_t><<<(unsigned)blocks, 256, 0, st>>>(mid, out, tp, vf, f0, items);
+        }
     } else {
         ds::GenericTask gt;
         gt.tp = tp;

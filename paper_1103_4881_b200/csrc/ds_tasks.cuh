@@ -13,9 +13,10 @@
 //                     any contiguous byte range of frames/planes maps to the
 //                     Mid range at 3/8 of its offset.  16-byte loads, warp
 //                     repack through shared memory into 16-byte stores.
-//   ds_vtask_kernel   V task, SPEC taps: thread = (frame, plane, 9-row group,
-//                     4 Mid columns); 8 LDG.32 (row 4 has zero weight),
-//                     4 STG.32.
+//   ds_vtask_kernel   V task, SPEC taps: item = (frame, plane, 9-row group,
+//                     4 Mid columns) in one flat 32-bit item space; 8 LDG.32
+//                     per item (row 4 has zero weight), 4 STG.32, two items
+//                     per thread step with all loads issued first.
 //   ds_htask_generic / ds_vtask_generic: any ds_stage_spec, one thread per
 //                     output element, literal tiler indexing.
 #pragma once
@@ -98,30 +99,87 @@ __device__ __forceinline__ uint32_t t_vquad(uint32_t a, uint32_t b, uint32_t wa,
     return __byte_perm(s_lo, s_hi, 0x7531);
 }
 
+// n / d for 0 <= n < 2^31 by multiply-high (host: m = ceil(2^(31+l) / d),
+// l = ceil(log2 d), s = l - 1; d = 1: m = 0 marks the identity)
+struct TDiv {
+    uint32_t d, m, s;
+};
+__device__ __forceinline__ uint32_t t_fdiv(const TDiv& f, uint32_t n) {
+    return f.m == 0 ? n : (__umulhi(n, f.m) >> f.s);
+}
+
+// Flat V-task item space over a block of frames: item = ((f * per_frame) +
+// plane start + g * quads + q), all < 2^31 (the host splits longer streams).
+struct VFlat {
+    uint32_t per_frame;                 // sum over the planes of quads * groups
+    TDiv fdiv;                          // / per_frame
+    uint32_t pstart[DS_MAX_PLANES];     // first item of each plane within a frame
+    TDiv qdiv[DS_MAX_PLANES];           // / quads of each plane
+    int32_t planes;
+};
+
+// item -> (column pointer into Mid, output pointer, row stride in VEC-byte words)
+template <typename VEC>
+__device__ __forceinline__ void t_vitem(const uint8_t* __restrict__ mid, uint8_t* __restrict__ out,
+                                        const TaskPlanes& tp, const VFlat& vf, int64_t f0, uint32_t it,
+                                        const VEC*& col, VEC*& o, int& wq) {
+    const uint32_t f = t_fdiv(vf.fdiv, it);
+    uint32_t r = it - f * vf.per_frame;
+    const int pl = (vf.planes > 2 && r >= vf.pstart[2]) ? 2 : (vf.planes > 1 && r >= vf.pstart[1]) ? 1 : 0;
+    r -= vf.pstart[pl];
+    const uint32_t g = t_fdiv(vf.qdiv[pl], r);
+    const uint32_t q = r - g * vf.qdiv[pl].d;
+    const int p = tp.plane_first + pl;
+    const int64_t fr = f0 + f;
+    wq = tp.Wm[p] / (int)sizeof(VEC);
+    col = reinterpret_cast<const VEC*>(mid + fr * tp.mid_frame + tp.mid_off[p] + (int64_t)9 * g * tp.Wm[p]) + q;
+    o = reinterpret_cast<VEC*>(out + fr * tp.out_frame + tp.out_off[p] + (int64_t)4 * g * tp.Wm[p]) + q;
+}
+
+__device__ __forceinline__ uint32_t t_vq(uint32_t a, uint32_t b, uint32_t wa, uint32_t wb) {
+    return t_vquad(a, b, wa, wb);
+}
+__device__ __forceinline__ uint2 t_vq(uint2 a, uint2 b, uint32_t wa, uint32_t wb) {
+    return make_uint2(t_vquad(a.x, b.x, wa, wb), t_vquad(a.y, b.y, wa, wb));
+}
+
+// V task, SPEC taps: item = (frame, plane, 9-row group g, sizeof(VEC) Mid
+// columns q); 8 row loads per item (row 4 has zero weight), 4 row stores.
+// Each thread takes two items per step (it, it + stride) and issues all 16
+// loads first.
+template <typename VEC>
 __global__ void __launch_bounds__(256)
     ds_vtask_kernel(const uint8_t* __restrict__ mid, uint8_t* __restrict__ out,
-                    const __grid_constant__ TaskPlanes tp) {
-    const int p = tp.plane_first + blockIdx.y;
-    const int quads = tp.Wm[p] >> 2;
-    const int groups = tp.H[p] / 9;
-    const int64_t items = (int64_t)quads * groups;
-    for (int64_t f = blockIdx.z; f < tp.n_frames; f += gridDim.z) {
-        const uint8_t* mp = mid + f * tp.mid_frame + tp.mid_off[p];
-        uint8_t* op = out + f * tp.out_frame + tp.out_off[p];
-        for (int64_t it = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; it < items;
-             it += (int64_t)gridDim.x * blockDim.x) {
-            const int g = (int)(it / quads), q = (int)(it - (int64_t)g * quads);
-            const uint32_t* col = reinterpret_cast<const uint32_t*>(mp + (int64_t)9 * g * tp.Wm[p]) + q;
-            const int wq = tp.Wm[p] >> 2;
-            const uint32_t m0 = __ldcs(col), m1 = __ldcs(col + wq), m2 = __ldcs(col + 2 * wq),
-                           m3 = __ldcs(col + 3 * wq), m5 = __ldcs(col + 5 * wq),
-                           m6 = __ldcs(col + 6 * wq), m7 = __ldcs(col + 7 * wq),
-                           m8 = __ldcs(col + 8 * wq);
-            uint32_t* o = reinterpret_cast<uint32_t*>(op + (int64_t)4 * g * tp.Wm[p]) + q;
-            __stcs(o, t_vquad(m0, m1, 96u, 160u));
-            __stcs(o + wq, t_vquad(m2, m3, 32u, 224u));
-            __stcs(o + 2 * wq, t_vquad(m5, m6, 224u, 32u));
-            __stcs(o + 3 * wq, t_vquad(m7, m8, 160u, 96u));
+                    const __grid_constant__ TaskPlanes tp, const __grid_constant__ VFlat vf, int64_t f0,
+                    uint32_t items) {
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t it = blockIdx.x * blockDim.x + threadIdx.x; it < items; it += 2 * stride) {
+        const VEC* ca;
+        VEC* oa;
+        int wa;
+        t_vitem<VEC>(mid, out, tp, vf, f0, it, ca, oa, wa);
+        const bool two = it + stride < items;
+        const VEC* cb = ca;
+        VEC* ob = oa;
+        int wb = wa;
+        if (two) t_vitem<VEC>(mid, out, tp, vf, f0, it + stride, cb, ob, wb);
+        const VEC a0 = __ldcs(ca), a1 = __ldcs(ca + wa), a2 = __ldcs(ca + 2 * wa), a3 = __ldcs(ca + 3 * wa),
+                  a5 = __ldcs(ca + 5 * wa), a6 = __ldcs(ca + 6 * wa), a7 = __ldcs(ca + 7 * wa),
+                  a8 = __ldcs(ca + 8 * wa);
+        VEC b0{}, b1{}, b2{}, b3{}, b5{}, b6{}, b7{}, b8{};
+        if (two) {
+            b0 = __ldcs(cb); b1 = __ldcs(cb + wb); b2 = __ldcs(cb + 2 * wb); b3 = __ldcs(cb + 3 * wb);
+            b5 = __ldcs(cb + 5 * wb); b6 = __ldcs(cb + 6 * wb); b7 = __ldcs(cb + 7 * wb); b8 = __ldcs(cb + 8 * wb);
+        }
+        __stcs(oa, t_vq(a0, a1, 96u, 160u));
+        __stcs(oa + wa, t_vq(a2, a3, 32u, 224u));
+        __stcs(oa + 2 * wa, t_vq(a5, a6, 224u, 32u));
+        __stcs(oa + 3 * wa, t_vq(a7, a8, 160u, 96u));
+        if (two) {
+            __stcs(ob, t_vq(b0, b1, 96u, 160u));
+            __stcs(ob + wb, t_vq(b2, b3, 32u, 224u));
+            __stcs(ob + 2 * wb, t_vq(b5, b6, 224u, 32u));
+            __stcs(ob + 3 * wb, t_vq(b7, b8, 160u, 96u));
         }
     }
 }
