@@ -424,6 +424,21 @@ def test_hd_300_frame_stream_bench_config():
                 assert pout[R, Cc] == oracle.pixel(pin, int(R), int(Cc))
 
 
+def test_hd_300_frame_stream_every_frame():
+    """BASELINE configs[2], the bench workload, verified on EVERY frame: all
+    300 device outputs against the oracle's direct nested loops (O2, pinned
+    equal to the tiler executor O1 by the CPU tests), frames regenerated on
+    the host by global index."""
+    W, H, N = 1920, 1080, 300
+    d = ds.Downscaler(W, H, 3)
+    x = ds.generate_frames(N, d.in_frame_bytes, seed=1)
+    y = d(x).cpu().numpy()
+    assert d.last_kernel() == FUSED
+    for f0 in range(0, N, 50):
+        fr = synth.random_frames(1, f0, 50, W, H)
+        _assert_same(y[f0: f0 + 50], oracle.direct_frames(fr, W, H), f"frames {f0}..{f0 + 49}")
+
+
 def test_cuda_graph_capture():
     """ds_run is capturable in a CUDA graph (the launch-bound 1-frame config
     replays a graph); replayed output equals the oracle."""
