@@ -123,7 +123,9 @@ typedef struct {
     int32_t general_band_reps[DS_MAX_PLANES];  /* K-N1g: V repetitions per unit */
     int64_t general_units_per_frame;
     int64_t general_stage_bytes_max;     /* K-N1g: staged bytes per unit: R rows (band + halo)
-                                            at a pitch of round_up(W, 16) + 32 (wrap pad) */
+                                            at a pitch of round_up(W, 16) + 32 (wrap pad), or
+                                            a column strip's window pitch */
+    int32_t general_strips[DS_MAX_PLANES];  /* K-N1g: column strips per plane (1 = whole rows) */
 } ds_plan_info;
 
 /* Fill *out with SPEC's downscaler (hfilter_8to3 S:527-535, vfilter_9to4
@@ -231,6 +233,13 @@ DS_API int ds_set_band_bytes(ds_handle* h, int64_t target_bytes);
  * without a V halo.  Output is unaffected.  Not synchronised with ds_run
  * calls in flight on other threads. */
 DS_API int ds_set_run_bands(ds_handle* h, int32_t bands);
+
+/* K-N1g stage size: the staged bytes one band may occupy (0 = default:
+ * 28 KiB with a V halo, 40 KiB without).  Planes whose k = 1 band does not
+ * fit are split into column strips (ds_plan_info.general_strips).  Output is
+ * unaffected; K-N1g stays ineligible if the result still exceeds shared
+ * memory.  Not synchronised with ds_run calls in flight on other threads. */
+DS_API int ds_set_general_stage_bytes(ds_handle* h, int64_t target_bytes);
 
 /* K-N1 launch shape that ds_run would use for n_frames:
  * grid CTAs, threads per CTA, dynamic shared memory bytes. */

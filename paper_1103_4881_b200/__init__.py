@@ -62,6 +62,7 @@ class ds_plan_info(C.Structure):
         ("general_band_reps", C.c_int32 * DS_MAX_PLANES),
         ("general_units_per_frame", C.c_int64),
         ("general_stage_bytes_max", C.c_int64),
+        ("general_strips", C.c_int32 * 3),
     ]
 
 
@@ -163,6 +164,7 @@ SIGNATURES = [
     ("ds_set_tuning", C.c_int, [C.c_void_p, C.c_int32, C.c_int32]),
     ("ds_set_band_bytes", C.c_int, [C.c_void_p, C.c_int64]),
     ("ds_set_run_bands", C.c_int, [C.c_void_p, C.c_int32]),
+    ("ds_set_general_stage_bytes", C.c_int, [C.c_void_p, C.c_int64]),
     ("ds_launch_shape", C.c_int, [C.c_void_p, C.c_int64, _PI32, _PI32, _PI32]),
     ("ds_mid_frame_bytes", C.c_int64, [C.c_void_p]),
     ("ds_run_htask", C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int32, C.c_int32,
@@ -460,6 +462,13 @@ class Downscaler:
         rc = lib().ds_set_run_bands(self._h, bands)
         if rc:
             raise DSError(rc, "ds_set_run_bands")
+
+    def set_general_stage_bytes(self, target: int) -> None:
+        """K-N1g: staged bytes per band (0 = default); wide planes split into column strips."""
+        rc = lib().ds_set_general_stage_bytes(self._h, target)
+        if rc:
+            raise DSError(rc, "ds_set_general_stage_bytes")
+        self.plan = self.get_plan()
 
     def get_plan(self):
         info = ds_plan_info()

@@ -86,8 +86,46 @@ int64_t fused_smem_bytes(int stages, int32_t stage_stride, int32_t out_stride) {
            (int64_t)2 * stages * 8;
 }
 
+// K-N1g per-plane geometry.  A band of k V repetitions stages
+// R = Sv (k-1) + Pv rows.  Whole rows (row + 32-byte wrap pad) when a k = 1
+// band fits the stage target; otherwise column strips of sw H repetitions
+// (a multiple of 16, so strip outputs start 16-byte aligned) whose input
+// window Sh (sw-1) + Ph is staged from its 16-aligned superset (+15 bytes of
+// phase, +20 bytes of window over-read slack).  k is then the largest divisor
+// of the band count whose rows still fit.
+GenGeom general_plane_geom(const ds_filter_spec& spec, int32_t W, int32_t Hp, int64_t target) {
+    GenGeom g;
+    const int Sh = spec.h.paving, Ph = spec.h.pattern;
+    const int np = W / Sh;
+    const int G = Hp / spec.v.paving;
+    const int64_t R1 = spec.v.pattern;
+    int64_t pitch = general_pitch(W);
+    g.strips = 1; g.sw = np; g.np_last = np;
+    auto strip_pitch = [&](int64_t sw) { return round_up((int64_t)Sh * (sw - 1) + Ph + 15 + 20, 16); };
+    if (R1 * pitch > target && np >= 32) {
+        int64_t sw = np / 16 * 16;
+        while (sw > 16 && (R1 * strip_pitch(sw) > target || strip_pitch(sw) > W)) sw -= 16;
+        if (sw >= 16 && sw < np && strip_pitch(sw) <= W) {
+            g.sw = (int32_t)sw;
+            g.strips = (int32_t)((np + sw - 1) / sw);
+            g.np_last = (int32_t)(np - (int64_t)(g.strips - 1) * sw);
+            pitch = strip_pitch(sw);
+        }
+    }
+    int best = 1;
+    for (int d = 1; d <= G; ++d) {
+        if (G % d) continue;
+        if (((int64_t)spec.v.paving * (d - 1) + spec.v.pattern) * pitch <= target) best = d;
+    }
+    g.k = best;
+    g.R = spec.v.paving * (best - 1) + spec.v.pattern;
+    g.pitch = (int32_t)pitch;
+    g.wm_max = spec.h.outputs * g.sw;
+    return g;
+}
+
 int make_plan(int32_t W, int32_t H, int32_t channels, const ds_filter_spec* spec_in,
-              ds_filter_spec* spec_out, ds_plan_info* info, int64_t unit_target) {
+              ds_filter_spec* spec_out, ds_plan_info* info, int64_t unit_target, int64_t general_target) {
     ds_filter_spec spec;
     if (spec_in) spec = *spec_in; else default_spec(&spec);
     if (W < 1 || H < 1) return DS_ESHAPE;
@@ -174,26 +212,21 @@ int make_plan(int32_t W, int32_t H, int32_t channels, const ds_filter_spec* spec
         int64_t units = 0, smax = 0, mmax = 0, omax = 0;
         // with a V halo (Pv > Sv) consecutive bands of a run reuse the halo's mid
         // rows, so small bands cost little and leave smem for a second mid buffer
-        const int64_t stage_target = spec.v.pattern > spec.v.paving ? kGeneralStageTargetReuse : kGeneralStageTarget;
+        const int64_t stage_target = general_stage_target(spec, general_target);
         for (int p = 0; p < channels; ++p) {
             const int G = pi.in_h[p] / spec.v.paving;
-            const int64_t pitch = general_pitch(pi.in_w[p]);
-            int best = 1;
-            for (int d = 1; d <= G; ++d) {
-                if (G % d) continue;
-                const int64_t R = (int64_t)spec.v.paving * (d - 1) + spec.v.pattern;
-                if (R * pitch <= stage_target) best = d;
-            }
-            const int64_t R = (int64_t)spec.v.paving * (best - 1) + spec.v.pattern;
-            pi.general_band_reps[p] = best;
-            units += G / best;
-            smax = std::max<int64_t>(smax, R * pitch);
-            mmax = std::max<int64_t>(mmax, (R + 3) * pi.out_w[p]);   // +3: dp4a row blocks
-            omax = std::max<int64_t>(omax, (int64_t)spec.v.outputs * best * pi.out_w[p]);
+            const GenGeom gg = general_plane_geom(spec, pi.in_w[p], pi.in_h[p], stage_target);
+            const int64_t R = gg.R, best = gg.k;
+            pi.general_band_reps[p] = gg.k;
+            pi.general_strips[p] = gg.strips;
+            units += (int64_t)gg.strips * (G / best);
+            smax = std::max<int64_t>(smax, R * gg.pitch);
+            mmax = std::max<int64_t>(mmax, (R + 3) * gg.wm_max);   // +3: dp4a row blocks
+            omax = std::max<int64_t>(omax, (int64_t)spec.v.outputs * best * gg.wm_max);
             // exact reciprocal index division: items * divisor < 2^32
-            const int64_t np = pi.in_w[p] / spec.h.paving;
+            const int64_t np = gg.sw;
             if (R * np * np >= (1LL << 32) ||
-                (int64_t)spec.v.outputs * best * pi.out_w[p] * pi.out_w[p] >= (1LL << 32))
+                (int64_t)spec.v.outputs * best * gg.wm_max * gg.wm_max >= (1LL << 32))
                 general = false;
         }
         const int64_t mids = spec.v.pattern > spec.v.paving ? 2 : 1;
@@ -205,7 +238,7 @@ int make_plan(int32_t W, int32_t H, int32_t channels, const ds_filter_spec* spec
     }
     pi.fused_general_eligible = general ? 1 : 0;
     if (!general) {
-        for (int p = 0; p < DS_MAX_PLANES; ++p) pi.general_band_reps[p] = 0;
+        for (int p = 0; p < DS_MAX_PLANES; ++p) pi.general_band_reps[p] = pi.general_strips[p] = 0;
         pi.general_units_per_frame = pi.general_stage_bytes_max = 0;
     }
     *info = pi;
@@ -380,12 +413,12 @@ int32_t general_runs(const ds_handle* h, int64_t n, int32_t* L) {
     int64_t bb[DS_MAX_PLANES], bbmax = 1;
     for (int q = 0; q < pi.n_planes; ++q) {
         L[q] = 1;
-        bb[q] = (int64_t)c.R[q] * pi.in_w[q];
+        bb[q] = (int64_t)c.R[q] * c.geom[q].pitch;
         bbmax = std::max(bbmax, bb[q]);
     }
     auto upf_of = [&](const int32_t* l) {
         int32_t u = 0;
-        for (int q = 0; q < pi.n_planes; ++q) u += (c.nb[q] + l[q] - 1) / l[q];
+        for (int q = 0; q < pi.n_planes; ++q) u += c.geom[q].strips * ((c.nb[q] + l[q] - 1) / l[q]);
         return u;
     };
     if (c.mid_alt == 0) return upf_of(L);
@@ -463,13 +496,14 @@ int configure_general(ds_handle* h) {
     int64_t smax = 0, mmax = 0, omax = 0;
     int32_t upf = 0;
     for (int p = 0; p < pi.n_planes; ++p) {
-        c.k[p] = pi.general_band_reps[p];
+        c.geom[p] = general_plane_geom(sp, pi.in_w[p], pi.in_h[p], general_stage_target(sp, h->general_target));
+        c.k[p] = c.geom[p].k;
         c.nb[p] = (pi.in_h[p] / sp.v.paving) / c.k[p];
-        c.R[p] = sp.v.paving * (c.k[p] - 1) + sp.v.pattern;
-        smax = std::max<int64_t>(smax, (int64_t)c.R[p] * general_pitch(pi.in_w[p]));
-        mmax = std::max<int64_t>(mmax, (int64_t)(c.R[p] + 3) * pi.out_w[p]);   // V reads 4-row blocks
-        omax = std::max<int64_t>(omax, (int64_t)sp.v.outputs * c.k[p] * pi.out_w[p]);
-        upf += (pi.in_h[p] / sp.v.paving) / c.k[p];
+        c.R[p] = c.geom[p].R;
+        smax = std::max<int64_t>(smax, (int64_t)c.R[p] * c.geom[p].pitch);
+        mmax = std::max<int64_t>(mmax, (int64_t)(c.R[p] + 3) * c.geom[p].wm_max);   // V reads 4-row blocks
+        omax = std::max<int64_t>(omax, (int64_t)sp.v.outputs * c.k[p] * c.geom[p].wm_max);
+        upf += c.geom[p].strips * c.nb[p];
     }
     c.upf = upf;
     c.stage_stride = (int32_t)round_up(smax, 128);
@@ -553,13 +587,33 @@ int launch_general(ds_handle* h, const uint8_t* in, int64_t n, uint8_t* out, cud
         P.unit_start = start;
         P.nb = c.nb[q];
         P.L = L[q];
-        P.hgroups = P.np <= 8 * 32 ? (8 * 32) / P.np : 1;     // consumer threads / np
+        const GenGeom& gg = c.geom[q];
+        P.strips = gg.strips;
+        P.sw = gg.sw;
+        P.runs = (P.nb + P.L - 1) / P.L;
+        P.runs_rcp = rcp32(P.runs);
+        auto groups = [](int np) { return np <= 8 * 32 ? (8 * 32) / np : 1; };   // consumer threads / np
+        if (gg.strips > 1) {
+            // per-strip geometry: regular strips (sw repetitions) and the last one
+            P.np_rcp = rcp32(gg.sw);
+            P.wm_rcp = rcp32(sp.h.outputs * gg.sw);
+            P.quads_rcp = rcp32(sp.h.outputs * gg.sw / 4);
+            P.hgroups = groups(gg.sw);
+            P.np_last = gg.np_last;
+            P.np_rcp_last = rcp32(gg.np_last);
+            P.wm_rcp_last = rcp32(sp.h.outputs * gg.np_last);
+            P.quads_rcp_last = rcp32(sp.h.outputs * gg.np_last / 4);
+            P.hgroups_last = groups(gg.np_last);
+        } else {
+            P.hgroups = groups(P.np);
+        }
         P.unit_out = sp.v.outputs * P.k * P.Wm;
         P.bulk_store = (out_al && P.out_off % 16 == 0 && P.unit_out % 16 == 0) ? 1 : 0;
+        P.bulk_rows = (out_al && P.out_off % 16 == 0 && P.Wm % 16 == 0) ? 1 : 0;
         P.coop = (in_al && P.W % 16 == 0 && P.W >= 32 && P.in_off % 16 == 0 && pi.in_frame_bytes % 16 == 0)
                      ? 0 : 1;
-        P.pitch = (int32_t)general_pitch(P.W);
-        start += (P.nb + P.L - 1) / P.L;
+        P.pitch = gg.pitch;
+        start += P.strips * P.runs;
     }
     const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(p.n_units, (int64_t)c.grid_per_sm * h->sm_count));
     general_fn(c.fast)<<<(unsigned)grid, c.threads, c.smem, st>>>(p);
@@ -899,10 +953,21 @@ DS_API int ds_set_band_bytes(ds_handle* h, int64_t target) {
     if (!h || target < 0) return DS_EINVAL;
     if (target == 0) target = kUnitTargetBytes;
     ds_plan_info pi;
-    const int rc = make_plan(h->W, h->H, h->channels, &h->spec, nullptr, &pi, target);
+    const int rc = make_plan(h->W, h->H, h->channels, &h->spec, nullptr, &pi, target, h->general_target);
     if (rc) return rc;
     h->plan = pi;
     h->band_target = target;
+    const int crc = configure_fused(h);
+    return crc ? crc : configure_general(h);
+}
+
+DS_API int ds_set_general_stage_bytes(ds_handle* h, int64_t target) {
+    if (!h || target < 0) return DS_EINVAL;
+    ds_plan_info pi;
+    const int rc = make_plan(h->W, h->H, h->channels, &h->spec, nullptr, &pi, h->band_target, target);
+    if (rc) return rc;
+    h->plan = pi;
+    h->general_target = target;
     const int crc = configure_fused(h);
     return crc ? crc : configure_general(h);
 }

@@ -10,7 +10,11 @@
 // of round_up(W, 16) + 32 bytes: the row, then a 32-byte pad holding its first
 // bytes again (row[j mod W]), so an H window that wraps past the row end
 // reads straight on into the pad -- no wrap test, no divergent slow
-// path.  Consumers run the H task on every staged row into a u8 intermediate
+// path.  A plane too wide for the stage budget is split into column strips of
+// S_w H repetitions (a multiple of 16): a unit then stages, per row, only its
+// strip's input window (o_h + S_h a, width S_h (S_w - 1) + P_h, modulo W) as
+// the 16-byte-aligned superset (two bulk copies when it wraps the row end)
+// and stores its output rows strip-wise.  Consumers run the H task on every staged row into a u8 intermediate
 // in shared memory, then the V task from it, stage the output band in
 // shared memory and bulk-store it.  Divisions by runtime values are exact
 // (truncation toward zero, then clamp): one multiply-high when the host
@@ -50,6 +54,24 @@ struct GenPlane {
     int32_t unit_out;          // Qv * k * Wm (output bytes of one band)
     int32_t bulk_store;
     int32_t coop;              // 1: rows staged by the producer warp with plain loads
+    // column strips (strips > 1): strip j covers H repetitions [j sw, min((j+1) sw, np))
+    int32_t strips, sw;        // strip count, repetitions per strip (last: np - (strips-1) sw)
+    int32_t runs;              // runs of bands per strip: ceil(nb / L)
+    int32_t np_last, hgroups_last;
+    uint32_t np_rcp_last, quads_rcp_last, wm_rcp_last, sw_rcp, runs_rcp;
+    int32_t bulk_rows;         // strips: output row segments may be bulk-stored (16-byte aligned)
+};
+
+// The part of a plane one unit covers: the whole width (strips == 1, staged
+// rows = row + wrap pad) or one column strip (staged rows = the strip's input
+// window from its 16-aligned superset).
+struct GenView {
+    int32_t np, wm, hgroups;   // H repetitions, mid/output bytes per row, H-pass row groups
+    uint32_t np_rcp, wm_rcp, quads_rcp;
+    int32_t col0;              // first output column of the unit (Qh * first repetition)
+    int32_t cbase, cwrap;      // window start of repetition t: cbase + Sh t, minus cwrap once if >= cwrap
+    int32_t unit_out;          // output bytes of one band: Qv k wm
+    int32_t strip, run;
 };
 
 struct GenStage {
@@ -130,6 +152,40 @@ __device__ __forceinline__ int32_t g_div_small(int32_t t, int32_t d, uint32_t rc
     return d == 1 ? t : (int32_t)__umulhi((uint32_t)t, rcp);
 }
 
+// Unit -> (strip, run) and the strip's geometry.  a = first repetition of
+// the strip, cs = its window start (o_h + S_h a) mod W; staged rows hold the
+// window from the 16-aligned superset start x0 = cs & ~15, so repetition t of
+// the strip starts at byte (cs - x0) + S_h t of its staged row.
+__device__ __forceinline__ GenView g_view(const GenPlane& P, int Sh, int Qh, int Qv, int local) {
+    GenView v;
+    if (P.strips == 1) {
+        v.np = P.np; v.wm = P.Wm; v.hgroups = P.hgroups;
+        v.np_rcp = P.np_rcp; v.wm_rcp = P.wm_rcp; v.quads_rcp = P.quads_rcp;
+        v.col0 = 0; v.cbase = P.oh; v.cwrap = P.W;
+        v.unit_out = P.unit_out;
+        v.strip = 0; v.run = local;
+        return v;
+    }
+    v.strip = (int)__umulhi((uint32_t)local, P.runs_rcp);
+    if (P.runs == 1) v.strip = local;
+    v.run = local - v.strip * P.runs;
+    const bool last = v.strip == P.strips - 1;
+    v.np = last ? P.np_last : P.sw;
+    v.wm = Qh * v.np;
+    v.hgroups = last ? P.hgroups_last : P.hgroups;
+    v.np_rcp = last ? P.np_rcp_last : P.np_rcp;
+    v.wm_rcp = last ? P.wm_rcp_last : P.wm_rcp;
+    v.quads_rcp = last ? P.quads_rcp_last : P.quads_rcp;
+    const int a = v.strip * P.sw;
+    v.col0 = Qh * a;
+    const int64_t cs = ((int64_t)P.oh + (int64_t)Sh * a) % P.W;
+    v.cbase = (int)(cs & 15);             // TMA superset phase (coop rows: staged from cs, see producer)
+    if (P.coop) v.cbase = 0;
+    v.cwrap = 0x7fffffff;
+    v.unit_out = Qv * P.k * v.wm;
+    return v;
+}
+
 // ---- H pass over one staged unit: item = (staged row r, H repetition r1),
 // Q outputs into mid row r at 3 r1 ...  The window starts at
 // c0 = (o_h + S_h r1) mod W < W and runs at most 19 bytes on, inside the row
@@ -162,23 +218,23 @@ __device__ __forceinline__ void g_h_win(uint32_t wb, uint32_t sel, uint32_t (&x)
 // np <= NC the threads form G = NC / np row groups (thread -> (group, r1));
 // with np > NC a thread takes columns tid, tid + NC, ... for every row.
 template <int Q, int FAST, int NC>
-__device__ __forceinline__ void g_h_pass(const GenStage& g, const GenPlane& P, uint32_t st, uint32_t mid,
-                                         int rows, int tid) {
-    const int np = P.np;
+__device__ __forceinline__ void g_h_pass(const GenStage& g, const GenPlane& P, const GenView& V, uint32_t st,
+                                         uint32_t mid, int rows, int tid) {
+    const int np = V.np;
     int r1 = tid, r = 0, G = 1;
     if (np <= NC) {
-        G = P.hgroups;                                // NC / np
-        r = g_div_small(tid, np, P.np_rcp);           // row group
+        G = V.hgroups;                                // NC / np
+        r = g_div_small(tid, np, V.np_rcp);           // row group
         if (r >= G) return;                           // idle: NC % np threads
         r1 = tid - r * np;
     }
     for (; r1 < np; r1 += NC) {
-        int c0 = P.oh + g.S * r1;
-        if (c0 >= P.W) c0 -= P.W;                     // oh < W and Sh*r1 < W
+        int c0 = V.cbase + g.S * r1;
+        if (c0 >= V.cwrap) c0 -= V.cwrap;             // whole rows: oh < W and Sh*r1 < W
         const uint32_t sel = 0x3210u + 0x1111u * (uint32_t)(c0 & 3);
-        const uint32_t wstep = G * P.pitch, mstep = G * P.Wm;
+        const uint32_t wstep = G * P.pitch, mstep = G * V.wm;
         uint32_t wb = st + r * P.pitch + (c0 & ~3);
-        uint32_t mo = mid + r * P.Wm + Q * r1;
+        uint32_t mo = mid + r * V.wm + Q * r1;
         int rr = r;
         for (; rr + G < rows; rr += 2 * G) {
             uint32_t xa[4], xb[4], oa[Q], ob[Q];
@@ -207,16 +263,16 @@ __device__ __forceinline__ void g_h_pass(const GenStage& g, const GenPlane& P, u
 // Taps outside s8: byte loop (same item space, same window bounds)
 template <int FAST, int NC>
 __device__ __forceinline__ void g_h_pass_bytes(const GenStage& g, const int32_t (*w)[DS_MAX_PATTERN],
-                                               const GenPlane& P, uint32_t st, uint32_t mid, int rows,
-                                               int tid) {
-    const int np = P.np, W = P.W, items = rows * np;
+                                               const GenPlane& P, const GenView& V, uint32_t st, uint32_t mid,
+                                               int rows, int tid) {
+    const int np = V.np, items = rows * np;
     for (int it = tid; it < items; it += NC) {
-        const int r = g_div_small(it, np, P.np_rcp);
+        const int r = g_div_small(it, np, V.np_rcp);
         const int r1 = it - r * np;
-        int c0 = P.oh + g.S * r1;
-        if (c0 >= W) c0 -= W;
+        int c0 = V.cbase + g.S * r1;
+        if (c0 >= V.cwrap) c0 -= V.cwrap;
         const uint32_t rowp = st + r * P.pitch + c0;
-        const uint32_t mo = mid + r * P.Wm + g.Q * r1;
+        const uint32_t mo = mid + r * V.wm + g.Q * r1;
         for (int j = 0; j < g.Q; ++j) {
             int32_t acc = g_bias<FAST>(g);
             for (int i = 0; i < g.P; ++i) acc += w[j][i] * (int32_t)lds8s(rowp + i);
@@ -261,11 +317,11 @@ __device__ __forceinline__ void g_v_quad(const GenStage& g, int k0, uint32_t mb,
 // ---- V pass (Wm % 4 == 0, s8 taps): item = (V repetition gi, 4 mid columns);
 // outputs in groups of at most 4 (QA, then QB) to bound live accumulators.
 template <int QA, int QB, int FAST, int NC>
-__device__ __forceinline__ void g_v_pass(const GenStage& g, const GenPlane& P, uint32_t mid, uint32_t ob,
-                                         int tid) {
-    const int Wm = P.Wm, quads = Wm >> 2, items = P.k * quads;
+__device__ __forceinline__ void g_v_pass(const GenStage& g, const GenPlane& P, const GenView& V, uint32_t mid,
+                                         uint32_t ob, int tid) {
+    const int Wm = V.wm, quads = Wm >> 2, items = P.k * quads;
     for (int it = tid; it < items; it += NC) {
-        const int gi = g_div_small(it, quads, P.quads_rcp);
+        const int gi = g_div_small(it, quads, V.quads_rcp);
         const int q = it - gi * quads;
         const uint32_t mb = mid + g.S * gi * Wm + 4 * q;
         const uint32_t ob0 = ob + (QA + QB) * gi * Wm + 4 * q;
@@ -276,10 +332,11 @@ __device__ __forceinline__ void g_v_pass(const GenStage& g, const GenPlane& P, u
 // V pass, general: item = output byte of the band
 template <int FAST, int NC>
 __device__ __forceinline__ void g_v_pass_bytes(const GenStage& g, const int32_t (*w)[DS_MAX_PATTERN],
-                                               const GenPlane& P, uint32_t mid, uint32_t ob, int tid) {
-    const int Wm = P.Wm;
-    for (int it = tid; it < P.unit_out; it += NC) {
-        const int orow = g_div_small(it, Wm, P.wm_rcp);
+                                               const GenPlane& P, const GenView& V, uint32_t mid, uint32_t ob,
+                                               int tid) {
+    const int Wm = V.wm;
+    for (int it = tid; it < V.unit_out; it += NC) {
+        const int orow = g_div_small(it, Wm, V.wm_rcp);
         const int c = it - orow * Wm;
         const int gi = orow / g.Q, kk = orow - gi * g.Q;
         const uint32_t mcol = mid + g.S * gi * Wm + c;
@@ -310,6 +367,17 @@ __device__ __forceinline__ void g_coop_row(uint8_t* dst, const uint8_t* src, int
         for (int x = lane; x < W; x += 32) dst[x] = __ldg(src + x);
     }
     dst[W + lane] = __ldg(src + (lane < W ? lane : lane % W));
+}
+
+// Producer-warp staging of one strip window row (plain loads): bytes
+// row[(cs + j) mod W] for j < len.
+__device__ __forceinline__ void g_coop_window(uint8_t* dst, const uint8_t* row, int W, int cs, int len, int lane) {
+    int c = cs + lane;
+    for (int j = lane; j < len; j += 32) {
+        while (c >= W) c -= W;
+        dst[j] = __ldg(row + c);
+        c += 32;
+    }
 }
 
 struct GenCursor {
@@ -382,8 +450,19 @@ __global__ void __launch_bounds__(9 * 32, DS_GEN_MINB) ds_fused_general_kernel(c
         bool first_round = true;
         for (; cur.u < p.n_units; cur.next()) {
             const GenPlane& P = p.pl[cur.plane(p)];
-            const int b0 = (cur.local - P.unit_start) * P.L, b1 = min(b0 + P.L, P.nb);
+            const GenView V = g_view(P, p.h.S, p.h.Q, p.v.Q, cur.local - P.unit_start);
+            const int b0 = V.run * P.L, b1 = min(b0 + P.L, P.nb);
             const uint8_t* plane = p.in + cur.f * p.in_frame + P.in_off;
+            // strips: the window [cs, cs + lw) mod W, staged from x0 = cs & ~15
+            int cs = 0, lw = 0, x0 = 0, seg0 = 0, seg1 = 0;
+            if (P.strips > 1) {
+                cs = (int)(((int64_t)P.oh + (int64_t)p.h.S * V.strip * P.sw) % P.W);
+                lw = p.h.S * (V.np - 1) + p.h.P;
+                x0 = cs & ~15;
+                const int x1 = (cs + lw + 15) & ~15;
+                seg0 = min(x1, P.W) - x0;
+                seg1 = x1 > P.W ? x1 - P.W : 0;
+            }
             for (int band = b0; band < b1; ++band) {
                 if (!first_round) mbar_wait_sleep(&empty[s], phase ^ 1);
                 uint8_t* dst = ring + (size_t)s * p.stage_stride;
@@ -392,7 +471,24 @@ __global__ void __launch_bounds__(9 * 32, DS_GEN_MINB) ds_fused_general_kernel(c
                 const int reuse = band > b0 ? p.ovl : 0;
                 const int rows = P.R - reuse;
                 const int row0 = (int)(((int64_t)P.ov + (int64_t)p.v.S * P.k * band + reuse) % P.H);
-                if (!P.coop) {
+                if (P.strips > 1) {
+                    if (!P.coop) {
+                        if (lane == 0) mbar_arrive_expect_tx(&full[s], (uint32_t)rows * (uint32_t)(seg0 + seg1));
+                        __syncwarp();
+                        for (int i = lane; i < rows; i += 32) {
+                            const uint8_t* src = plane + (int64_t)((row0 + i) % P.H) * P.W;
+                            uint8_t* d = dst + (size_t)i * P.pitch;
+                            bulk_g2s(d, src + x0, (uint32_t)seg0, &full[s], pol);
+                            if (seg1) bulk_g2s(d + seg0, src, (uint32_t)seg1, &full[s], pol);
+                        }
+                    } else {
+                        for (int i = 0; i < rows; ++i)
+                            g_coop_window(dst + (size_t)i * P.pitch, plane + (int64_t)((row0 + i) % P.H) * P.W,
+                                          P.W, cs, lw, lane);
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&full[s]);
+                    }
+                } else if (!P.coop) {
                     if (lane == 0) mbar_arrive_expect_tx(&full[s], (uint32_t)rows * (uint32_t)(P.W + 32));
                     __syncwarp();
                     for (int i = lane; i < rows; i += 32) {
@@ -418,7 +514,8 @@ __global__ void __launch_bounds__(9 * 32, DS_GEN_MINB) ds_fused_general_kernel(c
     uint32_t mpar = 0;                              // which mid buffer the next band writes
     for (; cur.u < p.n_units; cur.next()) {
         const GenPlane& P = p.pl[cur.plane(p)];
-        const int b0 = (cur.local - P.unit_start) * P.L, b1 = min(b0 + P.L, P.nb);
+        const GenView V = g_view(P, p.h.S, p.h.Q, p.v.Q, cur.local - P.unit_start);
+        const int b0 = V.run * P.L, b1 = min(b0 + P.L, P.nb);
         if (p.unit_count != nullptr && tid == 0) atomicAdd(p.unit_count + cur.u, 1u);
         for (int band = b0; band < b1; ++band) {
             const uint32_t st = smem_u32(ring) + s * p.stage_stride;
@@ -429,63 +526,85 @@ __global__ void __launch_bounds__(9 * 32, DS_GEN_MINB) ds_fused_general_kernel(c
             if (reuse) {
                 // the previous band's mid rows [Sv k, R) are this band's rows
                 // [0, ovl) (its buffer is not written again before two more barriers)
-                const uint32_t src = smem_u32(mid) + (mpar ^ 1) * p.mid_alt + p.v.S * P.k * P.Wm;
-                const int nbytes = reuse * P.Wm;
-                if ((P.Wm & 3) == 0)
+                const uint32_t src = smem_u32(mid) + (mpar ^ 1) * p.mid_alt + p.v.S * P.k * V.wm;
+                const int nbytes = reuse * V.wm;
+                if ((V.wm & 3) == 0)
                     for (int x = 4 * tid; x < nbytes; x += 4 * NC) sts32s(mid_s + x, lds32s(src + x));
                 else
                     for (int x = tid; x < nbytes; x += NC) sts8s(mid_s + x, lds8s(src + x));
             }
             const int rows = P.R - reuse;
-            const uint32_t mid_h = mid_s + reuse * P.Wm;
+            const uint32_t mid_h = mid_s + reuse * V.wm;
             mbar_wait(&full[s], phase);
 
             // ---- H task on every newly staged row -> mid (u8)
             if (p.h.s8) {
                 switch (p.h.Q) {
-                    case 1: g_h_pass<1, FAST, NC>(p.h, P, st, mid_h, rows, tid); break;
-                    case 2: g_h_pass<2, FAST, NC>(p.h, P, st, mid_h, rows, tid); break;
-                    case 3: g_h_pass<3, FAST, NC>(p.h, P, st, mid_h, rows, tid); break;
-                    case 4: g_h_pass<4, FAST, NC>(p.h, P, st, mid_h, rows, tid); break;
-                    case 5: g_h_pass<5, FAST, NC>(p.h, P, st, mid_h, rows, tid); break;
-                    case 6: g_h_pass<6, FAST, NC>(p.h, P, st, mid_h, rows, tid); break;
-                    case 7: g_h_pass<7, FAST, NC>(p.h, P, st, mid_h, rows, tid); break;
-                    default: g_h_pass<8, FAST, NC>(p.h, P, st, mid_h, rows, tid); break;
+                    case 1: g_h_pass<1, FAST, NC>(p.h, P, V, st, mid_h, rows, tid); break;
+                    case 2: g_h_pass<2, FAST, NC>(p.h, P, V, st, mid_h, rows, tid); break;
+                    case 3: g_h_pass<3, FAST, NC>(p.h, P, V, st, mid_h, rows, tid); break;
+                    case 4: g_h_pass<4, FAST, NC>(p.h, P, V, st, mid_h, rows, tid); break;
+                    case 5: g_h_pass<5, FAST, NC>(p.h, P, V, st, mid_h, rows, tid); break;
+                    case 6: g_h_pass<6, FAST, NC>(p.h, P, V, st, mid_h, rows, tid); break;
+                    case 7: g_h_pass<7, FAST, NC>(p.h, P, V, st, mid_h, rows, tid); break;
+                    default: g_h_pass<8, FAST, NC>(p.h, P, V, st, mid_h, rows, tid); break;
                 }
             } else {
-                g_h_pass_bytes<FAST, NC>(p.h, wh, P, st, mid_h, rows, tid);
+                g_h_pass_bytes<FAST, NC>(p.h, wh, P, V, st, mid_h, rows, tid);
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[s]);     // ring slot no longer read
             named_bar_sync(1, NC);                      // mid complete
 
             // ---- V task from mid -> output band
-            if (p.v.s8 && (P.Wm & 3) == 0) {
+            if (p.v.s8 && (V.wm & 3) == 0) {
                 switch (p.v.Q) {
-                    case 1: g_v_pass<1, 0, FAST, NC>(p.v, P, mid_s, ob_s, tid); break;
-                    case 2: g_v_pass<2, 0, FAST, NC>(p.v, P, mid_s, ob_s, tid); break;
-                    case 3: g_v_pass<3, 0, FAST, NC>(p.v, P, mid_s, ob_s, tid); break;
-                    case 4: g_v_pass<4, 0, FAST, NC>(p.v, P, mid_s, ob_s, tid); break;
-                    case 5: g_v_pass<4, 1, FAST, NC>(p.v, P, mid_s, ob_s, tid); break;
-                    case 6: g_v_pass<4, 2, FAST, NC>(p.v, P, mid_s, ob_s, tid); break;
-                    case 7: g_v_pass<4, 3, FAST, NC>(p.v, P, mid_s, ob_s, tid); break;
-                    default: g_v_pass<4, 4, FAST, NC>(p.v, P, mid_s, ob_s, tid); break;
+                    case 1: g_v_pass<1, 0, FAST, NC>(p.v, P, V, mid_s, ob_s, tid); break;
+                    case 2: g_v_pass<2, 0, FAST, NC>(p.v, P, V, mid_s, ob_s, tid); break;
+                    case 3: g_v_pass<3, 0, FAST, NC>(p.v, P, V, mid_s, ob_s, tid); break;
+                    case 4: g_v_pass<4, 0, FAST, NC>(p.v, P, V, mid_s, ob_s, tid); break;
+                    case 5: g_v_pass<4, 1, FAST, NC>(p.v, P, V, mid_s, ob_s, tid); break;
+                    case 6: g_v_pass<4, 2, FAST, NC>(p.v, P, V, mid_s, ob_s, tid); break;
+                    case 7: g_v_pass<4, 3, FAST, NC>(p.v, P, V, mid_s, ob_s, tid); break;
+                    default: g_v_pass<4, 4, FAST, NC>(p.v, P, V, mid_s, ob_s, tid); break;
                 }
             } else {
-                g_v_pass_bytes<FAST, NC>(p.v, wv, P, mid_s, ob_s, tid);
+                g_v_pass_bytes<FAST, NC>(p.v, wv, P, V, mid_s, ob_s, tid);
             }
-            uint8_t* dst = p.out + cur.f * p.out_frame + P.out_off + (int64_t)band * P.unit_out;
-            if (P.bulk_store) {
-                fence_proxy_async_smem();
-                named_bar_sync(1, NC);                  // output band complete; mid free
-                if (tid == 0) {
-                    bulk_s2g(dst, ob, (uint32_t)P.unit_out);
-                    bulk_commit();
-                    bulk_wait_read<1>();                // the other out slot is free
+            if (P.strips == 1) {
+                uint8_t* dst = p.out + cur.f * p.out_frame + P.out_off + (int64_t)band * P.unit_out;
+                if (P.bulk_store) {
+                    fence_proxy_async_smem();
+                    named_bar_sync(1, NC);              // output band complete; mid free
+                    if (tid == 0) {
+                        bulk_s2g(dst, ob, (uint32_t)P.unit_out);
+                        bulk_commit();
+                        bulk_wait_read<1>();            // the other out slot is free
+                    }
+                } else {
+                    named_bar_sync(1, NC);
+                    for (int x = tid; x < P.unit_out; x += NC) dst[x] = ob[x];
                 }
             } else {
-                named_bar_sync(1, NC);
-                for (int x = tid; x < P.unit_out; x += NC) dst[x] = ob[x];
+                // strip: Qv k output rows of V.wm bytes at column col0 of the plane
+                const int orows = p.v.Q * P.k;
+                uint8_t* dst = p.out + cur.f * p.out_frame + P.out_off + (int64_t)band * orows * P.Wm + V.col0;
+                if (P.bulk_rows && (V.wm & 15) == 0) {
+                    fence_proxy_async_smem();
+                    named_bar_sync(1, NC);
+                    if (tid == 0) {
+                        for (int r = 0; r < orows; ++r)
+                            bulk_s2g(dst + (int64_t)r * P.Wm, ob + (size_t)r * V.wm, (uint32_t)V.wm);
+                        bulk_commit();
+                        bulk_wait_read<1>();
+                    }
+                } else {
+                    named_bar_sync(1, NC);
+                    for (int x = tid; x < V.unit_out; x += NC) {
+                        const int r = g_div_small(x, V.wm, V.wm_rcp);
+                        dst[(int64_t)r * P.Wm + (x - r * V.wm)] = ob[x];
+                    }
+                }
             }
             if (++s == S) { s = 0; phase ^= 1; }
             oslot ^= 1;

@@ -61,9 +61,17 @@ constexpr int64_t kGeneralStageTarget = DS_GEN_STAGE_TARGET;  // K-N1g staged ro
 #endif
 constexpr int64_t kGeneralStageTargetReuse = DS_GEN_STAGE_TARGET_REUSE;  // ... when bands reuse a V halo
 
+// K-N1g per-plane geometry (ds_api.cu general_plane_geom)
+struct GenGeom {
+    int32_t strips = 1, sw = 0, np_last = 0;   // column strips, H repetitions per strip (last: np_last)
+    int32_t k = 0, R = 0, pitch = 0;          // V repetitions per band, staged rows, staged row stride
+    int32_t wm_max = 0;                       // widest mid / output row of a unit (bytes)
+};
+
 // K-N1g launch configuration (any stage spec).
 struct GeneralCfg {
     bool valid = false;
+    GenGeom geom[DS_MAX_PLANES];
     int32_t k[DS_MAX_PLANES] = {0, 0, 0};     // V repetitions per band
     int32_t nb[DS_MAX_PLANES] = {0, 0, 0};    // bands per plane
     int32_t R[DS_MAX_PLANES] = {0, 0, 0};     // staged rows per band (first band of a run)
@@ -95,6 +103,7 @@ struct ds_handle {
     dsi::GeneralCfg general;
     int kernel_pref = DS_KERNEL_AUTO;
     int32_t run_bands = 0;                  // ds_set_run_bands (0 = automatic)
+    int64_t general_target = 0;             // ds_set_general_stage_bytes (0 = default)
     uint32_t* debug_unit_count = nullptr;   // ds_set_debug_counter
     std::atomic<int> last_kernel{DS_KERNEL_AUTO};
     // ds_run_host / ds_run_schedule state (lazily allocated, guarded by host_mu)
@@ -117,7 +126,13 @@ bool ranges_overlap(const void* a, int64_t na, const void* b, int64_t nb);
 int run_device(ds_handle* h, const uint8_t* in, int64_t n, uint8_t* out, cudaStream_t st);
 void free_sched_state(ds_handle* h);
 int make_plan(int32_t W, int32_t H, int32_t channels, const ds_filter_spec* spec_in,
-              ds_filter_spec* spec_out, ds_plan_info* info, int64_t unit_target = kUnitTargetBytes);
+              ds_filter_spec* spec_out, ds_plan_info* info, int64_t unit_target = kUnitTargetBytes,
+              int64_t general_target = 0);
+// K-N1g stage target: explicit (ds_set_general_stage_bytes) or the default for the spec
+inline int64_t general_stage_target(const ds_filter_spec& spec, int64_t explicit_target) {
+    if (explicit_target > 0) return explicit_target;
+    return spec.v.pattern > spec.v.paving ? kGeneralStageTargetReuse : kGeneralStageTarget;
+}
 
 // Device binding: run with the handle's device current, restore after.
 struct DeviceGuard {

@@ -193,6 +193,25 @@ def test_plan_wide_planes_and_smem_limit():
     # slots fits 227 KB -> K-N1 with 1 group per band
     p = ds.ds_plan(7680, 4320, 1)
     assert p.fused_eligible == 1 and p.band_groups[0] == 1
-    # 11520-wide: 92,160 B per group -> 2 x 92,160 + 3 x 17,280 > 227 KB -> not K-N1
+    # 11520-wide: 92,160 B per group -> 2 x 92,160 + 3 x 17,280 > 227 KB -> not K-N1;
+    # K-N1g takes it in column strips (1440 H repetitions -> strips of a multiple of 16)
     p = ds.ds_plan(11520, 2160, 1)
-    assert p.fused_eligible == 0 and p.fused_general_eligible == 0
+    assert p.fused_eligible == 0 and p.fused_general_eligible == 1
+    assert p.general_strips[0] > 1 and p.general_stage_bytes_max <= 40 * 1024
+
+
+def test_plan_general_column_strips():
+    """K-N1g column strips: planes whose k = 1 band exceeds the
+    stage target are split; narrow planes keep whole rows; the stage knob
+    re-plans (ds_set_general_stage_bytes, exercised in test_parity_gpu)."""
+    h = dict(pattern=13, paving=8, origin=-2, weights=[[1, 3, 5, 3, 1]], divisor=13, bias=6)
+    v = dict(pattern=14, paving=9, origin=-2, weights=[[1, 2, 4, 2, 1]], divisor=10, bias=5)
+    spec = ds.make_spec(h=h, v=v)
+    hd = ds.ds_plan(1920, 1080, 3, spec)
+    assert hd.fused_general_eligible == 1 and list(hd.general_strips) == [1, 1, 1]
+    p8k = ds.ds_plan(7680, 4320, 3, spec)                  # was K-N2-only before strips
+    assert p8k.fused_general_eligible == 1
+    assert p8k.general_strips[0] > 1 and p8k.general_stage_bytes_max <= 28 * 1024
+    p4k = ds.ds_plan(3840, 2160, 3, spec)
+    assert p4k.general_strips[0] > 1 and p4k.general_stage_bytes_max <= 28 * 1024
+    assert ds.ds_plan(352, 288, 3, spec).general_strips[0] == 1

@@ -205,6 +205,66 @@ def test_halo_and_origin_spec(W, H, ch, kernel):
         _assert_same(got, want, f"halo, run bands {bands}")
 
 
+@pytest.mark.parametrize("stage_bytes", [1024, 2048, 3000])
+@pytest.mark.parametrize("spec_kind", ["halo", "spec_taps", "negative"])
+def test_general_column_strips(stage_bytes, spec_kind):
+    """K-N1g column strips (ds_set_general_stage_bytes forces them on small
+    frames): strip windows staged from 16-aligned supersets (wrapping the row
+    end under origin != 0), the last strip narrower, runs reusing the V halo
+    within a strip, strip-wise output rows -- against the oracle."""
+    W, H, ch = 352, 288, 3
+    if spec_kind == "halo":
+        hd, vd = _halo_spec()
+    elif spec_kind == "spec_taps":
+        hd = vd = None
+    else:
+        hd = dict(pattern=6, paving=4, origin=-1, weights=[[-1, 3, 3, -1], [0, 0, -1, 3, 3, -1]],
+                  divisor=4, bias=2)
+        vd = dict(pattern=11, paving=6, origin=3, weights=[[1, 2, 1], [0, 0, 0, 1, 2, 1, 0, 0, 0, 0, 4]],
+                  divisor=4, bias=-2)
+        W, H = 352, 288
+    spec = ds.make_spec(h=hd, v=vd, chroma=ds.DS_CHROMA_420)
+    d = ds.Downscaler(W, H, ch, spec=spec)
+    d.set_general_stage_bytes(stage_bytes)
+    assert d.plan.fused_general_eligible == 1 and d.plan.general_strips[0] > 1
+    fr = synth.random_frames(7, 0, 4, W, H, ch, 1)
+    if hd is None:
+        want = oracle.execute_frames(fr, W, H, ch, 1)
+    else:
+        want = oracle.execute_frames(fr, W, H, ch, 1, _oracle_stage(hd), _oracle_stage(vd))
+    for bands in (0, 1, 3):
+        d.set_run_bands(bands)
+        got = _run(d, fr, ds.DS_KERNEL_FUSED_GENERAL)
+        assert d.last_kernel() == ds.DS_KERNEL_FUSED_GENERAL
+        _assert_same(got, want, f"strips {stage_bytes} {spec_kind} run bands {bands}")
+    # misaligned input: strip windows staged by the producer warp (plain loads)
+    buf = torch.zeros(fr.size + 64, dtype=torch.uint8, device="cuda")
+    x = buf[3: 3 + fr.size]
+    x.copy_(torch.from_numpy(fr.ravel()).cuda())
+    y = torch.zeros(want.size, dtype=torch.uint8, device="cuda")
+    d.set_kernel(ds.DS_KERNEL_FUSED_GENERAL)
+    ds.ds_run(d.handle, x.data_ptr(), 4, y.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    _assert_same(y.cpu().numpy().reshape(want.shape), want, f"strips coop {stage_bytes} {spec_kind}")
+    d.set_general_stage_bytes(0)
+    assert list(d.plan.general_strips) == [1, 1, 1]
+    with pytest.raises(ds.DSError):
+        d.set_general_stage_bytes(-1)
+
+
+def test_general_strips_8k_halo():
+    """8K 4:2:0 under the halo spec: whole rows exceed shared memory, so
+    K-N1g runs in column strips (before strips this geometry fell back to
+    K-N2) -- sampled whole frames against the oracle."""
+    W, H = 7680, 4320
+    hd, vd = _halo_spec()
+    d = ds.Downscaler(W, H, 3, spec=ds.make_spec(h=hd, v=vd, chroma=ds.DS_CHROMA_420))
+    assert d.plan.fused_general_eligible == 1 and d.plan.general_strips[0] > 1
+    fr = synth.random_frames(11, 0, 2, W, H, 3, 1)
+    got = _run(d, fr, ds.DS_KERNEL_FUSED_GENERAL)
+    _assert_same(got, oracle.execute_frames(fr, W, H, 3, 1, _oracle_stage(hd), _oracle_stage(vd)), "8K strips")
+
+
 def test_negative_weights_and_other_ratio():
     """Negative lobes (truncation toward zero, clamp) and a 4->2 / 3->1 ratio."""
     hd = dict(pattern=6, paving=4, origin=-1, weights=[[-1, 3, 3, -1], [0, 0, -1, 3, 3, -1]],
