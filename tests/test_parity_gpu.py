@@ -613,9 +613,10 @@ def test_fused_kernel_fuzz():
     assert checked >= 30
 
 
-@pytest.mark.parametrize("kernel,halo", [(FUSED, False), (ds.DS_KERNEL_FUSED_GENERAL, False),
-                                         (ds.DS_KERNEL_FUSED_GENERAL, True)])
-def test_every_unit_processed_exactly_once(kernel, halo):
+@pytest.mark.parametrize("kernel,halo,strips", [(FUSED, False, False), (ds.DS_KERNEL_FUSED_GENERAL, False, False),
+                                                (ds.DS_KERNEL_FUSED_GENERAL, True, False),
+                                                (ds.DS_KERNEL_FUSED_GENERAL, True, True)])
+def test_every_unit_processed_exactly_once(kernel, halo, strips):
     """Debug unit accounting (ds_set_debug_counter): over many frame counts,
     band sizes and ring/CTA tunings (K-N1), and automatic or forced run
     lengths (K-N1g with a V halo), the persistent schedule processes every
@@ -624,6 +625,9 @@ def test_every_unit_processed_exactly_once(kernel, halo):
     spec = ds.make_spec(*_halo_spec(), chroma=ds.DS_CHROMA_420) if halo else None
     d = ds.Downscaler(W, H, 3, spec=spec)
     d.set_kernel(kernel)
+    if strips:                                   # units = (frame, plane, column strip, run)
+        d.set_general_stage_bytes(6000)
+        assert d.plan.general_strips[0] > 1
     L = ds.lib()
     x = ds.generate_frames(40, d.in_frame_bytes, seed=2)
     rng = np.random.default_rng(1)
