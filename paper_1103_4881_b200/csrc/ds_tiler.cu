@@ -16,6 +16,10 @@
 #include "ds.h"
 #include "ds_internal.h"
 
+#ifndef DS_COLS_MINB
+#define DS_COLS_MINB 4
+#endif
+
 namespace {
 
 struct TTiler {
@@ -52,7 +56,8 @@ struct TaskParams {
     int64_t tmult[3];
     // Affine path (host-proved: no tiler index wraps anywhere in the box, so the
     // element offset is A + sum_j a[j] r_j + b[e], all in [0, n) < 2^31)
-    int32_t affine;                    // 0: modulo path; 1: byte loads; 2: word loads + dp4a
+    int32_t affine;                    // 0: modulo path; 1: byte loads; 2: word loads + dp4a;
+                                       // 3: 4 consecutive repetitions (columns) per thread
     uint32_t in_A, out_A;
     uint32_t in_a[4], out_a[4];
     int32_t in_b[DS_MAX_PATTERN], out_b[DS_MAX_OUTPUTS];
@@ -62,6 +67,7 @@ struct TaskParams {
     int32_t fastdiv, fbias;
     uint32_t M, lo;
     int32_t dense;                     // affine == 2 and both tilers are dense row-major runs
+    uint32_t in_live;                  // bit e: pattern element e has a nonzero tap for some output
 };
 
 __device__ __forceinline__ int64_t t_mod(int64_t a, int64_t m) {
@@ -220,7 +226,8 @@ __device__ __forceinline__ void task_affine(const TaskParams& p, uint32_t q) {
     } else {
         int32_t pat[NI];
 #pragma unroll
-        for (int e = 0; e < NI; ++e) pat[e] = e < p.n_in ? (int32_t)__ldg(p.in + bi + p.in_b[e]) : 0;
+        for (int e = 0; e < NI; ++e)
+            pat[e] = (e < p.n_in && ((p.in_live >> e) & 1u)) ? (int32_t)__ldg(p.in + bi + p.in_b[e]) : 0;
 #pragma unroll
         for (int k = 0; k < DS_MAX_OUTPUTS; ++k) {
             if (k < p.n_out) {
@@ -305,7 +312,89 @@ __global__ void __launch_bounds__(256) ds_task_dense_kernel(const __grid_constan
         task_affine<NI, true>(p, q);
 }
 
+template <int NB>
+__device__ __forceinline__ void cols_load(const TaskParams& p, uint32_t q4, uint32_t (&x)[4 * NB], uint32_t& bo) {
+    uint32_t q = 4 * q4, bi = p.in_A;
+    bo = p.out_A;
+#pragma unroll
+    for (int j = 3; j >= 0; --j) {
+        if (j < p.nrep) {
+            const uint32_t qq = fdiv(p.rdiv[j], q);
+            const uint32_t r = q - qq * p.rdiv[j].d;
+            bi += p.in_a[j] * r;
+            bo += p.out_a[j] * r;
+            q = qq;
+        }
+    }
+#pragma unroll
+    for (int e = 0; e < 4 * NB; ++e)           // elements with no nonzero tap are not loaded
+        x[e] = (e < p.n_in && ((p.in_live >> e) & 1u))
+                   ? __ldg(reinterpret_cast<const uint32_t*>(p.in + bi + p.in_b[e])) : 0u;
+}
+template <int NB>
+__device__ __forceinline__ void cols_compute(const TaskParams& p, const uint32_t (&x)[4 * NB], uint32_t bo) {
+    int32_t acc[DS_MAX_OUTPUTS][4];
+    const int32_t b0 = p.fastdiv ? p.fbias : p.bias;
+#pragma unroll
+    for (int k = 0; k < DS_MAX_OUTPUTS; ++k)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[k][c] = b0;
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+        const uint32_t r0 = x[4 * b], r1 = x[4 * b + 1], r2 = x[4 * b + 2], r3 = x[4 * b + 3];
+        const uint32_t ta = __byte_perm(r0, r1, 0x5140), tb = __byte_perm(r2, r3, 0x5140);
+        const uint32_t tc = __byte_perm(r0, r1, 0x7362), td = __byte_perm(r2, r3, 0x7362);
+        const uint32_t c0 = __byte_perm(ta, tb, 0x5410), c1 = __byte_perm(ta, tb, 0x7632),
+                       c2 = __byte_perm(tc, td, 0x5410), c3 = __byte_perm(tc, td, 0x7632);
+#pragma unroll
+        for (int k = 0; k < DS_MAX_OUTPUTS; ++k) {
+            if (k < p.n_out) {
+                const uint32_t wq = p.wp[k][b];
+                acc[k][0] = t_dp4a(c0, wq, acc[k][0]);
+                acc[k][1] = t_dp4a(c1, wq, acc[k][1]);
+                acc[k][2] = t_dp4a(c2, wq, acc[k][2]);
+                acc[k][3] = t_dp4a(c3, wq, acc[k][3]);
+            }
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < DS_MAX_OUTPUTS; ++k) {
+        if (k < p.n_out) {
+            const uint32_t o = (uint32_t)t_out(p, acc[k][0]) | ((uint32_t)t_out(p, acc[k][1]) << 8) |
+                               ((uint32_t)t_out(p, acc[k][2]) << 16) | ((uint32_t)t_out(p, acc[k][3]) << 24);
+            *reinterpret_cast<uint32_t*>(p.out + bo + p.out_b[k]) = o;
+        }
+    }
+}
+
+// Column-vector task (host-proved: the innermost repetition dimension is
+// unit-stride in both arrays with an extent divisible by 4, every other
+// offset 4-byte aligned, s8 taps): a thread takes 4 consecutive repetitions.
+// Pattern element e of the 4 repetitions is one aligned word; 4 elements x 4
+// repetitions are transposed into 4 column words (one dp4a per 4 taps per
+// repetition), and output element k of the 4 repetitions is one word store.
+// This is the shape of the paper's V task (9 rows down a column -> 4 rows).
+// (Two quads per thread step measured slower: 64-99 registers, spills.)
+template <int NB>
+__global__ void __launch_bounds__(256, DS_COLS_MINB) ds_task_cols_kernel(const __grid_constant__ TaskParams p) {
+    const uint32_t quads = (uint32_t)(p.n_reps >> 2);
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t q4 = blockIdx.x * blockDim.x + threadIdx.x; q4 < quads; q4 += stride) {
+        uint32_t x[4 * NB], bo;
+        cols_load<NB>(p, q4, x, bo);
+        cols_compute<NB>(p, x, bo);
+    }
+}
+
 using TaskFn = void (*)(const TaskParams);
+TaskFn cols_fn(int ni) {
+    switch ((ni + 3) / 4) {
+        case 1: return ds_task_cols_kernel<1>;
+        case 2: return ds_task_cols_kernel<2>;
+        case 3: return ds_task_cols_kernel<3>;
+        default: return ds_task_cols_kernel<4>;
+    }
+}
 TaskFn dense_fn(int ni) {
     switch ((ni + 3) / 4) {
         case 1: return ds_task_dense_kernel<4>;
@@ -666,6 +755,9 @@ DS_API int ds_run_task(const uint8_t* in, const ds_tiler* t_in, uint8_t* out, co
             amax = std::max(amax, pos);
         }
         if (words) p.affine = 2;
+        for (int e = 0; e < p.n_in; ++e)
+            for (int k = 0; k < p.n_out; ++k)
+                if (body->weight[k][e] != 0) p.in_live |= 1u << e;
         // dense: both tilers are row-major runs over the repetition index
         bool dense = words && policy == DS_TOPO_FLAT &&
                      ((reinterpret_cast<uintptr_t>(in) + p.in_A) & 15) == 0 &&
@@ -677,6 +769,21 @@ DS_API int ds_run_task(const uint8_t* in, const ds_tiler* t_in, uint8_t* out, co
         }
         for (int k = 0; k < p.n_out; ++k) dense = dense && p.out_b[k] == k;
         p.dense = dense ? 1 : 0;
+        // column vectors: innermost repetition dim unit-stride in both arrays
+        // (extent % 4 == 0), all other offsets and both pointers 4-aligned, s8 taps
+        if (!dense && policy == DS_TOPO_FLAT) {
+            const int jl = nrep - 1;
+            bool cols = p.in_a[jl] == 1 && p.out_a[jl] == 1 && rep_shape[jl] % 4 == 0 &&
+                        p.in_A % 4 == 0 && p.out_A % 4 == 0 &&
+                        (reinterpret_cast<uintptr_t>(in) & 3) == 0 && (reinterpret_cast<uintptr_t>(out) & 3) == 0;
+            for (int j = 0; j < jl; ++j) cols = cols && p.in_a[j] % 4 == 0 && p.out_a[j] % 4 == 0;
+            for (int e = 0; e < p.n_in; ++e) cols = cols && (p.in_b[e] & 3) == 0;
+            for (int k = 0; k < p.n_out; ++k) cols = cols && (p.out_b[k] & 3) == 0;
+            for (int k = 0; k < p.n_out; ++k)
+                for (int e = 0; e < p.n_in; ++e)
+                    cols = cols && body->weight[k][e] >= -128 && body->weight[k][e] <= 127;
+            if (cols) p.affine = 3;
+        }
         // exact multiply-high division (same derivation as K-N1g's FASTDIV)
         const uint64_t D = (uint64_t)body->divisor;
         if (D == 1) {
@@ -688,7 +795,9 @@ DS_API int ds_run_task(const uint8_t* in, const ds_tiler* t_in, uint8_t* out, co
             }
         }
     }
-    const TaskFn fn = p.dense ? dense_fn(p.n_in) : p.affine ? affine_fn(p.n_in, p.affine == 2) : ds_task_kernel;
+    const TaskFn fn = p.dense ? dense_fn(p.n_in)
+                      : p.affine == 3 ? cols_fn(p.n_in)
+                      : p.affine ? affine_fn(p.n_in, p.affine == 2) : ds_task_kernel;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     if (policy == DS_TOPO_SPEC) {
         ds_topology topo;
@@ -706,7 +815,8 @@ DS_API int ds_run_task(const uint8_t* in, const ds_tiler* t_in, uint8_t* out, co
         }
         fn<<<grid, block, 0, st>>>(p);
     } else {
-        const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((p.n_reps + 255) / 256, (int64_t)sms * 16));
+        const int64_t items = p.affine == 3 ? p.n_reps / 4 : p.n_reps;      // column quads
+        const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((items + 255) / 256, (int64_t)sms * 16));
         fn<<<(unsigned)blocks, 256, 0, st>>>(p);
     }
     return cudaGetLastError() == cudaSuccess ? DS_OK : DS_ECUDA;

@@ -264,3 +264,44 @@ def test_run_task_affine_words(P):
                         ds.make_body(w, D, B, n_in=P))
             torch.cuda.synchronize()
             assert np.array_equal(y.cpu().numpy(), want), (origin, D, B)
+
+
+@pytest.mark.gpu
+def test_run_task_affine_columns():
+    """Column-vector path: the innermost repetition dim is unit-stride in both
+    arrays (extent % 4 == 0) and the pattern runs down a column, as in the
+    paper's V task; 4 repetitions per thread, 4x4 byte transposes + dp4a."""
+    rng = np.random.default_rng(99)
+    for trial in range(40):
+        P = int(rng.integers(1, 17))
+        Q = int(rng.integers(1, 9))
+        C = 4 * int(rng.integers(1, 40))                 # columns = innermost repetitions
+        G = int(rng.integers(1, 12))                     # row groups
+        S = int(rng.integers(1, P + 2))                  # row paving (overlapping windows when S < P)
+        step = int(rng.choice([1, 2, -1]))               # pattern step down the column
+        Hin = S * (G - 1) + abs(step) * (P - 1) + 1 + int(rng.integers(0, 5))
+        o = abs(step) * (P - 1) if step < 0 else 0
+        o += int(rng.integers(0, Hin - (S * (G - 1) + abs(step) * (P - 1))))
+        three = trial % 4 == 0
+        if three:
+            F = int(rng.integers(1, 4))
+            in_shape, out_shape = (F, Hin, C), (F, G * Q, C)
+            tin = (in_shape, (0, o, 0), [[1, 0, 0], [0, S, 0], [0, 0, 1]], [[0], [step], [0]], [P])
+            tout = (out_shape, (0, 0, 0), [[1, 0, 0], [0, Q, 0], [0, 0, 1]], [[0], [1], [0]], [Q])
+            reps = [F, G, C]
+        else:
+            in_shape, out_shape = (Hin, C), (G * Q, C)
+            tin = (in_shape, (o, 0), [[S, 0], [0, 1]], [[step], [0]], [P])
+            tout = (out_shape, (0, 0), [[Q, 0], [0, 1]], [[1], [0]], [Q])
+            reps = [G, C]
+        w = [[int(x) for x in rng.integers(-128, 128, P)] for _ in range(Q)]
+        D = int(rng.choice([1, 3, 8, 999983]))
+        B = int(rng.integers(-500, 500))
+        a = rng.integers(0, 256, in_shape).astype(np.uint8)
+        want = oracle.run_task(a, oracle.make_tiler(*tin), out_shape, oracle.make_tiler(*tout), reps,
+                               oracle.make_stage(P, P, 0, w, D, B))
+        y = torch.zeros(out_shape, dtype=torch.uint8, device="cuda")
+        ds.run_task(torch.from_numpy(a).cuda(), ds.make_tiler(*tin), y, ds.make_tiler(*tout), reps,
+                    ds.make_body(w, D, B, n_in=P))
+        torch.cuda.synchronize()
+        assert np.array_equal(y.cpu().numpy(), want), (trial, P, Q, C, G, S, step, D)

@@ -87,14 +87,45 @@ def generic_task(n=300, W=1920, H=1080):
     return res
 
 
+def generic_vtask(n=300, W=1920, H=1080):
+    """The paper's V task over n HD luma Mid planes (H rows x 3W/8) as ONE 3-D
+    Array-OL task (repetition (n, H/9, 3W/8); input pattern 9 rows down a
+    column, output pattern 4 rows), through ds_run_task vs K-N3's V kernel."""
+    Wm, Ho = W // 8 * 3, H // 9 * 4
+    mid = ds.generate_frames(n, H * Wm, seed=2).view(n, H, Wm)
+    out = torch.empty((n, Ho, Wm), dtype=torch.uint8, device="cuda")
+    spec = ds.ds_default_spec()
+    vw = [[spec.v.weight[k][i] for i in range(9)] for k in range(4)]
+    tin = ds.make_tiler((n, H, Wm), (0, 0, 0), [[1, 0, 0], [0, 9, 0], [0, 0, 1]], [[0], [1], [0]], [9])
+    tout = ds.make_tiler((n, Ho, Wm), (0, 0, 0), [[1, 0, 0], [0, 4, 0], [0, 0, 1]], [[0], [1], [0]], [4])
+    body = ds.make_body(vw, 8, 4, n_in=9)
+    res = {}
+    for pol, name in ((ds.DS_TOPO_FLAT, "flat"), (ds.DS_TOPO_SPEC, "spec_topology")):
+        res[f"ds_run_task_{name}_ms"] = timed(lambda: ds.run_task(mid, tin, out, tout, [n, H // 9, Wm], body,
+                                                                  policy=pol), 5)
+    ref = out.clone()
+    d = ds.Downscaler(W, H, 1)
+    out2 = torch.empty_like(out)
+    res["vtask_kernel_ms"] = timed(lambda: d.vtask(mid.view(n, -1), out2.view(n, -1)), 20)
+    res["bit_identical"] = bool(torch.equal(ref, out2))
+    res["bytes"] = n * (H * Wm * 8 // 9 + Ho * Wm)
+    res["ds_run_task_flat_gbs"] = res["bytes"] / res["ds_run_task_flat_ms"] / 1e6
+    res["vtask_kernel_gbs"] = res["bytes"] / res["vtask_kernel_ms"] / 1e6
+    return res
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default="gpurun_out/general_perf.json")
     ap.add_argument("--quick", action="store_true", help="K-N1g only, one line per spec")
     ap.add_argument("--run-bands", type=int, default=0, help="K-N1g bands per run (0 = automatic)")
+    ap.add_argument("--tasks", action="store_true", help="general task executor only (H and V tasks)")
     a = ap.parse_args()
     torch.cuda.set_device(0)
     halo = ds.make_spec(h=HALO_H, v=HALO_V)
+    if a.tasks:
+        print(json.dumps({"h": generic_task(), "v": generic_vtask()}))
+        return
     if a.quick:
         h = run(1920, 1080, 300, halo, [ds.DS_KERNEL_FUSED_GENERAL], steps=50, run_bands=a.run_bands)
         t = run(1920, 1080, 300, None, [ds.DS_KERNEL_FUSED_GENERAL], steps=50)
@@ -109,6 +140,7 @@ def main():
         "hd420_300_spec_taps": run(1920, 1080, 300, None,
                                    [ds.DS_KERNEL_FUSED, ds.DS_KERNEL_FUSED_GENERAL]),
         "generic_task_yhfk_300_hd_luma": generic_task(),
+        "generic_task_v_300_hd_luma": generic_vtask(),
     }
     os.makedirs(os.path.dirname(a.out) or ".", exist_ok=True)
     json.dump(out, open(a.out, "w"), indent=1)
