@@ -494,7 +494,6 @@ int configure_general(ds_handle* h) {
     if (!pi.fused_general_eligible) { h->general = c; return DS_OK; }
     const ds_filter_spec& sp = h->spec;
     int64_t smax = 0, mmax = 0, omax = 0;
-    int32_t upf = 0;
     for (int p = 0; p < pi.n_planes; ++p) {
         c.geom[p] = general_plane_geom(sp, pi.in_w[p], pi.in_h[p], general_stage_target(sp, h->general_target));
         c.k[p] = c.geom[p].k;
@@ -503,9 +502,7 @@ int configure_general(ds_handle* h) {
         smax = std::max<int64_t>(smax, (int64_t)c.R[p] * c.geom[p].pitch);
         mmax = std::max<int64_t>(mmax, (int64_t)(c.R[p] + 3) * c.geom[p].wm_max);   // V reads 4-row blocks
         omax = std::max<int64_t>(omax, (int64_t)sp.v.outputs * c.k[p] * c.geom[p].wm_max);
-        upf += c.geom[p].strips * c.nb[p];
     }
-    c.upf = upf;
     c.stage_stride = (int32_t)round_up(smax, 128);
     c.mid_stride = (int32_t)round_up(mmax, 128);
     c.ovl = std::max(0, sp.v.pattern - sp.v.paving);

@@ -2,24 +2,32 @@
 // (SURVEY f3): halos (pattern P > paving S) with toroidal wrap,
 // origin != 0, other ratios, negative lobes, any divisor.
 //
-// Same persistent, warp-specialised TMA pipeline as K-N1.  A work unit is
-// (frame, plane, band of k V repetitions).  Those repetitions read input rows
-// (o_v + S_v g + i) mod H for g in the band, i < P_v: R = S_v (k-1) + P_v
-// consecutive rows modulo H, i.e. the band plus its halo (the bottom halo
-// wraps to the plane's first rows).  The producer stages each row at a pitch
-// of round_up(W, 16) + 32 bytes: the row, then a 32-byte pad holding its first
-// bytes again (row[j mod W]), so an H window that wraps past the row end
-// reads straight on into the pad -- no wrap test, no divergent slow
-// path.  A plane too wide for the stage budget is split into column strips of
-// S_w H repetitions (a multiple of 16): a unit then stages, per row, only its
+// Same persistent, warp-specialised TMA pipeline as K-N1.  A band is k V
+// repetitions; they read input rows (o_v + S_v g + i) mod H for g in the
+// band, i < P_v: R = S_v (k-1) + P_v consecutive rows modulo H, i.e. the band
+// plus its halo (the bottom halo wraps to the plane's first rows).  A work
+// unit is (frame, plane, column strip, run of L consecutive bands): with a V
+// halo (P_v > S_v) each band after the first of a run copies the P_v - S_v
+// intermediate rows it shares with the previous band (two mid buffers) and
+// stages and H-filters only its S_v k new rows.
+//
+// Staging: whole rows at a pitch of round_up(W, 16) + 32 bytes -- the row,
+// then a 32-byte pad holding its first bytes again (row[j mod W]), so an H
+// window that wraps past the row end reads straight on into the pad.
+// A plane too wide for the stage budget is split into column strips of S_w H
+// repetitions (a multiple of 16): a unit then stages, per row, only its
 // strip's input window (o_h + S_h a, width S_h (S_w - 1) + P_h, modulo W) as
 // the 16-byte-aligned superset (two bulk copies when it wraps the row end)
-// and stores its output rows strip-wise.  Consumers run the H task on every staged row into a u8 intermediate
-// in shared memory, then the V task from it, stage the output band in
-// shared memory and bulk-store it.  Divisions by runtime values are exact
+// and stores its output rows strip-wise.  Unaligned planes are staged by the
+// producer warp with plain loads.
+//
+// Consumers run the H task on every newly staged row into a u8 intermediate
+// in shared memory -- column-fixed threads, one dp4a per 4 taps --
+// then the V task from it (4x4 byte transposes + dp4a), stage the output band
+// in shared memory and bulk-store it.  Divisions by runtime values are exact
 // (truncation toward zero, then clamp): one multiply-high when the host
-// proves the accumulator range allows it (FASTDIV), else a reciprocal plus one
-// correction step.
+// proves the accumulator range allows it, else a reciprocal plus one
+// correction step (g_out modes 0-2).
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>

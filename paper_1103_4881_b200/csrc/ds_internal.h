@@ -77,7 +77,6 @@ struct GeneralCfg {
     int32_t R[DS_MAX_PLANES] = {0, 0, 0};     // staged rows per band (first band of a run)
     int32_t ovl = 0;                          // Pv - Sv > 0: halo rows shared by consecutive bands
     int32_t mid_alt = 0;                      // second mid buffer offset (0: one buffer)
-    int32_t upf = 0;
     int32_t stage_stride = 0, mid_stride = 0, out_stride = 0;
     int stages = 2, ncw = 8;
     int fast = 0;                             // division mode (ds_general.cuh g_out): 0, 1 or 2
