@@ -45,10 +45,11 @@ namespace ds {
 
 struct GenPlane {
     int64_t in_off, out_off;
-    int32_t W, H, Wm;          // input row bytes, rows, mid/output row bytes
-    int32_t pitch;             // staged row stride: round_up(W, 16) + 32 (row, then wrap pad)
-    int32_t k;                 // V repetitions per unit
-    int32_t R;                 // staged rows per unit = Sv (k-1) + Pv
+    int32_t W, H, Wm;          // input row bytes, rows, output row bytes (= mid row bytes, whole rows)
+    int32_t pitch;             // staged row stride: round_up(W, 16) + 32 (row, then wrap pad),
+                               // or a strip window's stride (strips > 1)
+    int32_t k;                 // V repetitions per band
+    int32_t R;                 // staged rows of a run's first band = Sv (k-1) + Pv
     int32_t np;                // H repetitions per row = W / Sh
     uint32_t np_rcp;           // ceil(2^32 / np) (np > 1)
     uint32_t wm_rcp;           // ceil(2^32 / Wm) (Wm > 1)
