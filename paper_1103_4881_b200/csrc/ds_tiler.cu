@@ -109,26 +109,50 @@ __device__ __forceinline__ uint32_t fmod32(const FastDiv& f, uint32_t n) { retur
 // 32-bit path: origin + paving.r stays < 2^31 (host bound), one modulo per
 // dim.  Loops are fully unrolled over the maximum extents with predicates so
 // the pattern and index arrays stay in registers.
+// base[] is already reduced mod shape (t_base32) and foff < shape, so each
+// element index needs one conditional subtraction, not a modulo.
 __device__ __forceinline__ uint32_t t_lin32(const TTiler& t, const FastDiv* sd, const uint32_t* base,
                                             int f) {
     uint32_t off = 0;
 #pragma unroll
-    for (int d = 0; d < 4; ++d)
-        if (d < t.ndim) off += fmod32(sd[d], base[d] + (uint32_t)t.foff[f][d]) * (uint32_t)t.stride[d];
+    for (int d = 0; d < 4; ++d) {
+        if (d < t.ndim) {
+            uint32_t i = base[d] + (uint32_t)t.foff[f][d];
+            if (i >= sd[d].d) i -= sd[d].d;
+            off += i * (uint32_t)t.stride[d];
+        }
+    }
     return off;
 }
 
-__device__ __forceinline__ void t_base32(const TTiler& t, int nrep, const uint32_t* r, uint32_t* base) {
+// (origin + paving.r) mod shape per array dim: one modulo per dim per repetition
+__device__ __forceinline__ void t_base32(const TTiler& t, const FastDiv* sd, int nrep, const uint32_t* r,
+                                         uint32_t* base) {
 #pragma unroll
     for (int d = 0; d < 4; ++d) {
         uint32_t v = (uint32_t)t.origin[d];
 #pragma unroll
         for (int j = 0; j < 4; ++j)
             if (j < nrep) v += (uint32_t)t.pav[d][j] * r[j];
-        base[d] = v;
+        base[d] = d < t.ndim ? fmod32(sd[d], v) : 0u;
     }
 }
 
+// d = c + sum_i a.u8[i] * b.s8[i]
+__device__ __forceinline__ int32_t t_dp4a(uint32_t a, uint32_t b, int32_t c) {
+    int32_t d;
+    asm("dp4a.u32.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+__device__ __forceinline__ uint8_t t_out(const TaskParams& p, int32_t acc) {
+    if (p.fastdiv) return (uint8_t)min(__umulhi((uint32_t)max(acc, (int32_t)p.lo), p.M), 255u);
+    int32_t v = acc / p.divisor;                          // truncation toward zero (S:577)
+    return (uint8_t)(v < 0 ? 0 : (v > 255 ? 255 : v));
+}
+
+// Modulo path, 32-bit: NI = n_in rounded up to 4 (the MAC loop runs over NI
+// taps, not DS_MAX_PATTERN); exact multiply-high division when host-proved.
+template <int NI>
 __device__ __forceinline__ void task_one32(const TaskParams& p, uint32_t q) {
     uint32_t r[4] = {0, 0, 0, 0};
 #pragma unroll
@@ -140,28 +164,28 @@ __device__ __forceinline__ void task_one32(const TaskParams& p, uint32_t q) {
         }
     }
     uint32_t base[4];
-    t_base32(p.tin, p.nrep, r, base);
-    uint32_t pat[DS_MAX_PATTERN];
+    t_base32(p.tin, p.sdiv_in, p.nrep, r, base);
+    int32_t pat[NI];
 #pragma unroll
-    for (int f = 0; f < DS_MAX_PATTERN; ++f)
-        pat[f] = f < p.n_in ? (uint32_t)__ldg(p.in + t_lin32(p.tin, p.sdiv_in, base, f)) : 0u;
-    t_base32(p.tout, p.nrep, r, base);
+    for (int f = 0; f < NI; ++f)
+        pat[f] = (f < p.n_in && ((p.in_live >> f) & 1u))
+                     ? (int32_t)__ldg(p.in + t_lin32(p.tin, p.sdiv_in, base, f)) : 0;
+    t_base32(p.tout, p.sdiv_out, p.nrep, r, base);
 #pragma unroll
     for (int k = 0; k < DS_MAX_OUTPUTS; ++k) {
         if (k < p.n_out) {
-            int32_t acc = p.bias;
+            int32_t acc = p.fastdiv ? p.fbias : p.bias;
 #pragma unroll
-            for (int f = 0; f < DS_MAX_PATTERN; ++f) acc += p.w[k][f] * (int32_t)pat[f];
-            int32_t v = acc / p.divisor;                  // truncation toward zero
-            v = v < 0 ? 0 : (v > 255 ? 255 : v);
-            p.out[t_lin32(p.tout, p.sdiv_out, base, k)] = (uint8_t)v;
+            for (int f = 0; f < NI; ++f) acc += p.w[k][f] * pat[f];
+            p.out[t_lin32(p.tout, p.sdiv_out, base, k)] = t_out(p, acc);
         }
     }
 }
 
+template <int NI>
 __device__ __forceinline__ void task_one(const TaskParams& p, int64_t q) {
     if (p.fast32) {
-        task_one32(p, (uint32_t)q);
+        task_one32<NI>(p, (uint32_t)q);
         return;
     }
     int64_t r[4] = {0, 0, 0, 0}, base[4];
@@ -177,18 +201,6 @@ __device__ __forceinline__ void task_one(const TaskParams& p, int64_t q) {
         v = v < 0 ? 0 : (v > 255 ? 255 : v);
         p.out[t_lin(p.tout, base, k)] = (uint8_t)v;
     }
-}
-
-// d = c + sum_i a.u8[i] * b.s8[i]
-__device__ __forceinline__ int32_t t_dp4a(uint32_t a, uint32_t b, int32_t c) {
-    int32_t d;
-    asm("dp4a.u32.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
-    return d;
-}
-__device__ __forceinline__ uint8_t t_out(const TaskParams& p, int32_t acc) {
-    if (p.fastdiv) return (uint8_t)min(__umulhi((uint32_t)max(acc, (int32_t)p.lo), p.M), 255u);
-    int32_t v = acc / p.divisor;                          // truncation toward zero (S:577)
-    return (uint8_t)(v < 0 ? 0 : (v > 255 ? 255 : v));
 }
 
 // One elementary task on the affine path (same result as task_one: the
@@ -412,6 +424,7 @@ TaskFn affine_fn(int ni, bool words) {
     }
 }
 
+template <int NI>
 __global__ void __launch_bounds__(256, 1) ds_task_kernel(const __grid_constant__ TaskParams p) {
     if (p.policy == DS_TOPO_SPEC) {
         // NDRange work-item = one elementary task; guarded padding
@@ -427,12 +440,21 @@ __global__ void __launch_bounds__(256, 1) ds_task_kernel(const __grid_constant__
             if (c[d] >= p.tmult[d]) return;               // guard
             q = q * p.tmult[d] + c[d];
         }
-        task_one(p, q);
+        task_one<NI>(p, q);
         return;
     }
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < p.n_reps; q += stride)
-        task_one(p, q);
+        task_one<NI>(p, q);
+}
+
+TaskFn modulo_fn(int ni) {
+    switch ((ni + 3) / 4) {
+        case 1: return ds_task_kernel<4>;
+        case 2: return ds_task_kernel<8>;
+        case 3: return ds_task_kernel<12>;
+        default: return ds_task_kernel<16>;
+    }
 }
 
 __global__ void __launch_bounds__(256) ds_cover_count_kernel(const __grid_constant__ TaskParams p,
@@ -736,28 +758,40 @@ DS_API int ds_run_task(const uint8_t* in, const ds_tiler* t_in, uint8_t* out, co
     p.divisor = body->divisor;
     p.bias = body->bias;
     std::memcpy(p.w, body->weight, sizeof p.w);
+    // taps: s8-packed copies, live pattern elements, and the exact
+    // multiply-high division (same derivation as K-N1g's FASTDIV) -- all paths
+    bool s8 = true;
+    int64_t amax = 0;
+    for (int k = 0; k < p.n_out; ++k) {
+        int64_t pos = body->bias;
+        for (int e = 0; e < p.n_in; ++e) {
+            const int32_t w = body->weight[k][e];
+            if (w < -128 || w > 127) s8 = false;
+            if (w > 0) pos += 255LL * w;
+            if (w != 0) p.in_live |= 1u << e;
+            p.wp[k][e / 4] |= (uint32_t)(uint8_t)(int8_t)(w < -128 || w > 127 ? 0 : w) << (8 * (e % 4));
+        }
+        amax = std::max(amax, pos);
+    }
+    {
+        const uint64_t D = (uint64_t)body->divisor;
+        if (D == 1) {
+            if (amax < 0x7fffffffLL) { p.fastdiv = 1; p.M = 0xffffffffu; p.lo = 1; p.fbias = body->bias + 1; }
+        } else {
+            const uint64_t M = ((1ULL << 32) + D - 1) / D, e = M * D - (1ULL << 32);
+            if ((unsigned __int128)(uint64_t)amax * e < ((unsigned __int128)1 << 32)) {
+                p.fastdiv = 1; p.M = (uint32_t)M; p.lo = 0; p.fbias = body->bias;
+            }
+        }
+    }
     // affine path: both tilers wrap-free, 32-bit offsets and repetition index
     if (p.n_reps < (1LL << 31) && affine_tiler(*t_in, nrep, rep_shape, &p.in_A, p.in_a, p.in_b, DS_MAX_PATTERN) &&
         affine_tiler(*t_out, nrep, rep_shape, &p.out_A, p.out_a, p.out_b, DS_MAX_OUTPUTS)) {
         p.affine = 1;
-        bool words = p.n_in % 4 == 0 && (reinterpret_cast<uintptr_t>(in) & 3) == 0 && p.in_A % 4 == 0;
+        bool words = s8 && p.n_in % 4 == 0 && (reinterpret_cast<uintptr_t>(in) & 3) == 0 && p.in_A % 4 == 0;
         for (int j = 0; j < nrep; ++j) words = words && p.in_a[j] % 4 == 0;
         for (int e = 0; e < p.n_in; ++e) words = words && p.in_b[e] == e;
-        int64_t amax = 0;
-        for (int k = 0; k < p.n_out; ++k) {
-            int64_t pos = body->bias;
-            for (int e = 0; e < p.n_in; ++e) {
-                const int32_t w = body->weight[k][e];
-                if (w < -128 || w > 127) words = false;
-                if (w > 0) pos += 255LL * w;
-                p.wp[k][e / 4] |= (uint32_t)(uint8_t)(int8_t)(w < -128 || w > 127 ? 0 : w) << (8 * (e % 4));
-            }
-            amax = std::max(amax, pos);
-        }
         if (words) p.affine = 2;
-        for (int e = 0; e < p.n_in; ++e)
-            for (int k = 0; k < p.n_out; ++k)
-                if (body->weight[k][e] != 0) p.in_live |= 1u << e;
         // dense: both tilers are row-major runs over the repetition index
         bool dense = words && policy == DS_TOPO_FLAT &&
                      ((reinterpret_cast<uintptr_t>(in) + p.in_A) & 15) == 0 &&
@@ -771,7 +805,7 @@ DS_API int ds_run_task(const uint8_t* in, const ds_tiler* t_in, uint8_t* out, co
         p.dense = dense ? 1 : 0;
         // column vectors: innermost repetition dim unit-stride in both arrays
         // (extent % 4 == 0), all other offsets and both pointers 4-aligned, s8 taps
-        if (!dense && policy == DS_TOPO_FLAT) {
+        if (!dense && policy == DS_TOPO_FLAT && s8) {
             const int jl = nrep - 1;
             bool cols = p.in_a[jl] == 1 && p.out_a[jl] == 1 && rep_shape[jl] % 4 == 0 &&
                         p.in_A % 4 == 0 && p.out_A % 4 == 0 &&
@@ -779,25 +813,12 @@ DS_API int ds_run_task(const uint8_t* in, const ds_tiler* t_in, uint8_t* out, co
             for (int j = 0; j < jl; ++j) cols = cols && p.in_a[j] % 4 == 0 && p.out_a[j] % 4 == 0;
             for (int e = 0; e < p.n_in; ++e) cols = cols && (p.in_b[e] & 3) == 0;
             for (int k = 0; k < p.n_out; ++k) cols = cols && (p.out_b[k] & 3) == 0;
-            for (int k = 0; k < p.n_out; ++k)
-                for (int e = 0; e < p.n_in; ++e)
-                    cols = cols && body->weight[k][e] >= -128 && body->weight[k][e] <= 127;
             if (cols) p.affine = 3;
-        }
-        // exact multiply-high division (same derivation as K-N1g's FASTDIV)
-        const uint64_t D = (uint64_t)body->divisor;
-        if (D == 1) {
-            if (amax < 0x7fffffffLL) { p.fastdiv = 1; p.M = 0xffffffffu; p.lo = 1; p.fbias = body->bias + 1; }
-        } else {
-            const uint64_t M = ((1ULL << 32) + D - 1) / D, e = M * D - (1ULL << 32);
-            if ((unsigned __int128)(uint64_t)amax * e < ((unsigned __int128)1 << 32)) {
-                p.fastdiv = 1; p.M = (uint32_t)M; p.lo = 0; p.fbias = body->bias;
-            }
         }
     }
     const TaskFn fn = p.dense ? dense_fn(p.n_in)
                       : p.affine == 3 ? cols_fn(p.n_in)
-                      : p.affine ? affine_fn(p.n_in, p.affine == 2) : ds_task_kernel;
+                      : p.affine ? affine_fn(p.n_in, p.affine == 2) : modulo_fn(p.n_in);
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     if (policy == DS_TOPO_SPEC) {
         ds_topology topo;

@@ -78,6 +78,11 @@ def generic_task(n=300, W=1920, H=1080):
     for pol, name in ((ds.DS_TOPO_FLAT, "flat"), (ds.DS_TOPO_SPEC, "spec_topology")):
         ms = timed(lambda: ds.run_task(x, tin, mid, tout, [n, H, W // 8], body, policy=pol), 5)
         res[f"ds_run_task_{name}_ms"] = ms
+    # the same task with the input origin shifted by 3 columns: windows wrap at
+    # the row end, so the tiler is not affine -> the modulo path
+    tin_w = ds.make_tiler((n, H, W), (0, 0, 3), [[1, 0, 0], [0, 1, 0], [0, 0, 8]], [[0], [0], [1]], [8])
+    res["ds_run_task_wrapping_origin_ms"] = timed(
+        lambda: ds.run_task(x, tin_w, mid, tout, [n, H, W // 8], body), 5)
     d = ds.Downscaler(W, H, 1)
     res["htask_kernel_ms"] = timed(lambda: d.htask(x, mid2), 20)
     res["bit_identical"] = bool(torch.equal(mid, mid2))
