@@ -172,7 +172,8 @@ int make_plan(int32_t W, int32_t H, int32_t channels, const ds_filter_spec* spec
     if (any_narrow && pi.in_frame_bytes % 16 != 0) fused = false;
     if (fused) {
         // staged bytes per 9-row group: 8 live rows, or all 9 for narrow planes
-        auto per_group = [&](int p) { return (pi.in_w[p] % 16 == 0 ? 8LL : 9LL) * pi.in_w[p]; };
+        // and for short aligned rows staged as whole bands (k1_whole_band)
+        auto per_group = [&](int p) { return (k1_whole_band(pi.in_w[p]) || pi.in_w[p] % 16 ? 9LL : 8LL) * pi.in_w[p]; };
         // shrink the band target until a 2-deep ring fits one CTA's shared
         // memory (a caller's large ds_set_band_bytes never loses K-N1)
         const int G0 = pi.in_h[0] / 9;
@@ -258,12 +259,27 @@ int max_tasks(const ds_plan_info& pi) {
     return t;
 }
 
+// plane kinds of a K-N1 plan: bit 0 wide, bit 1 whole-band, bit 2 narrow
+int plan_modes(const ds_plan_info& pi) {
+    int m = 0;
+    for (int p = 0; p < pi.n_planes; ++p)
+        m |= pi.in_w[p] % 16 != 0 ? 4 : k1_whole_band(pi.in_w[p]) ? 2 : 1;
+    return m;
+}
+
+// Consumer warps for K-N1: fewer than 8 only for tiny planes.  (More than 8
+// was measured: no gain on CIF / SD at 11-12 warps, and 16 warps were slower
+// on HD, so a unit's 2 k chunks tasks are spread over 256 threads in rounds.)
+int pick_ncw(const ds_plan_info& pi) {
+    const int w = (max_tasks(pi) + 31) / 32;
+    return w <= 1 ? 1 : w <= 2 ? 2 : w <= 4 ? 4 : 8;
+}
+
 FusedCfg make_cfg(const ds_plan_info& pi) {
     FusedCfg c;
     c.plan = pi;
     if (!pi.fused_eligible) return c;
-    const int w = (max_tasks(pi) + 31) / 32;
-    c.ncw = w <= 1 ? 1 : w <= 2 ? 2 : w <= 4 ? 4 : 8;
+    c.ncw = pick_ncw(pi);
     c.stage_stride = (int32_t)round_up(pi.unit_in_bytes_max, 128);
     c.out_stride = (int32_t)round_up(pi.unit_out_bytes_max, 128);
     c.stages = (int)std::max<int64_t>(2, std::min<int64_t>(8, (kInFlightTarget + c.stage_stride / 2) /
@@ -291,12 +307,24 @@ int configure_fused(ds_handle* h) {
 
 using FusedFn = void (*)(const ds::FusedParams);
 
-FusedFn fused_fn(int ncw) {
+// Instantiations: 8 consumer warps for every combination of plane kinds a
+// plan can have (bit 0 wide, 1 whole-band, 2 narrow); tiny plans (1/2/4
+// warps) get the all-kinds kernel.
+FusedFn fused_fn(int ncw, int modes) {
     switch (ncw) {
-        case 1: return ds::ds_fused_band_kernel<1>;
-        case 2: return ds::ds_fused_band_kernel<2>;
-        case 4: return ds::ds_fused_band_kernel<4>;
-        default: return ds::ds_fused_band_kernel<8>;
+        case 1: return ds::ds_fused_band_kernel<1, 7>;
+        case 2: return ds::ds_fused_band_kernel<2, 7>;
+        case 4: return ds::ds_fused_band_kernel<4, 7>;
+        default: break;
+    }
+    switch (modes) {
+        case 1: return ds::ds_fused_band_kernel<8, 1>;
+        case 2: return ds::ds_fused_band_kernel<8, 2>;
+        case 3: return ds::ds_fused_band_kernel<8, 3>;
+        case 4: return ds::ds_fused_band_kernel<8, 4>;
+        case 5: return ds::ds_fused_band_kernel<8, 5>;
+        case 6: return ds::ds_fused_band_kernel<8, 6>;
+        default: return ds::ds_fused_band_kernel<8, 7>;
     }
 }
 
@@ -320,7 +348,7 @@ int prepare_cfg(FusedCfg& c) {
     const int stages = fit_stages(c, c.stages);
     const int sm = (int)fused_smem_bytes(stages, c.stage_stride, c.out_stride);
     const int threads = (c.ncw + 1) * 32;
-    FusedFn fn = fused_fn(c.ncw);
+    FusedFn fn = fused_fn(c.ncw, plan_modes(c.plan));
     // the attribute belongs to the kernel function (shared by every handle and
     // configuration using this instantiation): always the opt-in maximum
     if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit) !=
@@ -377,11 +405,12 @@ int launch_fused(ds_handle* h, const uint8_t* in, int64_t n, uint8_t* out, cudaS
         P.Wout = pi.out_w[q];
         P.k = pi.band_groups[q];
         P.narrow = (P.W % 16 != 0) ? 1 : 0;
+        P.whole = k1_whole_band(P.W) ? 1 : 0;
         P.chunks = (P.W + 15) / 16;
         P.tasks = 2 * P.k * P.chunks;
         P.chunks_rcp = P.chunks > 1 ? (uint32_t)((0x100000000ULL + P.chunks - 1) / P.chunks) : 0u;
         P.unit_start = start;
-        P.unit_in = (P.narrow ? 9 : 8) * P.k * P.W;
+        P.unit_in = (P.narrow || P.whole ? 9 : 8) * P.k * P.W;
         P.unit_out = 4 * P.k * P.Wout;
         P.bulk_store = (out_al && P.out_off % 16 == 0 && P.unit_out % 16 == 0) ? 1 : 0;
         start += pi.in_h[q] / (9 * P.k);
@@ -390,7 +419,7 @@ int launch_fused(ds_handle* h, const uint8_t* in, int64_t n, uint8_t* out, cudaS
     int rc = fused_grid(h, c, p.n_units, &grid, &block, &smem);
     if (rc) return rc;
     p.stages = c.run_stages;
-    fused_fn(c.ncw)<<<grid, block, smem, st>>>(p);
+    fused_fn(c.ncw, plan_modes(c.plan))<<<grid, block, smem, st>>>(p);
     return cudaGetLastError() == cudaSuccess ? DS_OK : DS_ECUDA;
 }
 

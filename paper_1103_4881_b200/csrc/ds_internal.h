@@ -83,6 +83,14 @@ struct GeneralCfg {
     int grid_per_sm = 0, threads = 0, smem = 0;
 };
 
+// K-N1: planes with W % 16 == 0 and rows shorter than this stage whole bands
+// (dead rows included) with one bulk copy per band instead of k + 1 copies of
+// 8 live rows: short rows make those copies small (CIF luma: 2.8 KB)
+#ifndef DS_K1_WHOLE_MAX_W
+#define DS_K1_WHOLE_MAX_W 512
+#endif
+inline bool k1_whole_band(int64_t W) { return W % 16 == 0 && W < DS_K1_WHOLE_MAX_W; }
+
 // K-N1g staged row stride: the row, rounded to 16 bytes, then the 32-byte wrap pad
 inline int64_t general_pitch(int64_t W) { return (W + 15) / 16 * 16 + 32; }
 

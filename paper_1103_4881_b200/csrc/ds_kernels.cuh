@@ -38,7 +38,8 @@ struct FusedPlane {
     int32_t narrow;            // 1: W % 16 == 8 -- the whole band (dead rows included) is
                                // bulk-copied from a 16-aligned superset; rows are 8-aligned
                                // in smem, the last chunk of a row holds one packet
-    int32_t reserved_;
+    int32_t whole;             // 1: W % 16 == 0 but short rows -- the whole band (dead rows
+                               // included) is one bulk copy: 9x fewer, larger TMA ops
 };
 
 struct FusedParams {
@@ -268,7 +269,98 @@ struct UnitCursor {
     }
 };
 
-template <int NCW>
+// ---- K-N1 consumer loops over one unit's tasks (task t = half-group
+// t / chunks, 16-byte chunk t % chunks).
+// Wide planes: the slot holds the 8 live rows of each group; half-group hg
+// reads slot rows 4 hg .. 4 hg + 3.
+template <int NC>
+__device__ __forceinline__ void k1_loop_wide(const uint8_t* st, uint8_t* ob, int W, int Wout, int chunks,
+                                             int tasks, uint32_t rcp, int tid) {
+    for (int t = tid; t < tasks; t += NC) {
+        const int hg = chunks == 1 ? t : (int)__umulhi((uint32_t)t, rcp);   // t / chunks
+        const int c = t - hg * chunks;
+        const uint8_t* base = st + (size_t)4 * hg * W + 16 * c;
+        uint4 r[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) r[j] = lds128(base + (size_t)j * W);
+        uint32_t lo[2], hi[2];
+        k1_task(r, hg & 1, lo, hi);
+        uint8_t* orow = ob + (size_t)2 * hg * Wout + 6 * c;
+#pragma unroll
+        for (int kk = 0; kk < 2; ++kk) {
+            uint8_t* d = orow + (size_t)kk * Wout;
+            sts16(d, lo[kk]);
+            sts16(d + 2, lo[kk] >> 16);
+            sts16(d + 4, hi[kk]);
+        }
+    }
+}
+// Whole band staged (short aligned rows): half-group hg reads slot rows
+// 9 (hg / 2) + 5 (hg % 2) + 0..3.
+template <int NC>
+__device__ __forceinline__ void k1_loop_whole(const uint8_t* st, uint8_t* ob, int W, int Wout, int chunks,
+                                              int tasks, uint32_t rcp, int tid) {
+    for (int t = tid; t < tasks; t += NC) {
+        const int hg = chunks == 1 ? t : (int)__umulhi((uint32_t)t, rcp);   // t / chunks
+        const int c = t - hg * chunks;
+        const int half = hg & 1;
+        const uint8_t* base = st + (size_t)(9 * (hg >> 1) + 5 * half) * W + 16 * c;
+        uint4 r[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) r[j] = lds128(base + (size_t)j * W);
+        uint32_t lo[2], hi[2];
+        k1_task(r, half, lo, hi);
+        uint8_t* orow = ob + (size_t)2 * hg * Wout + 6 * c;
+#pragma unroll
+        for (int kk = 0; kk < 2; ++kk) {
+            uint8_t* d = orow + (size_t)kk * Wout;
+            sts16(d, lo[kk]);
+            sts16(d + 2, lo[kk] >> 16);
+            sts16(d + 4, hi[kk]);
+        }
+    }
+}
+// Narrow plane (W % 16 == 8): st points at the band's first byte inside the
+// slot (phase applied); rows are 8-byte aligned; the last chunk of a row holds
+// one packet; output rows are odd -> byte stores.
+template <int NC>
+__device__ __forceinline__ void k1_loop_narrow(const uint8_t* st, uint8_t* ob, int W, int Wout, int chunks,
+                                               int tasks, uint32_t rcp, int tid) {
+    for (int t = tid; t < tasks; t += NC) {
+        const int hg = chunks == 1 ? t : (int)__umulhi((uint32_t)t, rcp);   // t / chunks
+        const int c = t - hg * chunks;
+        const int half = hg & 1;
+        const uint8_t* base = st + (size_t)(9 * (hg >> 1) + 5 * half) * W + 16 * c;
+        uint4 r[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const uint2 a = lds64(base + (size_t)j * W), b = lds64(base + (size_t)j * W + 8);
+            r[j] = make_uint4(a.x, a.y, b.x, b.y);
+        }
+        uint32_t lo[2], hi[2];
+        k1_task(r, half, lo, hi);
+        uint8_t* orow = ob + (size_t)2 * hg * Wout + 6 * c;
+        const bool two = c + 1 < chunks;
+#pragma unroll
+        for (int kk = 0; kk < 2; ++kk) {
+            uint8_t* d = orow + (size_t)kk * Wout;
+            sts8(d, lo[kk]);
+            sts8(d + 1, lo[kk] >> 8);
+            sts8(d + 2, lo[kk] >> 16);
+            if (two) {
+                sts8(d + 3, lo[kk] >> 24);
+                sts8(d + 4, hi[kk]);
+                sts8(d + 5, hi[kk] >> 8);
+            }
+        }
+    }
+}
+// MODES: bit 0 wide planes (8 live rows per group staged), bit 1 whole-band
+// planes (short aligned rows), bit 2 narrow planes (W % 16 == 8).  Each
+// instantiation compiles only the consumer loops its plan needs: a loop that
+// is present but unused measurably slows the others (a per-unit branch in
+// front of the HD loop cost 7.7%; out-of-line loops cost SD 14%).
+template <int NCW, int MODES>
 __global__ void __launch_bounds__((NCW + 1) * 32)
     ds_fused_band_kernel(const __grid_constant__ FusedParams p) {
     extern __shared__ __align__(1024) uint8_t smem[];
@@ -306,7 +398,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32)
                 const uint8_t* src =
                     p.in + cur.f * p.in_frame + P.in_off + (int64_t)band * 9 * P.k * P.W;
                 uint8_t* dst = ring + (size_t)s * p.stage_stride;
-                if (P.narrow) {
+                if ((MODES & 4) && P.narrow) {
                     // one copy of the whole band from its 16-aligned superset: the
                     // start is at most 8 bytes into the previous band (never before
                     // the buffer: frames are 16-aligned), the end at most 15 bytes
@@ -316,6 +408,9 @@ __global__ void __launch_bounds__((NCW + 1) * 32)
                     const uintptr_t a1 = (a + (uintptr_t)9 * P.k * P.W + 15) & ~uintptr_t(15);
                     mbar_arrive_expect_tx(&full[s], (uint32_t)(a1 - a0));
                     bulk_g2s(dst, reinterpret_cast<const uint8_t*>(a0), (uint32_t)(a1 - a0), &full[s], pol);
+                } else if ((MODES & 2) && P.whole) {
+                    mbar_arrive_expect_tx(&full[s], (uint32_t)P.unit_in);
+                    bulk_g2s(dst, src, (uint32_t)P.unit_in, &full[s], pol);      // rows 0..9k-1
                 } else {
                 mbar_arrive_expect_tx(&full[s], (uint32_t)P.unit_in);
                 // live rows of the band: 0..3 | 5..12 | 14..21 | ... | 9k-4..9k-1.
@@ -348,58 +443,13 @@ __global__ void __launch_bounds__((NCW + 1) * 32)
 
         mbar_wait(&full[s], phase);
 
-        if (!P.narrow) {
-            for (int t = tid; t < tasks; t += NC) {
-                const int hg = chunks == 1 ? t : (int)__umulhi((uint32_t)t, rcp);   // t / chunks
-                const int c = t - hg * chunks;
-                const uint8_t* base = st + (size_t)4 * hg * W + 16 * c;
-                uint4 r[4];
-#pragma unroll
-                for (int j = 0; j < 4; ++j) r[j] = lds128(base + (size_t)j * W);
-                uint32_t lo[2], hi[2];
-                k1_task(r, hg & 1, lo, hi);
-                uint8_t* orow = ob + (size_t)2 * hg * Wout + 6 * c;
-#pragma unroll
-                for (int kk = 0; kk < 2; ++kk) {
-                    uint8_t* d = orow + (size_t)kk * Wout;
-                    sts16(d, lo[kk]);
-                    sts16(d + 2, lo[kk] >> 16);
-                    sts16(d + 4, hi[kk]);
-                }
-            }
-        } else {
-            // narrow plane (W % 16 == 8): slot byte 0 is the band's 16-aligned
-            // superset start; rows are 8-byte aligned; the last chunk of a row
-            // holds one packet; output rows are odd -> byte stores
+        if ((MODES & 2) && P.whole) {
+            k1_loop_whole<NC>(st, ob, W, Wout, chunks, tasks, rcp, tid);
+        } else if ((MODES & 4) && P.narrow) {
             const int nphase = (int)((p.in_frame * cur.f + P.in_off + (int64_t)band * 9 * P.k * W) & 15);
-            for (int t = tid; t < tasks; t += NC) {
-                const int hg = chunks == 1 ? t : (int)__umulhi((uint32_t)t, rcp);   // t / chunks
-                const int c = t - hg * chunks;
-                const int half = hg & 1;
-                const uint8_t* base = st + nphase + (size_t)(9 * (hg >> 1) + 5 * half) * W + 16 * c;
-                uint4 r[4];
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const uint2 a = lds64(base + (size_t)j * W), b = lds64(base + (size_t)j * W + 8);
-                    r[j] = make_uint4(a.x, a.y, b.x, b.y);
-                }
-                uint32_t lo[2], hi[2];
-                k1_task(r, half, lo, hi);
-                uint8_t* orow = ob + (size_t)2 * hg * Wout + 6 * c;
-                const bool two = c + 1 < chunks;
-#pragma unroll
-                for (int kk = 0; kk < 2; ++kk) {
-                    uint8_t* d = orow + (size_t)kk * Wout;
-                    sts8(d, lo[kk]);
-                    sts8(d + 1, lo[kk] >> 8);
-                    sts8(d + 2, lo[kk] >> 16);
-                    if (two) {
-                        sts8(d + 3, lo[kk] >> 24);
-                        sts8(d + 4, hi[kk]);
-                        sts8(d + 5, hi[kk] >> 8);
-                    }
-                }
-            }
+            k1_loop_narrow<NC>(st + nphase, ob, W, Wout, chunks, tasks, rcp, tid);
+        } else if (MODES & 1) {
+            k1_loop_wide<NC>(st, ob, W, Wout, chunks, tasks, rcp, tid);
         }
         // every lane of this warp has consumed its reads of slot s
         __syncwarp();
