@@ -28,3 +28,13 @@ def pytest_collection_modifyitems(config, items):
     for it in items:
         if "gpu" in it.keywords:
             it.add_marker(skip)
+
+
+# Randomized parity tests scale with DS_FUZZ_SCALE (default 1): a sweep runs
+# e.g. DS_FUZZ_SCALE=10 for ten times the trials on fresh seeds.
+FUZZ_SCALE = max(1, int(os.environ.get("DS_FUZZ_SCALE", "1")))
+
+
+def fuzz_seed(base: int) -> int:
+    """The test's fixed seed at scale 1, a different stream per larger scale."""
+    return base if FUZZ_SCALE == 1 else base * 1000 + FUZZ_SCALE

@@ -6,6 +6,7 @@ import pytest
 
 import oracle
 import synth
+from conftest import FUZZ_SCALE, fuzz_seed
 
 torch = pytest.importorskip("torch")
 ds = pytest.importorskip("paper_1103_4881_b200")
@@ -308,9 +309,9 @@ def _random_spec(rng):
 def test_general_kernel_fuzz_random_specs():
     """Random separable specs (halos, gaps P < S, origins, negative taps,
     divisors incl. 1 and 2^20) on random geometries, K-N1g vs the oracle."""
-    rng = np.random.default_rng(2024)
+    rng = np.random.default_rng(fuzz_seed(2024))
     checked = 0
-    for trial in range(40):
+    for trial in range(40 * FUZZ_SCALE):
         hd, vd = _random_spec(rng)
         ch = int(rng.choice([1, 3]))
         chroma = int(rng.integers(0, 2))
@@ -325,11 +326,15 @@ def test_general_kernel_fuzz_random_specs():
         fr = synth.random_frames(trial, 0, 2, W, H, ch, chroma)
         want = oracle.execute_frames(fr, W, H, ch, chroma, _oracle_stage(hd), _oracle_stage(vd))
         d.set_run_bands(int(rng.choice([0, 1, 2, 3, 7, 1 << 20])))   # halo reuse across bands
+        if rng.random() < 0.3:                                         # column strips
+            d.set_general_stage_bytes(int(rng.choice([1024, 3000, 8000])))
+            if not d.plan.fused_general_eligible:
+                continue
         got = _run(d, fr, ds.DS_KERNEL_FUSED_GENERAL)
         assert d.last_kernel() == ds.DS_KERNEL_FUSED_GENERAL
-        _assert_same(got, want, f"fuzz {trial}: {W}x{H}x{ch} h={hd} v={vd}")
+        _assert_same(got, want, f"fuzz {trial}: {W}x{H}x{ch} h={hd} v={vd} strips={list(d.plan.general_strips)}")
         checked += 1
-    assert checked >= 25
+    assert checked >= 25 * FUZZ_SCALE
 
 
 # ------------------------------------------------------- alignment / API --
@@ -581,9 +586,9 @@ def test_fused_kernel_fuzz():
     """Random geometries (W % 16 == 0, H % 9 or 18 == 0), channel/chroma
     modes, frame counts, band sizes, ring depths and output-pointer
     alignments: K-N1 byte-for-byte against the oracle."""
-    rng = np.random.default_rng(4242)
+    rng = np.random.default_rng(fuzz_seed(4242))
     checked = 0
-    for trial in range(60):
+    for trial in range(60 * FUZZ_SCALE):
         ch = int(rng.choice([1, 3]))
         chroma = int(rng.integers(0, 2))
         wmul = 16 if (ch == 3 and chroma == 1) else 8          # includes W % 16 == 8 planes
@@ -610,7 +615,7 @@ def test_fused_kernel_fuzz():
         _assert_same(y.cpu().numpy(), want, f"trial {trial}: {W}x{H}x{ch} chroma={chroma} n={n} "
                                               f"band={band} off={off}")
         checked += 1
-    assert checked >= 30
+    assert checked >= 30 * FUZZ_SCALE
 
 
 @pytest.mark.parametrize("kernel,halo,strips", [(FUSED, False, False), (ds.DS_KERNEL_FUSED_GENERAL, False, False),

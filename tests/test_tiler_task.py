@@ -8,6 +8,7 @@ import pytest
 import oracle
 import paper_1103_4881_b200 as ds
 import synth
+from conftest import FUZZ_SCALE, fuzz_seed
 
 
 # ---------------------------------------------------------------- topology --
@@ -71,8 +72,8 @@ def _exact_out_tiler(rng, nrep_shape, npat_shape):
 @pytest.mark.gpu
 @pytest.mark.parametrize("policy", [ds.DS_TOPO_FLAT, ds.DS_TOPO_SPEC])
 def test_run_task_random_tilers(policy):
-    rng = np.random.default_rng(77 + policy)
-    for trial in range(60):
+    rng = np.random.default_rng(fuzz_seed(77 + policy))
+    for trial in range(60 * FUZZ_SCALE):
         nd = int(rng.integers(1, 4))
         in_shape = [int(rng.integers(1, 30)) for _ in range(nd)]
         R = int(rng.integers(1, 200))
@@ -210,8 +211,8 @@ def _affine_in_tiler(rng, in_shape, R, P):
 def test_run_task_affine_random(policy):
     """Wrap-free tilers take the affine path (offsets A + a.r + b[e], no
     modulo); results must equal the oracle's modulo tiler semantics."""
-    rng = np.random.default_rng(4881 + policy)
-    for trial in range(60):
+    rng = np.random.default_rng(fuzz_seed(4881 + policy))
+    for trial in range(60 * FUZZ_SCALE):
         nd = int(rng.integers(1, 4))
         R = int(rng.integers(1, 300))
         P = int(rng.integers(1, 17))
@@ -271,8 +272,8 @@ def test_run_task_affine_columns():
     """Column-vector path: the innermost repetition dim is unit-stride in both
     arrays (extent % 4 == 0) and the pattern runs down a column, as in the
     paper's V task; 4 repetitions per thread, 4x4 byte transposes + dp4a."""
-    rng = np.random.default_rng(99)
-    for trial in range(40):
+    rng = np.random.default_rng(fuzz_seed(99))
+    for trial in range(40 * FUZZ_SCALE):
         P = int(rng.integers(1, 17))
         Q = int(rng.integers(1, 9))
         C = 4 * int(rng.integers(1, 40))                 # columns = innermost repetitions
