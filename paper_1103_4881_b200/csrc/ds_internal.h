@@ -51,6 +51,11 @@ struct FusedCfg {
     int grid_per_sm = 0, threads = 0, smem = 0, run_stages = 0;
 };
 
+#ifndef DS_HTASK_TMA
+#define DS_HTASK_TMA 1
+#endif
+constexpr bool kHtaskTma = DS_HTASK_TMA != 0;      // K-N3 H task on the TMA pipeline (flat ranges)
+constexpr int64_t kHtaskUnit = 24 * 1024;          // its unit: input bytes per ring slot (x 128)
 constexpr int64_t kFineUnitTarget = 16 * 1024;      // small batches: more, smaller units
 #ifndef DS_GEN_STAGE_TARGET
 #define DS_GEN_STAGE_TARGET (40 * 1024)
@@ -110,6 +115,7 @@ struct ds_handle {
     dsi::GeneralCfg general;
     int kernel_pref = DS_KERNEL_AUTO;
     int32_t run_bands = 0;                  // ds_set_run_bands (0 = automatic)
+    bool htask_tma_ready = false;           // smem attribute set for ds_htask_tma_kernel
     int64_t general_target = 0;             // ds_set_general_stage_bytes (0 = default)
     uint32_t* debug_unit_count = nullptr;   // ds_set_debug_counter
     std::atomic<int> last_kernel{DS_KERNEL_AUTO};

@@ -103,7 +103,23 @@ int launch_htask(ds_handle* h, const uint8_t* in, int64_t n, uint8_t* mid, int p
             const int64_t chunks = bytes / 16;
             const int64_t blocks =
                 std::max<int64_t>(1, std::min<int64_t>((chunks + 255) / 256, (int64_t)h->sm_count * 16));
-            if (aligned(mid + mb, 16))
+            if (kHtaskTma && all && aligned(in, 16) && aligned(mid, 16) && bytes >= kHtaskUnit) {
+                // one flat range: the TMA pipeline (persistent, one CTA per SM)
+                constexpr int kStages = 4;
+                const int out_stride = (int)((kHtaskUnit / 8 * 3 + 127) & ~127);
+                const int smem = kStages * (int)kHtaskUnit + 3 * out_stride + 2 * kStages * 8;
+                if (!h->htask_tma_ready) {
+                    if (cudaFuncSetAttribute(ds::ds_htask_tma_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             smem) != cudaSuccess) {
+                        cudaGetLastError();
+                        return DS_ECUDA;
+                    }
+                    h->htask_tma_ready = true;
+                }
+                const int64_t units = (bytes + kHtaskUnit - 1) / kHtaskUnit;
+                const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(units, h->sm_count));
+                ds::ds_htask_tma_kernel<8><<<grid, 9 * 32, smem, st>>>(in, mid, bytes, (int32_t)kHtaskUnit, kStages);
+            } else if (aligned(mid + mb, 16))
                 ds::ds_htask_kernel<true><<<(unsigned)blocks, 256, 0, st>>>(in + ib, mid + mb, chunks);
             else
                 ds::ds_htask_kernel<false><<<(unsigned)blocks, 256, 0, st>>>(in + ib, mid + mb, chunks);

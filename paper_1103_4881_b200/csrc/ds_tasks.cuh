@@ -24,6 +24,7 @@
 #include <cuda_runtime.h>
 
 #include "ds.h"
+#include "ds_pipeline.cuh"
 
 namespace ds {
 
@@ -86,6 +87,88 @@ __global__ void __launch_bounds__(256)
             d[2] = (uint16_t)hi;
         }
     }
+}
+
+// H task on the TMA pipeline (the K-N1 building blocks without the V step):
+// a persistent grid streams units of `unit_in` bytes of the flat packet
+// stream (a multiple of 128) through a ring of bulk copies; consumers turn
+// 16-byte chunks into 6 Mid bytes in a shared output slot, which thread 0
+// bulk-stores to Mid at 3/8 of the unit's offset (16-byte aligned).  The last
+// unit may be short; a non-16-multiple output tail is stored cooperatively.
+template <int NCW>
+__global__ void __launch_bounds__((NCW + 1) * 32, 1)
+    ds_htask_tma_kernel(const uint8_t* __restrict__ in, uint8_t* __restrict__ mid, int64_t n_bytes,
+                        int32_t unit_in, int32_t stages) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    constexpr int NC = NCW * 32;
+    const int S = stages;
+    const int out_stride = (unit_in / 8 * 3 + 127) & ~127;
+    uint8_t* ring = smem;
+    uint8_t* outs = smem + (size_t)S * unit_in;
+    uint64_t* full = reinterpret_cast<uint64_t*>(outs + (size_t)3 * out_stride);
+    uint64_t* empty = full + S;
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], NCW);
+        }
+        fence_barrier_init();
+    }
+    __syncthreads();
+    const int64_t n_units = (n_bytes + unit_in - 1) / unit_in;
+    const int warp = tid >> 5, lane = tid & 31;
+    int s = 0;
+    uint32_t phase = 0;
+    if (warp == NCW) {
+        if (lane == 0) {
+            const uint64_t pol = policy_evict_first();
+            bool first_round = true;
+            for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x) {
+                if (!first_round) mbar_wait_sleep(&empty[s], phase ^ 1);
+                const uint32_t bytes = (uint32_t)min((int64_t)unit_in, n_bytes - u * unit_in);
+                mbar_arrive_expect_tx(&full[s], bytes);
+                bulk_g2s(ring + (size_t)s * unit_in, in + u * unit_in, bytes, &full[s], pol);
+                if (++s == S) { s = 0; phase ^= 1; first_round = false; }
+            }
+        }
+        return;
+    }
+    int oslot = 0;
+    for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x) {
+        const int bytes = (int)min((int64_t)unit_in, n_bytes - u * unit_in);
+        const int chunks = bytes >> 4;
+        const uint8_t* st = ring + (size_t)s * unit_in;
+        uint8_t* ob = outs + (size_t)oslot * out_stride;
+        mbar_wait(&full[s], phase);
+        for (int c = tid; c < chunks; c += NC) {
+            uint32_t lo, hi;
+            t_hchunk(lds128(st + 16 * c), lo, hi);
+            uint8_t* d = ob + 6 * c;
+            sts16(d, lo);
+            sts16(d + 2, lo >> 16);
+            sts16(d + 4, hi);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+        const int out_bytes = 6 * chunks;
+        uint8_t* dst = mid + u * (unit_in / 8 * 3);
+        if ((out_bytes & 15) == 0) {
+            fence_proxy_async_smem();
+            named_bar_sync(1, NC);
+            if (tid == 0) {
+                bulk_s2g_hint(dst, ob, (uint32_t)out_bytes, policy_evict_first());
+                bulk_commit();
+                bulk_wait_read<1>();
+            }
+        } else {
+            named_bar_sync(1, NC);
+            for (int x = tid; x < out_bytes; x += NC) dst[x] = ob[x];
+        }
+        if (++s == S) { s = 0; phase ^= 1; }
+        oslot = oslot == 2 ? 0 : oslot + 1;
+    }
+    if (tid == 0) bulk_wait_all();
 }
 
 // ------------------------------------------------------------ V task, SPEC --
