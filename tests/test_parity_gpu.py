@@ -162,6 +162,26 @@ def test_ragged_geometries(W, H, ch):
     _assert_same(got, oracle.execute_frames(fr, W, H, ch, 1), f"{W}x{H}x{ch}")
 
 
+@pytest.mark.parametrize("W,H,ch,chroma", [(16, 9, 1, 1), (8, 9, 1, 1), (16, 18, 3, 1), (32, 9, 1, 1),
+                                           (1920, 9, 1, 1), (8, 900, 1, 1), (16, 18, 3, 0), (2048, 18, 3, 1)])
+def test_degenerate_geometries_every_kernel(W, H, ch, chroma):
+    """Smallest planes (one 8- or 16-byte row, one 9-row group), a single
+    band over a wide plane and a tall narrow column, through every kernel that
+    can take them (K-N1, K-N1g, K-N2), at 1, 2 and 5 frames."""
+    d = ds.Downscaler(W, H, ch, chroma=chroma)
+    kernels = [GENERIC, ds.DS_KERNEL_FUSED_GENERAL] + ([FUSED] if d.plan.fused_eligible else [])
+    for n in (1, 2, 5):
+        fr = synth.random_frames(W * 7 + H, 3, n, W, H, ch, chroma)
+        want = oracle.execute_frames(fr, W, H, ch, chroma)
+        for k in kernels:
+            if k == ds.DS_KERNEL_FUSED_GENERAL and not d.plan.fused_general_eligible:
+                continue
+            got = _run(d, fr, k)
+            assert d.last_kernel() == k
+            _assert_same(got, want, f"{W}x{H}x{ch} chroma={chroma} n={n} kernel={k}")
+    d.set_kernel(ds.DS_KERNEL_AUTO)
+
+
 def test_zero_frames_noop():
     d = ds.Downscaler(352, 288, 3)
     x = torch.empty((0, d.in_frame_bytes), dtype=torch.uint8, device="cuda")
