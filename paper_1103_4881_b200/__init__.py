@@ -382,6 +382,23 @@ def tiler_coverage(t: ds_tiler, rep_shape, stream=None):
 
 
 # ------------------------------------------------------------ torch facade --
+def _torch_uint8():
+    import torch
+
+    return torch.uint8
+
+
+def _current_raw_stream(device_index):
+    """cudaStream_t of torch's current stream on the device (the raw query
+    when this torch has it: ~10x cheaper than torch.cuda.current_stream())."""
+    import torch
+
+    f = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+    if f is not None:
+        return f(device_index)
+    return torch.cuda.current_stream(device_index).cuda_stream
+
+
 class Downscaler:
     """``Downscaler(w, h, channels=3, chroma="420", spec=None)(frames)``.
 
@@ -408,7 +425,7 @@ class Downscaler:
         self.spec = spec
         self.w, self.h, self.channels = w, h, channels
         self.device = torch.cuda.current_device()
-        self._h = ds_create(w, h, channels, spec)
+        self._h = ds_create(w, h, channels, spec)       # loads libds.so (module-level _lib)
         self.in_frame_bytes = lib().ds_in_frame_bytes(self._h)
         self.out_frame_bytes = lib().ds_out_frame_bytes(self._h)
         self.plan = self.get_plan()
@@ -549,20 +566,24 @@ class Downscaler:
                            device=f"cuda:{self.device}")
 
     def __call__(self, frames, out=None, stream=None):
-        import torch
-
-        if frames.dtype != torch.uint8 or not frames.is_cuda or not frames.is_contiguous():
+        # Hot path for small batches: identity dtype checks, the raw current
+        # stream, and the library call directly (tools/host_overhead.py).
+        u8 = _torch_uint8()
+        if frames.dtype is not u8 or not frames.is_cuda or not frames.is_contiguous():
             raise ValueError("frames must be a contiguous torch.uint8 CUDA tensor")
-        if frames.numel() % self.in_frame_bytes:
+        total = frames.numel()
+        n = total // self.in_frame_bytes
+        if n * self.in_frame_bytes != total:
             raise ValueError("frames does not hold a whole number of frames")
-        n = frames.numel() // self.in_frame_bytes
         if out is None:
             out = self.alloc_out(n)
-        elif (out.dtype != torch.uint8 or not out.is_cuda or not out.is_contiguous()
+        elif (out.dtype is not u8 or not out.is_cuda or not out.is_contiguous()
               or out.numel() != n * self.out_frame_bytes):
             raise ValueError("out has the wrong dtype, device, layout or size")
-        s = stream if stream is not None else torch.cuda.current_stream()
-        ds_run(self._h, frames.data_ptr(), n, out.data_ptr(), s.cuda_stream)
+        sp = stream.cuda_stream if stream is not None else _current_raw_stream(frames.device.index)
+        rc = _lib.ds_run(self._h, frames.data_ptr(), n, out.data_ptr(), sp or None)
+        if rc:
+            raise DSError(rc, "ds_run")
         return out
 
     def run_host(self, host_frames, host_out=None, stream=None):
