@@ -650,6 +650,159 @@ int64_t next_pow2(int64_t x) {
 
 }  // namespace
 
+namespace {
+
+// Plan and launch one (validated) task.  With allow_peel, a task whose
+// tilers are not wrap-free over the whole box is split when a thin slab at one
+// end of one repetition dimension carries all the wrapping: the interior runs
+// on the affine / dense / column paths, the slab (origin moved to its start)
+// on the modulo path.  Output tilers are exact, so the parts write disjoint
+// elements and the split changes nothing but speed.
+int launch_task(const uint8_t* in, const ds_tiler& t_in, uint8_t* out, const ds_tiler& t_out, int32_t nrep,
+                const int64_t* rep_shape, const ds_task_body* body, int32_t policy, cudaStream_t st, int sms,
+                bool allow_peel) {
+    TaskParams p;
+    std::memset(&p, 0, sizeof p);
+    int rc = prep_reps(nrep, rep_shape, &p);
+    if (rc) return rc;
+    int64_t nin = 0, nout = 0;
+    if ((rc = prep_tiler(t_in, nrep, &p.tin, &nin))) return rc;
+    if ((rc = prep_tiler(t_out, nrep, &p.tout, &nout))) return rc;
+    p.in = in;
+    p.out = out;
+    p.policy = policy;
+    p.fast32 = (p.n_reps < (1LL << 31) && fits32(p, p.tin) && fits32(p, p.tout)) ? 1 : 0;
+    for (int j = 0; j < nrep; ++j) p.rdiv[j] = make_fdiv(p.rep[j]);
+    for (int d = 0; d < p.tin.ndim; ++d) p.sdiv_in[d] = make_fdiv(p.tin.shape[d]);
+    for (int d = 0; d < p.tout.ndim; ++d) p.sdiv_out[d] = make_fdiv(p.tout.shape[d]);
+    p.n_in = body->n_in;
+    p.n_out = body->n_out;
+    p.divisor = body->divisor;
+    p.bias = body->bias;
+    std::memcpy(p.w, body->weight, sizeof p.w);
+    // taps: s8-packed copies, live pattern elements, and the exact
+    // multiply-high division (same derivation as K-N1g's FASTDIV) -- all paths
+    bool s8 = true;
+    int64_t amax = 0;
+    for (int k = 0; k < p.n_out; ++k) {
+        int64_t pos = body->bias;
+        for (int e = 0; e < p.n_in; ++e) {
+            const int32_t w = body->weight[k][e];
+            if (w < -128 || w > 127) s8 = false;
+            if (w > 0) pos += 255LL * w;
+            if (w != 0) p.in_live |= 1u << e;
+            p.wp[k][e / 4] |= (uint32_t)(uint8_t)(int8_t)(w < -128 || w > 127 ? 0 : w) << (8 * (e % 4));
+        }
+        amax = std::max(amax, pos);
+    }
+    {
+        const uint64_t D = (uint64_t)body->divisor;
+        if (D == 1) {
+            if (amax < 0x7fffffffLL) { p.fastdiv = 1; p.M = 0xffffffffu; p.lo = 1; p.fbias = body->bias + 1; }
+        } else {
+            const uint64_t M = ((1ULL << 32) + D - 1) / D, e = M * D - (1ULL << 32);
+            if ((unsigned __int128)(uint64_t)amax * e < ((unsigned __int128)1 << 32)) {
+                p.fastdiv = 1; p.M = (uint32_t)M; p.lo = 0; p.fbias = body->bias;
+            }
+        }
+    }
+    // affine path: both tilers wrap-free, 32-bit offsets and repetition index
+    if (p.n_reps < (1LL << 31) && affine_tiler(t_in, nrep, rep_shape, &p.in_A, p.in_a, p.in_b, DS_MAX_PATTERN) &&
+        affine_tiler(t_out, nrep, rep_shape, &p.out_A, p.out_a, p.out_b, DS_MAX_OUTPUTS)) {
+        p.affine = 1;
+        bool words = s8 && p.n_in % 4 == 0 && (reinterpret_cast<uintptr_t>(in) & 3) == 0 && p.in_A % 4 == 0;
+        for (int j = 0; j < nrep; ++j) words = words && p.in_a[j] % 4 == 0;
+        for (int e = 0; e < p.n_in; ++e) words = words && p.in_b[e] == e;
+        if (words) p.affine = 2;
+        // dense: both tilers are row-major runs over the repetition index
+        bool dense = words && policy == DS_TOPO_FLAT &&
+                     ((reinterpret_cast<uintptr_t>(in) + p.in_A) & 15) == 0 &&
+                     ((reinterpret_cast<uintptr_t>(out) + p.out_A) & 3) == 0;
+        int64_t inner = 1;
+        for (int j = nrep - 1; j >= 0; --j) {
+            dense = dense && p.in_a[j] == (uint64_t)(p.n_in * inner) && p.out_a[j] == (uint64_t)(p.n_out * inner);
+            inner *= rep_shape[j];
+        }
+        for (int k = 0; k < p.n_out; ++k) dense = dense && p.out_b[k] == k;
+        p.dense = dense ? 1 : 0;
+        // column vectors: innermost repetition dim unit-stride in both arrays
+        // (extent % 4 == 0), all other offsets and both pointers 4-aligned, s8 taps
+        if (!dense && policy == DS_TOPO_FLAT && s8) {
+            const int jl = nrep - 1;
+            bool cols = p.in_a[jl] == 1 && p.out_a[jl] == 1 && rep_shape[jl] % 4 == 0 &&
+                        p.in_A % 4 == 0 && p.out_A % 4 == 0 &&
+                        (reinterpret_cast<uintptr_t>(in) & 3) == 0 && (reinterpret_cast<uintptr_t>(out) & 3) == 0;
+            for (int j = 0; j < jl; ++j) cols = cols && p.in_a[j] % 4 == 0 && p.out_a[j] % 4 == 0;
+            for (int e = 0; e < p.n_in; ++e) cols = cols && (p.in_b[e] & 3) == 0;
+            for (int k = 0; k < p.n_out; ++k) cols = cols && (p.out_b[k] & 3) == 0;
+            if (cols) p.affine = 3;
+        }
+    }
+    if (!p.affine && allow_peel && p.n_reps < (1LL << 31)) {
+        // a wrap confined to <= 8 repetitions at one end of one repetition dim
+        uint32_t A, a[4];
+        int32_t bi[DS_MAX_PATTERN], bo[DS_MAX_OUTPUTS];
+        auto shifted = [&](const ds_tiler& t, int j, int64_t by) {
+            ds_tiler u = t;
+            for (int d = 0; d < t.ndim; ++d)
+                u.origin[d] = h_mod(h_mod(t.origin[d], t.shape[d]) + h_mod(t.paving[d][j], t.shape[d]) * by,
+                                    t.shape[d]);
+            return u;
+        };
+        for (int j = nrep - 1; j >= 0; --j) {
+            const int64_t R = rep_shape[j];
+            for (int64_t t : {1, 2, 3, 4, 8}) {
+                if (t >= R) break;
+                int64_t rin[4], rsl[4];
+                for (int q = 0; q < nrep; ++q) rin[q] = rsl[q] = rep_shape[q];
+                rin[j] = R - t;
+                rsl[j] = t;
+                // slab at the end: interior [0, R - t) keeps the tilers
+                if (affine_tiler(t_in, nrep, rin, &A, a, bi, DS_MAX_PATTERN) &&
+                    affine_tiler(t_out, nrep, rin, &A, a, bo, DS_MAX_OUTPUTS)) {
+                    if ((rc = launch_task(in, t_in, out, t_out, nrep, rin, body, policy, st, sms, false))) return rc;
+                    return launch_task(in, shifted(t_in, j, R - t), out, shifted(t_out, j, R - t), nrep, rsl, body,
+                                       policy, st, sms, false);
+                }
+                // slab at the start: interior [t, R) has its origin moved by t
+                const ds_tiler hin = shifted(t_in, j, t), hout = shifted(t_out, j, t);
+                if (affine_tiler(hin, nrep, rin, &A, a, bi, DS_MAX_PATTERN) &&
+                    affine_tiler(hout, nrep, rin, &A, a, bo, DS_MAX_OUTPUTS)) {
+                    if ((rc = launch_task(in, hin, out, hout, nrep, rin, body, policy, st, sms, false))) return rc;
+                    return launch_task(in, t_in, out, t_out, nrep, rsl, body, policy, st, sms, false);
+                }
+            }
+        }
+    }
+    const TaskFn fn = p.dense ? dense_fn(p.n_in)
+                      : p.affine == 3 ? cols_fn(p.n_in)
+                      : p.affine ? affine_fn(p.n_in, p.affine == 2) : modulo_fn(p.n_in);
+    if (policy == DS_TOPO_SPEC) {
+        ds_topology topo;
+        if ((rc = ds_compute_topology(nrep, rep_shape, 1024, 3, 64, 256, &topo))) return rc;
+        p.tdim = topo.ndim;
+        dim3 block(1, 1, 1), grid(1, 1, 1);
+        const int64_t lim[3] = {2147483647LL, 65535LL, 65535LL};
+        for (int d = 0; d < topo.ndim; ++d) {
+            p.tmult[d] = topo.multiplicity[d];
+            const int ax = topo.ndim - 1 - d;      // last collapsed dim -> x
+            const int64_t g = topo.global[d] / topo.local[d];
+            if (g > lim[ax]) return DS_EUNSUPPORTED;
+            (ax == 0 ? block.x : ax == 1 ? block.y : block.z) = (unsigned)topo.local[d];
+            (ax == 0 ? grid.x : ax == 1 ? grid.y : grid.z) = (unsigned)g;
+        }
+        fn<<<grid, block, 0, st>>>(p);
+    } else {
+        const int64_t items = p.affine == 3 ? p.n_reps / 4 : p.n_reps;      // column quads
+        const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((items + 255) / 256, (int64_t)sms * 16));
+        fn<<<(unsigned)blocks, 256, 0, st>>>(p);
+    }
+    return cudaGetLastError() == cudaSuccess ? DS_OK : DS_ECUDA;
+}
+
+
+}  // namespace
+
 extern "C" {
 
 DS_API int ds_compute_topology(int32_t nrep, const int64_t* mult, int32_t max_wg, int32_t max_dims,
@@ -746,101 +899,8 @@ DS_API int ds_run_task(const uint8_t* in, const ds_tiler* t_in, uint8_t* out, co
         return DS_ECUDA;
     }
     if (!dsi::device_ptr_on(in, dev) || !dsi::device_ptr_on(out, dev)) return DS_EINVAL;
-    p.in = in;
-    p.out = out;
-    p.policy = policy;
-    p.fast32 = (p.n_reps < (1LL << 31) && fits32(p, p.tin) && fits32(p, p.tout)) ? 1 : 0;
-    for (int j = 0; j < nrep; ++j) p.rdiv[j] = make_fdiv(p.rep[j]);
-    for (int d = 0; d < p.tin.ndim; ++d) p.sdiv_in[d] = make_fdiv(p.tin.shape[d]);
-    for (int d = 0; d < p.tout.ndim; ++d) p.sdiv_out[d] = make_fdiv(p.tout.shape[d]);
-    p.n_in = body->n_in;
-    p.n_out = body->n_out;
-    p.divisor = body->divisor;
-    p.bias = body->bias;
-    std::memcpy(p.w, body->weight, sizeof p.w);
-    // taps: s8-packed copies, live pattern elements, and the exact
-    // multiply-high division (same derivation as K-N1g's FASTDIV) -- all paths
-    bool s8 = true;
-    int64_t amax = 0;
-    for (int k = 0; k < p.n_out; ++k) {
-        int64_t pos = body->bias;
-        for (int e = 0; e < p.n_in; ++e) {
-            const int32_t w = body->weight[k][e];
-            if (w < -128 || w > 127) s8 = false;
-            if (w > 0) pos += 255LL * w;
-            if (w != 0) p.in_live |= 1u << e;
-            p.wp[k][e / 4] |= (uint32_t)(uint8_t)(int8_t)(w < -128 || w > 127 ? 0 : w) << (8 * (e % 4));
-        }
-        amax = std::max(amax, pos);
-    }
-    {
-        const uint64_t D = (uint64_t)body->divisor;
-        if (D == 1) {
-            if (amax < 0x7fffffffLL) { p.fastdiv = 1; p.M = 0xffffffffu; p.lo = 1; p.fbias = body->bias + 1; }
-        } else {
-            const uint64_t M = ((1ULL << 32) + D - 1) / D, e = M * D - (1ULL << 32);
-            if ((unsigned __int128)(uint64_t)amax * e < ((unsigned __int128)1 << 32)) {
-                p.fastdiv = 1; p.M = (uint32_t)M; p.lo = 0; p.fbias = body->bias;
-            }
-        }
-    }
-    // affine path: both tilers wrap-free, 32-bit offsets and repetition index
-    if (p.n_reps < (1LL << 31) && affine_tiler(*t_in, nrep, rep_shape, &p.in_A, p.in_a, p.in_b, DS_MAX_PATTERN) &&
-        affine_tiler(*t_out, nrep, rep_shape, &p.out_A, p.out_a, p.out_b, DS_MAX_OUTPUTS)) {
-        p.affine = 1;
-        bool words = s8 && p.n_in % 4 == 0 && (reinterpret_cast<uintptr_t>(in) & 3) == 0 && p.in_A % 4 == 0;
-        for (int j = 0; j < nrep; ++j) words = words && p.in_a[j] % 4 == 0;
-        for (int e = 0; e < p.n_in; ++e) words = words && p.in_b[e] == e;
-        if (words) p.affine = 2;
-        // dense: both tilers are row-major runs over the repetition index
-        bool dense = words && policy == DS_TOPO_FLAT &&
-                     ((reinterpret_cast<uintptr_t>(in) + p.in_A) & 15) == 0 &&
-                     ((reinterpret_cast<uintptr_t>(out) + p.out_A) & 3) == 0;
-        int64_t inner = 1;
-        for (int j = nrep - 1; j >= 0; --j) {
-            dense = dense && p.in_a[j] == (uint64_t)(p.n_in * inner) && p.out_a[j] == (uint64_t)(p.n_out * inner);
-            inner *= rep_shape[j];
-        }
-        for (int k = 0; k < p.n_out; ++k) dense = dense && p.out_b[k] == k;
-        p.dense = dense ? 1 : 0;
-        // column vectors: innermost repetition dim unit-stride in both arrays
-        // (extent % 4 == 0), all other offsets and both pointers 4-aligned, s8 taps
-        if (!dense && policy == DS_TOPO_FLAT && s8) {
-            const int jl = nrep - 1;
-            bool cols = p.in_a[jl] == 1 && p.out_a[jl] == 1 && rep_shape[jl] % 4 == 0 &&
-                        p.in_A % 4 == 0 && p.out_A % 4 == 0 &&
-                        (reinterpret_cast<uintptr_t>(in) & 3) == 0 && (reinterpret_cast<uintptr_t>(out) & 3) == 0;
-            for (int j = 0; j < jl; ++j) cols = cols && p.in_a[j] % 4 == 0 && p.out_a[j] % 4 == 0;
-            for (int e = 0; e < p.n_in; ++e) cols = cols && (p.in_b[e] & 3) == 0;
-            for (int k = 0; k < p.n_out; ++k) cols = cols && (p.out_b[k] & 3) == 0;
-            if (cols) p.affine = 3;
-        }
-    }
-    const TaskFn fn = p.dense ? dense_fn(p.n_in)
-                      : p.affine == 3 ? cols_fn(p.n_in)
-                      : p.affine ? affine_fn(p.n_in, p.affine == 2) : modulo_fn(p.n_in);
-    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-    if (policy == DS_TOPO_SPEC) {
-        ds_topology topo;
-        if ((rc = ds_compute_topology(nrep, rep_shape, 1024, 3, 64, 256, &topo))) return rc;
-        p.tdim = topo.ndim;
-        dim3 block(1, 1, 1), grid(1, 1, 1);
-        const int64_t lim[3] = {2147483647LL, 65535LL, 65535LL};
-        for (int d = 0; d < topo.ndim; ++d) {
-            p.tmult[d] = topo.multiplicity[d];
-            const int ax = topo.ndim - 1 - d;      // last collapsed dim -> x
-            const int64_t g = topo.global[d] / topo.local[d];
-            if (g > lim[ax]) return DS_EUNSUPPORTED;
-            (ax == 0 ? block.x : ax == 1 ? block.y : block.z) = (unsigned)topo.local[d];
-            (ax == 0 ? grid.x : ax == 1 ? grid.y : grid.z) = (unsigned)g;
-        }
-        fn<<<grid, block, 0, st>>>(p);
-    } else {
-        const int64_t items = p.affine == 3 ? p.n_reps / 4 : p.n_reps;      // column quads
-        const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((items + 255) / 256, (int64_t)sms * 16));
-        fn<<<(unsigned)blocks, 256, 0, st>>>(p);
-    }
-    return cudaGetLastError() == cudaSuccess ? DS_OK : DS_ECUDA;
+    return launch_task(in, *t_in, out, *t_out, nrep, rep_shape, body, policy,
+                       reinterpret_cast<cudaStream_t>(stream), sms, policy == DS_TOPO_FLAT);
 }
 
 DS_API int ds_tiler_coverage(const ds_tiler* t, int32_t nrep, const int64_t* rep_shape, int64_t* overlaps,

@@ -306,3 +306,42 @@ def test_run_task_affine_columns():
                     ds.make_body(w, D, B, n_in=P))
         torch.cuda.synchronize()
         assert np.array_equal(y.cpu().numpy(), want), (trial, P, Q, C, G, S, step, D)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("shift", [3, -2, 5, -7])
+def test_run_task_peeled_wrap(shift):
+    """Tilers that wrap only at one end of one repetition dimension (an H task
+    whose column origin is shifted, a V task whose row origin is shifted) are
+    split: the wrap-free interior on the fast paths, the thin slab on the
+    modulo path -- the result must equal the oracle's modulo semantics."""
+    rng = np.random.default_rng(100 + shift)
+    n, H, W = 3, 18, 352
+    a = rng.integers(0, 256, (n, H, W)).astype(np.uint8)
+    hw = [[1, 5, 0, 0, 0, 0, 0, 0], [0, 0, 0, 3, 3, 0, 0, 0], [0, 0, 0, 0, 0, 0, 5, 1]]
+    # H task, column origin shifted: the last (shift > 0) or first (< 0) window of a row wraps
+    tin = ((n, H, W), (0, 0, shift), [[1, 0, 0], [0, 1, 0], [0, 0, 8]], [[0], [0], [1]], [8])
+    tout = ((n, H, W // 8 * 3), (0, 0, 0), [[1, 0, 0], [0, 1, 0], [0, 0, 3]], [[0], [0], [1]], [3])
+    reps = [n, H, W // 8]
+    want = oracle.run_task(a, oracle.make_tiler(*tin), tout[0], oracle.make_tiler(*tout), reps,
+                           oracle.make_stage(8, 8, 0, hw, 6, 3))
+    y = torch.zeros(tout[0], dtype=torch.uint8, device="cuda")
+    ds.run_task(torch.from_numpy(a).cuda(), ds.make_tiler(*tin), y, ds.make_tiler(*tout), reps,
+                ds.make_body(hw, 6, 3, n_in=8))
+    torch.cuda.synchronize()
+    assert np.array_equal(y.cpu().numpy(), want), "H task"
+    # V task, row origin shifted: the last / first 9-row window wraps down the plane
+    Wm = 132
+    m = rng.integers(0, 256, (n, H, Wm)).astype(np.uint8)
+    vw = [[3, 5, 0, 0, 0, 0, 0, 0, 0], [0, 0, 1, 7, 0, 0, 0, 0, 0], [0, 0, 0, 0, 0, 7, 1, 0, 0],
+          [0, 0, 0, 0, 0, 0, 0, 5, 3]]
+    tin = ((n, H, Wm), (0, shift, 0), [[1, 0, 0], [0, 9, 0], [0, 0, 1]], [[0], [1], [0]], [9])
+    tout = ((n, H // 9 * 4, Wm), (0, 0, 0), [[1, 0, 0], [0, 4, 0], [0, 0, 1]], [[0], [1], [0]], [4])
+    reps = [n, H // 9, Wm]
+    want = oracle.run_task(m, oracle.make_tiler(*tin), tout[0], oracle.make_tiler(*tout), reps,
+                           oracle.make_stage(9, 9, 0, vw, 8, 4))
+    y = torch.zeros(tout[0], dtype=torch.uint8, device="cuda")
+    ds.run_task(torch.from_numpy(m).cuda(), ds.make_tiler(*tin), y, ds.make_tiler(*tout), reps,
+                ds.make_body(vw, 8, 4, n_in=9))
+    torch.cuda.synchronize()
+    assert np.array_equal(y.cpu().numpy(), want), "V task"
