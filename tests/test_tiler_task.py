@@ -345,3 +345,27 @@ def test_run_task_peeled_wrap(shift):
                 ds.make_body(vw, 8, 4, n_in=9))
     torch.cuda.synchronize()
     assert np.array_equal(y.cpu().numpy(), want), "V task"
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("P,Q", [(4, 1), (8, 3), (12, 5), (16, 8)])
+def test_run_task_dense_large(P, Q):
+    """Large dense tasks (11,100 repetitions: 86 full warps of 128 plus a
+    ragged tail of 92) across pattern sizes 4-16 and 1-8 outputs, divisors on
+    both sides of the exact multiply-high bound."""
+    rng = np.random.default_rng(P * 10 + Q)
+    n, H, Wp = 3, 37, 100                          # 11,100 repetitions
+    W = P * Wp
+    a = rng.integers(0, 256, (n, H, W)).astype(np.uint8)
+    w = [[int(x) for x in rng.integers(-128, 128, P)] for _ in range(Q)]
+    tin = ((n, H, W), (0, 0, 0), [[1, 0, 0], [0, 1, 0], [0, 0, P]], [[0], [0], [1]], [P])
+    tout = ((n, H, Wp * Q), (0, 0, 0), [[1, 0, 0], [0, 1, 0], [0, 0, Q]], [[0], [0], [1]], [Q])
+    reps = [n, H, Wp]
+    for D, B in ((1, 0), (6, 3), (999983, 7)):
+        want = oracle.run_task(a, oracle.make_tiler(*tin), tout[0], oracle.make_tiler(*tout), reps,
+                               oracle.make_stage(P, P, 0, w, D, B))
+        y = torch.zeros(tout[0], dtype=torch.uint8, device="cuda")
+        ds.run_task(torch.from_numpy(a).cuda(), ds.make_tiler(*tin), y, ds.make_tiler(*tout), reps,
+                    ds.make_body(w, D, B, n_in=P))
+        torch.cuda.synchronize()
+        assert np.array_equal(y.cpu().numpy(), want), (P, Q, D, B)
