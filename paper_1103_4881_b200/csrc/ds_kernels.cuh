@@ -9,8 +9,11 @@
 //        warps run the horizontal task (taps S:530) and the vertical
 //        task (taps S:540) on-chip with the u8 intermediate in
 //        registers, stage the output band in shared memory and
-//        write it back with one TMA bulk store.  No tensor cores: this is a
-//        memory-bound stencil.
+//        write it back with one TMA bulk store.  Planes whose rows are not
+//        16-byte multiples ("narrow") or short ("whole-band") stage the whole
+//        band, dead rows included, in one copy; each plan shape gets its own
+//        instantiation (MODES) so unused consumer loops are not compiled in.
+//        No tensor cores: this is a memory-bound stencil.
 //   K-N2 ds_generic_kernel      one thread per output pixel, any stage spec
 //        (halos P > S, origin != 0, any taps), any alignment; follows the
 //        tiler definition e = (o + S r + f) mod n directly.
