@@ -63,11 +63,13 @@ enum { DS_MAX_PATTERN = 16, DS_MAX_OUTPUTS = 8, DS_MAX_PLANES = 3 };
 
 /* Kernel selection (ds_set_kernel / ds_last_kernel). */
 enum {
-    DS_KERNEL_AUTO = 0,     /* fused band kernel when eligible, else generic     */
+    DS_KERNEL_AUTO = 0,     /* K-N1 when eligible, else K-N1g, else K-N2         */
     DS_KERNEL_FUSED = 1,    /* K-N1: TMA-staged fused H+V band kernel            */
     DS_KERNEL_GENERIC = 2,  /* K-N2: one thread per output pixel, any spec       */
     DS_KERNEL_FUSED_GENERAL = 3  /* K-N1g: TMA-staged fused band kernel for any spec:
-                                    halo rows staged in smem, smem intermediate     */
+                                    halo rows staged in smem, smem intermediate,
+                                    runs of bands reusing the V halo, column strips
+                                    for wide planes                                 */
 };
 
 /*
@@ -115,13 +117,16 @@ typedef struct {
                                             SPEC's taps, every plane W % 16 in {0, 8}
                                             (8 also needs in_frame_bytes % 16 == 0),
                                             one 9-row group staged within smem      */
-    int32_t band_groups[DS_MAX_PLANES];  /* K-N1: 9-row groups per work unit     */
+    int32_t band_groups[DS_MAX_PLANES];  /* K-N1: 9-row groups per work unit (band);
+                                            rows < 512 B and W % 16 == 8 planes stage
+                                            the whole band, dead rows included       */
     int64_t units_per_frame;             /* K-N1 work units per frame            */
     int64_t unit_in_bytes_max;           /* K-N1 bytes staged per unit (max)     */
     int64_t unit_out_bytes_max;
     int32_t fused_general_eligible;      /* 1 if K-N1g can run this geometry+spec  */
-    int32_t general_band_reps[DS_MAX_PLANES];  /* K-N1g: V repetitions per unit */
-    int64_t general_units_per_frame;
+    int32_t general_band_reps[DS_MAX_PLANES];  /* K-N1g: V repetitions per band */
+    int64_t general_units_per_frame;     /* K-N1g bands per frame (strips x bands); a
+                                            launch groups them into runs (ds_units)  */
     int64_t general_stage_bytes_max;     /* K-N1g: staged bytes per unit: R rows (band + halo)
                                             at a pitch of round_up(W, 16) + 32 (wrap pad), or
                                             a column strip's window pitch */
