@@ -313,6 +313,18 @@ def run_reference(args):
 
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # `python bench.py --gpus N` outside torchrun: re-launch as N ranks on
+        # this node (the same launch the driver uses), rendezvous on 127.0.0.1
+        import socket
+
+        with socket.socket() as sock:
+            sock.bind(("127.0.0.1", 0))
+            port = sock.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__),
+               *sys.argv[1:]]
+        os.execv(sys.executable, cmd)
     if args.impl == "reference":
         return run_reference(args)
 
