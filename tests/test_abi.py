@@ -215,3 +215,56 @@ def test_plan_general_column_strips():
     p4k = ds.ds_plan(3840, 2160, 3, spec)
     assert p4k.general_strips[0] > 1 and p4k.general_stage_bytes_max <= 28 * 1024
     assert ds.ds_plan(352, 288, 3, spec).general_strips[0] == 1
+
+
+def test_plan_invariants_random():
+    """Host planners (K-N1 bands, K-N1g bands / strips) on random valid
+    geometries and specs: exact band tiling of every plane, unit counts,
+    staging within shared memory, strips only for wide planes."""
+    import numpy as np
+    rng = np.random.default_rng(7)
+    checked = 0
+    for _ in range(300):
+        ch = int(rng.choice([1, 3]))
+        chroma = int(rng.integers(0, 2))
+        h = None if rng.random() < 0.3 else dict(
+            pattern=int(rng.integers(1, 17)), paving=int(rng.choice([2, 4, 8, 16])), origin=int(rng.integers(-9, 9)),
+            weights=[[1, 2, 1]], divisor=4, bias=2)
+        v = None if rng.random() < 0.3 else dict(
+            pattern=int(rng.integers(1, 17)), paving=int(rng.choice([3, 6, 9, 12])), origin=int(rng.integers(-9, 9)),
+            weights=[[1, 2, 1]], divisor=4, bias=2)
+        sh = 8 if h is None else h["paving"]
+        sv = 9 if v is None else v["paving"]
+        mw = sh * (2 if ch == 3 and chroma else 1)
+        mh = sv * (2 if ch == 3 and chroma else 1)
+        W = mw * int(rng.integers(1, max(2, 8000 // mw)))
+        H = mh * int(rng.integers(1, max(2, 2200 // mh)))
+        spec = ds.make_spec(h=h, v=v, chroma=chroma)
+        try:
+            p = ds.ds_plan(W, H, ch, spec)
+        except ds.DSError:
+            continue
+        n = p.n_planes
+        if p.fused_eligible:
+            units = 0
+            for q in range(n):
+                k = p.band_groups[q]
+                assert k >= 1 and (p.in_h[q] // 9) % k == 0
+                units += p.in_h[q] // (9 * k)
+            assert units == p.units_per_frame
+            assert p.unit_in_bytes_max <= 227 * 1024
+        if p.fused_general_eligible:
+            units = 0
+            for q in range(n):
+                k, s = p.general_band_reps[q], p.general_strips[q]
+                G = p.in_h[q] // sv
+                assert k >= 1 and G % k == 0 and s >= 1
+                units += s * (G // k)
+                if s > 1:                                   # strips only when a whole-row band is too big
+                    pv = 9 if v is None else v["pattern"]
+                    target = 28 * 1024 if pv > sv else 40 * 1024
+                    assert pv * ((p.in_w[q] + 15) // 16 * 16 + 32) > target
+            assert units == p.general_units_per_frame
+            assert p.general_stage_bytes_max <= 227 * 1024
+        checked += 1
+    assert checked >= 150
