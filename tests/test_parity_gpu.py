@@ -470,6 +470,26 @@ def test_run_host_pinned_and_pageable():
         _assert_same(hout.numpy(), want, f"host pinned={pinned}")
 
 
+def test_run_host_general_spec():
+    """The host path under a halo spec (K-N1g; every input row crosses PCIe,
+    since only SPEC's taps have a dead row), chunked, pinned and pageable."""
+    W, H = 352, 288
+    hd, vd = _halo_spec()
+    d = ds.Downscaler(W, H, 3, spec=ds.make_spec(h=hd, v=vd, chroma=ds.DS_CHROMA_420))
+    n = 20
+    fr = synth.random_frames(21, 0, n, W, H)
+    want = oracle.execute_frames(fr, W, H, 3, 1, _oracle_stage(hd), _oracle_stage(vd))
+    for pinned in (True, False):
+        hin = torch.from_numpy(fr)
+        if pinned:
+            hin = hin.pin_memory()
+        d.set_host_chunk(6)
+        hout = d.run_host(hin)
+        torch.cuda.current_stream().synchronize()
+        assert d.last_kernel() == ds.DS_KERNEL_FUSED_GENERAL
+        _assert_same(hout.numpy(), want, f"host halo pinned={pinned}")
+
+
 def test_run_host_hd_auto_chunk():
     W, H = 1920, 1080
     d = ds.Downscaler(W, H, 3)
