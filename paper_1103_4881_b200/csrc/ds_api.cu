@@ -541,7 +541,7 @@ int configure_general(ds_handle* h) {
     // 2 CTAs x 8 consumer warps per SM with a 2-deep ring beat deeper rings
     // and 16-warp CTAs
     c.stages = 2;
-    c.ncw = 8;
+    c.ncw = DS_GEN_NCW;
 #ifndef DS_GEN_CTAS
 #define DS_GEN_CTAS 2
 #endif
@@ -618,7 +618,7 @@ int launch_general(ds_handle* h, const uint8_t* in, int64_t n, uint8_t* out, cud
         P.sw = gg.sw;
         P.runs = (P.nb + P.L - 1) / P.L;
         P.runs_rcp = rcp32(P.runs);
-        auto groups = [](int np) { return np <= 8 * 32 ? (8 * 32) / np : 1; };   // consumer threads / np
+        auto groups = [](int np) { return np <= DS_GEN_NCW * 32 ? (DS_GEN_NCW * 32) / np : 1; };   // threads / np
         if (gg.strips > 1) {
             // per-strip geometry: regular strips (sw repetitions) and the last one
             P.np_rcp = rcp32(gg.sw);

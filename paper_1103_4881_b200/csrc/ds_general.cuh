@@ -40,6 +40,9 @@
 #ifndef DS_GEN_MINB
 #define DS_GEN_MINB 2
 #endif
+#ifndef DS_GEN_NCW
+#define DS_GEN_NCW 8              // consumer warps per CTA
+#endif
 
 namespace ds {
 
@@ -417,8 +420,9 @@ struct GenCursor {
 // split across 4 SMSPs, so 18 warps need <= 102 registers each.
 
 template <int FAST>
-__global__ void __launch_bounds__(9 * 32, DS_GEN_MINB) ds_fused_general_kernel(const __grid_constant__ GeneralParams p) {
-    constexpr int NCW = 8;
+__global__ void __launch_bounds__((DS_GEN_NCW + 1) * 32, DS_GEN_MINB)
+    ds_fused_general_kernel(const __grid_constant__ GeneralParams p) {
+    constexpr int NCW = DS_GEN_NCW;
     extern __shared__ __align__(1024) uint8_t smem[];
     constexpr int NC = NCW * 32;
     const int S = p.stages;
