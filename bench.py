@@ -65,6 +65,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--gather", action="store_true", help="N>1: time the NCCL gather to rank 0")
+    ap.add_argument("--fused-gather", action="store_true",
+                    help="N>1: time ds_run writing straight into rank 0's buffer (CUDA IPC / NVLink)")
     return ap.parse_args()
 
 
@@ -449,6 +451,31 @@ def main():
         dist.all_reduce(gt, op=dist.ReduceOp.MAX)
         gather_ms = float(gt[0]) * 1e3
 
+    # ---- optional fused compute + gather: each rank's kernel stores its
+    # frames straight into rank 0's output buffer (CUDA IPC, NVLink P2P) -----
+    gather_fused_ms = None
+    if world > 1 and args.fused_gather:
+        from paper_1103_4881_b200.dist import share_rank0_tensor
+
+        full = (torch.empty((cfg["total"], fout), dtype=torch.uint8, device=dev) if rank == 0 else None)
+        full = share_rank0_tensor(full)
+        view = full[lo:hi]
+        d(x, view)                                     # warm (peer access enabled on first use)
+        torch.cuda.synchronize()
+        dist.barrier()
+        ks = max(1, args.e2e_steps)
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(ks):
+            d(x, view)
+        f1.record(stream)
+        torch.cuda.synchronize()
+        ft = torch.tensor([f0.elapsed_time(f1) / ks], dtype=torch.float64, device=coll_dev)
+        dist.all_reduce(ft, op=dist.ReduceOp.MAX)
+        gather_fused_ms = float(ft[0])
+        dist.barrier()
+        del view, full
+
     # ---- e2e: host pinned frames -> ds_run_host -> host, copies timed -------
     e2e = None
     if not args.no_e2e:
@@ -535,6 +562,7 @@ def main():
             "gpu_launches": args.steps,
             "clocks": clk.result(),
             "gather_ms": gather_ms,
+            "gather_fused_ms": gather_fused_ms,
             "timing": ("one CUDA graph of the K ds_run calls, replayed between two events"
                        if args.graph else "CUDA events around each ds_run on the launching stream"),
             "host_call_us": host_call_us,

@@ -156,13 +156,19 @@ DS_API ds_handle* ds_create(int32_t frame_w, int32_t frame_h, int32_t channels,
  *   in_frames : device pointer, n_frames * ds_in_frame_bytes(h) bytes, read
  *               only ("const", the read-only flowPort of P:132-135)
  *   out_frames: device pointer, n_frames * ds_out_frame_bytes(h) bytes
- * Both on the handle's device, caller-owned, not retained, must not
+ * in_frames on the handle's device; out_frames on it or on a peer GPU the
+ * handle's device can access (NVLink P2P, e.g. another rank's buffer
+ * mapped with CUDA IPC; peer access is enabled on first use): the kernel's
+ * output stores then travel over NVLink, fusing the gather of frame shards
+ * into the filtering.  Caller-owned, not retained, must not
  * overlap and must stay alive until work on `stream` completes.
  * Asynchronous on `stream`; faults surface at the caller's sync.
  * n_frames == 0 is a successful no-op.  Any alignment is accepted
- * (misalignment selects K-N2, never an error).
+ * (misalignment selects K-N1g's plain-load staging or plain stores, never
+ * an error).
  * Returns DS_OK, DS_EINVAL (NULL handle/pointer with n > 0, n < 0,
- * overlapping ranges, pointer not on the handle's device) or DS_ECUDA. */
+ * overlapping ranges, pointer neither on the handle's device nor on a
+ * reachable peer) or DS_ECUDA. */
 DS_API int ds_run(ds_handle* h, const uint8_t* in_frames, int64_t n_frames,
                   uint8_t* out_frames, ds_stream_t stream);
 

@@ -692,6 +692,32 @@ bool device_ptr_on(const void* p, int dev) {
     return a.device == dev;
 }
 
+// Output memory the kernels on `dev` may write: device memory of `dev`, or of
+// a peer GPU that `dev` can reach over NVLink / PCIe P2P (e.g. another rank's
+// buffer mapped with CUDA IPC: the fused compute + gather of dist.py).  Peer
+// access is enabled on first use.
+bool device_or_peer_ptr(const void* p, int dev) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    if (a.type != cudaMemoryTypeDevice && a.type != cudaMemoryTypeManaged) return false;
+    if (a.device == dev) return true;
+    int can = 0;
+    if (cudaDeviceCanAccessPeer(&can, dev, a.device) != cudaSuccess || !can) {
+        cudaGetLastError();
+        return false;
+    }
+    const cudaError_t e = cudaDeviceEnablePeerAccess(a.device, 0);   // current device is dev
+    if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) {
+        cudaGetLastError();
+        return false;
+    }
+    cudaGetLastError();                            // clear "already enabled"
+    return true;
+}
+
 bool ranges_overlap(const void* a, int64_t na, const void* b, int64_t nb) {
     const uintptr_t x = reinterpret_cast<uintptr_t>(a), y = reinterpret_cast<uintptr_t>(b);
     return x < y + (uintptr_t)nb && y < x + (uintptr_t)na;
@@ -820,7 +846,7 @@ DS_API int ds_run(ds_handle* h, const uint8_t* in, int64_t n, uint8_t* out, ds_s
     if (ranges_overlap(in, nin, out, nout)) return DS_EINVAL;
     DeviceGuard g(h->device);
     if (!g.ok) { cudaGetLastError(); return DS_ECUDA; }
-    if (!device_ptr_on(in, h->device) || !device_ptr_on(out, h->device)) return DS_EINVAL;
+    if (!device_ptr_on(in, h->device) || !device_or_peer_ptr(out, h->device)) return DS_EINVAL;
     return run_device(h, in, n, out, reinterpret_cast<cudaStream_t>(stream));
 }
 

@@ -135,6 +135,7 @@ void default_spec(ds_filter_spec* s);
 bool stage_equal(const ds_stage_spec& a, const ds_stage_spec& b);
 bool aligned16(const void* p);
 bool device_ptr_on(const void* p, int dev);
+bool device_or_peer_ptr(const void* p, int dev);
 bool ranges_overlap(const void* a, int64_t na, const void* b, int64_t nb);
 int run_device(ds_handle* h, const uint8_t* in, int64_t n, uint8_t* out, cudaStream_t st);
 void free_sched_state(ds_handle* h);

@@ -4,7 +4,11 @@ Frames carry no state between them ("no inter-frame
 state"), so rank r of P owns the contiguous block
 [floor(r N / P), floor((r+1) N / P)) and filters it with no communication.
 The only collective is the final gather of output shards to rank 0, in rank
-(= frame) order, over NCCL (NVLink/NVSwitch) -- never inside the filter.
+(= frame) order, over NCCL (NVLink/NVSwitch) -- never inside the filter.  The
+fused variant (run_sharded_fused_gather) has no separate gather at all: rank 0
+shares its output buffer through CUDA IPC and every rank's ds_run stores its
+frames straight into it over NVLink, so the transfer overlaps the filtering
+unit by unit.
 
 Host-side logic only; the per-rank compute is ds_run (Downscaler).  The
 gather works with any torch.distributed backend (NCCL on GPUs, gloo in the
@@ -74,3 +78,44 @@ def run_sharded(total_frames: int, w: int, h: int, channels: int = 3, chroma: st
     elif gather:
         full = y
     return full, y, (lo, hi)
+
+
+def share_rank0_tensor(t, group=None):
+    """Rank 0's CUDA tensor, mapped into every rank (CUDA IPC; torch's own
+    tensor-sharing reduction, the handle broadcast through the process
+    group).  Returns the local view (rank 0: t itself)."""
+    from torch.multiprocessing.reductions import reduce_tensor
+
+    rank = dist.get_rank(group)
+    obj = [reduce_tensor(t) if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    if rank == 0:
+        return t
+    fn, args = obj[0]
+    return fn(*args)
+
+
+def run_sharded_fused_gather(total_frames: int, w: int, h: int, channels: int = 3, chroma: str = "420",
+                             seed: int = 1, spec=None):
+    """Frame-sharded downscaling whose gather is fused into the kernels: rank
+    0 allocates the whole output; each rank maps it (CUDA IPC) and runs ds_run
+    with its slice [lo, hi) of that buffer as the output, so the bulk stores
+    of the output bands go to rank 0's HBM over NVLink while the rank is
+    still filtering.  Ranks never wait on one another inside the kernel; one
+    host barrier after the local synchronize ends the step.
+
+    Returns (rank-0 full output or None, (lo, hi))."""
+    from . import Downscaler, generate_frames
+
+    world = dist.get_world_size()
+    rank = dist.get_rank()
+    lo, hi = shard_range(total_frames, world, rank)
+    d = Downscaler(w, h, channels, chroma=chroma, spec=spec)
+    x = generate_frames(hi - lo, d.in_frame_bytes, seed=seed, first_frame=lo)
+    full = torch.empty((total_frames, d.out_frame_bytes), dtype=torch.uint8, device="cuda") if rank == 0 else None
+    full = share_rank0_tensor(full)
+    if hi > lo:
+        d(x, out=full[lo:hi])
+    torch.cuda.synchronize()
+    dist.barrier()
+    return (full if rank == 0 else None), (lo, hi)

@@ -1,6 +1,7 @@
 """torchrun worker for tests/test_dist_gpu.py: frame-sharded downscaling
-(paper_1103_4881_b200.dist.run_sharded) + gather to rank 0, which saves the
-gathered stream.  Launched with DS_DIST_BACKEND=gloo so several ranks can
+(paper_1103_4881_b200.dist.run_sharded) + gather to rank 0, or with argv[5] ==
+"fused" the gather fused into the kernels (run_sharded_fused_gather: every
+rank writes into rank 0's buffer through CUDA IPC); rank 0 saves the stream.  Launched with DS_DIST_BACKEND=gloo so several ranks can
 share one GPU (their kernels never wait on one another)."""
 import os
 import sys
@@ -10,14 +11,18 @@ import numpy as np
 import torch
 import torch.distributed as dist
 
-from paper_1103_4881_b200.dist import run_sharded
+from paper_1103_4881_b200.dist import run_sharded, run_sharded_fused_gather
 
 total, W, H, out_path = int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3]), sys.argv[4]
+mode = sys.argv[5] if len(sys.argv) > 5 else "nccl"
 backend = os.environ.get("DS_DIST_BACKEND", "nccl")
 local = int(os.environ.get("LOCAL_RANK", "0"))
 torch.cuda.set_device(local % torch.cuda.device_count())
 dist.init_process_group(backend)
-full, mine, (lo, hi) = run_sharded(total, W, H, 3, seed=3)
+if mode == "fused":
+    full, (lo, hi) = run_sharded_fused_gather(total, W, H, 3, seed=3)
+else:
+    full, mine, (lo, hi) = run_sharded(total, W, H, 3, seed=3)
 torch.cuda.synchronize()
 if dist.get_rank() == 0:
     np.save(out_path, full.cpu().numpy())

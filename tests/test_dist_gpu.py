@@ -24,8 +24,13 @@ def _port():
     return p
 
 
+@pytest.mark.parametrize("mode", ["nccl", "fused"])
 @pytest.mark.parametrize("ranks,total", [(2, 7), (3, 5)])
-def test_torchrun_sharded_gather(tmp_path, ranks, total):
+def test_torchrun_sharded_gather(tmp_path, ranks, total, mode):
+    """Frame-sharded runs gathered to rank 0 equal the 1-GPU run and the
+    oracle.  mode "fused": no separate gather -- every rank's ds_run writes
+    its frames into rank 0's buffer mapped through CUDA IPC (on one GPU the
+    ranks share the device; the kernels never wait on one another)."""
     torch = pytest.importorskip("torch")
     import paper_1103_4881_b200 as ds
 
@@ -34,7 +39,7 @@ def test_torchrun_sharded_gather(tmp_path, ranks, total):
     env = dict(os.environ, DS_DIST_BACKEND="gloo")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={ranks}",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()),
-           os.path.join(ROOT, "tests", "dist_worker.py"), str(total), str(W), str(H), out]
+           os.path.join(ROOT, "tests", "dist_worker.py"), str(total), str(W), str(H), out, mode]
     r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
     got = np.load(out)
