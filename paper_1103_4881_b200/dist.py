@@ -81,18 +81,22 @@ def run_sharded(total_frames: int, w: int, h: int, channels: int = 3, chroma: st
 
 
 def share_rank0_tensor(t, group=None):
-    """Rank 0's CUDA tensor, mapped into every rank (CUDA IPC; torch's own
-    tensor-sharing reduction, the handle broadcast through the process
-    group).  Returns the local view (rank 0: t itself)."""
-    from torch.multiprocessing.reductions import reduce_tensor
+    """Rank 0's tensor, mapped into every rank: serialised with the
+    multiprocessing pickler torch registers its sharing reductions with (a
+    CUDA tensor becomes a CUDA IPC handle; a CPU tensor a shared-memory name
+    under the file_system sharing strategy), the bytes broadcast through the
+    process group.  Returns the local view (rank 0: t itself)."""
+    import pickle
+    from multiprocessing.reduction import ForkingPickler
+
+    import torch.multiprocessing  # noqa: F401  (registers torch's reductions)
 
     rank = dist.get_rank(group)
-    obj = [reduce_tensor(t) if rank == 0 else None]
+    obj = [bytes(ForkingPickler.dumps(t)) if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0, group=group)
     if rank == 0:
         return t
-    fn, args = obj[0]
-    return fn(*args)
+    return pickle.loads(obj[0])
 
 
 def run_sharded_fused_gather(total_frames: int, w: int, h: int, channels: int = 3, chroma: str = "420",

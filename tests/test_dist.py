@@ -80,3 +80,42 @@ def test_gloo_sharded_equals_unsharded(world, total):
     want = oracle.execute_frames(synth.random_frames(5, 0, total, W, H), W, H)
     assert got.shape == want.shape
     assert np.array_equal(got, want)
+
+
+def _share_worker(rank, world, port, total, q):
+    from paper_1103_4881_b200.dist import share_rank0_tensor
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    # CPU storages travel by shared-memory name under the file_system strategy
+    # (the default passes file descriptors, which plain pickling cannot carry);
+    # CUDA tensors carry a CUDA IPC handle either way
+    mp.set_sharing_strategy("file_system")
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        full = torch.zeros((total, 4), dtype=torch.uint8).share_memory_() if rank == 0 else None
+        full = share_rank0_tensor(full)                   # every rank maps rank 0's buffer
+        lo, hi = shard_range(total, world, rank)
+        full[lo:hi] = rank + 1                            # each rank writes its own slice in place
+        dist.barrier()
+        if rank == 0:
+            q.put(full.numpy().copy())
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,total", [(2, 7), (3, 10)])
+def test_share_rank0_tensor_writes_land_in_rank0(world, total):
+    """The buffer sharing behind the fused gather (dist.share_rank0_tensor):
+    writes each rank makes into its slice of the mapped tensor are rank 0's
+    data, with no gather.  On the CPU the mapping is shared memory; ds_run
+    uses the same reduction for CUDA tensors (CUDA IPC)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    mp.spawn(_share_worker, args=(world, _free_port(), total, q), nprocs=world, join=True)
+    got = q.get()
+    want = np.zeros((total, 4), np.uint8)
+    for r in range(world):
+        lo, hi = shard_range(total, world, r)
+        want[lo:hi] = r + 1
+    assert np.array_equal(got, want)
