@@ -56,9 +56,12 @@ def parse():
     ap.add_argument("--ctas", type=int, default=0)
     ap.add_argument("--kernel", choices=["auto", "fused", "fused_general", "generic"], default="auto")
     ap.add_argument("--band-bytes", type=int, default=0, help="K-N1 band size (0 = default)")
-    ap.add_argument("--graph", action="store_true",
-                    help="capture the K timed ds_run calls in one CUDA graph and replay it "
-                         "(removes host launch overhead; for the launch-bound 1-frame config)")
+    ap.add_argument("--graph", dest="graph", action="store_true", default=True,
+                    help="(default) capture the K timed ds_run calls in one CUDA graph and time one "
+                         "replay: every step is still a full launch over the batch, without host "
+                         "launch gaps or per-step event records between them")
+    ap.add_argument("--no-graph", dest="graph", action="store_false",
+                    help="time each ds_run between its own CUDA events (per-launch median / best)")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
                     help="CPU-oracle sample budget (seconds of 1-core work)")
