@@ -1,0 +1,76 @@
+"""bench.py's JSON contract: the reference arm (the CPU oracle, runs here)
+and the workload / scaling labels on the CPU; the full line on the GPU."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+from conftest import ROOT
+
+BENCH = os.path.join(ROOT, "bench.py")
+
+
+def _line(args, timeout=600):
+    r = subprocess.run([sys.executable, BENCH, *args], capture_output=True, text=True, timeout=timeout,
+                       cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    return json.loads(lines[0])
+
+
+def test_reference_arm_line():
+    """--impl reference: the oracle as it stands, one frame per step, on one
+    core; the line carries the contract keys with e2e bytes zero."""
+    j = _line(["--impl", "reference", "--config", "qcif420", "--steps", "3", "--warmup", "1"])
+    assert j["impl"] == "reference" and j["unit"] == "frames/s" and j["value"] > 0
+    assert j["higher_is_better"] is True and j["n_gpus"] == 1 and j["steps"] == 3
+    cb = j["cpu_baseline"]
+    assert cb["kind"] == "oracle" and cb["cores"] == 1 and cb["value"] == j["value"] and cb["sample"]
+    assert j["e2e"] == {"value": j["value"], "unit": "frames/s", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}
+    assert "workload" in j["config"]
+
+
+def test_workload_labels():
+    """Weak scaling by default (300 HD frames per GPU; N = 1 is configs[2]),
+    --frames fixes the total (strong at N > 1); 4K is configs[4] per GPU."""
+    sys.path.insert(0, ROOT)
+    import bench
+
+    ns = lambda **kw: type("A", (), dict(dict(config="hd420", frames=0), **kw))()   # noqa: E731
+    w1 = bench.workload(ns(), 1)
+    assert w1["total"] == 300 and w1["scaling"] == "weak" and w1["name"].startswith("configs[2]")
+    w8 = bench.workload(ns(), 8)
+    assert w8["total"] == 2400 and w8["scaling"] == "weak"
+    s8 = bench.workload(ns(frames=3000), 8)
+    assert s8["total"] == 3000 and s8["scaling"] == "strong" and s8["name"].startswith("configs[3]")
+    k1 = bench.workload(ns(config="4k420"), 1)
+    assert k1["total"] == 1000 and k1["name"].startswith("configs[4]")
+    one = bench.workload(ns(frames=1), 1)
+    assert one["name"].startswith("configs[1]")
+
+
+@pytest.mark.gpu
+def test_bench_line_contract():
+    """The default arm's line on a B200: every contract key, a roofline for
+    the fused kernel, e2e through the host path, clocks sampled during the
+    timed region, K launches."""
+    j = _line(["--steps", "20", "--warmup", "3", "--cpu-seconds", "2"])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+              "scaling", "vs_baseline", "dtype", "data", "config", "roofline", "e2e", "cpu_baseline",
+              "gpu_launches", "clocks"):
+        assert k in j, k
+    assert j["steps"] == 20 and j["warmup"] >= 3 and j["gpu_launches"] == 20 and j["dtype"] == "u8"
+    r = j["roofline"]
+    assert r["bound"] == "hbm" and r["unit"] == "GB/s" and r["achieved"] > 0 and r["peak"] > 0
+    assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9
+    e = j["e2e"]
+    assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
+    assert e["matches_device_path"] is True
+    c = j["clocks"]
+    assert c["sm_max_mhz"] > 0 and isinstance(c["reasons"], list)
+    cb = j["cpu_baseline"]
+    assert cb["kind"] == "oracle" and cb["parity_bit_exact_frames"] == cb["parity_checked_frames"] > 0
