@@ -284,14 +284,14 @@ __global__ void __launch_bounds__(256) ds_task_affine_kernel(const __grid_consta
 // streaming map.  Each lane takes 4 consecutive repetitions (16-byte loads);
 // the warp stages its 128 Q output bytes in shared memory and writes them as
 // coalesced words.  Repetitions past the last full warp use task_affine.
-template <int NI>
+template <int NI, int Q>
 __global__ void __launch_bounds__(256) ds_task_dense_kernel(const __grid_constant__ TaskParams p) {
-    __shared__ __align__(16) uint8_t buf[8][128 * DS_MAX_OUTPUTS];
+    __shared__ __align__(16) uint32_t buf[8][32 * Q];
     const int lane = threadIdx.x & 31;
-    uint8_t* b = buf[threadIdx.x >> 5];
-    const uint32_t Q = (uint32_t)p.n_out;
+    uint32_t* b = buf[threadIdx.x >> 5];
     const uint32_t full = (uint32_t)(p.n_reps / 128);
     const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+    const int32_t b0 = p.fastdiv ? p.fbias : p.bias;
     for (uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < full; w += nw) {
         const uint32_t rep0 = w * 128 + 4 * lane;
         const uint4* src = reinterpret_cast<const uint4*>(p.in + p.in_A + (uint32_t)NI * rep0);
@@ -301,22 +301,26 @@ __global__ void __launch_bounds__(256) ds_task_dense_kernel(const __grid_constan
             const uint4 v = __ldg(src + i);
             x[4 * i] = v.x; x[4 * i + 1] = v.y; x[4 * i + 2] = v.z; x[4 * i + 3] = v.w;
         }
+        // the lane's 4 repetitions x Q outputs are 4 Q consecutive bytes: Q words
+        uint32_t ow[Q];
+#pragma unroll
+        for (int j = 0; j < Q; ++j) ow[j] = 0;
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
 #pragma unroll
-            for (int k = 0; k < DS_MAX_OUTPUTS; ++k) {
-                if (k < (int)Q) {
-                    int32_t acc = p.fastdiv ? p.fbias : p.bias;
+            for (int k = 0; k < Q; ++k) {
+                int32_t acc = b0;
 #pragma unroll
-                    for (int i = 0; i < NI / 4; ++i) acc = t_dp4a(x[r * (NI / 4) + i], p.wp[k][i], acc);
-                    b[(4 * lane + r) * Q + k] = t_out(p, acc);
-                }
+                for (int i = 0; i < NI / 4; ++i) acc = t_dp4a(x[r * (NI / 4) + i], p.wp[k][i], acc);
+                ow[(r * Q + k) >> 2] |= (uint32_t)t_out(p, acc) << (8 * ((r * Q + k) & 3));
             }
         }
+#pragma unroll
+        for (int j = 0; j < Q; ++j) b[lane * Q + j] = ow[j];
         __syncwarp();
         uint32_t* dst = reinterpret_cast<uint32_t*>(p.out + p.out_A + Q * 128 * w);
-        const uint32_t* bw = reinterpret_cast<const uint32_t*>(b);
-        for (uint32_t j = lane; j < 32 * Q; j += 32) dst[j] = bw[j];
+#pragma unroll
+        for (int j = 0; j < Q; ++j) dst[lane + 32 * j] = b[lane + 32 * j];
         __syncwarp();
     }
     const uint32_t stride = gridDim.x * blockDim.x;
@@ -407,12 +411,25 @@ TaskFn cols_fn(int ni) {
         default: return ds_task_cols_kernel<4>;
     }
 }
-TaskFn dense_fn(int ni) {
+template <int NI>
+TaskFn dense_fn_q(int q) {
+    switch (q) {
+        case 1: return ds_task_dense_kernel<NI, 1>;
+        case 2: return ds_task_dense_kernel<NI, 2>;
+        case 3: return ds_task_dense_kernel<NI, 3>;
+        case 4: return ds_task_dense_kernel<NI, 4>;
+        case 5: return ds_task_dense_kernel<NI, 5>;
+        case 6: return ds_task_dense_kernel<NI, 6>;
+        case 7: return ds_task_dense_kernel<NI, 7>;
+        default: return ds_task_dense_kernel<NI, 8>;
+    }
+}
+TaskFn dense_fn(int ni, int no) {
     switch ((ni + 3) / 4) {
-        case 1: return ds_task_dense_kernel<4>;
-        case 2: return ds_task_dense_kernel<8>;
-        case 3: return ds_task_dense_kernel<12>;
-        default: return ds_task_dense_kernel<16>;
+        case 1: return dense_fn_q<4>(no);
+        case 2: return dense_fn_q<8>(no);
+        case 3: return dense_fn_q<12>(no);
+        default: return dense_fn_q<16>(no);
     }
 }
 TaskFn affine_fn(int ni, bool words) {
@@ -774,7 +791,7 @@ int launch_task(const uint8_t* in, const ds_tiler& t_in, uint8_t* out, const ds_
             }
         }
     }
-    const TaskFn fn = p.dense ? dense_fn(p.n_in)
+    const TaskFn fn = p.dense ? dense_fn(p.n_in, p.n_out)
                       : p.affine == 3 ? cols_fn(p.n_in)
                       : p.affine ? affine_fn(p.n_in, p.affine == 2) : modulo_fn(p.n_in);
     if (policy == DS_TOPO_SPEC) {
