@@ -16,10 +16,6 @@
 #include "ds.h"
 #include "ds_internal.h"
 
-#ifndef DS_COLS_MINB
-#define DS_COLS_MINB 4
-#endif
-
 namespace {
 
 struct TTiler {
@@ -347,12 +343,12 @@ __device__ __forceinline__ void cols_load(const TaskParams& p, uint32_t q4, uint
         x[e] = (e < p.n_in && ((p.in_live >> e) & 1u))
                    ? __ldg(reinterpret_cast<const uint32_t*>(p.in + bi + p.in_b[e])) : 0u;
 }
-template <int NB>
+template <int NB, int Q>
 __device__ __forceinline__ void cols_compute(const TaskParams& p, const uint32_t (&x)[4 * NB], uint32_t bo) {
-    int32_t acc[DS_MAX_OUTPUTS][4];
+    int32_t acc[Q][4];
     const int32_t b0 = p.fastdiv ? p.fbias : p.bias;
 #pragma unroll
-    for (int k = 0; k < DS_MAX_OUTPUTS; ++k)
+    for (int k = 0; k < Q; ++k)
 #pragma unroll
         for (int c = 0; c < 4; ++c) acc[k][c] = b0;
 #pragma unroll
@@ -363,23 +359,19 @@ __device__ __forceinline__ void cols_compute(const TaskParams& p, const uint32_t
         const uint32_t c0 = __byte_perm(ta, tb, 0x5410), c1 = __byte_perm(ta, tb, 0x7632),
                        c2 = __byte_perm(tc, td, 0x5410), c3 = __byte_perm(tc, td, 0x7632);
 #pragma unroll
-        for (int k = 0; k < DS_MAX_OUTPUTS; ++k) {
-            if (k < p.n_out) {
-                const uint32_t wq = p.wp[k][b];
-                acc[k][0] = t_dp4a(c0, wq, acc[k][0]);
-                acc[k][1] = t_dp4a(c1, wq, acc[k][1]);
-                acc[k][2] = t_dp4a(c2, wq, acc[k][2]);
-                acc[k][3] = t_dp4a(c3, wq, acc[k][3]);
-            }
+        for (int k = 0; k < Q; ++k) {
+            const uint32_t wq = p.wp[k][b];
+            acc[k][0] = t_dp4a(c0, wq, acc[k][0]);
+            acc[k][1] = t_dp4a(c1, wq, acc[k][1]);
+            acc[k][2] = t_dp4a(c2, wq, acc[k][2]);
+            acc[k][3] = t_dp4a(c3, wq, acc[k][3]);
         }
     }
 #pragma unroll
-    for (int k = 0; k < DS_MAX_OUTPUTS; ++k) {
-        if (k < p.n_out) {
-            const uint32_t o = (uint32_t)t_out(p, acc[k][0]) | ((uint32_t)t_out(p, acc[k][1]) << 8) |
-                               ((uint32_t)t_out(p, acc[k][2]) << 16) | ((uint32_t)t_out(p, acc[k][3]) << 24);
-            *reinterpret_cast<uint32_t*>(p.out + bo + p.out_b[k]) = o;
-        }
+    for (int k = 0; k < Q; ++k) {
+        const uint32_t o = (uint32_t)t_out(p, acc[k][0]) | ((uint32_t)t_out(p, acc[k][1]) << 8) |
+                           ((uint32_t)t_out(p, acc[k][2]) << 16) | ((uint32_t)t_out(p, acc[k][3]) << 24);
+        *reinterpret_cast<uint32_t*>(p.out + bo + p.out_b[k]) = o;
     }
 }
 
@@ -391,24 +383,40 @@ __device__ __forceinline__ void cols_compute(const TaskParams& p, const uint32_t
 // repetition), and output element k of the 4 repetitions is one word store.
 // This is the shape of the paper's V task (9 rows down a column -> 4 rows).
 // (Two quads per thread step measured slower: 64-99 registers, spills.)
-template <int NB>
-__global__ void __launch_bounds__(256, DS_COLS_MINB) ds_task_cols_kernel(const __grid_constant__ TaskParams p) {
+// registers scale with the live words (4 NB) and accumulators (4 Q): small
+// shapes (the paper's V task: NB 3, Q 4) run 8 blocks per SM, large ones fewer
+constexpr int cols_minb(int nb, int q) { return nb * q <= 12 ? 8 : nb * q <= 24 ? 6 : 4; }
+template <int NB, int Q>
+__global__ void __launch_bounds__(256, cols_minb(NB, Q)) ds_task_cols_kernel(const __grid_constant__ TaskParams p) {
     const uint32_t quads = (uint32_t)(p.n_reps >> 2);
     const uint32_t stride = gridDim.x * blockDim.x;
     for (uint32_t q4 = blockIdx.x * blockDim.x + threadIdx.x; q4 < quads; q4 += stride) {
         uint32_t x[4 * NB], bo;
         cols_load<NB>(p, q4, x, bo);
-        cols_compute<NB>(p, x, bo);
+        cols_compute<NB, Q>(p, x, bo);
     }
 }
 
 using TaskFn = void (*)(const TaskParams);
-TaskFn cols_fn(int ni) {
+template <int NB>
+TaskFn cols_fn_q(int q) {
+    switch (q) {
+        case 1: return ds_task_cols_kernel<NB, 1>;
+        case 2: return ds_task_cols_kernel<NB, 2>;
+        case 3: return ds_task_cols_kernel<NB, 3>;
+        case 4: return ds_task_cols_kernel<NB, 4>;
+        case 5: return ds_task_cols_kernel<NB, 5>;
+        case 6: return ds_task_cols_kernel<NB, 6>;
+        case 7: return ds_task_cols_kernel<NB, 7>;
+        default: return ds_task_cols_kernel<NB, 8>;
+    }
+}
+TaskFn cols_fn(int ni, int no) {
     switch ((ni + 3) / 4) {
-        case 1: return ds_task_cols_kernel<1>;
-        case 2: return ds_task_cols_kernel<2>;
-        case 3: return ds_task_cols_kernel<3>;
-        default: return ds_task_cols_kernel<4>;
+        case 1: return cols_fn_q<1>(no);
+        case 2: return cols_fn_q<2>(no);
+        case 3: return cols_fn_q<3>(no);
+        default: return cols_fn_q<4>(no);
     }
 }
 template <int NI>
@@ -792,7 +800,7 @@ int launch_task(const uint8_t* in, const ds_tiler& t_in, uint8_t* out, const ds_
         }
     }
     const TaskFn fn = p.dense ? dense_fn(p.n_in, p.n_out)
-                      : p.affine == 3 ? cols_fn(p.n_in)
+                      : p.affine == 3 ? cols_fn(p.n_in, p.n_out)
                       : p.affine ? affine_fn(p.n_in, p.affine == 2) : modulo_fn(p.n_in);
     if (policy == DS_TOPO_SPEC) {
         ds_topology topo;
