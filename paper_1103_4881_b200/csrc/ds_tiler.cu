@@ -203,7 +203,7 @@ __device__ __forceinline__ void task_one(const TaskParams& p, int64_t q) {
 // offsets are the S:248-252 element indices, proved wrap-free on the host).
 // NI = n_in rounded up to 4 (weights past n_in are zero); WORDS: the pattern is
 // NI contiguous, 4-byte aligned input bytes and the taps fit s8.
-template <int NI, bool WORDS>
+template <int NI, bool WORDS, int Q>
 __device__ __forceinline__ void task_affine(const TaskParams& p, uint32_t q) {
     uint32_t bi = p.in_A, bo = p.out_A;
 #pragma unroll
@@ -216,20 +216,18 @@ __device__ __forceinline__ void task_affine(const TaskParams& p, uint32_t q) {
             q = qq;
         }
     }
-    int32_t acc[DS_MAX_OUTPUTS];
+    int32_t acc[Q];
     if (WORDS) {
         uint32_t x[NI / 4];
         const uint32_t* src = reinterpret_cast<const uint32_t*>(p.in + bi);
 #pragma unroll
         for (int i = 0; i < NI / 4; ++i) x[i] = __ldg(src + i);
 #pragma unroll
-        for (int k = 0; k < DS_MAX_OUTPUTS; ++k) {
-            if (k < p.n_out) {
-                int32_t a = p.bias;
+        for (int k = 0; k < Q; ++k) {
+            int32_t a = p.bias;
 #pragma unroll
-                for (int i = 0; i < NI / 4; ++i) a = t_dp4a(x[i], p.wp[k][i], a);
-                acc[k] = a;
-            }
+            for (int i = 0; i < NI / 4; ++i) a = t_dp4a(x[i], p.wp[k][i], a);
+            acc[k] = a;
         }
     } else {
         int32_t pat[NI];
@@ -237,21 +235,18 @@ __device__ __forceinline__ void task_affine(const TaskParams& p, uint32_t q) {
         for (int e = 0; e < NI; ++e)
             pat[e] = (e < p.n_in && ((p.in_live >> e) & 1u)) ? (int32_t)__ldg(p.in + bi + p.in_b[e]) : 0;
 #pragma unroll
-        for (int k = 0; k < DS_MAX_OUTPUTS; ++k) {
-            if (k < p.n_out) {
-                int32_t a = p.bias;
+        for (int k = 0; k < Q; ++k) {
+            int32_t a = p.bias;
 #pragma unroll
-                for (int e = 0; e < NI; ++e) a += p.w[k][e] * pat[e];
-                acc[k] = a;
-            }
+            for (int e = 0; e < NI; ++e) a += p.w[k][e] * pat[e];
+            acc[k] = a;
         }
     }
 #pragma unroll
-    for (int k = 0; k < DS_MAX_OUTPUTS; ++k)
-        if (k < p.n_out) p.out[bo + p.out_b[k]] = t_out(p, acc[k] + (p.fastdiv ? p.fbias - p.bias : 0));
+    for (int k = 0; k < Q; ++k) p.out[bo + p.out_b[k]] = t_out(p, acc[k] + (p.fastdiv ? p.fbias - p.bias : 0));
 }
 
-template <int NI, bool WORDS>
+template <int NI, bool WORDS, int Q>
 __global__ void __launch_bounds__(256) ds_task_affine_kernel(const __grid_constant__ TaskParams p) {
     if (p.policy == DS_TOPO_SPEC) {
         const uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
@@ -266,12 +261,12 @@ __global__ void __launch_bounds__(256) ds_task_affine_kernel(const __grid_consta
             if (c[d] >= (uint32_t)p.tmult[d]) return;     // guard
             q = q * (uint32_t)p.tmult[d] + c[d];
         }
-        task_affine<NI, WORDS>(p, q);
+        task_affine<NI, WORDS, Q>(p, q);
         return;
     }
     const uint32_t stride = gridDim.x * blockDim.x;
     for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < (uint32_t)p.n_reps; q += stride)
-        task_affine<NI, WORDS>(p, q);
+        task_affine<NI, WORDS, Q>(p, q);
 }
 
 // Dense task (host-proved: input element offset in_A + n_in q + e, output
@@ -321,7 +316,7 @@ __global__ void __launch_bounds__(256) ds_task_dense_kernel(const __grid_constan
     }
     const uint32_t stride = gridDim.x * blockDim.x;
     for (uint32_t q = full * 128 + blockIdx.x * blockDim.x + threadIdx.x; q < (uint32_t)p.n_reps; q += stride)
-        task_affine<NI, true>(p, q);
+        task_affine<NI, true, Q>(p, q);
 }
 
 template <int NB>
@@ -440,12 +435,25 @@ TaskFn dense_fn(int ni, int no) {
         default: return dense_fn_q<16>(no);
     }
 }
-TaskFn affine_fn(int ni, bool words) {
+template <int NI, bool WORDS>
+TaskFn affine_fn_q(int q) {
+    switch (q) {
+        case 1: return ds_task_affine_kernel<NI, WORDS, 1>;
+        case 2: return ds_task_affine_kernel<NI, WORDS, 2>;
+        case 3: return ds_task_affine_kernel<NI, WORDS, 3>;
+        case 4: return ds_task_affine_kernel<NI, WORDS, 4>;
+        case 5: return ds_task_affine_kernel<NI, WORDS, 5>;
+        case 6: return ds_task_affine_kernel<NI, WORDS, 6>;
+        case 7: return ds_task_affine_kernel<NI, WORDS, 7>;
+        default: return ds_task_affine_kernel<NI, WORDS, 8>;
+    }
+}
+TaskFn affine_fn(int ni, bool words, int no) {
     switch ((ni + 3) / 4) {
-        case 1: return words ? ds_task_affine_kernel<4, true> : ds_task_affine_kernel<4, false>;
-        case 2: return words ? ds_task_affine_kernel<8, true> : ds_task_affine_kernel<8, false>;
-        case 3: return words ? ds_task_affine_kernel<12, true> : ds_task_affine_kernel<12, false>;
-        default: return words ? ds_task_affine_kernel<16, true> : ds_task_affine_kernel<16, false>;
+        case 1: return words ? affine_fn_q<4, true>(no) : affine_fn_q<4, false>(no);
+        case 2: return words ? affine_fn_q<8, true>(no) : affine_fn_q<8, false>(no);
+        case 3: return words ? affine_fn_q<12, true>(no) : affine_fn_q<12, false>(no);
+        default: return words ? affine_fn_q<16, true>(no) : affine_fn_q<16, false>(no);
     }
 }
 
@@ -801,7 +809,7 @@ int launch_task(const uint8_t* in, const ds_tiler& t_in, uint8_t* out, const ds_
     }
     const TaskFn fn = p.dense ? dense_fn(p.n_in, p.n_out)
                       : p.affine == 3 ? cols_fn(p.n_in, p.n_out)
-                      : p.affine ? affine_fn(p.n_in, p.affine == 2) : modulo_fn(p.n_in);
+                      : p.affine ? affine_fn(p.n_in, p.affine == 2, p.n_out) : modulo_fn(p.n_in);
     if (policy == DS_TOPO_SPEC) {
         ds_topology topo;
         if ((rc = ds_compute_topology(nrep, rep_shape, 1024, 3, 64, 256, &topo))) return rc;
