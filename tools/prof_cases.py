@@ -1,7 +1,8 @@
 """Profiling targets for the non-headline rows (run under ncu, one kernel family each):
    python tools/prof_cases.py tasks   -> K-N3 ds_htask_kernel + ds_vtask_kernel (300 HD 4:2:0)
    python tools/prof_cases.py general -> K-N1g on the halo spec (300 HD 4:2:0)
-   python tools/prof_cases.py runtask -> ds_task_kernel (yhfk over 300 HD luma planes, 3-D task)"""
+   python tools/prof_cases.py runtask -> ds_run_task on yhfk over 300 HD luma planes (3-D task: dense path)
+   python tools/prof_cases.py runtask_v -> ds_run_task on the V task over 300 HD luma planes (column path)"""
 import os
 import sys
 
@@ -27,6 +28,18 @@ elif what == "general":
     y = d.alloc_out(300)
     for _ in range(3):
         d(x, y)
+elif what == "runtask_v":
+    # the paper's V task as one 3-D task (the column path)
+    n, H, W = 300, 1080, 1920
+    Wm, Ho = W // 8 * 3, H // 9 * 4
+    mid = ds.generate_frames(n, H * Wm, seed=2).view(n, H, Wm)
+    out = torch.empty((n, Ho, Wm), dtype=torch.uint8, device="cuda")
+    spec = ds.ds_default_spec()
+    vw = [[spec.v.weight[k][i] for i in range(9)] for k in range(4)]
+    tin = ds.make_tiler((n, H, Wm), (0, 0, 0), [[1, 0, 0], [0, 9, 0], [0, 0, 1]], [[0], [1], [0]], [9])
+    tout = ds.make_tiler((n, Ho, Wm), (0, 0, 0), [[1, 0, 0], [0, 4, 0], [0, 0, 1]], [[0], [1], [0]], [4])
+    for _ in range(3):
+        ds.run_task(mid, tin, out, tout, [n, H // 9, Wm], ds.make_body(vw, 8, 4, n_in=9))
 elif what == "runtask":
     n, H, W = 300, 1080, 1920
     x = ds.generate_frames(n, W * H, seed=1)
