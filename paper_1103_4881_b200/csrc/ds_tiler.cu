@@ -38,7 +38,7 @@ struct TaskParams {
     uint8_t* out;
     int64_t n_reps;
     int32_t fast32;                    // every index quantity < 2^31 (host-checked)
-    int32_t reserved_;
+    int32_t noclamp;                   // fastdiv and every acc in [0, 256 D): output = umulhi(acc, M)
     FastDiv rdiv[4];                   // repetition extents
     FastDiv sdiv_in[4], sdiv_out[4];   // array extents
     int32_t nrep;
@@ -144,6 +144,13 @@ __device__ __forceinline__ uint8_t t_out(const TaskParams& p, int32_t acc) {
     if (p.fastdiv) return (uint8_t)min(__umulhi((uint32_t)max(acc, (int32_t)p.lo), p.M), 255u);
     int32_t v = acc / p.divisor;                          // truncation toward zero
     return (uint8_t)(v < 0 ? 0 : (v > 255 ? 255 : v));
+}
+
+// t_out where the host proved the clamps never fire (noclamp): one umulhi
+template <bool NC>
+__device__ __forceinline__ uint32_t t_outc(const TaskParams& p, int32_t acc) {
+    if (NC) return __umulhi((uint32_t)acc, p.M);
+    return t_out(p, acc);
 }
 
 // Modulo path, 32-bit: NI = n_in rounded up to 4 (the MAC loop runs over NI
@@ -275,11 +282,9 @@ __global__ void __launch_bounds__(256) ds_task_affine_kernel(const __grid_consta
 // streaming map.  Each lane takes 4 consecutive repetitions (16-byte loads);
 // the warp stages its 128 Q output bytes in shared memory and writes them as
 // coalesced words.  Repetitions past the last full warp use task_affine.
-template <int NI, int Q>
-__global__ void __launch_bounds__(256) ds_task_dense_kernel(const __grid_constant__ TaskParams p) {
-    __shared__ __align__(16) uint32_t buf[8][32 * Q];
+template <int NI, int Q, bool NC>
+__device__ __forceinline__ void dense_loop(const TaskParams& p, uint32_t* b) {
     const int lane = threadIdx.x & 31;
-    uint32_t* b = buf[threadIdx.x >> 5];
     const uint32_t full = (uint32_t)(p.n_reps / 128);
     const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
     const int32_t b0 = p.fastdiv ? p.fbias : p.bias;
@@ -303,7 +308,7 @@ __global__ void __launch_bounds__(256) ds_task_dense_kernel(const __grid_constan
                 int32_t acc = b0;
 #pragma unroll
                 for (int i = 0; i < NI / 4; ++i) acc = t_dp4a(x[r * (NI / 4) + i], p.wp[k][i], acc);
-                ow[(r * Q + k) >> 2] |= (uint32_t)t_out(p, acc) << (8 * ((r * Q + k) & 3));
+                ow[(r * Q + k) >> 2] |= t_outc<NC>(p, acc) << (8 * ((r * Q + k) & 3));
             }
         }
 #pragma unroll
@@ -314,6 +319,14 @@ __global__ void __launch_bounds__(256) ds_task_dense_kernel(const __grid_constan
         for (int j = 0; j < Q; ++j) dst[lane + 32 * j] = b[lane + 32 * j];
         __syncwarp();
     }
+}
+template <int NI, int Q>
+__global__ void __launch_bounds__(256) ds_task_dense_kernel(const __grid_constant__ TaskParams p) {
+    __shared__ __align__(16) uint32_t buf[8][32 * Q];
+    uint32_t* b = buf[threadIdx.x >> 5];
+    if (p.noclamp) dense_loop<NI, Q, true>(p, b);
+    else dense_loop<NI, Q, false>(p, b);
+    const uint32_t full = (uint32_t)(p.n_reps / 128);
     const uint32_t stride = gridDim.x * blockDim.x;
     for (uint32_t q = full * 128 + blockIdx.x * blockDim.x + threadIdx.x; q < (uint32_t)p.n_reps; q += stride)
         task_affine<NI, true, Q>(p, q);
@@ -338,7 +351,7 @@ __device__ __forceinline__ void cols_load(const TaskParams& p, uint32_t q4, uint
         x[e] = (e < p.n_in && ((p.in_live >> e) & 1u))
                    ? __ldg(reinterpret_cast<const uint32_t*>(p.in + bi + p.in_b[e])) : 0u;
 }
-template <int NB, int Q>
+template <int NB, int Q, bool NC>
 __device__ __forceinline__ void cols_compute(const TaskParams& p, const uint32_t (&x)[4 * NB], uint32_t bo) {
     int32_t acc[Q][4];
     const int32_t b0 = p.fastdiv ? p.fbias : p.bias;
@@ -364,8 +377,8 @@ __device__ __forceinline__ void cols_compute(const TaskParams& p, const uint32_t
     }
 #pragma unroll
     for (int k = 0; k < Q; ++k) {
-        const uint32_t o = (uint32_t)t_out(p, acc[k][0]) | ((uint32_t)t_out(p, acc[k][1]) << 8) |
-                           ((uint32_t)t_out(p, acc[k][2]) << 16) | ((uint32_t)t_out(p, acc[k][3]) << 24);
+        const uint32_t o = t_outc<NC>(p, acc[k][0]) | (t_outc<NC>(p, acc[k][1]) << 8) |
+                           (t_outc<NC>(p, acc[k][2]) << 16) | (t_outc<NC>(p, acc[k][3]) << 24);
         *reinterpret_cast<uint32_t*>(p.out + bo + p.out_b[k]) = o;
     }
 }
@@ -381,15 +394,20 @@ __device__ __forceinline__ void cols_compute(const TaskParams& p, const uint32_t
 // registers scale with the live words (4 NB) and accumulators (4 Q): small
 // shapes (the paper's V task: NB 3, Q 4) run 8 blocks per SM, large ones fewer
 constexpr int cols_minb(int nb, int q) { return nb * q <= 12 ? 8 : nb * q <= 24 ? 6 : 4; }
-template <int NB, int Q>
-__global__ void __launch_bounds__(256, cols_minb(NB, Q)) ds_task_cols_kernel(const __grid_constant__ TaskParams p) {
+template <int NB, int Q, bool NC>
+__device__ __forceinline__ void cols_loop(const TaskParams& p) {
     const uint32_t quads = (uint32_t)(p.n_reps >> 2);
     const uint32_t stride = gridDim.x * blockDim.x;
     for (uint32_t q4 = blockIdx.x * blockDim.x + threadIdx.x; q4 < quads; q4 += stride) {
         uint32_t x[4 * NB], bo;
         cols_load<NB>(p, q4, x, bo);
-        cols_compute<NB, Q>(p, x, bo);
+        cols_compute<NB, Q, NC>(p, x, bo);
     }
+}
+template <int NB, int Q>
+__global__ void __launch_bounds__(256, cols_minb(NB, Q)) ds_task_cols_kernel(const __grid_constant__ TaskParams p) {
+    if (p.noclamp) cols_loop<NB, Q, true>(p);
+    else cols_loop<NB, Q, false>(p);
 }
 
 using TaskFn = void (*)(const TaskParams);
@@ -716,17 +734,19 @@ int launch_task(const uint8_t* in, const ds_tiler& t_in, uint8_t* out, const ds_
     // taps: s8-packed copies, live pattern elements, and the exact
     // multiply-high division (same derivation as K-N1g's FASTDIV) -- all paths
     bool s8 = true;
-    int64_t amax = 0;
+    int64_t amax = 0, amin = 0;
     for (int k = 0; k < p.n_out; ++k) {
-        int64_t pos = body->bias;
+        int64_t pos = body->bias, neg = body->bias;
         for (int e = 0; e < p.n_in; ++e) {
             const int32_t w = body->weight[k][e];
             if (w < -128 || w > 127) s8 = false;
             if (w > 0) pos += 255LL * w;
+            if (w < 0) neg += 255LL * w;
             if (w != 0) p.in_live |= 1u << e;
             p.wp[k][e / 4] |= (uint32_t)(uint8_t)(int8_t)(w < -128 || w > 127 ? 0 : w) << (8 * (e % 4));
         }
         amax = std::max(amax, pos);
+        amin = k == 0 ? neg : std::min(amin, neg);
     }
     {
         const uint64_t D = (uint64_t)body->divisor;
@@ -738,6 +758,8 @@ int launch_task(const uint8_t* in, const ds_tiler& t_in, uint8_t* out, const ds_
                 p.fastdiv = 1; p.M = (uint32_t)M; p.lo = 0; p.fbias = body->bias;
             }
         }
+        // neither clamp can fire: acc (+1 when D == 1) >= lo and trunc(amax / D) <= 255
+        p.noclamp = p.fastdiv && amin >= 0 && (uint64_t)amax / D <= 255;
     }
     // affine path: both tilers wrap-free, 32-bit offsets and repetition index
     if (p.n_reps < (1LL << 31) && affine_tiler(t_in, nrep, rep_shape, &p.in_A, p.in_a, p.in_b, DS_MAX_PATTERN) &&

@@ -267,6 +267,20 @@ def test_run_task_affine_words(P):
             assert np.array_equal(y.cpu().numpy(), want), (origin, D, B)
 
 
+def _noclamp_body(rng, P, Q):
+    """A body whose clamps can never fire (non-negative taps, bias in [0, D),
+    D >= every output's tap sum, so 0 <= acc / D <= 255 and outputs reach 255):
+    the kernels' host-proved noclamp branch.  D == 1 too (one unit tap)."""
+    if rng.integers(0, 3) == 0:
+        w = [[0] * P for _ in range(Q)]
+        for k in range(Q):
+            w[k][int(rng.integers(0, P))] = 1
+        return w, 1, 0
+    w = [[int(x) for x in rng.integers(0, 128, P)] for _ in range(Q)]
+    D = max(1, max(sum(r) for r in w))
+    return w, D, int(rng.integers(0, D))
+
+
 @pytest.mark.gpu
 def test_run_task_affine_columns():
     """Column-vector path: the innermost repetition dim is unit-stride in both
@@ -295,9 +309,12 @@ def test_run_task_affine_columns():
             tin = (in_shape, (o, 0), [[S, 0], [0, 1]], [[step], [0]], [P])
             tout = (out_shape, (0, 0), [[Q, 0], [0, 1]], [[1], [0]], [Q])
             reps = [G, C]
-        w = [[int(x) for x in rng.integers(-128, 128, P)] for _ in range(Q)]
-        D = int(rng.choice([1, 3, 8, 999983]))
-        B = int(rng.integers(-500, 500))
+        if trial % 3 == 1:
+            w, D, B = _noclamp_body(rng, P, Q)
+        else:
+            w = [[int(x) for x in rng.integers(-128, 128, P)] for _ in range(Q)]
+            D = int(rng.choice([1, 3, 8, 999983]))
+            B = int(rng.integers(-500, 500))
         a = rng.integers(0, 256, in_shape).astype(np.uint8)
         want = oracle.run_task(a, oracle.make_tiler(*tin), out_shape, oracle.make_tiler(*tout), reps,
                                oracle.make_stage(P, P, 0, w, D, B))
@@ -361,7 +378,9 @@ def test_run_task_dense_large(P, Q):
     tin = ((n, H, W), (0, 0, 0), [[1, 0, 0], [0, 1, 0], [0, 0, P]], [[0], [0], [1]], [P])
     tout = ((n, H, Wp * Q), (0, 0, 0), [[1, 0, 0], [0, 1, 0], [0, 0, Q]], [[0], [0], [1]], [Q])
     reps = [n, H, Wp]
-    for D, B in ((1, 0), (6, 3), (999983, 7)):
+    bodies = [(w, D, B) for D, B in ((1, 0), (6, 3), (999983, 7))]
+    bodies += [_noclamp_body(rng, P, Q) for _ in range(3)]
+    for w, D, B in bodies:
         want = oracle.run_task(a, oracle.make_tiler(*tin), tout[0], oracle.make_tiler(*tout), reps,
                                oracle.make_stage(P, P, 0, w, D, B))
         y = torch.zeros(tout[0], dtype=torch.uint8, device="cuda")
