@@ -64,6 +64,10 @@ struct TaskParams {
     uint32_t M, lo;
     int32_t dense;                     // affine == 2 and both tilers are dense row-major runs
     uint32_t in_live;                  // bit e: pattern element e has a nonzero tap for some output
+    // column path: in_b with every element that has no tap (dead, or past
+    // n_in) aliased to the first live one, so all 4 NB word loads are
+    // unconditional (zero taps ignore the value; the repeat is an L1 hit)
+    int32_t in_bl[DS_MAX_PATTERN];
 };
 
 __device__ __forceinline__ int64_t t_mod(int64_t a, int64_t m) {
@@ -160,7 +164,9 @@ __device__ __forceinline__ void task_one32(const TaskParams& p, uint32_t q) {
     uint32_t r[4] = {0, 0, 0, 0};
 #pragma unroll
     for (int j = 3; j >= 0; --j) {
-        if (j < p.nrep) {
+        if (j == 0) {
+            r[0] = q;                          // q < rep[0]: no division
+        } else if (j < p.nrep) {
             const uint32_t qq = fdiv(p.rdiv[j], q);
             r[j] = q - qq * p.rdiv[j].d;
             q = qq;
@@ -215,7 +221,10 @@ __device__ __forceinline__ void task_affine(const TaskParams& p, uint32_t q) {
     uint32_t bi = p.in_A, bo = p.out_A;
 #pragma unroll
     for (int j = 3; j >= 0; --j) {
-        if (j < p.nrep) {
+        if (j == 0) {                          // q < rep[0]: no division
+            bi += p.in_a[0] * q;
+            bo += p.out_a[0] * q;
+        } else if (j < p.nrep) {
             const uint32_t qq = fdiv(p.rdiv[j], q);
             const uint32_t r = q - qq * p.rdiv[j].d;
             bi += p.in_a[j] * r;
@@ -338,7 +347,10 @@ __device__ __forceinline__ void cols_load(const TaskParams& p, uint32_t q4, uint
     bo = p.out_A;
 #pragma unroll
     for (int j = 3; j >= 0; --j) {
-        if (j < p.nrep) {
+        if (j == 0) {                          // q < rep[0]: no division
+            bi += p.in_a[0] * q;
+            bo += p.out_a[0] * q;
+        } else if (j < p.nrep) {
             const uint32_t qq = fdiv(p.rdiv[j], q);
             const uint32_t r = q - qq * p.rdiv[j].d;
             bi += p.in_a[j] * r;
@@ -346,10 +358,10 @@ __device__ __forceinline__ void cols_load(const TaskParams& p, uint32_t q4, uint
             q = qq;
         }
     }
+    const uint8_t* src = p.in + bi;
 #pragma unroll
-    for (int e = 0; e < 4 * NB; ++e)           // elements with no nonzero tap are not loaded
-        x[e] = (e < p.n_in && ((p.in_live >> e) & 1u))
-                   ? __ldg(reinterpret_cast<const uint32_t*>(p.in + bi + p.in_b[e])) : 0u;
+    for (int e = 0; e < 4 * NB; ++e)           // elements with no nonzero tap re-read a live one
+        x[e] = __ldg(reinterpret_cast<const uint32_t*>(src + p.in_bl[e]));
 }
 template <int NB, int Q, bool NC>
 __device__ __forceinline__ void cols_compute(const TaskParams& p, const uint32_t (&x)[4 * NB], uint32_t bo) {
@@ -790,7 +802,13 @@ int launch_task(const uint8_t* in, const ds_tiler& t_in, uint8_t* out, const ds_
             for (int j = 0; j < jl; ++j) cols = cols && p.in_a[j] % 4 == 0 && p.out_a[j] % 4 == 0;
             for (int e = 0; e < p.n_in; ++e) cols = cols && (p.in_b[e] & 3) == 0;
             for (int k = 0; k < p.n_out; ++k) cols = cols && (p.out_b[k] & 3) == 0;
-            if (cols) p.affine = 3;
+            if (cols) {
+                p.affine = 3;
+                int first = 0;
+                while (first < p.n_in - 1 && !((p.in_live >> first) & 1u)) ++first;
+                for (int e = 0; e < DS_MAX_PATTERN; ++e)
+                    p.in_bl[e] = (e < p.n_in && ((p.in_live >> e) & 1u)) ? p.in_b[e] : p.in_b[first];
+            }
         }
     }
     if (!p.affine && allow_peel && p.n_reps < (1LL << 31)) {
