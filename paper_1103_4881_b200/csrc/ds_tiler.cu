@@ -248,8 +248,7 @@ __device__ __forceinline__ void task_affine(const TaskParams& p, uint32_t q) {
     } else {
         int32_t pat[NI];
 #pragma unroll
-        for (int e = 0; e < NI; ++e)
-            pat[e] = (e < p.n_in && ((p.in_live >> e) & 1u)) ? (int32_t)__ldg(p.in + bi + p.in_b[e]) : 0;
+        for (int e = 0; e < NI; ++e) pat[e] = (int32_t)__ldg(p.in + bi + p.in_bl[e]);   // aliased: no predicates
 #pragma unroll
         for (int k = 0; k < Q; ++k) {
             int32_t a = p.bias;
@@ -742,7 +741,8 @@ int launch_task(const uint8_t* in, const ds_tiler& t_in, uint8_t* out, const ds_
     p.n_out = body->n_out;
     p.divisor = body->divisor;
     p.bias = body->bias;
-    std::memcpy(p.w, body->weight, sizeof p.w);
+    for (int k = 0; k < p.n_out; ++k)              // taps past n_in (or n_out) are zero
+        for (int e = 0; e < p.n_in; ++e) p.w[k][e] = body->weight[k][e];
     // taps: s8-packed copies, live pattern elements, and the exact
     // multiply-high division (same derivation as K-N1g's FASTDIV) -- all paths
     bool s8 = true;
@@ -802,14 +802,14 @@ int launch_task(const uint8_t* in, const ds_tiler& t_in, uint8_t* out, const ds_
             for (int j = 0; j < jl; ++j) cols = cols && p.in_a[j] % 4 == 0 && p.out_a[j] % 4 == 0;
             for (int e = 0; e < p.n_in; ++e) cols = cols && (p.in_b[e] & 3) == 0;
             for (int k = 0; k < p.n_out; ++k) cols = cols && (p.out_b[k] & 3) == 0;
-            if (cols) {
-                p.affine = 3;
-                int first = 0;
-                while (first < p.n_in - 1 && !((p.in_live >> first) & 1u)) ++first;
-                for (int e = 0; e < DS_MAX_PATTERN; ++e)
-                    p.in_bl[e] = (e < p.n_in && ((p.in_live >> e) & 1u)) ? p.in_b[e] : p.in_b[first];
-            }
+            if (cols) p.affine = 3;
         }
+        // loads of elements with no tap (dead, or past n_in) re-read the first
+        // live element: unconditional loads, the zero taps ignore the value
+        int first = 0;
+        while (first < p.n_in - 1 && !((p.in_live >> first) & 1u)) ++first;
+        for (int e = 0; e < DS_MAX_PATTERN; ++e)
+            p.in_bl[e] = (e < p.n_in && ((p.in_live >> e) & 1u)) ? p.in_b[e] : p.in_b[first];
     }
     if (!p.affine && allow_peel && p.n_reps < (1LL << 31)) {
         // a wrap confined to <= 8 repetitions at one end of one repetition dim
