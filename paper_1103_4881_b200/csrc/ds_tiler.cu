@@ -68,6 +68,10 @@ struct TaskParams {
     // n_in) aliased to the first live one, so all 4 NB word loads are
     // unconditional (zero taps ignore the value; the repeat is an L1 hit)
     int32_t in_bl[DS_MAX_PATTERN];
+    // word path: (in + element offset) mod 4, the same for every repetition
+    // (all repetition strides are multiples of 4); nonzero -> NI/4 + 1 aligned
+    // words funnelled by m bytes
+    int32_t in_shift;
 };
 
 __device__ __forceinline__ int64_t t_mod(int64_t a, int64_t m) {
@@ -235,9 +239,21 @@ __device__ __forceinline__ void task_affine(const TaskParams& p, uint32_t q) {
     int32_t acc[Q];
     if (WORDS) {
         uint32_t x[NI / 4];
-        const uint32_t* src = reinterpret_cast<const uint32_t*>(p.in + bi);
+        const uint32_t* src = reinterpret_cast<const uint32_t*>(p.in + bi - p.in_shift);
+        if (p.in_shift) {
+            // the last aligned word holds byte bi + NI - 1, so it stays inside the allocation
+            const uint32_t sel = 0x3210u + 0x1111u * (uint32_t)p.in_shift;
+            uint32_t lo = __ldg(src);
 #pragma unroll
-        for (int i = 0; i < NI / 4; ++i) x[i] = __ldg(src + i);
+            for (int i = 0; i < NI / 4; ++i) {
+                const uint32_t hi = __ldg(src + i + 1);
+                x[i] = __byte_perm(lo, hi, sel);
+                lo = hi;
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < NI / 4; ++i) x[i] = __ldg(src + i);
+        }
 #pragma unroll
         for (int k = 0; k < Q; ++k) {
             int32_t a = p.bias;
@@ -777,10 +793,13 @@ int launch_task(const uint8_t* in, const ds_tiler& t_in, uint8_t* out, const ds_
     if (p.n_reps < (1LL << 31) && affine_tiler(t_in, nrep, rep_shape, &p.in_A, p.in_a, p.in_b, DS_MAX_PATTERN) &&
         affine_tiler(t_out, nrep, rep_shape, &p.out_A, p.out_a, p.out_b, DS_MAX_OUTPUTS)) {
         p.affine = 1;
-        bool words = s8 && p.n_in % 4 == 0 && (reinterpret_cast<uintptr_t>(in) & 3) == 0 && p.in_A % 4 == 0;
+        bool words = s8 && p.n_in % 4 == 0;
         for (int j = 0; j < nrep; ++j) words = words && p.in_a[j] % 4 == 0;
         for (int e = 0; e < p.n_in; ++e) words = words && p.in_b[e] == e;
-        if (words) p.affine = 2;
+        if (words) {
+            p.affine = 2;
+            p.in_shift = (int32_t)((reinterpret_cast<uintptr_t>(in) + p.in_A) & 3);
+        }
         // dense: both tilers are row-major runs over the repetition index
         bool dense = words && policy == DS_TOPO_FLAT &&
                      ((reinterpret_cast<uintptr_t>(in) + p.in_A) & 15) == 0 &&

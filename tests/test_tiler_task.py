@@ -246,25 +246,30 @@ def test_run_task_affine_words(P):
     """Contiguous, word-aligned patterns with s8 taps take the dense streaming
     path (both tilers row-major runs; 20 full warps of 128 repetitions plus a
     ragged tail) -- a 3-D repetition space, frames outermost, as in the paper's
-    yhfk task; a 1-byte-shifted origin forces the affine byte path."""
+    yhfk task.  Origins shifted by 1-3 bytes (and an input pointer 1 byte into
+    its allocation) take the word path with aligned loads funnelled by the
+    misalignment."""
     rng = np.random.default_rng(P)
     n, H, Wp = 3, 37, 24
     W = P * Wp
     a = rng.integers(0, 256, (n, H, W)).astype(np.uint8)
     Q = {4: 1, 8: 3, 12: 5, 16: 8}[P]       # dense path: 128 Q output bytes per warp
     w = [[int(x) for x in rng.integers(-128, 128, P)] for _ in range(Q)]
-    for origin in ((0, 0, 0), (0, 0, 1)):
+    for origin, poff in (((0, 0, 0), 0), ((0, 0, 1), 0), ((0, 0, 2), 0), ((0, 0, 3), 0), ((0, 0, 0), 1)):
         reps = [n, H, Wp - (1 if origin[2] else 0)]
         tin = ((n, H, W), origin, [[1, 0, 0], [0, 1, 0], [0, 0, P]], [[0], [0], [1]], [P])
         tout = ((n, H, reps[2] * Q), (0, 0, 0), [[1, 0, 0], [0, 1, 0], [0, 0, Q]], [[0], [0], [1]], [Q])
+        store = torch.zeros(a.size + 16, dtype=torch.uint8, device="cuda")
+        x = store[poff:poff + a.size].view(a.shape)
+        x.copy_(torch.from_numpy(a))
         for D, B in ((1, 0), (6, 3), (1 << 20, 5)):
             want = oracle.run_task(a, oracle.make_tiler(*tin), tout[0], oracle.make_tiler(*tout), reps,
                                    oracle.make_stage(P, P, 0, w, D, B))
             y = torch.zeros(tout[0], dtype=torch.uint8, device="cuda")
-            ds.run_task(torch.from_numpy(a).cuda(), ds.make_tiler(*tin), y, ds.make_tiler(*tout), reps,
+            ds.run_task(x, ds.make_tiler(*tin), y, ds.make_tiler(*tout), reps,
                         ds.make_body(w, D, B, n_in=P))
             torch.cuda.synchronize()
-            assert np.array_equal(y.cpu().numpy(), want), (origin, D, B)
+            assert np.array_equal(y.cpu().numpy(), want), (origin, poff, D, B)
 
 
 def _noclamp_body(rng, P, Q):
