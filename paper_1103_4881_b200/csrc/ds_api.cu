@@ -427,7 +427,7 @@ int launch_fused(ds_handle* h, const uint8_t* in, int64_t n, uint8_t* out, cudaS
 using GeneralFn = void (*)(const ds::GeneralParams);
 
 int64_t general_smem(const GeneralCfg& c, int stages) {
-    return (int64_t)stages * c.stage_stride + c.mid_stride + c.mid_alt + 2LL * c.out_stride + 2LL * stages * 8;
+    return (int64_t)stages * c.stage_stride + c.mid_stride + c.mid_alt + 2LL * c.out_stride + (2LL * stages + 1) * 8;
 }
 
 // K-N1g run lengths for a launch over n frames: with a V halo, a unit is a

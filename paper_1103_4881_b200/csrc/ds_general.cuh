@@ -431,6 +431,7 @@ __global__ void __launch_bounds__((DS_GEN_NCW + 1) * 32, DS_GEN_MINB)
     uint8_t* outs = mid + p.mid_stride + p.mid_alt;
     uint64_t* full = reinterpret_cast<uint64_t*>(outs + (size_t)2 * p.out_stride);
     uint64_t* empty = full + S;
+    uint64_t* outb = empty + S;                     // the band's V writes are complete (NCW arrivals)
     __shared__ int32_t wh[DS_MAX_OUTPUTS][DS_MAX_PATTERN], wv[DS_MAX_OUTPUTS][DS_MAX_PATTERN];
 
     const int tid = threadIdx.x;
@@ -443,6 +444,7 @@ __global__ void __launch_bounds__((DS_GEN_NCW + 1) * 32, DS_GEN_MINB)
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], NCW);
         }
+        mbar_init(outb, NCW);
         fence_barrier_init();
     }
     __syncthreads();
@@ -525,6 +527,7 @@ __global__ void __launch_bounds__((DS_GEN_NCW + 1) * 32, DS_GEN_MINB)
 
     int oslot = 0;
     uint32_t mpar = 0;                              // which mid buffer the next band writes
+    uint32_t opar = 0;                              // outb phase
     for (; cur.u < p.n_units; cur.next()) {
         const GenPlane& P = p.pl[cur.plane(p)];
         const GenView V = g_view(P, p.h.S, p.h.Q, p.v.Q, cur.local - P.unit_start);
@@ -586,7 +589,23 @@ __global__ void __launch_bounds__((DS_GEN_NCW + 1) * 32, DS_GEN_MINB)
             }
             if (P.strips == 1) {
                 uint8_t* dst = p.out + cur.f * p.out_frame + P.out_off + (int64_t)band * P.unit_out;
-                if (P.bulk_store) {
+                if (P.bulk_store && p.mid_alt) {
+                    // Only the storing thread waits for the band's V writes; the other
+                    // warps go on to the next band's H pass.  That writes the other mid
+                    // buffer (two mid buffers: mid_alt), and this band's mid and out slot
+                    // are rewritten only after the next band's mid barrier, which thread 0
+                    // reaches after bulk_wait_read (the other out slot is free).
+                    fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(outb);
+                    if (tid == 0) {
+                        mbar_wait(outb, opar);
+                        bulk_s2g(dst, ob, (uint32_t)P.unit_out);
+                        bulk_commit();
+                        bulk_wait_read<1>();
+                    }
+                    opar ^= 1;
+                } else if (P.bulk_store) {
                     fence_proxy_async_smem();
                     named_bar_sync(1, NC);              // output band complete; mid free
                     if (tid == 0) {
@@ -602,7 +621,19 @@ __global__ void __launch_bounds__((DS_GEN_NCW + 1) * 32, DS_GEN_MINB)
                 // strip: Qv k output rows of V.wm bytes at column col0 of the plane
                 const int orows = p.v.Q * P.k;
                 uint8_t* dst = p.out + cur.f * p.out_frame + P.out_off + (int64_t)band * orows * P.Wm + V.col0;
-                if (P.bulk_rows && (V.wm & 15) == 0) {
+                if (P.bulk_rows && (V.wm & 15) == 0 && p.mid_alt) {
+                    fence_proxy_async_smem();           // as above: only the storing thread waits
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(outb);
+                    if (tid == 0) {
+                        mbar_wait(outb, opar);
+                        for (int r = 0; r < orows; ++r)
+                            bulk_s2g(dst + (int64_t)r * P.Wm, ob + (size_t)r * V.wm, (uint32_t)V.wm);
+                        bulk_commit();
+                        bulk_wait_read<1>();
+                    }
+                    opar ^= 1;
+                } else if (P.bulk_rows && (V.wm & 15) == 0) {
                     fence_proxy_async_smem();
                     named_bar_sync(1, NC);
                     if (tid == 0) {
