@@ -302,8 +302,10 @@ __device__ __forceinline__ void g_v_quad(const GenStage& g, int k0, uint32_t mb,
     for (int kk = 0; kk < Q; ++kk)
 #pragma unroll
         for (int e = 0; e < 4; ++e) acc[kk][e] = g_bias<FAST>(g);
-    const int nb = (g.P + 3) >> 2;
-    for (int b4 = 0; b4 < nb; ++b4) {
+    const int nb = (g.P + 3) >> 2;                  // <= DS_MAX_PATTERN / 4
+#pragma unroll
+    for (int b4 = 0; b4 < DS_MAX_PATTERN / 4; ++b4) {
+        if (b4 >= nb) break;
         const uint32_t rb = mb + 4 * b4 * Wm;
         const uint32_t r0 = lds32s(rb), r1 = lds32s(rb + Wm), r2 = lds32s(rb + 2 * Wm), r3 = lds32s(rb + 3 * Wm);
         const uint32_t ta = __byte_perm(r0, r1, 0x5140), tb = __byte_perm(r2, r3, 0x5140);
