@@ -222,8 +222,9 @@ DS_API int ds_set_kernel(ds_handle* h, int32_t kernel);
 DS_API int ds_last_kernel(const ds_handle* h);
 
 /* K-N1 tuning: ring stages per CTA (2..8) and CTAs per SM (0 = maximum
- * occupancy).  Defaults: one CTA per SM and a ring of ~120 KB (the TMA
- * read optimum measured by tools/bw_probe).  Returns DS_EINVAL when out of
+ * occupancy).  Defaults: up to 3 CTAs per SM (as many as fit) whose rings
+ * together hold ~120 KB, at least 2 stages each (120 KB in flight per SM is
+ * the TMA read optimum measured by tools/bw_probe).  Returns DS_EINVAL when out of
  * range.  Not synchronised with ds_run calls in flight on other threads. */
 DS_API int ds_set_tuning(ds_handle* h, int32_t stages, int32_t ctas_per_sm);
 

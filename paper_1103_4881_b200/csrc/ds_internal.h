@@ -15,6 +15,7 @@ constexpr int kHostSlots = 3;                       // ds_run_host pipeline dept
 constexpr int64_t kUnitTargetBytes = 32 * 1024;     // K-N1 band size target (bytes staged)
 constexpr int64_t kInFlightTarget = 120 * 1024;     // K-N1 bytes in flight per SM (measured
                                                     // optimum of tools/bw_probe tma_read)
+constexpr int kK1Ctas = 3;                          // K-N1 CTAs per SM (cap; what fits runs)
 constexpr int kSmemLimit = 227 * 1024;              // per-CTA opt-in maximum
 constexpr int64_t kHostChunkBytes = 96LL << 20;     // ds_run_host chunk target (tools/e2e_sweep.py)
 

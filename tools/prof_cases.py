@@ -2,7 +2,8 @@
    python tools/prof_cases.py tasks   -> K-N3 ds_htask_kernel + ds_vtask_kernel (300 HD 4:2:0)
    python tools/prof_cases.py general -> K-N1g on the halo spec (300 HD 4:2:0)
    python tools/prof_cases.py runtask -> ds_run_task on yhfk over 300 HD luma planes (3-D task: dense path)
-   python tools/prof_cases.py runtask_v -> ds_run_task on the V task over 300 HD luma planes (column path)"""
+   python tools/prof_cases.py runtask_v -> ds_run_task on the V task over 300 HD luma planes (column path)
+   python tools/prof_cases.py sd420 -> K-N1 on 300 PAL SD 4:2:0 frames (wide luma + narrow chroma planes)"""
 import os
 import sys
 
@@ -22,6 +23,12 @@ if what == "tasks":
     for _ in range(3):
         d.htask(x, mid)
         d.vtask(mid, y)
+elif what == "sd420":
+    d = ds.Downscaler(720, 576, 3)
+    x = ds.generate_frames(300, d.in_frame_bytes, seed=1)
+    y = d.alloc_out(300)
+    for _ in range(3):
+        d(x, y)
 elif what == "general":
     d = ds.Downscaler(1920, 1080, 3, spec=ds.make_spec(h=HALO_H, v=HALO_V))
     x = ds.generate_frames(300, d.in_frame_bytes, seed=1)
