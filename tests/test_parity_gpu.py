@@ -415,7 +415,7 @@ def test_tuning_does_not_change_results():
     for band in (0, 8 * 1920, 64 * 1024, 1):
         d.set_band_bytes(band)
         for stages in (2, 3, 5, 8):
-            for ctas in (0, 1, 2):
+            for ctas in (0, 1, 2, 3):
                 d.set_tuning(stages, ctas)
                 y = d(x)
                 torch.cuda.synchronize()
