@@ -360,27 +360,94 @@ __device__ __forceinline__ void g_v_pass_bytes(const GenStage& g, const int32_t 
     }
 }
 
-// Producer-warp staging of one row for planes the TMA cannot copy: the W
-// row bytes, then the 32-byte wrap pad row[j mod W].
-__device__ __forceinline__ void g_coop_row(uint8_t* dst, const uint8_t* src, int W, int lane) {
-    if ((((uintptr_t)src | (uintptr_t)W) & 3) == 0) {
-        const uint32_t* s4 = reinterpret_cast<const uint32_t*>(src);
-        uint32_t* d4 = reinterpret_cast<uint32_t*>(dst);
-        const int n4 = W >> 2;
-        int x = lane;
-        for (; x + 96 < n4; x += 128) {             // 4 loads in flight per lane
-            const uint32_t a = __ldg(s4 + x), b = __ldg(s4 + x + 32), c = __ldg(s4 + x + 64),
-                           d = __ldg(s4 + x + 96);
-            d4[x] = a;
-            d4[x + 32] = b;
-            d4[x + 64] = c;
-            d4[x + 96] = d;
+// Producer-warp staging of the `rows` rows (row0 + i) mod H of a plane the
+// TMA cannot copy (unaligned rows or pointer): each staged row is the W row
+// bytes, then the 32-byte wrap pad row[j mod W].  Items (row, word) are walked
+// with incremental indices and loaded kCoopBatch per lane before their stores:
+// the shared destination and global source may alias as far as the compiler
+// knows, so a plain load-store loop serialises on DRAM latency (SD/QCIF chroma
+// rows are 22-90 words: one round trip per word per row).
+constexpr int kCoopBatch = 8;
+__device__ __forceinline__ void cp_async_ca(uint32_t dst, const void* src, int bytes) {
+    if (bytes == 8) asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+    else asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+__device__ __forceinline__ void g_coop_rows(uint8_t* dst, int pitch, const uint8_t* plane, int row0, int rows,
+                                            int H, int W, int lane) {
+    const int G = ((((uintptr_t)plane | (uintptr_t)W) & 7) == 0) ? 8
+                  : ((((uintptr_t)plane | (uintptr_t)W) & 3) == 0) ? 4 : 0;
+    if (G) {
+        // 4- or 8-byte aligned rows: cp.async (no register staging), every copy
+        // of the band in flight at once, one wait.  A row is W / G chunks, then
+        // (W >= 32) the 32-byte pad as the row's first 32 / G chunks.
+        const int nr = W / G, n = nr + (W >= 32 ? 32 / G : 0);
+        const int total = rows * n;
+        const uint32_t d0 = (uint32_t)__cvta_generic_to_shared(dst);
+        int r = lane / n, x = lane - (lane / n) * n;
+        for (int it = lane; it < total; it += 32) {
+            int rr = row0 + r;
+            if (rr >= H) rr -= H;
+            const uint8_t* src = plane + (int64_t)rr * W + (int64_t)(x < nr ? x : x - nr) * G;
+            cp_async_ca(d0 + (uint32_t)(r * pitch + x * G), src, G);
+            x += 32;
+            while (x >= n) { x -= n; ++r; }
         }
-        for (; x < n4; x += 32) d4[x] = __ldg(s4 + x);
-    } else {
-        for (int x = lane; x < W; x += 32) dst[x] = __ldg(src + x);
+        if (W < 32) {                                // pad of a short row: row[j mod W]
+            const int pc = lane % W;
+            for (int i = 0; i < rows; ++i) {
+                int rr = row0 + i;
+                if (rr >= H) rr -= H;
+                dst[(size_t)i * pitch + W + lane] = __ldg(plane + (int64_t)rr * W + pc);
+            }
+        }
+        cp_async_wait_all();
+        return;
     }
-    dst[W + lane] = __ldg(src + (lane < W ? lane : lane % W));
+    const bool words = (((uintptr_t)plane | (uintptr_t)W) & 3) == 0;
+    const int n = words ? W >> 2 : W;               // items per row
+    const int total = rows * n;
+    int r = lane / n, x = lane - (lane / n) * n;    // item lane
+    for (int it0 = 0; it0 < total; it0 += 32 * kCoopBatch) {
+        uint32_t v[kCoopBatch];
+        int dr[kCoopBatch], dx[kCoopBatch];
+#pragma unroll
+        for (int j = 0; j < kCoopBatch; ++j) {
+            dr[j] = r;
+            dx[j] = x;
+            if (it0 + 32 * j + lane < total) {
+                int rr = row0 + r;
+                if (rr >= H) rr -= H;
+                const uint8_t* src = plane + (int64_t)rr * W;
+                v[j] = words ? __ldg(reinterpret_cast<const uint32_t*>(src) + x) : (uint32_t)__ldg(src + x);
+            }
+            x += 32;
+            while (x >= n) { x -= n; ++r; }
+        }
+#pragma unroll
+        for (int j = 0; j < kCoopBatch; ++j) {
+            if (it0 + 32 * j + lane < total) {
+                uint8_t* d = dst + (size_t)dr[j] * pitch;
+                if (words) reinterpret_cast<uint32_t*>(d)[dx[j]] = v[j];
+                else d[dx[j]] = (uint8_t)v[j];
+            }
+        }
+    }
+    const int pc = lane < W ? lane : lane % W;      // pad column j -> row[j mod W]
+    for (int i0 = 0; i0 < rows; i0 += kCoopBatch) {
+        uint32_t v[kCoopBatch];
+#pragma unroll
+        for (int j = 0; j < kCoopBatch; ++j) {
+            if (i0 + j < rows) {
+                int rr = row0 + i0 + j;
+                if (rr >= H) rr -= H;
+                v[j] = __ldg(plane + (int64_t)rr * W + pc);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < kCoopBatch; ++j)
+            if (i0 + j < rows) dst[(size_t)(i0 + j) * pitch + W + lane] = (uint8_t)v[j];
+    }
 }
 
 // Producer-warp staging of one strip window row (plain loads): bytes
@@ -515,9 +582,7 @@ __global__ void __launch_bounds__((DS_GEN_NCW + 1) * 32, DS_GEN_MINB)
                         bulk_g2s(d + P.W, src, 32u, &full[s], pol);
                     }
                 } else {
-                    for (int i = 0; i < rows; ++i)
-                        g_coop_row(dst + (size_t)i * P.pitch, plane + (int64_t)((row0 + i) % P.H) * P.W, P.W,
-                                   lane);
+                    g_coop_rows(dst, P.pitch, plane, row0, rows, P.H, P.W, lane);
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&full[s]);      // release: generic smem writes
                 }
