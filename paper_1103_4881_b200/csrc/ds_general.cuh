@@ -422,6 +422,49 @@ __device__ __forceinline__ void g_coop_rows(uint8_t* dst, int pitch, const uint8
         cp_async_wait_all();
         return;
     }
+    if ((W & 3) == 0) {
+        // misaligned plane, W % 4 == 0: every row has the same misalignment m,
+        // and each staged word k (row bytes 4k..4k+3; pad words: row bytes
+        // 4p..4p+3) is two aligned source words funnelled by m bytes.  The
+        // second word holds a valid row byte, so it stays inside the allocation.
+        const uint32_t m = (uint32_t)((uintptr_t)plane & 3);
+        const uint32_t sel = 0x3210u + 0x1111u * m;
+        const int nr = W >> 2, n = nr + (W >= 32 ? 8 : 0);
+        const int total = rows * n;
+        int r = lane / n, x = lane - (lane / n) * n;
+        for (int it0 = 0; it0 < total; it0 += 32 * kCoopBatch) {
+            uint32_t lo[kCoopBatch], hi[kCoopBatch];
+            int dr[kCoopBatch], dx[kCoopBatch];
+#pragma unroll
+            for (int j = 0; j < kCoopBatch; ++j) {
+                dr[j] = r;
+                dx[j] = x;
+                if (it0 + 32 * j + lane < total) {
+                    int rr = row0 + r;
+                    if (rr >= H) rr -= H;
+                    const uint32_t* a = reinterpret_cast<const uint32_t*>(
+                        plane + (int64_t)rr * W + 4 * (int64_t)(x < nr ? x : x - nr) - m);
+                    lo[j] = __ldg(a);
+                    hi[j] = __ldg(a + 1);
+                }
+                x += 32;
+                while (x >= n) { x -= n; ++r; }
+            }
+#pragma unroll
+            for (int j = 0; j < kCoopBatch; ++j)
+                if (it0 + 32 * j + lane < total)
+                    reinterpret_cast<uint32_t*>(dst + (size_t)dr[j] * pitch)[dx[j]] = __byte_perm(lo[j], hi[j], sel);
+        }
+        if (W < 32) {
+            const int pc = lane % W;
+            for (int i = 0; i < rows; ++i) {
+                int rr = row0 + i;
+                if (rr >= H) rr -= H;
+                dst[(size_t)i * pitch + W + lane] = __ldg(plane + (int64_t)rr * W + pc);
+            }
+        }
+        return;
+    }
     const bool words = (((uintptr_t)plane | (uintptr_t)W) & 3) == 0;
     const int n = words ? W >> 2 : W;               // items per row
     const int total = rows * n;
@@ -470,12 +513,51 @@ __device__ __forceinline__ void g_coop_rows(uint8_t* dst, int pitch, const uint8
 
 // Producer-warp staging of one strip window row (plain loads): bytes
 // row[(cs + j) mod W] for j < len.
-__device__ __forceinline__ void g_coop_window(uint8_t* dst, const uint8_t* row, int W, int cs, int len, int lane) {
-    int c = cs + lane;
-    for (int j = lane; j < len; j += 32) {
-        while (c >= W) c -= W;
-        dst[j] = __ldg(row + c);
-        c += 32;
+// Strip windows of `rows` rows (row0 + i) mod H for planes the TMA cannot copy:
+// staged word q of a row is window bytes 4q..4q+3, i.e. row[(cs + 4q + t) mod W]:
+// two aligned source words funnelled by that address's misalignment (batched
+// kCoopBatch per lane before the stores), or bytes for the one word per row
+// that straddles the row end.  Writes up to 3 bytes past len (the pitch has
+// room: >= len + 35).
+__device__ __forceinline__ void g_coop_windows(uint8_t* dst, int pitch, const uint8_t* plane, int row0, int rows,
+                                               int H, int W, int cs, int len, int lane) {
+    const int n = (len + 3) >> 2;
+    const int total = rows * n;
+    int r = lane / n, x = lane - (lane / n) * n;
+    for (int it0 = 0; it0 < total; it0 += 32 * kCoopBatch) {
+        uint32_t v[kCoopBatch];
+        int dr[kCoopBatch], dx[kCoopBatch];
+#pragma unroll
+        for (int j = 0; j < kCoopBatch; ++j) {
+            dr[j] = r;
+            dx[j] = x;
+            if (it0 + 32 * j + lane < total) {
+                int rr = row0 + r;
+                if (rr >= H) rr -= H;
+                const uint8_t* row = plane + (int64_t)rr * W;
+                int c = cs + 4 * x;
+                while (c >= W) c -= W;
+                if (c + 3 < W) {
+                    const uintptr_t a = (uintptr_t)(row + c);
+                    const uint32_t* w = reinterpret_cast<const uint32_t*>(a & ~(uintptr_t)3);
+                    v[j] = __byte_perm(__ldg(w), __ldg(w + 1), 0x3210u + 0x1111u * (uint32_t)(a & 3));
+                } else {
+                    uint32_t b = 0;
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) {
+                        const int ct = c + t >= W ? c + t - W : c + t;   // c < W, so one wrap at most
+                        b |= (uint32_t)__ldg(row + ct) << (8 * t);
+                    }
+                    v[j] = b;
+                }
+            }
+            x += 32;
+            while (x >= n) { x -= n; ++r; }
+        }
+#pragma unroll
+        for (int j = 0; j < kCoopBatch; ++j)
+            if (it0 + 32 * j + lane < total)
+                reinterpret_cast<uint32_t*>(dst + (size_t)dr[j] * pitch)[dx[j]] = v[j];
     }
 }
 
@@ -584,9 +666,7 @@ __global__ void __launch_bounds__((DS_GEN_NCW + 1) * 32, DS_GEN_MINB)
                             if (seg1) bulk_g2s(d + seg0, src, (uint32_t)seg1, &full[s], pol);
                         }
                     } else {
-                        for (int i = 0; i < rows; ++i)
-                            g_coop_window(dst + (size_t)i * P.pitch, plane + (int64_t)((row0 + i) % P.H) * P.W,
-                                          P.W, cs, lw, lane);
+                        g_coop_windows(dst, P.pitch, plane, row0, rows, P.H, P.W, cs, lw, lane);
                         __syncwarp();
                         if (lane == 0) mbar_arrive(&full[s]);
                     }
