@@ -358,6 +358,34 @@ def test_general_kernel_fuzz_random_specs():
 
 
 # ------------------------------------------------------- alignment / API --
+@pytest.mark.parametrize("off", [1, 2, 3, 4, 8])
+@pytest.mark.parametrize("W,H,strips", [(352, 288, False), (352, 288, True), (32, 36, False)])
+def test_general_rows_staged_by_producer(off, W, H, strips):
+    """Input the TMA cannot copy (pointer `off` bytes into its allocation) is
+    staged by K-N1g's producer warp: cp.async for 4/8-byte aligned rows,
+    aligned words funnelled by the misalignment otherwise, strip windows the
+    same way (with bytes for the word that straddles the row end), and the
+    32-byte wrap pad from row[j mod W] (rows shorter than 32 bytes: the 16-byte
+    chroma rows of 32x36) -- halo spec with origin -2, against the oracle."""
+    hd, vd = _halo_spec()
+    spec = ds.make_spec(h=hd, v=vd, chroma=ds.DS_CHROMA_420)
+    d = ds.Downscaler(W, H, 3, spec=spec)
+    if strips:
+        d.set_general_stage_bytes(2048)
+        assert d.plan.general_strips[0] > 1
+    fr = synth.random_frames(9, 0, 3, W, H, 3, 1)
+    want = oracle.execute_frames(fr, W, H, 3, 1, _oracle_stage(hd), _oracle_stage(vd))
+    buf = torch.zeros(fr.size + 64, dtype=torch.uint8, device="cuda")
+    x = buf[off: off + fr.size]
+    x.copy_(torch.from_numpy(fr.ravel()).cuda())
+    y = torch.zeros(want.size, dtype=torch.uint8, device="cuda")
+    d.set_kernel(ds.DS_KERNEL_FUSED_GENERAL)
+    ds.ds_run(d.handle, x.data_ptr(), 3, y.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert d.last_kernel() == ds.DS_KERNEL_FUSED_GENERAL
+    _assert_same(y.cpu().numpy().reshape(want.shape), want, f"off={off} {W}x{H} strips={strips}")
+
+
 def test_misaligned_pointers():
     """Misaligned input moves off K-N1 (TMA needs 16-byte sources) to K-N1g,
     which stages the rows with plain loads; misaligned output makes K-N1 fall
