@@ -472,9 +472,13 @@ int32_t general_runs(const ds_handle* h, int64_t n, int32_t* L) {
     return upf_of(L);
 }
 
-GeneralFn general_fn(int fast) {
-    return fast == 2 ? ds::ds_fused_general_kernel<2>
-                     : fast == 1 ? ds::ds_fused_general_kernel<1> : ds::ds_fused_general_kernel<0>;
+// cs: some plane of the call is staged by the consumers (ds_fused_general_kernel)
+GeneralFn general_fn(int fast, bool cs) {
+    if (cs)
+        return fast == 2 ? ds::ds_fused_general_kernel<2, true>
+                         : fast == 1 ? ds::ds_fused_general_kernel<1, true> : ds::ds_fused_general_kernel<0, true>;
+    return fast == 2 ? ds::ds_fused_general_kernel<2, false>
+                     : fast == 1 ? ds::ds_fused_general_kernel<1, false> : ds::ds_fused_general_kernel<0, false>;
 }
 
 // Stage constants for K-N1g.  FASTDIV (M != 0): floor(a / D) = umulhi(a, M)
@@ -553,19 +557,23 @@ int configure_general(ds_handle* h) {
     c.smem = (int)general_smem(c, c.stages);
     const ds::GenStage gh = gen_stage(sp.h), gv = gen_stage(sp.v);
     c.fast = (gh.M == 0 || gv.M == 0) ? 0 : (gh.exact && gv.exact) ? 2 : 1;
-    GeneralFn fn = general_fn(c.fast);
     DeviceGuard g(h->device);
-    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             kSmemLimit - 2 * DS_MAX_OUTPUTS * DS_MAX_PATTERN * 4) != cudaSuccess) {
-        cudaGetLastError();
-        return DS_ECUDA;
+    int occ_min = 1 << 30;
+    for (bool cs : {false, true}) {
+        GeneralFn fn = general_fn(c.fast, cs);
+        if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 kSmemLimit - 2 * DS_MAX_OUTPUTS * DS_MAX_PATTERN * 4) != cudaSuccess) {
+            cudaGetLastError();
+            return DS_ECUDA;
+        }
+        int occ = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, c.threads, c.smem) != cudaSuccess || occ < 1) {
+            cudaGetLastError();
+            return DS_ECUDA;
+        }
+        occ_min = std::min(occ_min, occ);
     }
-    int occ = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, c.threads, c.smem) != cudaSuccess || occ < 1) {
-        cudaGetLastError();
-        return DS_ECUDA;
-    }
-    c.grid_per_sm = std::min(occ, want_ctas);
+    c.grid_per_sm = std::min(occ_min, want_ctas);
 
     c.valid = true;
     h->general = c;
@@ -586,6 +594,7 @@ int launch_general(ds_handle* h, const uint8_t* in, int64_t n, uint8_t* out, cud
     int32_t L[DS_MAX_PLANES] = {1, 1, 1};
     p.upf = general_runs(h, n, L);
     p.n_units = n * p.upf;
+    bool cs = false;
     p.n_planes = pi.n_planes;
     p.stages = c.stages;
     p.stage_stride = c.stage_stride;
@@ -642,10 +651,14 @@ int launch_general(ds_handle* h, const uint8_t* in, int64_t n, uint8_t* out, cud
         P.coop = (in_al && P.W % 16 == 0 && P.W >= 32 && P.in_off % 16 == 0 && pi.in_frame_bytes % 16 == 0)
                      ? 0 : 1;
         P.pitch = gg.pitch;
+        // consumer staging (the device's g_coop_async test, for every frame)
+        if (P.coop && (P.strips > 1 || ((reinterpret_cast<uintptr_t>(in) + P.in_off) & 3) != 0 || (P.W & 3) != 0 ||
+                       (n > 1 && (pi.in_frame_bytes & 3) != 0)))
+            cs = true;
         start += P.strips * P.runs;
     }
     const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(p.n_units, (int64_t)c.grid_per_sm * h->sm_count));
-    general_fn(c.fast)<<<(unsigned)grid, c.threads, c.smem, st>>>(p);
+    general_fn(c.fast, cs)<<<(unsigned)grid, c.threads, c.smem, st>>>(p);
     return cudaGetLastError() == cudaSuccess ? DS_OK : DS_ECUDA;
 }
 

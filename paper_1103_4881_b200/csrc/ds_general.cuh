@@ -561,6 +561,181 @@ __device__ __forceinline__ void g_coop_windows(uint8_t* dst, int pitch, const ui
     }
 }
 
+// rows of this plane go by cp.async (4- or 8-byte aligned pointer and W)
+__device__ __forceinline__ bool g_coop_async(const uint8_t* plane, int W) {
+    return (((uintptr_t)plane | (uintptr_t)W) & 3) == 0;
+}
+template <int NT>
+__device__ __forceinline__ void gc_pads_nt(uint8_t* dst, int pitch, const uint8_t* plane, int row0, int rows,
+                                            int H, int W, int t) {
+    const int total = rows * 32;
+    for (int it0 = 0; it0 < total; it0 += NT * kCoopBatch) {
+        uint32_t v[kCoopBatch];
+#pragma unroll
+        for (int j = 0; j < kCoopBatch; ++j) {
+            const int it = it0 + NT * j + t;
+            if (it < total) {
+                int rr = row0 + (it >> 5);
+                if (rr >= H) rr -= H;
+                const int jc = it & 31;
+                v[j] = __ldg(plane + (int64_t)rr * W + (jc < W ? jc : jc % W));
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < kCoopBatch; ++j) {
+            const int it = it0 + NT * j + t;
+            if (it < total) dst[(size_t)(it >> 5) * pitch + W + (it & 31)] = (uint8_t)v[j];
+        }
+    }
+}
+
+template <int NT>
+__device__ __forceinline__ void gc_rows_nt(uint8_t* dst, int pitch, const uint8_t* plane, int row0, int rows,
+                                            int H, int W, int t) {
+    const int G = ((((uintptr_t)plane | (uintptr_t)W) & 7) == 0) ? 8
+                  : ((((uintptr_t)plane | (uintptr_t)W) & 3) == 0) ? 4 : 0;
+    if (G) {
+        // 4- or 8-byte aligned rows: cp.async (no register staging), every copy
+        // of the band in flight at once, one wait.  A row is W / G chunks, then
+        // (W >= 32) the 32-byte pad as the row's first 32 / G chunks.
+        const int nr = W / G, n = nr + (W >= 32 ? 32 / G : 0);
+        const int total = rows * n;
+        const uint32_t d0 = (uint32_t)__cvta_generic_to_shared(dst);
+        int r = t / n, x = t - (t / n) * n;
+        for (int it = t; it < total; it += NT) {
+            int rr = row0 + r;
+            if (rr >= H) rr -= H;
+            const uint8_t* src = plane + (int64_t)rr * W + (int64_t)(x < nr ? x : x - nr) * G;
+            cp_async_ca(d0 + (uint32_t)(r * pitch + x * G), src, G);
+            x += NT;
+            if (NT <= 32) { while (x >= n) { x -= n; ++r; } } else if (x >= n) { const int q = x / n; r += q; x -= q * n; }
+        }
+        if (W < 32) gc_pads_nt<NT>(dst, pitch, plane, row0, rows, H, W, t);   // short rows: row[j mod W]
+        cp_async_wait_all();
+        return;
+    }
+    if ((W & 3) == 0) {
+        // misaligned plane, W % 4 == 0: every row has the same misalignment m,
+        // and each staged word k (row bytes 4k..4k+3; pad words: row bytes
+        // 4p..4p+3) is two aligned source words funnelled by m bytes.  The
+        // second word holds a valid row byte, so it stays inside the allocation.
+        const uint32_t m = (uint32_t)((uintptr_t)plane & 3);
+        const uint32_t sel = 0x3210u + 0x1111u * m;
+        const int nr = W >> 2, n = nr + (W >= 32 ? 8 : 0);
+        const int total = rows * n;
+        int r = t / n, x = t - (t / n) * n;
+        for (int it0 = 0; it0 < total; it0 += NT * kCoopBatch) {
+            uint32_t lo[kCoopBatch], hi[kCoopBatch];
+            int dr[kCoopBatch], dx[kCoopBatch];
+#pragma unroll
+            for (int j = 0; j < kCoopBatch; ++j) {
+                dr[j] = r;
+                dx[j] = x;
+                if (it0 + NT * j + t < total) {
+                    int rr = row0 + r;
+                    if (rr >= H) rr -= H;
+                    const uint32_t* a = reinterpret_cast<const uint32_t*>(
+                        plane + (int64_t)rr * W + 4 * (int64_t)(x < nr ? x : x - nr) - m);
+                    lo[j] = __ldg(a);
+                    hi[j] = __ldg(a + 1);
+                }
+                x += NT;
+                if (NT <= 32) { while (x >= n) { x -= n; ++r; } } else if (x >= n) { const int q = x / n; r += q; x -= q * n; }
+            }
+#pragma unroll
+            for (int j = 0; j < kCoopBatch; ++j)
+                if (it0 + NT * j + t < total)
+                    reinterpret_cast<uint32_t*>(dst + (size_t)dr[j] * pitch)[dx[j]] = __byte_perm(lo[j], hi[j], sel);
+        }
+        if (W < 32) gc_pads_nt<NT>(dst, pitch, plane, row0, rows, H, W, t);
+        return;
+    }
+    const bool words = (((uintptr_t)plane | (uintptr_t)W) & 3) == 0;
+    const int n = words ? W >> 2 : W;               // items per row
+    const int total = rows * n;
+    int r = t / n, x = t - (t / n) * n;    // item t
+    for (int it0 = 0; it0 < total; it0 += NT * kCoopBatch) {
+        uint32_t v[kCoopBatch];
+        int dr[kCoopBatch], dx[kCoopBatch];
+#pragma unroll
+        for (int j = 0; j < kCoopBatch; ++j) {
+            dr[j] = r;
+            dx[j] = x;
+            if (it0 + NT * j + t < total) {
+                int rr = row0 + r;
+                if (rr >= H) rr -= H;
+                const uint8_t* src = plane + (int64_t)rr * W;
+                v[j] = words ? __ldg(reinterpret_cast<const uint32_t*>(src) + x) : (uint32_t)__ldg(src + x);
+            }
+            x += NT;
+            if (NT <= 32) { while (x >= n) { x -= n; ++r; } } else if (x >= n) { const int q = x / n; r += q; x -= q * n; }
+        }
+#pragma unroll
+        for (int j = 0; j < kCoopBatch; ++j) {
+            if (it0 + NT * j + t < total) {
+                uint8_t* d = dst + (size_t)dr[j] * pitch;
+                if (words) reinterpret_cast<uint32_t*>(d)[dx[j]] = v[j];
+                else d[dx[j]] = (uint8_t)v[j];
+            }
+        }
+    }
+    gc_pads_nt<NT>(dst, pitch, plane, row0, rows, H, W, t);
+}
+
+template <int NT>
+__device__ __forceinline__ void gc_windows_nt(uint8_t* dst, int pitch, const uint8_t* plane, int row0, int rows,
+                                               int H, int W, int cs, int len, int t) {
+    const int n = (len + 3) >> 2;
+    const int total = rows * n;
+    int r = t / n, x = t - (t / n) * n;
+    for (int it0 = 0; it0 < total; it0 += NT * kCoopBatch) {
+        uint32_t v[kCoopBatch];
+        int dr[kCoopBatch], dx[kCoopBatch];
+#pragma unroll
+        for (int j = 0; j < kCoopBatch; ++j) {
+            dr[j] = r;
+            dx[j] = x;
+            if (it0 + NT * j + t < total) {
+                int rr = row0 + r;
+                if (rr >= H) rr -= H;
+                const uint8_t* row = plane + (int64_t)rr * W;
+                int c = cs + 4 * x;
+                while (c >= W) c -= W;
+                if (c + 3 < W) {
+                    const uintptr_t a = (uintptr_t)(row + c);
+                    const uint32_t* w = reinterpret_cast<const uint32_t*>(a & ~(uintptr_t)3);
+                    v[j] = __byte_perm(__ldg(w), __ldg(w + 1), 0x3210u + 0x1111u * (uint32_t)(a & 3));
+                } else {
+                    uint32_t b = 0;
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) {
+                        const int ct = c + t >= W ? c + t - W : c + t;   // c < W, so one wrap at most
+                        b |= (uint32_t)__ldg(row + ct) << (8 * t);
+                    }
+                    v[j] = b;
+                }
+            }
+            x += NT;
+            if (NT <= 32) { while (x >= n) { x -= n; ++r; } } else if (x >= n) { const int q = x / n; r += q; x -= q * n; }
+        }
+#pragma unroll
+        for (int j = 0; j < kCoopBatch; ++j)
+            if (it0 + NT * j + t < total)
+                reinterpret_cast<uint32_t*>(dst + (size_t)dr[j] * pitch)[dx[j]] = v[j];
+    }
+}
+
+// Consumer-side staging (CS instantiations only; out of line): strip windows
+// (cs >= 0) or whole rows, over NT threads.  gc_*_nt are g_coop_* over NT
+// threads instead of one warp.
+template <int NT>
+__device__ __noinline__ void g_coop_stage_consumers(uint8_t* dst, int pitch, const uint8_t* plane, int row0,
+                                                    int rows, int H, int W, int cs, int len, int t) {
+    if (cs >= 0) gc_windows_nt<NT>(dst, pitch, plane, row0, rows, H, W, cs, len, t);
+    else gc_rows_nt<NT>(dst, pitch, plane, row0, rows, H, W, t);
+}
+
+
 struct GenCursor {
     int64_t u, f;
     int32_t local, gdiv, gmod, upf;
@@ -588,7 +763,10 @@ struct GenCursor {
 // 2 CTAs x (8 consumer + 1 producer) warps per SM: the register file is
 // split across 4 SMSPs, so 18 warps need <= 102 registers each.
 
-template <int FAST>
+// CS: some plane's rows are staged by the consumers (misaligned words, strip
+// windows of planes the TMA cannot copy: 8x the producer warp's loads in
+// flight); a separate instantiation, so the CS = false kernel is unchanged.
+template <int FAST, bool CS>
 __global__ void __launch_bounds__((DS_GEN_NCW + 1) * 32, DS_GEN_MINB)
     ds_fused_general_kernel(const __grid_constant__ GeneralParams p) {
     constexpr int NCW = DS_GEN_NCW;
@@ -666,8 +844,8 @@ __global__ void __launch_bounds__((DS_GEN_NCW + 1) * 32, DS_GEN_MINB)
                             if (seg1) bulk_g2s(d + seg0, src, (uint32_t)seg1, &full[s], pol);
                         }
                     } else {
-                        g_coop_windows(dst, P.pitch, plane, row0, rows, P.H, P.W, cs, lw, lane);
-                        __syncwarp();
+                        if (!CS) g_coop_windows(dst, P.pitch, plane, row0, rows, P.H, P.W, cs, lw, lane);
+                        __syncwarp();                   // CS: the consumers stage it
                         if (lane == 0) mbar_arrive(&full[s]);
                     }
                 } else if (!P.coop) {
@@ -680,7 +858,8 @@ __global__ void __launch_bounds__((DS_GEN_NCW + 1) * 32, DS_GEN_MINB)
                         bulk_g2s(d + P.W, src, 32u, &full[s], pol);
                     }
                 } else {
-                    g_coop_rows(dst, P.pitch, plane, row0, rows, P.H, P.W, lane);
+                    // CS: rows cp.async cannot take are staged by the consumers
+                    if (!CS || g_coop_async(plane, P.W)) g_coop_rows(dst, P.pitch, plane, row0, rows, P.H, P.W, lane);
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&full[s]);      // release: generic smem writes
                 }
@@ -717,6 +896,16 @@ __global__ void __launch_bounds__((DS_GEN_NCW + 1) * 32, DS_GEN_MINB)
             const int rows = P.R - reuse;
             const uint32_t mid_h = mid_s + reuse * V.wm;
             mbar_wait(&full[s], phase);
+            if (CS && P.coop) {
+                const uint8_t* plane = p.in + cur.f * p.in_frame + P.in_off;
+                if (P.strips > 1 || !g_coop_async(plane, P.W)) {
+                    const int row0 = (int)(((int64_t)P.ov + (int64_t)p.v.S * P.k * band + reuse) % P.H);
+                    const int cs = P.strips > 1 ? (int)(((int64_t)P.oh + (int64_t)p.h.S * V.strip * P.sw) % P.W) : -1;
+                    g_coop_stage_consumers<NC>(ring + (size_t)s * p.stage_stride, P.pitch, plane, row0, rows, P.H,
+                                               P.W, cs, p.h.S * (V.np - 1) + p.h.P, tid);
+                    named_bar_sync(1, NC);
+                }
+            }
 
             // ---- H task on every newly staged row -> mid (u8)
             if (p.h.s8) {
