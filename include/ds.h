@@ -156,21 +156,33 @@ DS_API ds_handle* ds_create(int32_t frame_w, int32_t frame_h, int32_t channels,
  *   in_frames : device pointer, n_frames * ds_in_frame_bytes(h) bytes, read
  *               only ("const", the read-only flowPort of P:132-135)
  *   out_frames: device pointer, n_frames * ds_out_frame_bytes(h) bytes
- * in_frames on the handle's device; out_frames on it or on a peer GPU the
- * handle's device can access (NVLink P2P, e.g. another rank's buffer
- * mapped with CUDA IPC; peer access is enabled on first use): the kernel's
- * output stores then travel over NVLink, fusing the gather of frame shards
- * into the filtering.  Caller-owned, not retained, must not
- * overlap and must stay alive until work on `stream` completes.
+ * in_frames and out_frames on the handle's device.  out_frames may instead
+ * lie on a peer GPU that was enabled for this handle with ds_enable_peer
+ * (e.g. another rank's buffer mapped with CUDA IPC): the kernel's output
+ * stores then travel over NVLink, fusing the gather of frame shards
+ * into the filtering.  ds_run itself never enables peer access
+ * and has no context-wide side effects.  Caller-owned, not retained, must
+ * not overlap and must stay alive until work on `stream` completes.
  * Asynchronous on `stream`; faults surface at the caller's sync.
  * n_frames == 0 is a successful no-op.  Any alignment is accepted
  * (misalignment selects K-N1g's plain-load staging or plain stores, never
  * an error).
  * Returns DS_OK, DS_EINVAL (NULL handle/pointer with n > 0, n < 0,
- * overlapping ranges, pointer neither on the handle's device nor on a
- * reachable peer) or DS_ECUDA. */
+ * overlapping ranges, a pointer that is not device memory, in_frames not on
+ * the handle's device, out_frames neither on it nor on an enabled peer) or
+ * DS_ECUDA. */
 DS_API int ds_run(ds_handle* h, const uint8_t* in_frames, int64_t n_frames,
                   uint8_t* out_frames, ds_stream_t stream);
+
+/* Allow ds_run on this handle to store its output into memory of GPU
+ * peer_device (the gather of frame shards fused into the
+ * kernels' output stores over NVLink / NVSwitch).  Enables CUDA peer access
+ * from the handle's device to peer_device -- a context-wide setting of the
+ * calling process, made here once and explicitly, never inside ds_run.
+ * peer_device == the handle's device is a no-op.  Idempotent.
+ * Returns DS_OK, DS_EINVAL (NULL handle, no such device), DS_EUNSUPPORTED
+ * (the devices cannot access each other) or DS_ECUDA. */
+DS_API int ds_enable_peer(ds_handle* h, int32_t peer_device);
 
 /* Same result from HOST buffers (the paper's host-resident setting, P:146,
  * P:148): the library streams chunks of frames host -> device, runs the
@@ -230,9 +242,9 @@ DS_API int ds_set_tuning(ds_handle* h, int32_t stages, int32_t ctas_per_sm);
 
 /* K-N1 work-unit (band) size: the largest number of 9-row groups whose
  * staged bytes stay <= target_bytes for plane 0, other planes matched to
- * it (0 = default, 32 KiB).  Resets ds_set_tuning to the defaults for the
- * new unit size.  Output is unaffected.  Not synchronised with ds_run calls
- * in flight on other threads. */
+ * it (0 = default, 32 KiB).  An explicit ds_set_tuning is kept (re-applied
+ * to the new unit size).  On error the handle is left unchanged.  Output is
+ * unaffected.  Not synchronised with ds_run calls in flight on other threads. */
 DS_API int ds_set_band_bytes(ds_handle* h, int64_t target_bytes);
 
 /* K-N1g run length: with a V halo (v.pattern > v.paving) a work unit is a
@@ -250,13 +262,32 @@ DS_API int ds_set_run_bands(ds_handle* h, int32_t bands);
  * 28 KiB with a V halo, 40 KiB without).  Planes whose k = 1 band does not
  * fit are split into column strips (ds_plan_info.general_strips).  Output is
  * unaffected; K-N1g stays ineligible if the result still exceeds shared
- * memory.  Not synchronised with ds_run calls in flight on other threads. */
+ * memory.  An explicit ds_set_tuning is kept; on error the handle is left
+ * unchanged.  Not synchronised with ds_run calls in flight on other threads. */
 DS_API int ds_set_general_stage_bytes(ds_handle* h, int64_t target_bytes);
 
 /* K-N1 launch shape that ds_run would use for n_frames:
  * grid CTAs, threads per CTA, dynamic shared memory bytes. */
 DS_API int ds_launch_shape(const ds_handle* h, int64_t n_frames, int32_t* grid,
                            int32_t* block, int32_t* smem_bytes);
+
+/* Launch description of a kernel for a ds_run over n frames (bench.py's
+ * report row: kernel, stages, ctas_per_sm). */
+typedef struct {
+    int32_t kernel;              /* DS_KERNEL_FUSED / _FUSED_GENERAL / _GENERIC        */
+    int32_t grid, block, smem_bytes;
+    int32_t stages;              /* ring slots per CTA (persistent kernels; 0 for K-N2) */
+    int32_t ctas_per_sm;         /* resident CTAs per SM the grid is sized for         */
+    int32_t consumer_warps;      /* compute warps per CTA (plus one producer warp)     */
+    int64_t units;               /* work units of the launch (K-N2: output bytes)      */
+    int64_t unit_in_bytes_max;   /* bytes staged per unit                              */
+} ds_launch;
+
+/* Fill *out for `kernel` (DS_KERNEL_FUSED, DS_KERNEL_FUSED_GENERAL or
+ * DS_KERNEL_GENERIC) as ds_run would launch it for n_frames on this handle.
+ * Host-only.  Returns DS_OK, DS_EINVAL, or DS_EUNSUPPORTED if that kernel
+ * cannot run the handle. */
+DS_API int ds_launch_info(const ds_handle* h, int64_t n_frames, int32_t kernel, ds_launch* out);
 
 /* ---- the paper's unfused structure and its transfer schedules
  *

@@ -110,6 +110,23 @@ class ds_task_body(C.Structure):
     ]
 
 
+class ds_launch(C.Structure):
+    _fields_ = [
+        ("kernel", C.c_int32),
+        ("grid", C.c_int32),
+        ("block", C.c_int32),
+        ("smem_bytes", C.c_int32),
+        ("stages", C.c_int32),
+        ("ctas_per_sm", C.c_int32),
+        ("consumer_warps", C.c_int32),
+        ("units", C.c_int64),
+        ("unit_in_bytes_max", C.c_int64),
+    ]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
 class ds_topology(C.Structure):
     _fields_ = [
         ("ndim", C.c_int32),
@@ -150,6 +167,7 @@ SIGNATURES = [
                           C.POINTER(ds_plan_info)]),
     ("ds_create", C.c_void_p, [C.c_int32, C.c_int32, C.c_int32, C.POINTER(ds_filter_spec)]),
     ("ds_run", C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),
+    ("ds_enable_peer", C.c_int, [C.c_void_p, C.c_int32]),
     ("ds_run_host", C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),
     ("ds_set_host_chunk", C.c_int, [C.c_void_p, C.c_int64]),
     ("ds_destroy", None, [C.c_void_p]),
@@ -166,6 +184,7 @@ SIGNATURES = [
     ("ds_set_run_bands", C.c_int, [C.c_void_p, C.c_int32]),
     ("ds_set_general_stage_bytes", C.c_int, [C.c_void_p, C.c_int64]),
     ("ds_launch_shape", C.c_int, [C.c_void_p, C.c_int64, _PI32, _PI32, _PI32]),
+    ("ds_launch_info", C.c_int, [C.c_void_p, C.c_int64, C.c_int32, C.POINTER(ds_launch)]),
     ("ds_mid_frame_bytes", C.c_int64, [C.c_void_p]),
     ("ds_run_htask", C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int32, C.c_int32,
                                C.c_void_p]),
@@ -399,6 +418,22 @@ def _current_raw_stream(device_index):
     return torch.cuda.current_stream(device_index).cuda_stream
 
 
+def _check_u8(t, what: str, cuda: bool, numel: int | None = None, unit: int | None = None) -> int:
+    """Argument checks shared by the facade's calls: a contiguous uint8 tensor
+    on the right side of the bus, holding a whole number of `unit`-byte
+    frames (returns that number) and, if given, exactly `numel` elements."""
+    if t.dtype is not _torch_uint8() or bool(t.is_cuda) != cuda or not t.is_contiguous():
+        raise ValueError(f"{what} must be a contiguous {'CUDA' if cuda else 'CPU'} torch.uint8 tensor")
+    n = t.numel()
+    if numel is not None and n != numel:
+        raise ValueError(f"{what} holds {n} bytes, expected {numel}")
+    if unit is not None:
+        if n % unit:
+            raise ValueError(f"{what} does not hold a whole number of {unit}-byte frames")
+        return n // unit
+    return n
+
+
 class Downscaler:
     """``Downscaler(w, h, channels=3, chroma="420", spec=None)(frames)``.
 
@@ -455,6 +490,13 @@ class Downscaler:
             out.append(((a.value, b.value), (c.value, d.value)))
         return out
 
+    def enable_peer(self, peer_device: int) -> None:
+        """ds_enable_peer: let ds_run store its output on GPU ``peer_device``
+        (a buffer mapped from another rank, the fused gather of dist.py)."""
+        rc = lib().ds_enable_peer(self._h, int(peer_device))
+        if rc:
+            raise DSError(rc, "ds_enable_peer")
+
     def set_kernel(self, kernel: int) -> None:
         rc = lib().ds_set_kernel(self._h, kernel)
         if rc:
@@ -506,6 +548,15 @@ class Downscaler:
             raise DSError(rc, "ds_launch_shape")
         return g.value, b.value, s.value
 
+    def launch_info(self, n_frames: int, kernel: int | None = None) -> dict:
+        """ds_launch_info for `kernel` (default: the kernel of the last ds_run)."""
+        li = ds_launch()
+        k = self.last_kernel() if kernel is None else kernel
+        rc = lib().ds_launch_info(self._h, n_frames, k, C.byref(li))
+        if rc:
+            raise DSError(rc, "ds_launch_info")
+        return li.as_dict()
+
     # ---- the paper's unfused structure / schedules (SURVEY f1, f2) --------
     @property
     def mid_frame_bytes(self) -> int:
@@ -515,9 +566,10 @@ class Downscaler:
         """H task alone (K-N3): frames -> Mid (n, mid_frame_bytes) in HBM."""
         import torch
 
-        n = frames.numel() // self.in_frame_bytes
+        n = _check_u8(frames, "frames", True, unit=self.in_frame_bytes)
         if mid is None:
             mid = torch.empty((n, self.mid_frame_bytes), dtype=torch.uint8, device=frames.device)
+        _check_u8(mid, "mid", True, numel=n * self.mid_frame_bytes)
         p0, pc = planes if planes is not None else (0, self.channels)
         s = stream if stream is not None else torch.cuda.current_stream()
         rc = lib().ds_run_htask(self._h, frames.data_ptr(), n, mid.data_ptr(), p0, pc, s.cuda_stream)
@@ -529,9 +581,10 @@ class Downscaler:
         """V task alone (K-N3): Mid -> frames out."""
         import torch
 
-        n = mid.numel() // self.mid_frame_bytes
+        n = _check_u8(mid, "mid", True, unit=self.mid_frame_bytes)
         if out is None:
             out = self.alloc_out(n)
+        _check_u8(out, "out", True, numel=n * self.out_frame_bytes)
         p0, pc = planes if planes is not None else (0, self.channels)
         s = stream if stream is not None else torch.cuda.current_stream()
         rc = lib().ds_run_vtask(self._h, mid.data_ptr(), n, out.data_ptr(), p0, pc, s.cuda_stream)
@@ -547,10 +600,11 @@ class Downscaler:
         (host_out, stats dict)."""
         import torch
 
-        n = host_frames.numel() // self.in_frame_bytes
+        n = _check_u8(host_frames, "host_frames", False, unit=self.in_frame_bytes)
         if host_out is None:
             host_out = torch.empty((n, self.out_frame_bytes), dtype=torch.uint8,
                                    pin_memory=host_frames.is_pinned())
+        _check_u8(host_out, "host_out", False, numel=n * self.out_frame_bytes)
         st = ds_schedule_stats()
         s = stream if stream is not None else torch.cuda.current_stream()
         rc = lib().ds_run_schedule(self._h, host_frames.data_ptr(), n, host_out.data_ptr(), schedule,
@@ -591,12 +645,11 @@ class Downscaler:
         Asynchronous on the stream; synchronise before reading host_out."""
         import torch
 
-        if host_frames.dtype != torch.uint8 or host_frames.is_cuda or not host_frames.is_contiguous():
-            raise ValueError("host_frames must be a contiguous CPU torch.uint8 tensor")
-        n = host_frames.numel() // self.in_frame_bytes
+        n = _check_u8(host_frames, "host_frames", False, unit=self.in_frame_bytes)
         if host_out is None:
             host_out = torch.empty((n, self.out_frame_bytes), dtype=torch.uint8,
                                    pin_memory=host_frames.is_pinned())
+        _check_u8(host_out, "host_out", False, numel=n * self.out_frame_bytes)
         s = stream if stream is not None else torch.cuda.current_stream()
         ds_run_host(self._h, host_frames.data_ptr(), n, host_out.data_ptr(), s.cuda_stream)
         return host_out

@@ -22,6 +22,7 @@ NVCC_FLAGS = [
 def sources():
     return sorted(glob.glob(os.path.join(PKG, "csrc", "*.cu")) +
                   glob.glob(os.path.join(PKG, "csrc", "*.cuh")) +
+                  glob.glob(os.path.join(PKG, "csrc", "*.h")) +
                   [os.path.join(ROOT, "include", "ds.h")])
 
 
@@ -33,15 +34,33 @@ def stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile every csrc/*.cu to an object in parallel, then link libds.so."""
     if not force and not stale():
         return LIB
+    from concurrent.futures import ThreadPoolExecutor
+
     cu = [s for s in sources() if s.endswith(".cu")]
-    tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [NVCC, *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), *cu, "-o", tmp]
+    tag = f".tmp{os.getpid()}"
+    flags = [f for f in NVCC_FLAGS if f != "-shared"]
     if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-    subprocess.check_call(cmd)
-    os.replace(tmp, LIB)
+        flags = ["-Xptxas=-v", *flags]
+
+    def compile_one(src):
+        obj = os.path.join(PKG, "csrc", os.path.basename(src) + tag + ".o")
+        subprocess.check_call([NVCC, *flags, "-I", os.path.join(ROOT, "include"), "-c", src, "-o", obj])
+        return obj
+
+    with ThreadPoolExecutor(max_workers=len(cu)) as ex:
+        objs = list(ex.map(compile_one, cu))
+    tmp = LIB + tag
+    try:
+        subprocess.check_call([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared",
+                               "-Xcompiler", "-fPIC", *objs, "-o", tmp])
+        os.replace(tmp, LIB)
+    finally:
+        for o in objs:
+            if os.path.exists(o):
+                os.remove(o)
     return LIB
 
 

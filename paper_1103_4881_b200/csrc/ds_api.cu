@@ -708,30 +708,20 @@ bool device_ptr_on(const void* p, int dev) {
     return a.device == dev;
 }
 
-// Output memory the kernels on `dev` may write: device memory of `dev`, or of
-// a peer GPU that `dev` can reach over NVLink / PCIe P2P (e.g. another rank's
-// buffer mapped with CUDA IPC: the fused compute + gather of dist.py).  Peer
-// access is enabled on first use.
-bool device_or_peer_ptr(const void* p, int dev) {
+// Output memory the kernels of handle h may write: device memory of h's
+// device, or of a peer GPU the caller has enabled explicitly with
+// ds_enable_peer (e.g. another rank's buffer mapped with CUDA IPC: the fused
+// compute + gather of dist.py).  No side effects: ds_run never enables peer
+// access itself (a pointer not on the handle's device is DS_EINVAL).
+bool out_ptr_ok(const ds_handle* h, const void* p) {
     cudaPointerAttributes a;
     if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
         cudaGetLastError();
         return false;
     }
     if (a.type != cudaMemoryTypeDevice && a.type != cudaMemoryTypeManaged) return false;
-    if (a.device == dev) return true;
-    int can = 0;
-    if (cudaDeviceCanAccessPeer(&can, dev, a.device) != cudaSuccess || !can) {
-        cudaGetLastError();
-        return false;
-    }
-    const cudaError_t e = cudaDeviceEnablePeerAccess(a.device, 0);   // current device is dev
-    if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) {
-        cudaGetLastError();
-        return false;
-    }
-    cudaGetLastError();                            // clear "already enabled"
-    return true;
+    if (a.device == h->device) return true;
+    return a.device >= 0 && a.device < 64 && ((h->peer_mask.load() >> a.device) & 1ull);
 }
 
 bool ranges_overlap(const void* a, int64_t na, const void* b, int64_t nb) {
@@ -862,8 +852,31 @@ DS_API int ds_run(ds_handle* h, const uint8_t* in, int64_t n, uint8_t* out, ds_s
     if (ranges_overlap(in, nin, out, nout)) return DS_EINVAL;
     DeviceGuard g(h->device);
     if (!g.ok) { cudaGetLastError(); return DS_ECUDA; }
-    if (!device_ptr_on(in, h->device) || !device_or_peer_ptr(out, h->device)) return DS_EINVAL;
+    if (!device_ptr_on(in, h->device) || !out_ptr_ok(h, out)) return DS_EINVAL;
     return run_device(h, in, n, out, reinterpret_cast<cudaStream_t>(stream));
+}
+
+DS_API int ds_enable_peer(ds_handle* h, int32_t peer_device) {
+    if (!h || peer_device < 0 || peer_device >= 64) return DS_EINVAL;
+    if (peer_device == h->device) return DS_OK;
+    int count = 0, can = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess) { cudaGetLastError(); return DS_ECUDA; }
+    if (peer_device >= count) return DS_EINVAL;
+    if (cudaDeviceCanAccessPeer(&can, h->device, peer_device) != cudaSuccess) {
+        cudaGetLastError();
+        return DS_ECUDA;
+    }
+    if (!can) return DS_EUNSUPPORTED;
+    DeviceGuard g(h->device);
+    if (!g.ok) { cudaGetLastError(); return DS_ECUDA; }
+    const cudaError_t e = cudaDeviceEnablePeerAccess(peer_device, 0);
+    if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) {
+        cudaGetLastError();
+        return DS_ECUDA;
+    }
+    cudaGetLastError();                            // clear "already enabled"
+    h->peer_mask.fetch_or(1ull << peer_device);
+    return DS_OK;
 }
 
 DS_API int ds_set_host_chunk(ds_handle* h, int64_t frames) {
@@ -1010,34 +1023,66 @@ DS_API int ds_last_kernel(const ds_handle* h) { return h ? h->last_kernel.load()
 
 DS_API int ds_set_tuning(ds_handle* h, int32_t stages, int32_t ctas_per_sm) {
     if (!h || stages < 2 || stages > 8 || ctas_per_sm < 0 || ctas_per_sm > 32) return DS_EINVAL;
-    h->fused.stages = stages;
-    h->fused.ctas_per_sm = ctas_per_sm;
-    h->fine = FusedCfg{};          // an explicit tuning applies to every call size
+    FusedCfg c = h->fused;
+    c.stages = stages;
+    c.ctas_per_sm = ctas_per_sm;
     DeviceGuard g(h->device);
-    return prepare_cfg(h->fused);
+    const int rc = prepare_cfg(c);
+    if (rc) return rc;
+    h->fused = c;
+    h->fine = FusedCfg{};          // an explicit tuning applies to every call size
+    h->tune_stages = stages;       // kept across ds_set_band_bytes / ds_set_general_stage_bytes
+    h->tune_ctas = ctas_per_sm;
+    return DS_OK;
+}
+
+// Re-plan the handle with new band / stage targets: the new plan and its
+// configurations are committed only if all of them succeed (a failure leaves
+// the handle exactly as it was), and an explicit ds_set_tuning is re-applied.
+static int replan(ds_handle* h, int64_t band_target, int64_t general_target) {
+    ds_plan_info pi;
+    int rc = make_plan(h->W, h->H, h->channels, &h->spec, nullptr, &pi, band_target, general_target);
+    if (rc) return rc;
+    const ds_plan_info old_plan = h->plan;
+    const FusedCfg old_fused = h->fused, old_fine = h->fine;
+    const GeneralCfg old_general = h->general;
+    const int64_t old_band = h->band_target, old_gen = h->general_target;
+    h->plan = pi;
+    h->band_target = band_target;
+    h->general_target = general_target;
+    rc = configure_fused(h);
+    if (!rc) rc = configure_general(h);
+    if (!rc && h->tune_stages > 0 && h->fused.valid) {
+        FusedCfg c = h->fused;
+        c.stages = h->tune_stages;
+        c.ctas_per_sm = h->tune_ctas;
+        DeviceGuard g(h->device);
+        rc = prepare_cfg(c);
+        if (!rc) {
+            h->fused = c;
+            h->fine = FusedCfg{};
+        }
+    }
+    if (rc) {
+        h->plan = old_plan;
+        h->fused = old_fused;
+        h->fine = old_fine;
+        h->general = old_general;
+        h->band_target = old_band;
+        h->general_target = old_gen;
+    }
+    return rc;
 }
 
 DS_API int ds_set_band_bytes(ds_handle* h, int64_t target) {
     if (!h || target < 0) return DS_EINVAL;
     if (target == 0) target = kUnitTargetBytes;
-    ds_plan_info pi;
-    const int rc = make_plan(h->W, h->H, h->channels, &h->spec, nullptr, &pi, target, h->general_target);
-    if (rc) return rc;
-    h->plan = pi;
-    h->band_target = target;
-    const int crc = configure_fused(h);
-    return crc ? crc : configure_general(h);
+    return replan(h, target, h->general_target);
 }
 
 DS_API int ds_set_general_stage_bytes(ds_handle* h, int64_t target) {
     if (!h || target < 0) return DS_EINVAL;
-    ds_plan_info pi;
-    const int rc = make_plan(h->W, h->H, h->channels, &h->spec, nullptr, &pi, h->band_target, target);
-    if (rc) return rc;
-    h->plan = pi;
-    h->general_target = target;
-    const int crc = configure_fused(h);
-    return crc ? crc : configure_general(h);
+    return replan(h, h->band_target, target);
 }
 
 DS_API int ds_set_run_bands(ds_handle* h, int32_t bands) {
@@ -1075,6 +1120,48 @@ DS_API int ds_launch_shape(const ds_handle* h, int64_t n, int32_t* grid, int32_t
     if (block) *block = bl;
     if (smem) *smem = sm;
     return DS_OK;
+}
+
+DS_API int ds_launch_info(const ds_handle* h, int64_t n, int32_t kernel, ds_launch* out) {
+    if (!h || n < 0 || !out) return DS_EINVAL;
+    std::memset(out, 0, sizeof *out);
+    out->kernel = kernel;
+    if (kernel == DS_KERNEL_FUSED) {
+        if (!h->plan.fused_eligible || !h->fused.valid) return DS_EUNSUPPORTED;
+        const FusedCfg& c = pick_cfg(h, n);
+        int gr, bl, sm;
+        const int rc = fused_grid(h, c, std::max<int64_t>(1, n * c.plan.units_per_frame), &gr, &bl, &sm);
+        if (rc) return rc;
+        out->grid = gr; out->block = bl; out->smem_bytes = sm;
+        out->stages = c.run_stages;
+        out->ctas_per_sm = c.grid_per_sm;
+        out->consumer_warps = c.ncw;
+        out->units = n * c.plan.units_per_frame;
+        out->unit_in_bytes_max = c.plan.unit_in_bytes_max;
+        return DS_OK;
+    }
+    if (kernel == DS_KERNEL_FUSED_GENERAL) {
+        const GeneralCfg& c = h->general;
+        if (!h->plan.fused_general_eligible || !c.valid) return DS_EUNSUPPORTED;
+        int32_t L[DS_MAX_PLANES];
+        const int64_t units = n * general_runs(h, n, L);
+        out->grid = (int32_t)std::max<int64_t>(1, std::min<int64_t>(units, (int64_t)c.grid_per_sm * h->sm_count));
+        out->block = c.threads; out->smem_bytes = c.smem;
+        out->stages = c.stages;
+        out->ctas_per_sm = c.grid_per_sm;
+        out->consumer_warps = c.ncw;
+        out->units = units;
+        out->unit_in_bytes_max = h->plan.general_stage_bytes_max;
+        return DS_OK;
+    }
+    if (kernel == DS_KERNEL_GENERIC) {
+        out->block = 256;
+        const int64_t total_out = n * h->plan.out_frame_bytes;
+        out->grid = (int32_t)std::max<int64_t>(1, std::min<int64_t>((total_out + 255) / 256, (int64_t)h->sm_count * 8));
+        out->units = total_out;
+        return DS_OK;
+    }
+    return DS_EINVAL;
 }
 
 DS_API int ds_generate(uint8_t* dev, int64_t n_bytes, uint64_t seed, int64_t start,

@@ -116,10 +116,12 @@ struct ds_handle {
     dsi::GeneralCfg general;
     int kernel_pref = DS_KERNEL_AUTO;
     int32_t run_bands = 0;                  // ds_set_run_bands (0 = automatic)
+    int32_t tune_stages = 0, tune_ctas = 0; // explicit ds_set_tuning (0 stages = none)
     bool htask_tma_ready = false;           // smem attribute set for ds_htask_tma_kernel
     int64_t general_target = 0;             // ds_set_general_stage_bytes (0 = default)
     uint32_t* debug_unit_count = nullptr;   // ds_set_debug_counter
     std::atomic<int> last_kernel{DS_KERNEL_AUTO};
+    std::atomic<uint64_t> peer_mask{0};     // ds_enable_peer: peer devices ds_run may store to
     // ds_run_host / ds_run_schedule state (lazily allocated, guarded by host_mu)
     std::mutex host_mu;
     int64_t host_chunk = 0;      // frames per chunk, 0 = auto
@@ -136,7 +138,7 @@ void default_spec(ds_filter_spec* s);
 bool stage_equal(const ds_stage_spec& a, const ds_stage_spec& b);
 bool aligned16(const void* p);
 bool device_ptr_on(const void* p, int dev);
-bool device_or_peer_ptr(const void* p, int dev);
+bool out_ptr_ok(const ds_handle* h, const void* p);
 bool ranges_overlap(const void* a, int64_t na, const void* b, int64_t nb);
 int run_device(ds_handle* h, const uint8_t* in, int64_t n, uint8_t* out, cudaStream_t st);
 void free_sched_state(ds_handle* h);

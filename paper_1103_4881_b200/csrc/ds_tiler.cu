@@ -47,9 +47,11 @@ struct TaskParams {
     TTiler tin, tout;
     int32_t n_in, n_out, divisor, bias;
     int32_t w[DS_MAX_OUTPUTS][DS_MAX_PATTERN];
-    // DS_TOPO_SPEC: collapsed multiplicity (row-major, last fastest -> CUDA x)
+    // DS_TOPO_SPEC: collapsed multiplicity (row-major, last fastest) and the
+    // CUDA axis (0 = x, 1 = y, 2 = z) each collapsed dim is launched along
     int32_t tdim;
     int64_t tmult[3];
+    int32_t tax[3];
     // Affine path (host-proved: no tiler index wraps anywhere in the box, so the
     // element offset is A + sum_j a[j] r_j + b[e], all in [0, n) < 2^31)
     int32_t affine;                    // 0: modulo path; 1: byte loads; 2: word loads + dp4a;
@@ -280,17 +282,13 @@ __device__ __forceinline__ void task_affine(const TaskParams& p, uint32_t q) {
 template <int NI, bool WORDS, int Q>
 __global__ void __launch_bounds__(256) ds_task_affine_kernel(const __grid_constant__ TaskParams p) {
     if (p.policy == DS_TOPO_SPEC) {
-        const uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
-        const uint32_t y = blockIdx.y * blockDim.y + threadIdx.y;
-        const uint32_t z = blockIdx.z * blockDim.z + threadIdx.z;
-        uint32_t c[3] = {0, 0, 0};
-        if (p.tdim == 1) { c[0] = x; }
-        else if (p.tdim == 2) { c[0] = y; c[1] = x; }
-        else { c[0] = z; c[1] = y; c[2] = x; }
+        const uint32_t hw[3] = {blockIdx.x * blockDim.x + threadIdx.x, blockIdx.y * blockDim.y + threadIdx.y,
+                                blockIdx.z * blockDim.z + threadIdx.z};
         uint32_t q = 0;
         for (int d = 0; d < p.tdim; ++d) {
-            if (c[d] >= (uint32_t)p.tmult[d]) return;     // guard
-            q = q * (uint32_t)p.tmult[d] + c[d];
+            const uint32_t c = hw[p.tax[d]];
+            if (c >= (uint32_t)p.tmult[d]) return;        // guard
+            q = q * (uint32_t)p.tmult[d] + c;
         }
         task_affine<NI, WORDS, Q>(p, q);
         return;
@@ -506,17 +504,14 @@ template <int NI>
 __global__ void __launch_bounds__(256, 1) ds_task_kernel(const __grid_constant__ TaskParams p) {
     if (p.policy == DS_TOPO_SPEC) {
         // NDRange work-item = one elementary task; guarded padding
-        const int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-        const int64_t y = (int64_t)blockIdx.y * blockDim.y + threadIdx.y;
-        const int64_t z = (int64_t)blockIdx.z * blockDim.z + threadIdx.z;
-        int64_t c[3] = {0, 0, 0};
-        if (p.tdim == 1) { c[0] = x; }
-        else if (p.tdim == 2) { c[0] = y; c[1] = x; }
-        else { c[0] = z; c[1] = y; c[2] = x; }
+        const int64_t hw[3] = {(int64_t)blockIdx.x * blockDim.x + threadIdx.x,
+                               (int64_t)blockIdx.y * blockDim.y + threadIdx.y,
+                               (int64_t)blockIdx.z * blockDim.z + threadIdx.z};
         int64_t q = 0;
         for (int d = 0; d < p.tdim; ++d) {
-            if (c[d] >= p.tmult[d]) return;               // guard
-            q = q * p.tmult[d] + c[d];
+            const int64_t c = hw[p.tax[d]];
+            if (c >= p.tmult[d]) return;                  // guard
+            q = q * p.tmult[d] + c;
         }
         task_one<NI>(p, q);
         return;
@@ -873,17 +868,34 @@ int launch_task(const uint8_t* in, const ds_tiler& t_in, uint8_t* out, const ds_
         ds_topology topo;
         if ((rc = ds_compute_topology(nrep, rep_shape, 1024, 3, 64, 256, &topo))) return rc;
         p.tdim = topo.ndim;
-        dim3 block(1, 1, 1), grid(1, 1, 1);
-        const int64_t lim[3] = {2147483647LL, 65535LL, 65535LL};
-        for (int d = 0; d < topo.ndim; ++d) {
-            p.tmult[d] = topo.multiplicity[d];
-            const int ax = topo.ndim - 1 - d;      // last collapsed dim -> x
-            const int64_t g = topo.global[d] / topo.local[d];
-            if (g > lim[ax]) return DS_EUNSUPPORTED;
-            (ax == 0 ? block.x : ax == 1 ? block.y : block.z) = (unsigned)topo.local[d];
-            (ax == 0 ? grid.x : ax == 1 ? grid.y : grid.z) = (unsigned)g;
+        // CUDA limits: block (1024, 1024, 64), grid (2^31 - 1, 65535, 65535).
+        // Each collapsed dim goes to its own axis; the preferred assignment
+        // puts the last (fastest) dim on x, the first permutation of the
+        // axes that fits both limits is launched.
+        const int64_t blim[3] = {1024, 1024, 64}, glim[3] = {2147483647LL, 65535LL, 65535LL};
+        static const int perms[6][3] = {{0, 1, 2}, {0, 2, 1}, {1, 0, 2}, {1, 2, 0}, {2, 0, 1}, {2, 1, 0}};
+        bool placed = false;
+        for (int pi = 0; pi < 6 && !placed; ++pi) {
+            // perms[pi][k] = axis of the k-th dim counted from the last one
+            bool fits = true;
+            for (int k = 0; k < topo.ndim && fits; ++k) {
+                const int d = topo.ndim - 1 - k, ax = perms[pi][k];
+                if (topo.ndim < 3 && ax >= topo.ndim) fits = false;
+                if (topo.local[d] > blim[ax] || topo.global[d] / topo.local[d] > glim[ax]) fits = false;
+            }
+            if (!fits) continue;
+            dim3 block(1, 1, 1), grid(1, 1, 1);
+            for (int k = 0; k < topo.ndim; ++k) {
+                const int d = topo.ndim - 1 - k, ax = perms[pi][k];
+                p.tmult[d] = topo.multiplicity[d];
+                p.tax[d] = ax;
+                (ax == 0 ? block.x : ax == 1 ? block.y : block.z) = (unsigned)topo.local[d];
+                (ax == 0 ? grid.x : ax == 1 ? grid.y : grid.z) = (unsigned)(topo.global[d] / topo.local[d]);
+            }
+            fn<<<grid, block, 0, st>>>(p);
+            placed = true;
         }
-        fn<<<grid, block, 0, st>>>(p);
+        if (!placed) return DS_EUNSUPPORTED;
     } else {
         const int64_t items = p.affine == 3 ? p.n_reps / 4 : p.n_reps;      // column quads
         const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((items + 255) / 256, (int64_t)sms * 16));

@@ -27,35 +27,61 @@ def shard_range(total: int, world: int, rank: int) -> tuple[int, int]:
     return (total * rank) // world, (total * (rank + 1)) // world
 
 
-def gather_frames(local: torch.Tensor, total: int, group=None, dst: int = 0):
-    """Gather every rank's (n_r, frame_bytes) shard to `dst` in frame order.
+def gather_frames(local: torch.Tensor, total: int, group=None, dst: int = 0, out=None):
+    """Gather every rank's (n_r, frame_bytes) shard to `dst` in frame order
+    (collective C-1).  `local` may also be already padded to
+    (m, frame_bytes), its first n_r rows valid: then nothing is copied.
 
-    Uses point-to-point batches (shards may differ in size by one frame).
-    Returns the (total, frame_bytes) tensor on dst, None elsewhere (on the
-    host when the group's backend is gloo)."""
+    One collective that every rank of the group enters: shards differ by at
+    most one frame (shard_range), so each rank pads its shard to
+    m = ceil(total / world) frames and the group runs ``dist.gather`` of
+    equal-sized tensors (NCCL: one grouped send/recv on the group's
+    communicator; gloo: the same on the host).  dst then compacts the
+    per-rank blocks [r*m, r*m + n_r) to the frame-ordered [lo_r, hi_r) in
+    place, moving rows only towards the front, rank by rank.  No plain
+    send/recv is mixed with batched P2P, so NCCL's lazily created
+    communicators cannot mismatch.
+
+    `out` (dst only, optional): a (world*m, frame_bytes) receive buffer to
+    reuse across calls (padded_gather_rows gives its row count).  Returns the
+    (total, frame_bytes) tensor on dst (a view of `out` when given), None
+    elsewhere; on the host when the group's backend is gloo."""
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     if local.is_cuda and dist.get_backend(group) == "gloo":
         local = local.cpu()              # gloo moves host tensors (tests on one GPU)
-    fb = local.shape[1] if local.dim() == 2 else local.numel()
+    lo, hi = shard_range(total, world, rank)
+    n = hi - lo
+    m = padded_gather_rows(total, world) // world
+    if local.dim() != 2 or local.shape[0] not in (n, m):
+        raise ValueError(f"rank {rank}: local must be ({n} or {m}, frame_bytes) for shard [{lo}, {hi})")
+    fb = local.shape[1]
+    if total == 0:
+        return local.new_empty((0, fb)) if rank == dst else None
+    if local.shape[0] < m:               # pad to the common shard size
+        send = local.new_zeros((m, fb))
+        send[:n].copy_(local[:n])
+    else:
+        send = local.contiguous()
     if rank != dst:
-        if local.numel():
-            dist.send(local.contiguous(), dst, group=group)
+        dist.gather(send, None, dst=dst, group=group)
         return None
-    out = torch.empty((total, fb), dtype=local.dtype, device=local.device)
-    ops = []
-    for r in range(world):
-        lo, hi = shard_range(total, world, r)
-        if hi == lo:
-            continue
-        if r == dst:
-            out[lo:hi].copy_(local.view(hi - lo, fb))
-        else:
-            ops.append(dist.P2POp(dist.irecv, out[lo:hi], r, group=group))
-    if ops:
-        for req in dist.batch_isend_irecv(ops):
-            req.wait()
-    return out
+    if out is None:
+        out = local.new_empty((world * m, fb))
+    elif tuple(out.shape) != (world * m, fb) or out.dtype != local.dtype or out.device != local.device:
+        raise ValueError("out must be a (padded_gather_rows(total, world), frame_bytes) buffer like local")
+    dist.gather(send, [out[r * m:(r + 1) * m] for r in range(world)], dst=dst, group=group)
+    for r in range(1, world):            # compact: rows only move towards the front
+        a, b = shard_range(total, world, r)
+        if b > a and a != r * m:
+            src = out[r * m:r * m + (b - a)]
+            out[a:b].copy_(src.clone() if b > r * m else src)   # clone when the ranges overlap
+    return out[:total]
+
+
+def padded_gather_rows(total: int, world: int) -> int:
+    """Rows of gather_frames' receive buffer: world x ceil(total / world)."""
+    return world * (-(-total // world) if total else 0)
 
 
 def run_sharded(total_frames: int, w: int, h: int, channels: int = 3, chroma: str = "420",
@@ -118,6 +144,7 @@ def run_sharded_fused_gather(total_frames: int, w: int, h: int, channels: int = 
     x = generate_frames(hi - lo, d.in_frame_bytes, seed=seed, first_frame=lo)
     full = torch.empty((total_frames, d.out_frame_bytes), dtype=torch.uint8, device="cuda") if rank == 0 else None
     full = share_rank0_tensor(full)
+    d.enable_peer(full.device.index)        # explicit, once: ds_run has no side effects
     if hi > lo:
         d(x, out=full[lo:hi])
     torch.cuda.synchronize()

@@ -34,8 +34,43 @@ def splitmix64(x: np.ndarray) -> np.ndarray:
         return z ^ (z >> np.uint64(31))
 
 
-def random_bytes(seed: int, start: int, count: int, chunk: int = 1 << 24) -> np.ndarray:
-    """Bytes i = start .. start+count-1 of the seeded stream."""
+_CLIB = None
+
+
+def build(force: bool = False) -> str:
+    """Compile synth_gen.c (the same generator in C) to libsynth.so."""
+    import os
+    import subprocess
+
+    here = os.path.dirname(os.path.abspath(__file__))
+    src, so = os.path.join(here, "synth_gen.c"), os.path.join(here, "libsynth.so")
+    if force or not os.path.exists(so) or os.path.getmtime(so) < os.path.getmtime(src):
+        tmp = so + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", "-std=c11", "-O2", "-fPIC", "-shared", "-o", tmp, src])
+        os.replace(tmp, so)
+    return so
+
+
+def _clib():
+    """libsynth.so, built on first use; None if no C compiler is at hand
+    (then the numpy generator below serves alone)."""
+    global _CLIB
+    if _CLIB is None:
+        import ctypes
+
+        try:
+            L = ctypes.CDLL(build())
+            L.synth_random_bytes.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
+                                             ctypes.c_void_p]
+            L.synth_random_bytes.restype = None
+            _CLIB = L
+        except Exception:
+            _CLIB = False
+    return _CLIB or None
+
+
+def random_bytes_numpy(seed: int, start: int, count: int, chunk: int = 1 << 24) -> np.ndarray:
+    """Bytes i = start .. start+count-1 of the seeded stream (numpy form)."""
     out = np.empty(count, np.uint8)
     with np.errstate(over="ignore"):
         base = np.uint64(seed) * GOLDEN
@@ -43,6 +78,20 @@ def random_bytes(seed: int, start: int, count: int, chunk: int = 1 << 24) -> np.
             n = min(chunk, count - lo)
             idx = np.arange(start + lo, start + lo + n, dtype=np.uint64) + base
             out[lo: lo + n] = (splitmix64(idx) >> np.uint64(56)).astype(np.uint8)
+    return out
+
+
+def random_bytes(seed: int, start: int, count: int, out: np.ndarray | None = None) -> np.ndarray:
+    """Bytes i = start .. start+count-1 of the seeded stream (C when built,
+    else numpy; the two are byte-identical)."""
+    if out is None:
+        out = np.empty(count, np.uint8)
+    L = _clib()
+    if L is None:
+        out[:] = random_bytes_numpy(seed, start, count)
+        return out
+    assert out.dtype == np.uint8 and out.flags.c_contiguous and out.size == count
+    L.synth_random_bytes(seed % (1 << 64), start, count, out.ctypes.data)
     return out
 
 
@@ -60,10 +109,11 @@ def in_frame_bytes(W: int, H: int, channels: int = 3, chroma: int = 1) -> int:
 
 
 def random_frames(seed: int, first_frame: int, n: int, W: int, H: int, channels: int = 3,
-                  chroma: int = 1) -> np.ndarray:
+                  chroma: int = 1, out: np.ndarray | None = None) -> np.ndarray:
     """Frames first_frame .. first_frame+n-1 of the seeded stream, (n, frame_bytes)."""
     fb = in_frame_bytes(W, H, channels, chroma)
-    return random_bytes(seed, first_frame * fb, n * fb).reshape(n, fb)
+    flat = None if out is None else out.reshape(-1)
+    return random_bytes(seed, first_frame * fb, n * fb, out=flat).reshape(n, fb)
 
 
 def _assemble(planes_fn, n, W, H, channels, chroma):

@@ -158,6 +158,7 @@ def test_null_handle_calls():
     assert L.ds_run(None, None, 0, None, None) == ds.DS_EINVAL
     assert L.ds_in_frame_bytes(None) == -1
     assert L.ds_set_kernel(None, 0) == ds.DS_EINVAL
+    assert L.ds_enable_peer(None, 0) == ds.DS_EINVAL
     L.ds_destroy(None)                                    # NULL-safe
     assert L.ds_generate(None, 0, 1, 0, None) == ds.DS_OK   # n = 0 no-op
     assert L.ds_generate(None, 16, 1, 0, None) == ds.DS_EINVAL

@@ -72,5 +72,41 @@ def test_bench_line_contract():
     assert e["matches_device_path"] is True
     c = j["clocks"]
     assert c["sm_max_mhz"] > 0 and isinstance(c["reasons"], list)
+    assert c["samples"] >= 20 and c["samples_in_timed_region"] >= 1
     cb = j["cpu_baseline"]
-    assert cb["kind"] == "oracle" and cb["parity_bit_exact_frames"] == cb["parity_checked_frames"] > 0
+    assert cb["kind"] == "oracle" and cb["cores"] == 1 and cb["value"] > 0
+    p = j["parity"]
+    assert p["frames_checked"] == p["frames_total"] == 300 and p["bit_exact"] is True
+    assert j["stages"] >= 2 and j["ctas_per_sm"] >= 1
+    # both arms print the same config object (the driver's same_config check)
+    ref = _line(["--impl", "reference", "--steps", "2", "--warmup", "1"])
+    assert ref["config"] == j["config"]
+
+
+@pytest.mark.gpu
+def test_bench_halo_spec_line():
+    """--spec halo: the K-N1g kernel on the halo spec, roofline on in + out
+    bytes, every frame checked against O1 with the spec's stages."""
+    j = _line(["--spec", "halo", "--steps", "10", "--warmup", "3", "--cpu-seconds", "2", "--no-ncu"])
+    assert j["roofline"]["kernel"] == "ds_fused_general_kernel"
+    fin, fout = j["config"]["in_frame_bytes"], j["config"]["out_frame_bytes"]
+    assert j["roofline"]["algorithmic_bytes_per_launch"] == 300 * (fin + fout)
+    p = j["parity"]
+    assert p["bit_exact"] is True and p["frames_checked"] == 300 and p["oracle"].startswith("O1")
+    ref = _line(["--impl", "reference", "--spec", "halo", "--steps", "2", "--warmup", "1"])
+    assert ref["config"] == j["config"]
+
+
+def test_config_dict_is_shared_by_both_arms():
+    """Both arms build `config` with bench.config_dict from the same inputs."""
+    sys.path.insert(0, ROOT)
+    import bench
+
+    for spec in ("spec", "halo"):
+        a = bench.parse(["--spec", spec])
+        cfg = bench.workload(a, 1)
+        c = bench.config_dict(a, cfg, 1)
+        assert c["in_frame_bytes"] == 3110400 and c["out_frame_bytes"] == 518400
+    j = _line(["--impl", "reference", "--config", "qcif420", "--steps", "1", "--warmup", "0"])
+    a = bench.parse(["--config", "qcif420"])
+    assert j["config"] == bench.config_dict(a, bench.workload(a, 1), 1)

@@ -40,9 +40,10 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, total, W, H, q):
+def _worker(rank, world, port, total, W, H, q, padded=False):
     import oracle
     import synth
+    from paper_1103_4881_b200.dist import padded_gather_rows
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -51,17 +52,29 @@ def _worker(rank, world, port, total, W, H, q):
         frames = synth.random_frames(5, lo, hi - lo, W, H)          # by GLOBAL frame index
         fin, fout = oracle.frame_bytes(W, H)
         local = oracle.execute_frames(frames, W, H) if hi > lo else np.zeros((0, fout), np.uint8)
-        full = gather_frames(torch.from_numpy(local.copy()), total)
-        if rank == 0:
-            q.put(full.numpy())
-        else:
-            assert full is None
+        local = torch.from_numpy(local.copy())
+        m = padded_gather_rows(total, world) // world
+        if padded:                       # the shard already sits in an (m, fout) buffer
+            buf = torch.full((m, fout), 77, dtype=torch.uint8)
+            buf[: hi - lo] = local
+            local = buf
+        out = torch.empty((world * m, fout), dtype=torch.uint8) if rank == 0 else None
+        for rep in range(2):             # the receive buffer is reused across calls
+            full = gather_frames(local, total, out=out)
+            if rank == 0:
+                q.put(full.numpy().copy())
+            else:
+                assert full is None
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,total", [(2, 7), (3, 5), (2, 1)])
-def test_gloo_sharded_equals_unsharded(world, total):
+@pytest.mark.parametrize("world,total,padded", [(2, 7, False), (3, 5, False), (2, 1, False), (3, 11, False),
+                                                (4, 2, False), (2, 7, True), (3, 10, True)])
+def test_gloo_sharded_equals_unsharded(world, total, padded):
+    """One dist.gather of equal padded shards (the NCCL-safe form: every rank
+    enters the same collective) reassembles the stream in frame order for
+    uneven shards, empty shards and pre-padded shards."""
     import oracle
     import synth
 
@@ -69,17 +82,41 @@ def test_gloo_sharded_equals_unsharded(world, total):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, total, W, H, q))
+    procs = [ctx.Process(target=_worker, args=(r, world, port, total, W, H, q, padded))
              for r in range(world)]
     for p in procs:
         p.start()
-    got = q.get(timeout=120)
+    got = [q.get(timeout=120) for _ in range(2)]
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
     want = oracle.execute_frames(synth.random_frames(5, 0, total, W, H), W, H)
-    assert got.shape == want.shape
-    assert np.array_equal(got, want)
+    for g in got:
+        assert g.shape == want.shape
+        assert np.array_equal(g, want)
+
+
+def test_gather_rejects_a_wrong_shard_shape():
+    """A local shard that does not match shard_range fails before any
+    collective (no rank can hang in a mismatched gather)."""
+    ctx = mp.get_context("spawn")
+    port = _free_port()
+    p = ctx.Process(target=_bad_shard_worker, args=(port,))
+    p.start()
+    p.join(timeout=120)
+    assert p.exitcode == 0
+
+
+def _bad_shard_worker(port):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        with pytest.raises(ValueError):
+            gather_frames(torch.zeros((3, 8), dtype=torch.uint8), 5)
+        full = gather_frames(torch.ones((5, 8), dtype=torch.uint8), 5)
+        assert full.shape == (5, 8) and int(full.sum()) == 40
+    finally:
+        dist.destroy_process_group()
 
 
 def _share_worker(rank, world, port, total, q):

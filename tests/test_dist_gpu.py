@@ -1,6 +1,8 @@
 """Multi-process sharded path on the GPU: torchrun with 2 and 3 ranks on one
-GPU (gloo backend), run_sharded + gather; the gathered stream must equal the
-single-process output and the oracle (frames are independent)."""
+GPU (gloo process group), run_sharded + gather, or the gather fused into the
+kernels; with two or more GPUs also one rank per GPU over NCCL.  The gathered
+stream must equal the single-process output and the oracle (frames are
+independent)."""
 import os
 import socket
 import subprocess
@@ -24,19 +26,13 @@ def _port():
     return p
 
 
-@pytest.mark.parametrize("mode", ["nccl", "fused"])
-@pytest.mark.parametrize("ranks,total", [(2, 7), (3, 5)])
-def test_torchrun_sharded_gather(tmp_path, ranks, total, mode):
-    """Frame-sharded runs gathered to rank 0 equal the 1-GPU run and the
-    oracle.  mode "fused": no separate gather -- every rank's ds_run writes
-    its frames into rank 0's buffer mapped through CUDA IPC (on one GPU the
-    ranks share the device; the kernels never wait on one another)."""
+def _run(tmp_path, ranks, total, mode, backend):
     torch = pytest.importorskip("torch")
     import paper_1103_4881_b200 as ds
 
     W, H = 352, 288
     out = str(tmp_path / "gathered.npy")
-    env = dict(os.environ, DS_DIST_BACKEND="gloo")
+    env = dict(os.environ, DS_DIST_BACKEND=backend)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={ranks}",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()),
            os.path.join(ROOT, "tests", "dist_worker.py"), str(total), str(W), str(H), out, mode]
@@ -49,3 +45,27 @@ def test_torchrun_sharded_gather(tmp_path, ranks, total, mode):
     assert np.array_equal(got, single)
     want = oracle.execute_frames(synth.random_frames(3, 0, total, W, H), W, H)
     assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("mode", ["gather", "fused"])
+@pytest.mark.parametrize("ranks,total", [(2, 7), (3, 5)])
+def test_torchrun_sharded_gather_one_gpu(tmp_path, ranks, total, mode):
+    """Frame-sharded runs gathered to rank 0 equal the 1-GPU run and the
+    oracle, with several ranks on one GPU over a gloo process group.  mode
+    "fused": no separate gather -- every rank's ds_run writes its frames into
+    rank 0's buffer mapped through CUDA IPC (on one GPU the ranks share the
+    device; the kernels never wait on one another)."""
+    _run(tmp_path, ranks, total, mode, "gloo")
+
+
+@pytest.mark.parametrize("mode", ["gather", "fused"])
+def test_torchrun_sharded_gather_nccl(tmp_path, mode):
+    """One rank per GPU over NCCL (NVLink / NVSwitch): the padded dist.gather
+    and the fused gather through peer stores (ds_enable_peer).  Needs >= 2
+    GPUs; uneven shards (total not a multiple of the rank count)."""
+    torch = pytest.importorskip("torch")
+    n = torch.cuda.device_count()
+    if n < 2:
+        pytest.skip("needs two or more GPUs (NCCL refuses two ranks on one device)")
+    ranks = min(n, 4)
+    _run(tmp_path, ranks, 2 * ranks + 1, mode, "nccl")

@@ -431,6 +431,36 @@ def test_run_errors():
     assert L.ds_run(d.handle, hx.data_ptr(), 2, y.data_ptr(), s) == ds.DS_EINVAL
     assert L.ds_run(d.handle, 0, 2, y.data_ptr(), s) == ds.DS_EINVAL
     assert L.ds_run(d.handle, x.data_ptr(), 0, y.data_ptr(), s) == ds.DS_OK
+    # pinned host output: not device memory, and no peer can make it one
+    hy = torch.zeros((2, d.out_frame_bytes), dtype=torch.uint8, pin_memory=True)
+    assert L.ds_run(d.handle, x.data_ptr(), 2, hy.data_ptr(), s) == ds.DS_EINVAL
+    # ds_enable_peer: own device is a no-op; a device that does not exist is EINVAL
+    assert L.ds_enable_peer(d.handle, torch.cuda.current_device()) == ds.DS_OK
+    assert L.ds_enable_peer(d.handle, torch.cuda.device_count()) == ds.DS_EINVAL
+    assert L.ds_enable_peer(d.handle, -1) == ds.DS_EINVAL
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs two GPUs")
+def test_peer_output_needs_explicit_enable():
+    """ds_run returns DS_EINVAL for an output on another GPU and
+    enables nothing itself; after ds_enable_peer the same call stores the
+    frames on the peer (the fused gather's path) bit-exactly."""
+    W, H = 352, 288
+    torch.cuda.set_device(0)
+    d = ds.Downscaler(W, H, 3)
+    fr = synth.random_frames(21, 0, 4, W, H)
+    x = torch.from_numpy(fr).cuda(0)
+    y1 = torch.zeros((4, d.out_frame_bytes), dtype=torch.uint8, device="cuda:1")
+    L = ds.lib()
+    s = torch.cuda.current_stream().cuda_stream
+    assert L.ds_run(d.handle, x.data_ptr(), 4, y1.data_ptr(), s) == ds.DS_EINVAL
+    rc = L.ds_enable_peer(d.handle, 1)
+    if rc == ds.DS_EUNSUPPORTED:
+        pytest.skip("GPUs 0 and 1 cannot access each other")
+    assert rc == ds.DS_OK
+    assert L.ds_run(d.handle, x.data_ptr(), 4, y1.data_ptr(), s) == ds.DS_OK
+    torch.cuda.synchronize()
+    _assert_same(y1.cpu().numpy(), oracle.execute_frames(fr, W, H), "peer output")
 
 
 def test_tuning_does_not_change_results():
@@ -570,6 +600,13 @@ def test_hd_300_frame_stream_every_frame():
     for f0 in range(0, N, 50):
         fr = synth.random_frames(1, f0, 50, W, H)
         _assert_same(y[f0: f0 + 50], oracle.direct_frames(fr, W, H), f"frames {f0}..{f0 + 49}")
+    for chroma in (0,):                 # HD 4:4:4 (the three-equal-planes reading, A4) too
+        d4 = ds.Downscaler(W, H, 3, chroma=chroma)
+        y4 = d4(ds.generate_frames(N, d4.in_frame_bytes, seed=1)).cpu().numpy()
+        from oracle.verify import verify_stream
+
+        r = verify_stream(y4, W, H, 3, chroma, seed=1)
+        assert r["frames_checked"] == N and r["bit_exact"], r
 
 
 def test_cuda_graph_capture():
@@ -622,32 +659,37 @@ def test_every_output_byte_written(kernel, W, H, ch, n):
         assert (b[:guard] == sentinel).all() and (b[-guard:] == sentinel).all(), "write outside output"
 
 
-@pytest.mark.parametrize("W,H,N", [(1920, 1080, 3000), (3840, 2160, 1000)])
-def test_full_size_streams_sampled(W, H, N):
-    """BASELINE configs[3] (3000 HD frames; the whole stream on one GPU, i.e.
-    every rank's shard at once) and configs[4] (1000 4K frames) at full size
-    in bench.py's launch configuration: whole-frame oracle checks on frames
-    spread over the stream (first, last, shard boundaries for 2/4/8 GPUs) and
-    O3 per-pixel samples on more."""
-    d = ds.Downscaler(W, H, 3)
+@pytest.mark.parametrize("W,H,N,chroma", [(1920, 1080, 3000, 1), (3840, 2160, 1000, 1),
+                                          (3840, 2160, 1000, 0)])
+def test_full_size_streams_every_frame(W, H, N, chroma):
+    """BASELINE configs[3] (3000 HD 4:2:0 frames: the whole stream on one GPU,
+    i.e. every rank's shard at once) and configs[4] (1000 4K frames, 4:2:0 and
+    4:4:4) at full size in bench.py's launch configuration (one ds_run over
+    the stream, default tuning), verified on EVERY frame byte for byte
+     against the oracle's direct loops (O2), fanned out
+    over the host cores as single-threaded processes that regenerate the
+    frames by global index (oracle/verify.py); plus O3 per-pixel samples."""
+    from oracle.verify import verify_stream
+
+    d = ds.Downscaler(W, H, 3, chroma=chroma)
     x = ds.generate_frames(N, d.in_frame_bytes, seed=1)
     y = d(x)
     torch.cuda.synchronize()
     assert d.last_kernel() == FUSED
-    boundaries = sorted({0, N - 1, N // 8, N // 4 - 1, N // 2, 3 * N // 8, N - N // 8})
-    for f in boundaries[:6]:
-        fr = synth.random_frames(1, f, 1, W, H)
-        _assert_same(y[f].cpu().numpy()[None], oracle.execute_frames(fr, W, H), f"frame {f}")
+    del x
+    host = y.cpu().numpy()
+    del y
+    torch.cuda.empty_cache()
+    r = verify_stream(host, W, H, 3, chroma, seed=1)
+    assert r["frames_checked"] == N and r["bit_exact"], r
     rng = np.random.default_rng(N)
-    for f in rng.choice(N, 8, replace=False):
-        fr = synth.random_frames(1, int(f), 1, W, H)[0]
-        out = y[int(f)].cpu().numpy()
-        for pin, pout in zip(oracle.split_planes(fr, W, H), oracle.split_planes(out, W, H, out=True)):
+    for f in rng.choice(N, 4, replace=False):
+        fr = synth.random_frames(1, int(f), 1, W, H, 3, chroma)[0]
+        for pin, pout in zip(oracle.split_planes(fr, W, H, 3, chroma),
+                             oracle.split_planes(host[int(f)], W, H, 3, chroma, out=True)):
             ho, wo = pout.shape
             for R, Cc in zip(rng.integers(0, ho, 100), rng.integers(0, wo, 100)):
                 assert pout[R, Cc] == oracle.pixel(pin, int(R), int(Cc))
-    del x, y
-    torch.cuda.empty_cache()
 
 
 def test_fused_kernel_fuzz():

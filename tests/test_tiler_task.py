@@ -185,6 +185,28 @@ def test_run_task_large_extents(policy):
     assert np.array_equal(y.cpu().numpy(), want)
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("rep", [(4096, 2, 1), (2, 4096, 1), (1, 3, 70000)])
+def test_run_task_spec_topology_axis_limits(rep):
+    """DS_TOPO_SPEC launches whose power-of-two box is large along the first
+    dimension (rep [4096, 2, 1] gives local[0] = 128 > the 64-thread block.z
+    limit): the launch picks CUDA axes that fit, the result is the oracle's."""
+    n0, n1, n2 = rep
+    shape = (n0, n1, n2 * 2)
+    rng = np.random.default_rng(5)
+    a = rng.integers(0, 256, shape).astype(np.uint8)
+    tin_args = (shape, (0, 0, 0), [[1, 0, 0], [0, 1, 0], [0, 0, 2]], [[0], [0], [1]], [2])
+    tout_args = (rep, (0, 0, 0), [[1, 0, 0], [0, 1, 0], [0, 0, 1]], [[0], [0], [0]], [1])
+    w = [[3, 5]]
+    want = oracle.run_task(a, oracle.make_tiler(*tin_args), rep, oracle.make_tiler(*tout_args), list(rep),
+                           oracle.make_stage(2, 2, 0, w, 8, 4))
+    y = torch.zeros(rep, dtype=torch.uint8, device="cuda")
+    ds.run_task(torch.from_numpy(a).cuda(), ds.make_tiler(*tin_args), y, ds.make_tiler(*tout_args), list(rep),
+                ds.make_body(w, 8, 4, n_in=2), policy=ds.DS_TOPO_SPEC)
+    torch.cuda.synchronize()
+    assert np.array_equal(y.cpu().numpy(), want)
+
+
 def _affine_in_tiler(rng, in_shape, R, P):
     """A wrap-free 1-rep / 1-pattern input tiler on `in_shape` (possibly with
     negative paving or fitting and a shifted origin): the affine task path."""
