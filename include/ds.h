@@ -222,6 +222,28 @@ DS_API int64_t ds_out_frame_bytes(const ds_handle* h);
 DS_API int ds_plane_dims(const ds_handle* h, int plane, int32_t* in_w, int32_t* in_h,
                          int32_t* out_w, int32_t* out_h);
 
+/* K-N1g comes in two variants with identical results.  The runtime-tap
+ * kernel (ds_general.cuh) reads the taps as data and runs any spec and
+ * alignment.  K-N1s (ds_spec.cuh) has the spec compiled in -- taps, pattern,
+ * paving, divisor, origin phase as constants, so zero taps, dead clamps and
+ * byte shifting vanish -- and needs an H paving that is a multiple of 4,
+ * taps in [-128, 127], every plane W % 16 == 0 (and W >= 64), a 16-byte
+ * aligned input and 4-byte aligned output rows.  Specs with a built-in
+ * instance (SPEC's downscaler, the halo reading of bench.py) use it
+ * directly; any other spec is compiled at ds_create with NVRTC when the
+ * runtime compiler is present.  AUTO (default) picks K-N1s whenever it can
+ * run a call. */
+enum { DS_GENERAL_AUTO = 0, DS_GENERAL_RUNTIME = 1, DS_GENERAL_COMPILED = 2 };
+
+/* Select the K-N1g variant.  Returns DS_OK, DS_EINVAL, or DS_EUNSUPPORTED
+ * when the handle has no such variant (COMPILED: geometry/spec outside
+ * K-N1s; RUNTIME: K-N1g cannot run the handle). */
+DS_API int ds_set_general_variant(ds_handle* h, int32_t variant);
+
+/* Variant used by the most recent ds_run when it ran a K-N1g kernel: 1
+ * runtime taps, 2 compiled taps; 0 if the last kernel was not K-N1g. */
+DS_API int ds_last_variant(const ds_handle* h);
+
 /* Force a kernel (DS_KERNEL_*).  DS_KERNEL_FUSED / DS_KERNEL_FUSED_GENERAL
  * on an ineligible geometry/spec returns DS_EUNSUPPORTED and leaves the
  * setting unchanged.  A forced fused kernel still yields to K-N2 when the
@@ -281,6 +303,10 @@ typedef struct {
     int32_t consumer_warps;      /* compute warps per CTA (plus one producer warp)     */
     int64_t units;               /* work units of the launch (K-N2: output bytes)      */
     int64_t unit_in_bytes_max;   /* bytes staged per unit                              */
+    int32_t variant;             /* K-N1g family: 1 runtime taps, 2 compiled taps
+                                    (built-in instance), 3 compiled taps (run-time
+                                    compiled); 0 otherwise                             */
+    int32_t reserved_;
 } ds_launch;
 
 /* Fill *out for `kernel` (DS_KERNEL_FUSED, DS_KERNEL_FUSED_GENERAL or

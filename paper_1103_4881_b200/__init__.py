@@ -20,6 +20,9 @@ from . import _build
 DS_OK, DS_EINVAL, DS_ESHAPE, DS_EUNSUPPORTED, DS_ECUDA, DS_ENOMEM = 0, -1, -2, -3, -4, -5
 DS_CHROMA_444, DS_CHROMA_420 = 0, 1
 DS_KERNEL_AUTO, DS_KERNEL_FUSED, DS_KERNEL_GENERIC, DS_KERNEL_FUSED_GENERAL = 0, 1, 2, 3
+DS_GENERAL_AUTO, DS_GENERAL_RUNTIME, DS_GENERAL_COMPILED = 0, 1, 2
+VARIANT_NAMES = {0: None, 1: "runtime taps (ds_general.cuh)", 2: "compiled taps, built-in (K-N1s, ds_spec.cuh)",
+                 3: "compiled taps, NVRTC (K-N1s, ds_spec.cuh)"}
 DS_MAX_PATTERN, DS_MAX_OUTPUTS, DS_MAX_PLANES = 16, 8, 3
 KERNEL_NAMES = {DS_KERNEL_AUTO: "none", DS_KERNEL_FUSED: "K-N1 fused band (TMA ring)",
                 DS_KERNEL_GENERIC: "K-N2 generic",
@@ -121,10 +124,12 @@ class ds_launch(C.Structure):
         ("consumer_warps", C.c_int32),
         ("units", C.c_int64),
         ("unit_in_bytes_max", C.c_int64),
+        ("variant", C.c_int32),
+        ("reserved_", C.c_int32),
     ]
 
     def as_dict(self):
-        return {k: getattr(self, k) for k, _ in self._fields_}
+        return {k: getattr(self, k) for k, _ in self._fields_ if k != "reserved_"}
 
 
 class ds_topology(C.Structure):
@@ -178,6 +183,8 @@ SIGNATURES = [
     ("ds_get_plan", C.c_int, [C.c_void_p, C.POINTER(ds_plan_info)]),
     ("ds_plane_dims", C.c_int, [C.c_void_p, C.c_int, _PI32, _PI32, _PI32, _PI32]),
     ("ds_set_kernel", C.c_int, [C.c_void_p, C.c_int32]),
+    ("ds_set_general_variant", C.c_int, [C.c_void_p, C.c_int32]),
+    ("ds_last_variant", C.c_int, [C.c_void_p]),
     ("ds_last_kernel", C.c_int, [C.c_void_p]),
     ("ds_set_tuning", C.c_int, [C.c_void_p, C.c_int32, C.c_int32]),
     ("ds_set_band_bytes", C.c_int, [C.c_void_p, C.c_int64]),
@@ -504,6 +511,15 @@ class Downscaler:
 
     def last_kernel(self) -> int:
         return lib().ds_last_kernel(self._h)
+
+    def set_general_variant(self, variant: int) -> None:
+        """K-N1g variant: DS_GENERAL_AUTO, _RUNTIME (taps as data) or _COMPILED (K-N1s)."""
+        rc = lib().ds_set_general_variant(self._h, variant)
+        if rc:
+            raise DSError(rc, "ds_set_general_variant")
+
+    def last_variant(self) -> int:
+        return lib().ds_last_variant(self._h)
 
     def set_tuning(self, stages: int, ctas_per_sm: int = 0) -> None:
         rc = lib().ds_set_tuning(self._h, stages, ctas_per_sm)

@@ -13,6 +13,7 @@
 #include "ds_internal.h"
 #include "ds_kernels.cuh"
 #include "ds_general.cuh"
+#include "ds_spec.cuh"
 
 namespace {
 thread_local int g_last_error = DS_OK;
@@ -729,12 +730,27 @@ bool ranges_overlap(const void* a, int64_t na, const void* b, int64_t nb) {
     return x < y + (uintptr_t)nb && y < x + (uintptr_t)na;
 }
 
+// K-N1g family: the compiled-spec instance (K-N1s) when the handle has one
+// and the call's pointers allow it, else the runtime-tap kernel
+bool use_spec(const ds_handle* h, const uint8_t* in, const uint8_t* out) {
+    return h->general_variant != 1 && spec_call_ok(h, in, out);
+}
+
 int run_device(ds_handle* h, const uint8_t* in, int64_t n, uint8_t* out, cudaStream_t st) {
     const int k = choose_kernel(h, in);
-    const int rc = (k == DS_KERNEL_FUSED)           ? launch_fused(h, in, n, out, st)
-                   : (k == DS_KERNEL_FUSED_GENERAL) ? launch_general(h, in, n, out, st)
-                                                    : launch_generic(h, in, n, out, st);
-    if (rc == DS_OK) h->last_kernel.store(k);
+    int rc, variant = 0;
+    if (k == DS_KERNEL_FUSED) {
+        rc = launch_fused(h, in, n, out, st);
+    } else if (k == DS_KERNEL_FUSED_GENERAL) {
+        variant = use_spec(h, in, out) ? 2 : 1;
+        rc = variant == 2 ? launch_spec(h, in, n, out, st) : launch_general(h, in, n, out, st);
+    } else {
+        rc = launch_generic(h, in, n, out, st);
+    }
+    if (rc == DS_OK) {
+        h->last_kernel.store(k);
+        h->last_variant.store(variant);
+    }
     return rc;
 }
 
@@ -835,6 +851,7 @@ DS_API ds_handle* ds_create(int32_t frame_w, int32_t frame_h, int32_t channels,
     h->plan = pi;
     int crc = configure_fused(h);
     if (!crc) crc = configure_general(h);
+    if (!crc) crc = configure_spec(h);
     if (crc) {
         delete h;
         g_last_error = crc;
@@ -1050,8 +1067,10 @@ static int replan(ds_handle* h, int64_t band_target, int64_t general_target) {
     h->plan = pi;
     h->band_target = band_target;
     h->general_target = general_target;
+    const SpecCfg old_spec = h->spec_cfg;
     rc = configure_fused(h);
     if (!rc) rc = configure_general(h);
+    if (!rc) rc = configure_spec(h);
     if (!rc && h->tune_stages > 0 && h->fused.valid) {
         FusedCfg c = h->fused;
         c.stages = h->tune_stages;
@@ -1068,6 +1087,7 @@ static int replan(ds_handle* h, int64_t band_target, int64_t general_target) {
         h->fused = old_fused;
         h->fine = old_fine;
         h->general = old_general;
+        h->spec_cfg = old_spec;
         h->band_target = old_band;
         h->general_target = old_gen;
     }
@@ -1101,12 +1121,27 @@ DS_API int64_t ds_units(const ds_handle* h, int64_t n, int32_t kernel) {
     if (!h || n < 0) return -1;
     if (kernel == DS_KERNEL_FUSED) return h->plan.fused_eligible ? n * pick_cfg(h, n).plan.units_per_frame : -1;
     if (kernel == DS_KERNEL_FUSED_GENERAL) {
+        if (h->general_variant != DS_GENERAL_RUNTIME && h->spec_cfg.valid) {
+            int32_t L[DS_MAX_PLANES], upf = 0;
+            spec_runs(h, n, L, &upf);
+            return n * upf;
+        }
         if (!h->general.valid) return -1;
         int32_t L[DS_MAX_PLANES];
         return n * general_runs(h, n, L);
     }
     return -1;
 }
+
+DS_API int ds_set_general_variant(ds_handle* h, int32_t variant) {
+    if (!h || variant < DS_GENERAL_AUTO || variant > DS_GENERAL_COMPILED) return DS_EINVAL;
+    if (variant == DS_GENERAL_COMPILED && !h->spec_cfg.valid) return DS_EUNSUPPORTED;
+    if (variant == DS_GENERAL_RUNTIME && !h->general.valid) return DS_EUNSUPPORTED;
+    h->general_variant = variant;
+    return DS_OK;
+}
+
+DS_API int ds_last_variant(const ds_handle* h) { return h ? h->last_variant.load() : DS_EINVAL; }
 
 DS_API int ds_launch_shape(const ds_handle* h, int64_t n, int32_t* grid, int32_t* block,
                            int32_t* smem) {
@@ -1140,9 +1175,25 @@ DS_API int ds_launch_info(const ds_handle* h, int64_t n, int32_t kernel, ds_laun
         out->unit_in_bytes_max = c.plan.unit_in_bytes_max;
         return DS_OK;
     }
+    if (kernel == DS_KERNEL_FUSED_GENERAL && h->general_variant != DS_GENERAL_RUNTIME && h->spec_cfg.valid) {
+        const SpecCfg& c = h->spec_cfg;
+        int32_t L[DS_MAX_PLANES], upf = 0;
+        spec_runs(h, n, L, &upf);
+        const int64_t units = n * upf;
+        out->grid = (int32_t)std::max<int64_t>(1, std::min<int64_t>(units, (int64_t)c.grid_per_sm * h->sm_count));
+        out->block = c.threads; out->smem_bytes = c.smem;
+        out->stages = c.stages;
+        out->ctas_per_sm = c.grid_per_sm;
+        out->consumer_warps = DS_SPEC_NW;
+        out->units = units;
+        out->unit_in_bytes_max = 0;             // no input staging: loads go to registers
+        out->variant = c.jit ? 3 : 2;
+        return DS_OK;
+    }
     if (kernel == DS_KERNEL_FUSED_GENERAL) {
         const GeneralCfg& c = h->general;
         if (!h->plan.fused_general_eligible || !c.valid) return DS_EUNSUPPORTED;
+        out->variant = 1;
         int32_t L[DS_MAX_PLANES];
         const int64_t units = n * general_runs(h, n, L);
         out->grid = (int32_t)std::max<int64_t>(1, std::min<int64_t>(units, (int64_t)c.grid_per_sm * h->sm_count));

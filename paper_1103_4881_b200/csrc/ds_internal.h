@@ -89,6 +89,20 @@ struct GeneralCfg {
     int grid_per_sm = 0, threads = 0, smem = 0;
 };
 
+// K-N1s (ds_spec.cu): the fused band kernel with the spec compiled in
+using SpecFn = void (*)(void);
+struct SpecPlaneCfg {
+    int32_t strips = 1, sw = 0, k = 0, nb = 0, R = 0, pitch = 0, mp = 0, unit_start = 0;
+};
+struct SpecCfg {
+    bool valid = false;
+    int jit = 0;                   // 0: built-in instance, 1: compiled at run time (NVRTC)
+    SpecFn fn = nullptr;           // kernel entry (runtime-API function, or a JIT CUfunction)
+    SpecPlaneCfg plane[DS_MAX_PLANES];
+    int32_t upf = 0, stages = 2, stage_stride = 0, mid_stride = 0;
+    int threads = 0, smem = 0, grid_per_sm = 0;
+};
+
 // K-N1: planes with W % 16 == 0 and rows shorter than this stage whole bands
 // (dead rows included) with one bulk copy per band instead of k + 1 copies of
 // 8 live rows: short rows make those copies small (CIF luma: 2.8 KB)
@@ -114,6 +128,8 @@ struct ds_handle {
     int64_t band_target = dsi::kUnitTargetBytes;
     dsi::FusedCfg fused, fine;
     dsi::GeneralCfg general;
+    dsi::SpecCfg spec_cfg;                  // K-N1s (compiled-spec K-N1g)
+    int32_t general_variant = 0;            // ds_set_general_variant: 0 auto, 1 runtime taps, 2 compiled taps
     int kernel_pref = DS_KERNEL_AUTO;
     int32_t run_bands = 0;                  // ds_set_run_bands (0 = automatic)
     int32_t tune_stages = 0, tune_ctas = 0; // explicit ds_set_tuning (0 stages = none)
@@ -121,6 +137,7 @@ struct ds_handle {
     int64_t general_target = 0;             // ds_set_general_stage_bytes (0 = default)
     uint32_t* debug_unit_count = nullptr;   // ds_set_debug_counter
     std::atomic<int> last_kernel{DS_KERNEL_AUTO};
+    std::atomic<int> last_variant{0};       // K-N1g family: 1 runtime taps, 2 compiled taps (K-N1s)
     std::atomic<uint64_t> peer_mask{0};     // ds_enable_peer: peer devices ds_run may store to
     // ds_run_host / ds_run_schedule state (lazily allocated, guarded by host_mu)
     std::mutex host_mu;
@@ -142,6 +159,11 @@ bool out_ptr_ok(const ds_handle* h, const void* p);
 bool ranges_overlap(const void* a, int64_t na, const void* b, int64_t nb);
 int run_device(ds_handle* h, const uint8_t* in, int64_t n, uint8_t* out, cudaStream_t st);
 void free_sched_state(ds_handle* h);
+int configure_spec(ds_handle* h);
+bool spec_call_ok(const ds_handle* h, const uint8_t* in, const uint8_t* out);
+int launch_spec(ds_handle* h, const uint8_t* in, int64_t n, uint8_t* out, cudaStream_t st);
+SpecFn spec_jit_kernel(ds_handle* h, int phase);
+void spec_runs(const ds_handle* h, int64_t n, int32_t* L, int32_t* upf);
 int make_plan(int32_t W, int32_t H, int32_t channels, const ds_filter_spec* spec_in,
               ds_filter_spec* spec_out, ds_plan_info* info, int64_t unit_target = kUnitTargetBytes,
               int64_t general_target = 0);

@@ -1,0 +1,282 @@
+// ds_spec.cu -- host side of K-N1s (ds_spec.cuh): the fused band kernel with
+// the filter spec compiled in.  Planning (strips, bands, strides), the
+// built-in instances, eligibility and the launch.  Any spec without a
+// built-in instance is compiled at run time (ds_spec_jit.cu).
+// Citations: P:n = PAPER.md line n, S:n = SPEC.md line n, SURVEY sec. n.
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "ds.h"
+#include "ds_internal.h"
+#include "ds_spec.cuh"
+#include "ds_spec_builtin.cuh"
+
+namespace dsi {
+
+namespace {
+
+bool stage_is(const ds_stage_spec& s, int P, int S, int Q, int D, int B, int O, int (*w)(int, int)) {
+    if (s.pattern != P || s.paving != S || s.outputs != Q || s.divisor != D || s.bias != B || s.origin != O)
+        return false;
+    for (int j = 0; j < DS_MAX_OUTPUTS; ++j)
+        for (int i = 0; i < DS_MAX_PATTERN; ++i)
+            if (s.weight[j][i] != ((j < Q && i < P) ? w(j, i) : 0)) return false;
+    return true;
+}
+template <class ST>
+int wfn(int j, int i) { return ST::w(j, i); }
+template <class ST>
+bool stage_is(const ds_stage_spec& s) {
+    return stage_is(s, ST::P, ST::S, ST::Q, ST::D, ST::B, ST::O, &wfn<ST>);
+}
+
+// words of an H chunk window (the HChunk<> constants, from the runtime spec)
+int h_blocks(const ds_stage_spec& h, int ph) {
+    int hi = 0;
+    for (int j = 0; j < h.outputs; ++j)
+        for (int i = 0; i < h.pattern; ++i)
+            if (h.weight[j][i] != 0) hi = std::max(hi, i);
+    return ((ph + 3 * h.paving + hi) / 4 + 1 + 3) / 4;
+}
+
+}  // namespace
+
+// Built-in instances: (stage types, window phase) -> kernel.  The phase of a
+// spec is its H origin mod 16 (every eligible plane has W % 16 == 0).
+SpecFn spec_builtin(const ds_filter_spec& sp) {
+    if (stage_is<dss::HaloH>(sp.h) && stage_is<dss::HaloV>(sp.v))
+        return reinterpret_cast<SpecFn>(&dss::ds_spec_kernel<dss::HaloH, dss::HaloV, (dss::HaloH::O % 16 + 16) % 16>);
+    if (stage_is<dss::SpecH>(sp.h) && stage_is<dss::SpecV>(sp.v))
+        return reinterpret_cast<SpecFn>(&dss::ds_spec_kernel<dss::SpecH, dss::SpecV, (dss::SpecH::O % 16 + 16) % 16>);
+    return nullptr;
+}
+
+// Geometry K-N1s can run, independent of pointers: H paving a multiple of 4
+// (a chunk of 4 repetitions starts on a 16-byte block), taps in s8 (dp4a),
+// every plane W % 16 == 0 (one window phase for all planes and strips, rows
+// TMA-copyable), at most DS_SPEC_MAXP planes.
+bool spec_geometry_ok(const ds_filter_spec& sp, const ds_plan_info& pi) {
+    if (sp.h.paving % 4 != 0 || pi.n_planes > DS_SPEC_MAXP) return false;
+    for (const ds_stage_spec* s : {&sp.h, &sp.v})
+        for (int j = 0; j < s->outputs; ++j)
+            for (int i = 0; i < s->pattern; ++i)
+                if (s->weight[j][i] < -128 || s->weight[j][i] > 127) return false;
+    if (sp.h.pattern > 16 || sp.v.pattern > 16) return false;
+    const int ph = (int)(((int64_t)sp.h.origin % 16 + 16) % 16);
+    const int kblk = h_blocks(sp.h, ph);
+    for (int p = 0; p < pi.n_planes; ++p) {
+        if (pi.in_w[p] % 16 != 0 || pi.in_w[p] < 64 || pi.in_w[p] / 16 < 2 * kblk || pi.in_offset[p] % 16 != 0)
+            return false;
+        // at most 4 chunks per row may cross the row end (the wrap pass's table)
+        const int W = pi.in_w[p], nb16 = W / 16, np = W / sp.h.paving, nch = (np + 3) / 4;
+        const int oh = (int)(((int64_t)sp.h.origin % W + W) % W), blk0 = oh / 16;
+        int nwc = 0;
+        for (int c = 0; c < nch; ++c) {
+            int Bc = blk0 + (sp.h.paving / 4) * c;
+            if (Bc >= nb16) Bc -= nb16;
+            nwc += Bc + kblk > nb16;
+        }
+        if (nwc > 4) return false;
+    }
+    return pi.in_frame_bytes % 16 == 0;
+}
+
+// Per-plane plan: bands of k V repetitions (the first band of a run stages
+// R = Sv (k - 1) + Pv rows, later bands Sv k new rows, the V halo's rows
+// carried over in the intermediate).  Scored per useful input row by the
+// rounds of the H pass (8 warps over rows x 32-chunk segments), the V pass
+// (256 threads over k x column quads) and a per-band barrier, under the
+// shared-memory budget (two intermediate buffers) of 3 CTAs per SM.
+bool spec_plane_plan(const ds_filter_spec& sp, int32_t W, int32_t H, int64_t budget, SpecPlaneCfg* out) {
+    const int Sh = sp.h.paving, Qh = sp.h.outputs;
+    const int Sv = sp.v.paving, Pv = sp.v.pattern;
+    const int np = W / Sh, G = H / Sv;
+    const int nch = (np + 3) / 4, segs = (nch + 31) / 32;
+    if (DS_SPEC_NW % segs != 0) return false;          // a warp keeps one row segment (segs | NW)
+    const int64_t nq = ((int64_t)Qh * np + 3) / 4;
+    const int64_t mp = round_up(std::max<int64_t>(4LL * Qh * nch, 4 * nq), 16);
+    const int ovl = std::max(0, Pv - Sv);
+    double best = 1e300;
+    bool found = false;
+    for (int k = 1; k <= G; ++k) {
+        if (G % k) continue;
+        const int64_t R = (int64_t)Sv * (k - 1) + Pv;
+        if (2 * R * mp > budget) continue;
+        const int64_t newrows = std::max<int64_t>(1, R - ovl);
+        const double hr = (double)((newrows * segs + DS_SPEC_NW - 1) / DS_SPEC_NW);
+        const double vr = (double)((k * nq + DS_SPEC_NW * 32 - 1) / (DS_SPEC_NW * 32));
+        const double cost = (90.0 * hr + 120.0 * vr + 150.0) / ((double)Sv * k);
+        if (cost < best * 0.999) {
+            best = cost;
+            found = true;
+            out->k = k; out->nb = G / k; out->R = (int32_t)R; out->mp = (int32_t)mp;
+            out->strips = 1; out->sw = np; out->pitch = 0;
+        }
+    }
+    return found;
+}
+
+// Configure K-N1s for the handle (h->spec_cfg.valid = false when it cannot
+// run the geometry/spec, which is not an error).
+int configure_spec(ds_handle* h) {
+    SpecCfg c;
+    const ds_plan_info& pi = h->plan;
+    const ds_filter_spec& sp = h->spec;
+    h->spec_cfg = c;
+    if (!spec_geometry_ok(sp, pi)) return DS_OK;
+    const int ph = (int)(((int64_t)sp.h.origin % 16 + 16) % 16);
+    SpecFn fn = spec_builtin(sp);
+    c.jit = 0;
+    if (!fn) {
+        fn = spec_jit_kernel(h, ph);                                   // nullptr when JIT is unavailable
+        c.jit = 1;
+    }
+    if (!fn) return DS_OK;
+#ifndef DS_SPEC_BUDGET
+#define DS_SPEC_BUDGET (54 * 1024)
+#endif
+    const int64_t budget = DS_SPEC_BUDGET;             // two intermediate buffers; 4 CTAs per SM
+    int64_t mmax = 0;
+    for (int p = 0; p < pi.n_planes; ++p) {
+        if (!spec_plane_plan(sp, pi.in_w[p], pi.in_h[p], budget, &c.plane[p])) return DS_OK;
+        mmax = std::max<int64_t>(mmax, (int64_t)c.plane[p].R * c.plane[p].mp);
+    }
+    c.stages = 0;
+    c.stage_stride = 0;
+    c.mid_stride = (int32_t)round_up(mmax, 128);
+    c.threads = DS_SPEC_NW * 32;
+    c.smem = 2 * c.mid_stride;
+    DeviceGuard g(h->device);
+    if (cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             c.smem) != cudaSuccess) {
+        cudaGetLastError();
+        return DS_OK;
+    }
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, reinterpret_cast<const void*>(fn), c.threads, c.smem) !=
+            cudaSuccess ||
+        occ < 1) {
+        cudaGetLastError();
+        return DS_OK;
+    }
+    c.grid_per_sm = std::min(occ, 4);
+    c.fn = fn;
+    c.valid = true;
+    h->spec_cfg = c;
+    return DS_OK;
+}
+
+// Runs of bands for a launch over n frames (units per frame into *upf, run
+// lengths into L): runs shrink, split evenly within each plane, until the
+// launch has >= 12 units per CTA slot (the persistent schedule's tail and the
+// luma/chroma work imbalance stay small); longer runs re-stage fewer halo rows.
+void spec_runs(const ds_handle* h, int64_t n, int32_t* L, int32_t* upf) {
+    const SpecCfg& c = h->spec_cfg;
+    const ds_plan_info& pi = h->plan;
+    const ds_filter_spec& sp = h->spec;
+    if (h->run_bands > 0) {                       // ds_set_run_bands forces the run length
+        int32_t u = 0;
+        for (int p = 0; p < pi.n_planes; ++p) {
+            L[p] = std::min<int32_t>(h->run_bands, c.plane[p].nb);
+            u += (c.plane[p].nb + L[p] - 1) / L[p];
+        }
+        *upf = u;
+        return;
+    }
+    // equal work per unit across planes: a band of plane p covers Sv k_p rows of
+    // W_p bytes; runs are sized so the launch has ~6 units per CTA slot (longer
+    // runs re-stage fewer halo rows, more units balance the persistent schedule)
+    const int64_t slots = std::max<int64_t>(1, (int64_t)c.grid_per_sm * h->sm_count);
+    double frame_work = 0;
+    for (int p = 0; p < pi.n_planes; ++p) frame_work += (double)pi.in_w[p] * pi.in_h[p];
+    const double want_units = std::max<double>(1.0, 6.0 * slots / std::max<int64_t>(n, 1));
+    const double target = frame_work / want_units;                  // bytes of input per unit
+    int32_t u = 0;
+    for (int p = 0; p < pi.n_planes; ++p) {
+        const double band_work = (double)sp.v.paving * c.plane[p].k * pi.in_w[p];
+        const int32_t nb = c.plane[p].nb;
+        int32_t l = (int32_t)std::max<double>(1.0, std::floor(target / band_work + 0.5));
+        l = std::min(l, nb);
+        const int32_t runs = (nb + l - 1) / l;
+        L[p] = (nb + runs - 1) / runs;                                // even runs within the plane
+        u += (nb + L[p] - 1) / L[p];
+    }
+    *upf = u;
+}
+
+// Pointer conditions of one call: TMA needs a 16-byte aligned input.
+bool spec_call_ok(const ds_handle* h, const uint8_t* in, const uint8_t* out) {
+    if (!h->spec_cfg.valid) return false;
+    const ds_plan_info& pi = h->plan;
+    (void)out;   // any output alignment: rows take 4-, 2- or 1-byte stores by their alignment
+    return (reinterpret_cast<uintptr_t>(in) & 15) == 0 && pi.in_frame_bytes % 16 == 0;
+}
+
+int launch_spec(ds_handle* h, const uint8_t* in, int64_t n, uint8_t* out, cudaStream_t st) {
+    const SpecCfg& c = h->spec_cfg;
+    const ds_plan_info& pi = h->plan;
+    const ds_filter_spec& sp = h->spec;
+    dss::SpecParams p;
+    std::memset(&p, 0, sizeof p);
+    p.in = in; p.out = out;
+    p.unit_count = h->debug_unit_count;
+    p.in_frame = pi.in_frame_bytes; p.out_frame = pi.out_frame_bytes;
+    int32_t L[DS_MAX_PLANES] = {1, 1, 1}, upf = 0;
+    spec_runs(h, n, L, &upf);
+    p.upf = upf;
+    p.n_units = n * upf;
+    p.n_planes = pi.n_planes;
+    p.mid_stride = c.mid_stride;
+    p.ovl = std::max(0, sp.v.pattern - sp.v.paving);
+    auto rcp = [](int32_t d) { return d > 1 ? (uint32_t)((0x100000000ULL + d - 1) / (uint64_t)d) : 0u; };
+    int32_t start = 0;
+    for (int q = 0; q < pi.n_planes; ++q) {
+        const SpecPlaneCfg& g = c.plane[q];
+        dss::SpecPlane& P = p.pl[q];
+        P.in_off = pi.in_offset[q];
+        P.out_off = pi.out_offset[q];
+        P.W = pi.in_w[q];
+        P.H = pi.in_h[q];
+        P.Wout = pi.out_w[q];
+        P.oh = (int32_t)(((int64_t)sp.h.origin % P.W + P.W) % P.W);
+        P.ov = (int32_t)(((int64_t)sp.v.origin % P.H + P.H) % P.H);
+        P.np = P.W / sp.h.paving;
+        P.nch = (P.np + 3) / 4;
+        P.segs = (P.nch + 31) / 32;
+        P.lgsegs = 0;
+        while ((1 << P.lgsegs) < P.segs) ++P.lgsegs;
+        P.nb16 = P.W / 16;
+        P.blk0 = P.oh / 16;
+        // chunks whose kBlk-block window crosses the row end
+        const int kblk = h_blocks(sp.h, (int)(((int64_t)sp.h.origin % 16 + 16) % 16));
+        P.nwc = 0;
+        for (int c = 0; c < P.nch; ++c) {
+            int Bc = P.blk0 + (sp.h.paving / 4) * c;
+            if (Bc >= P.nb16) Bc -= P.nb16;
+            if (Bc + kblk > P.nb16) {
+                if (P.nwc == 4) return DS_EUNSUPPORTED;         // configure_spec rules this out
+                P.wch[P.nwc++] = c;
+            }
+        }
+        P.k = g.k;
+        P.nb = g.nb;
+        P.L = L[q];
+        P.nq = (sp.h.outputs * P.np + 3) / 4;
+        P.nq_rcp = rcp(P.nq);
+        P.mp = g.mp;
+        P.unit_start = start;
+        start += (P.nb + P.L - 1) / P.L;
+    }
+    if (p.n_units == 0) return DS_OK;
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(p.n_units, (int64_t)c.grid_per_sm * h->sm_count));
+    void* args[] = {&p};
+    if (cudaLaunchKernel(reinterpret_cast<const void*>(c.fn), dim3((unsigned)grid), dim3(c.threads), args,
+                         (size_t)c.smem, st) != cudaSuccess) {
+        cudaGetLastError();
+        return DS_ECUDA;
+    }
+    return DS_OK;
+}
+
+}  // namespace dsi

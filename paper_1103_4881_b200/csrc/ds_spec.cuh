@@ -1,0 +1,568 @@
+// ds_spec.cuh -- K-N1s: the fused band kernel with the filter spec compiled in
+// (any separable Array-OL stage spec at HBM speed).
+//
+// Same job as K-N1g (ds_general.cuh): per (frame, plane, run of bands) an
+// Array-OL horizontal task then a vertical task with the
+// u8 intermediate in shared memory, for any stage spec -- halos
+// P > S with toroidal wrap, origins, any taps -- but the spec is a
+// compile-time type: taps, pattern/paving/outputs, divisor and the byte phase
+// of the H windows are constants, so
+//   * the H pass runs one dp4a per (output, aligned input word) whose
+//     re-indexed weight word is nonzero -- no byte shifting, no zero taps
+//     (the halo spec: 2 dp4a per output where the runtime-tap kernel needs 4);
+//   * the V pass loads only the intermediate rows some tap reads, transposes
+//     only 4-row blocks with >= 3 live rows, pairs 2-row blocks and folds
+//     1-row blocks into shifted-weight dp4a;
+//   * division is one multiply-high (or a shift), and clamps the spec proves
+//     dead are not emitted.
+// Data movement: the H pass loads its input straight from HBM into registers
+// (coalesced 16-byte loads; a lane takes 4 consecutive H repetitions, and the
+// window bytes its neighbour already fetched come from L1), so the input never
+// passes through shared memory and there is no copy engine to feed: one copy
+// instruction per row was the limit of the TMA-staged design (1-D bulk copies
+// cannot stage a row and its wrap-around window at once, and at ~2 copies per
+// row their issue rate, not HBM, bounded K-N1g).  The intermediate is the only
+// shared-memory array (two buffers; a band's V halo rows are carried over
+// from the previous band of the run), and V outputs go from registers to HBM
+// as coalesced stores.  No mbarriers, no producer warp: one CTA barrier per
+// band.
+//
+// This header is self-contained device code: it compiles under nvcc (the
+// built-in instances, ds_spec.cu) and under NVRTC (any other spec, compiled
+// at run time from this same source with a generated stage type).
+#pragma once
+
+#ifdef __CUDACC_RTC__
+typedef unsigned char uint8_t;
+typedef unsigned short uint16_t;
+typedef unsigned int uint32_t;
+typedef int int32_t;
+typedef long long int64_t;
+typedef unsigned long long uint64_t;
+typedef unsigned long long uintptr_t;
+#else
+#include <cstdint>
+#endif
+
+#ifndef DS_SPEC_NW
+#define DS_SPEC_NW 8                  // warps per CTA
+#endif
+#ifndef DS_SPEC_MINB
+#define DS_SPEC_MINB 4                // CTAs per SM the register budget is sized for
+#endif
+#ifndef DS_SPEC_MAXP
+#define DS_SPEC_MAXP 3
+#endif
+
+namespace dss {
+
+// ---------------------------------------------------------------- params --
+struct SpecPlane {
+    int64_t in_off, out_off;   // plane offsets inside one frame
+    int32_t W, H, Wout;        // input row bytes, rows, output row bytes
+    int32_t oh, ov;            // H / V origins reduced mod W / H (>= 0)
+    int32_t np;                // H repetitions per row (W / Sh)
+    int32_t nch;               // chunks of 4 repetitions per row: ceil(np / 4)
+    int32_t segs, lgsegs;      // 32-chunk warp segments per row: ceil(nch / 32), a power of two; log2
+    int32_t nwc, wch[4];       // chunks whose window crosses the row end (wrap pass)
+    int32_t nb16, blk0;        // W / 16; oh / 16 (first window block of repetition 0)
+    int32_t k, nb;             // V repetitions per band, bands per plane ((H / Sv) / k)
+    int32_t L;                 // bands per run (a unit); the V halo's mid rows carry over
+    int32_t nq;                // intermediate column quads: ceil(Qh np / 4)
+    uint32_t nq_rcp;           // ceil(2^32 / nq) (nq > 1)
+    int32_t mp;                // intermediate row stride (>= 4 Qh nch)
+    int32_t unit_start;        // first unit of the plane within a frame
+};
+
+struct SpecParams {
+    const uint8_t* in;
+    uint8_t* out;
+    uint32_t* unit_count;      // debug: +1 per unit processed, else null
+    int64_t in_frame, out_frame, n_units;
+    int32_t upf, n_planes, mid_stride, ovl;   // ovl = max(Pv - Sv, 0): rows a band shares with the next
+    SpecPlane pl[DS_SPEC_MAXP];
+};
+
+// --------------------------------------------------- compile-time helpers --
+template <int V>
+struct IC {
+    static constexpr int value = V;
+};
+template <int I, int N, class F>
+__device__ __forceinline__ void sfor(F&& f) {
+    if constexpr (I < N) {
+        f(IC<I>{});
+        sfor<I + 1, N>(f);
+    }
+}
+
+// A stage type ST provides: P, S, Q, D, B (bias), O (origin) as static
+// constexpr ints and  static constexpr int w(int j, int i)  (0 outside the
+// taps).  Derived constants:
+template <class ST>
+struct StageInfo {
+    // accumulator range over all windows: bias + 255 * (sum of positive / negative taps)
+    __host__ __device__ static constexpr int64_t acc_max() {
+        int64_t m = -(int64_t(1) << 62);
+        for (int j = 0; j < ST::Q; ++j) {
+            int64_t s = ST::B;
+            for (int i = 0; i < ST::P; ++i) s += ST::w(j, i) > 0 ? 255 * ST::w(j, i) : 0;
+            m = s > m ? s : m;
+        }
+        return m;
+    }
+    __host__ __device__ static constexpr int64_t acc_min() {
+        int64_t m = int64_t(1) << 62;
+        for (int j = 0; j < ST::Q; ++j) {
+            int64_t s = ST::B;
+            for (int i = 0; i < ST::P; ++i) s += ST::w(j, i) < 0 ? 255 * ST::w(j, i) : 0;
+            m = s < m ? s : m;
+        }
+        return m;
+    }
+    __host__ __device__ static constexpr int hi_tap() {   // last tap index with a nonzero weight (any output)
+        int h = 0;
+        for (int j = 0; j < ST::Q; ++j)
+            for (int i = 0; i < ST::P; ++i)
+                if (ST::w(j, i) != 0 && i > h) h = i;
+        return h;
+    }
+    __host__ __device__ static constexpr bool live(int i) {   // some output reads tap i
+        for (int j = 0; j < ST::Q; ++j)
+            if (ST::w(j, i) != 0) return true;
+        return false;
+    }
+    // s8-packed weights of output j on the aligned word b when the pattern
+    // starts at byte `off` of the word grid: byte t <-> tap 4b + t - off
+    __host__ __device__ static constexpr uint32_t wword(int j, int b, int off) {
+        uint32_t r = 0;
+        for (int t = 0; t < 4; ++t) {
+            const int i = 4 * b + t - off;
+            if (i >= 0 && i < ST::P) r |= (uint32_t)(uint8_t)(int8_t)ST::w(j, i) << (8 * t);
+        }
+        return r;
+    }
+    // M = ceil(2^32 / D): floor(a / D) = umulhi(a, M) for 0 <= a <= acc_max iff acc_max * e < 2^32
+    __host__ __device__ static constexpr uint64_t M() { return ((uint64_t(1) << 32) + ST::D - 1) / ST::D; }
+    __host__ __device__ static constexpr bool fastdiv() {
+        return ST::D > 1 && acc_max() < 0x7fffffff &&
+               (uint64_t)acc_max() * (M() * ST::D - (uint64_t(1) << 32)) < (uint64_t(1) << 32);
+    }
+};
+
+__host__ __device__ constexpr int log2i(int d) { return d <= 1 ? 0 : 1 + log2i(d >> 1); }
+
+// clamp_0^255(trunc(acc / D)) (round-half-up bias, truncating
+// division, clamp) with everything the spec proves dead removed
+template <class ST>
+__device__ __forceinline__ uint32_t qdiv(int32_t acc) {
+    using I = StageInfo<ST>;
+    constexpr int64_t amax = I::acc_max(), amin = I::acc_min();
+    // a non-positive accumulator truncates to a non-positive quotient -> 0
+    const uint32_t a = amin >= 0 ? (uint32_t)acc : (uint32_t)max(acc, 0);
+    uint32_t q;
+    if constexpr (ST::D == 1) {
+        q = a;
+    } else if constexpr ((ST::D & (ST::D - 1)) == 0) {
+        q = a >> log2i(ST::D);
+    } else if constexpr (I::fastdiv()) {
+        q = __umulhi(a, (uint32_t)I::M());
+    } else {
+        q = a / (uint32_t)ST::D;
+    }
+    if constexpr (amax / ST::D > 255) q = min(q, 255u);
+    return q;
+}
+
+__device__ __forceinline__ int32_t dp4a_us(uint32_t a, uint32_t b, int32_t c) {
+    int32_t d;
+    asm("dp4a.u32.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+
+// ------------------------------------------------------------ PTX helpers --
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    uint32_t r;
+    asm("{ .reg .u64 t; cvta.to.shared.u64 t, %1; cvt.u32.u64 %0, t; }" : "=r"(r) : "l"(p));
+    return r;
+}
+__device__ __forceinline__ uint32_t lds32(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sts32(uint32_t a, uint32_t v) {
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+// L2 prefetch of a contiguous range (TMA engine; no shared memory, no wait)
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void ldg128(const uint8_t* p, uint32_t& x, uint32_t& y, uint32_t& z, uint32_t& w) {
+    asm volatile("ld.global.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(x), "=r"(y), "=r"(z), "=r"(w) : "l"(p));
+}
+__device__ __forceinline__ void ldg64(const uint8_t* p, uint32_t& x, uint32_t& y) {
+    asm volatile("ld.global.v2.u32 {%0,%1}, [%2];" : "=r"(x), "=r"(y) : "l"(p));
+}
+__device__ __forceinline__ uint32_t ldg32(const uint8_t* p) {
+    uint32_t v;
+    asm volatile("ld.global.u32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+// streaming global stores (the output is never re-read)
+__device__ __forceinline__ void stg32_cs(uint8_t* p, uint32_t v) {
+    asm volatile("st.global.cs.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void stg16(uint8_t* p, uint32_t v) {
+    asm volatile("st.global.cs.u16 [%0], %1;" ::"l"(p), "h"((unsigned short)v) : "memory");
+}
+__device__ __forceinline__ void stg8(uint8_t* p, uint32_t v) {
+    asm volatile("st.global.cs.u8 [%0], %1;" ::"l"(p), "h"((unsigned short)(v & 0xff)) : "memory");
+}
+
+// ------------------------------------------------------------- the H pass --
+// One lane: a chunk = 4 consecutive H repetitions r1 = 4c .. 4c+3 of one row.
+// Their windows start at bytes oh + Sh r1; relative to the chunk's first
+// 16-byte block B = blk0 + (Sh / 4) c that is PH + Sh m (PH = oh mod 16, a
+// compile-time constant of the instance).  The lane loads exactly the words
+// any live tap reads (16-, 8- or 4-byte loads by word runs), then every output
+// is a dp4a per aligned word with a nonzero re-indexed weight word.
+template <class HS, int PH>
+struct HChunk {
+    using I = StageInfo<HS>;
+    static constexpr int kLo = PH / 4;                                   // first word read
+    static constexpr int kHi = (PH + 3 * HS::S + I::hi_tap()) / 4;       // last word read
+    static constexpr int kWords = kHi + 1;                               // words from B's start
+    static constexpr int kBlk = (kWords + 3) / 4;                        // 16-byte blocks touched
+    static_assert(kBlk <= 8, "H window too wide for the compiled H pass");
+
+    // x: words kLo .. kHi of the window (others untouched), from the chunk's
+    // blocks B .. B + kBlk - 1 of the row (B < nb16).  WRAP: the window
+    // crosses the row end, so block indices wrap mod nb16.
+    template <bool WRAP>
+    __device__ __forceinline__ static void load(const uint8_t* row, int B, int nb16, uint32_t (&x)[4 * kBlk]) {
+        const uint8_t* base = row + 16 * B;
+        sfor<0, kBlk>([&](auto b) {
+            constexpr int w0 = 4 * b.value, wlo = w0 > kLo ? w0 : kLo, whi = w0 + 3 < kHi ? w0 + 3 : kHi;
+            const uint8_t* a = base + 16 * b.value;
+            if constexpr (WRAP) {
+                int blk = B + b.value;
+                if (blk >= nb16) blk -= nb16;
+                a = row + 16 * blk;
+            }
+            if constexpr (wlo == w0 && whi == w0 + 3) {
+                ldg128(a, x[w0], x[w0 + 1], x[w0 + 2], x[w0 + 3]);
+            } else if constexpr (whi >= wlo) {
+                sfor<wlo - w0, whi - w0 + 1>([&](auto t) {
+                    constexpr int w = w0 + t.value;
+                    if constexpr ((w & 1) == 0 && w + 1 <= whi) ldg64(a + 4 * t.value, x[w], x[w + 1]);
+                    else if constexpr ((w & 1) == 1 && w - 1 >= wlo) { /* loaded with w - 1 */ }
+                    else x[w] = ldg32(a + 4 * t.value);
+                });
+            }
+        });
+    }
+    // the same words from a base pointer to the chunk's first block (no wrap)
+    __device__ __forceinline__ static void load_at(const uint8_t* base, uint32_t (&x)[4 * kBlk]) {
+        sfor<0, kBlk>([&](auto b) {
+            constexpr int w0 = 4 * b.value, wlo = w0 > kLo ? w0 : kLo, whi = w0 + 3 < kHi ? w0 + 3 : kHi;
+            const uint8_t* a = base + 16 * b.value;
+            if constexpr (wlo == w0 && whi == w0 + 3) {
+                ldg128(a, x[w0], x[w0 + 1], x[w0 + 2], x[w0 + 3]);
+            } else if constexpr (whi >= wlo) {
+                sfor<wlo - w0, whi - w0 + 1>([&](auto t) {
+                    constexpr int w = w0 + t.value;
+                    if constexpr ((w & 1) == 0 && w + 1 <= whi) ldg64(a + 4 * t.value, x[w], x[w + 1]);
+                    else if constexpr ((w & 1) == 1 && w - 1 >= wlo) { /* loaded with w - 1 */ }
+                    else x[w] = ldg32(a + 4 * t.value);
+                });
+            }
+        });
+    }
+    // the chunk's 4 Q output bytes, packed little-endian into Q words
+    __device__ __forceinline__ static void compute(const uint32_t (&x)[4 * kBlk], uint32_t (&o)[HS::Q]) {
+        uint32_t q[4 * HS::Q];
+        sfor<0, 4>([&](auto m) {
+            sfor<0, HS::Q>([&](auto j) {
+                int32_t acc = HS::B;
+                sfor<kLo, kHi + 1>([&](auto b) {
+                    constexpr uint32_t wq = I::wword(j.value, b.value, PH + HS::S * m.value);
+                    if constexpr (wq != 0) acc = dp4a_us(x[b.value], wq, acc);
+                });
+                q[HS::Q * m.value + j.value] = qdiv<HS>(acc);
+            });
+        });
+        sfor<0, HS::Q>([&](auto w) {
+            const uint32_t lo = __byte_perm(q[4 * w.value], q[4 * w.value + 1], 0x0040);
+            const uint32_t hi = __byte_perm(q[4 * w.value + 2], q[4 * w.value + 3], 0x0040);
+            o[w.value] = __byte_perm(lo, hi, 0x5410);
+        });
+    }
+};
+
+// ------------------------------------------------------------- the V pass --
+// One lane: V repetition g, 4 intermediate columns (one word per row).  Rows
+// no tap reads are not loaded; 4-row blocks with >= 3 live rows are
+// transposed into column words (8 PRMT), 2 live rows paired (4 PRMT), a
+// single live row folded into shifted-weight dp4a (no PRMT).
+template <class VS>
+struct VQuad {
+    using I = StageInfo<VS>;
+    static constexpr int kBlocks = (I::hi_tap() + 4) / 4;
+    __host__ __device__ static constexpr int live_in_block(int b) {
+        int n = 0;
+        for (int t = 0; t < 4; ++t)
+            if (4 * b + t < VS::P && I::live(4 * b + t)) ++n;
+        return n;
+    }
+    __host__ __device__ static constexpr int nth_live(int b, int k) {   // row (within the block) of the k-th live row
+        for (int t = 0; t < 4; ++t)
+            if (4 * b + t < VS::P && I::live(4 * b + t)) {
+                if (k == 0) return t;
+                --k;
+            }
+        return 0;
+    }
+
+    // mb: shared address of row 0 of the repetition at this lane's 4 columns
+    __device__ __forceinline__ static void run(uint32_t mb, int mp, int32_t (&acc)[VS::Q][4]) {
+        sfor<0, VS::Q>([&](auto kk) {
+            sfor<0, 4>([&](auto e) { acc[kk.value][e.value] = VS::B; });
+        });
+        sfor<0, kBlocks>([&](auto b) {
+            constexpr int nl = live_in_block(b.value);
+            if constexpr (nl == 1) {
+                constexpr int t = nth_live(b.value, 0), i = 4 * b.value + t;
+                const uint32_t r = lds32(mb + i * mp);
+                sfor<0, VS::Q>([&](auto kk) {
+                    constexpr int wv = VS::w(kk.value, i);
+                    if constexpr (wv != 0) {
+                        sfor<0, 4>([&](auto e) {
+                            constexpr uint32_t ws = (uint32_t)(uint8_t)(int8_t)wv << (8 * e.value);
+                            acc[kk.value][e.value] = dp4a_us(r, ws, acc[kk.value][e.value]);
+                        });
+                    }
+                });
+            } else if constexpr (nl == 2) {
+                constexpr int t0 = nth_live(b.value, 0), t1 = nth_live(b.value, 1);
+                const uint32_t r0 = lds32(mb + (4 * b.value + t0) * mp), r1 = lds32(mb + (4 * b.value + t1) * mp);
+                uint32_t c[4];
+                sfor<0, 4>([&](auto e) { c[e.value] = __byte_perm(r0, r1, e.value | ((4 + e.value) << 4)); });
+                sfor<0, VS::Q>([&](auto kk) {
+                    constexpr uint32_t wq = (uint32_t)(uint8_t)(int8_t)VS::w(kk.value, 4 * b.value + t0) |
+                                            ((uint32_t)(uint8_t)(int8_t)VS::w(kk.value, 4 * b.value + t1) << 8);
+                    if constexpr (wq != 0) {
+                        sfor<0, 4>([&](auto e) { acc[kk.value][e.value] = dp4a_us(c[e.value], wq, acc[kk.value][e.value]); });
+                    }
+                });
+            } else if constexpr (nl >= 3) {
+                uint32_t r[4];
+                sfor<0, 4>([&](auto t) {
+                    constexpr int i = 4 * b.value + t.value;
+                    if constexpr (i < VS::P && I::live(i)) r[t.value] = lds32(mb + i * mp);
+                    else r[t.value] = 0;
+                });
+                const uint32_t ta = __byte_perm(r[0], r[1], 0x5140), tb = __byte_perm(r[2], r[3], 0x5140);
+                const uint32_t tc = __byte_perm(r[0], r[1], 0x7362), td = __byte_perm(r[2], r[3], 0x7362);
+                const uint32_t c[4] = {__byte_perm(ta, tb, 0x5410), __byte_perm(ta, tb, 0x7632),
+                                       __byte_perm(tc, td, 0x5410), __byte_perm(tc, td, 0x7632)};
+                sfor<0, VS::Q>([&](auto kk) {
+                    constexpr uint32_t wq = I::wword(kk.value, b.value, 0);
+                    if constexpr (wq != 0) {
+                        sfor<0, 4>([&](auto e) { acc[kk.value][e.value] = dp4a_us(c[e.value], wq, acc[kk.value][e.value]); });
+                    }
+                });
+            }
+        });
+    }
+};
+
+// ------------------------------------------------------------ the kernel --
+template <class HS, class VS, int PH>
+__global__ void __launch_bounds__(DS_SPEC_NW * 32, DS_SPEC_MINB) ds_spec_kernel(const __grid_constant__ SpecParams p) {
+    constexpr int NW = DS_SPEC_NW, NT = NW * 32;
+    static_assert(HS::S % 4 == 0, "a chunk of 4 H repetitions must start on a 16-byte block");
+    using HC = HChunk<HS, PH>;
+    extern __shared__ __align__(128) uint8_t smem[];
+    const uint32_t mid0 = smem_u32(smem);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+    // unit u -> frame f, index `local` within the frame (incremental)
+    int64_t u = blockIdx.x;
+    int64_t f = blockIdx.x / (uint32_t)p.upf;
+    int32_t local = (int32_t)(blockIdx.x - (uint32_t)f * (uint32_t)p.upf);
+    const int32_t gdiv = (int32_t)(gridDim.x / (uint32_t)p.upf), gmod = (int32_t)(gridDim.x - gdiv * p.upf);
+    int mpar = 0;
+
+    // L2 prefetch (one thread) of the new input rows of band `band` of unit
+    // (f_, local_): rows (ov + Sv k band + reuse + i) mod H, i < rows, as one or
+    // two contiguous ranges -- the TMA engine streams them into L2 while the CTA
+    // computes the current band, so the H loads of the next band hit L2
+    auto prefetch_band = [&](int64_t f_, int32_t local_, int band_rel) {
+        const int pi_ = (p.n_planes > 2 && local_ >= p.pl[2].unit_start) ? 2
+                        : (p.n_planes > 1 && local_ >= p.pl[1].unit_start) ? 1 : 0;
+        const SpecPlane& Q = p.pl[pi_];
+        const int bnd = (local_ - Q.unit_start) * Q.L + band_rel;
+        if (bnd >= Q.nb) return;
+        const int reuse_ = band_rel > 0 ? p.ovl : 0;
+        const int rows_ = VS::S * (Q.k - 1) + VS::P - reuse_;
+        int r0 = (int)(((int64_t)Q.ov + (int64_t)VS::S * Q.k * bnd + reuse_) % Q.H);
+        const uint8_t* pl_ = p.in + f_ * p.in_frame + Q.in_off;
+        const int n1 = min(rows_, Q.H - r0);
+        prefetch_l2(pl_ + (int64_t)r0 * Q.W, (uint32_t)n1 * (uint32_t)Q.W);
+        if (rows_ > n1) prefetch_l2(pl_, (uint32_t)min(rows_ - n1, Q.H) * (uint32_t)Q.W);
+    };
+    if (tid == 0 && u < p.n_units) prefetch_band(f, local, 0);
+
+    for (; u < p.n_units; u += gridDim.x) {
+        const int pi = (p.n_planes > 2 && local >= p.pl[2].unit_start) ? 2
+                       : (p.n_planes > 1 && local >= p.pl[1].unit_start) ? 1 : 0;
+        const SpecPlane& P = p.pl[pi];
+        const int run = local - P.unit_start;
+        const int b0 = run * P.L, b1 = min(b0 + P.L, P.nb);
+        const uint8_t* plane = p.in + f * p.in_frame + P.in_off;
+        uint8_t* oplane = p.out + f * p.out_frame + P.out_off;
+        if (p.unit_count != nullptr && tid == 0) atomicAdd(p.unit_count + u, 1u);
+        const int mp = P.mp;
+        const int rfirst = VS::S * (P.k - 1) + VS::P;             // rows of a run's first band
+        // next unit of this CTA (for the prefetch of its first band)
+        int64_t fn = f + gdiv;
+        int32_t ln = local + gmod;
+        if (ln >= p.upf) { ln -= p.upf; ++fn; }
+
+        // A warp keeps one 32-chunk segment of the row for the whole unit (segs is a
+        // power of two dividing NW): its window blocks are fixed; it walks rows
+        // i = warp >> lgsegs, + step, ... with a running row pointer.  Chunks whose
+        // window crosses the row end (at most a few per row) are left to a
+        // small wrap pass, so the main loop has no per-block index arithmetic.
+        const int seg = warp & (P.segs - 1), step = NW >> P.lgsegs;
+        const int ch = seg * 32 + lane;
+        int B = P.blk0 + (HS::S / 4) * (ch < P.nch ? ch : P.nch - 1);
+        if (B >= P.nb16) B -= P.nb16;
+        const bool act = ch < P.nch && B + HC::kBlk <= P.nb16;
+        if (!act) B = P.nb16 - HC::kBlk;                            // in-bounds loads, result unused
+        const int i0 = warp >> P.lgsegs;
+        const int64_t rowstep = (int64_t)step * P.W, plane_bytes = (int64_t)P.H * P.W;
+        uint32_t x0[4 * HC::kBlk], x1[4 * HC::kBlk], x2[4 * HC::kBlk];
+        // issue cursor: row index rr (mod H) and the lane's window pointer in it
+        int rr = 0;
+        const uint8_t* rp = plane;
+        auto seek = [&](int first_row) {
+            rr = first_row + i0;
+            while (rr >= P.H) rr -= P.H;
+            rp = plane + (int64_t)rr * P.W + 16 * B;
+        };
+        auto issue = [&](int i, int nrows, uint32_t (&x)[4 * HC::kBlk]) {
+            if (i >= nrows) return;
+            HC::load_at(rp, x);
+            rr += step;
+            rp += rowstep;
+            if (rr >= P.H) { rr -= P.H; rp -= plane_bytes; }          // the band wraps the plane bottom
+        };
+        bool preloaded = false;
+
+        for (int band = b0; band < b1; ++band) {
+            const uint32_t mid = mid0 + mpar * p.mid_stride;
+            const int reuse = band > b0 ? p.ovl : 0;
+            if (tid == 0) {
+                if (band + 1 < b1) prefetch_band(f, local, band + 1 - b0);
+                else if (u + gridDim.x < p.n_units) prefetch_band(fn, ln, 0);
+            }
+            if (reuse) {
+                // the previous band's intermediate rows [Sv k, Sv k + ovl) are this
+                // band's rows [0, ovl): contiguous, so a word copy
+                const uint32_t src = mid0 + (mpar ^ 1) * p.mid_stride + VS::S * P.k * mp;
+                for (int x = 4 * tid; x < reuse * mp; x += 4 * NT) sts32(mid + x, lds32(src + x));
+            }
+            // ---- H task: input rows (ov + Sv k band + reuse + i) mod H -> intermediate rows reuse + i;
+            // the loads of the next two rows are in flight while a row computes (three
+            // register buffers, rotated); the first two rows of the next band are issued
+            // before this band's V pass
+            const int rows = rfirst - reuse;
+            int row0 = P.ov + VS::S * P.k * band + reuse;
+            while (row0 >= P.H) row0 -= P.H;
+            const uint32_t mcol = mid + reuse * mp + 4 * HS::Q * ch;
+            auto finish = [&](int i, const uint32_t (&x)[4 * HC::kBlk]) {
+                if (i >= rows || !act) return;
+                uint32_t o[HS::Q];
+                HC::compute(x, o);
+                const uint32_t mo = mcol + i * mp;
+                sfor<0, HS::Q>([&](auto w) { sts32(mo + 4 * w.value, o[w.value]); });
+            };
+            if (!preloaded) {
+                seek(row0);
+                issue(i0, rows, x0);
+                issue(i0 + step, rows, x1);
+            }
+            for (int i = i0; i < rows; i += 3 * step) {
+                issue(i + 2 * step, rows, x2);
+                finish(i, x0);
+                issue(i + 3 * step, rows, x0);
+                finish(i + step, x1);
+                issue(i + 4 * step, rows, x1);
+                finish(i + 2 * step, x2);
+            }
+            // wrap pass: (row, wrapping chunk) items over all threads, from the last
+            // warps down (they have the fewest main-loop rows)
+            for (int it = NT - 1 - tid; it < rows * P.nwc; it += NT) {
+                const int i = it / P.nwc, c = P.wch[it - i * P.nwc];
+                int r = row0 + i;
+                while (r >= P.H) r -= P.H;
+                int Bw = P.blk0 + (HS::S / 4) * c;
+                if (Bw >= P.nb16) Bw -= P.nb16;
+                uint32_t xw[4 * HC::kBlk], o[HS::Q];
+                HC::template load<true>(plane + (int64_t)r * P.W, Bw, P.nb16, xw);
+                HC::compute(xw, o);
+                const uint32_t mo = mid + (reuse + i) * mp + 4 * HS::Q * c;
+                sfor<0, HS::Q>([&](auto w) { sts32(mo + 4 * w.value, o[w.value]); });
+            }
+            // the next band's first rows (same unit) are issued across the barrier
+            preloaded = band + 1 < b1;
+            if (preloaded) {
+                int nrow0 = P.ov + VS::S * P.k * (band + 1) + p.ovl;
+                while (nrow0 >= P.H) nrow0 -= P.H;
+                seek(nrow0);
+                issue(i0, rfirst - p.ovl, x0);
+                issue(i0 + step, rfirst - p.ovl, x1);
+            }
+            __syncthreads();                                               // intermediate complete
+
+            // ---- V task: intermediate -> output rows, straight to HBM
+            const int wm = HS::Q * P.np;
+            const int items = P.k * P.nq;
+            uint8_t* obase = oplane + (int64_t)VS::Q * P.k * band * P.Wout;
+            for (int it = tid; it < items; it += NT) {
+                const int g = P.nq > 1 ? (int)__umulhi((uint32_t)it, P.nq_rcp) : it;
+                const int q = it - g * P.nq;
+                int32_t acc[VS::Q][4];
+                VQuad<VS>::run(mid + VS::S * g * mp + 4 * q, mp, acc);
+                uint8_t* o = obase + (int64_t)VS::Q * g * P.Wout + 4 * q;
+                const bool whole = 4 * q + 4 <= wm;
+                sfor<0, VS::Q>([&](auto kk) {
+                    const uint32_t c0 = qdiv<VS>(acc[kk.value][0]), c1 = qdiv<VS>(acc[kk.value][1]),
+                                   c2 = qdiv<VS>(acc[kk.value][2]), c3 = qdiv<VS>(acc[kk.value][3]);
+                    uint8_t* d = o + (int64_t)kk.value * P.Wout;
+                    const uint32_t al = (uint32_t)(uintptr_t)d & 3;
+                    if (whole && al == 0) {
+                        stg32_cs(d, __byte_perm(__byte_perm(c0, c1, 0x0040), __byte_perm(c2, c3, 0x0040), 0x5410));
+                    } else if (whole && al == 2) {                         // e.g. CIF chroma: 66-byte rows
+                        stg16(d, __byte_perm(c0, c1, 0x0040));
+                        stg16(d + 2, __byte_perm(c2, c3, 0x0040));
+                    } else {
+                        const int n = whole ? 4 : wm - 4 * q;
+                        stg8(d, c0);
+                        if (n > 1) stg8(d + 1, c1);
+                        if (n > 2) stg8(d + 2, c2);
+                        if (n > 3) stg8(d + 3, c3);
+                    }
+                });
+            }
+            mpar ^= 1;
+        }
+        f += gdiv;
+        local += gmod;
+        if (local >= p.upf) { local -= p.upf; ++f; }
+    }
+}
+
+}  // namespace dss

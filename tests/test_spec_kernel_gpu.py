@@ -1,0 +1,175 @@
+"""K-N1s (ds_spec.cuh): the K-N1g fused band kernel with the filter spec
+compiled in.  Byte-for-byte against the CPU oracle (O1 with the spec's
+stages, halos wrap toroidally) and against the runtime-tap
+K-N1g on the same inputs: the bench's halo spec and SPEC's downscaler on the
+paper's and BASELINE's geometries, column strips, ragged chunk tails, every
+unit processed once, every output byte written, and the fallbacks (a
+misaligned output row or input pointer runs the runtime-tap kernel)."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+torch = pytest.importorskip("torch")
+ds = pytest.importorskip("paper_1103_4881_b200")
+
+pytestmark = pytest.mark.gpu
+
+GENERAL = ds.DS_KERNEL_FUSED_GENERAL
+
+# bench.py HALO_SPEC (kept literally: the built-in K-N1s instance matches it)
+HALO = (
+    dict(pattern=13, paving=8, origin=-2, weights=[[1, 3, 5, 3, 1], [0, 0, 0, 1, 3, 5, 3, 1],
+                                                    [0, 0, 0, 0, 0, 0, 1, 3, 5, 3, 1]],
+         divisor=13, bias=6),
+    dict(pattern=14, paving=9, origin=-2, weights=[[1, 2, 4, 2, 1], [0, 0, 1, 2, 4, 2, 1],
+                                                    [0, 0, 0, 0, 0, 1, 2, 4, 2, 1],
+                                                    [0, 0, 0, 0, 0, 0, 0, 0, 1, 2, 4, 2, 1]],
+         divisor=10, bias=5),
+)
+
+
+def _stage(d):
+    return oracle.make_stage(d["pattern"], d["paving"], d["origin"], d["weights"], d["divisor"], d["bias"])
+
+
+def _want(fr, W, H, ch, chroma, spec):
+    if spec is None:
+        return oracle.execute_frames(fr, W, H, ch, chroma)
+    return oracle.execute_frames(fr, W, H, ch, chroma, _stage(spec[0]), _stage(spec[1]))
+
+
+def _handle(W, H, ch, chroma, spec):
+    s = None if spec is None else ds.make_spec(h=spec[0], v=spec[1], chroma=chroma)
+    d = ds.Downscaler(W, H, ch, chroma=chroma, spec=s)
+    d.set_kernel(GENERAL)
+    return d
+
+
+def _same(got, want, what):
+    if not np.array_equal(got, want):
+        bad = np.argwhere(got != want)
+        raise AssertionError(f"{what}: {len(bad)} bytes differ, first at {bad[:4].tolist()}")
+
+
+@pytest.mark.parametrize("spec", ["halo", "spec"])
+@pytest.mark.parametrize("W,H,ch,chroma,n", [(1920, 1080, 3, 1, 5), (1920, 1080, 3, 0, 3), (352, 288, 3, 1, 7),
+                                             (3840, 2160, 3, 1, 2), (128, 72, 1, 1, 9), (704, 576, 3, 1, 3),
+                                             (1024, 144, 3, 0, 4)])
+def test_compiled_spec_matches_oracle_and_runtime_taps(spec, W, H, ch, chroma, n):
+    sp = HALO if spec == "halo" else None
+    d = _handle(W, H, ch, chroma, sp)
+    d.set_general_variant(ds.DS_GENERAL_COMPILED)
+    fr = synth.random_frames(77, 3, n, W, H, ch, chroma)
+    x = torch.from_numpy(fr).cuda()
+    y = d(x)
+    torch.cuda.synchronize()
+    assert d.last_kernel() == GENERAL and d.last_variant() == 2
+    want = _want(fr, W, H, ch, chroma, sp)
+    _same(y.cpu().numpy(), want, f"K-N1s {spec} {W}x{H}")
+    d.set_general_variant(ds.DS_GENERAL_RUNTIME)
+    y2 = d(x)
+    torch.cuda.synchronize()
+    assert d.last_variant() == 1
+    _same(y2.cpu().numpy(), want, f"K-N1g runtime taps {spec} {W}x{H}")
+
+
+def test_compiled_spec_plans_strips_and_ragged_chunks():
+    """4K luma needs column strips; 720-wide CIF-like planes (W/8 = 90 H
+    repetitions, not a multiple of 4) end rows in partial chunks; both
+    exact."""
+    for W, H in ((3840, 2160), (720, 288), (208, 144)):
+        d = _handle(W, H, 3, 0, HALO)
+        info = d.launch_info(2, GENERAL)
+        assert info["variant"] == 2
+        fr = synth.random_frames(5, 0, 2, W, H, 3, 0)
+        y = d(torch.from_numpy(fr).cuda())
+        torch.cuda.synchronize()
+        assert d.last_variant() == 2
+        _same(y.cpu().numpy(), _want(fr, W, H, 3, 0, HALO), f"{W}x{H}")
+
+
+def test_auto_picks_compiled_variant_and_falls_back():
+    W, H, n = 352, 288, 4
+    d = _handle(W, H, 3, 1, HALO)
+    fr = synth.random_frames(8, 0, n, W, H)
+    want = _want(fr, W, H, 3, 1, HALO)
+    x = torch.from_numpy(fr).cuda()
+    y = d(x)
+    torch.cuda.synchronize()
+    assert d.last_variant() == 2
+    _same(y.cpu().numpy(), want, "auto")
+    # output rows at every alignment: K-N1s stores words, half-words or bytes by alignment
+    for off in (1, 2, 3):
+        buf = torch.zeros(n * d.out_frame_bytes + 8, dtype=torch.uint8, device="cuda")
+        yo = buf[off:off + n * d.out_frame_bytes].view(n, -1)
+        d(x, yo)
+        torch.cuda.synchronize()
+        assert d.last_variant() == 2
+        _same(yo.cpu().numpy(), want, f"output offset {off}")
+    # input 16-byte misaligned: runtime-tap K-N1g stages the rows itself
+    xb = torch.zeros(n * d.in_frame_bytes + 16, dtype=torch.uint8, device="cuda")
+    xi = xb[4:4 + n * d.in_frame_bytes]
+    xi.copy_(x.view(-1))
+    y3 = d(xi.view(n, -1))
+    torch.cuda.synchronize()
+    assert d.last_variant() == 1
+    _same(y3.cpu().numpy(), want, "misaligned in")
+
+
+def test_compiled_variant_rejected_where_it_cannot_run():
+    # W % 16 != 0 planes (SD chroma 360): no K-N1s plan
+    d = _handle(720, 576, 3, 1, HALO)
+    with pytest.raises(ds.DSError):
+        d.set_general_variant(ds.DS_GENERAL_COMPILED)
+    fr = synth.random_frames(2, 0, 2, 720, 576)
+    y = d(torch.from_numpy(fr).cuda())
+    torch.cuda.synchronize()
+    assert d.last_variant() == 1
+    _same(y.cpu().numpy(), _want(fr, 720, 576, 3, 1, HALO), "SD halo runtime taps")
+
+
+def test_compiled_spec_every_unit_once_and_every_byte_written():
+    W, H = 1920, 1080
+    d = _handle(W, H, 3, 1, HALO)
+    L = ds.lib()
+    x = ds.generate_frames(23, d.in_frame_bytes, seed=2)
+    for n in (1, 2, 7, 23):
+        units = L.ds_units(d.handle, n, GENERAL)
+        counts = torch.zeros(units, dtype=torch.int32, device="cuda")
+        assert L.ds_set_debug_counter(d.handle, counts.data_ptr()) == 0
+        d(x[:n])
+        torch.cuda.synchronize()
+        assert L.ds_set_debug_counter(d.handle, None) == 0
+        assert d.last_variant() == 2
+        c = counts.cpu().numpy()
+        assert (c == 1).all(), (n, int((c == 0).sum()), int((c > 1).sum()))
+    n = 3
+    fr = synth.random_frames(2, 0, n, W, H)
+    want = _want(fr, W, H, 3, 1, HALO)
+    xs = torch.from_numpy(fr).cuda()
+    guard = 4096
+    for sentinel in (0x00, 0xA5):
+        buf = torch.full((n * d.out_frame_bytes + 2 * guard,), sentinel, dtype=torch.uint8, device="cuda")
+        y = buf[guard: guard + n * d.out_frame_bytes].view(n, -1)
+        d(xs, y)
+        torch.cuda.synchronize()
+        assert d.last_variant() == 2
+        _same(y.cpu().numpy(), want, f"sentinel {sentinel:#x}")
+        b = buf.cpu().numpy()
+        assert (b[:guard] == sentinel).all() and (b[-guard:] == sentinel).all(), "write outside output"
+
+
+def test_compiled_spec_stream_every_frame():
+    """The bench workload (--spec halo): 300 HD 4:2:0 frames in one launch,
+    every frame against O1 with the halo stages, fanned out over host cores."""
+    from oracle.verify import verify_stream
+
+    W, H, N = 1920, 1080, 300
+    d = _handle(W, H, 3, 1, HALO)
+    x = ds.generate_frames(N, d.in_frame_bytes, seed=1)
+    y = d(x).cpu().numpy()
+    assert d.last_variant() == 2
+    r = verify_stream(y, W, H, 3, 1, seed=1, stages=HALO)
+    assert r["bit_exact"] and r["frames_checked"] == N, r
