@@ -268,6 +268,9 @@ int launch_spec(ds_handle* h, const uint8_t* in, int64_t n, uint8_t* out, cudaSt
         P.unit_start = start;
         start += (P.nb + P.L - 1) / P.L;
     }
+    p.out_al4 = (reinterpret_cast<uintptr_t>(out) & 3) == 0 && pi.out_frame_bytes % 4 == 0;
+    for (int q = 0; q < pi.n_planes; ++q)
+        if (pi.out_offset[q] % 4 || pi.out_w[q] % 4) p.out_al4 = 0;
     if (p.n_units == 0) return DS_OK;
     const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(p.n_units, (int64_t)c.grid_per_sm * h->sm_count));
     void* args[] = {&p};

@@ -50,6 +50,9 @@ typedef unsigned long long uintptr_t;
 #ifndef DS_SPEC_MINB
 #define DS_SPEC_MINB 4                // CTAs per SM the register budget is sized for
 #endif
+#ifndef DS_SPEC_DEPTH
+#define DS_SPEC_DEPTH 2               // H row loads in flight per warp (register buffers; 3 measured slower)
+#endif
 #ifndef DS_SPEC_MAXP
 #define DS_SPEC_MAXP 3
 #endif
@@ -80,6 +83,7 @@ struct SpecParams {
     uint32_t* unit_count;      // debug: +1 per unit processed, else null
     int64_t in_frame, out_frame, n_units;
     int32_t upf, n_planes, mid_stride, ovl;   // ovl = max(Pv - Sv, 0): rows a band shares with the next
+    int32_t out_al4, reserved_;               // 1: every output row starts 4-byte aligned
     SpecPlane pl[DS_SPEC_MAXP];
 };
 
@@ -132,13 +136,47 @@ struct StageInfo {
             if (ST::w(j, i) != 0) return true;
         return false;
     }
+    // Float division (fs = 1 or 2; 0 = not used): floor(a / D) = round((fs a - c) / (fs D))
+    // with c = fs (D - 1) / 2 an integer (fs = 2 for even D), since the exact
+    // value then sits >= 1 / (2 fs D) away from a rounding tie.  The dot product
+    // accumulates fs a - c on top of the bit pattern of 2^23 (0x4B000000 + y is
+    // the float 2^23 + y for 0 <= y < 2^23), so one FADD recovers fs a - c as a
+    // float and one FFMA with 1 / (fs D) plus the magic 1.5 * 2^23 rounds it to
+    // an integer in the low mantissa bits -- byte 0 of the result is the
+    // quotient.  Two FMA-pipe ops that either FMA unit can run, instead of an
+    // IMAD.HI on the heavy unit the dp4a also need.  Used when: D > 1 is not a
+    // power of two, 0 <= fs amin - c, fs amax < 2^20 (error < 1 / (16 D) from
+    // 1 / (fs D) in float), amax / D <= 255 (no clamp), fs w fits s8.
+    __host__ __device__ static constexpr int fs_for(int s) {
+        if (ST::D <= 1 || (ST::D & (ST::D - 1)) == 0) return 0;
+        if (acc_min() < 0) return 0;
+        const int64_t c = (int64_t)s * (ST::D - 1) / 2;
+        if ((int64_t)s * acc_min() < c || (int64_t)s * acc_max() >= (int64_t(1) << 20)) return 0;
+        if (acc_max() / ST::D > 255) return 0;
+        for (int j = 0; j < ST::Q; ++j)
+            for (int i = 0; i < ST::P; ++i)
+                if (s * ST::w(j, i) < -128 || s * ST::w(j, i) > 127) return 0;
+        return s;
+    }
+    __host__ __device__ static constexpr int fs() {
+#ifdef DS_SPEC_NO_FDIV
+        return 0;
+#else
+        return fs_for(ST::D % 2 ? 1 : 2);
+#endif
+    }
+    // the accumulator's start value and tap weights as the dot products use them
+    __host__ __device__ static constexpr int32_t acc0() {
+        return fs() ? (int32_t)(0x4B000000 + fs() * ST::B - fs() * (ST::D - 1) / 2) : ST::B;
+    }
+    __host__ __device__ static constexpr int ws(int j, int i) { return fs() ? fs() * ST::w(j, i) : ST::w(j, i); }
     // s8-packed weights of output j on the aligned word b when the pattern
     // starts at byte `off` of the word grid: byte t <-> tap 4b + t - off
     __host__ __device__ static constexpr uint32_t wword(int j, int b, int off) {
         uint32_t r = 0;
         for (int t = 0; t < 4; ++t) {
             const int i = 4 * b + t - off;
-            if (i >= 0 && i < ST::P) r |= (uint32_t)(uint8_t)(int8_t)ST::w(j, i) << (8 * t);
+            if (i >= 0 && i < ST::P) r |= (uint32_t)(uint8_t)(int8_t)ws(j, i) << (8 * t);
         }
         return r;
     }
@@ -173,6 +211,19 @@ __device__ __forceinline__ uint32_t qdiv(int32_t acc) {
     if constexpr (amax / ST::D > 255) q = min(q, 255u);
     return q;
 }
+// the output byte of an accumulator started at StageInfo<ST>::acc0(): byte 0
+// of the result is clamp_0^255(trunc(acc / D)) (higher bytes are not defined)
+template <class ST>
+__device__ __forceinline__ uint32_t qbyte(int32_t acc) {
+    using I = StageInfo<ST>;
+    if constexpr (I::fs() != 0) {
+        constexpr float R = 1.0f / (float)(I::fs() * ST::D);
+        const float y = __uint_as_float((uint32_t)acc) - 8388608.0f;    // fs a - c, exact
+        return __float_as_uint(fmaf(y, R, 12582912.0f));
+    } else {
+        return qdiv<ST>(acc);
+    }
+}
 
 __device__ __forceinline__ int32_t dp4a_us(uint32_t a, uint32_t b, int32_t c) {
     int32_t d;
@@ -190,6 +241,12 @@ __device__ __forceinline__ uint32_t lds32(uint32_t a) {
     uint32_t v;
     asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
     return v;
+}
+// store only when p (no branch: inactive lanes of a warp fall through)
+__device__ __forceinline__ void sts32_if(uint32_t a, uint32_t v, bool p) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.shared.u32 [%0], %1;\n}" ::"r"(a), "r"(v),
+                 "r"((uint32_t)p)
+                 : "memory");
 }
 __device__ __forceinline__ void sts32(uint32_t a, uint32_t v) {
     asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
@@ -284,12 +341,12 @@ struct HChunk {
         uint32_t q[4 * HS::Q];
         sfor<0, 4>([&](auto m) {
             sfor<0, HS::Q>([&](auto j) {
-                int32_t acc = HS::B;
+                int32_t acc = I::acc0();
                 sfor<kLo, kHi + 1>([&](auto b) {
                     constexpr uint32_t wq = I::wword(j.value, b.value, PH + HS::S * m.value);
                     if constexpr (wq != 0) acc = dp4a_us(x[b.value], wq, acc);
                 });
-                q[HS::Q * m.value + j.value] = qdiv<HS>(acc);
+                q[HS::Q * m.value + j.value] = qbyte<HS>(acc);
             });
         });
         sfor<0, HS::Q>([&](auto w) {
@@ -327,7 +384,7 @@ struct VQuad {
     // mb: shared address of row 0 of the repetition at this lane's 4 columns
     __device__ __forceinline__ static void run(uint32_t mb, int mp, int32_t (&acc)[VS::Q][4]) {
         sfor<0, VS::Q>([&](auto kk) {
-            sfor<0, 4>([&](auto e) { acc[kk.value][e.value] = VS::B; });
+            sfor<0, 4>([&](auto e) { acc[kk.value][e.value] = I::acc0(); });
         });
         sfor<0, kBlocks>([&](auto b) {
             constexpr int nl = live_in_block(b.value);
@@ -335,7 +392,7 @@ struct VQuad {
                 constexpr int t = nth_live(b.value, 0), i = 4 * b.value + t;
                 const uint32_t r = lds32(mb + i * mp);
                 sfor<0, VS::Q>([&](auto kk) {
-                    constexpr int wv = VS::w(kk.value, i);
+                    constexpr int wv = I::ws(kk.value, i);
                     if constexpr (wv != 0) {
                         sfor<0, 4>([&](auto e) {
                             constexpr uint32_t ws = (uint32_t)(uint8_t)(int8_t)wv << (8 * e.value);
@@ -349,8 +406,8 @@ struct VQuad {
                 uint32_t c[4];
                 sfor<0, 4>([&](auto e) { c[e.value] = __byte_perm(r0, r1, e.value | ((4 + e.value) << 4)); });
                 sfor<0, VS::Q>([&](auto kk) {
-                    constexpr uint32_t wq = (uint32_t)(uint8_t)(int8_t)VS::w(kk.value, 4 * b.value + t0) |
-                                            ((uint32_t)(uint8_t)(int8_t)VS::w(kk.value, 4 * b.value + t1) << 8);
+                    constexpr uint32_t wq = (uint32_t)(uint8_t)(int8_t)I::ws(kk.value, 4 * b.value + t0) |
+                                            ((uint32_t)(uint8_t)(int8_t)I::ws(kk.value, 4 * b.value + t1) << 8);
                     if constexpr (wq != 0) {
                         sfor<0, 4>([&](auto e) { acc[kk.value][e.value] = dp4a_us(c[e.value], wq, acc[kk.value][e.value]); });
                     }
@@ -443,7 +500,10 @@ __global__ void __launch_bounds__(DS_SPEC_NW * 32, DS_SPEC_MINB) ds_spec_kernel(
         if (!act) B = P.nb16 - HC::kBlk;                            // in-bounds loads, result unused
         const int i0 = warp >> P.lgsegs;
         const int64_t rowstep = (int64_t)step * P.W, plane_bytes = (int64_t)P.H * P.W;
-        uint32_t x0[4 * HC::kBlk], x1[4 * HC::kBlk], x2[4 * HC::kBlk];
+        uint32_t x0[4 * HC::kBlk], x1[4 * HC::kBlk];
+#if DS_SPEC_DEPTH != 2
+        uint32_t x2[4 * HC::kBlk];
+#endif
         // issue cursor: row index rr (mod H) and the lane's window pointer in it
         int rr = 0;
         const uint8_t* rp = plane;
@@ -483,12 +543,24 @@ __global__ void __launch_bounds__(DS_SPEC_NW * 32, DS_SPEC_MINB) ds_spec_kernel(
             while (row0 >= P.H) row0 -= P.H;
             const uint32_t mcol = mid + reuse * mp + 4 * HS::Q * ch;
             auto finish = [&](int i, const uint32_t (&x)[4 * HC::kBlk]) {
-                if (i >= rows || !act) return;
+                if (i >= rows) return;                                  // warp-uniform
                 uint32_t o[HS::Q];
-                HC::compute(x, o);
+                HC::compute(x, o);                                      // inactive lanes: garbage, not stored
                 const uint32_t mo = mcol + i * mp;
-                sfor<0, HS::Q>([&](auto w) { sts32(mo + 4 * w.value, o[w.value]); });
+                sfor<0, HS::Q>([&](auto w) { sts32_if(mo + 4 * w.value, o[w.value], act); });
             };
+#if DS_SPEC_DEPTH == 2
+            if (!preloaded) {
+                seek(row0);
+                issue(i0, rows, x0);
+            }
+            for (int i = i0; i < rows; i += 2 * step) {
+                issue(i + step, rows, x1);
+                finish(i, x0);
+                issue(i + 2 * step, rows, x0);
+                finish(i + step, x1);
+            }
+#else
             if (!preloaded) {
                 seek(row0);
                 issue(i0, rows, x0);
@@ -502,6 +574,7 @@ __global__ void __launch_bounds__(DS_SPEC_NW * 32, DS_SPEC_MINB) ds_spec_kernel(
                 issue(i + 4 * step, rows, x1);
                 finish(i + 2 * step, x2);
             }
+#endif
             // wrap pass: (row, wrapping chunk) items over all threads, from the last
             // warps down (they have the fewest main-loop rows)
             for (int it = NT - 1 - tid; it < rows * P.nwc; it += NT) {
@@ -523,7 +596,9 @@ __global__ void __launch_bounds__(DS_SPEC_NW * 32, DS_SPEC_MINB) ds_spec_kernel(
                 while (nrow0 >= P.H) nrow0 -= P.H;
                 seek(nrow0);
                 issue(i0, rfirst - p.ovl, x0);
+#if DS_SPEC_DEPTH != 2
                 issue(i0 + step, rfirst - p.ovl, x1);
+#endif
             }
             __syncthreads();                                               // intermediate complete
 
@@ -539,10 +614,10 @@ __global__ void __launch_bounds__(DS_SPEC_NW * 32, DS_SPEC_MINB) ds_spec_kernel(
                 uint8_t* o = obase + (int64_t)VS::Q * g * P.Wout + 4 * q;
                 const bool whole = 4 * q + 4 <= wm;
                 sfor<0, VS::Q>([&](auto kk) {
-                    const uint32_t c0 = qdiv<VS>(acc[kk.value][0]), c1 = qdiv<VS>(acc[kk.value][1]),
-                                   c2 = qdiv<VS>(acc[kk.value][2]), c3 = qdiv<VS>(acc[kk.value][3]);
+                    const uint32_t c0 = qbyte<VS>(acc[kk.value][0]), c1 = qbyte<VS>(acc[kk.value][1]),
+                                   c2 = qbyte<VS>(acc[kk.value][2]), c3 = qbyte<VS>(acc[kk.value][3]);
                     uint8_t* d = o + (int64_t)kk.value * P.Wout;
-                    const uint32_t al = (uint32_t)(uintptr_t)d & 3;
+                    const uint32_t al = p.out_al4 ? 0u : (uint32_t)(uintptr_t)d & 3;
                     if (whole && al == 0) {
                         stg32_cs(d, __byte_perm(__byte_perm(c0, c1, 0x0040), __byte_perm(c2, c3, 0x0040), 0x5410));
                     } else if (whole && al == 2) {                         // e.g. CIF chroma: 66-byte rows
