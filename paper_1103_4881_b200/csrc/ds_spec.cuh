@@ -50,9 +50,6 @@ typedef unsigned long long uintptr_t;
 #ifndef DS_SPEC_MINB
 #define DS_SPEC_MINB 4                // CTAs per SM the register budget is sized for
 #endif
-#ifndef DS_SPEC_DEPTH
-#define DS_SPEC_DEPTH 2               // H row loads in flight per warp (register buffers; 3 measured slower)
-#endif
 #ifndef DS_SPEC_MAXP
 #define DS_SPEC_MAXP 3
 #endif
@@ -217,9 +214,21 @@ template <class ST>
 __device__ __forceinline__ uint32_t qbyte(int32_t acc) {
     using I = StageInfo<ST>;
     if constexpr (I::fs() != 0) {
-        constexpr float R = 1.0f / (float)(I::fs() * ST::D);
-        const float y = __uint_as_float((uint32_t)acc) - 8388608.0f;    // fs a - c, exact
-        return __float_as_uint(fmaf(y, R, 12582912.0f));
+        constexpr int sD = I::fs() * ST::D;
+        constexpr int64_t ymax = I::fs() * I::acc_max();
+        if constexpr (ymax * sD < (int64_t(1) << 21)) {
+            // one FFMA: with R = n / 2^23 (n = round(2^23 / (fs D))), 2^23 R is an
+            // integer, so K = 1.5 * 2^23 - 2^23 R is exact and (2^23 + y) R + K =
+            // 1.5 * 2^23 + y R; |y (R - 1 / (fs D))| <= ymax 2^-24 < 1 / (8 fs D)
+            constexpr int64_t n = ((int64_t(1) << 24) / sD + 1) / 2;   // round(2^23 / sD)
+            constexpr float R = (float)n / 8388608.0f;
+            constexpr float K = 12582912.0f - (float)n;
+            return __float_as_uint(fmaf(__uint_as_float((uint32_t)acc), R, K));
+        } else {
+            constexpr float R = 1.0f / (float)sD;
+            const float y = __uint_as_float((uint32_t)acc) - 8388608.0f;    // fs a - c, exact
+            return __float_as_uint(fmaf(y, R, 12582912.0f));
+        }
     } else {
         return qdiv<ST>(acc);
     }
@@ -247,6 +256,12 @@ __device__ __forceinline__ void sts32_if(uint32_t a, uint32_t v, bool p) {
     asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.shared.u32 [%0], %1;\n}" ::"r"(a), "r"(v),
                  "r"((uint32_t)p)
                  : "memory");
+}
+__device__ __forceinline__ void lds128(uint32_t a, uint32_t& x, uint32_t& y, uint32_t& z, uint32_t& w) {
+    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(x), "=r"(y), "=r"(z), "=r"(w) : "r"(a));
+}
+__device__ __forceinline__ void sts128(uint32_t a, uint32_t x, uint32_t y, uint32_t z, uint32_t w) {
+    asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(a), "r"(x), "r"(y), "r"(z), "r"(w) : "memory");
 }
 __device__ __forceinline__ void sts32(uint32_t a, uint32_t v) {
     asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
@@ -501,9 +516,6 @@ __global__ void __launch_bounds__(DS_SPEC_NW * 32, DS_SPEC_MINB) ds_spec_kernel(
         const int i0 = warp >> P.lgsegs;
         const int64_t rowstep = (int64_t)step * P.W, plane_bytes = (int64_t)P.H * P.W;
         uint32_t x0[4 * HC::kBlk], x1[4 * HC::kBlk];
-#if DS_SPEC_DEPTH != 2
-        uint32_t x2[4 * HC::kBlk];
-#endif
         // issue cursor: row index rr (mod H) and the lane's window pointer in it
         int rr = 0;
         const uint8_t* rp = plane;
@@ -512,13 +524,14 @@ __global__ void __launch_bounds__(DS_SPEC_NW * 32, DS_SPEC_MINB) ds_spec_kernel(
             while (rr >= P.H) rr -= P.H;
             rp = plane + (int64_t)rr * P.W + 16 * B;
         };
-        auto issue = [&](int i, int nrows, uint32_t (&x)[4 * HC::kBlk]) {
-            if (i >= nrows) return;
+        auto issue = [&](uint32_t (&x)[4 * HC::kBlk]) {
             HC::load_at(rp, x);
             rr += step;
             rp += rowstep;
             if (rr >= P.H) { rr -= P.H; rp -= plane_bytes; }          // the band wraps the plane bottom
         };
+        // rows this warp computes in a band of `rows` rows: i0, i0 + step, ...
+        auto my_rows = [&](int rows) { return rows > i0 ? (rows - i0 + step - 1) / step : 0; };
         bool preloaded = false;
 
         for (int band = b0; band < b1; ++band) {
@@ -530,51 +543,42 @@ __global__ void __launch_bounds__(DS_SPEC_NW * 32, DS_SPEC_MINB) ds_spec_kernel(
             }
             if (reuse) {
                 // the previous band's intermediate rows [Sv k, Sv k + ovl) are this
-                // band's rows [0, ovl): contiguous, so a word copy
+                // band's rows [0, ovl): contiguous, so a 16-byte vector copy
                 const uint32_t src = mid0 + (mpar ^ 1) * p.mid_stride + VS::S * P.k * mp;
-                for (int x = 4 * tid; x < reuse * mp; x += 4 * NT) sts32(mid + x, lds32(src + x));
+                for (int x = 16 * tid; x < reuse * mp; x += 16 * NT) {
+                    uint32_t a0, a1, a2, a3;
+                    lds128(src + x, a0, a1, a2, a3);
+                    sts128(mid + x, a0, a1, a2, a3);
+                }
             }
             // ---- H task: input rows (ov + Sv k band + reuse + i) mod H -> intermediate rows reuse + i;
-            // the loads of the next two rows are in flight while a row computes (three
-            // register buffers, rotated); the first two rows of the next band are issued
-            // before this band's V pass
+            // the next row's loads are in flight while a row computes (two register
+            // buffers); the first row of the next band is issued before this band's
+            // V pass
             const int rows = rfirst - reuse;
             int row0 = P.ov + VS::S * P.k * band + reuse;
             while (row0 >= P.H) row0 -= P.H;
-            const uint32_t mcol = mid + reuse * mp + 4 * HS::Q * ch;
-            auto finish = [&](int i, const uint32_t (&x)[4 * HC::kBlk]) {
-                if (i >= rows) return;                                  // warp-uniform
+            const uint32_t mcol = mid + (reuse + i0) * mp + 4 * HS::Q * ch;
+            const uint32_t mstep = step * mp;
+            auto finish = [&](int k, const uint32_t (&x)[4 * HC::kBlk]) {
                 uint32_t o[HS::Q];
                 HC::compute(x, o);                                      // inactive lanes: garbage, not stored
-                const uint32_t mo = mcol + i * mp;
+                const uint32_t mo = mcol + k * mstep;
                 sfor<0, HS::Q>([&](auto w) { sts32_if(mo + 4 * w.value, o[w.value], act); });
             };
-#if DS_SPEC_DEPTH == 2
-            if (!preloaded) {
+            const int n_my = my_rows(rows);
+            if (!preloaded && n_my > 0) {
                 seek(row0);
-                issue(i0, rows, x0);
+                issue(x0);
             }
-            for (int i = i0; i < rows; i += 2 * step) {
-                issue(i + step, rows, x1);
-                finish(i, x0);
-                issue(i + 2 * step, rows, x0);
-                finish(i + step, x1);
+            int k = 0;
+            for (; k + 2 <= n_my; k += 2) {                             // rows k and k + 1 are this warp's
+                issue(x1);
+                finish(k, x0);
+                if (k + 2 < n_my) issue(x0);
+                finish(k + 1, x1);
             }
-#else
-            if (!preloaded) {
-                seek(row0);
-                issue(i0, rows, x0);
-                issue(i0 + step, rows, x1);
-            }
-            for (int i = i0; i < rows; i += 3 * step) {
-                issue(i + 2 * step, rows, x2);
-                finish(i, x0);
-                issue(i + 3 * step, rows, x0);
-                finish(i + step, x1);
-                issue(i + 4 * step, rows, x1);
-                finish(i + 2 * step, x2);
-            }
-#endif
+            if (k < n_my) finish(k, x0);
             // wrap pass: (row, wrapping chunk) items over all threads, from the last
             // warps down (they have the fewest main-loop rows)
             for (int it = NT - 1 - tid; it < rows * P.nwc; it += NT) {
@@ -589,48 +593,56 @@ __global__ void __launch_bounds__(DS_SPEC_NW * 32, DS_SPEC_MINB) ds_spec_kernel(
                 const uint32_t mo = mid + (reuse + i) * mp + 4 * HS::Q * c;
                 sfor<0, HS::Q>([&](auto w) { sts32(mo + 4 * w.value, o[w.value]); });
             }
-            // the next band's first rows (same unit) are issued across the barrier
-            preloaded = band + 1 < b1;
+            // the next band's first row (same unit) is issued across the barrier
+            preloaded = band + 1 < b1 && my_rows(rfirst - p.ovl) > 0;
             if (preloaded) {
                 int nrow0 = P.ov + VS::S * P.k * (band + 1) + p.ovl;
                 while (nrow0 >= P.H) nrow0 -= P.H;
                 seek(nrow0);
-                issue(i0, rfirst - p.ovl, x0);
-#if DS_SPEC_DEPTH != 2
-                issue(i0 + step, rfirst - p.ovl, x1);
-#endif
+                issue(x0);
             }
             __syncthreads();                                               // intermediate complete
 
             // ---- V task: intermediate -> output rows, straight to HBM
-            const int wm = HS::Q * P.np;
-            const int items = P.k * P.nq;
-            uint8_t* obase = oplane + (int64_t)VS::Q * P.k * band * P.Wout;
-            for (int it = tid; it < items; it += NT) {
-                const int g = P.nq > 1 ? (int)__umulhi((uint32_t)it, P.nq_rcp) : it;
-                const int q = it - g * P.nq;
-                int32_t acc[VS::Q][4];
-                VQuad<VS>::run(mid + VS::S * g * mp + 4 * q, mp, acc);
-                uint8_t* o = obase + (int64_t)VS::Q * g * P.Wout + 4 * q;
-                const bool whole = 4 * q + 4 <= wm;
-                sfor<0, VS::Q>([&](auto kk) {
-                    const uint32_t c0 = qbyte<VS>(acc[kk.value][0]), c1 = qbyte<VS>(acc[kk.value][1]),
-                                   c2 = qbyte<VS>(acc[kk.value][2]), c3 = qbyte<VS>(acc[kk.value][3]);
-                    uint8_t* d = o + (int64_t)kk.value * P.Wout;
-                    const uint32_t al = p.out_al4 ? 0u : (uint32_t)(uintptr_t)d & 3;
-                    if (whole && al == 0) {
-                        stg32_cs(d, __byte_perm(__byte_perm(c0, c1, 0x0040), __byte_perm(c2, c3, 0x0040), 0x5410));
-                    } else if (whole && al == 2) {                         // e.g. CIF chroma: 66-byte rows
-                        stg16(d, __byte_perm(c0, c1, 0x0040));
-                        stg16(d + 2, __byte_perm(c2, c3, 0x0040));
-                    } else {
-                        const int n = whole ? 4 : wm - 4 * q;
-                        stg8(d, c0);
-                        if (n > 1) stg8(d + 1, c1);
-                        if (n > 2) stg8(d + 2, c2);
-                        if (n > 3) stg8(d + 3, c3);
-                    }
-                });
+            {
+                const int wm = HS::Q * P.np;
+                const int items = P.k * P.nq;
+                uint8_t* obase = oplane + (int64_t)VS::Q * P.k * band * P.Wout;
+                auto vitem = [&](int it, auto fast) {
+                    const int g = P.nq > 1 ? (int)__umulhi((uint32_t)it, P.nq_rcp) : it;
+                    const int q = it - g * P.nq;
+                    int32_t acc[VS::Q][4];
+                    VQuad<VS>::run(mid + VS::S * g * mp + 4 * q, mp, acc);
+                    uint8_t* o = obase + (int64_t)VS::Q * g * P.Wout + 4 * q;
+                    sfor<0, VS::Q>([&](auto kk) {
+                        const uint32_t c0 = qbyte<VS>(acc[kk.value][0]), c1 = qbyte<VS>(acc[kk.value][1]),
+                                       c2 = qbyte<VS>(acc[kk.value][2]), c3 = qbyte<VS>(acc[kk.value][3]);
+                        uint8_t* d = o + (int64_t)kk.value * P.Wout;
+                        if constexpr (decltype(fast)::value == 1) {
+                            stg32_cs(d, __byte_perm(__byte_perm(c0, c1, 0x0040), __byte_perm(c2, c3, 0x0040), 0x5410));
+                        } else {
+                            const bool whole = 4 * q + 4 <= wm;
+                            const uint32_t al = (uint32_t)(uintptr_t)d & 3;
+                            if (whole && al == 0) {
+                                stg32_cs(d, __byte_perm(__byte_perm(c0, c1, 0x0040), __byte_perm(c2, c3, 0x0040), 0x5410));
+                            } else if (whole && al == 2) {                 // e.g. CIF chroma: 66-byte rows
+                                stg16(d, __byte_perm(c0, c1, 0x0040));
+                                stg16(d + 2, __byte_perm(c2, c3, 0x0040));
+                            } else {
+                                const int n = whole ? 4 : wm - 4 * q;
+                                stg8(d, c0);
+                                if (n > 1) stg8(d + 1, c1);
+                                if (n > 2) stg8(d + 2, c2);
+                                if (n > 3) stg8(d + 3, c3);
+                            }
+                        }
+                    });
+                };
+                if (p.out_al4 && wm % 4 == 0) {                         // every quad a whole aligned word
+                    for (int it = tid; it < items; it += NT) vitem(it, IC<1>{});
+                } else {
+                    for (int it = tid; it < items; it += NT) vitem(it, IC<0>{});
+                }
             }
             mpar ^= 1;
         }

@@ -32,12 +32,22 @@ def _check(D, B, wsum):
         pytest.skip("stage not eligible for the float division")
     c = s * (D - 1) // 2
     a = np.arange(B, B + 255 * wsum + 1, dtype=np.int64)
+    want = np.minimum(a // D, 255)
     y = (s * a - c).astype(np.float64)                         # exact in float32 too (< 2^21)
-    R = np.float64(np.float32(1.0) / np.float32(s * D))        # fl(1 / (fs D)), float32 division
+    sD, ymax = s * D, s * (B + 255 * wsum)
+    # two-op form: FADD (exact) then FFMA with fl(1 / (fs D))
+    R = np.float64(np.float32(1.0) / np.float32(sD))
     G = (y * R + 12582912.0).astype(np.float32)                # single rounding to float32
     low = G.view(np.uint32) & 0xFF
-    want = np.minimum(a // D, 255)
     assert np.array_equal(low, want), (D, B, int(np.argmax(low != want)))
+    # one-op form (ymax * fs D < 2^21): FFMA straight on the accumulator's bits
+    # 2^23 + y, R = round(2^23 / (fs D)) / 2^23, K = 1.5 * 2^23 - 2^23 R
+    if ymax * sD < (1 << 21):
+        n = ((1 << 24) // sD + 1) // 2
+        F = 8388608.0 + y
+        G1 = (F * (n / 8388608.0) + (12582912.0 - n)).astype(np.float32)   # exact product + K, one rounding
+        low1 = G1.view(np.uint32) & 0xFF
+        assert np.array_equal(low1, want), (D, B, "one-op", int(np.argmax(low1 != want)))
 
 
 @pytest.mark.parametrize("D,B,wsum", [(13, 6, 13), (10, 5, 10), (6, 3, 6), (3, 1, 3), (5, 2, 5), (7, 3, 7),
