@@ -1135,7 +1135,13 @@ DS_API int64_t ds_units(const ds_handle* h, int64_t n, int32_t kernel) {
 
 DS_API int ds_set_general_variant(ds_handle* h, int32_t variant) {
     if (!h || variant < DS_GENERAL_AUTO || variant > DS_GENERAL_COMPILED) return DS_EINVAL;
-    if (variant == DS_GENERAL_COMPILED && !h->spec_cfg.valid) return DS_EUNSUPPORTED;
+    if (variant == DS_GENERAL_COMPILED && !h->spec_cfg.valid) {
+        // no built-in instance: compile K-N1s for this spec now (NVRTC)
+        h->spec_jit_req = true;
+        const int rc = configure_spec(h);
+        if (rc) return rc;
+        if (!h->spec_cfg.valid) return DS_EUNSUPPORTED;
+    }
     if (variant == DS_GENERAL_RUNTIME && !h->general.valid) return DS_EUNSUPPORTED;
     h->general_variant = variant;
     return DS_OK;

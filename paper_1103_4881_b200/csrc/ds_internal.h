@@ -130,6 +130,7 @@ struct ds_handle {
     dsi::GeneralCfg general;
     dsi::SpecCfg spec_cfg;                  // K-N1s (compiled-spec K-N1g)
     int32_t general_variant = 0;            // ds_set_general_variant: 0 auto, 1 runtime taps, 2 compiled taps
+    bool spec_jit_req = false;              // compile K-N1s at run time for a spec without a built-in instance
     int kernel_pref = DS_KERNEL_AUTO;
     int32_t run_bands = 0;                  // ds_set_run_bands (0 = automatic)
     int32_t tune_stages = 0, tune_ctas = 0; // explicit ds_set_tuning (0 stages = none)
@@ -163,6 +164,11 @@ int configure_spec(ds_handle* h);
 bool spec_call_ok(const ds_handle* h, const uint8_t* in, const uint8_t* out);
 int launch_spec(ds_handle* h, const uint8_t* in, int64_t n, uint8_t* out, cudaStream_t st);
 SpecFn spec_jit_kernel(ds_handle* h, int phase);
+bool spec_jit_available();
+const char* spec_jit_log();
+int spec_jit_set_smem(SpecFn fn, int smem);
+int spec_jit_occupancy(SpecFn fn, int threads, int smem, int* occ);
+int spec_jit_launch(SpecFn fn, unsigned grid, unsigned threads, unsigned smem, cudaStream_t st, void** args);
 void spec_runs(const ds_handle* h, int64_t n, int32_t* L, int32_t* upf);
 int make_plan(int32_t W, int32_t H, int32_t channels, const ds_filter_spec* spec_in,
               ds_filter_spec* spec_out, ds_plan_info* info, int64_t unit_target = kUnitTargetBytes,

@@ -4,6 +4,7 @@
 // built-in instance is compiled at run time (ds_spec_jit.cu).
 // Citations: P:n = PAPER.md line n, S:n = SPEC.md line n, SURVEY sec. n.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -129,7 +130,11 @@ int configure_spec(ds_handle* h) {
     SpecFn fn = spec_builtin(sp);
     c.jit = 0;
     if (!fn) {
-        fn = spec_jit_kernel(h, ph);                                   // nullptr when JIT is unavailable
+        // no built-in instance: compile one at run time when asked for
+        // (ds_set_general_variant(DS_GENERAL_COMPILED) or DS_SPEC_JIT=1)
+        const char* env = getenv("DS_SPEC_JIT");
+        if (!h->spec_jit_req && !(env && env[0] == '1')) return DS_OK;
+        fn = spec_jit_kernel(h, ph);                                   // nullptr when NVRTC is unavailable
         c.jit = 1;
     }
     if (!fn) return DS_OK;
@@ -148,17 +153,21 @@ int configure_spec(ds_handle* h) {
     c.threads = DS_SPEC_NW * 32;
     c.smem = 2 * c.mid_stride;
     DeviceGuard g(h->device);
-    if (cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             c.smem) != cudaSuccess) {
-        cudaGetLastError();
-        return DS_OK;
-    }
     int occ = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, reinterpret_cast<const void*>(fn), c.threads, c.smem) !=
-            cudaSuccess ||
-        occ < 1) {
-        cudaGetLastError();
-        return DS_OK;
+    if (c.jit) {
+        if (spec_jit_set_smem(fn, c.smem) || spec_jit_occupancy(fn, c.threads, c.smem, &occ) || occ < 1) return DS_OK;
+    } else {
+        if (cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 c.smem) != cudaSuccess) {
+            cudaGetLastError();
+            return DS_OK;
+        }
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, reinterpret_cast<const void*>(fn), c.threads, c.smem) !=
+                cudaSuccess ||
+            occ < 1) {
+            cudaGetLastError();
+            return DS_OK;
+        }
     }
     c.grid_per_sm = std::min(occ, 4);
     c.fn = fn;
@@ -274,6 +283,7 @@ int launch_spec(ds_handle* h, const uint8_t* in, int64_t n, uint8_t* out, cudaSt
     if (p.n_units == 0) return DS_OK;
     const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(p.n_units, (int64_t)c.grid_per_sm * h->sm_count));
     void* args[] = {&p};
+    if (c.jit) return spec_jit_launch(c.fn, (unsigned)grid, (unsigned)c.threads, (unsigned)c.smem, st, args);
     if (cudaLaunchKernel(reinterpret_cast<const void*>(c.fn), dim3((unsigned)grid), dim3(c.threads), args,
                          (size_t)c.smem, st) != cudaSuccess) {
         cudaGetLastError();

@@ -34,6 +34,7 @@
 
 #ifdef __CUDACC_RTC__
 typedef unsigned char uint8_t;
+typedef signed char int8_t;
 typedef unsigned short uint16_t;
 typedef unsigned int uint32_t;
 typedef int int32_t;
@@ -315,10 +316,10 @@ struct HChunk {
     __device__ __forceinline__ static void load(const uint8_t* row, int B, int nb16, uint32_t (&x)[4 * kBlk]) {
         const uint8_t* base = row + 16 * B;
         sfor<0, kBlk>([&](auto b) {
-            constexpr int w0 = 4 * b.value, wlo = w0 > kLo ? w0 : kLo, whi = w0 + 3 < kHi ? w0 + 3 : kHi;
-            const uint8_t* a = base + 16 * b.value;
+            constexpr int w0 = 4 * decltype(b)::value, wlo = w0 > kLo ? w0 : kLo, whi = w0 + 3 < kHi ? w0 + 3 : kHi;
+            const uint8_t* a = base + 16 * decltype(b)::value;
             if constexpr (WRAP) {
-                int blk = B + b.value;
+                int blk = B + decltype(b)::value;
                 if (blk >= nb16) blk -= nb16;
                 a = row + 16 * blk;
             }
@@ -326,10 +327,10 @@ struct HChunk {
                 ldg128(a, x[w0], x[w0 + 1], x[w0 + 2], x[w0 + 3]);
             } else if constexpr (whi >= wlo) {
                 sfor<wlo - w0, whi - w0 + 1>([&](auto t) {
-                    constexpr int w = w0 + t.value;
-                    if constexpr ((w & 1) == 0 && w + 1 <= whi) ldg64(a + 4 * t.value, x[w], x[w + 1]);
+                    constexpr int w = w0 + decltype(t)::value;
+                    if constexpr ((w & 1) == 0 && w + 1 <= whi) ldg64(a + 4 * decltype(t)::value, x[w], x[w + 1]);
                     else if constexpr ((w & 1) == 1 && w - 1 >= wlo) { /* loaded with w - 1 */ }
-                    else x[w] = ldg32(a + 4 * t.value);
+                    else x[w] = ldg32(a + 4 * decltype(t)::value);
                 });
             }
         });
@@ -337,16 +338,16 @@ struct HChunk {
     // the same words from a base pointer to the chunk's first block (no wrap)
     __device__ __forceinline__ static void load_at(const uint8_t* base, uint32_t (&x)[4 * kBlk]) {
         sfor<0, kBlk>([&](auto b) {
-            constexpr int w0 = 4 * b.value, wlo = w0 > kLo ? w0 : kLo, whi = w0 + 3 < kHi ? w0 + 3 : kHi;
-            const uint8_t* a = base + 16 * b.value;
+            constexpr int w0 = 4 * decltype(b)::value, wlo = w0 > kLo ? w0 : kLo, whi = w0 + 3 < kHi ? w0 + 3 : kHi;
+            const uint8_t* a = base + 16 * decltype(b)::value;
             if constexpr (wlo == w0 && whi == w0 + 3) {
                 ldg128(a, x[w0], x[w0 + 1], x[w0 + 2], x[w0 + 3]);
             } else if constexpr (whi >= wlo) {
                 sfor<wlo - w0, whi - w0 + 1>([&](auto t) {
-                    constexpr int w = w0 + t.value;
-                    if constexpr ((w & 1) == 0 && w + 1 <= whi) ldg64(a + 4 * t.value, x[w], x[w + 1]);
+                    constexpr int w = w0 + decltype(t)::value;
+                    if constexpr ((w & 1) == 0 && w + 1 <= whi) ldg64(a + 4 * decltype(t)::value, x[w], x[w + 1]);
                     else if constexpr ((w & 1) == 1 && w - 1 >= wlo) { /* loaded with w - 1 */ }
-                    else x[w] = ldg32(a + 4 * t.value);
+                    else x[w] = ldg32(a + 4 * decltype(t)::value);
                 });
             }
         });
@@ -358,16 +359,16 @@ struct HChunk {
             sfor<0, HS::Q>([&](auto j) {
                 int32_t acc = I::acc0();
                 sfor<kLo, kHi + 1>([&](auto b) {
-                    constexpr uint32_t wq = I::wword(j.value, b.value, PH + HS::S * m.value);
-                    if constexpr (wq != 0) acc = dp4a_us(x[b.value], wq, acc);
+                    constexpr uint32_t wq = I::wword(decltype(j)::value, decltype(b)::value, PH + HS::S * decltype(m)::value);
+                    if constexpr (wq != 0) acc = dp4a_us(x[decltype(b)::value], wq, acc);
                 });
-                q[HS::Q * m.value + j.value] = qbyte<HS>(acc);
+                q[HS::Q * decltype(m)::value + decltype(j)::value] = qbyte<HS>(acc);
             });
         });
         sfor<0, HS::Q>([&](auto w) {
-            const uint32_t lo = __byte_perm(q[4 * w.value], q[4 * w.value + 1], 0x0040);
-            const uint32_t hi = __byte_perm(q[4 * w.value + 2], q[4 * w.value + 3], 0x0040);
-            o[w.value] = __byte_perm(lo, hi, 0x5410);
+            const uint32_t lo = __byte_perm(q[4 * decltype(w)::value], q[4 * decltype(w)::value + 1], 0x0040);
+            const uint32_t hi = __byte_perm(q[4 * decltype(w)::value + 2], q[4 * decltype(w)::value + 3], 0x0040);
+            o[decltype(w)::value] = __byte_perm(lo, hi, 0x5410);
         });
     }
 };
@@ -399,49 +400,49 @@ struct VQuad {
     // mb: shared address of row 0 of the repetition at this lane's 4 columns
     __device__ __forceinline__ static void run(uint32_t mb, int mp, int32_t (&acc)[VS::Q][4]) {
         sfor<0, VS::Q>([&](auto kk) {
-            sfor<0, 4>([&](auto e) { acc[kk.value][e.value] = I::acc0(); });
+            sfor<0, 4>([&](auto e) { acc[decltype(kk)::value][decltype(e)::value] = I::acc0(); });
         });
         sfor<0, kBlocks>([&](auto b) {
-            constexpr int nl = live_in_block(b.value);
+            constexpr int nl = live_in_block(decltype(b)::value);
             if constexpr (nl == 1) {
-                constexpr int t = nth_live(b.value, 0), i = 4 * b.value + t;
+                constexpr int t = nth_live(decltype(b)::value, 0), i = 4 * decltype(b)::value + t;
                 const uint32_t r = lds32(mb + i * mp);
                 sfor<0, VS::Q>([&](auto kk) {
-                    constexpr int wv = I::ws(kk.value, i);
+                    constexpr int wv = I::ws(decltype(kk)::value, i);
                     if constexpr (wv != 0) {
                         sfor<0, 4>([&](auto e) {
-                            constexpr uint32_t ws = (uint32_t)(uint8_t)(int8_t)wv << (8 * e.value);
-                            acc[kk.value][e.value] = dp4a_us(r, ws, acc[kk.value][e.value]);
+                            constexpr uint32_t ws = (uint32_t)(uint8_t)(int8_t)wv << (8 * decltype(e)::value);
+                            acc[decltype(kk)::value][decltype(e)::value] = dp4a_us(r, ws, acc[decltype(kk)::value][decltype(e)::value]);
                         });
                     }
                 });
             } else if constexpr (nl == 2) {
-                constexpr int t0 = nth_live(b.value, 0), t1 = nth_live(b.value, 1);
-                const uint32_t r0 = lds32(mb + (4 * b.value + t0) * mp), r1 = lds32(mb + (4 * b.value + t1) * mp);
+                constexpr int t0 = nth_live(decltype(b)::value, 0), t1 = nth_live(decltype(b)::value, 1);
+                const uint32_t r0 = lds32(mb + (4 * decltype(b)::value + t0) * mp), r1 = lds32(mb + (4 * decltype(b)::value + t1) * mp);
                 uint32_t c[4];
-                sfor<0, 4>([&](auto e) { c[e.value] = __byte_perm(r0, r1, e.value | ((4 + e.value) << 4)); });
+                sfor<0, 4>([&](auto e) { c[decltype(e)::value] = __byte_perm(r0, r1, decltype(e)::value | ((4 + decltype(e)::value) << 4)); });
                 sfor<0, VS::Q>([&](auto kk) {
-                    constexpr uint32_t wq = (uint32_t)(uint8_t)(int8_t)I::ws(kk.value, 4 * b.value + t0) |
-                                            ((uint32_t)(uint8_t)(int8_t)I::ws(kk.value, 4 * b.value + t1) << 8);
+                    constexpr uint32_t wq = (uint32_t)(uint8_t)(int8_t)I::ws(decltype(kk)::value, 4 * decltype(b)::value + t0) |
+                                            ((uint32_t)(uint8_t)(int8_t)I::ws(decltype(kk)::value, 4 * decltype(b)::value + t1) << 8);
                     if constexpr (wq != 0) {
-                        sfor<0, 4>([&](auto e) { acc[kk.value][e.value] = dp4a_us(c[e.value], wq, acc[kk.value][e.value]); });
+                        sfor<0, 4>([&](auto e) { acc[decltype(kk)::value][decltype(e)::value] = dp4a_us(c[decltype(e)::value], wq, acc[decltype(kk)::value][decltype(e)::value]); });
                     }
                 });
             } else if constexpr (nl >= 3) {
                 uint32_t r[4];
                 sfor<0, 4>([&](auto t) {
-                    constexpr int i = 4 * b.value + t.value;
-                    if constexpr (i < VS::P && I::live(i)) r[t.value] = lds32(mb + i * mp);
-                    else r[t.value] = 0;
+                    constexpr int i = 4 * decltype(b)::value + decltype(t)::value;
+                    if constexpr (i < VS::P && I::live(i)) r[decltype(t)::value] = lds32(mb + i * mp);
+                    else r[decltype(t)::value] = 0;
                 });
                 const uint32_t ta = __byte_perm(r[0], r[1], 0x5140), tb = __byte_perm(r[2], r[3], 0x5140);
                 const uint32_t tc = __byte_perm(r[0], r[1], 0x7362), td = __byte_perm(r[2], r[3], 0x7362);
                 const uint32_t c[4] = {__byte_perm(ta, tb, 0x5410), __byte_perm(ta, tb, 0x7632),
                                        __byte_perm(tc, td, 0x5410), __byte_perm(tc, td, 0x7632)};
                 sfor<0, VS::Q>([&](auto kk) {
-                    constexpr uint32_t wq = I::wword(kk.value, b.value, 0);
+                    constexpr uint32_t wq = I::wword(decltype(kk)::value, decltype(b)::value, 0);
                     if constexpr (wq != 0) {
-                        sfor<0, 4>([&](auto e) { acc[kk.value][e.value] = dp4a_us(c[e.value], wq, acc[kk.value][e.value]); });
+                        sfor<0, 4>([&](auto e) { acc[decltype(kk)::value][decltype(e)::value] = dp4a_us(c[decltype(e)::value], wq, acc[decltype(kk)::value][decltype(e)::value]); });
                     }
                 });
             }
@@ -564,7 +565,7 @@ __global__ void __launch_bounds__(DS_SPEC_NW * 32, DS_SPEC_MINB) ds_spec_kernel(
                 uint32_t o[HS::Q];
                 HC::compute(x, o);                                      // inactive lanes: garbage, not stored
                 const uint32_t mo = mcol + k * mstep;
-                sfor<0, HS::Q>([&](auto w) { sts32_if(mo + 4 * w.value, o[w.value], act); });
+                sfor<0, HS::Q>([&](auto w) { sts32_if(mo + 4 * decltype(w)::value, o[decltype(w)::value], act); });
             };
             const int n_my = my_rows(rows);
             if (!preloaded && n_my > 0) {
@@ -591,7 +592,7 @@ __global__ void __launch_bounds__(DS_SPEC_NW * 32, DS_SPEC_MINB) ds_spec_kernel(
                 HC::template load<true>(plane + (int64_t)r * P.W, Bw, P.nb16, xw);
                 HC::compute(xw, o);
                 const uint32_t mo = mid + (reuse + i) * mp + 4 * HS::Q * c;
-                sfor<0, HS::Q>([&](auto w) { sts32(mo + 4 * w.value, o[w.value]); });
+                sfor<0, HS::Q>([&](auto w) { sts32(mo + 4 * decltype(w)::value, o[decltype(w)::value]); });
             }
             // the next band's first row (same unit) is issued across the barrier
             preloaded = band + 1 < b1 && my_rows(rfirst - p.ovl) > 0;
@@ -615,9 +616,9 @@ __global__ void __launch_bounds__(DS_SPEC_NW * 32, DS_SPEC_MINB) ds_spec_kernel(
                     VQuad<VS>::run(mid + VS::S * g * mp + 4 * q, mp, acc);
                     uint8_t* o = obase + (int64_t)VS::Q * g * P.Wout + 4 * q;
                     sfor<0, VS::Q>([&](auto kk) {
-                        const uint32_t c0 = qbyte<VS>(acc[kk.value][0]), c1 = qbyte<VS>(acc[kk.value][1]),
-                                       c2 = qbyte<VS>(acc[kk.value][2]), c3 = qbyte<VS>(acc[kk.value][3]);
-                        uint8_t* d = o + (int64_t)kk.value * P.Wout;
+                        const uint32_t c0 = qbyte<VS>(acc[decltype(kk)::value][0]), c1 = qbyte<VS>(acc[decltype(kk)::value][1]),
+                                       c2 = qbyte<VS>(acc[decltype(kk)::value][2]), c3 = qbyte<VS>(acc[decltype(kk)::value][3]);
+                        uint8_t* d = o + (int64_t)decltype(kk)::value * P.Wout;
                         if constexpr (decltype(fast)::value == 1) {
                             stg32_cs(d, __byte_perm(__byte_perm(c0, c1, 0x0040), __byte_perm(c2, c3, 0x0040), 0x5410));
                         } else {

@@ -173,3 +173,62 @@ def test_compiled_spec_stream_every_frame():
     assert d.last_variant() == 2
     r = verify_stream(y, W, H, 3, 1, seed=1, stages=HALO)
     assert r["bit_exact"] and r["frames_checked"] == N, r
+
+
+# a spec with no built-in instance: origins 3 / -5 (window phases 3 and 11), sparse
+# and uneven taps, a pattern shorter than the paving in V's output 1
+OTHER = (
+    dict(pattern=13, paving=8, origin=3,
+         weights=[[1, 2, 3, 0, 0, 0, 0, 0, 0, 0, 0, 1, 1], [0, 0, 0, 2, 2, 2, 0, 0, 0, 0, 0, 0, 2],
+                  [0, 0, 0, 0, 0, 0, 4, 4, 1, 1, 0, 0, 0]], divisor=8, bias=4),
+    dict(pattern=14, paving=9, origin=-5,
+         weights=[[2, 2, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 4], [0, 0, 4, 4],
+                  [0, 0, 0, 0, 0, 3, 3, 0, 0, 0, 0, 2], [0, 0, 0, 0, 0, 0, 0, 5, 3]], divisor=8, bias=4),
+)
+
+
+@pytest.mark.parametrize("spec,W,H,chroma", [("other", 1920, 1080, 1), ("other", 352, 288, 1),
+                                            ("negative", 704, 576, 0), ("odd_divisor", 1024, 144, 1)])
+def test_run_time_compiled_spec(spec, W, H, chroma):
+    """A spec without a built-in instance: ds_set_general_variant(COMPILED)
+    compiles K-N1s for it at run time (NVRTC, from the same kernel source);
+    the output equals the oracle and the runtime-tap kernel."""
+    rng = np.random.default_rng(len(spec) + W)
+    if spec == "other":
+        sp = OTHER
+    elif spec == "negative":           # negative lobes: the clamp at 0 is live
+        sp = (dict(pattern=12, paving=8, origin=-3, weights=[[-1, 4, 9, 4, -1], [0, 0, 0, -1, 5, 8, 5, -1],
+                                                             [0, 0, 0, 0, 0, 0, -2, 6, 9, 6, -2]],
+                   divisor=15, bias=7),
+              dict(pattern=11, paving=9, origin=2, weights=[[-1, 6, 6, -1], [0, 0, 0, 1, 4, 4, 1], [0, 0, 0, 0, 0, 2, 3, 2],
+                                                            [0, 0, 0, 0, 0, 0, 0, 1, 3, 3, 1]], divisor=10, bias=5))
+    else:                              # odd divisors (float division path) with random taps
+        wh = [[int(x) for x in rng.integers(0, 9, 10)] for _ in range(3)]
+        wv = [[int(x) for x in rng.integers(0, 9, 12)] for _ in range(4)]
+        sp = (dict(pattern=10, paving=8, origin=5, weights=wh, divisor=int(sum(wh[0])) | 1, bias=3),
+              dict(pattern=12, paving=9, origin=-1, weights=wv, divisor=int(sum(wv[0])) | 1, bias=2))
+    d = _handle(W, H, 3, chroma, sp)
+    try:
+        d.set_general_variant(ds.DS_GENERAL_COMPILED)
+    except ds.DSError as e:
+        pytest.fail(f"run-time compilation unavailable: {e}")
+    assert d.launch_info(2, GENERAL)["variant"] == 3
+    n = 3
+    fr = synth.random_frames(91, 0, n, W, H, 3, chroma)
+    x = torch.from_numpy(fr).cuda()
+    y = d(x)
+    torch.cuda.synchronize()
+    assert d.last_variant() == 2
+    want = _want(fr, W, H, 3, chroma, sp)
+    _same(y.cpu().numpy(), want, f"K-N1s (run-time compiled) {spec} {W}x{H}")
+    d.set_general_variant(ds.DS_GENERAL_RUNTIME)
+    _same(d(x).cpu().numpy(), want, f"runtime taps {spec}")
+
+
+def test_run_time_compilation_refused_outside_k1s():
+    # taps outside s8 cannot go through dp4a: no compiled variant
+    sp = (dict(pattern=8, paving=8, origin=0, weights=[[200, 5], [0, 0, 0, 3, 3], [0, 0, 0, 0, 0, 0, 5, 1]],
+               divisor=206, bias=3), None)
+    d = _handle(352, 288, 3, 1, (sp[0], HALO[1]))
+    with pytest.raises(ds.DSError):
+        d.set_general_variant(ds.DS_GENERAL_COMPILED)

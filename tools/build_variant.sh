@@ -3,4 +3,4 @@
 name=$1; shift
 cd "$(dirname "$0")/.." && /usr/local/cuda/bin/nvcc -std=c++17 -O3 -lineinfo -gencode arch=compute_100a,code=sm_100a \
   -Xcompiler -fPIC,-fvisibility=hidden -shared -Xptxas=-v "$@" -I include paper_1103_4881_b200/csrc/*.cu \
-  -o paper_1103_4881_b200/libds_$name.so 2>&1 | grep -A2 "general_kernel" | grep -E "Used|spill"
+  -ldl -o paper_1103_4881_b200/libds_$name.so 2>&1 | grep -A2 "general_kernel" | grep -E "Used|spill"
