@@ -322,7 +322,7 @@ def ncu_measure(args, timeout_s=240):
     if args.stages or args.ctas:
         child += ["--stages", str(args.stages), "--ctas", str(args.ctas)]
     cmd = [ncu, "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum",
-           "--clock-control", "none", "--kernel-name", "regex:^ds_(fused|generic)", "--launch-skip", "3",
+           "--clock-control", "none", "--kernel-name", "regex:^ds_(fused|generic|spec)", "--launch-skip", "3",
            "--launch-count", "1", "--csv", *child]
     try:
         r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout_s, cwd=ROOT)

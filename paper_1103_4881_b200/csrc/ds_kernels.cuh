@@ -128,6 +128,41 @@ __device__ __forceinline__ void k1_task(const uint4 (&r)[4], int half, uint32_t 
     }
 }
 
+// Store a task's two 6-byte output pieces (rows orow and orow + Wout, bytes
+// 6c .. 6c+5; the output slot is 16-byte aligned).  Even chunks
+// start on a word (word, then half-word), odd chunks on a half-word (half-word,
+// then word): one 4-byte and one 2-byte store per row with per-lane addresses
+// and data instead of three 2-byte stores (DS_K1_STORE6 = 0: three).
+#ifndef DS_K1_STORE6
+#define DS_K1_STORE6 1
+#endif
+__device__ __forceinline__ void k1_store6(uint8_t* orow, int Wout, int c, const uint32_t (&lo)[2],
+                                          const uint32_t (&hi)[2]) {
+#pragma unroll
+    for (int kk = 0; kk < 2; ++kk) {
+        uint8_t* d = orow + (size_t)kk * Wout;
+#if DS_K1_STORE6
+        if ((Wout & 3) != 0) {                       // rows not word-aligned (e.g. 66-byte CIF chroma)
+            sts16(d, lo[kk]);
+            sts16(d + 2, lo[kk] >> 16);
+            sts16(d + 4, hi[kk]);
+            continue;
+        }
+        const bool odd = c & 1;
+        const uint32_t w = odd ? __byte_perm(lo[kk], hi[kk], 0x5432) : lo[kk];   // bytes 2..5 : 0..3
+        const uint32_t h = odd ? lo[kk] : hi[kk];                                 // bytes 0..1 : 4..5
+        uint8_t* dw = d + (odd ? 2 : 0);
+        uint8_t* dh = d + (odd ? 0 : 4);
+        asm volatile("st.shared.u32 [%0], %1;" ::"r"(smem_u32(dw)), "r"(w) : "memory");
+        sts16(dh, h);
+#else
+        sts16(d, lo[kk]);
+        sts16(d + 2, lo[kk] >> 16);
+        sts16(d + 4, hi[kk]);
+#endif
+    }
+}
+
 // ------------------------------------------------------------------- K-N1 --
 // Work unit = (frame, plane, band of k 9-row groups), full plane width.
 // Ring slot layout: for group g, rows 8g..8g+3 hold input rows 9g+0..3 and
@@ -184,13 +219,7 @@ __device__ __forceinline__ void k1_loop_wide(const uint8_t* st, uint8_t* ob, int
         uint32_t lo[2], hi[2];
         k1_task(r, hg & 1, lo, hi);
         uint8_t* orow = ob + (size_t)2 * hg * Wout + 6 * c;
-#pragma unroll
-        for (int kk = 0; kk < 2; ++kk) {
-            uint8_t* d = orow + (size_t)kk * Wout;
-            sts16(d, lo[kk]);
-            sts16(d + 2, lo[kk] >> 16);
-            sts16(d + 4, hi[kk]);
-        }
+        k1_store6(orow, Wout, c, lo, hi);
     }
 }
 // Whole band staged (short aligned rows): half-group hg reads slot rows
@@ -209,13 +238,7 @@ __device__ __forceinline__ void k1_loop_whole(const uint8_t* st, uint8_t* ob, in
         uint32_t lo[2], hi[2];
         k1_task(r, half, lo, hi);
         uint8_t* orow = ob + (size_t)2 * hg * Wout + 6 * c;
-#pragma unroll
-        for (int kk = 0; kk < 2; ++kk) {
-            uint8_t* d = orow + (size_t)kk * Wout;
-            sts16(d, lo[kk]);
-            sts16(d + 2, lo[kk] >> 16);
-            sts16(d + 4, hi[kk]);
-        }
+        k1_store6(orow, Wout, c, lo, hi);
     }
 }
 // Narrow plane (W % 16 == 8): st points at the band's first byte inside the

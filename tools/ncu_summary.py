@@ -93,6 +93,8 @@ def main():
     ap.add_argument("--launches", default=os.path.join(ROOT, "gpurun_out", "launches.csv"))
     ap.add_argument("--rep", action="append", default=[])
     ap.add_argument("--note", default="")
+    ap.add_argument("--build", default="", help="library source hash the captures were made on "
+                                                  "(default: the current tree's, bench.source_hash)")
     ap.add_argument("--frames", type=int, action="append", default=[],
                     help="frames per profiled launch, one per --rep (default: bench defaults)")
     a = ap.parse_args()
@@ -139,8 +141,14 @@ def main():
         rd = scale(*d["dram__bytes_read.sum"])
         wr = scale(*d["dram__bytes_write.sum"])
         dur = scale(*d["gpu__time_duration.sum"])
+        import sys
+
+        sys.path.insert(0, ROOT)
+        import bench
+
         summ[cfg] = {"dram_bytes_per_launch": rd + wr, "dram_read_bytes": rd, "dram_write_bytes": wr,
                      "duration_us_under_ncu": dur, "frames_per_launch": frames,
+                     "build_sha": a.build or bench.source_hash(),
                      "source": f"profiles/{a.round}/ncu_full_{cfg}.txt (ncu --set full --clock-control none)"}
     if a.rep:
         json.dump(summ, open(summ_path, "w"), indent=1)
