@@ -264,7 +264,7 @@ DS_API int ds_set_tuning(ds_handle* h, int32_t stages, int32_t ctas_per_sm);
 
 /* K-N1 work-unit (band) size: the largest number of 9-row groups whose
  * staged bytes stay <= target_bytes for plane 0, other planes matched to
- * it (0 = default, 32 KiB).  An explicit ds_set_tuning is kept (re-applied
+ * it (0 = default: 32 KiB, or 8 KiB for frames under 64 KiB such as QCIF).  An explicit ds_set_tuning is kept (re-applied
  * to the new unit size).  On error the handle is left unchanged.  Output is
  * unaffected.  Not synchronised with ds_run calls in flight on other threads. */
 DS_API int ds_set_band_bytes(ds_handle* h, int64_t target_bytes);

@@ -289,6 +289,12 @@ FusedCfg make_cfg(const ds_plan_info& pi) {
     c.stages = (int)std::max<int64_t>(
         2, std::min<int64_t>(8, (kInFlightTarget + kK1Ctas * c.stage_stride / 2) / (kK1Ctas * c.stage_stride)));
     c.ctas_per_sm = kK1Ctas;
+    if (pi.in_frame_bytes < kSmallFrameBytes) {
+        // small frames (8 KB bands): as many CTAs per SM as fit, 3-deep rings
+        // (QCIF x 2000: 0.58 -> 0.66 of the copy peak, profiles/r02/k1_small_sweep.txt)
+        c.stages = 3;
+        c.ctas_per_sm = 0;
+    }
     c.valid = true;
     return c;
 }
@@ -849,6 +855,11 @@ DS_API ds_handle* ds_create(int32_t frame_w, int32_t frame_h, int32_t channels,
     h->W = frame_w; h->H = frame_h; h->channels = channels;
     h->spec = spec;
     h->plan = pi;
+    h->band_target = default_band_target(pi.in_frame_bytes);
+    if (h->band_target != kUnitTargetBytes) {
+        ds_plan_info ps;
+        if (make_plan(frame_w, frame_h, channels, &spec, nullptr, &ps, h->band_target) == DS_OK) h->plan = ps;
+    }
     int crc = configure_fused(h);
     if (!crc) crc = configure_general(h);
     if (!crc) crc = configure_spec(h);
@@ -1096,7 +1107,7 @@ static int replan(ds_handle* h, int64_t band_target, int64_t general_target) {
 
 DS_API int ds_set_band_bytes(ds_handle* h, int64_t target) {
     if (!h || target < 0) return DS_EINVAL;
-    if (target == 0) target = kUnitTargetBytes;
+    if (target == 0) target = default_band_target(h->plan.in_frame_bytes);
     return replan(h, target, h->general_target);
 }
 

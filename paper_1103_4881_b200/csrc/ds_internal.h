@@ -13,6 +13,13 @@ namespace dsi {
 
 constexpr int kHostSlots = 3;                       // ds_run_host pipeline depth
 constexpr int64_t kUnitTargetBytes = 32 * 1024;     // K-N1 band size target (bytes staged)
+constexpr int64_t kSmallFrameBytes = 64 * 1024;     // frames below this (QCIF: 38 KB) ...
+constexpr int64_t kSmallUnitTargetBytes = 8 * 1024; // ... take 8 KB bands: more, smaller units and CTAs
+                                                    // (QCIF x 2000: 0.58 -> 0.66 of the copy peak,
+                                                    // profiles/r02/k1_small_sweep.txt)
+inline int64_t default_band_target(int64_t in_frame_bytes) {
+    return in_frame_bytes < kSmallFrameBytes ? kSmallUnitTargetBytes : kUnitTargetBytes;
+}
 constexpr int64_t kInFlightTarget = 120 * 1024;     // K-N1 bytes in flight per SM (measured
                                                     // optimum of tools/bw_probe tma_read)
 constexpr int kK1Ctas = 3;                          // K-N1 CTAs per SM (cap; what fits runs)

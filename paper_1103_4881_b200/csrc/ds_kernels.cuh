@@ -132,9 +132,11 @@ __device__ __forceinline__ void k1_task(const uint4 (&r)[4], int half, uint32_t 
 // 6c .. 6c+5; the output slot is 16-byte aligned).  Even chunks
 // start on a word (word, then half-word), odd chunks on a half-word (half-word,
 // then word): one 4-byte and one 2-byte store per row with per-lane addresses
-// and data instead of three 2-byte stores (DS_K1_STORE6 = 0: three).
+// and data instead of three 2-byte stores.  Measured 0.5-1% slower than the
+// three 2-byte stores on HD/4K (same-call A/B, profiles/r02/k1_store6_ab.txt),
+// so DS_K1_STORE6 defaults to 0.
 #ifndef DS_K1_STORE6
-#define DS_K1_STORE6 1
+#define DS_K1_STORE6 0
 #endif
 __device__ __forceinline__ void k1_store6(uint8_t* orow, int Wout, int c, const uint32_t (&lo)[2],
                                           const uint32_t (&hi)[2]) {

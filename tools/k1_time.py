@@ -11,9 +11,12 @@ import torch
 import paper_1103_4881_b200 as ds
 
 CFG = {"hd420": (1920, 1080, 1, 300), "hd444": (1920, 1080, 0, 300), "4k420": (3840, 2160, 1, 300),
-       "cif420": (352, 288, 1, 2000)}
+       "cif420": (352, 288, 1, 2000), "qcif420": (176, 144, 1, 2000), "cif420_300": (352, 288, 1, 300)}
 out = []
+only = sys.argv[1].split(",") if len(sys.argv) > 1 else list(CFG)
 for name, (W, H, chroma, n) in CFG.items():
+    if name not in only:
+        continue
     d = ds.Downscaler(W, H, 3, chroma=chroma)
     x = ds.generate_frames(n, d.in_frame_bytes, seed=1)
     y = d.alloc_out(n)
