@@ -194,12 +194,16 @@ void spec_runs(const ds_handle* h, int64_t n, int32_t* L, int32_t* upf) {
         return;
     }
     // equal work per unit across planes: a band of plane p covers Sv k_p rows of
-    // W_p bytes; runs are sized so the launch has ~6 units per CTA slot (longer
+    // W_p bytes; runs are sized so the launch has ~4 units per CTA slot (3/4/6/10 measured
+    // 0.2320/0.2273/0.2287/0.2384 ms on 300 HD halo frames) (longer
     // runs re-stage fewer halo rows, more units balance the persistent schedule)
     const int64_t slots = std::max<int64_t>(1, (int64_t)c.grid_per_sm * h->sm_count);
     double frame_work = 0;
     for (int p = 0; p < pi.n_planes; ++p) frame_work += (double)pi.in_w[p] * pi.in_h[p];
-    const double want_units = std::max<double>(1.0, 6.0 * slots / std::max<int64_t>(n, 1));
+#ifndef DS_SPEC_UNITS_PER_SLOT
+#define DS_SPEC_UNITS_PER_SLOT 4.0
+#endif
+    const double want_units = std::max<double>(1.0, DS_SPEC_UNITS_PER_SLOT * slots / std::max<int64_t>(n, 1));
     const double target = frame_work / want_units;                  // bytes of input per unit
     int32_t u = 0;
     for (int p = 0; p < pi.n_planes; ++p) {

@@ -48,6 +48,15 @@ typedef unsigned long long uintptr_t;
 #ifndef DS_SPEC_NW
 #define DS_SPEC_NW 8                  // warps per CTA
 #endif
+#if DS_SPEC_NW == 8
+#define DS_SPEC_LGNW 3
+#elif DS_SPEC_NW == 16
+#define DS_SPEC_LGNW 4
+#elif DS_SPEC_NW == 4
+#define DS_SPEC_LGNW 2
+#else
+#error "DS_SPEC_NW must be 4, 8 or 16"
+#endif
 #ifndef DS_SPEC_MINB
 #define DS_SPEC_MINB 4                // CTAs per SM the register budget is sized for
 #endif
@@ -532,7 +541,8 @@ __global__ void __launch_bounds__(DS_SPEC_NW * 32, DS_SPEC_MINB) ds_spec_kernel(
             if (rr >= P.H) { rr -= P.H; rp -= plane_bytes; }          // the band wraps the plane bottom
         };
         // rows this warp computes in a band of `rows` rows: i0, i0 + step, ...
-        auto my_rows = [&](int rows) { return rows > i0 ? (rows - i0 + step - 1) / step : 0; };
+        const int lgstep = DS_SPEC_LGNW - P.lgsegs;                // step is a power of two
+        auto my_rows = [&](int rows) { return rows > i0 ? (rows - i0 + step - 1) >> lgstep : 0; };
         bool preloaded = false;
 
         for (int band = b0; band < b1; ++band) {
