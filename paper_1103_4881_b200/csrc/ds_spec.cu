@@ -177,9 +177,7 @@ int configure_spec(ds_handle* h) {
 }
 
 // Runs of bands for a launch over n frames (units per frame into *upf, run
-// lengths into L): runs shrink, split evenly within each plane, until the
-// launch has >= 12 units per CTA slot (the persistent schedule's tail and the
-// luma/chroma work imbalance stay small); longer runs re-stage fewer halo rows.
+// lengths into L): ds_set_run_bands forces them; otherwise see below.
 void spec_runs(const ds_handle* h, int64_t n, int32_t* L, int32_t* upf) {
     const SpecCfg& c = h->spec_cfg;
     const ds_plan_info& pi = h->plan;
@@ -194,9 +192,10 @@ void spec_runs(const ds_handle* h, int64_t n, int32_t* L, int32_t* upf) {
         return;
     }
     // equal work per unit across planes: a band of plane p covers Sv k_p rows of
-    // W_p bytes; runs are sized so the launch has ~4 units per CTA slot (3/4/6/10 measured
-    // 0.2320/0.2273/0.2287/0.2384 ms on 300 HD halo frames) (longer
-    // runs re-stage fewer halo rows, more units balance the persistent schedule)
+    // W_p bytes; runs are sized so the launch has ~4 units per CTA slot (longer runs
+    // re-stage fewer halo rows and pay less per-unit setup, more units balance the
+    // persistent schedule; 3 / 4 / 6 / 10 per slot measured 0.2320 / 0.2273 / 0.2287 /
+    // 0.2384 ms on 300 HD halo frames)
     const int64_t slots = std::max<int64_t>(1, (int64_t)c.grid_per_sm * h->sm_count);
     double frame_work = 0;
     for (int p = 0; p < pi.n_planes; ++p) frame_work += (double)pi.in_w[p] * pi.in_h[p];
