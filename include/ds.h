@@ -230,9 +230,11 @@ DS_API int ds_plane_dims(const ds_handle* h, int plane, int32_t* in_w, int32_t* 
  * taps in [-128, 127], every plane W % 16 == 0 (and W >= 64), a 16-byte
  * aligned input and 4-byte aligned output rows.  Specs with a built-in
  * instance (SPEC's downscaler, the halo reading of bench.py) use it
- * directly; any other spec is compiled at ds_create with NVRTC when the
- * runtime compiler is present.  AUTO (default) picks K-N1s whenever it can
- * run a call. */
+ * directly; any other spec is compiled at ds_create with NVRTC (about
+ * 0.3 s, once per spec and process) when the runtime compiler is present
+ * (environment DS_SPEC_JIT=0 turns that off; DS_GENERAL_COMPILED still
+ * compiles on request).  AUTO (default) picks K-N1s whenever it can run a
+ * call. */
 enum { DS_GENERAL_AUTO = 0, DS_GENERAL_RUNTIME = 1, DS_GENERAL_COMPILED = 2 };
 
 /* Select the K-N1g variant.  Returns DS_OK, DS_EINVAL, or DS_EUNSUPPORTED

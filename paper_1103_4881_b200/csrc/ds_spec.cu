@@ -130,10 +130,11 @@ int configure_spec(ds_handle* h) {
     SpecFn fn = spec_builtin(sp);
     c.jit = 0;
     if (!fn) {
-        // no built-in instance: compile one at run time when asked for
-        // (ds_set_general_variant(DS_GENERAL_COMPILED) or DS_SPEC_JIT=1)
+        // no built-in instance: compile one at run time (NVRTC, ~0.3 s once per
+        // spec and process); DS_SPEC_JIT=0 leaves such specs to the runtime-tap
+        // kernel unless ds_set_general_variant(DS_GENERAL_COMPILED) asks for it
         const char* env = getenv("DS_SPEC_JIT");
-        if (!h->spec_jit_req && !(env && env[0] == '1')) return DS_OK;
+        if (!h->spec_jit_req && env && env[0] == '0') return DS_OK;
         fn = spec_jit_kernel(h, ph);                                   // nullptr when NVRTC is unavailable
         c.jit = 1;
     }

@@ -207,15 +207,18 @@ def _oracle_stage(d):
 
 
 @pytest.mark.parametrize("W,H,ch", [(48, 27, 1), (352, 288, 3), (64, 36, 3), (1920, 1080, 3)])
-@pytest.mark.parametrize("kernel", [ds.DS_KERNEL_FUSED_GENERAL, GENERIC])
-def test_halo_and_origin_spec(W, H, ch, kernel):
+@pytest.mark.parametrize("kernel,variant", [(ds.DS_KERNEL_FUSED_GENERAL, ds.DS_GENERAL_RUNTIME),
+                                            (ds.DS_KERNEL_FUSED_GENERAL, ds.DS_GENERAL_AUTO), (GENERIC, 0)])
+def test_halo_and_origin_spec(W, H, ch, kernel, variant):
     """P > S halos with toroidal wrap and origin != 0:
-    K-N1g (halo rows staged in smem, smem intermediate; runs of bands that
-    reuse the halo's intermediate rows, forced from 1 band to whole planes)
-    and K-N2."""
+    K-N1g with runtime taps (halo rows staged in smem, smem intermediate;
+    runs of bands that reuse the halo's intermediate rows, forced from 1 band
+    to whole planes), K-N1g's default (K-N1s compiled for this spec at run time
+    where it can run) and K-N2."""
     hd, vd = _halo_spec()
     spec = ds.make_spec(h=hd, v=vd, chroma=ds.DS_CHROMA_420)
     d = ds.Downscaler(W, H, ch, spec=spec)
+    d.set_general_variant(variant)
     assert d.plan.fused_general_eligible == 1 and d.plan.fused_eligible == 0
     fr = synth.random_frames(9, 0, 3, W, H, ch, 1)
     want = oracle.execute_frames(fr, W, H, ch, 1, _oracle_stage(hd), _oracle_stage(vd))
@@ -246,6 +249,7 @@ def test_general_column_strips(stage_bytes, spec_kind):
         W, H = 352, 288
     spec = ds.make_spec(h=hd, v=vd, chroma=ds.DS_CHROMA_420)
     d = ds.Downscaler(W, H, ch, spec=spec)
+    d.set_general_variant(ds.DS_GENERAL_RUNTIME)                 # strips are the runtime-tap kernel's
     d.set_general_stage_bytes(stage_bytes)
     assert d.plan.fused_general_eligible == 1 and d.plan.general_strips[0] > 1
     fr = synth.random_frames(7, 0, 4, W, H, ch, 1)
@@ -280,6 +284,7 @@ def test_general_strips_8k_halo():
     W, H = 7680, 4320
     hd, vd = _halo_spec()
     d = ds.Downscaler(W, H, 3, spec=ds.make_spec(h=hd, v=vd, chroma=ds.DS_CHROMA_420))
+    d.set_general_variant(ds.DS_GENERAL_RUNTIME)
     assert d.plan.fused_general_eligible == 1 and d.plan.general_strips[0] > 1
     fr = synth.random_frames(11, 0, 2, W, H, 3, 1)
     got = _run(d, fr, ds.DS_KERNEL_FUSED_GENERAL)
@@ -300,11 +305,14 @@ def test_negative_weights_and_other_ratio():
     _assert_same(_run(d, fr, GENERIC), want, "negative K-N2")
 
 
+@pytest.mark.parametrize("variant", [ds.DS_GENERAL_RUNTIME, ds.DS_GENERAL_AUTO])
 @pytest.mark.parametrize("W,H,ch,chroma", [(352, 288, 3, 1), (1920, 1080, 3, 1), (1920, 1080, 3, 0),
                                            (48, 27, 1, 1)])
-def test_general_kernel_on_spec_taps(W, H, ch, chroma):
-    """K-N1g forced on SPEC's own downscaler equals the oracle (and K-N1)."""
+def test_general_kernel_on_spec_taps(W, H, ch, chroma, variant):
+    """K-N1g forced on SPEC's own downscaler equals the oracle (and K-N1),
+    with runtime taps and as K-N1s (the built-in SPEC instance)."""
     d = ds.Downscaler(W, H, ch, chroma=chroma)
+    d.set_general_variant(variant)
     fr = synth.random_frames(17, 0, 3, W, H, ch, chroma)
     got = _run(d, fr, ds.DS_KERNEL_FUSED_GENERAL)
     assert d.last_kernel() == ds.DS_KERNEL_FUSED_GENERAL
@@ -330,7 +338,7 @@ def test_general_kernel_fuzz_random_specs():
     """Random separable specs (halos, gaps P < S, origins, negative taps,
     divisors incl. 1 and 2^20) on random geometries, K-N1g vs the oracle."""
     rng = np.random.default_rng(fuzz_seed(2024))
-    checked = 0
+    checked = compiled = 0
     for trial in range(40 * FUZZ_SCALE):
         hd, vd = _random_spec(rng)
         ch = int(rng.choice([1, 3]))
@@ -350,11 +358,22 @@ def test_general_kernel_fuzz_random_specs():
             d.set_general_stage_bytes(int(rng.choice([1024, 3000, 8000])))
             if not d.plan.fused_general_eligible:
                 continue
+        d.set_general_variant(ds.DS_GENERAL_RUNTIME)
         got = _run(d, fr, ds.DS_KERNEL_FUSED_GENERAL)
-        assert d.last_kernel() == ds.DS_KERNEL_FUSED_GENERAL
+        assert d.last_kernel() == ds.DS_KERNEL_FUSED_GENERAL and d.last_variant() == 1
         _assert_same(got, want, f"fuzz {trial}: {W}x{H}x{ch} h={hd} v={vd} strips={list(d.plan.general_strips)}")
         checked += 1
+        # the same spec with the spec compiled in (K-N1s, NVRTC) wherever it can run
+        try:
+            d.set_general_variant(ds.DS_GENERAL_COMPILED)
+        except ds.DSError:
+            continue
+        got = _run(d, fr, ds.DS_KERNEL_FUSED_GENERAL)
+        assert d.last_variant() == 2
+        _assert_same(got, want, f"fuzz {trial} K-N1s: {W}x{H}x{ch} h={hd} v={vd}")
+        compiled += 1
     assert checked >= 25 * FUZZ_SCALE
+    assert compiled >= 1
 
 
 # ------------------------------------------------------- alignment / API --
@@ -741,6 +760,7 @@ def test_every_unit_processed_exactly_once(kernel, halo, strips):
     d = ds.Downscaler(W, H, 3, spec=spec)
     d.set_kernel(kernel)
     if strips:                                   # units = (frame, plane, column strip, run)
+        d.set_general_variant(ds.DS_GENERAL_RUNTIME)
         d.set_general_stage_bytes(6000)
         assert d.plan.general_strips[0] > 1
     L = ds.lib()
