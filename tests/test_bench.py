@@ -110,3 +110,27 @@ def test_config_dict_is_shared_by_both_arms():
     j = _line(["--impl", "reference", "--config", "qcif420", "--steps", "1", "--warmup", "0"])
     a = bench.parse(["--config", "qcif420"])
     assert j["config"] == bench.config_dict(a, bench.workload(a, 1), 1)
+
+
+@pytest.mark.gpu
+def test_bench_two_ranks_one_gpu_line():
+    """The N > 1 bench path on one GPU (two torchrun ranks, gloo process group):
+    max-over-ranks timing, the padded gather to rank 0 (warmed up, repeated),
+    the fused gather (same device, no probe), the 1-GPU solo run, every
+    gathered frame checked against the oracle, cpu_baseline on rank 0."""
+    env = dict(os.environ, DS_DIST_BACKEND="gloo")
+    r = subprocess.run([sys.executable, BENCH, "--gpus", "2", "--steps", "3", "--warmup", "3",
+                        "--cpu-seconds", "1", "--no-ncu"], capture_output=True, text=True, timeout=900,
+                       cwd=ROOT, env=env)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    j = json.loads(lines[0])
+    assert j["n_gpus"] == 2 and j["scaling"] == "weak" and j["config"]["frames"] == 600
+    g = j["gather"]
+    assert g["reps"] == 5 and g["gather_ms"] > 0 and g["bytes"] == 600 * j["config"]["out_frame_bytes"]
+    assert j["gather_fused"] is not None and j["gather_fused"]["matches_gather"] is True
+    assert j["solo_1gpu"]["frames_1gpu"] == 300 and j["speedup_vs_1gpu"] > 0
+    p = j["parity"]
+    assert p["frames_checked"] == p["frames_total"] == 600 and p["bit_exact"] is True
+    assert j["cpu_baseline"]["cores"] == 1
