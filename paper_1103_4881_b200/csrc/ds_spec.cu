@@ -96,7 +96,9 @@ bool spec_plane_plan(const ds_filter_spec& sp, int32_t W, int32_t H, int64_t bud
     const int nch = (np + 3) / 4, segs = (nch + 31) / 32;
     if (DS_SPEC_NW % segs != 0) return false;          // a warp keeps one row segment (segs | NW)
     const int64_t nq = ((int64_t)Qh * np + 3) / 4;
-    const int64_t mp = round_up(std::max<int64_t>(4LL * Qh * nch, 4 * nq), 16);
+    // row stride: every chunk a warp segment covers plus one scratch chunk (the
+    // H pass's inactive lanes store there unconditionally), and every V quad
+    const int64_t mp = round_up(std::max<int64_t>(4LL * Qh * (32LL * segs + 1), 4 * nq), 16);
     const int ovl = std::max(0, Pv - Sv);
     double best = 1e300;
     bool found = false;

@@ -58,7 +58,7 @@ typedef unsigned long long uintptr_t;
 #error "DS_SPEC_NW must be 4, 8 or 16"
 #endif
 #ifndef DS_SPEC_MINB
-#define DS_SPEC_MINB 4                // CTAs per SM the register budget is sized for
+#define DS_SPEC_MINB 3                // CTAs per SM the register budget is sized for (4: 64 regs, constants rematerialised; measured slower)
 #endif
 #ifndef DS_SPEC_MAXP
 #define DS_SPEC_MAXP 3
@@ -524,21 +524,22 @@ __global__ void __launch_bounds__(DS_SPEC_NW * 32, DS_SPEC_MINB) ds_spec_kernel(
         const bool act = ch < P.nch && B + HC::kBlk <= P.nb16;
         if (!act) B = P.nb16 - HC::kBlk;                            // in-bounds loads, result unused
         const int i0 = warp >> P.lgsegs;
-        const int64_t rowstep = (int64_t)step * P.W, plane_bytes = (int64_t)P.H * P.W;
+        // issue cursor: a 32-bit byte offset of the lane's window in the plane
+        // (planes are < 2^31 bytes); it advances `step` rows per issue and wraps
+        // at the plane bottom by one compare and subtract
+        const uint32_t rowstep = (uint32_t)(step * P.W), plane_bytes = (uint32_t)P.H * (uint32_t)P.W;
+        const uint8_t* const wbase = plane + 16 * B;
+        uint32_t roff = 0;
         uint32_t x0[4 * HC::kBlk], x1[4 * HC::kBlk];
-        // issue cursor: row index rr (mod H) and the lane's window pointer in it
-        int rr = 0;
-        const uint8_t* rp = plane;
         auto seek = [&](int first_row) {
-            rr = first_row + i0;
+            int rr = first_row + i0;
             while (rr >= P.H) rr -= P.H;
-            rp = plane + (int64_t)rr * P.W + 16 * B;
+            roff = (uint32_t)rr * (uint32_t)P.W;
         };
         auto issue = [&](uint32_t (&x)[4 * HC::kBlk]) {
-            HC::load_at(rp, x);
-            rr += step;
-            rp += rowstep;
-            if (rr >= P.H) { rr -= P.H; rp -= plane_bytes; }          // the band wraps the plane bottom
+            HC::load_at(wbase + roff, x);
+            roff += rowstep;
+            if (roff >= plane_bytes) roff -= plane_bytes;
         };
         // rows this warp computes in a band of `rows` rows: i0, i0 + step, ...
         const int lgstep = DS_SPEC_LGNW - P.lgsegs;                // step is a power of two
@@ -569,13 +570,16 @@ __global__ void __launch_bounds__(DS_SPEC_NW * 32, DS_SPEC_MINB) ds_spec_kernel(
             const int rows = rfirst - reuse;
             int row0 = P.ov + VS::S * P.k * band + reuse;
             while (row0 >= P.H) row0 -= P.H;
-            const uint32_t mcol = mid + (reuse + i0) * mp + 4 * HS::Q * ch;
+            // inactive lanes (past the row, or a wrapping chunk left to the wrap
+            // pass) store their garbage into a scratch chunk past the row's
+            // chunks (mp >= 4 Qh (32 segs + 1)), so the stores need no predicate
+            const uint32_t mcol = mid + (reuse + i0) * mp + 4 * HS::Q * (act ? ch : 32 * P.segs);
             const uint32_t mstep = step * mp;
             auto finish = [&](int k, const uint32_t (&x)[4 * HC::kBlk]) {
                 uint32_t o[HS::Q];
-                HC::compute(x, o);                                      // inactive lanes: garbage, not stored
+                HC::compute(x, o);
                 const uint32_t mo = mcol + k * mstep;
-                sfor<0, HS::Q>([&](auto w) { sts32_if(mo + 4 * decltype(w)::value, o[decltype(w)::value], act); });
+                sfor<0, HS::Q>([&](auto w) { sts32(mo + 4 * decltype(w)::value, o[decltype(w)::value]); });
             };
             const int n_my = my_rows(rows);
             if (!preloaded && n_my > 0) {
