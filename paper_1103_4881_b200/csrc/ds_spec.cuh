@@ -60,6 +60,9 @@ typedef unsigned long long uintptr_t;
 #ifndef DS_SPEC_MINB
 #define DS_SPEC_MINB 3                // CTAs per SM the register budget is sized for (4: 64 regs, constants rematerialised; measured slower)
 #endif
+#ifndef DS_SPEC_DEPTH3
+#define DS_SPEC_DEPTH3 0              // 1: three rows of H loads in flight per warp instead of two
+#endif
 #ifndef DS_SPEC_MAXP
 #define DS_SPEC_MAXP 3
 #endif
@@ -531,6 +534,9 @@ __global__ void __launch_bounds__(DS_SPEC_NW * 32, DS_SPEC_MINB) ds_spec_kernel(
         const uint8_t* const wbase = plane + 16 * B;
         uint32_t roff = 0;
         uint32_t x0[4 * HC::kBlk], x1[4 * HC::kBlk];
+#if DS_SPEC_DEPTH3
+        uint32_t x2[4 * HC::kBlk];
+#endif
         auto seek = [&](int first_row) {
             int rr = first_row + i0;
             while (rr >= P.H) rr -= P.H;
@@ -587,6 +593,20 @@ __global__ void __launch_bounds__(DS_SPEC_NW * 32, DS_SPEC_MINB) ds_spec_kernel(
                 issue(x0);
             }
             int k = 0;
+#if DS_SPEC_DEPTH3
+            // three register buffers: rows k, k + 1, k + 2 in flight
+            if (n_my > 1) issue(x1);
+            for (; k + 3 <= n_my; k += 3) {
+                issue(x2);
+                finish(k, x0);
+                if (k + 3 < n_my) issue(x0);
+                finish(k + 1, x1);
+                if (k + 4 < n_my) issue(x1);
+                finish(k + 2, x2);
+            }
+            if (k < n_my) finish(k, x0);
+            if (k + 1 < n_my) finish(k + 1, x1);
+#else
             for (; k + 2 <= n_my; k += 2) {                             // rows k and k + 1 are this warp's
                 issue(x1);
                 finish(k, x0);
@@ -594,6 +614,7 @@ __global__ void __launch_bounds__(DS_SPEC_NW * 32, DS_SPEC_MINB) ds_spec_kernel(
                 finish(k + 1, x1);
             }
             if (k < n_my) finish(k, x0);
+#endif
             // wrap pass: (row, wrapping chunk) items over all threads, from the last
             // warps down (they have the fewest main-loop rows)
             for (int it = NT - 1 - tid; it < rows * P.nwc; it += NT) {
