@@ -860,7 +860,8 @@ def main():
 
     if rank == 0:
         kname = {ds.DS_KERNEL_FUSED: "ds_fused_band_kernel",
-                 ds.DS_KERNEL_FUSED_GENERAL: "ds_fused_general_kernel"}.get(kernel_used, "ds_generic_kernel")
+                 ds.DS_KERNEL_FUSED_GENERAL: ("ds_spec_kernel" if d.last_variant() == 2 else
+                                              "ds_fused_general_kernel")}.get(kernel_used, "ds_generic_kernel")
         line = {
             "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": world,
             "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": total_ms / args.steps,
@@ -869,6 +870,7 @@ def main():
             "data": f"synthetic (splitmix64 counter-hash frames by global byte index, seed {args.seed})",
             "config": config_dict(args, cfg, world),
             "launch": dict(launch or {}, kernel_name=ds.KERNEL_NAMES.get(kernel_used),
+                           variant_name=ds.VARIANT_NAMES.get((launch or {}).get("variant")),
                            frames_per_rank=n, band_groups=list(d.plan.band_groups)[: cfg["channels"]],
                            units_per_frame=d.plan.units_per_frame),
             "stages": (launch or {}).get("stages"),

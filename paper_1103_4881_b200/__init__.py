@@ -26,7 +26,7 @@ VARIANT_NAMES = {0: None, 1: "runtime taps (ds_general.cuh)", 2: "compiled taps,
 DS_MAX_PATTERN, DS_MAX_OUTPUTS, DS_MAX_PLANES = 16, 8, 3
 KERNEL_NAMES = {DS_KERNEL_AUTO: "none", DS_KERNEL_FUSED: "K-N1 fused band (TMA ring)",
                 DS_KERNEL_GENERIC: "K-N2 generic",
-                DS_KERNEL_FUSED_GENERAL: "K-N1g fused band, any spec (TMA ring, smem halo + mid)"}
+                DS_KERNEL_FUSED_GENERAL: "K-N1g fused band, any spec (variant: runtime taps or K-N1s)"}
 
 
 class ds_stage_spec(C.Structure):

@@ -88,7 +88,7 @@ def test_bench_halo_spec_line():
     """--spec halo: the K-N1g kernel on the halo spec, roofline on in + out
     bytes, every frame checked against O1 with the spec's stages."""
     j = _line(["--spec", "halo", "--steps", "10", "--warmup", "3", "--cpu-seconds", "2", "--no-ncu"])
-    assert j["roofline"]["kernel"] == "ds_fused_general_kernel"
+    assert j["roofline"]["kernel"] == "ds_spec_kernel" and j["launch"]["variant"] == 2
     fin, fout = j["config"]["in_frame_bytes"], j["config"]["out_frame_bytes"]
     assert j["roofline"]["algorithmic_bytes_per_launch"] == 300 * (fin + fout)
     p = j["parity"]
