@@ -69,6 +69,8 @@ bool spec_geometry_ok(const ds_filter_spec& sp, const ds_plan_info& pi) {
     for (int p = 0; p < pi.n_planes; ++p) {
         if (pi.in_w[p] % 16 != 0 || pi.in_w[p] < 64 || pi.in_w[p] / 16 < 2 * kblk || pi.in_offset[p] % 16 != 0)
             return false;
+        // the row cursor advances up to NW rows per step with one wrap test
+        if (pi.in_h[p] <= DS_SPEC_NW) return false;
         // at most 4 chunks per row may cross the row end (the wrap pass's table)
         const int W = pi.in_w[p], nb16 = W / 16, np = W / sp.h.paving, nch = (np + 3) / 4;
         const int oh = (int)(((int64_t)sp.h.origin % W + W) % W), blk0 = oh / 16;
