@@ -381,7 +381,8 @@ __device__ __forceinline__ void g_v_pass_bytes(const GenStage& g, const int32_t 
 // Producer-warp staging of the `rows` rows (row0 + i) mod H of a plane the
 // TMA cannot copy (unaligned rows or pointer): each staged row is the W row
 // bytes, then the 32-byte wrap pad row[j mod W].  Items (row, word) are walked
-// with incremental indices and loaded kCoopBatch per lane before their stores:
+// with incremental indices (a band of R > H rows wraps more than once: row
+// indices reduce by a loop) and loaded kCoopBatch per lane before their stores:
 // the shared destination and global source may alias as far as the compiler
 // knows, so a plain load-store loop serialises on DRAM latency (SD/QCIF chroma
 // rows are 22-90 words: one round trip per word per row).
@@ -405,7 +406,7 @@ __device__ __forceinline__ void g_coop_rows(uint8_t* dst, int pitch, const uint8
         int r = lane / n, x = lane - (lane / n) * n;
         for (int it = lane; it < total; it += 32) {
             int rr = row0 + r;
-            if (rr >= H) rr -= H;
+            while (rr >= H) rr -= H;
             const uint8_t* src = plane + (int64_t)rr * W + (int64_t)(x < nr ? x : x - nr) * G;
             cp_async_ca(d0 + (uint32_t)(r * pitch + x * G), src, G);
             x += 32;
@@ -415,7 +416,7 @@ __device__ __forceinline__ void g_coop_rows(uint8_t* dst, int pitch, const uint8
             const int pc = lane % W;
             for (int i = 0; i < rows; ++i) {
                 int rr = row0 + i;
-                if (rr >= H) rr -= H;
+                while (rr >= H) rr -= H;
                 dst[(size_t)i * pitch + W + lane] = __ldg(plane + (int64_t)rr * W + pc);
             }
         }
@@ -441,7 +442,7 @@ __device__ __forceinline__ void g_coop_rows(uint8_t* dst, int pitch, const uint8
                 dx[j] = x;
                 if (it0 + 32 * j + lane < total) {
                     int rr = row0 + r;
-                    if (rr >= H) rr -= H;
+                    while (rr >= H) rr -= H;
                     const uint32_t* a = reinterpret_cast<const uint32_t*>(
                         plane + (int64_t)rr * W + 4 * (int64_t)(x < nr ? x : x - nr) - m);
                     lo[j] = __ldg(a);
@@ -459,7 +460,7 @@ __device__ __forceinline__ void g_coop_rows(uint8_t* dst, int pitch, const uint8
             const int pc = lane % W;
             for (int i = 0; i < rows; ++i) {
                 int rr = row0 + i;
-                if (rr >= H) rr -= H;
+                while (rr >= H) rr -= H;
                 dst[(size_t)i * pitch + W + lane] = __ldg(plane + (int64_t)rr * W + pc);
             }
         }
@@ -478,7 +479,7 @@ __device__ __forceinline__ void g_coop_rows(uint8_t* dst, int pitch, const uint8
             dx[j] = x;
             if (it0 + 32 * j + lane < total) {
                 int rr = row0 + r;
-                if (rr >= H) rr -= H;
+                while (rr >= H) rr -= H;
                 const uint8_t* src = plane + (int64_t)rr * W;
                 v[j] = words ? __ldg(reinterpret_cast<const uint32_t*>(src) + x) : (uint32_t)__ldg(src + x);
             }
@@ -501,7 +502,7 @@ __device__ __forceinline__ void g_coop_rows(uint8_t* dst, int pitch, const uint8
         for (int j = 0; j < kCoopBatch; ++j) {
             if (i0 + j < rows) {
                 int rr = row0 + i0 + j;
-                if (rr >= H) rr -= H;
+                while (rr >= H) rr -= H;
                 v[j] = __ldg(plane + (int64_t)rr * W + pc);
             }
         }
@@ -533,7 +534,7 @@ __device__ __forceinline__ void g_coop_windows(uint8_t* dst, int pitch, const ui
             dx[j] = x;
             if (it0 + 32 * j + lane < total) {
                 int rr = row0 + r;
-                if (rr >= H) rr -= H;
+                while (rr >= H) rr -= H;
                 const uint8_t* row = plane + (int64_t)rr * W;
                 int c = cs + 4 * x;
                 while (c >= W) c -= W;
@@ -576,7 +577,7 @@ __device__ __forceinline__ void gc_pads_nt(uint8_t* dst, int pitch, const uint8_
             const int it = it0 + NT * j + t;
             if (it < total) {
                 int rr = row0 + (it >> 5);
-                if (rr >= H) rr -= H;
+                while (rr >= H) rr -= H;
                 const int jc = it & 31;
                 v[j] = __ldg(plane + (int64_t)rr * W + (jc < W ? jc : jc % W));
             }
@@ -604,7 +605,7 @@ __device__ __forceinline__ void gc_rows_nt(uint8_t* dst, int pitch, const uint8_
         int r = t / n, x = t - (t / n) * n;
         for (int it = t; it < total; it += NT) {
             int rr = row0 + r;
-            if (rr >= H) rr -= H;
+            while (rr >= H) rr -= H;
             const uint8_t* src = plane + (int64_t)rr * W + (int64_t)(x < nr ? x : x - nr) * G;
             cp_async_ca(d0 + (uint32_t)(r * pitch + x * G), src, G);
             x += NT;
@@ -633,7 +634,7 @@ __device__ __forceinline__ void gc_rows_nt(uint8_t* dst, int pitch, const uint8_
                 dx[j] = x;
                 if (it0 + NT * j + t < total) {
                     int rr = row0 + r;
-                    if (rr >= H) rr -= H;
+                    while (rr >= H) rr -= H;
                     const uint32_t* a = reinterpret_cast<const uint32_t*>(
                         plane + (int64_t)rr * W + 4 * (int64_t)(x < nr ? x : x - nr) - m);
                     lo[j] = __ldg(a);
@@ -663,7 +664,7 @@ __device__ __forceinline__ void gc_rows_nt(uint8_t* dst, int pitch, const uint8_
             dx[j] = x;
             if (it0 + NT * j + t < total) {
                 int rr = row0 + r;
-                if (rr >= H) rr -= H;
+                while (rr >= H) rr -= H;
                 const uint8_t* src = plane + (int64_t)rr * W;
                 v[j] = words ? __ldg(reinterpret_cast<const uint32_t*>(src) + x) : (uint32_t)__ldg(src + x);
             }
@@ -697,7 +698,7 @@ __device__ __forceinline__ void gc_windows_nt(uint8_t* dst, int pitch, const uin
             dx[j] = x;
             if (it0 + NT * j + t < total) {
                 int rr = row0 + r;
-                if (rr >= H) rr -= H;
+                while (rr >= H) rr -= H;
                 const uint8_t* row = plane + (int64_t)rr * W;
                 int c = cs + 4 * x;
                 while (c >= W) c -= W;

@@ -104,7 +104,9 @@ struct SpecPlaneCfg {
 struct SpecCfg {
     bool valid = false;
     int jit = 0;                   // 0: built-in instance, 1: compiled at run time (NVRTC)
-    SpecFn fn = nullptr;           // kernel entry (runtime-API function, or a JIT CUfunction)
+    SpecFn fn = nullptr;           // kernel entry for the plan's row alignment (runtime-API function, or a JIT CUfunction)
+    SpecFn fn_al[3] = {};          // entries by call row alignment 16 / 8 / 4 (built-in: all up to al; JIT: al only)
+    int al = 16;                   // row alignment of the plan (frame size, plane offsets, widths)
     SpecPlaneCfg plane[DS_MAX_PLANES];
     int32_t upf = 0, stages = 2, stage_stride = 0, mid_stride = 0;
     int threads = 0, smem = 0, grid_per_sm = 0;
@@ -170,7 +172,7 @@ void free_sched_state(ds_handle* h);
 int configure_spec(ds_handle* h);
 bool spec_call_ok(const ds_handle* h, const uint8_t* in, const uint8_t* out);
 int launch_spec(ds_handle* h, const uint8_t* in, int64_t n, uint8_t* out, cudaStream_t st);
-SpecFn spec_jit_kernel(ds_handle* h, int phase);
+SpecFn spec_jit_kernel(ds_handle* h, int phase, int align);
 bool spec_jit_available();
 const char* spec_jit_log();
 int spec_jit_set_smem(SpecFn fn, int smem);

@@ -32,31 +32,71 @@ bool stage_is(const ds_stage_spec& s) {
     return stage_is(s, ST::P, ST::S, ST::Q, ST::D, ST::B, ST::O, &wfn<ST>);
 }
 
-// words of an H chunk window (the HChunk<> constants, from the runtime spec)
-int h_blocks(const ds_stage_spec& h, int ph) {
+// words of an H chunk window (the HChunk<> constants, from the runtime spec):
+// first and last word read from the chunk's first block, 16-byte blocks touched
+void h_words(const ds_stage_spec& h, int ph, int* klo, int* khi) {
     int hi = 0;
     for (int j = 0; j < h.outputs; ++j)
         for (int i = 0; i < h.pattern; ++i)
             if (h.weight[j][i] != 0) hi = std::max(hi, i);
-    return ((ph + 3 * h.paving + hi) / 4 + 1 + 3) / 4;
+    *klo = ph / 4;
+    *khi = (ph + 3 * h.paving + hi) / 4;
 }
+int64_t floor16(int64_t o) { return o >= 0 ? o / 16 : -((-o + 15) / 16); }
+
+int al_index(int al) { return al == 16 ? 0 : al == 8 ? 1 : 2; }
 
 }  // namespace
 
-// Built-in instances: (stage types, window phase) -> kernel.  The phase of a
-// spec is its H origin mod 16 (every eligible plane has W % 16 == 0).
-SpecFn spec_builtin(const ds_filter_spec& sp) {
-    if (stage_is<dss::HaloH>(sp.h) && stage_is<dss::HaloV>(sp.v))
-        return reinterpret_cast<SpecFn>(&dss::ds_spec_kernel<dss::HaloH, dss::HaloV, (dss::HaloH::O % 16 + 16) % 16>);
-    if (stage_is<dss::SpecH>(sp.h) && stage_is<dss::SpecV>(sp.v))
-        return reinterpret_cast<SpecFn>(&dss::ds_spec_kernel<dss::SpecH, dss::SpecV, (dss::SpecH::O % 16 + 16) % 16>);
+// The H origin of a plane reduced to (-W/2, W/2]: window bytes are taken mod W
+// (S:251), so this is the same filter, and the windows of every chunk not
+// crossing the row end start at this value's phase mod 16.
+int64_t spec_h_origin(int64_t origin, int64_t W) {
+    int64_t o = (origin % W + W) % W;
+    if (o > W / 2) o -= W;
+    return o;
+}
+
+// The window phase every plane shares (the instance's PH), or -1.
+int spec_phase(const ds_filter_spec& sp, const ds_plan_info& pi) {
+    int ph = -1;
+    for (int p = 0; p < pi.n_planes; ++p) {
+        const int q = (int)((spec_h_origin(sp.h.origin, pi.in_w[p]) % 16 + 16) % 16);
+        if (ph >= 0 && q != ph) return -1;
+        ph = q;
+    }
+    return ph;
+}
+
+// Alignment (16, 8 or 4; 0: none) of every row start of a frame-aligned call:
+// frame size, plane offsets and row widths.
+int spec_plan_align(const ds_plan_info& pi) {
+    int64_t a = pi.in_frame_bytes;
+    for (int p = 0; p < pi.n_planes; ++p) a |= pi.in_offset[p] | pi.in_w[p];
+    return a % 16 == 0 ? 16 : a % 8 == 0 ? 8 : a % 4 == 0 ? 4 : 0;
+}
+
+// Built-in instances: (stage types, window phase, row alignment) -> kernel.
+SpecFn spec_builtin(const ds_filter_spec& sp, int ph, int al) {
+    auto pick = [al](auto k16, auto k8, auto k4) {
+        return al == 16 ? reinterpret_cast<SpecFn>(k16) : al == 8 ? reinterpret_cast<SpecFn>(k8) : reinterpret_cast<SpecFn>(k4);
+    };
+    constexpr int kHaloPh = (dss::HaloH::O % 16 + 16) % 16, kSpecPh = (dss::SpecH::O % 16 + 16) % 16;
+    if (ph == kHaloPh && stage_is<dss::HaloH>(sp.h) && stage_is<dss::HaloV>(sp.v))
+        return pick(&dss::ds_spec_kernel<dss::HaloH, dss::HaloV, kHaloPh, 16>,
+                    &dss::ds_spec_kernel<dss::HaloH, dss::HaloV, kHaloPh, 8>,
+                    &dss::ds_spec_kernel<dss::HaloH, dss::HaloV, kHaloPh, 4>);
+    if (ph == kSpecPh && stage_is<dss::SpecH>(sp.h) && stage_is<dss::SpecV>(sp.v))
+        return pick(&dss::ds_spec_kernel<dss::SpecH, dss::SpecV, kSpecPh, 16>,
+                    &dss::ds_spec_kernel<dss::SpecH, dss::SpecV, kSpecPh, 8>,
+                    &dss::ds_spec_kernel<dss::SpecH, dss::SpecV, kSpecPh, 4>);
     return nullptr;
 }
 
 // Geometry K-N1s can run, independent of pointers: H paving a multiple of 4
-// (a chunk of 4 repetitions starts on a 16-byte block), taps in s8 (dp4a),
-// every plane W % 16 == 0 (one window phase for all planes and strips, rows
-// TMA-copyable), at most DS_SPEC_MAXP planes.
+// (a chunk of 4 repetitions starts on a 16-byte block of its window), taps in
+// s8 (dp4a), rows 4-byte aligned within the frame (W % 4 == 0 follows from
+// W % Sh == 0), one window phase for all planes, at most DS_SPEC_MAXP planes.
 bool spec_geometry_ok(const ds_filter_spec& sp, const ds_plan_info& pi) {
     if (sp.h.paving % 4 != 0 || pi.n_planes > DS_SPEC_MAXP) return false;
     for (const ds_stage_spec* s : {&sp.h, &sp.v})
@@ -64,25 +104,28 @@ bool spec_geometry_ok(const ds_filter_spec& sp, const ds_plan_info& pi) {
             for (int i = 0; i < s->pattern; ++i)
                 if (s->weight[j][i] < -128 || s->weight[j][i] > 127) return false;
     if (sp.h.pattern > 16 || sp.v.pattern > 16) return false;
-    const int ph = (int)(((int64_t)sp.h.origin % 16 + 16) % 16);
-    const int kblk = h_blocks(sp.h, ph);
+    if (spec_plan_align(pi) == 0) return false;
+    const int ph = spec_phase(sp, pi);
+    if (ph < 0) return false;
+    int klo, khi;
+    h_words(sp.h, ph, &klo, &khi);
+    const int kblk = (khi + 4) / 4;
     for (int p = 0; p < pi.n_planes; ++p) {
-        if (pi.in_w[p] % 16 != 0 || pi.in_w[p] < 64 || pi.in_w[p] / 16 < 2 * kblk || pi.in_offset[p] % 16 != 0)
-            return false;
+        const int W = pi.in_w[p];
+        if (W < 64 || W / 16 < 2 * kblk) return false;
         // the row cursor advances up to NW rows per step with one wrap test
         if (pi.in_h[p] <= DS_SPEC_NW) return false;
         // at most 4 chunks per row may cross the row end (the wrap pass's table)
-        const int W = pi.in_w[p], nb16 = W / 16, np = W / sp.h.paving, nch = (np + 3) / 4;
-        const int oh = (int)(((int64_t)sp.h.origin % W + W) % W), blk0 = oh / 16;
+        const int np = W / sp.h.paving, nch = (np + 3) / 4;
+        const int64_t blk0 = floor16(spec_h_origin(sp.h.origin, W));
         int nwc = 0;
         for (int c = 0; c < nch; ++c) {
-            int Bc = blk0 + (sp.h.paving / 4) * c;
-            if (Bc >= nb16) Bc -= nb16;
-            nwc += Bc + kblk > nb16;
+            const int64_t B = blk0 + (sp.h.paving / 4) * c;
+            nwc += !(16 * B + 4 * klo >= 0 && 16 * B + 4 * (khi + 1) <= W);
         }
         if (nwc > 4) return false;
     }
-    return pi.in_frame_bytes % 16 == 0;
+    return true;
 }
 
 // Per-plane plan: bands of k V repetitions (the first band of a run stages
@@ -130,8 +173,12 @@ int configure_spec(ds_handle* h) {
     const ds_filter_spec& sp = h->spec;
     h->spec_cfg = c;
     if (!spec_geometry_ok(sp, pi)) return DS_OK;
-    const int ph = (int)(((int64_t)sp.h.origin % 16 + 16) % 16);
-    SpecFn fn = spec_builtin(sp);
+    const int ph = spec_phase(sp, pi), al = spec_plan_align(pi);
+    c.al = al;
+    // built-in: an instance for the plan's row alignment and each lower one
+    // (calls whose input pointer is less aligned than the plan)
+    for (int a = al; a >= 4; a /= 2) c.fn_al[al_index(a)] = spec_builtin(sp, ph, a);
+    SpecFn fn = c.fn_al[al_index(al)];
     c.jit = 0;
     if (!fn) {
         // no built-in instance: compile one at run time (NVRTC, ~0.3 s once per
@@ -139,7 +186,8 @@ int configure_spec(ds_handle* h) {
         // kernel unless ds_set_general_variant(DS_GENERAL_COMPILED) asks for it
         const char* env = getenv("DS_SPEC_JIT");
         if (!h->spec_jit_req && env && env[0] == '0') return DS_OK;
-        fn = spec_jit_kernel(h, ph);                                   // nullptr when NVRTC is unavailable
+        fn = spec_jit_kernel(h, ph, al);                               // nullptr when NVRTC is unavailable
+        c.fn_al[al_index(al)] = fn;                                    // the plan's alignment only
         c.jit = 1;
     }
     if (!fn) return DS_OK;
@@ -162,11 +210,12 @@ int configure_spec(ds_handle* h) {
     if (c.jit) {
         if (spec_jit_set_smem(fn, c.smem) || spec_jit_occupancy(fn, c.threads, c.smem, &occ) || occ < 1) return DS_OK;
     } else {
-        if (cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 c.smem) != cudaSuccess) {
-            cudaGetLastError();
-            return DS_OK;
-        }
+        for (SpecFn f : c.fn_al)
+            if (f && cudaFuncSetAttribute(reinterpret_cast<const void*>(f), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          c.smem) != cudaSuccess) {
+                cudaGetLastError();
+                return DS_OK;
+            }
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, reinterpret_cast<const void*>(fn), c.threads, c.smem) !=
                 cudaSuccess ||
             occ < 1) {
@@ -222,12 +271,20 @@ void spec_runs(const ds_handle* h, int64_t n, int32_t* L, int32_t* upf) {
     *upf = u;
 }
 
-// Pointer conditions of one call: TMA needs a 16-byte aligned input.
+// Instance for one call: the plan's row alignment lowered to the input
+// pointer's (16, 8 or 4 bytes); nullptr when there is none (a pointer not
+// 4-byte aligned, or a run-time compiled spec whose one instance needs more).
+SpecFn spec_call_fn(const ds_handle* h, const uint8_t* in) {
+    const SpecCfg& c = h->spec_cfg;
+    if (!c.valid) return nullptr;
+    int a = c.al;
+    while (a >= 4 && (reinterpret_cast<uintptr_t>(in) & (uintptr_t)(a - 1)) != 0) a /= 2;
+    return a >= 4 ? c.fn_al[al_index(a)] : nullptr;
+}
+
 bool spec_call_ok(const ds_handle* h, const uint8_t* in, const uint8_t* out) {
-    if (!h->spec_cfg.valid) return false;
-    const ds_plan_info& pi = h->plan;
     (void)out;   // any output alignment: rows take 4-, 2- or 1-byte stores by their alignment
-    return (reinterpret_cast<uintptr_t>(in) & 15) == 0 && pi.in_frame_bytes % 16 == 0;
+    return spec_call_fn(h, in) != nullptr;
 }
 
 int launch_spec(ds_handle* h, const uint8_t* in, int64_t n, uint8_t* out, cudaStream_t st) {
@@ -256,7 +313,7 @@ int launch_spec(ds_handle* h, const uint8_t* in, int64_t n, uint8_t* out, cudaSt
         P.W = pi.in_w[q];
         P.H = pi.in_h[q];
         P.Wout = pi.out_w[q];
-        P.oh = (int32_t)(((int64_t)sp.h.origin % P.W + P.W) % P.W);
+        P.oh = (int32_t)spec_h_origin(sp.h.origin, P.W);
         P.ov = (int32_t)(((int64_t)sp.v.origin % P.H + P.H) % P.H);
         P.np = P.W / sp.h.paving;
         P.nch = (P.np + 3) / 4;
@@ -264,14 +321,14 @@ int launch_spec(ds_handle* h, const uint8_t* in, int64_t n, uint8_t* out, cudaSt
         P.lgsegs = 0;
         while ((1 << P.lgsegs) < P.segs) ++P.lgsegs;
         P.nb16 = P.W / 16;
-        P.blk0 = P.oh / 16;
-        // chunks whose kBlk-block window crosses the row end
-        const int kblk = h_blocks(sp.h, (int)(((int64_t)sp.h.origin % 16 + 16) % 16));
+        P.blk0 = (int32_t)floor16(P.oh);
+        // chunks whose window words are not all inside the row (wrap pass)
+        int klo, khi;
+        h_words(sp.h, (int)((P.oh % 16 + 16) % 16), &klo, &khi);
         P.nwc = 0;
         for (int c = 0; c < P.nch; ++c) {
-            int Bc = P.blk0 + (sp.h.paving / 4) * c;
-            if (Bc >= P.nb16) Bc -= P.nb16;
-            if (Bc + kblk > P.nb16) {
+            const int64_t B = P.blk0 + (sp.h.paving / 4) * c;
+            if (!(16 * B + 4 * klo >= 0 && 16 * B + 4 * (khi + 1) <= P.W)) {
                 if (P.nwc == 4) return DS_EUNSUPPORTED;         // configure_spec rules this out
                 P.wch[P.nwc++] = c;
             }
@@ -290,9 +347,11 @@ int launch_spec(ds_handle* h, const uint8_t* in, int64_t n, uint8_t* out, cudaSt
         if (pi.out_offset[q] % 4 || pi.out_w[q] % 4) p.out_al4 = 0;
     if (p.n_units == 0) return DS_OK;
     const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(p.n_units, (int64_t)c.grid_per_sm * h->sm_count));
+    const SpecFn fn = spec_call_fn(h, in);
+    if (!fn) return DS_EUNSUPPORTED;                                  // run_device checked spec_call_ok
     void* args[] = {&p};
-    if (c.jit) return spec_jit_launch(c.fn, (unsigned)grid, (unsigned)c.threads, (unsigned)c.smem, st, args);
-    if (cudaLaunchKernel(reinterpret_cast<const void*>(c.fn), dim3((unsigned)grid), dim3(c.threads), args,
+    if (c.jit) return spec_jit_launch(fn, (unsigned)grid, (unsigned)c.threads, (unsigned)c.smem, st, args);
+    if (cudaLaunchKernel(reinterpret_cast<const void*>(fn), dim3((unsigned)grid), dim3(c.threads), args,
                          (size_t)c.smem, st) != cudaSuccess) {
         cudaGetLastError();
         return DS_ECUDA;

@@ -73,12 +73,12 @@ namespace dss {
 struct SpecPlane {
     int64_t in_off, out_off;   // plane offsets inside one frame
     int32_t W, H, Wout;        // input row bytes, rows, output row bytes
-    int32_t oh, ov;            // H / V origins reduced mod W / H (>= 0)
+    int32_t oh, ov;            // H origin reduced to (-W/2, W/2]; V origin reduced mod H (>= 0)
     int32_t np;                // H repetitions per row (W / Sh)
     int32_t nch;               // chunks of 4 repetitions per row: ceil(np / 4)
     int32_t segs, lgsegs;      // 32-chunk warp segments per row: ceil(nch / 32), a power of two; log2
     int32_t nwc, wch[4];       // chunks whose window crosses the row end (wrap pass)
-    int32_t nb16, blk0;        // W / 16; oh / 16 (first window block of repetition 0)
+    int32_t nb16, blk0;        // W / 16 (floor); floor(oh / 16): first window block of repetition 0 (may be < 0)
     int32_t k, nb;             // V repetitions per band, bands per plane ((H / Sv) / k)
     int32_t L;                 // bands per run (a unit); the V halo's mid rows carry over
     int32_t nq;                // intermediate column quads: ceil(Qh np / 4)
@@ -283,6 +283,12 @@ __device__ __forceinline__ void sts32(uint32_t a, uint32_t v) {
 __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
+// the 16-byte aligned part of a range (the bulk prefetch needs 16-byte
+// aligned addresses and sizes; rows of AL < 16 calls lose at most 15 + 15 bytes)
+__device__ __forceinline__ void prefetch_range(const uint8_t* p, uint32_t bytes) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(p), s = (a + 15) & ~(uintptr_t)15, e = (a + bytes) & ~(uintptr_t)15;
+    if (e > s) prefetch_l2(reinterpret_cast<const void*>(s), (uint32_t)(e - s));
+}
 __device__ __forceinline__ void ldg128(const uint8_t* p, uint32_t& x, uint32_t& y, uint32_t& z, uint32_t& w) {
     asm volatile("ld.global.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(x), "=r"(y), "=r"(z), "=r"(w) : "l"(p));
 }
@@ -307,58 +313,64 @@ __device__ __forceinline__ void stg8(uint8_t* p, uint32_t v) {
 
 // ------------------------------------------------------------- the H pass --
 // One lane: a chunk = 4 consecutive H repetitions r1 = 4c .. 4c+3 of one row.
-// Their windows start at bytes oh + Sh r1; relative to the chunk's first
-// 16-byte block B = blk0 + (Sh / 4) c that is PH + Sh m (PH = oh mod 16, a
-// compile-time constant of the instance).  The lane loads exactly the words
-// any live tap reads (16-, 8- or 4-byte loads by word runs), then every output
-// is a dp4a per aligned word with a nonzero re-indexed weight word.
-template <class HS, int PH>
+// Their windows start at bytes o + Sh r1 (o: the plane's H origin reduced to
+// (-W/2, W/2]); relative to the chunk's first 16-byte block B = floor(o / 16)
+// + (Sh / 4) c that is PH + Sh m (PH = o mod 16, a compile-time constant of
+// the instance).  The lane loads exactly the words any live tap reads (loads
+// of up to AL bytes by word runs: AL = 16, 8 or 4 is the alignment of every
+// row start in the call), then every output is a dp4a per aligned word with a
+// nonzero re-indexed weight word.
+template <class HS, int PH, int AL = 16>
 struct HChunk {
     using I = StageInfo<HS>;
+    static_assert(AL == 16 || AL == 8 || AL == 4, "row alignment 16, 8 or 4");
     static constexpr int kLo = PH / 4;                                   // first word read
     static constexpr int kHi = (PH + 3 * HS::S + I::hi_tap()) / 4;       // last word read
     static constexpr int kWords = kHi + 1;                               // words from B's start
     static constexpr int kBlk = (kWords + 3) / 4;                        // 16-byte blocks touched
     static_assert(kBlk <= 8, "H window too wide for the compiled H pass");
 
-    // x: words kLo .. kHi of the window (others untouched), from the chunk's
-    // blocks B .. B + kBlk - 1 of the row (B < nb16).  WRAP: the window
-    // crosses the row end, so block indices wrap mod nb16.
-    template <bool WRAP>
-    __device__ __forceinline__ static void load(const uint8_t* row, int B, int nb16, uint32_t (&x)[4 * kBlk]) {
-        const uint8_t* base = row + 16 * B;
-        sfor<0, kBlk>([&](auto b) {
-            constexpr int w0 = 4 * decltype(b)::value, wlo = w0 > kLo ? w0 : kLo, whi = w0 + 3 < kHi ? w0 + 3 : kHi;
-            const uint8_t* a = base + 16 * decltype(b)::value;
-            if constexpr (WRAP) {
+    // x: words kLo .. kHi of the window whose block 0 is block B of the row
+    // (B may be negative or run past the row end; others untouched), taken mod
+    // W.  Used by the wrap pass for the few chunks per row whose window
+    // crosses the row end.  16-byte rows (AL = 16): whole blocks mod W / 16;
+    // else word by word (W % 4 == 0, so no word straddles the row end).
+    __device__ __forceinline__ static void load_wrap(const uint8_t* row, int B, int W, uint32_t (&x)[4 * kBlk]) {
+        if constexpr (AL == 16) {
+            const int nb16 = W >> 4;
+            sfor<0, kBlk>([&](auto b) {
+                constexpr int w0 = 4 * decltype(b)::value, wlo = w0 > kLo ? w0 : kLo, whi = w0 + 3 < kHi ? w0 + 3 : kHi;
                 int blk = B + decltype(b)::value;
-                if (blk >= nb16) blk -= nb16;
-                a = row + 16 * blk;
-            }
-            if constexpr (wlo == w0 && whi == w0 + 3) {
-                ldg128(a, x[w0], x[w0 + 1], x[w0 + 2], x[w0 + 3]);
-            } else if constexpr (whi >= wlo) {
-                sfor<wlo - w0, whi - w0 + 1>([&](auto t) {
-                    constexpr int w = w0 + decltype(t)::value;
-                    if constexpr ((w & 1) == 0 && w + 1 <= whi) ldg64(a + 4 * decltype(t)::value, x[w], x[w + 1]);
-                    else if constexpr ((w & 1) == 1 && w - 1 >= wlo) { /* loaded with w - 1 */ }
-                    else x[w] = ldg32(a + 4 * decltype(t)::value);
-                });
-            }
-        });
+                if (blk < 0) blk += nb16;
+                else if (blk >= nb16) blk -= nb16;
+                const uint8_t* a = row + 16 * blk;
+                if constexpr (wlo == w0 && whi == w0 + 3) {
+                    ldg128(a, x[w0], x[w0 + 1], x[w0 + 2], x[w0 + 3]);
+                } else if constexpr (whi >= wlo) {
+                    sfor<wlo - w0, whi - w0 + 1>([&](auto t) { x[w0 + decltype(t)::value] = ldg32(a + 4 * decltype(t)::value); });
+                }
+            });
+        } else {
+            sfor<kLo, kHi + 1>([&](auto w) {
+                int off = 16 * B + 4 * decltype(w)::value;
+                if (off < 0) off += W;
+                else if (off >= W) off -= W;
+                x[decltype(w)::value] = ldg32(row + off);
+            });
+        }
     }
     // the same words from a base pointer to the chunk's first block (no wrap)
     __device__ __forceinline__ static void load_at(const uint8_t* base, uint32_t (&x)[4 * kBlk]) {
         sfor<0, kBlk>([&](auto b) {
             constexpr int w0 = 4 * decltype(b)::value, wlo = w0 > kLo ? w0 : kLo, whi = w0 + 3 < kHi ? w0 + 3 : kHi;
             const uint8_t* a = base + 16 * decltype(b)::value;
-            if constexpr (wlo == w0 && whi == w0 + 3) {
+            if constexpr (AL == 16 && wlo == w0 && whi == w0 + 3) {
                 ldg128(a, x[w0], x[w0 + 1], x[w0 + 2], x[w0 + 3]);
             } else if constexpr (whi >= wlo) {
                 sfor<wlo - w0, whi - w0 + 1>([&](auto t) {
                     constexpr int w = w0 + decltype(t)::value;
-                    if constexpr ((w & 1) == 0 && w + 1 <= whi) ldg64(a + 4 * decltype(t)::value, x[w], x[w + 1]);
-                    else if constexpr ((w & 1) == 1 && w - 1 >= wlo) { /* loaded with w - 1 */ }
+                    if constexpr (AL >= 8 && (w & 1) == 0 && w + 1 <= whi) ldg64(a + 4 * decltype(t)::value, x[w], x[w + 1]);
+                    else if constexpr (AL >= 8 && (w & 1) == 1 && w - 1 >= wlo) { /* loaded with w - 1 */ }
                     else x[w] = ldg32(a + 4 * decltype(t)::value);
                 });
             }
@@ -463,11 +475,11 @@ struct VQuad {
 };
 
 // ------------------------------------------------------------ the kernel --
-template <class HS, class VS, int PH>
+template <class HS, class VS, int PH, int AL>
 __global__ void __launch_bounds__(DS_SPEC_NW * 32, DS_SPEC_MINB) ds_spec_kernel(const __grid_constant__ SpecParams p) {
     constexpr int NW = DS_SPEC_NW, NT = NW * 32;
     static_assert(HS::S % 4 == 0, "a chunk of 4 H repetitions must start on a 16-byte block");
-    using HC = HChunk<HS, PH>;
+    using HC = HChunk<HS, PH, AL>;
     extern __shared__ __align__(128) uint8_t smem[];
     const uint32_t mid0 = smem_u32(smem);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -494,8 +506,8 @@ __global__ void __launch_bounds__(DS_SPEC_NW * 32, DS_SPEC_MINB) ds_spec_kernel(
         int r0 = (int)(((int64_t)Q.ov + (int64_t)VS::S * Q.k * bnd + reuse_) % Q.H);
         const uint8_t* pl_ = p.in + f_ * p.in_frame + Q.in_off;
         const int n1 = min(rows_, Q.H - r0);
-        prefetch_l2(pl_ + (int64_t)r0 * Q.W, (uint32_t)n1 * (uint32_t)Q.W);
-        if (rows_ > n1) prefetch_l2(pl_, (uint32_t)min(rows_ - n1, Q.H) * (uint32_t)Q.W);
+        prefetch_range(pl_ + (int64_t)r0 * Q.W, (uint32_t)n1 * (uint32_t)Q.W);
+        if (rows_ > n1) prefetch_range(pl_, (uint32_t)min(rows_ - n1, Q.H) * (uint32_t)Q.W);
     };
     if (tid == 0 && u < p.n_units) prefetch_band(f, local, 0);
 
@@ -522,9 +534,9 @@ __global__ void __launch_bounds__(DS_SPEC_NW * 32, DS_SPEC_MINB) ds_spec_kernel(
         // small wrap pass, so the main loop has no per-block index arithmetic.
         const int seg = warp & (P.segs - 1), step = NW >> P.lgsegs;
         const int ch = seg * 32 + lane;
-        int B = P.blk0 + (HS::S / 4) * (ch < P.nch ? ch : P.nch - 1);
-        if (B >= P.nb16) B -= P.nb16;
-        const bool act = ch < P.nch && B + HC::kBlk <= P.nb16;
+        // the chunk's window words inside the row: the main loop's; else the wrap pass's
+        int B = P.blk0 + (HS::S / 4) * ch;
+        const bool act = ch < P.nch && 16 * B + 4 * HC::kLo >= 0 && 16 * B + 4 * (HC::kHi + 1) <= P.W;
         if (!act) B = P.nb16 - HC::kBlk;                            // in-bounds loads, result unused
         const int i0 = warp >> P.lgsegs;
         // issue cursor: a 32-bit byte offset of the lane's window in the plane
@@ -621,10 +633,8 @@ __global__ void __launch_bounds__(DS_SPEC_NW * 32, DS_SPEC_MINB) ds_spec_kernel(
                 const int i = it / P.nwc, c = P.wch[it - i * P.nwc];
                 int r = row0 + i;
                 while (r >= P.H) r -= P.H;
-                int Bw = P.blk0 + (HS::S / 4) * c;
-                if (Bw >= P.nb16) Bw -= P.nb16;
                 uint32_t xw[4 * HC::kBlk], o[HS::Q];
-                HC::template load<true>(plane + (int64_t)r * P.W, Bw, P.nb16, xw);
+                HC::load_wrap(plane + (int64_t)r * P.W, P.blk0 + (HS::S / 4) * c, P.W, xw);
                 HC::compute(xw, o);
                 const uint32_t mo = mid + (reuse + i) * mp + 4 * HS::Q * c;
                 sfor<0, HS::Q>([&](auto w) { sts32(mo + 4 * decltype(w)::value, o[decltype(w)::value]); });

@@ -142,9 +142,10 @@ bool spec_jit_available() {
 
 const char* spec_jit_log() { return g_last_log.c_str(); }
 
-// Compile (or fetch from the cache) K-N1s for the handle's spec and window
-// phase on the current device.  Returns a CUfunction as SpecFn, or nullptr.
-SpecFn spec_jit_kernel(ds_handle* h, int phase) {
+// Compile (or fetch from the cache) K-N1s for the handle's spec, window phase
+// and row alignment on the current device.  Returns a CUfunction as SpecFn, or
+// nullptr.
+SpecFn spec_jit_kernel(ds_handle* h, int phase, int align) {
     std::lock_guard<std::mutex> lk(g_mu);
     init_locked();
     if (!g_nvrtc.ok || !g_drv.ok) {
@@ -169,7 +170,7 @@ SpecFn spec_jit_kernel(ds_handle* h, int phase) {
     src += stage_source("JitV", h->spec.v);
     src += "}  // namespace dss\n";
     char name[96];
-    std::snprintf(name, sizeof name, "&dss::ds_spec_kernel<dss::JitH, dss::JitV, %d>", phase);
+    std::snprintf(name, sizeof name, "&dss::ds_spec_kernel<dss::JitH, dss::JitV, %d, %d>", phase, align);
     char arch[64];
     std::snprintf(arch, sizeof arch, "--gpu-architecture=sm_%d%d%s", major, minor, major >= 9 ? "a" : "");
     const std::string key = std::to_string(h->device) + "|" + arch + "|" + name + "|" + src;

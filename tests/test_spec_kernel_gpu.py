@@ -3,8 +3,10 @@ compiled in.  Byte-for-byte against the CPU oracle (O1 with the spec's
 stages, halos wrap toroidally) and against the runtime-tap
 K-N1g on the same inputs: the bench's halo spec and SPEC's downscaler on the
 paper's and BASELINE's geometries, column strips, ragged chunk tails, every
-unit processed once, every output byte written, and the fallbacks (a
-misaligned output row or input pointer runs the runtime-tap kernel)."""
+unit processed once, every output byte written, rows and input pointers
+aligned to 8 or 4 bytes only, and the fallbacks (an input pointer not 4-byte
+aligned, or planes without a common window phase, run the runtime-tap
+kernel)."""
 import numpy as np
 import pytest
 
@@ -108,26 +110,87 @@ def test_auto_picks_compiled_variant_and_falls_back():
         torch.cuda.synchronize()
         assert d.last_variant() == 2
         _same(yo.cpu().numpy(), want, f"output offset {off}")
-    # input 16-byte misaligned: runtime-tap K-N1g stages the rows itself
+    # input pointer 4- or 8-byte aligned: K-N1s with 4- / 8-byte loads; not
+    # 4-byte aligned: runtime-tap K-N1g stages the rows itself
     xb = torch.zeros(n * d.in_frame_bytes + 16, dtype=torch.uint8, device="cuda")
-    xi = xb[4:4 + n * d.in_frame_bytes]
-    xi.copy_(x.view(-1))
-    y3 = d(xi.view(n, -1))
-    torch.cuda.synchronize()
-    assert d.last_variant() == 1
-    _same(y3.cpu().numpy(), want, "misaligned in")
+    for off, variant in ((4, 2), (8, 2), (12, 2), (1, 1), (2, 1), (7, 1)):
+        xi = xb[off:off + n * d.in_frame_bytes]
+        xi.copy_(x.view(-1))
+        y3 = d(xi.view(n, -1))
+        torch.cuda.synchronize()
+        assert d.last_variant() == variant, off
+        _same(y3.cpu().numpy(), want, f"input offset {off}")
 
 
 def test_compiled_variant_rejected_where_it_cannot_run():
-    # W % 16 != 0 planes (SD chroma 360): no K-N1s plan
-    d = _handle(720, 576, 3, 1, HALO)
+    # QCIF chroma rows (88 B) are narrower than two 13-tap H windows: no K-N1s plan
+    d = _handle(176, 144, 3, 1, HALO)
     with pytest.raises(ds.DSError):
         d.set_general_variant(ds.DS_GENERAL_COMPILED)
-    fr = synth.random_frames(2, 0, 2, 720, 576)
+    fr = synth.random_frames(2, 0, 2, 176, 144)
     y = d(torch.from_numpy(fr).cuda())
     torch.cuda.synchronize()
     assert d.last_variant() == 1
-    _same(y.cpu().numpy(), _want(fr, 720, 576, 3, 1, HALO), "SD halo runtime taps")
+    _same(y.cpu().numpy(), _want(fr, 176, 144, 3, 1, HALO), "QCIF halo runtime taps")
+
+
+@pytest.mark.parametrize("spec", ["halo", "spec"])
+@pytest.mark.parametrize("W,H,ch,chroma,n", [(720, 576, 3, 1, 4), (720, 288, 3, 1, 3), (360, 288, 1, 1, 5),
+                                             (1400, 198, 3, 0, 2)])
+def test_compiled_spec_rows_8_byte_aligned(spec, W, H, ch, chroma, n):
+    """Rows that are not 16-byte multiples (PAL / NTSC SD chroma: 360 B; a
+    360-wide luma plane; 1400 = 87.5 blocks): K-N1s with 8-byte loads, the
+    windows crossing the row end computed word by word."""
+    sp = HALO if spec == "halo" else None
+    d = _handle(W, H, ch, chroma, sp)
+    d.set_general_variant(ds.DS_GENERAL_COMPILED)
+    fr = synth.random_frames(31, 2, n, W, H, ch, chroma)
+    x = torch.from_numpy(fr).cuda()
+    y = d(x)
+    torch.cuda.synchronize()
+    assert d.last_variant() == 2
+    want = _want(fr, W, H, ch, chroma, sp)
+    _same(y.cpu().numpy(), want, f"K-N1s {spec} {W}x{H}")
+    # and from a 4-byte aligned pointer (4-byte loads)
+    xb = torch.zeros(x.numel() + 16, dtype=torch.uint8, device="cuda")
+    xi = xb[4:4 + x.numel()]
+    xi.copy_(x.view(-1))
+    y2 = d(xi.view(n, -1))
+    torch.cuda.synchronize()
+    assert d.last_variant() == 2
+    _same(y2.cpu().numpy(), want, f"K-N1s {spec} {W}x{H} input offset 4")
+
+
+@pytest.mark.parametrize("W,H", [(88, 72), (104, 72), (88, 36), (136, 90)])
+def test_runtime_taps_band_taller_than_plane(W, H):
+    """Planes whose rows the TMA cannot copy (W % 16 == 8) are staged by the
+    producer warp; when one band plus its V halo has more rows than the plane
+    (QCIF chroma: 77 > 72 rows), the halo rows wrap past the plane bottom
+    more than once.  Runtime taps and compiled spec, both exact."""
+    fr = synth.random_frames(12, 0, 3, W, H, 1, 1)
+    want = _want(fr, W, H, 1, 1, HALO)
+    d = _handle(W, H, 1, 1, HALO)
+    x = torch.from_numpy(fr).cuda()
+    for variant in (ds.DS_GENERAL_RUNTIME, ds.DS_GENERAL_AUTO):
+        d.set_general_variant(variant)
+        y = d(x)
+        torch.cuda.synchronize()
+        _same(y.cpu().numpy(), want, f"{W}x{H} variant {d.last_variant()}")
+
+
+def test_compiled_spec_planes_with_different_window_phases_fall_back():
+    """An H origin of 200 reduces to 200 on 720-byte luma rows (phase 8) and
+    to -160 on 360-byte chroma rows (phase 0): one compiled instance cannot
+    serve both planes, so the runtime-tap kernel runs; results exact."""
+    sp = (dict(HALO[0], origin=200), HALO[1])
+    d = _handle(720, 576, 3, 1, sp)
+    with pytest.raises(ds.DSError):
+        d.set_general_variant(ds.DS_GENERAL_COMPILED)
+    fr = synth.random_frames(4, 0, 2, 720, 576)
+    y = d(torch.from_numpy(fr).cuda())
+    torch.cuda.synchronize()
+    assert d.last_variant() == 1
+    _same(y.cpu().numpy(), _want(fr, 720, 576, 3, 1, sp), "phase mismatch")
 
 
 def test_compiled_spec_every_unit_once_and_every_byte_written():
@@ -188,7 +251,8 @@ OTHER = (
 
 
 @pytest.mark.parametrize("spec,W,H,chroma", [("other", 1920, 1080, 1), ("other", 352, 288, 1),
-                                            ("negative", 704, 576, 0), ("odd_divisor", 1024, 144, 1)])
+                                            ("negative", 704, 576, 0), ("odd_divisor", 1024, 144, 1),
+                                            ("other", 720, 576, 1), ("negative", 1400, 198, 0)])
 def test_run_time_compiled_spec(spec, W, H, chroma):
     """A spec without a built-in instance: ds_set_general_variant(COMPILED)
     compiles K-N1s for it at run time (NVRTC, from the same kernel source);
