@@ -376,6 +376,53 @@ def test_general_kernel_fuzz_random_specs():
     assert compiled >= 1
 
 
+def test_general_kernel_fuzz_unaligned_geometry():
+    """Random specs on geometries the TMA cannot stage (any W % 16, planes
+    shorter than one band plus its halo) from input pointers 0-15 bytes into
+    their allocation: K-N1g (producer- or consumer-staged rows) and, where it
+    can run (H paving % 4 == 0, rows 4-byte aligned), K-N1s with 16-, 8- or
+    4-byte loads -- against the oracle."""
+    rng = np.random.default_rng(fuzz_seed(77))
+    checked = compiled = 0
+    for trial in range(40 * FUZZ_SCALE):
+        hd, vd = _random_spec(rng)
+        if rng.random() < 0.5:                       # a paving K-N1s can take
+            hd["paving"] = int(rng.choice([4, 8, 12]))
+        ch = int(rng.choice([1, 3]))
+        chroma = int(rng.integers(0, 2))
+        sub = 2 if ch == 3 and chroma == 1 else 1
+        mult_w = hd["paving"] * sub
+        mult_h = vd["paving"] * sub
+        W = mult_w * int(rng.integers(max(1, 32 // mult_w), max(2, 400 // mult_w + 1)))
+        H = mult_h * int(rng.integers(1, max(2, 40 // mult_h + 1)))
+        spec = ds.make_spec(h=hd, v=vd, chroma=chroma)
+        d = ds.Downscaler(W, H, ch, spec=spec)
+        if not d.plan.fused_general_eligible:
+            continue
+        n = int(rng.integers(1, 4))
+        fr = synth.random_frames(trial, 0, n, W, H, ch, chroma)
+        want = oracle.execute_frames(fr, W, H, ch, chroma, _oracle_stage(hd), _oracle_stage(vd))
+        d.set_run_bands(int(rng.choice([0, 1, 2, 1 << 20])))
+        d.set_kernel(ds.DS_KERNEL_FUSED_GENERAL)
+        off = int(rng.choice([0, 4, 8, 12, 1, 2, 3, 5]))
+        buf = torch.zeros(fr.size + 32, dtype=torch.uint8, device="cuda")
+        x = buf[off:off + fr.size].view(n, -1)
+        x.copy_(torch.from_numpy(fr).view(n, -1))
+        what = f"unaligned fuzz {trial}: {W}x{H}x{ch}/{chroma} off {off} h={hd} v={vd}"
+        for variant in (ds.DS_GENERAL_RUNTIME, ds.DS_GENERAL_COMPILED):
+            try:
+                d.set_general_variant(variant)
+            except ds.DSError:
+                continue
+            y = d(x)
+            torch.cuda.synchronize()
+            _assert_same(y.cpu().numpy(), want, f"{what} variant {d.last_variant()}")
+            checked += d.last_variant() == 1
+            compiled += d.last_variant() == 2
+    assert checked >= 25 * FUZZ_SCALE
+    assert compiled >= 1
+
+
 # ------------------------------------------------------- alignment / API --
 @pytest.mark.parametrize("off", [1, 2, 3, 4, 8])
 @pytest.mark.parametrize("W,H,strips", [(352, 288, False), (352, 288, True), (32, 36, False)])
