@@ -100,6 +100,7 @@ struct GeneralCfg {
 using SpecFn = void (*)(void);
 struct SpecPlaneCfg {
     int32_t strips = 1, sw = 0, k = 0, nb = 0, R = 0, pitch = 0, mp = 0, unit_start = 0;
+    int32_t rows_alloc = 0;        // K-N1s: intermediate rows per buffer (R + rows per warp - 1)
 };
 struct SpecCfg {
     bool valid = false;

@@ -44,6 +44,22 @@ void h_words(const ds_stage_spec& h, int ph, int* klo, int* khi) {
 }
 int64_t floor16(int64_t o) { return o >= 0 ? o / 16 : -((-o + 15) / 16); }
 
+// Lanes of a row of nch chunks: segs 32-chunk warp segments (a power of two
+// dividing NW), or, for rows of at most 16 chunks, 2^lgrpw rows per warp of
+// 32 >> lgrpw chunk lanes each.  A warp's row step, (NW / segs) 2^lgrpw, stays
+// below the plane height H (the row cursor wraps with one subtraction).
+bool spec_lanes(int nch, int H, int* segs, int* lgrpw) {
+    int s = 1;
+    while (32 * s < nch) s *= 2;
+    if (s > DS_SPEC_NW || H <= DS_SPEC_NW / s) return false;
+    int lg = 0;
+    if (s == 1)
+        while (lg < 5 && (32 >> (lg + 1)) >= nch && (DS_SPEC_NW << (lg + 1)) < H) ++lg;
+    *segs = s;
+    *lgrpw = lg;
+    return true;
+}
+
 int al_index(int al) { return al == 16 ? 0 : al == 8 ? 1 : 2; }
 
 }  // namespace
@@ -112,15 +128,16 @@ bool spec_geometry_ok(const ds_filter_spec& sp, const ds_plan_info& pi) {
     const int kblk = (khi + 4) / 4;
     for (int p = 0; p < pi.n_planes; ++p) {
         const int W = pi.in_w[p];
-        if (W < 64 || W / 16 < 2 * kblk) return false;
-        // the row cursor advances up to NW rows per step with one wrap test
-        if (pi.in_h[p] <= DS_SPEC_NW) return false;
+        if (W < 64 || W / 16 < kblk) return false;        // a window fits in a row
         // at most 4 chunks per row may cross the row end (the wrap pass's table)
         const int np = W / sp.h.paving, nch = (np + 3) / 4;
+        int segs, lgrpw;
+        if (!spec_lanes(nch, pi.in_h[p], &segs, &lgrpw)) return false;
         const int64_t blk0 = floor16(spec_h_origin(sp.h.origin, W));
         int nwc = 0;
         for (int c = 0; c < nch; ++c) {
             const int64_t B = blk0 + (sp.h.paving / 4) * c;
+            if (16 * B + 4 * klo < -W || 16 * B + 4 * (khi + 1) > 2 * W) return false;   // one wrap at most
             nwc += !(16 * B + 4 * klo >= 0 && 16 * B + 4 * (khi + 1) <= W);
         }
         if (nwc > 4) return false;
@@ -138,27 +155,33 @@ bool spec_plane_plan(const ds_filter_spec& sp, int32_t W, int32_t H, int64_t bud
     const int Sh = sp.h.paving, Qh = sp.h.outputs;
     const int Sv = sp.v.paving, Pv = sp.v.pattern;
     const int np = W / Sh, G = H / Sv;
-    const int nch = (np + 3) / 4, segs = (nch + 31) / 32;
-    if (DS_SPEC_NW % segs != 0) return false;          // a warp keeps one row segment (segs | NW)
+    const int nch = (np + 3) / 4;
+    int segs, lgrpw;
+    if (!spec_lanes(nch, H, &segs, &lgrpw)) return false;
+    const int rpw = 1 << lgrpw, cw = 32 >> lgrpw;
     const int64_t nq = ((int64_t)Qh * np + 3) / 4;
-    // row stride: every chunk a warp segment covers plus one scratch chunk (the
+    // row stride: every chunk the row's lanes cover plus one scratch chunk (the
     // H pass's inactive lanes store there unconditionally), and every V quad
-    const int64_t mp = round_up(std::max<int64_t>(4LL * Qh * (32LL * segs + 1), 4 * nq), 16);
+    const int64_t mp = round_up(std::max<int64_t>(4LL * Qh * ((int64_t)cw * segs + 1), 4 * nq), 16);
     const int ovl = std::max(0, Pv - Sv);
     double best = 1e300;
     bool found = false;
     for (int k = 1; k <= G; ++k) {
         if (G % k) continue;
         const int64_t R = (int64_t)Sv * (k - 1) + Pv;
-        if (2 * R * mp > budget) continue;
+        // + rpw - 1 rows: a warp's last pass may run past the band's rows on
+        // its later row lanes; their (unread) results land there
+        if (2 * (R + rpw - 1) * mp > budget) continue;
         const int64_t newrows = std::max<int64_t>(1, R - ovl);
-        const double hr = (double)((newrows * segs + DS_SPEC_NW - 1) / DS_SPEC_NW);
+        const int64_t per_pass = (int64_t)(DS_SPEC_NW / segs) * rpw;
+        const double hr = (double)((newrows + per_pass - 1) / per_pass);
         const double vr = (double)((k * nq + DS_SPEC_NW * 32 - 1) / (DS_SPEC_NW * 32));
         const double cost = (90.0 * hr + 120.0 * vr + 150.0) / ((double)Sv * k);
         if (cost < best * 0.999) {
             best = cost;
             found = true;
             out->k = k; out->nb = G / k; out->R = (int32_t)R; out->mp = (int32_t)mp;
+            out->rows_alloc = (int32_t)(R + rpw - 1);
             out->strips = 1; out->sw = np; out->pitch = 0;
         }
     }
@@ -198,7 +221,7 @@ int configure_spec(ds_handle* h) {
     int64_t mmax = 0;
     for (int p = 0; p < pi.n_planes; ++p) {
         if (!spec_plane_plan(sp, pi.in_w[p], pi.in_h[p], budget, &c.plane[p])) return DS_OK;
-        mmax = std::max<int64_t>(mmax, (int64_t)c.plane[p].R * c.plane[p].mp);
+        mmax = std::max<int64_t>(mmax, (int64_t)c.plane[p].rows_alloc * c.plane[p].mp);
     }
     c.stages = 0;
     c.stage_stride = 0;
@@ -317,7 +340,7 @@ int launch_spec(ds_handle* h, const uint8_t* in, int64_t n, uint8_t* out, cudaSt
         P.ov = (int32_t)(((int64_t)sp.v.origin % P.H + P.H) % P.H);
         P.np = P.W / sp.h.paving;
         P.nch = (P.np + 3) / 4;
-        P.segs = (P.nch + 31) / 32;
+        if (!spec_lanes(P.nch, P.H, &P.segs, &P.lgrpw)) return DS_EUNSUPPORTED;   // configure_spec rules this out
         P.lgsegs = 0;
         while ((1 << P.lgsegs) < P.segs) ++P.lgsegs;
         P.nb16 = P.W / 16;

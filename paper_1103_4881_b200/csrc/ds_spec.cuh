@@ -76,7 +76,8 @@ struct SpecPlane {
     int32_t oh, ov;            // H origin reduced to (-W/2, W/2]; V origin reduced mod H (>= 0)
     int32_t np;                // H repetitions per row (W / Sh)
     int32_t nch;               // chunks of 4 repetitions per row: ceil(np / 4)
-    int32_t segs, lgsegs;      // 32-chunk warp segments per row: ceil(nch / 32), a power of two; log2
+    int32_t segs, lgsegs;      // 32-chunk warp segments per row (a power of two >= nch / 32); log2
+    int32_t lgrpw;             // log2 rows per warp (segs == 1): 32 >> lgrpw chunk lanes per row
     int32_t nwc, wch[4];       // chunks whose window crosses the row end (wrap pass)
     int32_t nb16, blk0;        // W / 16 (floor); floor(oh / 16): first window block of repetition 0 (may be < 0)
     int32_t k, nb;             // V repetitions per band, bands per plane ((H / Sv) / k)
@@ -532,13 +533,17 @@ __global__ void __launch_bounds__(DS_SPEC_NW * 32, DS_SPEC_MINB) ds_spec_kernel(
         // i = warp >> lgsegs, + step, ... with a running row pointer.  Chunks whose
         // window crosses the row end (at most a few per row) are left to a
         // small wrap pass, so the main loop has no per-block index arithmetic.
-        const int seg = warp & (P.segs - 1), step = NW >> P.lgsegs;
-        const int ch = seg * 32 + lane;
+        // Rows of at most 16 chunks: a warp takes 2^lgrpw rows at once, lane
+        // groups of 32 >> lgrpw chunk lanes (row lane rsub).
+        const int lgrpw = P.lgrpw, cwm = (32 >> lgrpw) - 1;
+        const int seg = warp & (P.segs - 1), step = (NW >> P.lgsegs) << lgrpw;
+        const int ch = seg * 32 + (lane & cwm);
         // the chunk's window words inside the row: the main loop's; else the wrap pass's
         int B = P.blk0 + (HS::S / 4) * ch;
         const bool act = ch < P.nch && 16 * B + 4 * HC::kLo >= 0 && 16 * B + 4 * (HC::kHi + 1) <= P.W;
         if (!act) B = P.nb16 - HC::kBlk;                            // in-bounds loads, result unused
-        const int i0 = warp >> P.lgsegs;
+        const int i0w = (warp >> P.lgsegs) << lgrpw;               // the warp's first row
+        const int i0 = i0w + (lane >> (5 - lgrpw));                 // this lane's
         // issue cursor: a 32-bit byte offset of the lane's window in the plane
         // (planes are < 2^31 bytes); it advances `step` rows per issue and wraps
         // at the plane bottom by one compare and subtract
@@ -559,9 +564,11 @@ __global__ void __launch_bounds__(DS_SPEC_NW * 32, DS_SPEC_MINB) ds_spec_kernel(
             roff += rowstep;
             if (roff >= plane_bytes) roff -= plane_bytes;
         };
-        // rows this warp computes in a band of `rows` rows: i0, i0 + step, ...
-        const int lgstep = DS_SPEC_LGNW - P.lgsegs;                // step is a power of two
-        auto my_rows = [&](int rows) { return rows > i0 ? (rows - i0 + step - 1) >> lgstep : 0; };
+        // passes of this warp over a band of `rows` rows: rows i0w + rsub, + step,
+        // ...; a later row lane may run one row past the band in the last pass
+        // (its result lands in the buffer's spare rows, never read)
+        const int lgstep = DS_SPEC_LGNW - P.lgsegs + lgrpw;        // step is a power of two
+        auto my_rows = [&](int rows) { return rows > i0w ? (rows - i0w + step - 1) >> lgstep : 0; };
         bool preloaded = false;
 
         for (int band = b0; band < b1; ++band) {
@@ -590,8 +597,8 @@ __global__ void __launch_bounds__(DS_SPEC_NW * 32, DS_SPEC_MINB) ds_spec_kernel(
             while (row0 >= P.H) row0 -= P.H;
             // inactive lanes (past the row, or a wrapping chunk left to the wrap
             // pass) store their garbage into a scratch chunk past the row's
-            // chunks (mp >= 4 Qh (32 segs + 1)), so the stores need no predicate
-            const uint32_t mcol = mid + (reuse + i0) * mp + 4 * HS::Q * (act ? ch : 32 * P.segs);
+            // chunks (mp >= 4 Qh ((cwm + 1) segs + 1)), so the stores need no predicate
+            const uint32_t mcol = mid + (reuse + i0) * mp + 4 * HS::Q * (act ? ch : (cwm + 1) * P.segs);
             const uint32_t mstep = step * mp;
             auto finish = [&](int k, const uint32_t (&x)[4 * HC::kBlk]) {
                 uint32_t o[HS::Q];

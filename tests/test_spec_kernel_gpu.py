@@ -123,15 +123,36 @@ def test_auto_picks_compiled_variant_and_falls_back():
 
 
 def test_compiled_variant_rejected_where_it_cannot_run():
-    # QCIF chroma rows (88 B) are narrower than two 13-tap H windows: no K-N1s plan
-    d = _handle(176, 144, 3, 1, HALO)
+    # 48-byte chroma rows (96x72 4:2:0) are shorter than K-N1s's 64-byte minimum
+    d = _handle(96, 72, 3, 1, HALO)
     with pytest.raises(ds.DSError):
         d.set_general_variant(ds.DS_GENERAL_COMPILED)
-    fr = synth.random_frames(2, 0, 2, 176, 144)
+    fr = synth.random_frames(2, 0, 2, 96, 72)
     y = d(torch.from_numpy(fr).cuda())
     torch.cuda.synchronize()
     assert d.last_variant() == 1
-    _same(y.cpu().numpy(), _want(fr, 176, 144, 3, 1, HALO), "QCIF halo runtime taps")
+    _same(y.cpu().numpy(), _want(fr, 96, 72, 3, 1, HALO), "96x72 halo runtime taps")
+
+
+@pytest.mark.parametrize("spec", ["halo", "spec"])
+@pytest.mark.parametrize("W,H,ch,chroma,n", [(176, 144, 3, 1, 6), (352, 288, 3, 1, 4), (64, 90, 1, 1, 5),
+                                             (88, 72, 1, 1, 7), (200, 36, 1, 1, 4)])
+def test_compiled_spec_several_rows_per_warp(spec, W, H, ch, chroma, n):
+    """Rows of at most 16 chunks (64 H repetitions) are taken 2, 4 or 8 to a
+    warp (QCIF chroma: 3 chunks, 8 rows per warp); a warp's last pass may run
+    past the band's rows on its later row lanes.  Exact, every unit once."""
+    sp = HALO if spec == "halo" else None
+    d = _handle(W, H, ch, chroma, sp)
+    d.set_general_variant(ds.DS_GENERAL_COMPILED)
+    fr = synth.random_frames(41, 5, n, W, H, ch, chroma)
+    want = _want(fr, W, H, ch, chroma, sp)
+    x = torch.from_numpy(fr).cuda()
+    for rb in (0, 1, 3):
+        d.set_run_bands(rb)
+        y = d(x)
+        torch.cuda.synchronize()
+        assert d.last_variant() == 2
+        _same(y.cpu().numpy(), want, f"K-N1s {spec} {W}x{H} run_bands {rb}")
 
 
 @pytest.mark.parametrize("spec", ["halo", "spec"])
