@@ -314,6 +314,18 @@ int launch_spec(ds_handle* h, const uint8_t* in, int64_t n, uint8_t* out, cudaSt
     const SpecCfg& c = h->spec_cfg;
     const ds_plan_info& pi = h->plan;
     const ds_filter_spec& sp = h->spec;
+    // the kernel counts units in 32 bits: at most one unit per band per frame
+    int64_t upf_max = 0;
+    for (int q = 0; q < pi.n_planes; ++q) upf_max += c.plane[q].nb;
+    const int64_t cap = std::max<int64_t>(1, (int64_t)INT32_MAX / std::max<int64_t>(upf_max, 1));
+    if (n > cap) {
+        for (int64_t off = 0; off < n; off += cap) {
+            const int rc = launch_spec(h, in + off * pi.in_frame_bytes, std::min(cap, n - off),
+                                       out + off * pi.out_frame_bytes, st);
+            if (rc != DS_OK) return rc;
+        }
+        return DS_OK;
+    }
     dss::SpecParams p;
     std::memset(&p, 0, sizeof p);
     p.in = in; p.out = out;

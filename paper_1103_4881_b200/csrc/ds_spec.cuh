@@ -485,11 +485,28 @@ __global__ void __launch_bounds__(DS_SPEC_NW * 32, DS_SPEC_MINB) ds_spec_kernel(
     const uint32_t mid0 = smem_u32(smem);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
-    // unit u -> frame f, index `local` within the frame (incremental)
-    int64_t u = blockIdx.x;
-    int64_t f = blockIdx.x / (uint32_t)p.upf;
-    int32_t local = (int32_t)(blockIdx.x - (uint32_t)f * (uint32_t)p.upf);
-    const int32_t gdiv = (int32_t)(gridDim.x / (uint32_t)p.upf), gmod = (int32_t)(gridDim.x - gdiv * p.upf);
+    // Units: CTA b takes units b, b + grid, ...; unit u -> frame f = u / upf and
+    // unit (u mod upf + f) mod upf of that frame: rotating by the frame index is
+    // a bijection per frame, and it hands a CTA every unit kind even when upf
+    // divides the grid (units differ in size: planes, run lengths; unrotated,
+    // 1200 HD halo frames ran 25% slower).  Incremental: no division per unit.
+    const int32_t n_units = (int32_t)p.n_units;          // < 2^31 (the host splits larger calls)
+    const int32_t upf = p.upf;
+    int32_t u = blockIdx.x;
+    int32_t f = (int32_t)(blockIdx.x / (uint32_t)upf);
+    int32_t lraw = (int32_t)blockIdx.x - f * upf;        // u mod upf
+    int32_t fm = (int32_t)((uint32_t)f % (uint32_t)upf); // f mod upf
+    const int32_t gdiv = (int32_t)(gridDim.x / (uint32_t)upf), gmod = (int32_t)gridDim.x - gdiv * upf;
+    const int32_t gdm = (int32_t)((uint32_t)gdiv % (uint32_t)upf);
+    auto rot = [&](int32_t lr, int32_t fmod) { const int32_t l = lr + fmod; return l >= upf ? l - upf : l; };
+    auto advance = [&](int32_t& f_, int32_t& lr, int32_t& fm_) {
+        f_ += gdiv;
+        fm_ += gdm;
+        lr += gmod;
+        if (lr >= upf) { lr -= upf; ++f_; ++fm_; }
+        if (fm_ >= upf) fm_ -= upf;
+    };
+    int32_t local = rot(lraw, fm);
     int mpar = 0;
 
     // L2 prefetch (one thread) of the new input rows of band `band` of unit
@@ -510,9 +527,9 @@ __global__ void __launch_bounds__(DS_SPEC_NW * 32, DS_SPEC_MINB) ds_spec_kernel(
         prefetch_range(pl_ + (int64_t)r0 * Q.W, (uint32_t)n1 * (uint32_t)Q.W);
         if (rows_ > n1) prefetch_range(pl_, (uint32_t)min(rows_ - n1, Q.H) * (uint32_t)Q.W);
     };
-    if (tid == 0 && u < p.n_units) prefetch_band(f, local, 0);
+    if (tid == 0 && u < n_units) prefetch_band(f, local, 0);
 
-    for (; u < p.n_units; u += gridDim.x) {
+    for (; u < n_units; u += gridDim.x) {
         const int pi = (p.n_planes > 2 && local >= p.pl[2].unit_start) ? 2
                        : (p.n_planes > 1 && local >= p.pl[1].unit_start) ? 1 : 0;
         const SpecPlane& P = p.pl[pi];
@@ -524,9 +541,9 @@ __global__ void __launch_bounds__(DS_SPEC_NW * 32, DS_SPEC_MINB) ds_spec_kernel(
         const int mp = P.mp;
         const int rfirst = VS::S * (P.k - 1) + VS::P;             // rows of a run's first band
         // next unit of this CTA (for the prefetch of its first band)
-        int64_t fn = f + gdiv;
-        int32_t ln = local + gmod;
-        if (ln >= p.upf) { ln -= p.upf; ++fn; }
+        int32_t fn = f, lrn = lraw, fmn = fm;
+        advance(fn, lrn, fmn);
+        const int32_t ln = rot(lrn, fmn);
 
         // A warp keeps one 32-chunk segment of the row for the whole unit (segs is a
         // power of two dividing NW): its window blocks are fixed; it walks rows
@@ -575,8 +592,11 @@ __global__ void __launch_bounds__(DS_SPEC_NW * 32, DS_SPEC_MINB) ds_spec_kernel(
             const uint32_t mid = mid0 + mpar * p.mid_stride;
             const int reuse = band > b0 ? p.ovl : 0;
             if (tid == 0) {
-                if (band + 1 < b1) prefetch_band(f, local, band + 1 - b0);
-                else if (u + gridDim.x < p.n_units) prefetch_band(fn, ln, 0);
+                if (band + 1 < b1) {
+                    prefetch_band(f, local, band + 1 - b0);
+                } else if (u + (int32_t)gridDim.x < n_units) {    // the next unit's first band
+                    prefetch_band(fn, ln, 0);
+                }
             }
             if (reuse) {
                 // the previous band's intermediate rows [Sv k, Sv k + ovl) are this
@@ -699,9 +719,10 @@ __global__ void __launch_bounds__(DS_SPEC_NW * 32, DS_SPEC_MINB) ds_spec_kernel(
             }
             mpar ^= 1;
         }
-        f += gdiv;
-        local += gmod;
-        if (local >= p.upf) { local -= p.upf; ++f; }
+        f = fn;
+        lraw = lrn;
+        fm = fmn;
+        local = ln;
     }
 }
 

@@ -24,6 +24,25 @@ def timed(fn, steps=20):
     return a.elapsed_time(b) / steps
 
 
+h, v = bench.HALO_SPEC
+# SPEC_TIME_CFGS="WxHxCHxCHROMA:N,...": other geometries, compiled variant only
+cfgs = os.environ.get("SPEC_TIME_CFGS")
+if cfgs:
+    out = []
+    for c in cfgs.split(","):
+        g, n = c.split(":")
+        W, H, ch, chroma = (int(t) for t in g.split("x"))
+        n = int(n)
+        d = ds.Downscaler(W, H, ch, chroma=chroma, spec=ds.make_spec(h=h, v=v, chroma=chroma))
+        d.set_kernel(ds.DS_KERNEL_FUSED_GENERAL)
+        x = ds.generate_frames(n, d.in_frame_bytes, seed=1)
+        y = d.alloc_out(n)
+        ms = timed(lambda: d(x, y))
+        out.append(f"{g}:{n}={ms:.4f}ms({n * (d.in_frame_bytes + d.out_frame_bytes) / ms / 1e6:.0f}GB/s,v{d.last_variant()})")
+        del x, y, d
+        torch.cuda.empty_cache()
+    print(" ".join(out), flush=True)
+    sys.exit(0)
 W, H, n = 1920, 1080, 300
 h, v = bench.HALO_SPEC
 d = ds.Downscaler(W, H, 3, spec=ds.make_spec(h=h, v=v))
