@@ -258,10 +258,13 @@ DS_API int ds_set_kernel(ds_handle* h, int32_t kernel);
 DS_API int ds_last_kernel(const ds_handle* h);
 
 /* K-N1 tuning: ring stages per CTA (2..8) and CTAs per SM (0 = maximum
- * occupancy).  Defaults: up to 3 CTAs per SM (as many as fit) whose rings
- * together hold ~120 KB, at least 2 stages each (120 KB in flight per SM is
- * the TMA read optimum measured by tools/bw_probe).  Returns DS_EINVAL when out of
- * range.  Not synchronised with ds_run calls in flight on other threads. */
+ * occupancy), for every call size.  Defaults: up to 3 CTAs per SM (as many as
+ * fit) whose rings together hold ~120 KB, at least 2 stages each (120 KB in
+ * flight per SM is the TMA read optimum measured by tools/bw_probe); where
+ * that is 2 CTAs per SM (HD and wider), calls of at most 3 GiB of input run
+ * one CTA per SM with 4 stages (measured faster below ~3 GB, slower above).
+ * Returns DS_EINVAL when out of range.  Not synchronised with ds_run calls
+ * in flight on other threads. */
 DS_API int ds_set_tuning(ds_handle* h, int32_t stages, int32_t ctas_per_sm);
 
 /* K-N1 work-unit (band) size: the largest number of 9-row groups whose

@@ -312,6 +312,18 @@ int configure_fused(ds_handle* h) {
     DeviceGuard g(h->device);
     int rc = prepare_cfg(h->fused);
     if (!rc) rc = prepare_cfg(h->fine);
+    // Wide plans (2 CTAs per SM) on calls of up to ~3 GB of input: one CTA per
+    // SM with a 4-deep ring of the same units measured 2-4% faster (HD 4:2:0
+    // 150-900 frames, HD 4:4:4 300, 4K 100-150), and 1.5-7% slower on longer
+    // calls (HD 1200/3000, HD 4:4:4 600, 4K 300/1000); CIF/SD plans (3 CTAs
+    // per SM) lose 20-26% at one CTA (profiles/r02/k1_cta_ab*.txt).
+    h->onecta = FusedCfg{};
+    if (!rc && h->fused.valid && h->fused.grid_per_sm == 2) {
+        FusedCfg c = h->fused;
+        c.stages = 4;
+        c.ctas_per_sm = 1;
+        if (prepare_cfg(c) == DS_OK && c.grid_per_sm == 1) h->onecta = c;
+    }
     return rc;
 }
 
@@ -348,6 +360,7 @@ int fit_stages(const FusedCfg& c, int want) {
 // Which configuration a call of n frames uses.
 const FusedCfg& pick_cfg(const ds_handle* h, int64_t n) {
     if (h->fine.valid && n * h->fused.plan.units_per_frame < 2LL * h->sm_count) return h->fine;
+    if (h->onecta.valid && n * h->plan.in_frame_bytes <= kOneCtaMaxBytes) return h->onecta;
     return h->fused;
 }
 
@@ -1059,6 +1072,7 @@ DS_API int ds_set_tuning(ds_handle* h, int32_t stages, int32_t ctas_per_sm) {
     if (rc) return rc;
     h->fused = c;
     h->fine = FusedCfg{};          // an explicit tuning applies to every call size
+    h->onecta = FusedCfg{};
     h->tune_stages = stages;       // kept across ds_set_band_bytes / ds_set_general_stage_bytes
     h->tune_ctas = ctas_per_sm;
     return DS_OK;
@@ -1072,7 +1086,7 @@ static int replan(ds_handle* h, int64_t band_target, int64_t general_target) {
     int rc = make_plan(h->W, h->H, h->channels, &h->spec, nullptr, &pi, band_target, general_target);
     if (rc) return rc;
     const ds_plan_info old_plan = h->plan;
-    const FusedCfg old_fused = h->fused, old_fine = h->fine;
+    const FusedCfg old_fused = h->fused, old_fine = h->fine, old_onecta = h->onecta;
     const GeneralCfg old_general = h->general;
     const int64_t old_band = h->band_target, old_gen = h->general_target;
     h->plan = pi;
@@ -1091,12 +1105,14 @@ static int replan(ds_handle* h, int64_t band_target, int64_t general_target) {
         if (!rc) {
             h->fused = c;
             h->fine = FusedCfg{};
+            h->onecta = FusedCfg{};
         }
     }
     if (rc) {
         h->plan = old_plan;
         h->fused = old_fused;
         h->fine = old_fine;
+        h->onecta = old_onecta;
         h->general = old_general;
         h->spec_cfg = old_spec;
         h->band_target = old_band;

@@ -23,6 +23,10 @@ inline int64_t default_band_target(int64_t in_frame_bytes) {
 constexpr int64_t kInFlightTarget = 120 * 1024;     // K-N1 bytes in flight per SM (measured
                                                     // optimum of tools/bw_probe tma_read)
 constexpr int kK1Ctas = 3;                          // K-N1 CTAs per SM (cap; what fits runs)
+constexpr int64_t kOneCtaMaxBytes = 3LL << 30;      // K-N1 calls up to this much input (wide
+                                                    // plans) run one CTA per SM x 4 stages:
+                                                    // measured crossover 2.8-3.7 GB
+                                                    // (profiles/r02/k1_cta_ab4.txt)
 constexpr int kSmemLimit = 227 * 1024;              // per-CTA opt-in maximum
 constexpr int64_t kHostChunkBytes = 96LL << 20;     // ds_run_host chunk target (tools/e2e_sweep.py)
 
@@ -137,6 +141,9 @@ struct ds_handle {
     // coarse units than 2 per SM, e.g. one HD frame)
     int64_t band_target = dsi::kUnitTargetBytes;
     dsi::FusedCfg fused, fine;
+    // `onecta`: the coarse plan at one CTA per SM and a 4-deep ring, for calls
+    // of at most kOneCtaMaxBytes of input when `fused` runs 2 CTAs per SM
+    dsi::FusedCfg onecta;
     dsi::GeneralCfg general;
     dsi::SpecCfg spec_cfg;                  // K-N1s (compiled-spec K-N1g)
     int32_t general_variant = 0;            // ds_set_general_variant: 0 auto, 1 runtime taps, 2 compiled taps

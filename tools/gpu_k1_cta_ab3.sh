@@ -1,6 +1,6 @@
 # K-N1 launch shape vs launch length: HD 3000 frames, 4K 300 frames (driver-style bench, graph replay)
 mkdir -p gpurun_out; : > gpurun_out/k1_cta_ab3.txt
-for spec in "hd420 3000" "4k420 300" "4k444 300" "hd420 1200"; do
+for spec in ${SPECS:-"hd420 3000" "4k420 300" "4k444 300" "hd420 1200"}; do
 set -- $spec
 for i in 1 2; do
   for v in default one; do

@@ -11,7 +11,9 @@ import torch
 import paper_1103_4881_b200 as ds
 
 CFG = {"hd420": (1920, 1080, 1, 300), "hd444": (1920, 1080, 0, 300), "4k420": (3840, 2160, 1, 300),
-       "cif420": (352, 288, 1, 2000), "qcif420": (176, 144, 1, 2000), "cif420_300": (352, 288, 1, 300)}
+       "cif420": (352, 288, 1, 2000), "qcif420": (176, 144, 1, 2000), "cif420_300": (352, 288, 1, 300),
+       "hd420_1200": (1920, 1080, 1, 1200), "hd420_3000": (1920, 1080, 1, 3000), "4k420_1000": (3840, 2160, 1, 1000),
+       "sd420": (720, 576, 1, 2000)}
 out = []
 only = sys.argv[1].split(",") if len(sys.argv) > 1 else list(CFG)
 for name, (W, H, chroma, n) in CFG.items():
