@@ -306,6 +306,16 @@ def test_run_time_compiled_spec(spec, W, H, chroma):
     assert d.last_variant() == 2
     want = _want(fr, W, H, 3, chroma, sp)
     _same(y.cpu().numpy(), want, f"K-N1s (run-time compiled) {spec} {W}x{H}")
+    # the run-time compiled instance is built for the plan's row alignment only:
+    # an input pointer less aligned than that runs the runtime-tap kernel
+    plan_al = 16 if d.in_frame_bytes % 16 == 0 and W % 16 == 0 else 8
+    xb = torch.zeros(x.numel() + 16, dtype=torch.uint8, device="cuda")
+    xi = xb[4:4 + x.numel()].view(n, -1)
+    xi.copy_(x)
+    y4 = d(xi)
+    torch.cuda.synchronize()
+    assert d.last_variant() == (2 if plan_al == 4 else 1)
+    _same(y4.cpu().numpy(), want, f"{spec} input offset 4")
     d.set_general_variant(ds.DS_GENERAL_RUNTIME)
     _same(d(x).cpu().numpy(), want, f"runtime taps {spec}")
 
