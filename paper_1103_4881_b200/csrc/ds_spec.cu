@@ -60,7 +60,7 @@ bool spec_lanes(int nch, int H, int* segs, int* lgrpw) {
     return true;
 }
 
-int al_index(int al) { return al == 16 ? 0 : al == 8 ? 1 : 2; }
+int al_index(int al) { return al == 16 ? 0 : al == 8 ? 1 : al == 4 ? 2 : 3; }
 
 }  // namespace
 
@@ -94,18 +94,21 @@ int spec_plan_align(const ds_plan_info& pi) {
 
 // Built-in instances: (stage types, window phase, row alignment) -> kernel.
 SpecFn spec_builtin(const ds_filter_spec& sp, int ph, int al) {
-    auto pick = [al](auto k16, auto k8, auto k4) {
-        return al == 16 ? reinterpret_cast<SpecFn>(k16) : al == 8 ? reinterpret_cast<SpecFn>(k8) : reinterpret_cast<SpecFn>(k4);
+    auto pick = [al](auto k16, auto k8, auto k4, auto k1) {
+        return al == 16 ? reinterpret_cast<SpecFn>(k16) : al == 8 ? reinterpret_cast<SpecFn>(k8)
+               : al == 4 ? reinterpret_cast<SpecFn>(k4) : reinterpret_cast<SpecFn>(k1);
     };
     constexpr int kHaloPh = (dss::HaloH::O % 16 + 16) % 16, kSpecPh = (dss::SpecH::O % 16 + 16) % 16;
     if (ph == kHaloPh && stage_is<dss::HaloH>(sp.h) && stage_is<dss::HaloV>(sp.v))
         return pick(&dss::ds_spec_kernel<dss::HaloH, dss::HaloV, kHaloPh, 16>,
                     &dss::ds_spec_kernel<dss::HaloH, dss::HaloV, kHaloPh, 8>,
-                    &dss::ds_spec_kernel<dss::HaloH, dss::HaloV, kHaloPh, 4>);
+                    &dss::ds_spec_kernel<dss::HaloH, dss::HaloV, kHaloPh, 4>,
+                    &dss::ds_spec_kernel<dss::HaloH, dss::HaloV, kHaloPh, 1>);
     if (ph == kSpecPh && stage_is<dss::SpecH>(sp.h) && stage_is<dss::SpecV>(sp.v))
         return pick(&dss::ds_spec_kernel<dss::SpecH, dss::SpecV, kSpecPh, 16>,
                     &dss::ds_spec_kernel<dss::SpecH, dss::SpecV, kSpecPh, 8>,
-                    &dss::ds_spec_kernel<dss::SpecH, dss::SpecV, kSpecPh, 4>);
+                    &dss::ds_spec_kernel<dss::SpecH, dss::SpecV, kSpecPh, 4>,
+                    &dss::ds_spec_kernel<dss::SpecH, dss::SpecV, kSpecPh, 1>);
     return nullptr;
 }
 
@@ -199,8 +202,10 @@ int configure_spec(ds_handle* h) {
     const int ph = spec_phase(sp, pi), al = spec_plan_align(pi);
     c.al = al;
     // built-in: an instance for the plan's row alignment and each lower one
-    // (calls whose input pointer is less aligned than the plan)
+    // (calls whose input pointer is less aligned than the plan), and the
+    // funnel-shifting one for pointers that are not 4-byte aligned
     for (int a = al; a >= 4; a /= 2) c.fn_al[al_index(a)] = spec_builtin(sp, ph, a);
+    c.fn_al[al_index(1)] = spec_builtin(sp, ph, 1);
     SpecFn fn = c.fn_al[al_index(al)];
     c.jit = 0;
     if (!fn) {
@@ -302,7 +307,7 @@ SpecFn spec_call_fn(const ds_handle* h, const uint8_t* in) {
     if (!c.valid) return nullptr;
     int a = c.al;
     while (a >= 4 && (reinterpret_cast<uintptr_t>(in) & (uintptr_t)(a - 1)) != 0) a /= 2;
-    return a >= 4 ? c.fn_al[al_index(a)] : nullptr;
+    return c.fn_al[al_index(a >= 4 ? a : 1)];
 }
 
 bool spec_call_ok(const ds_handle* h, const uint8_t* in, const uint8_t* out) {
@@ -377,6 +382,7 @@ int launch_spec(ds_handle* h, const uint8_t* in, int64_t n, uint8_t* out, cudaSt
         P.unit_start = start;
         start += (P.nb + P.L - 1) / P.L;
     }
+    p.in_mis = (int32_t)(reinterpret_cast<uintptr_t>(in) & 3);           // AL = 1 instances
     p.out_al4 = (reinterpret_cast<uintptr_t>(out) & 3) == 0 && pi.out_frame_bytes % 4 == 0;
     for (int q = 0; q < pi.n_planes; ++q)
         if (pi.out_offset[q] % 4 || pi.out_w[q] % 4) p.out_al4 = 0;

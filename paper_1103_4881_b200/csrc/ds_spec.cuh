@@ -94,7 +94,8 @@ struct SpecParams {
     uint32_t* unit_count;      // debug: +1 per unit processed, else null
     int64_t in_frame, out_frame, n_units;
     int32_t upf, n_planes, mid_stride, ovl;   // ovl = max(Pv - Sv, 0): rows a band shares with the next
-    int32_t out_al4, reserved_;               // 1: every output row starts 4-byte aligned
+    int32_t out_al4;                          // 1: every output row starts 4-byte aligned
+    int32_t in_mis;                           // AL = 1 instances: input pointer mod 4 (every row start's)
     SpecPlane pl[DS_SPEC_MAXP];
 };
 
@@ -319,12 +320,14 @@ __device__ __forceinline__ void stg8(uint8_t* p, uint32_t v) {
 // + (Sh / 4) c that is PH + Sh m (PH = o mod 16, a compile-time constant of
 // the instance).  The lane loads exactly the words any live tap reads (loads
 // of up to AL bytes by word runs: AL = 16, 8 or 4 is the alignment of every
-// row start in the call), then every output is a dp4a per aligned word with a
+// row start in the call; AL = 1: rows start m = 1..3 bytes past a 4-byte
+// boundary, and each window word is funnel-shifted out of the two aligned
+// words it straddles), then every output is a dp4a per aligned word with a
 // nonzero re-indexed weight word.
 template <class HS, int PH, int AL = 16>
 struct HChunk {
     using I = StageInfo<HS>;
-    static_assert(AL == 16 || AL == 8 || AL == 4, "row alignment 16, 8 or 4");
+    static_assert(AL == 16 || AL == 8 || AL == 4 || AL == 1, "row alignment 16, 8, 4, or 1 (funnelled)");
     static constexpr int kLo = PH / 4;                                   // first word read
     static constexpr int kHi = (PH + 3 * HS::S + I::hi_tap()) / 4;       // last word read
     static constexpr int kWords = kHi + 1;                               // words from B's start
@@ -336,8 +339,20 @@ struct HChunk {
     // W.  Used by the wrap pass for the few chunks per row whose window
     // crosses the row end.  16-byte rows (AL = 16): whole blocks mod W / 16;
     // else word by word (W % 4 == 0, so no word straddles the row end).
-    __device__ __forceinline__ static void load_wrap(const uint8_t* row, int B, int W, uint32_t (&x)[4 * kBlk]) {
-        if constexpr (AL == 16) {
+    __device__ __forceinline__ static void load_wrap(const uint8_t* row, int B, int W, uint32_t (&x)[4 * kBlk],
+                                                     int mis = 0) {
+        if constexpr (AL == 1) {
+            // each word from the two aligned words around it: both hold one of
+            // its (valid) bytes, so neither read leaves the allocation
+            const uint8_t* ra = row - mis;
+            sfor<kLo, kHi + 1>([&](auto w) {
+                int off = 16 * B + 4 * decltype(w)::value;
+                if (off < 0) off += W;
+                else if (off >= W) off -= W;
+                const uint32_t lo = ldg32(ra + off), hi = ldg32(ra + off + 4);
+                x[decltype(w)::value] = __funnelshift_r(lo, hi, 8 * mis);
+            });
+        } else if constexpr (AL == 16) {
             const int nb16 = W >> 4;
             sfor<0, kBlk>([&](auto b) {
                 constexpr int w0 = 4 * decltype(b)::value, wlo = w0 > kLo ? w0 : kLo, whi = w0 + 3 < kHi ? w0 + 3 : kHi;
@@ -361,7 +376,18 @@ struct HChunk {
         }
     }
     // the same words from a base pointer to the chunk's first block (no wrap)
-    __device__ __forceinline__ static void load_at(const uint8_t* base, uint32_t (&x)[4 * kBlk]) {
+    __device__ __forceinline__ static void load_at(const uint8_t* base, uint32_t (&x)[4 * kBlk], int mis = 0) {
+        if constexpr (AL == 1) {
+            // aligned words kLo .. kHi + 1 from base - mis, then one funnel
+            // shift per window word (the last aligned word holds a valid byte)
+            const uint8_t* ba = base - mis;
+            uint32_t a[kHi - kLo + 2];
+            sfor<0, kHi - kLo + 2>([&](auto t) { a[decltype(t)::value] = ldg32(ba + 4 * (kLo + decltype(t)::value)); });
+            sfor<0, kHi - kLo + 1>([&](auto t) {
+                x[kLo + decltype(t)::value] = __funnelshift_r(a[decltype(t)::value], a[decltype(t)::value + 1], 8 * mis);
+            });
+            return;
+        }
         sfor<0, kBlk>([&](auto b) {
             constexpr int w0 = 4 * decltype(b)::value, wlo = w0 > kLo ? w0 : kLo, whi = w0 + 3 < kHi ? w0 + 3 : kHi;
             const uint8_t* a = base + 16 * decltype(b)::value;
@@ -577,7 +603,7 @@ __global__ void __launch_bounds__(DS_SPEC_NW * 32, DS_SPEC_MINB) ds_spec_kernel(
             roff = (uint32_t)rr * (uint32_t)P.W;
         };
         auto issue = [&](uint32_t (&x)[4 * HC::kBlk]) {
-            HC::load_at(wbase + roff, x);
+            HC::load_at(wbase + roff, x, p.in_mis);
             roff += rowstep;
             if (roff >= plane_bytes) roff -= plane_bytes;
         };
@@ -661,7 +687,7 @@ __global__ void __launch_bounds__(DS_SPEC_NW * 32, DS_SPEC_MINB) ds_spec_kernel(
                 int r = row0 + i;
                 while (r >= P.H) r -= P.H;
                 uint32_t xw[4 * HC::kBlk], o[HS::Q];
-                HC::load_wrap(plane + (int64_t)r * P.W, P.blk0 + (HS::S / 4) * c, P.W, xw);
+                HC::load_wrap(plane + (int64_t)r * P.W, P.blk0 + (HS::S / 4) * c, P.W, xw, p.in_mis);
                 HC::compute(xw, o);
                 const uint32_t mo = mid + (reuse + i) * mp + 4 * HS::Q * c;
                 sfor<0, HS::Q>([&](auto w) { sts32(mo + 4 * decltype(w)::value, o[decltype(w)::value]); });

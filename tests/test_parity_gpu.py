@@ -444,12 +444,19 @@ def test_general_rows_staged_by_producer(off, W, H, strips):
     buf = torch.zeros(fr.size + 64, dtype=torch.uint8, device="cuda")
     x = buf[off: off + fr.size]
     x.copy_(torch.from_numpy(fr.ravel()).cuda())
-    y = torch.zeros(want.size, dtype=torch.uint8, device="cuda")
     d.set_kernel(ds.DS_KERNEL_FUSED_GENERAL)
-    ds.ds_run(d.handle, x.data_ptr(), 3, y.data_ptr(), torch.cuda.current_stream().cuda_stream)
-    torch.cuda.synchronize()
-    assert d.last_kernel() == ds.DS_KERNEL_FUSED_GENERAL
-    _assert_same(y.cpu().numpy().reshape(want.shape), want, f"off={off} {W}x{H} strips={strips}")
+    # the runtime-tap kernel's staging; then whatever AUTO picks (K-N1s where it
+    # can run: 4/8-byte loads or funnel-shifted words)
+    for variant in (ds.DS_GENERAL_RUNTIME, ds.DS_GENERAL_AUTO):
+        d.set_general_variant(variant)
+        y = torch.zeros(want.size, dtype=torch.uint8, device="cuda")
+        ds.ds_run(d.handle, x.data_ptr(), 3, y.data_ptr(), torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        assert d.last_kernel() == ds.DS_KERNEL_FUSED_GENERAL
+        if variant == ds.DS_GENERAL_RUNTIME:
+            assert d.last_variant() == 1
+        _assert_same(y.cpu().numpy().reshape(want.shape), want,
+                     f"off={off} {W}x{H} strips={strips} variant {d.last_variant()}")
 
 
 def test_misaligned_pointers():

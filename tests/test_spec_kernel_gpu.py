@@ -4,9 +4,9 @@ stages, halos wrap toroidally) and against the runtime-tap
 K-N1g on the same inputs: the bench's halo spec and SPEC's downscaler on the
 paper's and BASELINE's geometries, column strips, ragged chunk tails, every
 unit processed once, every output byte written, rows and input pointers
-aligned to 8 or 4 bytes only, and the fallbacks (an input pointer not 4-byte
-aligned, or planes without a common window phase, run the runtime-tap
-kernel)."""
+aligned to 8 or 4 bytes only or not at all (funnel-shifted words), and the
+fallbacks (planes without a common window phase, or a run-time compiled spec
+from a less aligned pointer, run the runtime-tap kernel)."""
 import numpy as np
 import pytest
 
@@ -111,9 +111,9 @@ def test_auto_picks_compiled_variant_and_falls_back():
         assert d.last_variant() == 2
         _same(yo.cpu().numpy(), want, f"output offset {off}")
     # input pointer 4- or 8-byte aligned: K-N1s with 4- / 8-byte loads; not
-    # 4-byte aligned: runtime-tap K-N1g stages the rows itself
+    # 4-byte aligned: K-N1s funnel-shifts each window word out of two aligned words
     xb = torch.zeros(n * d.in_frame_bytes + 16, dtype=torch.uint8, device="cuda")
-    for off, variant in ((4, 2), (8, 2), (12, 2), (1, 1), (2, 1), (7, 1)):
+    for off, variant in ((4, 2), (8, 2), (12, 2), (1, 2), (2, 2), (7, 2)):
         xi = xb[off:off + n * d.in_frame_bytes]
         xi.copy_(x.view(-1))
         y3 = d(xi.view(n, -1))
@@ -172,14 +172,15 @@ def test_compiled_spec_rows_8_byte_aligned(spec, W, H, ch, chroma, n):
     assert d.last_variant() == 2
     want = _want(fr, W, H, ch, chroma, sp)
     _same(y.cpu().numpy(), want, f"K-N1s {spec} {W}x{H}")
-    # and from a 4-byte aligned pointer (4-byte loads)
+    # and from a 4-byte aligned pointer (4-byte loads) or none (funnel shifts)
     xb = torch.zeros(x.numel() + 16, dtype=torch.uint8, device="cuda")
-    xi = xb[4:4 + x.numel()]
-    xi.copy_(x.view(-1))
-    y2 = d(xi.view(n, -1))
-    torch.cuda.synchronize()
-    assert d.last_variant() == 2
-    _same(y2.cpu().numpy(), want, f"K-N1s {spec} {W}x{H} input offset 4")
+    for off in (4, 3):
+        xi = xb[off:off + x.numel()]
+        xi.copy_(x.view(-1))
+        y2 = d(xi.view(n, -1))
+        torch.cuda.synchronize()
+        assert d.last_variant() == 2
+        _same(y2.cpu().numpy(), want, f"K-N1s {spec} {W}x{H} input offset {off}")
 
 
 @pytest.mark.parametrize("W,H", [(88, 72), (104, 72), (88, 36), (136, 90)])
