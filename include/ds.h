@@ -227,14 +227,18 @@ DS_API int ds_plane_dims(const ds_handle* h, int plane, int32_t* in_w, int32_t* 
  * alignment.  K-N1s (ds_spec.cuh) has the spec compiled in -- taps, pattern,
  * paving, divisor, origin phase as constants, so zero taps, dead clamps and
  * byte shifting vanish -- and needs an H paving that is a multiple of 4,
- * taps in [-128, 127], every plane W % 16 == 0 (and W >= 64), a 16-byte
- * aligned input and 4-byte aligned output rows.  Specs with a built-in
- * instance (SPEC's downscaler, the halo reading of bench.py) use it
- * directly; any other spec is compiled at ds_create with NVRTC (about
- * 0.3 s, once per spec and process) when the runtime compiler is present
- * (environment DS_SPEC_JIT=0 turns that off; DS_GENERAL_COMPILED still
- * compiles on request).  AUTO (default) picks K-N1s whenever it can run a
- * call. */
+ * taps in [-128, 127], at most 3 planes, rows of at least 64 bytes that hold
+ * one H window, and an H origin with the same phase mod 16 on every plane
+ * once reduced to (-W/2, W/2].  Any input and output alignment: rows are
+ * read with 16-, 8- or 4-byte loads by their alignment, or as words
+ * funnel-shifted out of aligned ones.  Specs with a built-in instance
+ * (SPEC's downscaler, the halo reading of bench.py) use it directly; any
+ * other spec is compiled at ds_create with NVRTC (about 0.3 s, once per spec
+ * and process) when the runtime compiler is present (environment
+ * DS_SPEC_JIT=0 turns that off; DS_GENERAL_COMPILED still compiles on
+ * request) for the plan's row alignment only: calls from a less aligned
+ * input pointer then run the runtime-tap kernel.  AUTO (default) picks
+ * K-N1s whenever it can run a call. */
 enum { DS_GENERAL_AUTO = 0, DS_GENERAL_RUNTIME = 1, DS_GENERAL_COMPILED = 2 };
 
 /* Select the K-N1g variant.  Returns DS_OK, DS_EINVAL, or DS_EUNSUPPORTED
@@ -279,8 +283,8 @@ DS_API int ds_set_band_bytes(ds_handle* h, int64_t target_bytes);
  * reuses the previous band's intermediate rows for the Pv - Sv halo rows
  * instead of staging and H-filtering them again.  bands > 0 forces that
  * many bands per run (clamped to the plane); 0 (default) picks runs per
- * launch, split evenly within each plane, as long as the launch keeps
- * >= 16 units per CTA slot.  No effect
+ * launch, split evenly within each plane, sized for a few units per CTA
+ * slot (K-N1s: ~4).  No effect
  * without a V halo.  Output is unaffected.  Not synchronised with ds_run
  * calls in flight on other threads. */
 DS_API int ds_set_run_bands(ds_handle* h, int32_t bands);
