@@ -222,7 +222,19 @@ int configure_spec(ds_handle* h) {
 #ifndef DS_SPEC_BUDGET
 #define DS_SPEC_BUDGET (54 * 1024)
 #endif
-    const int64_t budget = DS_SPEC_BUDGET;             // two intermediate buffers; 4 CTAs per SM
+#ifndef DS_SPEC_BUDGET_NARROW
+#define DS_SPEC_BUDGET_NARROW (64 * 1024)
+#endif
+    // shared memory for the two intermediate buffers: 54 KB, or 64 KB when a
+    // plane takes several rows per warp (short rows make a band of the larger
+    // budget cheap; CIF / SD x 2000 halo: -5%; HD at 64 KB: +3%,
+    // profiles/r02/k1s_budget_ab.txt).  3 CTAs per SM fit either way.
+    bool narrow = false;
+    for (int p = 0; p < pi.n_planes; ++p) {
+        int segs, lgrpw;
+        narrow |= spec_lanes((pi.in_w[p] / sp.h.paving + 3) / 4, pi.in_h[p], &segs, &lgrpw) && lgrpw > 0;
+    }
+    const int64_t budget = narrow ? DS_SPEC_BUDGET_NARROW : DS_SPEC_BUDGET;
     int64_t mmax = 0;
     for (int p = 0; p < pi.n_planes; ++p) {
         if (!spec_plane_plan(sp, pi.in_w[p], pi.in_h[p], budget, &c.plane[p])) return DS_OK;
