@@ -178,8 +178,18 @@ bool spec_plane_plan(const ds_filter_spec& sp, int32_t W, int32_t H, int64_t bud
         const int64_t newrows = std::max<int64_t>(1, R - ovl);
         const int64_t per_pass = (int64_t)(DS_SPEC_NW / segs) * rpw;
         const double hr = (double)((newrows + per_pass - 1) / per_pass);
-        const double vr = (double)((k * nq + DS_SPEC_NW * 32 - 1) / (DS_SPEC_NW * 32));
+#if DS_SPEC_WS
+        constexpr int ntv = DS_SPEC_NWV * 32;                  // the V warps
+#else
+        constexpr int ntv = DS_SPEC_NW * 32;
+#endif
+        const double vr = (double)((k * nq + ntv - 1) / ntv);
+#if DS_SPEC_WS
+        // H and V warps overlap: the slower group sets the pace
+        const double cost = (std::max(90.0 * hr, 120.0 * vr) + 150.0) / ((double)Sv * k);
+#else
         const double cost = (90.0 * hr + 120.0 * vr + 150.0) / ((double)Sv * k);
+#endif
         if (cost < best * 0.999) {
             best = cost;
             found = true;
@@ -219,6 +229,14 @@ int configure_spec(ds_handle* h) {
         c.jit = 1;
     }
     if (!fn) return DS_OK;
+#if DS_SPEC_WS                                           // 2 CTAs per SM
+#ifndef DS_SPEC_BUDGET
+#define DS_SPEC_BUDGET (100 * 1024)
+#endif
+#ifndef DS_SPEC_BUDGET_NARROW
+#define DS_SPEC_BUDGET_NARROW (100 * 1024)
+#endif
+#endif
 #ifndef DS_SPEC_BUDGET
 #define DS_SPEC_BUDGET (54 * 1024)
 #endif
@@ -243,7 +261,7 @@ int configure_spec(ds_handle* h) {
     c.stages = 0;
     c.stage_stride = 0;
     c.mid_stride = (int32_t)round_up(mmax, 128);
-    c.threads = DS_SPEC_NW * 32;
+    c.threads = DS_SPEC_THREADS;
     c.smem = 2 * c.mid_stride;
     DeviceGuard g(h->device);
     int occ = 0;

@@ -57,8 +57,23 @@ typedef unsigned long long uintptr_t;
 #else
 #error "DS_SPEC_NW must be 4, 8 or 16"
 #endif
+#ifndef DS_SPEC_WS
+#define DS_SPEC_WS 0                  // 1: warp-specialised (DS_SPEC_NW H warps + DS_SPEC_NWV V warps, named barriers)
+#endif
+#ifndef DS_SPEC_NWV
+#define DS_SPEC_NWV 4                 // V warps of the warp-specialised kernel
+#endif
 #ifndef DS_SPEC_MINB
+#if DS_SPEC_WS
+#define DS_SPEC_MINB 2
+#else
 #define DS_SPEC_MINB 3                // CTAs per SM the register budget is sized for (4: 64 regs, constants rematerialised; measured slower)
+#endif
+#endif
+#if DS_SPEC_WS
+#define DS_SPEC_THREADS ((DS_SPEC_NW + DS_SPEC_NWV) * 32)
+#else
+#define DS_SPEC_THREADS (DS_SPEC_NW * 32)
 #endif
 #ifndef DS_SPEC_DEPTH3
 #define DS_SPEC_DEPTH3 0              // 1: three rows of H loads in flight per warp instead of two
@@ -281,6 +296,9 @@ __device__ __forceinline__ void sts128(uint32_t a, uint32_t x, uint32_t y, uint3
 __device__ __forceinline__ void sts32(uint32_t a, uint32_t v) {
     asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
+// named barriers (warp-specialised kernel): arrive does not wait
+__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void named_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 // L2 prefetch of a contiguous range (TMA engine; no shared memory, no wait)
 __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
@@ -503,8 +521,18 @@ struct VQuad {
 
 // ------------------------------------------------------------ the kernel --
 template <class HS, class VS, int PH, int AL>
-__global__ void __launch_bounds__(DS_SPEC_NW * 32, DS_SPEC_MINB) ds_spec_kernel(const __grid_constant__ SpecParams p) {
+__global__ void __launch_bounds__(DS_SPEC_THREADS, DS_SPEC_MINB) ds_spec_kernel(const __grid_constant__ SpecParams p) {
+    // NW warps run the H pass (NT threads); with DS_SPEC_WS, NWV more warps run
+    // the V pass (NTV threads) and the two groups hand the two intermediate
+    // buffers back and forth through named barriers: FULL[b] = 1 + b (H arrives,
+    // V waits), EMPTY[b] = 3 + b (V arrives, H waits), 5: the H warps alone
     constexpr int NW = DS_SPEC_NW, NT = NW * 32;
+    [[maybe_unused]] constexpr int NTALL = DS_SPEC_THREADS;
+#if DS_SPEC_WS
+    constexpr int NTV = DS_SPEC_NWV * 32;
+#else
+    constexpr int NTV = NT;
+#endif
     static_assert(HS::S % 4 == 0, "a chunk of 4 H repetitions must start on a 16-byte block");
     using HC = HChunk<HS, PH, AL>;
     extern __shared__ __align__(128) uint8_t smem[];
@@ -554,6 +582,17 @@ __global__ void __launch_bounds__(DS_SPEC_NW * 32, DS_SPEC_MINB) ds_spec_kernel(
         if (rows_ > n1) prefetch_range(pl_, (uint32_t)min(rows_ - n1, Q.H) * (uint32_t)Q.W);
     };
     if (tid == 0 && u < n_units) prefetch_band(f, local, 0);
+#if DS_SPEC_WS
+    const bool hrole = warp < NW;
+    const int vtid = tid - NT;                            // V role: 0 .. NTV - 1
+    if (!hrole) {                                         // both buffers start empty
+        named_arrive(3, NTALL);
+        named_arrive(4, NTALL);
+    }
+#else
+    constexpr bool hrole = true;
+    const int vtid = tid;
+#endif
 
     for (; u < n_units; u += gridDim.x) {
         const int pi = (p.n_planes > 2 && local >= p.pl[2].unit_start) ? 2
@@ -617,6 +656,11 @@ __global__ void __launch_bounds__(DS_SPEC_NW * 32, DS_SPEC_MINB) ds_spec_kernel(
         for (int band = b0; band < b1; ++band) {
             const uint32_t mid = mid0 + mpar * p.mid_stride;
             const int reuse = band > b0 ? p.ovl : 0;
+          if (hrole) {
+#if DS_SPEC_WS
+            named_sync(3 + mpar, NTALL);                  // V is done with this buffer (band - 2)
+            if (reuse) named_sync(5, NT);                 // every H warp is done with band - 1
+#endif
             if (tid == 0) {
                 if (band + 1 < b1) {
                     prefetch_band(f, local, band + 1 - b0);
@@ -700,7 +744,15 @@ __global__ void __launch_bounds__(DS_SPEC_NW * 32, DS_SPEC_MINB) ds_spec_kernel(
                 seek(nrow0);
                 issue(x0);
             }
+#if DS_SPEC_WS
+            named_arrive(1 + mpar, NTALL);                // intermediate complete
+          }
+          if (!hrole) {
+            named_sync(1 + mpar, NTALL);
+#else
+          }
             __syncthreads();                                               // intermediate complete
+#endif
 
             // ---- V task: intermediate -> output rows, straight to HBM
             {
@@ -738,11 +790,15 @@ __global__ void __launch_bounds__(DS_SPEC_NW * 32, DS_SPEC_MINB) ds_spec_kernel(
                     });
                 };
                 if (p.out_al4 && wm % 4 == 0) {                         // every quad a whole aligned word
-                    for (int it = tid; it < items; it += NT) vitem(it, IC<1>{});
+                    for (int it = vtid; it < items; it += NTV) vitem(it, IC<1>{});
                 } else {
-                    for (int it = tid; it < items; it += NT) vitem(it, IC<0>{});
+                    for (int it = vtid; it < items; it += NTV) vitem(it, IC<0>{});
                 }
             }
+#if DS_SPEC_WS
+            named_arrive(3 + mpar, NTALL);                // this buffer may be refilled
+          }
+#endif
             mpar ^= 1;
         }
         f = fn;
@@ -750,6 +806,12 @@ __global__ void __launch_bounds__(DS_SPEC_NW * 32, DS_SPEC_MINB) ds_spec_kernel(
         fm = fmn;
         local = ln;
     }
+#if DS_SPEC_WS
+    if (hrole) {                                          // take the V warps' last two arrivals
+        named_sync(3 + mpar, NTALL);
+        named_sync(3 + (mpar ^ 1), NTALL);
+    }
+#endif
 }
 
 }  // namespace dss

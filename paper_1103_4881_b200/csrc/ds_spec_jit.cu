@@ -161,8 +161,10 @@ SpecFn spec_jit_kernel(ds_handle* h, int phase, int align) {
         return nullptr;
     }
     char defs[256];
-    std::snprintf(defs, sizeof defs, "#define DS_SPEC_NW %d\n#define DS_SPEC_MINB %d\n#define DS_SPEC_MAXP %d\n",
-                  DS_SPEC_NW, DS_SPEC_MINB, DS_SPEC_MAXP);
+    std::snprintf(defs, sizeof defs,
+                  "#define DS_SPEC_NW %d\n#define DS_SPEC_MINB %d\n#define DS_SPEC_MAXP %d\n#define DS_SPEC_WS %d\n"
+                  "#define DS_SPEC_NWV %d\n",
+                  DS_SPEC_NW, DS_SPEC_MINB, DS_SPEC_MAXP, DS_SPEC_WS, DS_SPEC_NWV);
     std::string src = defs;
     src += kSpecSrc;
     src += "\nnamespace dss {\n";
