@@ -140,7 +140,14 @@ bool spec_jit_available() {
     return g_nvrtc.ok && g_drv.ok;
 }
 
-const char* spec_jit_log() { return g_last_log.c_str(); }
+// The last compilation's log, copied per calling thread (stable until that
+// thread calls again).
+const char* spec_jit_log() {
+    thread_local std::string copy;
+    std::lock_guard<std::mutex> lk(g_mu);
+    copy = g_last_log;
+    return copy.c_str();
+}
 
 // Compile (or fetch from the cache) K-N1s for the handle's spec, window phase
 // and row alignment on the current device.  Returns a CUfunction as SpecFn, or
