@@ -110,8 +110,8 @@ struct SpecCfg {
     bool valid = false;
     int jit = 0;                   // 0: built-in instance, 1: compiled at run time (NVRTC)
     SpecFn fn = nullptr;           // kernel entry for the plan's row alignment (runtime-API function, or a JIT CUfunction)
-    SpecFn fn_al[4] = {};          // entries by call row alignment 16 / 8 / 4 / not 4 (built-in: all up to al
-                                   // and the funnelled one; JIT: al only)
+    SpecFn fn_al[7] = {};          // entries by call row alignment 16 / 8 / 4 / not 4 / 16-byte rows 4, 8, 12
+                                   // bytes off (built-in: all that apply; JIT: the plan's alignment only)
     int al = 16;                   // row alignment of the plan (frame size, plane offsets, widths)
     SpecPlaneCfg plane[DS_MAX_PLANES];
     int32_t upf = 0, stages = 2, stage_stride = 0, mid_stride = 0;

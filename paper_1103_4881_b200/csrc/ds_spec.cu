@@ -60,7 +60,9 @@ bool spec_lanes(int nch, int H, int* segs, int* lgrpw) {
     return true;
 }
 
-int al_index(int al) { return al == 16 ? 0 : al == 8 ? 1 : al == 4 ? 2 : 3; }
+// instance slots: row alignment 16, 8, 4, unaligned (1), and 16-byte rows 4 / 8 /
+// 12 bytes past a boundary (17 / 18 / 19)
+int al_index(int al) { return al == 16 ? 0 : al == 8 ? 1 : al == 4 ? 2 : al == 1 ? 3 : al - 13; }
 
 }  // namespace
 
@@ -94,21 +96,34 @@ int spec_plan_align(const ds_plan_info& pi) {
 
 // Built-in instances: (stage types, window phase, row alignment) -> kernel.
 SpecFn spec_builtin(const ds_filter_spec& sp, int ph, int al) {
-    auto pick = [al](auto k16, auto k8, auto k4, auto k1) {
-        return al == 16 ? reinterpret_cast<SpecFn>(k16) : al == 8 ? reinterpret_cast<SpecFn>(k8)
-               : al == 4 ? reinterpret_cast<SpecFn>(k4) : reinterpret_cast<SpecFn>(k1);
+    auto pick = [al](auto k16, auto k8, auto k4, auto k1, auto k17, auto k18, auto k19) {
+        switch (al) {
+            case 16: return reinterpret_cast<SpecFn>(k16);
+            case 8: return reinterpret_cast<SpecFn>(k8);
+            case 4: return reinterpret_cast<SpecFn>(k4);
+            case 17: return reinterpret_cast<SpecFn>(k17);
+            case 18: return reinterpret_cast<SpecFn>(k18);
+            case 19: return reinterpret_cast<SpecFn>(k19);
+            default: return reinterpret_cast<SpecFn>(k1);
+        }
     };
     constexpr int kHaloPh = (dss::HaloH::O % 16 + 16) % 16, kSpecPh = (dss::SpecH::O % 16 + 16) % 16;
     if (ph == kHaloPh && stage_is<dss::HaloH>(sp.h) && stage_is<dss::HaloV>(sp.v))
         return pick(&dss::ds_spec_kernel<dss::HaloH, dss::HaloV, kHaloPh, 16>,
                     &dss::ds_spec_kernel<dss::HaloH, dss::HaloV, kHaloPh, 8>,
                     &dss::ds_spec_kernel<dss::HaloH, dss::HaloV, kHaloPh, 4>,
-                    &dss::ds_spec_kernel<dss::HaloH, dss::HaloV, kHaloPh, 1>);
+                    &dss::ds_spec_kernel<dss::HaloH, dss::HaloV, kHaloPh, 1>,
+                    &dss::ds_spec_kernel<dss::HaloH, dss::HaloV, kHaloPh, 17>,
+                    &dss::ds_spec_kernel<dss::HaloH, dss::HaloV, kHaloPh, 18>,
+                    &dss::ds_spec_kernel<dss::HaloH, dss::HaloV, kHaloPh, 19>);
     if (ph == kSpecPh && stage_is<dss::SpecH>(sp.h) && stage_is<dss::SpecV>(sp.v))
         return pick(&dss::ds_spec_kernel<dss::SpecH, dss::SpecV, kSpecPh, 16>,
                     &dss::ds_spec_kernel<dss::SpecH, dss::SpecV, kSpecPh, 8>,
                     &dss::ds_spec_kernel<dss::SpecH, dss::SpecV, kSpecPh, 4>,
-                    &dss::ds_spec_kernel<dss::SpecH, dss::SpecV, kSpecPh, 1>);
+                    &dss::ds_spec_kernel<dss::SpecH, dss::SpecV, kSpecPh, 1>,
+                    &dss::ds_spec_kernel<dss::SpecH, dss::SpecV, kSpecPh, 17>,
+                    &dss::ds_spec_kernel<dss::SpecH, dss::SpecV, kSpecPh, 18>,
+                    &dss::ds_spec_kernel<dss::SpecH, dss::SpecV, kSpecPh, 19>);
     return nullptr;
 }
 
@@ -216,6 +231,8 @@ int configure_spec(ds_handle* h) {
     // funnel-shifting one for pointers that are not 4-byte aligned
     for (int a = al; a >= 4; a /= 2) c.fn_al[al_index(a)] = spec_builtin(sp, ph, a);
     c.fn_al[al_index(1)] = spec_builtin(sp, ph, 1);
+    if (al == 16)
+        for (int a = 17; a <= 19; ++a) c.fn_al[al_index(a)] = spec_builtin(sp, ph, a);
     SpecFn fn = c.fn_al[al_index(al)];
     c.jit = 0;
     if (!fn) {
@@ -335,6 +352,12 @@ void spec_runs(const ds_handle* h, int64_t n, int32_t* L, int32_t* upf) {
 SpecFn spec_call_fn(const ds_handle* h, const uint8_t* in) {
     const SpecCfg& c = h->spec_cfg;
     if (!c.valid) return nullptr;
+    const uintptr_t m16 = reinterpret_cast<uintptr_t>(in) & 15;
+    if (c.al == 16 && m16 != 0 && (m16 & 3) == 0) {
+        // 16-byte rows from a pointer 4, 8 or 12 bytes off: the word-shift
+        // instance (16-byte block loads) when there is one
+        if (SpecFn fs = c.fn_al[al_index(16 + (int)(m16 >> 2))]) return fs;
+    }
     int a = c.al;
     while (a >= 4 && (reinterpret_cast<uintptr_t>(in) & (uintptr_t)(a - 1)) != 0) a /= 2;
     return c.fn_al[al_index(a >= 4 ? a : 1)];

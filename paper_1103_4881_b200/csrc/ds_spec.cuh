@@ -338,14 +338,18 @@ __device__ __forceinline__ void stg8(uint8_t* p, uint32_t v) {
 // + (Sh / 4) c that is PH + Sh m (PH = o mod 16, a compile-time constant of
 // the instance).  The lane loads exactly the words any live tap reads (loads
 // of up to AL bytes by word runs: AL = 16, 8 or 4 is the alignment of every
-// row start in the call; AL = 1: rows start m = 1..3 bytes past a 4-byte
-// boundary, and each window word is funnel-shifted out of the two aligned
-// words it straddles), then every output is a dp4a per aligned word with a
-// nonzero re-indexed weight word.
+// row start in the call; AL = 17, 18, 19: every row starts s = AL - 16 words
+// past a 16-byte boundary (16-byte rows, a pointer 4, 8 or 12 bytes off), so
+// the lane loads the aligned 16-byte blocks around its window and renames
+// words; AL = 1: rows start m = 1..3 bytes past a 4-byte boundary, and each
+// window word is funnel-shifted out of the two aligned words it straddles),
+// then every output is a dp4a per aligned word with a nonzero re-indexed
+// weight word.
 template <class HS, int PH, int AL = 16>
 struct HChunk {
     using I = StageInfo<HS>;
-    static_assert(AL == 16 || AL == 8 || AL == 4 || AL == 1, "row alignment 16, 8, 4, or 1 (funnelled)");
+    static_assert(AL == 16 || AL == 8 || AL == 4 || AL == 1 || (AL >= 17 && AL <= 19),
+                  "row alignment 16, 8, 4, 1 (funnelled) or 17..19 (16-byte blocks, word shift)");
     static constexpr int kLo = PH / 4;                                   // first word read
     static constexpr int kHi = (PH + 3 * HS::S + I::hi_tap()) / 4;       // last word read
     static constexpr int kWords = kHi + 1;                               // words from B's start
@@ -404,6 +408,20 @@ struct HChunk {
             sfor<0, kHi - kLo + 1>([&](auto t) {
                 x[kLo + decltype(t)::value] = __funnelshift_r(a[decltype(t)::value], a[decltype(t)::value + 1], 8 * mis);
             });
+            return;
+        }
+        if constexpr (AL > 16) {
+            // window word w is aligned word w + s of the 16-byte aligned base;
+            // every touched aligned block is loaded whole (it holds a window
+            // word, so it lies in the allocation's pages)
+            constexpr int sh = AL - 16, alo = kLo + sh, ahi = kHi + sh;
+            const uint8_t* ab = base - 4 * sh;
+            uint32_t a[4 * (ahi / 4 + 1)];
+            sfor<alo / 4, ahi / 4 + 1>([&](auto b) {
+                constexpr int w0 = 4 * decltype(b)::value;
+                ldg128(ab + 16 * decltype(b)::value, a[w0], a[w0 + 1], a[w0 + 2], a[w0 + 3]);
+            });
+            sfor<kLo, kHi + 1>([&](auto w) { x[decltype(w)::value] = a[decltype(w)::value + sh]; });
             return;
         }
         sfor<0, kBlk>([&](auto b) {
