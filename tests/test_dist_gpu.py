@@ -69,3 +69,12 @@ def test_torchrun_sharded_gather_nccl(tmp_path, mode):
         pytest.skip("needs two or more GPUs (NCCL refuses two ranks on one device)")
     ranks = min(n, 4)
     _run(tmp_path, ranks, 2 * ranks + 1, mode, "nccl")
+
+
+@pytest.mark.parametrize("mode", ["gather", "fused"])
+def test_torchrun_sharded_nccl_single_rank(tmp_path, mode):
+    """The NCCL plumbing on one GPU: a one-rank NCCL group (eager init bound
+    to the device) runs the padded dist.gather and the broadcast of rank 0's
+    CUDA IPC handle (fused mode) through NCCL itself -- the code path the
+    multi-GPU run takes, minus the peer traffic."""
+    _run(tmp_path, 1, 5, mode, "nccl")
