@@ -745,7 +745,9 @@ __global__ void __launch_bounds__(DS_SPEC_THREADS, DS_SPEC_MINB) ds_spec_kernel(
             // wrap pass: (row, wrapping chunk) items over all threads, from the last
             // warps down (they have the fewest main-loop rows)
             for (int it = NT - 1 - tid; it < rows * P.nwc; it += NT) {
-                const int i = it / P.nwc, c = P.wch[it - i * P.nwc];
+                // it / nwc for nwc <= 4 and it < 2^14: a 16-bit reciprocal
+                const int i = (int)(((uint32_t)it * (uint32_t)(P.nwc == 1 ? 65536 : P.nwc == 2 ? 32768 : P.nwc == 3 ? 21846 : 16384)) >> 16);
+                const int c = P.wch[it - i * P.nwc];
                 int r = row0 + i;
                 while (r >= P.H) r -= P.H;
                 uint32_t xw[4 * HC::kBlk], o[HS::Q];
