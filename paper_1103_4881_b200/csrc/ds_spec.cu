@@ -298,7 +298,11 @@ int configure_spec(ds_handle* h) {
             return DS_OK;
         }
     }
-    c.grid_per_sm = std::min(occ, 4);
+    // CTAs per SM: up to 4 when a plane takes several rows per warp, else 3 --
+    // wide rows make large bands, and a fourth CTA's prefetched band costs the
+    // others theirs in L2 (HD halo: 0.239 ms at 4 CTAs, 0.213 at 3, with the
+    // same 64-register build; QCIF / CIF x 2000: 4-7% faster at 4)
+    c.grid_per_sm = std::min(occ, narrow ? 4 : 3);
     c.fn = fn;
     c.valid = true;
     h->spec_cfg = c;

@@ -593,7 +593,7 @@ __global__ void __launch_bounds__(DS_SPEC_THREADS, DS_SPEC_MINB) ds_spec_kernel(
         if (bnd >= Q.nb) return;
         const int reuse_ = band_rel > 0 ? p.ovl : 0;
         const int rows_ = VS::S * (Q.k - 1) + VS::P - reuse_;
-        int r0 = (int)(((int64_t)Q.ov + (int64_t)VS::S * Q.k * bnd + reuse_) % Q.H);
+        int r0 = (int)((uint32_t)(Q.ov + VS::S * Q.k * bnd + reuse_) % (uint32_t)Q.H);   // < 2^31
         const uint8_t* pl_ = p.in + f_ * p.in_frame + Q.in_off;
         const int n1 = min(rows_, Q.H - r0);
         prefetch_range(pl_ + (int64_t)r0 * Q.W, (uint32_t)n1 * (uint32_t)Q.W);
